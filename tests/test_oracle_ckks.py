@@ -1,0 +1,154 @@
+"""Pins for the O-RNS CKKS layer: encode/encrypt round trips,
+the automorphism slot-rotation invariant, homomorphic add/mult/rotate against
+plain slot-wise arithmetic, the chained-squaring error bound of P:1049-1055,
+and the exact scalar-constant encoding."""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import ckks as orc
+from synth.params import toy
+
+
+@pytest.fixture(scope="module")
+def P():
+    return toy(log_n=10, n_q=6, scale_bits=40, n_p=2, alpha=2)
+
+
+@pytest.fixture(scope="module")
+def keys(P):
+    return orc.keygen(P, seed=123, rotations=[1, 2, 3, 5, -1, 64])
+
+
+def test_embedding_roundtrip(P):
+    rng = np.random.default_rng(0)
+    v = rng.uniform(-1, 1, P.n // 2)
+    m = orc.embed_inverse(v, P.n)
+    assert np.max(np.abs(orc.embed(m, P.n).real - v)) < 1e-12
+    assert np.max(np.abs(orc.embed(m, P.n).imag)) < 1e-12
+
+
+def test_embedding_is_evaluation_at_roots():
+    # z_j = m(zeta^(5^j mod 2N)) written out directly at N=16
+    n = 16
+    rng = np.random.default_rng(1)
+    m = rng.normal(size=n)
+    z = orc.embed(m, n)
+    for j in range(n // 2):
+        root = np.exp(1j * np.pi * pow(5, j, 2 * n) / n)
+        assert abs(np.polyval(m[::-1], root) - z[j]) < 1e-9
+
+
+@pytest.mark.parametrize("k", [1, 3, -2, 5])
+def test_automorphism_rotates_slots(k):
+    # decode(sigma_{5^k}(encode(v))) = roll(v, -k)
+    n = 32
+    rng = np.random.default_rng(k + 10)
+    v = rng.uniform(-1, 1, n // 2)
+    m = np.rint(orc.embed_inverse(v, n) * 2 ** 30).astype(np.int64)
+    g = pow(5, k % (n // 2), 2 * n)
+    out = np.zeros(n)
+    for i, x in enumerate(m):
+        j = i * g % (2 * n)
+        if j < n:
+            out[j] += x
+        else:
+            out[j - n] -= x
+    z = orc.embed(out / 2 ** 30, n).real
+    assert np.max(np.abs(z - np.roll(v, -k))) < 1e-6
+
+
+def test_encrypt_decrypt_roundtrip(P, keys):
+    rng = np.random.default_rng(2)
+    v = rng.uniform(-1, 1, 128)
+    ct = orc.encrypt_vector(P, keys, v, P.L, seed=5, index=0)
+    out = orc.decrypt_vector(P, keys, ct)
+    assert np.max(np.abs(out - v)) < 2 ** -20
+
+
+def test_hadd_hmult_rotate(P, keys):
+    rng = np.random.default_rng(3)
+    n = 128
+    a, b = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    ca = orc.encrypt_vector(P, keys, a, P.L, seed=6, index=0)
+    cb = orc.encrypt_vector(P, keys, b, P.L, seed=6, index=1)
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    s = orc.decrypt_vector(P, keys, ev.add(ca, cb))
+    assert np.max(np.abs(s - (a + b))) < 2 ** -20
+    m = ev.mul_rescale(ca, cb)
+    assert m.level == P.L - 1
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, m) - a * b)) < 2 ** -18
+    for k in (1, 3, -1, 64):
+        r = ev.rotate(ca, k)
+        assert np.max(np.abs(orc.decrypt_vector(P, keys, r) - np.roll(a, -k))) < 2 ** -20
+    # Rot(Enc([0,1,2,...]),1) -> [1,2,...,0]
+    ramp = np.arange(n) / n
+    cr = orc.encrypt_vector(P, keys, ramp, P.L, seed=6, index=2)
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, ev.rotate(cr, 1)) - np.roll(ramp, -1))) < 2 ** -20
+
+
+def test_plain_mult_and_scalar(P, keys):
+    rng = np.random.default_rng(4)
+    n = 128
+    a, w = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    ca = orc.encrypt_vector(P, keys, a, P.L, seed=7, index=0)
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    ql = P.q[P.L]
+    pt = orc.encode(P, w, ql, P.L)
+    r = ev.rescale(ev.pmult(ca, pt, ql))
+    assert r.scale == ca.scale  # PMult at Delta_pt = q_l preserves scale exactly (c-6)
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, r) - a * w)) < 2 ** -20
+    r2 = ev.rescale(ev.pmult_scalar(ca, -1.0 / 3.0))
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, r2) + a / 3)) < 2 ** -20
+
+
+def test_chained_squarings_error(keys):
+    # cumulative rescale error ~ L * 2^-Delta; S:139 -- 11 squarings of Enc(0.9)
+    # hybrid KS needs P >= the largest digit product: alpha=2 digits (<= 100 bits) vs P ~ 2^120
+    P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
+    k = orc.keygen(P, seed=77)
+    ev = orc.Evaluator(P, k.rlk)
+    x = np.linspace(0.9999, 0.99995, 16)  # x^(2^11) stays O(1)
+    ct = orc.encrypt_vector(P, k, x, P.L, seed=8, index=0)
+    want = x.copy()
+    for _ in range(11):
+        ct = ev.square_rescale(ct)
+        want = want * want
+    assert ct.level == 0
+    got = orc.decrypt_vector(P, k, ct)
+    # relative error bounded by 2^11 amplification of the fresh error (~2^-30)
+    assert np.max(np.abs(got - want) / np.abs(want)) < 1e-4
+    with pytest.raises(orc.DepthError):
+        ev.rescale(ev.relin(ev.tensor(ct, ct)))
+
+
+@pytest.mark.parametrize("c", [0.5, -0.5, 1 / 3, -1 / 3, 2.5e-7, 0.1, -0.75, 1.0])
+def test_scalar_encoding_exact(c):
+    q = (1 << 60) - 93  # any 60-bit odd modulus
+    v = orc.encode_scalar(c, q)
+    exact = Fraction(c) * q
+    assert abs(Fraction(v) - exact) <= Fraction(1, 2)
+    if abs(Fraction(v) - exact) == Fraction(1, 2):
+        assert abs(v) > abs(exact)  # ties away from zero
+
+
+def test_missing_key_and_scale_errors(P, keys):
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    ct = orc.encrypt_vector(P, keys, np.zeros(8), P.L, seed=1, index=0)
+    with pytest.raises(KeyError):
+        ev.rotate(ct, 7)
+    ct2 = orc.Ct([c.copy() for c in ct.c], ct.level, ct.scale * 2, ct.n_slots)
+    with pytest.raises(orc.ScaleError):
+        ev.add(ct, ct2)
+
+
+def test_evk_sizes_match_paper():
+    # vital relin key 22.5 MiB = dnum 3 x 2 x (11 Q + 4 P) limbs x 2^15 x 8 B
+    from synth.params import make_params
+    P = make_params(15, 11, 40, 4, 4, name="vital-paper")
+    assert P.dnum() == 3
+    size = P.dnum() * 2 * (len(P.q) + len(P.p)) * P.n * 8
+    assert size / 2 ** 20 == pytest.approx(22.5)
+    # ciphertext 5.5 MiB = 2 x 11 limbs x 2^15 x 8 B
+    assert 2 * len(P.q) * P.n * 8 / 2 ** 20 == pytest.approx(5.5)
