@@ -1,0 +1,447 @@
+"""The mmFHE kernel circuits over the O-RNS evaluator -- TEST INFRASTRUCTURE ONLY.
+
+Each function follows the paper's kernel in the paper's order and notation,
+with the canonical circuit pinned in SURVEY §8(c)-7 (relinearisation
+placement, rescale placement, BSGS split, overflow folds).  The CUDA library
+implements the same logical op sequence independently (csrc/chains.cpp);
+``op trace`` equality plus bit-exact residues is the parity gate.
+
+Kernels:
+  K1 Energy Integration              Eq. energy
+  K2 Soft Power Attention            Eqs. soft_power_weight/soft_argmax_stats P:777-788
+  K2b Doppler soft power             Eq. gesture_soft_power
+  K3 Block-diagonal DFT, BSGS        Eqs. dft_kernel/dft_re P:797-815, BSGS P:164-176
+  K4 Soft I/Q                        Eqs. phase_mask/phase_iq P:821-829
+  K5 FIR (Toeplitz)                  Eq. fir_iq
+  K6 Notch mask                      Eq. notch_mask
+  K7 Taylor differential phase       Eq. taylor_arctan
+  FC square-activation MLP           Eq. mlp_forward
+Pipelines: vital signs P:901-902, dynamic classification P:904-907,
+Table tab:depth P:914-949.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from oracle import ckks as orc
+from oracle import dsp
+
+
+@dataclass
+class ChainCfg:
+    R: int = 64
+    D: int = 32
+    A: int = 4
+    F: int = 32
+    gamma: int = 2              # K2 sharpening exponent (power of two)
+    p_phi: int = 2              # K4 mask exponent (reading #1)
+    taylor_order: int = 1       # K7: 1 (evaluated variant) or 3
+    n_slots: int = 0            # packing period n
+    bsgs_baby: int = 0          # K3 baby steps b; 0 -> ceil(sqrt(2D-1))
+    fc_dims: tuple = (4096, 64, 32, 8)
+    notch_width: int = 1
+    fs: float = 20.0
+    bands: tuple = ((0.1, 0.6), (0.8, 2.5))   # RR, HR
+
+
+def rot(v: np.ndarray, k: int) -> np.ndarray:
+    """Rot(v, k)[j] = v[(j + k) mod n] (left rotation)."""
+    return np.roll(v, -k)
+
+
+def ceil_sqrt(x: int) -> int:
+    return int(math.ceil(math.sqrt(x)))
+
+
+class PlainBook:
+    """Public plaintext operands encoded by the oracle at the level
+    they are used, Delta_pt = q_level unless a scale is given.  Parity mode
+    imports exactly these residues into the GPU context by (name, level)."""
+
+    def __init__(self, P):
+        self.P = P
+        self.entries: dict = {}
+
+    def vec(self, name: str, values: np.ndarray, level: int, scale: float | None = None):
+        key = (name, level)
+        if key not in self.entries:
+            sc = float(self.P.q[level]) if scale is None else float(scale)
+            self.entries[key] = (orc.encode(self.P, values, sc, level), sc, np.asarray(values))
+        res, sc, _ = self.entries[key]
+        return res, sc
+
+
+# ------------------------------------------------------------------ evaluator ext
+
+class CircuitEvaluator(orc.Evaluator):
+    """Logical ops used by the circuits, each recorded once in the trace."""
+
+    def tensor_sum(self, pairs) -> orc.Ct:
+        """sum_i tensor(a_i, b_i) -- the lazy-relinearisation input (c-6)."""
+        a0 = pairs[0][0]
+        self._rec("tensor_sum", a0.level, str(len(pairs)))
+        qs = self.qs(a0.level)
+        acc = None
+        for a, b in pairs:
+            if a.level != b.level or a.level != a0.level:
+                raise ValueError("level mismatch")
+            d0 = orc.poly_mul(qs, a.c[0], b.c[0])
+            d1 = orc.poly_add(qs, orc.poly_mul(qs, a.c[0], b.c[1]), orc.poly_mul(qs, a.c[1], b.c[0]))
+            d2 = orc.poly_mul(qs, a.c[1], b.c[1])
+            t = [d0, d1, d2]
+            acc = t if acc is None else [orc.poly_add(qs, x, y) for x, y in zip(acc, t)]
+        sc = pairs[0][0].scale * pairs[0][1].scale
+        for a, b in pairs:
+            if a.scale * b.scale != sc:
+                raise orc.ScaleError("tensor_sum scale mismatch")
+        return orc.Ct(acc, a0.level, sc, a0.n_slots)
+
+    def pmult_sum(self, terms) -> orc.Ct:
+        """sum_i pt_i (.) ct_i, all at one level and equal products of scales."""
+        ct0 = terms[0][1]
+        self._rec("pmult_sum", ct0.level, str(len(terms)))
+        qs = self.qs(ct0.level)
+        acc = None
+        sc = None
+        for (pt, pts), ct in terms:
+            if ct.level != ct0.level:
+                raise ValueError("level mismatch")
+            t = [orc.poly_mul(qs, x, pt[: ct.level + 1]) for x in ct.c]
+            acc = t if acc is None else [orc.poly_add(qs, x, y) for x, y in zip(acc, t)]
+            s = ct.scale * pts
+            if sc is None:
+                sc = s
+            elif s != sc:
+                raise orc.ScaleError("pmult_sum scale mismatch")
+        return orc.Ct(acc, ct0.level, sc, ct0.n_slots)
+
+    def lincomb_scalar(self, cts, coefs) -> orc.Ct:
+        """sum_k round-half-away(c_k q_l) ct_k (exact scalar encoding, c-5)."""
+        ct0 = cts[0]
+        self._rec("lincomb", ct0.level, str(len(cts)))
+        qs = self.qs(ct0.level)
+        ql = self.P.q[ct0.level]
+        acc = None
+        for ct, c in zip(cts, coefs):
+            if ct.level != ct0.level or ct.scale != ct0.scale:
+                raise orc.ScaleError("lincomb operands must share level and scale")
+            v = orc.encode_scalar(float(c), ql)
+            res = np.array([v % q for q in qs], dtype=np.uint64)
+            t = [orc.poly_scalar(qs, x, res) for x in ct.c]
+            acc = t if acc is None else [orc.poly_add(qs, x, y) for x, y in zip(acc, t)]
+        return orc.Ct(acc, ct0.level, ct0.scale * ql, ct0.n_slots)
+
+    def add_plain(self, ct: orc.Ct, pt) -> orc.Ct:
+        res, sc = pt
+        if sc != ct.scale:
+            raise orc.ScaleError("add_plain scale mismatch")
+        self._rec("add_plain", ct.level)
+        qs = self.qs(ct.level)
+        return orc.Ct([orc.poly_add(qs, ct.c[0], res[: ct.level + 1]), ct.c[1]], ct.level, ct.scale, ct.n_slots)
+
+    def pmult_rescale(self, ct, pt) -> orc.Ct:
+        return self.rescale(self.pmult_sum([(pt, ct)]))
+
+    def relin_rescale(self, ct) -> orc.Ct:
+        return self.rescale(self.relin(ct))
+
+
+# ------------------------------------------------------------------ K1 / K2
+
+def k1_energy(ev: CircuitEvaluator, re_list, im_list) -> orc.Ct:
+    """K1: E = rescale(relin(sum_t tensor(re_t,re_t) + tensor(im_t,im_t)))."""
+    pairs = []
+    for re, im in zip(re_list, im_list):
+        pairs += [(re, re), (im, im)]
+    return ev.relin_rescale(ev.tensor_sum(pairs))
+
+
+def k2_soft_attention(ev: CircuitEvaluator, book: PlainBook, E: orc.Ct, cfg: ChainCfg):
+    """K2a: w = E^gamma by log2(gamma) squarings; N = rotsum_R(w (.) ramp'),
+    D = rotsum_R(w (.) one'), ramp'_r = r/(F^2 R), one'_r = 1/(F^2 R)."""
+    w = E
+    for _ in range(int(math.log2(cfg.gamma))):
+        w = ev.relin_rescale(ev.tensor_sum([(w, w)]))
+    n = E.n_slots
+    R, F = cfg.R, cfg.F
+    ramp = np.zeros(n)
+    one = np.zeros(n)
+    ramp[:R] = np.arange(R) / (F * F * R)
+    one[:R] = 1.0 / (F * F * R)
+    Nn = ev.pmult_rescale(w, book.vec("k2.ramp", ramp, w.level))
+    Dd = ev.pmult_rescale(w, book.vec("k2.one", one, w.level))
+    return ev.rotsum(Nn, R, 1), ev.rotsum(Dd, R, 1)
+
+
+def vitals_v1(ev, book, re_list, im_list, cfg):
+    """Chain V1 = K1 -> K2; the client decrypts N and D, r_hat = N/D."""
+    return k2_soft_attention(ev, book, k1_energy(ev, re_list, im_list), cfg)
+
+
+# ------------------------------------------------------------------ K3 (BSGS)
+
+def block_diag_diagonal(M: np.ndarray, n: int, o: int) -> np.ndarray:
+    """diag_o of I_{n/D} (x) M: diag_o[j] = Mt[j, (j+o) mod n] (Halevi-Shoup)."""
+    D = M.shape[0]
+    out = np.zeros(n, dtype=M.dtype)
+    for j in range(n):
+        c = (j + o) % n
+        if j // D == c // D:
+            out[j] = M[j % D, c % D]
+    return out
+
+
+def k3_schedule(cfg: ChainCfg):
+    """BSGS split over the offsets o in [-(D-1), D-1]: o = o_min + g'b + s."""
+    D = cfg.D
+    d = 2 * D - 1
+    b = cfg.bsgs_baby or ceil_sqrt(d)
+    g = -(-d // b)
+    o_min = -(D - 1)
+    giants = []
+    for gp in range(g):
+        G = o_min + gp * b
+        babies = [s for s in range(b) if G + s <= D - 1]
+        giants.append((gp, G, babies))
+    return b, giants
+
+
+def k3_doppler_dft(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg: ChainCfg):
+    """K3 (Eqs. dft_re/dft_im P:805-815): d_re = C~ v_re - S~ v_im, d_im = S~ v_re + C~ v_im
+    via BSGS with pre-rotated diagonals; one rescale after the giant sum (c-6)."""
+    n = v_re.n_slots
+    lvl = v_re.level
+    W = dsp.dft_matrix(cfg.D)
+    C, S = W.real, W.imag
+    b, giants = k3_schedule(cfg)
+    xr = [v_re] + [ev.rotate(v_re, s) for s in range(1, b)]
+    xi = [v_im] + [ev.rotate(v_im, s) for s in range(1, b)]
+    out_re = out_im = None
+    for gp, G, babies in giants:
+        t_re, t_im = [], []
+        for s in babies:
+            o = G + s
+            dc = rot(block_diag_diagonal(C, n, o), -G)
+            ds = rot(block_diag_diagonal(S, n, o), -G)
+            pc = book.vec(f"k3.c.{gp}.{s}", dc, lvl)
+            ps = book.vec(f"k3.s.{gp}.{s}", ds, lvl)
+            pns = book.vec(f"k3.ns.{gp}.{s}", -ds, lvl)
+            t_re += [(pc, xr[s]), (pns, xi[s])]
+            t_im += [(ps, xr[s]), (pc, xi[s])]
+        ir = ev.rotate(ev.pmult_sum(t_re), G)
+        ii = ev.rotate(ev.pmult_sum(t_im), G)
+        out_re = ir if out_re is None else ev.add(out_re, ir)
+        out_im = ii if out_im is None else ev.add(out_im, ii)
+    return ev.rescale(out_re), ev.rescale(out_im)
+
+
+# ------------------------------------------------------------------ gesture frame
+
+def k1_power(ev, d_re, d_im):
+    """K1 on the K3 output: P = rescale(relin(tensor(d_re,d_re) + tensor(d_im,d_im)))."""
+    return ev.relin_rescale(ev.tensor_sum([(d_re, d_re), (d_im, d_im)]))
+
+
+def k6_notch(ev, book, P_ct, cfg):
+    """K6: P (.) m~ with m~[d] = m[d]/s, s = R A (sum w)^2 (P:887 fold)."""
+    n = P_ct.n_slots
+    s = dsp.spectral_scale(cfg.R, cfg.A, cfg.D)
+    mask = np.tile(dsp.notch_mask(cfg.D, cfg.notch_width) / s, n // cfg.D)
+    return ev.pmult_rescale(P_ct, book.vec("k6.mask", mask, P_ct.level))
+
+
+def k2_doppler_soft_power(ev, Pm, cfg):
+    """K2b (Eq. gesture_soft_power): S = rotsum over the n/D blocks
+    (stride D; every block then holds sum_{a,r}, reading #8); S^gamma by squarings;
+    f = Pm (.) S^gamma (P:906 'feature weighting')."""
+    S = ev.rotsum(Pm, Pm.n_slots // cfg.D, cfg.D)
+    for _ in range(int(math.log2(cfg.gamma))):
+        S = ev.relin_rescale(ev.tensor_sum([(S, S)]))
+    return ev.relin_rescale(ev.tensor_sum([(ev.drop_to(Pm, S.level), S)]))
+
+
+def gesture_frame(ev, book, v_re, v_im, cfg):
+    """Per frame: K3 -> K1 -> K6 -> K2b -> weighting."""
+    d_re, d_im = k3_doppler_dft(ev, book, v_re, v_im, cfg)
+    P_ct = k1_power(ev, d_re, d_im)
+    Pm = k6_notch(ev, book, P_ct, cfg)
+    return k2_doppler_soft_power(ev, Pm, cfg)
+
+
+def frame_accumulate(ev, feats):
+    """FA: homomorphic sum over frames (depth 0)."""
+    acc = feats[0]
+    for f in feats[1:]:
+        acc = ev.add(acc, f)
+    return acc
+
+
+# ------------------------------------------------------------------ FC
+
+def fc_diagonal(W: np.ndarray, n_in: int, i: int) -> np.ndarray:
+    """Hybrid diagonal: diag_i[j] = W[j mod h, (j+i) mod n_in], j < n_in."""
+    h = W.shape[0]
+    j = np.arange(n_in)
+    return W[j % h, (j + i) % n_in]
+
+
+def fc_schedule(h: int):
+    b = ceil_sqrt(h)
+    g = -(-h // b)
+    return b, [(gp, gp * b, [s for s in range(b) if gp * b + s < h]) for gp in range(g)]
+
+
+def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int, square: bool):
+    """One layer of Eq. mlp_forward: z = sum_i diag_i (.) Rot(x, i) by BSGS,
+    y = rotsum_{n_in/h}(z, stride h) (h-periodic W x), + b, then (.)^2 unless last."""
+    h = W.shape[0]
+    lvl = x.level
+    b, giants = fc_schedule(h)
+    babies = [x] + [ev.rotate(x, s) for s in range(1, min(b, h))]
+    acc = None
+    for gp, G, ss in giants:
+        terms = []
+        for s in ss:
+            dg = rot(fc_diagonal(W, n_in, G + s), -G)
+            terms.append((book.vec(f"fc{layer}.d.{gp}.{s}", dg, lvl), babies[s]))
+        inner = ev.pmult_sum(terms)
+        if G:
+            inner = ev.rotate(inner, G)
+        acc = inner if acc is None else ev.add(acc, inner)
+    z = ev.rescale(acc)
+    y = ev.rotsum(z, n_in // h, h)
+    y = ev.add_plain(y, book.vec(f"fc{layer}.bias", np.asarray(bias, dtype=np.float64), y.level, scale=y.scale))
+    if square:
+        y = ev.relin_rescale(ev.tensor_sum([(y, y)]))
+    return y
+
+
+def pad_fc(Ws, bs, dims):
+    """Pad the last layer's rows to dims[-1] (5 logits -> 8)."""
+    Ws = [np.asarray(W, dtype=np.float64) for W in Ws]
+    bs = [np.asarray(b, dtype=np.float64) for b in bs]
+    h = dims[-1]
+    if Ws[-1].shape[0] < h:
+        pad = h - Ws[-1].shape[0]
+        Ws[-1] = np.vstack([Ws[-1], np.zeros((pad, Ws[-1].shape[1]))])
+        bs[-1] = np.concatenate([bs[-1], np.zeros(pad)])
+    return Ws, bs
+
+
+def gesture_fc(ev, book, feat, Ws, bs, cfg):
+    """FC1 -> x^2 -> FC2 -> x^2 -> FC3."""
+    dims = cfg.fc_dims
+    Ws, bs = pad_fc(Ws, bs, dims)
+    x = feat
+    for layer in range(len(Ws)):
+        x = fc_layer(ev, book, x, Ws[layer], bs[layer], dims[layer], layer + 1, layer < len(Ws) - 1)
+    return x
+
+
+# ------------------------------------------------------------------ vital V2
+
+def k4_soft_iq(ev, re, im, cfg):
+    """K4, P_phi = 2^k: p = |z|^2, m = p^P_phi, i = m re, q = m im,
+    I = rotsum_R(i), Q = rotsum_R(q) (slot 0 valid)."""
+    p = ev.relin_rescale(ev.tensor_sum([(re, re), (im, im)]))
+    m = p
+    for _ in range(int(math.log2(cfg.p_phi))):
+        m = ev.relin_rescale(ev.tensor_sum([(m, m)]))
+    i = ev.relin_rescale(ev.tensor_sum([(m, ev.drop_to(re, m.level))]))
+    q = ev.relin_rescale(ev.tensor_sum([(m, ev.drop_to(im, m.level))]))
+    return ev.rotsum(i, cfg.R, 1), ev.rotsum(q, cfg.R, 1)
+
+
+def k5_fir(ev, xs, taps):
+    """K5: x_f[t] = rescale(sum_{k <= t} h[k] x[t-k]) (causal Toeplitz)."""
+    out = []
+    for t in range(len(xs)):
+        ks = [k for k in range(len(taps)) if t - k >= 0]
+        out.append(ev.rescale(ev.lincomb_scalar([xs[t - k] for k in ks], [taps[k] for k in ks])))
+    return out
+
+
+def k7_taylor_phase(ev, If, Qf, order):
+    """K7: y[t] = Q_f[t] I_f[t-1] - I_f[t] Q_f[t-1]; first order y,
+    third order y x^2 - y^3/3 (literal polynomial, reading #2); t = 1..F-1."""
+    out = []
+    for t in range(1, len(If)):
+        ty = ev.tensor_sum([(Qf[t], If[t - 1])])
+        ty2 = ev.tensor_sum([(If[t], Qf[t - 1])])
+        y = ev.relin_rescale(ev.sub(ty, ty2))
+        if order == 1:
+            out.append(y)
+            continue
+        x = ev.relin_rescale(ev.tensor_sum([(If[t], If[t - 1]), (Qf[t], Qf[t - 1])]))
+        x2 = ev.relin_rescale(ev.tensor_sum([(x, x)]))
+        y2 = ev.relin_rescale(ev.tensor_sum([(y, y)]))
+        yt = ev.rescale(ev.lincomb_scalar([y], [-1.0 / 3.0]))
+        yx2 = ev.relin_rescale(ev.tensor_sum([(ev.drop_to(y, x2.level), x2)]))
+        y3 = ev.relin_rescale(ev.tensor_sum([(y2, yt)]))
+        out.append(ev.add(yx2, y3))
+    return out
+
+
+def vp_band_power(ev, ys, bins):
+    """VP+ (P:279-288): X[k] = sum_t c_{k,t} y[t] (+ j s_{k,t}), P_k = |X[k]|^2."""
+    Fp = len(ys)
+    out = []
+    for k in bins:
+        c, s = dsp.narrowband_dft_coefs(Fp, int(k))
+        xr = ev.rescale(ev.lincomb_scalar(ys, c))
+        xi = ev.rescale(ev.lincomb_scalar(ys, s))
+        out.append(ev.relin_rescale(ev.tensor_sum([(xr, xr), (xi, xi)])))
+    return out
+
+
+def vitals_v2(ev, re_list, im_list, taps_by_band, cfg):
+    """Chain V2: K4 -> K5 -> K7 -> narrowband DFT -> |X|^2 per band;
+    returns {band index: [P_k ciphertexts]} (sharpen/average on the client, reading #4)."""
+    IQ = [k4_soft_iq(ev, re, im, cfg) for re, im in zip(re_list, im_list)]
+    I = [a for a, _ in IQ]
+    Q = [b for _, b in IQ]
+    out = {}
+    for bi, taps in enumerate(taps_by_band):
+        If = k5_fir(ev, I, taps)
+        Qf = k5_fir(ev, Q, taps)
+        ys = k7_taylor_phase(ev, If, Qf, cfg.taylor_order)
+        bins = dsp.band_bins(len(ys), cfg.fs, cfg.bands[bi])
+        out[bi] = vp_band_power(ev, ys, bins)
+    return out
+
+
+# ------------------------------------------------------------------ key sets
+
+def rotsum_steps(count: int, stride: int):
+    out, s, c = [], stride, 1
+    while c < count:
+        out.append(s)
+        s *= 2
+        c *= 2
+    return out
+
+
+def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
+    """Rotation amounts (normalised to [0, N/2)) a chain needs."""
+    half = n_ring // 2
+    ks = set()
+    if chain in ("k2_soft_attention", "vitals_v1", "k4_soft_iq", "vitals_v2"):
+        ks |= set(rotsum_steps(cfg.R, 1))
+    if chain in ("k3_doppler_dft", "gesture_frame", "gesture"):
+        b, giants = k3_schedule(cfg)
+        ks |= set(range(1, b))
+        ks |= {G for _, G, _ in giants if G != 0}
+    if chain in ("k2_doppler_soft_power", "gesture_frame", "gesture"):
+        ks |= set(rotsum_steps(cfg.n_slots // cfg.D, cfg.D))
+    if chain in ("gesture_fc", "gesture"):
+        dims = cfg.fc_dims
+        for layer in range(len(dims) - 1):
+            h = dims[layer + 1]
+            b, giants = fc_schedule(h)
+            ks |= set(range(1, min(b, h)))
+            ks |= {G for _, G, _ in giants if G != 0}
+            ks |= set(rotsum_steps(dims[layer] // h, h))
+    return sorted({k % half for k in ks} - {0})

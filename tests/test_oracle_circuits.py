@@ -1,0 +1,226 @@
+"""Pins for the oracle's kernel circuits.
+
+* schedule checks on plaintext slot vectors (BSGS K3, hybrid-diagonal FC):
+  written with numpy rolls, compared with the plain matrix products;
+* the DFT matrix of Eq. dft_kernel against numpy's fftshift(fft(w x));
+* encrypted chains (O-RNS) decrypted and compared with O-DSP closed forms at
+  the north-star gate: normwise 1e-3 relative;
+* data obliviousness (Theorem P:999-1006): identical op traces on different
+  inputs.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import ckks as orc
+from oracle import circuits as cc
+from oracle import dsp
+from synth import radar
+from synth.params import toy
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rel_err(got, want):
+    return float(np.max(np.abs(np.asarray(got) - np.asarray(want))) / max(np.max(np.abs(want)), 1e-300))
+
+
+def test_dft_matrix_is_shifted_windowed_fft():
+    D = 32
+    rng = np.random.default_rng(0)
+    x = rng.normal(size=D) + 1j * rng.normal(size=D)
+    W = dsp.dft_matrix(D)
+    want = np.fft.fftshift(np.fft.fft(np.hanning(D) * x))
+    assert np.allclose(W @ x, want, atol=1e-12)
+
+
+@pytest.mark.parametrize("D,b", [(8, 0), (32, 0), (32, 4), (16, 5)])
+def test_k3_bsgs_schedule_on_plain_slots(D, b):
+    """The BSGS schedule (pre-rotated diagonals, babies, giants) reproduces the
+    block-diagonal matvec exactly on plaintext slot vectors."""
+    n = 4 * D
+    cfg = cc.ChainCfg(D=D, bsgs_baby=b)
+    rng = np.random.default_rng(D + b)
+    M = rng.normal(size=(D, D))
+    x = rng.normal(size=n)
+    bb, giants = cc.k3_schedule(cfg)
+    babies = [cc.rot(x, s) for s in range(bb)]
+    y = np.zeros(n)
+    n_rot = bb - 1
+    for gp, G, ss in giants:
+        inner = sum(cc.rot(cc.block_diag_diagonal(M, n, G + s), -G) * babies[s] for s in ss)
+        y += cc.rot(inner, G)
+        n_rot += G != 0
+    want = (np.kron(np.eye(n // D), M) @ x)
+    assert np.allclose(y, want)
+    # 2D-1 nonzero diagonals; ~2 sqrt(d) rotations per input
+    assert sum(len(ss) for _, _, ss in giants) == 2 * D - 1
+    if D == 32 and b == 0:
+        assert n_rot == 15  # 7 baby + 8 giant; x2 inputs -> 30 HRots per frame
+
+
+@pytest.mark.parametrize("h,n_in", [(8, 64), (16, 64), (5, 40)])
+def test_fc_hybrid_diagonal_on_plain_slots(h, n_in):
+    rng = np.random.default_rng(h)
+    W = rng.normal(size=(h, n_in))
+    x = rng.normal(size=n_in)
+    b, giants = cc.fc_schedule(h)
+    babies = [cc.rot(x, s) for s in range(b)]
+    z = np.zeros(n_in)
+    for gp, G, ss in giants:
+        z += cc.rot(sum(cc.rot(cc.fc_diagonal(W, n_in, G + s), -G) * babies[s] for s in ss), G)
+    if n_in % h == 0:
+        y = sum(cc.rot(z, c * h) for c in range(n_in // h))
+        assert np.allclose(y[:h], W @ x)
+        assert np.allclose(y, np.tile(W @ x, n_in // h))
+
+
+def test_golden_spec_worked_values():
+    with open(os.path.join(GOLDEN, "spec_worked_values.json")) as f:
+        g = json.load(f)
+    k1 = g["k1_energy_single"]
+    assert dsp.energy(np.array([[complex(*k1["z"])]]))[0] == k1["E"]
+    k6 = g["k6_notch_D32"]
+    m = dsp.notch_mask(32)
+    assert [int(i) for i in np.nonzero(m == 0)[0]] == k6["zeroed"]
+    assert np.array_equal(m * m, m)  # idempotent
+    k2 = g["k2_gamma_powers"]
+    E = np.array(k2["E"], dtype=float)
+    assert list(E ** k2["gamma"]) == k2["w"]
+    pk = g["packing"]
+    assert pk["A"] * pk["R"] * pk["D"] == pk["active"]
+    rec = g["recover"]
+    assert rec["N"] / rec["D"] == rec["r_hat"]
+
+
+# ------------------------------------------------------------------ encrypted chains
+
+@pytest.fixture(scope="module")
+def Pg():
+    # 12 Q limbs (depth 11, Table tab:depth) at N=2^10; alpha=2 so P covers each digit
+    return toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
+
+
+def _enc(P, keys, v, level, idx, seed=31):
+    return orc.encrypt_vector(P, keys, v, level, seed=seed, index=idx)
+
+
+def test_k1_k2_vital_v1(Pg):
+    P = Pg
+    cfg = cc.ChainCfg(R=16, F=6, gamma=2, n_slots=P.n // 2)
+    z, truth = radar.vital_scene(cfg.R, cfg.F, 20.0, seed=1001)
+    zt = radar.preprocess_vital(z)
+    keys = orc.keygen(P, seed=2001, rotations=cc.required_rotations("vitals_v1", cfg, P.n))
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    lvl = 3
+    re = [_enc(P, keys, radar.pack_vital(zt[t].real, cfg.n_slots), lvl, 2 * t) for t in range(cfg.F)]
+    im = [_enc(P, keys, radar.pack_vital(zt[t].imag, cfg.n_slots), lvl, 2 * t + 1) for t in range(cfg.F)]
+    E = cc.k1_energy(ev, re, im)
+    E_dec = orc.decrypt_vector(P, keys, E)[: cfg.R]
+    assert rel_err(E_dec, dsp.energy(zt)) < 1e-3
+    Nc, Dc = cc.k2_soft_attention(ev, book, E, cfg)
+    assert Nc.level == 0
+    N = orc.decrypt_vector(P, keys, Nc)[0]
+    D = orc.decrypt_vector(P, keys, Dc)[0]
+    Np, Dp, rp = dsp.soft_attention(dsp.energy(zt), cfg.gamma, cfg.F)
+    assert abs(N - Np) <= 1e-3 * abs(Np) and abs(D - Dp) <= 1e-3 * abs(Dp)
+    assert round(N / D) == round(rp)
+
+
+def _gesture_setup(P, A=2, R=4, D=8, F=2, seed=5):
+    n = A * R * D
+    cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8))
+    Z, _ = radar.gesture_scene(A, R, D, F, seed=seed, cls=seed % 5)
+    Zt = radar.preprocess_gesture(Z)
+    return cfg, Zt
+
+
+def test_gesture_frame_and_fc(Pg):
+    P = Pg
+    cfg, Zt = _gesture_setup(P)
+    keys = orc.keygen(P, seed=2002, rotations=cc.required_rotations("gesture", cfg, P.n))
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    lvl = P.L
+    feats, feats_plain = [], []
+    for t in range(cfg.F):
+        v = radar.pack_doppler(Zt[t])
+        cr = _enc(P, keys, v.real, lvl, 2 * t)
+        ci = _enc(P, keys, v.imag, lvl, 2 * t + 1)
+        if t == 0:
+            dre, dim = cc.k3_doppler_dft(ev, book, cr, ci, cfg)
+            want = dsp.doppler_dft(v, cfg.D)
+            assert rel_err(orc.decrypt_vector(P, keys, dre), want.real) < 1e-3
+            assert rel_err(orc.decrypt_vector(P, keys, dim), want.imag) < 1e-3
+        f = cc.gesture_frame(ev, book, cr, ci, cfg)
+        assert f.level == lvl - 6  # Table tab:depth: feature weighting at Sigma 6
+        fp = dsp.gesture_frame_features(v, cfg.A, cfg.R, cfg.D, cfg.gamma)
+        assert rel_err(orc.decrypt_vector(P, keys, f), fp) < 1e-3
+        feats.append(f)
+        feats_plain.append(fp)
+    feat = cc.frame_accumulate(ev, feats)
+    xp = np.sum(feats_plain, axis=0)
+    dims = cfg.fc_dims
+    Ws, bs = radar.fc_weights([dims[0], dims[1], dims[2], 5], seed=7)
+    Ws[0] = Ws[0] / max(np.max(np.abs(Ws[0] @ xp)), 1e-30) * 0.8  # pre-activations O(1)
+    logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
+    assert logits.level == lvl - 11  # Sigma 11
+    got = orc.decrypt_vector(P, keys, logits)[:5]
+    want = dsp.mlp_forward(xp, Ws, bs)
+    assert rel_err(got, want) < 1e-3
+    assert int(np.argmax(got)) == int(np.argmax(want))
+
+
+def test_vitals_v2_small(Pg):
+    P = toy(log_n=10, n_q=8, scale_bits=40, n_p=2, alpha=2)
+    cfg = cc.ChainCfg(R=8, F=16, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=2.0,
+                      bands=((0.1, 0.6), (0.7, 1.0)))
+    z, _ = radar.vital_scene(cfg.R, cfg.F, cfg.fs, seed=1003)
+    zt = radar.preprocess_vital(z)
+    keys = orc.keygen(P, seed=2003, rotations=cc.required_rotations("vitals_v2", cfg, P.n))
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    lvl = 7
+    re = [_enc(P, keys, radar.pack_vital(zt[t].real, cfg.n_slots), lvl, 2 * t) for t in range(cfg.F)]
+    im = [_enc(P, keys, radar.pack_vital(zt[t].imag, cfg.n_slots), lvl, 2 * t + 1) for t in range(cfg.F)]
+    taps = [np.array([0.2, 0.3, 0.3, 0.2]), np.array([0.25, -0.5, 0.25])]
+    out = cc.vitals_v2(ev, re, im, taps, cfg)
+    I = np.array([dsp.soft_iq(zt[t], cfg.p_phi)[0] for t in range(cfg.F)])
+    Q = np.array([dsp.soft_iq(zt[t], cfg.p_phi)[1] for t in range(cfg.F)])
+    for bi, h in enumerate(taps):
+        y = dsp.taylor_phase(dsp.fir(I, h), dsp.fir(Q, h), cfg.taylor_order)
+        bins = dsp.band_bins(len(y), cfg.fs, cfg.bands[bi])
+        want = dsp.narrowband_power(y, bins)
+        got = np.array([orc.decrypt_vector(P, keys, c)[0] for c in out[bi]])
+        assert len(got) == len(bins) > 0
+        assert out[bi][0].level == 0
+        assert rel_err(got, want) < 1e-3
+
+
+def test_trace_is_data_oblivious(Pg):
+    P = toy(log_n=10, n_q=4, scale_bits=40, n_p=2, alpha=2)
+    cfg = cc.ChainCfg(R=8, F=3, gamma=2, n_slots=P.n // 2)
+    keys = orc.keygen(P, seed=9, rotations=cc.required_rotations("vitals_v1", cfg, P.n))
+    traces = []
+    for seed in (1, 2):
+        rng = np.random.default_rng(seed)
+        ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+        book = cc.PlainBook(P)
+        re = [_enc(P, keys, rng.uniform(-1, 1, 8), 3, t, seed) for t in range(cfg.F)]
+        im = [_enc(P, keys, rng.uniform(-1, 1, 8), 3, 10 + t, seed) for t in range(cfg.F)]
+        cc.vitals_v1(ev, book, re, im, cfg)
+        traces.append(ev.trace)
+    assert traces[0] == traces[1] and len(traces[0]) > 10
+
+
+def test_required_rotation_counts():
+    # SURVEY §8(d) key table: C3 needs 14 keys, C4 31 (amounts normalised to [0, N/2))
+    n_ring = 1 << 16
+    cfg = cc.ChainCfg(A=4, R=32, D=32, n_slots=4096, gamma=4, fc_dims=(4096, 64, 32, 8))
+    k3 = cc.required_rotations("k3_doppler_dft", cfg, n_ring)
+    assert len(k3) == 14
+    assert (n_ring // 2 - 31) in k3 and 25 in k3
+    vital = cc.required_rotations("vitals_v1", cc.ChainCfg(R=128), n_ring)
+    assert vital == [1, 2, 4, 8, 16, 32, 64]
