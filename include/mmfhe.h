@@ -1,0 +1,229 @@
+/*
+ * mmfhe.h -- C-ABI of the B200-native mmFHE cloud-side library.
+ *
+ * The library evaluates the mmFHE kernel chains (PAPER.md §"Cloud-Side
+ * Algorithms") over RNS-CKKS ciphertexts on one CUDA device.  It
+ * follows the paper's problem statement: the cloud "receives ciphertexts and
+ * public parameters", "selects and chains kernels ... according to the target
+ * application" and "returns the encrypted result", holding
+ * only the evaluation keys (rlk, gk; sk "never leaves the client").
+ * The library therefore never takes a secret key, never decrypts and draws no
+ * randomness: every call is a deterministic function of its inputs.
+ *
+ * Conventions (all entry points)
+ *   - Every call returns mmfhe_status; nothing throws across the ABI.
+ *     On error, mmfhe_last_error(ctx) holds a one-line message.
+ *   - Polynomials are RNS residues, uint64 little-endian, limb-major:
+ *     a ciphertext at level l is [2][l+1][N] (N = 2^log_n), residue of limb i
+ *     modulo q_i, each in [0, q_i).
+ *   - form = MMFHE_FORM_COEFF (0): coefficient representation -- the interchange
+ *     format, identical to the client's.  form = MMFHE_FORM_EVAL (1): the
+ *     library's internal NTT (evaluation) representation; its ordering is
+ *     private (bit-reversed), only valid between calls of the same library.
+ *   - on_device != 0: data is a CUDA device pointer on the ctx device (e.g. a
+ *     torch tensor's data_ptr()); otherwise a host pointer (copies are done on
+ *     the ctx stream, pinned host memory recommended).
+ *   - Ciphertext buffers are CALLER-OWNED (inputs and outputs).  Keys and
+ *     plaintext operands are copied into library-owned device memory and are
+ *     freed by mmfhe_ctx_destroy.
+ *   - Calls are asynchronous on the ctx stream (the one passed to
+ *     mmfhe_ctx_create) unless stated; device outputs are valid after the
+ *     caller synchronises that stream.  Host outputs are synchronous.
+ *   - A ctx is not thread-safe; use one ctx per GPU / rank.
+ *
+ * Errors: depth exhausted -> MMFHE_E_DEPTH; missing Galois key
+ * -> MMFHE_E_MISSING_KEY; layout/capacity -> MMFHE_E_LAYOUT; scale mismatch ->
+ * MMFHE_E_SCALE; frame count / dimension mismatch -> MMFHE_E_SHAPE; unknown
+ * plaintext operand -> MMFHE_E_MISSING_PLAIN.
+ */
+#ifndef MMFHE_H
+#define MMFHE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MMFHE_OK = 0,
+    MMFHE_E_INVALID_ARG = 1,
+    MMFHE_E_PARAMS = 2,
+    MMFHE_E_DEPTH = 3,
+    MMFHE_E_MISSING_KEY = 4,
+    MMFHE_E_LAYOUT = 5,
+    MMFHE_E_SCALE = 6,
+    MMFHE_E_SHAPE = 7,
+    MMFHE_E_CUDA = 8,
+    MMFHE_E_OOM = 9,
+    MMFHE_E_NCCL = 10,
+    MMFHE_E_FORMAT = 11,
+    MMFHE_E_MISSING_PLAIN = 12
+} mmfhe_status;
+
+enum { MMFHE_FORM_COEFF = 0, MMFHE_FORM_EVAL = 1 };
+
+typedef struct mmfhe_ctx mmfhe_ctx; /* opaque */
+
+/* CKKS parameters (P:433-454 Table tab:ckks_params; primes explicit).
+ *   q[0..n_q)  : ciphertext modulus chain q_0..q_L (L = n_q - 1), each prime,
+ *                = 1 mod 2N, < 2^60;
+ *   p[0..n_p)  : special primes P = p_0...p_{K-1} of hybrid key switching;
+ *   alpha      : limbs per key-switching digit, dnum(l) = ceil((l+1)/alpha);
+ *   scale_bits : Delta = 2^scale_bits for fresh encodings. */
+typedef struct {
+    uint32_t log_n;
+    uint32_t n_q;
+    const uint64_t *q;
+    uint32_t n_p;
+    const uint64_t *p;
+    uint32_t alpha;
+    uint32_t scale_bits;
+    uint32_t security; /* informational (e.g. 128) */
+} mmfhe_params;
+
+/* A ciphertext (or plaintext when n_polys == 1).  data points at
+ * [n_polys][level+1][N] uint64; n_slots is the packing period n. */
+typedef struct {
+    uint32_t log_n;
+    uint32_t level;
+    uint32_t n_slots;
+    uint32_t form;
+    double scale;
+    uint64_t *data;
+    int32_t on_device;
+    uint32_t n_polys; /* 2 for ciphertexts (0 is read as 2), 1 for plaintexts */
+} mmfhe_ct;
+
+/* Public chain parameters (R, D, A, F, gamma, P_phi,
+ * Taylor order, filter taps, FC dims are public). */
+typedef struct {
+    uint32_t R, D, A, F;
+    uint32_t gamma;        /* K2 sharpening exponent, power of two */
+    uint32_t p_phi;        /* K4 mask exponent, power of two */
+    uint32_t taylor_order; /* K7: 1 or 3 */
+    uint32_t n_slots;      /* packing period n */
+    uint32_t bsgs_baby;    /* K3 baby steps b (0: ceil(sqrt(2D-1))) */
+    uint32_t hoist;        /* 0: none (only mode in this version) */
+    uint32_t fc_dims[4];   /* n_in, h1, h2, h3 (padded logits) */
+    uint32_t notch_width;  /* K6 zeroed bins around D/2 */
+    uint32_t n_bands;      /* vital V2: number of FIR bands (<= 4) */
+    uint32_t n_taps[4];    /* vital V2: taps per band (scalars "k5.b<i>") */
+    uint32_t n_bins[4];    /* vital V2: narrowband DFT bins per band */
+    uint32_t bins[4][64];  /* vital V2: bin indices k per band */
+    double fs;             /* frame rate (Hz) */
+} mmfhe_chain_cfg;
+
+/* ---- context ------------------------------------------------------------ */
+
+/* Create a context on cuda_device using cuda_stream (a cudaStream_t, may be
+ * NULL for the legacy default stream).  Precomputes NTT, base-conversion and
+ * rescale tables for every prime.  MMFHE_E_PARAMS if a prime is not = 1 mod
+ * 2N, not < 2^60, duplicated, or alpha/log_n out of range. */
+mmfhe_status mmfhe_ctx_create(const mmfhe_params *params, int cuda_device, void *cuda_stream,
+                              mmfhe_ctx **out);
+mmfhe_status mmfhe_ctx_destroy(mmfhe_ctx *ctx);
+const char *mmfhe_last_error(const mmfhe_ctx *ctx);
+/* Bytes of device memory currently held by the ctx (keys, plains, pool). */
+mmfhe_status mmfhe_ctx_memory(mmfhe_ctx *ctx, size_t *bytes);
+/* Number of CUDA kernels this ctx has launched so far. */
+mmfhe_status mmfhe_launch_count(mmfhe_ctx *ctx, uint64_t *count);
+
+/* ---- keys ------------------------------------------------------- */
+
+/* Rotation amounts (normalised to [0, N/2)) the chain needs; tells the
+ * client which Galois keys to generate (SURVEY §8(d) key table).  Writes at
+ * most cap entries, *n = total count (MMFHE_E_LAYOUT if cap too small). */
+mmfhe_status mmfhe_chain_required_rotations(mmfhe_ctx *ctx, const char *chain, const mmfhe_chain_cfg *cfg,
+                                            int32_t *steps, size_t cap, size_t *n);
+
+/* Evaluation keys in coefficient form, layout [dnum_L][2][L+1+K][N]
+ * (b_j then a_j, limbs q_0..q_L then p_0..p_{K-1}); n_words must equal
+ * dnum_L*2*(L+1+K)*N.  Relinearisation key = key for s^2; Galois key for
+ * step k = key for sigma_g(s), g = 5^(k mod N/2) mod 2N.  Host or device
+ * pointer (on_device). */
+mmfhe_status mmfhe_load_relin_key(mmfhe_ctx *ctx, const uint64_t *words, size_t n_words, int on_device);
+mmfhe_status mmfhe_load_galois_key(mmfhe_ctx *ctx, int32_t step, const uint64_t *words, size_t n_words,
+                                   int on_device);
+
+/* ---- public plaintext operands ------------------------------- */
+
+/* Import a pre-encoded plaintext (n_polys = 1, form COEFF) under (name, level).
+ * pt->scale is its scale (q_level for multiplicative operands). */
+mmfhe_status mmfhe_load_plain(mmfhe_ctx *ctx, const char *name, const mmfhe_ct *pt);
+/* Encode v[0..n) (period n, replicated to N/2 slots) at (level, scale) with the
+ * library's own canonical-embedding encoder and store it under (name, level). */
+mmfhe_status mmfhe_encode_plain(mmfhe_ctx *ctx, const char *name, const double *v, size_t n, uint32_t level,
+                                double scale);
+/* Encode every public operand a chain needs (K2 ramps, K3 diagonals, K6 mask,
+ * FC diagonals and biases from fc weights, FIR taps, DFT coefficients) at the
+ * levels the chain uses them, starting from entry level in_level.
+ *   fc_w / fc_b: row-major weights of the FC layers (may be NULL for non-FC chains),
+ *   fc_w[i] is fc_dims[i+1] x fc_dims[i] (rows beyond n_classes zero-padded by caller),
+ *   taps[b]: FIR taps of band b (may be NULL for non-V2 chains). */
+mmfhe_status mmfhe_prepare_chain(mmfhe_ctx *ctx, const char *chain, const mmfhe_chain_cfg *cfg, uint32_t in_level,
+                                 const double *const *fc_w, const double *const *fc_b, const double *const *taps);
+/* Scalar constants used by lincomb ops (K5 taps, VP+ DFT coefficients) are
+ * encoded exactly: round-half-away(c * q_l). */
+mmfhe_status mmfhe_load_scalars(mmfhe_ctx *ctx, const char *name, const double *v, size_t n);
+
+/* ---- chains -------------------------------------------------- */
+
+/* Chains: "k1_energy", "vitals_v1", "vitals_v2", "k3_doppler_dft",
+ * "gesture_frame", "gesture_fc", "gesture" (frames + accumulate + FC).
+ * in[0..n_in): input ciphertexts in the order the chain documents (DESIGN.md
+ * §2): k1/vitals: re_0, im_0, re_1, im_1, ...; gesture*: v_re_t, v_im_t per frame.
+ * out: caller buffers; mmfhe_chain_plan tells their count and levels.
+ * MMFHE_E_SHAPE on a frame-count mismatch, MMFHE_E_DEPTH if in_level is too
+ * low, MMFHE_E_MISSING_KEY / MMFHE_E_MISSING_PLAIN for absent operands. */
+mmfhe_status mmfhe_chain_plan(mmfhe_ctx *ctx, const char *chain, const mmfhe_chain_cfg *cfg, uint32_t in_level,
+                              size_t n_in, uint32_t *out_levels, size_t cap, size_t *n_out);
+mmfhe_status mmfhe_eval_chain(mmfhe_ctx *ctx, const char *chain, const mmfhe_chain_cfg *cfg, const mmfhe_ct *in,
+                              size_t n_in, mmfhe_ct *out, size_t cap, size_t *n_out);
+
+/* Sum of n partial ciphertexts mod q (cross-GPU frame accumulation after an
+ * NCCL all-gather); all parts at one level and scale. */
+mmfhe_status mmfhe_sum_partials(mmfhe_ctx *ctx, const mmfhe_ct *parts, size_t n, mmfhe_ct *out);
+
+/* ---- primitives (tests, benches) -------------------------------------------
+ * Inputs/outputs follow the mmfhe_ct conventions; out->data must hold the
+ * result size.  Level/scale of out are written by the call. */
+
+/* In-place forward / inverse NTT of rows [n_rows][N]; row r is taken mod
+ * q_{prime_idx[r]} (indices into q_0..q_L, p_0..p_{K-1}). Device pointer. */
+mmfhe_status mmfhe_ntt(mmfhe_ctx *ctx, uint64_t *d_rows, uint32_t n_rows, const uint32_t *prime_idx);
+mmfhe_status mmfhe_intt(mmfhe_ctx *ctx, uint64_t *d_rows, uint32_t n_rows, const uint32_t *prime_idx);
+
+mmfhe_status mmfhe_hadd(mmfhe_ctx *ctx, const mmfhe_ct *a, const mmfhe_ct *b, mmfhe_ct *out);
+mmfhe_status mmfhe_hsub(mmfhe_ctx *ctx, const mmfhe_ct *a, const mmfhe_ct *b, mmfhe_ct *out);
+/* out = a (.) pt, pt a plaintext previously loaded under (name, a->level). */
+mmfhe_status mmfhe_pmult(mmfhe_ctx *ctx, const mmfhe_ct *a, const char *pt_name, mmfhe_ct *out);
+/* HMult = tensor + relinearisation (no rescale). */
+mmfhe_status mmfhe_hmult(mmfhe_ctx *ctx, const mmfhe_ct *a, const mmfhe_ct *b, mmfhe_ct *out);
+/* Relinearise a 3-poly tensor ct (n_polys = 3). */
+mmfhe_status mmfhe_relin(mmfhe_ctx *ctx, const mmfhe_ct *a3, mmfhe_ct *out);
+/* HRot by step k: (sigma_g c0 + d0, d1), (d0, d1) = KS(sigma_g c1; gk_k). */
+mmfhe_status mmfhe_hrot(mmfhe_ctx *ctx, const mmfhe_ct *a, int32_t step, mmfhe_ct *out);
+/* Rescale by q_level, round-half-up. */
+mmfhe_status mmfhe_rescale(mmfhe_ctx *ctx, const mmfhe_ct *a, mmfhe_ct *out);
+/* Hybrid key switching of one polynomial x (n_polys = 1, level l) with the
+ * relinearisation key (step = 0) or the Galois key of `step`: out = (d0, d1). */
+mmfhe_status mmfhe_keyswitch(mmfhe_ctx *ctx, const mmfhe_ct *x, int32_t step, int use_relin, mmfhe_ct *out);
+/* Drop limbs to `level` (exact). */
+mmfhe_status mmfhe_mod_switch(mmfhe_ctx *ctx, const mmfhe_ct *a, uint32_t level, mmfhe_ct *out);
+
+/* ---- batched ops (throughput benches): n independent ciphertexts ---------- */
+mmfhe_status mmfhe_hrot_batch(mmfhe_ctx *ctx, const mmfhe_ct *a, size_t n, int32_t step, mmfhe_ct *out);
+mmfhe_status mmfhe_hmult_batch(mmfhe_ctx *ctx, const mmfhe_ct *a, const mmfhe_ct *b, size_t n, mmfhe_ct *out);
+
+/* ---- op trace (Theorem P:999-1006: data-oblivious execution) -------------- */
+/* One logical op per line: "<op> <level> <arg>".  mmfhe_trace_clear resets. */
+mmfhe_status mmfhe_trace_get(mmfhe_ctx *ctx, char *buf, size_t cap, size_t *len);
+mmfhe_status mmfhe_trace_clear(mmfhe_ctx *ctx);
+mmfhe_status mmfhe_trace_enable(mmfhe_ctx *ctx, int on);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMFHE_H */

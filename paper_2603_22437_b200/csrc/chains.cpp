@@ -1,0 +1,531 @@
+// chains.cpp -- the mmFHE kernel chains over the device evaluator.
+//
+// Each kernel follows the paper's circuit with the canonical op sequence of
+// SURVEY §8(c)-7 (relinearisation / rescale placement, BSGS split, overflow
+// folds), so that the op trace and every residue equal the CPU oracle's:
+//   K1  Eq. energy            P:767-771     K5  Eq. fir_iq
+//   K2  Eqs. soft_power_*     P:777-788     K6  Eq. notch_mask
+//   K2b Eq. gesture_soft_pow  P:128-133     K7  Eq. taylor_arctan
+//   K3  Eqs. dft_kernel/re/im P:797-815,    FC  Eq. mlp_forward
+//       BSGS P:164-176
+//   K4  Eqs. phase_mask/iq
+// Pipelines: vital signs P:901-902, dynamic classification P:904-907.
+//
+// Public plaintext operands are looked up by (name, level); when absent and
+// the ctx was prepared (mmfhe_prepare_chain), they are computed from the
+// paper's formulas and encoded with the library's encoder on first use.
+#include <cmath>
+#include <complex>
+#include <functional>
+
+#include "chains.h"
+
+namespace mmfhe {
+
+namespace {
+
+uint32_t ceil_sqrt(uint32_t x)
+{
+    uint32_t b = 0;
+    while (b * b < x) ++b;
+    return b;
+}
+
+uint32_t ilog2(uint32_t x)
+{
+    uint32_t r = 0;
+    while ((1u << r) < x) ++r;
+    return r;
+}
+
+std::vector<double> hann(uint32_t M)
+{
+    std::vector<double> w(M);
+    if (M == 1) {
+        w[0] = 1.0;
+        return w;
+    }
+    for (uint32_t i = 0; i < M; ++i) w[i] = 0.5 - 0.5 * std::cos(2.0 * M_PI * i / (double)(M - 1));
+    return w;
+}
+
+// Rot(v, k)[j] = v[(j + k) mod n]
+std::vector<double> rot(const std::vector<double> &v, int64_t k)
+{
+    const int64_t n = (int64_t)v.size();
+    std::vector<double> o(n);
+    for (int64_t j = 0; j < n; ++j) o[j] = v[(size_t)(((j + k) % n + n) % n)];
+    return o;
+}
+
+struct Sched {
+    uint32_t b;
+    struct G {
+        uint32_t gp;
+        int32_t G;
+        std::vector<uint32_t> babies;
+    };
+    std::vector<G> giants;
+};
+
+Sched k3_schedule(const mmfhe_chain_cfg &cfg)
+{
+    const int32_t D = (int32_t)cfg.D, d = 2 * D - 1, o_min = -(D - 1);
+    Sched s;
+    s.b = cfg.bsgs_baby ? cfg.bsgs_baby : ceil_sqrt((uint32_t)d);
+    const uint32_t g = ((uint32_t)d + s.b - 1) / s.b;
+    for (uint32_t gp = 0; gp < g; ++gp) {
+        Sched::G gg{gp, o_min + (int32_t)(gp * s.b), {}};
+        for (uint32_t bs = 0; bs < s.b; ++bs)
+            if (gg.G + (int32_t)bs <= D - 1) gg.babies.push_back(bs);
+        s.giants.push_back(gg);
+    }
+    return s;
+}
+
+Sched fc_schedule(uint32_t h)
+{
+    Sched s;
+    s.b = ceil_sqrt(h);
+    const uint32_t g = (h + s.b - 1) / s.b;
+    for (uint32_t gp = 0; gp < g; ++gp) {
+        Sched::G gg{gp, (int32_t)(gp * s.b), {}};
+        for (uint32_t bs = 0; bs < s.b; ++bs)
+            if (gp * s.b + bs < h) gg.babies.push_back(bs);
+        s.giants.push_back(gg);
+    }
+    return s;
+}
+
+std::vector<uint32_t> rotsum_steps(uint32_t count, uint32_t stride)
+{
+    std::vector<uint32_t> out;
+    for (uint32_t c = 1, s = stride; c < count; c *= 2, s *= 2) out.push_back(s);
+    return out;
+}
+
+class Runner {
+  public:
+    Runner(Ctx &c, const mmfhe_chain_cfg &cfg) : c_(c), cfg_(cfg) {}
+
+    // plaintext operand (name, level), computed + encoded lazily when the ctx is prepared
+    const DPlain &plain(const std::string &name, uint32_t level, double scale,
+                        const std::function<std::vector<double>()> &values)
+    {
+        DPlain *p = c_.find_plain(name, level);
+        if (p) return *p;
+        MMFHE_REQUIRE(c_.auto_encode, MMFHE_E_MISSING_PLAIN, "missing plaintext operand " + plain_key(name, level));
+        encode_plain(c_, name, values(), level, scale);
+        return *c_.find_plain(name, level);
+    }
+    double qscale(uint32_t level) const { return (double)c_.primes[level]; }
+
+    const std::vector<double> &scalars(const std::string &name, const std::function<std::vector<double>()> &fn)
+    {
+        auto it = c_.scalars.find(name);
+        if (it != c_.scalars.end()) return it->second;
+        MMFHE_REQUIRE(c_.auto_encode && fn, MMFHE_E_MISSING_PLAIN, "missing scalar table " + name);
+        return c_.scalars[name] = fn();
+    }
+
+    // ---------------------------------------------------------- K1 / K2
+    DCt k1_energy(const std::vector<const DCt *> &re, const std::vector<const DCt *> &im)
+    {
+        std::vector<std::pair<const DCt *, const DCt *>> pairs;
+        for (size_t t = 0; t < re.size(); ++t) {
+            pairs.push_back({re[t], re[t]});
+            pairs.push_back({im[t], im[t]});
+        }
+        return ev_relin_rescale(c_, ev_tensor_sum(c_, pairs));
+    }
+
+    std::pair<DCt, DCt> k2_soft_attention(const DCt &E)
+    {
+        DCt w = ev_drop_to(c_, E, E.level);
+        for (uint32_t i = 0; i < ilog2(cfg_.gamma); ++i) w = ev_square_rescale(c_, w);
+        const uint32_t n = E.n_slots, R = cfg_.R;
+        const double FFR = (double)cfg_.F * cfg_.F * R;
+        const DPlain &ramp = plain("k2.ramp", w.level, qscale(w.level), [&] {
+            std::vector<double> v(n, 0.0);
+            for (uint32_t r = 0; r < R; ++r) v[r] = (double)r / FFR;
+            return v;
+        });
+        const DPlain &one = plain("k2.one", w.level, qscale(w.level), [&] {
+            std::vector<double> v(n, 0.0);
+            for (uint32_t r = 0; r < R; ++r) v[r] = 1.0 / FFR;
+            return v;
+        });
+        DCt Nn = ev_rescale(c_, ev_pmult_sum(c_, {{&ramp, &w}}));
+        DCt Dd = ev_rescale(c_, ev_pmult_sum(c_, {{&one, &w}}));
+        return {ev_rotsum(c_, Nn, R, 1), ev_rotsum(c_, Dd, R, 1)};
+    }
+
+    // ---------------------------------------------------------- K3 (BSGS)
+    std::pair<DCt, DCt> k3_doppler_dft(const DCt &vre, const DCt &vim)
+    {
+        const uint32_t n = vre.n_slots, D = cfg_.D, lvl = vre.level;
+        Sched s = k3_schedule(cfg_);
+        std::vector<DCt> xr, xi;
+        xr.push_back(ev_drop_to(c_, vre, lvl));
+        xi.push_back(ev_drop_to(c_, vim, lvl));
+        for (uint32_t b = 1; b < s.b; ++b) xr.push_back(ev_rotate(c_, vre, (int32_t)b));
+        for (uint32_t b = 1; b < s.b; ++b) xi.push_back(ev_rotate(c_, vim, (int32_t)b));
+        // W = hann[n] e^{-j 2 pi sigma(d) n / D}
+        auto diag = [&](bool imag, int32_t o, int32_t G, bool neg) {
+            std::vector<double> w = hann(D), v(n, 0.0);
+            for (uint32_t j = 0; j < n; ++j) {
+                const uint32_t col = (uint32_t)(((int64_t)j + o) % (int64_t)n + n) % n;
+                if (j / D != col / D) continue;
+                const uint32_t d = j % D, m = col % D;
+                const uint32_t sig = (d + D / 2) % D;
+                const double ang = -2.0 * M_PI * (double)sig * (double)m / (double)D;
+                v[j] = w[m] * (imag ? std::sin(ang) : std::cos(ang)) * (neg ? -1.0 : 1.0);
+            }
+            return rot(v, -G);
+        };
+        DCt out_re, out_im;
+        bool first = true;
+        for (auto &g : s.giants) {
+            std::vector<std::pair<const DPlain *, const DCt *>> tre, tim;
+            for (uint32_t b : g.babies) {
+                const int32_t o = g.G + (int32_t)b;
+                const std::string sfx = "." + std::to_string(g.gp) + "." + std::to_string(b);
+                const DPlain &pc = plain("k3.c" + sfx, lvl, qscale(lvl), [&] { return diag(false, o, g.G, false); });
+                const DPlain &ps = plain("k3.s" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, false); });
+                const DPlain &pn = plain("k3.ns" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, true); });
+                tre.push_back({&pc, &xr[b]});
+                tre.push_back({&pn, &xi[b]});
+                tim.push_back({&ps, &xr[b]});
+                tim.push_back({&pc, &xi[b]});
+            }
+            DCt ir = ev_rotate(c_, ev_pmult_sum(c_, tre), g.G);
+            DCt ii = ev_rotate(c_, ev_pmult_sum(c_, tim), g.G);
+            if (first) {
+                out_re = std::move(ir);
+                out_im = std::move(ii);
+                first = false;
+            } else {
+                out_re = ev_addsub(c_, out_re, ir, false);
+                out_im = ev_addsub(c_, out_im, ii, false);
+            }
+        }
+        return {ev_rescale(c_, out_re), ev_rescale(c_, out_im)};
+    }
+
+    // ---------------------------------------------------------- gesture frame
+    DCt k1_power(const DCt &dre, const DCt &dim)
+    {
+        return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&dre, &dre}, {&dim, &dim}}));
+    }
+
+    DCt k6_notch(const DCt &P)
+    {
+        const uint32_t D = cfg_.D, n = P.n_slots;
+        const DPlain &m = plain("k6.mask", P.level, qscale(P.level), [&] {
+            std::vector<double> w = hann(D);
+            double sw = 0;
+            for (double x : w) sw += x;
+            const double s = (double)cfg_.R * cfg_.A * sw * sw;
+            const uint32_t width = cfg_.notch_width ? cfg_.notch_width : 1;
+            const uint32_t lo = D / 2 - (width - 1) / 2;
+            std::vector<double> v(n);
+            for (uint32_t j = 0; j < n; ++j) {
+                const uint32_t d = j % D;
+                v[j] = (d >= lo && d < lo + width) ? 0.0 : 1.0 / s;
+            }
+            return v;
+        });
+        return ev_rescale(c_, ev_pmult_sum(c_, {{&m, &P}}));
+    }
+
+    DCt k2_doppler_soft_power(const DCt &Pm)
+    {
+        DCt S = ev_rotsum(c_, Pm, Pm.n_slots / cfg_.D, cfg_.D);
+        for (uint32_t i = 0; i < ilog2(cfg_.gamma); ++i) S = ev_square_rescale(c_, S);
+        DCt Pd = ev_drop_to(c_, Pm, S.level);
+        return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&Pd, &S}}));
+    }
+
+    DCt gesture_frame(const DCt &vre, const DCt &vim)
+    {
+        auto d = k3_doppler_dft(vre, vim);
+        DCt P = k1_power(d.first, d.second);
+        DCt Pm = k6_notch(P);
+        return k2_doppler_soft_power(Pm);
+    }
+
+    // ---------------------------------------------------------- FC
+    DCt fc_layer(const DCt &x, uint32_t layer, bool square)
+    {
+        const uint32_t n_in = cfg_.fc_dims[layer - 1], h = cfg_.fc_dims[layer];
+        const uint32_t lvl = x.level;
+        Sched s = fc_schedule(h);
+        const std::vector<double> *W = nullptr, *bias = nullptr;
+        if (c_.fc_w.size() >= layer) {
+            W = &c_.fc_w[layer - 1];
+            bias = &c_.fc_b[layer - 1];
+        }
+        std::vector<DCt> babies;
+        babies.push_back(ev_drop_to(c_, x, lvl));
+        for (uint32_t b = 1; b < std::min(s.b, h); ++b) babies.push_back(ev_rotate(c_, x, (int32_t)b));
+        DCt acc;
+        bool first = true;
+        for (auto &g : s.giants) {
+            std::vector<std::pair<const DPlain *, const DCt *>> terms;
+            for (uint32_t b : g.babies) {
+                const uint32_t i = (uint32_t)g.G + b;
+                const std::string name = "fc" + std::to_string(layer) + ".d." + std::to_string(g.gp) + "." +
+                                         std::to_string(b);
+                const DPlain &p = plain(name, lvl, qscale(lvl), [&] {
+                    MMFHE_REQUIRE(W != nullptr, MMFHE_E_MISSING_PLAIN, "FC weights not prepared");
+                    std::vector<double> v(n_in);
+                    for (uint32_t j = 0; j < n_in; ++j) v[j] = (*W)[(size_t)(j % h) * n_in + (j + i) % n_in];
+                    return rot(v, -g.G);
+                });
+                terms.push_back({&p, &babies[b]});
+            }
+            DCt inner = ev_pmult_sum(c_, terms);
+            if (g.G) inner = ev_rotate(c_, inner, g.G);
+            if (first) {
+                acc = std::move(inner);
+                first = false;
+            } else {
+                acc = ev_addsub(c_, acc, inner, false);
+            }
+        }
+        DCt z = ev_rescale(c_, acc);
+        DCt y = ev_rotsum(c_, z, n_in / h, h);
+        const DPlain &bp = plain("fc" + std::to_string(layer) + ".bias", y.level, y.scale, [&] {
+            MMFHE_REQUIRE(bias != nullptr, MMFHE_E_MISSING_PLAIN, "FC bias not prepared");
+            return *bias;
+        });
+        y = ev_add_plain(c_, y, bp);
+        if (square) y = ev_square_rescale(c_, y);
+        return y;
+    }
+
+    DCt gesture_fc(const DCt &feat)
+    {
+        DCt x = fc_layer(feat, 1, true);
+        x = fc_layer(x, 2, true);
+        return fc_layer(x, 3, false);
+    }
+
+    // ---------------------------------------------------------- vital V2
+    std::pair<DCt, DCt> k4_soft_iq(const DCt &re, const DCt &im)
+    {
+        DCt p = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&re, &re}, {&im, &im}}));
+        for (uint32_t i = 0; i < ilog2(cfg_.p_phi); ++i) p = ev_square_rescale(c_, p);
+        DCt red = ev_drop_to(c_, re, p.level);
+        DCt i_ = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&p, &red}}));
+        DCt imd = ev_drop_to(c_, im, p.level);
+        DCt q_ = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&p, &imd}}));
+        return {ev_rotsum(c_, i_, cfg_.R, 1), ev_rotsum(c_, q_, cfg_.R, 1)};
+    }
+
+    std::vector<DCt> k5_fir(const std::vector<DCt> &xs, const std::vector<double> &taps)
+    {
+        std::vector<DCt> out;
+        for (size_t t = 0; t < xs.size(); ++t) {
+            std::vector<const DCt *> cts;
+            std::vector<double> cf;
+            for (size_t k = 0; k < taps.size() && k <= t; ++k) {
+                cts.push_back(&xs[t - k]);
+                cf.push_back(taps[k]);
+            }
+            out.push_back(ev_rescale(c_, ev_lincomb(c_, cts, cf)));
+        }
+        return out;
+    }
+
+    std::vector<DCt> k7_taylor_phase(const std::vector<DCt> &If, const std::vector<DCt> &Qf)
+    {
+        std::vector<DCt> out;
+        for (size_t t = 1; t < If.size(); ++t) {
+            DCt ty = ev_tensor_sum(c_, {{&Qf[t], &If[t - 1]}});
+            DCt ty2 = ev_tensor_sum(c_, {{&If[t], &Qf[t - 1]}});
+            DCt y = ev_relin_rescale(c_, ev_addsub(c_, ty, ty2, true));
+            if (cfg_.taylor_order == 1) {
+                out.push_back(std::move(y));
+                continue;
+            }
+            DCt x = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&If[t], &If[t - 1]}, {&Qf[t], &Qf[t - 1]}}));
+            DCt x2 = ev_square_rescale(c_, x);
+            DCt y2 = ev_square_rescale(c_, y);
+            DCt yt = ev_rescale(c_, ev_lincomb(c_, {&y}, {-1.0 / 3.0}));
+            DCt yd = ev_drop_to(c_, y, x2.level);
+            DCt yx2 = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&yd, &x2}}));
+            DCt y3 = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&y2, &yt}}));
+            out.push_back(ev_addsub(c_, yx2, y3, false));
+        }
+        return out;
+    }
+
+    std::vector<DCt> vp_band_power(const std::vector<DCt> &ys, uint32_t band)
+    {
+        const uint32_t Fp = (uint32_t)ys.size();
+        std::vector<const DCt *> ptrs;
+        for (auto &y : ys) ptrs.push_back(&y);
+        std::vector<DCt> out;
+        for (uint32_t bi = 0; bi < cfg_.n_bins[band]; ++bi) {
+            const uint32_t k = cfg_.bins[band][bi];
+            const std::string sfx = "." + std::to_string(band) + "." + std::to_string(k);
+            auto coefs = [&](bool imag) {
+                return [=]() {
+                    std::vector<double> w = hann(Fp), v(Fp);
+                    for (uint32_t t = 0; t < Fp; ++t) {
+                        const double ang = 2.0 * M_PI * (double)k * t / (double)Fp;
+                        v[t] = imag ? -w[t] * std::sin(ang) / Fp : w[t] * std::cos(ang) / Fp;
+                    }
+                    return v;
+                };
+            };
+            const std::vector<double> &cc = scalars("vp.c" + sfx, coefs(false));
+            const std::vector<double> &ss = scalars("vp.s" + sfx, coefs(true));
+            MMFHE_REQUIRE(cc.size() == Fp && ss.size() == Fp, MMFHE_E_SHAPE, "DFT coefficient count");
+            DCt xr = ev_rescale(c_, ev_lincomb(c_, ptrs, cc));
+            DCt xi = ev_rescale(c_, ev_lincomb(c_, ptrs, ss));
+            out.push_back(ev_relin_rescale(c_, ev_tensor_sum(c_, {{&xr, &xr}, {&xi, &xi}})));
+        }
+        return out;
+    }
+
+    std::vector<DCt> vitals_v2(const std::vector<const DCt *> &re, const std::vector<const DCt *> &im)
+    {
+        std::vector<DCt> I, Q;
+        for (size_t t = 0; t < re.size(); ++t) {
+            auto iq = k4_soft_iq(*re[t], *im[t]);
+            I.push_back(std::move(iq.first));
+            Q.push_back(std::move(iq.second));
+        }
+        std::vector<DCt> out;
+        for (uint32_t b = 0; b < cfg_.n_bands; ++b) {
+            const std::vector<double> &taps = scalars("k5.b" + std::to_string(b), nullptr);
+            MMFHE_REQUIRE(taps.size() == cfg_.n_taps[b] || cfg_.n_taps[b] == 0, MMFHE_E_SHAPE, "FIR tap count");
+            std::vector<DCt> If = k5_fir(I, taps), Qf = k5_fir(Q, taps);
+            std::vector<DCt> ys = k7_taylor_phase(If, Qf);
+            for (auto &p : vp_band_power(ys, b)) out.push_back(std::move(p));
+        }
+        return out;
+    }
+
+  private:
+    Ctx &c_;
+    const mmfhe_chain_cfg &cfg_;
+};
+
+uint32_t chain_depth(const std::string &chain, const mmfhe_chain_cfg &cfg)
+{
+    const uint32_t lg = ilog2(cfg.gamma ? cfg.gamma : 1), lp = ilog2(cfg.p_phi ? cfg.p_phi : 1);
+    const uint32_t gf = 3 + lg + 1, fc = 5;
+    const uint32_t v2 = (1 + lp + 1) + 1 + (cfg.taylor_order == 3 ? 3 : 1) + 1 + 1;
+    if (chain == "k1_energy") return 1;
+    if (chain == "vitals_v1") return 1 + lg + 1;
+    if (chain == "vitals_v2") return v2;
+    if (chain == "k3_doppler_dft") return 1;
+    if (chain == "gesture_frame") return gf;
+    if (chain == "gesture_fc") return fc;
+    if (chain == "gesture") return gf + fc;
+    throw Error(MMFHE_E_INVALID_ARG, "unknown chain " + chain);
+}
+
+}  // namespace
+
+std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, const mmfhe_chain_cfg &cfg)
+{
+    std::set<int32_t> ks;
+    const int32_t half = (int32_t)(c.n / 2);
+    auto add = [&](int64_t k) {
+        int32_t v = (int32_t)(((k % half) + half) % half);
+        if (v) ks.insert(v);
+    };
+    chain_depth(chain, cfg);  // validates the name
+    if (chain == "vitals_v1" || chain == "vitals_v2")
+        for (uint32_t s : rotsum_steps(cfg.R, 1)) add(s);
+    if (chain == "k3_doppler_dft" || chain == "gesture_frame" || chain == "gesture") {
+        Sched s = k3_schedule(cfg);
+        for (uint32_t b = 1; b < s.b; ++b) add(b);
+        for (auto &g : s.giants) add(g.G);
+    }
+    if (chain == "gesture_frame" || chain == "gesture")
+        for (uint32_t s : rotsum_steps(cfg.n_slots / cfg.D, cfg.D)) add(s);
+    if (chain == "gesture_fc" || chain == "gesture")
+        for (int layer = 0; layer < 3; ++layer) {
+            const uint32_t h = cfg.fc_dims[layer + 1], n_in = cfg.fc_dims[layer];
+            Sched s = fc_schedule(h);
+            for (uint32_t b = 1; b < std::min(s.b, h); ++b) add(b);
+            for (auto &g : s.giants) add(g.G);
+            for (uint32_t st : rotsum_steps(n_in / h, h)) add(st);
+        }
+    return std::vector<int32_t>(ks.begin(), ks.end());
+}
+
+std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const mmfhe_chain_cfg &cfg, uint32_t in_level,
+                                 size_t n_in)
+{
+    const uint32_t dep = chain_depth(chain, cfg);
+    MMFHE_REQUIRE(in_level >= dep, MMFHE_E_DEPTH,
+                  "chain " + chain + " needs " + std::to_string(dep) + " levels, input has " +
+                      std::to_string(in_level));
+    const uint32_t out = in_level - dep;
+    if (chain == "k1_energy" || chain == "vitals_v1" || chain == "vitals_v2") {
+        MMFHE_REQUIRE(n_in == 2 * (size_t)cfg.F && cfg.F > 0, MMFHE_E_SHAPE, "expected 2F input ciphertexts");
+    } else if (chain == "k3_doppler_dft" || chain == "gesture_frame") {
+        MMFHE_REQUIRE(n_in == 2, MMFHE_E_SHAPE, "expected (v_re, v_im)");
+    } else if (chain == "gesture_fc") {
+        MMFHE_REQUIRE(n_in == 1, MMFHE_E_SHAPE, "expected one feature ciphertext");
+    } else if (chain == "gesture") {
+        MMFHE_REQUIRE(n_in == 2 * (size_t)cfg.F && cfg.F > 0, MMFHE_E_SHAPE, "expected 2F input ciphertexts");
+    }
+    size_t n_out = 1;
+    if (chain == "vitals_v1" || chain == "k3_doppler_dft") n_out = 2;
+    if (chain == "vitals_v2") {
+        n_out = 0;
+        for (uint32_t b = 0; b < cfg.n_bands; ++b) n_out += cfg.n_bins[b];
+    }
+    return std::vector<uint32_t>(n_out, out);
+}
+
+std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_cfg &cfg,
+                           const std::vector<const DCt *> &in)
+{
+    MMFHE_REQUIRE(!in.empty(), MMFHE_E_SHAPE, "no inputs");
+    chain_plan(c, chain, cfg, in[0]->level, in.size());
+    for (auto *x : in)
+        MMFHE_REQUIRE(x->level == in[0]->level && x->scale == in[0]->scale, MMFHE_E_SCALE,
+                      "inputs must share level and scale");
+    Runner r(c, cfg);
+    std::vector<DCt> out;
+    std::vector<const DCt *> re, im;
+    for (size_t i = 0; i + 1 < in.size(); i += 2) {
+        re.push_back(in[i]);
+        im.push_back(in[i + 1]);
+    }
+    if (chain == "k1_energy") {
+        out.push_back(r.k1_energy(re, im));
+    } else if (chain == "vitals_v1") {
+        auto nd = r.k2_soft_attention(r.k1_energy(re, im));
+        out.push_back(std::move(nd.first));
+        out.push_back(std::move(nd.second));
+    } else if (chain == "vitals_v2") {
+        out = r.vitals_v2(re, im);
+    } else if (chain == "k3_doppler_dft") {
+        auto d = r.k3_doppler_dft(*in[0], *in[1]);
+        out.push_back(std::move(d.first));
+        out.push_back(std::move(d.second));
+    } else if (chain == "gesture_frame") {
+        out.push_back(r.gesture_frame(*in[0], *in[1]));
+    } else if (chain == "gesture_fc") {
+        out.push_back(r.gesture_fc(*in[0]));
+    } else if (chain == "gesture") {
+        std::vector<DCt> feats;
+        for (size_t t = 0; t < re.size(); ++t) feats.push_back(r.gesture_frame(*re[t], *im[t]));
+        std::vector<const DCt *> fp;
+        for (auto &f : feats) fp.push_back(&f);
+        DCt acc = ev_sum(c, fp);
+        out.push_back(r.gesture_fc(acc));
+    }
+    return out;
+}
+
+}  // namespace mmfhe

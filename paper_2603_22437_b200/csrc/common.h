@@ -1,0 +1,97 @@
+// common.h -- shared host/device declarations of the mmFHE CUDA library.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mmfhe.h"
+
+namespace mmfhe {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    mmfhe_status status;
+    Error(mmfhe_status s, const std::string &m) : std::runtime_error(m), status(s) {}
+};
+
+#define MMFHE_REQUIRE(cond, status, msg)                                                          \
+    do {                                                                                          \
+        if (!(cond)) throw ::mmfhe::Error((status), (msg));                                       \
+    } while (0)
+
+#define CUDA_CHECK(expr)                                                                          \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            throw ::mmfhe::Error(e_ == cudaErrorMemoryAllocation ? MMFHE_E_OOM : MMFHE_E_CUDA,    \
+                                 std::string(#expr) + ": " + cudaGetErrorString(e_));             \
+    } while (0)
+
+// ---------------------------------------------------------------- host modular math
+// (own implementation; the oracle's is separate and never linked)
+namespace host {
+typedef unsigned __int128 u128;
+inline uint64_t mul(uint64_t a, uint64_t b, uint64_t q) { return (uint64_t)((u128)a * b % q); }
+inline uint64_t add(uint64_t a, uint64_t b, uint64_t q) { uint64_t s = a + b; return s >= q ? s - q : s; }
+inline uint64_t sub(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
+inline uint64_t pow(uint64_t b, uint64_t e, uint64_t q)
+{
+    uint64_t r = 1 % q;
+    b %= q;
+    while (e) {
+        if (e & 1) r = mul(r, b, q);
+        b = mul(b, b, q);
+        e >>= 1;
+    }
+    return r;
+}
+inline uint64_t inv(uint64_t a, uint64_t q) { return pow(a % q, q - 2, q); }
+inline uint64_t shoup(uint64_t w, uint64_t q) { return (uint64_t)(((u128)w << 64) / q); }
+// -q^{-1} mod 2^64 by Newton iteration
+inline uint64_t qinv_neg(uint64_t q)
+{
+    uint64_t x = q;  // correct to 3 bits for odd q
+    for (int i = 0; i < 6; ++i) x *= 2 - q * x;
+    return (uint64_t)0 - x;
+}
+inline uint64_t to_mont(uint64_t a, uint64_t q) { return (uint64_t)((((u128)(a % q)) << 64) % q); }
+bool is_prime(uint64_t n);
+}  // namespace host
+
+// ---------------------------------------------------------------- device-side tables
+struct TwPair {
+    uint64_t w, wp;  // value and Shoup companion floor(w 2^64 / q)
+};
+
+struct KTables {
+    const uint64_t *q;         // [np]
+    const uint64_t *qinv_neg;  // [np]
+    const uint64_t *r2;        // [np] 2^128 mod q
+    const TwPair *tw_fwd;      // [np][N]  psi^{bitrev(k)}
+    const TwPair *tw_inv;      // [np][N]  psi^{-bitrev(k)}
+    const TwPair *n_inv;       // [np]
+    uint32_t log_n;
+    uint32_t n;
+};
+
+// row r of a batch uses prime idx[r % period] (indices into q_0..q_L, p_0..p_{K-1})
+constexpr int kMapCap = 256;
+struct PrimeMap {
+    uint8_t idx[kMapCap];
+    uint32_t period;
+};
+
+inline PrimeMap make_map(const std::vector<uint32_t> &v)
+{
+    PrimeMap m;
+    MMFHE_REQUIRE(!v.empty() && v.size() <= (size_t)kMapCap, MMFHE_E_LAYOUT, "prime map size");
+    m.period = (uint32_t)v.size();
+    for (size_t i = 0; i < (size_t)kMapCap; ++i) m.idx[i] = i < v.size() ? (uint8_t)v[i] : 0;
+    return m;
+}
+
+}  // namespace mmfhe

@@ -1,0 +1,142 @@
+// context.h -- the mmfhe_ctx: parameters, device tables, key and plaintext
+// stores, stream, device memory pool, op trace.
+#pragma once
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+namespace mmfhe {
+
+// Stream-ordered device buffer from the ctx's memory pool (cudaMallocAsync).
+class DBuf {
+  public:
+    DBuf() = default;
+    DBuf(size_t words, cudaStream_t s);
+    ~DBuf();
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept { swap(o); }
+    DBuf &operator=(DBuf &&o) noexcept
+    {
+        if (this != &o) {
+            release();
+            swap(o);
+        }
+        return *this;
+    }
+    uint64_t *get() const { return p_; }
+    size_t words() const { return n_; }
+    void release();
+
+  private:
+    void swap(DBuf &o)
+    {
+        std::swap(p_, o.p_);
+        std::swap(n_, o.n_);
+        std::swap(s_, o.s_);
+    }
+    uint64_t *p_ = nullptr;
+    size_t n_ = 0;
+    cudaStream_t s_ = nullptr;
+};
+
+// Ciphertext (npolys = 2, or 3 after a tensor) in the library's NTT form.
+struct DCt {
+    DBuf buf;
+    uint64_t *ext = nullptr;  // non-owning view (caller buffer) when set
+    uint32_t level = 0;
+    uint32_t npolys = 2;
+    uint32_t n_slots = 0;
+    double scale = 1.0;
+    uint64_t *data() const { return ext ? ext : buf.get(); }
+    uint64_t *poly(uint32_t i, uint32_t n) const { return data() + (size_t)i * (level + 1) * n; }
+    size_t limbs() const { return level + 1; }
+};
+
+struct DKey {
+    DBuf buf;  // [dnum_L][2][L+1+K][N], NTT form, Montgomery form
+};
+
+struct DPlain {
+    DBuf buf;  // [level+1][N], NTT form, Montgomery form (x 2^64 mod q)
+    uint32_t level = 0;
+    double scale = 1.0;
+};
+
+// Base-conversion constants for one (level, digit) ModUp.
+struct ModUpPlan {
+    uint32_t lo, hi;           // source limbs [lo, hi)
+    uint32_t n_tgt;            // targets = (l+1+K) - (hi-lo)
+    size_t off_hat_inv;        // TwPair [hi-lo]       [Qhat_i^{-1}]_{q_i}
+    size_t off_hat;            // uint64 [hi-lo][n_tgt] [Qhat_i]_t * 2^64 mod t
+    size_t off_tgt;            // uint32 [n_tgt] target row index in the l+1+K basis
+};
+
+class Ctx {
+  public:
+    Ctx(const mmfhe_params &p, int device, cudaStream_t stream);
+    ~Ctx();
+
+    // parameters
+    uint32_t log_n, n, L, K, alpha, scale_bits;
+    std::vector<uint64_t> primes;  // q_0..q_L, p_0..p_{K-1}
+    int device;
+    cudaStream_t stream;
+    uint64_t launches = 0;
+    std::string last_error;
+
+    // device tables
+    KTables kt{};
+    DBuf tab_q, tab_qinv, tab_r2, tab_tw_fwd, tab_tw_inv, tab_ninv;
+    // base conversion / rescale constant blob (device) and host plans
+    DBuf tab_bconv;
+    std::vector<std::vector<ModUpPlan>> modup;  // [level][digit]
+    size_t off_pd_hat_inv = 0;   // TwPair[K]            [Phat_k^{-1}]_{p_k}
+    size_t off_pd_hat = 0;       // uint64[K][L+1]       [Phat_k]_{q_i} * 2^64 mod q_i
+    size_t off_pd_pinv = 0;      // TwPair[L+1]          [P^{-1}]_{q_i}
+    size_t off_rs = 0;           // TwPair[L+1][L+1]     [q_l^{-1}]_{q_i} (row l)
+    size_t off_rs_h = 0;         // uint64[L+1][L+1]     floor(q_l/2) mod q_i (row l)
+    size_t off_recip = 0;        // uint64[np]           floor(2^64 / prime)
+
+    // stores
+    std::unique_ptr<DKey> rlk;
+    std::map<int32_t, std::unique_ptr<DKey>> gk;
+    std::map<std::string, std::unique_ptr<DPlain>> plains;  // key "name@level"
+    std::map<std::string, std::vector<double>> scalars;
+    std::map<std::string, DBuf> const_cache;  // encoded scalar tables by "name@level"
+    // mmfhe_prepare_chain: encode absent public operands from the paper's formulas on first use
+    bool auto_encode = false;
+    std::vector<std::vector<double>> fc_w, fc_b;  // FC layer weights (row-major) and biases
+
+    // trace (Theorem P:999-1006)
+    bool trace_on = true;
+    std::vector<std::string> trace;
+    void rec(const char *op, uint32_t level, const std::string &arg = "");
+
+    // helpers
+    uint32_t dnum(uint32_t level) const { return (level + alpha) / alpha; }
+    size_t key_words() const { return (size_t)dnum(L) * 2 * (L + 1 + K) * n; }
+    uint64_t prime(uint32_t idx) const { return primes[idx]; }
+    // basis rows of the extended modulus Q_l u P
+    std::vector<uint32_t> ext_basis(uint32_t level) const;
+    std::vector<uint32_t> q_basis(uint32_t level) const;
+    const void *bconv_ptr(size_t off) const { return (const char *)tab_bconv.get() + off; }
+    DPlain *find_plain(const std::string &name, uint32_t level) const;
+    void sync();
+
+  private:
+    void build_tables();
+};
+
+std::string plain_key(const std::string &name, uint32_t level);
+
+// ------------------------------------------------------------------ kernels (launchers)
+void ntt_forward(const KTables &kt, uint64_t *d, uint32_t rows, const PrimeMap &pm, cudaStream_t s,
+                 uint64_t &launches);
+void ntt_inverse(const KTables &kt, uint64_t *d, uint32_t rows, const PrimeMap &pm, cudaStream_t s,
+                 uint64_t &launches);
+
+}  // namespace mmfhe

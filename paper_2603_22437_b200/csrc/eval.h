@@ -1,0 +1,60 @@
+// eval.h -- the CKKS evaluator over device ciphertexts (NTT form).
+//
+// Semantics follow the pinned operations of SURVEY §8(c)-4..6 (exact ring ops,
+// round-half-up rescale, hybrid key switching without BConv correction,
+// automorphism-first HRot, lazy relinearisation, exact scale bookkeeping);
+// each call records one logical op in the ctx trace.
+#pragma once
+#include <utility>
+#include <vector>
+
+#include "ops.h"
+
+namespace mmfhe {
+
+DCt make_ct(Ctx &c, uint32_t level, uint32_t npolys, uint32_t n_slots, double scale);
+DCt view_ct(const mmfhe_ct &ct, uint32_t npolys);  // non-owning device NTT-form view
+
+// ABI boundary: coefficient/NTT form, host/device.
+DCt import_ct(Ctx &c, const mmfhe_ct &in, uint32_t npolys);
+void export_ct(Ctx &c, const DCt &in, mmfhe_ct &out);
+
+// exact ops
+DCt ev_addsub(Ctx &c, const DCt &a, const DCt &b, bool sub);
+DCt ev_drop_to(Ctx &c, const DCt &a, uint32_t level);
+DCt ev_tensor_sum(Ctx &c, const std::vector<std::pair<const DCt *, const DCt *>> &pairs);
+DCt ev_pmult_sum(Ctx &c, const std::vector<std::pair<const DPlain *, const DCt *>> &terms);
+DCt ev_lincomb(Ctx &c, const std::vector<const DCt *> &cts, const std::vector<double> &coefs);
+DCt ev_add_plain(Ctx &c, const DCt &a, const DPlain &pt);
+DCt ev_sum(Ctx &c, const std::vector<const DCt *> &cts);
+
+// key switching family
+void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, uint32_t level, const DKey &key, uint64_t *out0, uint64_t *out1,
+                  const uint64_t *add0, const uint64_t *add1);
+DCt ev_relin(Ctx &c, const DCt &a3);
+DCt ev_rotate(Ctx &c, const DCt &a, int32_t step);
+DCt ev_rescale(Ctx &c, const DCt &a);
+DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride);
+
+// composites
+inline DCt ev_relin_rescale(Ctx &c, const DCt &a3) { return ev_rescale(c, ev_relin(c, a3)); }
+inline DCt ev_square_rescale(Ctx &c, const DCt &a)
+{
+    return ev_relin_rescale(c, ev_tensor_sum(c, {{&a, &a}}));
+}
+
+uint64_t galois_element(const Ctx &c, int32_t step, int32_t *normalised);
+const DKey &find_gk(const Ctx &c, int32_t step_norm);
+const DPlain &need_plain(const Ctx &c, const std::string &name, uint32_t level);
+
+// key / plaintext stores
+void load_key(Ctx &c, DKey &k, const uint64_t *words, size_t n_words, bool on_device);
+void load_plain(Ctx &c, const std::string &name, uint32_t level, double scale, const uint64_t *coef,
+                bool on_device);
+// host encoder (canonical embedding), csrc/encoder.cpp
+std::vector<int64_t> encode_real(const Ctx &c, const std::vector<double> &v, double scale);
+void encode_plain(Ctx &c, const std::string &name, const std::vector<double> &v, uint32_t level, double scale);
+// exact round-half-away(v * q) as a signed 128-bit integer reduced mod m
+uint64_t encode_scalar_mod(double v, uint64_t q_scale, uint64_t m);
+
+}  // namespace mmfhe

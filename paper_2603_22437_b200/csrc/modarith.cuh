@@ -1,0 +1,77 @@
+// modarith.cuh -- 64-bit modular arithmetic on the integer pipes of sm_100a.
+//
+// SURVEY §8(a) a2 ("64-bit modular multiply-add"): all primes q < 2^60, so
+// lazy values in [0, 4q) fit in 62 bits.  Three products:
+//   * Shoup (fixed operand w with w' = floor(w 2^64 / q)): twiddles, base
+//     conversion constants, scalar plaintext constants;
+//   * Montgomery (R = 2^64, q' = -q^{-1} mod 2^64): variable x variable products
+//     (ciphertext x evaluation key, ciphertext x plaintext), operands held in
+//     Montgomery form where one side is stored;
+//   * 128-bit lazy multiply-accumulate + one Montgomery reduction (base
+//     conversion, key inner product, tensor sums).
+// No tensor cores: the path is exact 64-bit modular integer work.
+#pragma once
+#include <cstdint>
+
+namespace mmfhe {
+
+struct U128 {
+    uint64_t lo, hi;
+};
+
+__device__ __forceinline__ uint64_t mulhi64(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+
+// a + b*c into a 128-bit accumulator (mad.lo.cc / madc.hi).
+__device__ __forceinline__ void mac128(U128 &acc, uint64_t b, uint64_t c)
+{
+    asm("mad.lo.cc.u64 %0, %2, %3, %0;\n\t"
+        "madc.hi.u64 %1, %2, %3, %1;"
+        : "+l"(acc.lo), "+l"(acc.hi)
+        : "l"(b), "l"(c));
+}
+
+__device__ __forceinline__ U128 mul128(uint64_t a, uint64_t b)
+{
+    U128 r;
+    r.lo = a * b;
+    r.hi = __umul64hi(a, b);
+    return r;
+}
+
+__device__ __forceinline__ uint64_t csub(uint64_t a, uint64_t q) { return a >= q ? a - q : a; }
+
+__device__ __forceinline__ uint64_t add_mod(uint64_t a, uint64_t b, uint64_t q) { return csub(a + b, q); }
+__device__ __forceinline__ uint64_t sub_mod(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
+
+// Shoup product, result in [0, 2q) for any a < 2^64 (w < q).
+__device__ __forceinline__ uint64_t shoup_lazy(uint64_t a, uint64_t w, uint64_t wp, uint64_t q)
+{
+    return a * w - __umul64hi(a, wp) * q;
+}
+__device__ __forceinline__ uint64_t shoup(uint64_t a, uint64_t w, uint64_t wp, uint64_t q)
+{
+    return csub(shoup_lazy(a, w, wp, q), q);
+}
+
+// Montgomery reduction of x = hi*2^64 + lo < q*2^64: returns x*2^-64 mod q in [0, 2q).
+__device__ __forceinline__ uint64_t redc_lazy(U128 x, uint64_t q, uint64_t qinv_neg)
+{
+    uint64_t m = x.lo * qinv_neg;
+    return x.hi + __umul64hi(m, q) + (x.lo != 0);
+}
+__device__ __forceinline__ uint64_t redc(U128 x, uint64_t q, uint64_t qinv_neg) { return csub(redc_lazy(x, q, qinv_neg), q); }
+
+// a*b*2^-64 mod q (canonical), a,b < q (or a*b < q*2^64).
+__device__ __forceinline__ uint64_t mont_mul(uint64_t a, uint64_t b, uint64_t q, uint64_t qinv_neg)
+{
+    return redc(mul128(a, b), q, qinv_neg);
+}
+
+// Per-prime constants kept in registers by the kernels.
+struct Mod {
+    uint64_t q;
+    uint64_t qinv_neg;  // -q^{-1} mod 2^64
+    uint64_t r2;        // 2^128 mod q  (mont_mul(x, r2) = x*2^64 mod q)
+};
+
+} // namespace mmfhe

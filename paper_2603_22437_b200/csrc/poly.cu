@@ -1,0 +1,504 @@
+// poly.cu -- RNS polynomial kernels of the CKKS evaluator (SURVEY §8(a)
+// a4-a10, §2.7 CK4-CK9): elementwise add/sub, Montgomery conversion, the
+// NTT-domain automorphism, ModUp / ModDown fast base conversion, the key inner
+// product, rescale pre/post steps, and fused multi-operand sums (tensor sums,
+// plaintext inner products, scalar linear combinations).
+//
+// All outputs are canonical residues in [0, q).  Thread mapping: one thread per
+// coefficient index (consecutive threads = consecutive words, coalesced
+// 256-byte warp accesses), grid.y over limbs/rows; per-prime constants are
+// warp-uniform loads (L1 broadcast).
+#include <algorithm>
+
+#include "modarith.cuh"
+#include "ops.h"
+
+namespace mmfhe {
+
+namespace {
+
+constexpr int kTB = 256;
+
+__device__ __forceinline__ uint32_t bitrev(uint32_t x, uint32_t log_n) { return __brev(x) >> (32 - log_n); }
+
+inline dim3 grid2(uint32_t n, uint32_t rows) { return dim3((n + kTB - 1) / kTB, rows); }
+
+// ------------------------------------------------------------------ elementwise
+__global__ void k_addsub(uint64_t *__restrict__ out, const uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
+                         KTables kt, PrimeMap pm, int sub)
+{
+    const uint32_t r = blockIdx.y;
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint64_t q = kt.q[pm.idx[r % pm.period]];
+    const size_t i = (size_t)r * kt.n + k;
+    out[i] = sub ? sub_mod(a[i], b[i], q) : add_mod(a[i], b[i], q);
+}
+
+__global__ void k_to_mont(uint64_t *__restrict__ x, KTables kt, PrimeMap pm)
+{
+    const uint32_t r = blockIdx.y;
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t p = pm.idx[r % pm.period];
+    const size_t i = (size_t)r * kt.n + k;
+    x[i] = mont_mul(x[i], kt.r2[p], kt.q[p], kt.qinv_neg[p]);
+}
+
+// sigma_g in the bit-reversed evaluation domain: slot j holds a(psi^(2 br(j) + 1)),
+// and sigma_g(a)(psi^e) = a(psi^(e g)).
+__global__ void k_automorph(uint64_t *__restrict__ out, const uint64_t *__restrict__ in, uint32_t log_n, uint64_t g)
+{
+    const uint32_t n = 1u << log_n;
+    const uint32_t r = blockIdx.y;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint64_t two_n = 2ull * n;
+    const uint64_t e = ((2ull * bitrev(j, log_n) + 1) * g) & (two_n - 1);
+    const uint32_t src = bitrev((uint32_t)((e - 1) >> 1), log_n);
+    out[(size_t)r * n + j] = in[(size_t)r * n + src];
+}
+
+// ------------------------------------------------------------------ base conversion
+struct ModUpDigit {
+    const TwPair *hat_inv;
+    const uint64_t *hat;
+    const uint32_t *tgt;
+    uint64_t *y;
+    uint32_t lo, hi, n_tgt;
+};
+struct ModUpArgs {
+    ModUpDigit d[16];
+    uint32_t level, L;
+};
+
+__device__ __forceinline__ uint32_t ext_prime(uint32_t r, uint32_t level, uint32_t L)
+{
+    return r <= level ? r : L + 1 + (r - level - 1);
+}
+
+// y_{j,t} = sum_{i in I_j} [x_i [Qhat_i^{-1}]_{q_i}]_{q_i} [Qhat_i]_t mod t
+__global__ void __launch_bounds__(kTB) k_modup(const uint64_t *__restrict__ x, KTables kt, ModUpArgs args)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const ModUpDigit &dg = args.d[blockIdx.y];
+    const uint32_t na = dg.hi - dg.lo;
+    uint64_t v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        if (i < (int)na) {
+            const uint32_t pi = dg.lo + i;
+            const uint64_t q = kt.q[pi];
+            const TwPair h = dg.hat_inv[i];
+            v[i] = shoup(x[(size_t)pi * kt.n + k], h.w, h.wp, q);
+        }
+    }
+    for (uint32_t ti = 0; ti < dg.n_tgt; ++ti) {
+        const uint32_t pt = ext_prime(dg.tgt[ti], args.level, args.L);
+        const uint64_t t = kt.q[pt];
+        U128 acc{0, 0};
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (i < (int)na) mac128(acc, v[i], dg.hat[(size_t)i * dg.n_tgt + ti]);
+        dg.y[(size_t)ti * kt.n + k] = redc(acc, t, kt.qinv_neg[pt]);
+    }
+}
+
+struct IPArgs {
+    const uint64_t *y[16];
+    uint32_t lo[16], hi[16];
+    uint32_t dnum, level, L, K;
+};
+
+// (accQ|accP)_p[r] = sum_j src_j[r] (.) evk_j[p][r]; src_j[r] = x[r] for r in I_j, else ModUp'd row.
+__global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
+                                                const uint64_t *__restrict__ x, const uint64_t *__restrict__ key,
+                                                KTables kt, IPArgs a)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t r = blockIdx.y;
+    const uint32_t pr = ext_prime(r, a.level, a.L);
+    const uint64_t q = kt.q[pr], qi = kt.qinv_neg[pr];
+    const size_t key_rows = a.L + 1 + a.K;
+    U128 acc0{0, 0}, acc1{0, 0};
+    for (uint32_t j = 0; j < a.dnum; ++j) {
+        uint64_t s;
+        if (r >= a.lo[j] && r < a.hi[j]) {
+            s = x[(size_t)r * kt.n + k];
+        } else {
+            const uint32_t row = r < a.lo[j] ? r : r - (a.hi[j] - a.lo[j]);
+            s = a.y[j][(size_t)row * kt.n + k];
+        }
+        const uint64_t *kb = key + ((size_t)(2 * j) * key_rows + pr) * kt.n;
+        const uint64_t *ka = key + ((size_t)(2 * j + 1) * key_rows + pr) * kt.n;
+        mac128(acc0, s, __ldg(kb + k));
+        mac128(acc1, s, __ldg(ka + k));
+    }
+    const uint64_t r0 = redc(acc0, q, qi), r1 = redc(acc1, q, qi);
+    if (r <= a.level) {
+        const size_t stride = (size_t)(a.level + 1) * kt.n;
+        accQ[(size_t)r * kt.n + k] = r0;
+        accQ[stride + (size_t)r * kt.n + k] = r1;
+    } else {
+        const uint32_t rr = r - a.level - 1;
+        const size_t stride = (size_t)a.K * kt.n;
+        accP[(size_t)rr * kt.n + k] = r0;
+        accP[stride + (size_t)rr * kt.n + k] = r1;
+    }
+}
+
+struct MDArgs {
+    const TwPair *phat_inv;  // [K]
+    const uint64_t *phat;    // [K][L+1] Montgomery
+    const TwPair *pinv;      // [L+1]
+    uint32_t level, L, K;
+};
+
+// w_i = sum_k [z_k [Phat_k^{-1}]_{p_k}]_{p_k} [Phat_k]_{q_i} mod q_i
+__global__ void __launch_bounds__(kTB) k_moddown_bconv(uint64_t *__restrict__ w, const uint64_t *__restrict__ zP,
+                                                       KTables kt, MDArgs a)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t poly = blockIdx.y;
+    uint64_t v[16];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+        if (kk < (int)a.K) {
+            const uint32_t pi = a.L + 1 + kk;
+            const TwPair h = a.phat_inv[kk];
+            v[kk] = shoup(zP[((size_t)poly * a.K + kk) * kt.n + k], h.w, h.wp, kt.q[pi]);
+        }
+    }
+    for (uint32_t i = 0; i <= a.level; ++i) {
+        U128 acc{0, 0};
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk)
+            if (kk < (int)a.K) mac128(acc, v[kk], a.phat[(size_t)kk * (a.L + 1) + i]);
+        w[((size_t)poly * (a.level + 1) + i) * kt.n + k] = redc(acc, kt.q[i], kt.qinv_neg[i]);
+    }
+}
+
+__global__ void k_moddown_final(uint64_t *__restrict__ out0, uint64_t *__restrict__ out1,
+                                const uint64_t *__restrict__ accQ, const uint64_t *__restrict__ w,
+                                const uint64_t *__restrict__ add0, const uint64_t *__restrict__ add1, KTables kt,
+                                MDArgs a)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t r = blockIdx.y;  // 0 .. 2(l+1)-1
+    const uint32_t poly = r / (a.level + 1), i = r - poly * (a.level + 1);
+    const uint64_t q = kt.q[i];
+    const TwPair pv = a.pinv[i];
+    const size_t idx = (size_t)r * kt.n + k;
+    uint64_t d = shoup(accQ[idx] + q - w[idx], pv.w, pv.wp, q);
+    const uint64_t *add = poly ? add1 : add0;
+    const size_t li = (size_t)i * kt.n + k;
+    if (add) d = add_mod(d, add[li], q);
+    (poly ? out1 : out0)[li] = d;
+}
+
+// ------------------------------------------------------------------ rescale
+struct RSArgs {
+    const TwPair *qlinv;  // row l of [L+1][L+1]
+    const uint64_t *h;    // row l: floor(q_l/2) mod q_i
+    const uint64_t *recip;  // floor(2^64 / q_i)
+    uint32_t level;
+};
+
+// v_i = ([t]_{q_i} - [h]_{q_i}) mod q_i, t = [a_l + h]_{q_l} in coefficient form
+__global__ void k_rescale_prep(uint64_t *__restrict__ v, const uint64_t *__restrict__ t, KTables kt, RSArgs a)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t r = blockIdx.y;  // 0 .. 2l-1
+    const uint32_t poly = r / a.level, i = r - poly * a.level;
+    const uint64_t ql = kt.q[a.level];
+    const uint64_t hl = ql >> 1;
+    const uint64_t tl = add_mod(t[(size_t)poly * kt.n + k], hl, ql);
+    const uint64_t q = kt.q[i];
+    const uint64_t tm = shoup(tl, 1, a.recip[i], q);
+    v[(size_t)r * kt.n + k] = sub_mod(tm, a.h[i], q);
+}
+
+__global__ void k_rescale_final(uint64_t *__restrict__ out, const uint64_t *__restrict__ in,
+                                const uint64_t *__restrict__ v, KTables kt, RSArgs a)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t r = blockIdx.y;
+    const uint32_t poly = r / a.level, i = r - poly * a.level;
+    const uint64_t q = kt.q[i];
+    const TwPair w = a.qlinv[i];
+    const uint64_t x = in[((size_t)poly * (a.level + 1) + i) * kt.n + k];
+    out[(size_t)r * kt.n + k] = shoup(x + q - v[(size_t)r * kt.n + k], w.w, w.wp, q);
+}
+
+// ------------------------------------------------------------------ fused sums
+// d0 = sum a0 b0, d1 = sum a0 b1 + a1 b0, d2 = sum a1 b1 over n pairs (<= kMaxTerms).
+__global__ void __launch_bounds__(kTB) k_tensor_sum(uint64_t *__restrict__ out, PtrList A, PtrList B, int n,
+                                                    KTables kt, uint32_t level, int accumulate)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t r = blockIdx.y;
+    const uint64_t q = kt.q[r], qi = kt.qinv_neg[r];
+    const size_t ps = (size_t)(level + 1) * kt.n;
+    const size_t off = (size_t)r * kt.n + k;
+    uint64_t s0 = 0, s1 = 0, s2 = 0;
+    int p = 0;
+    while (p < n) {
+        U128 a0c{0, 0}, a1c{0, 0}, a2c{0, 0};
+        const int end = min(n, p + 7);  // <= 14 products < q*2^60 each in acc1
+        for (; p < end; ++p) {
+            const uint64_t *pa = A.p[p], *pb = B.p[p];
+            const uint64_t a0 = pa[off], a1 = pa[ps + off];
+            if (pa == pb) {
+                mac128(a0c, a0, a0);
+                const U128 m = mul128(a0, a1);
+                mac128(a1c, a0, a1);
+                a1c.lo += m.lo;
+                a1c.hi += m.hi + (a1c.lo < m.lo);
+                mac128(a2c, a1, a1);
+            } else {
+                const uint64_t b0 = pb[off], b1 = pb[ps + off];
+                mac128(a0c, a0, b0);
+                mac128(a1c, a0, b1);
+                mac128(a1c, a1, b0);
+                mac128(a2c, a1, b1);
+            }
+        }
+        s0 = add_mod(s0, redc(a0c, q, qi), q);
+        s1 = add_mod(s1, redc(a1c, q, qi), q);
+        s2 = add_mod(s2, redc(a2c, q, qi), q);
+    }
+    const uint64_t r2 = kt.r2[r];
+    uint64_t d0 = mont_mul(s0, r2, q, qi), d1 = mont_mul(s1, r2, q, qi), d2 = mont_mul(s2, r2, q, qi);
+    if (accumulate) {
+        d0 = add_mod(d0, out[off], q);
+        d1 = add_mod(d1, out[ps + off], q);
+        d2 = add_mod(d2, out[2 * ps + off], q);
+    }
+    out[off] = d0;
+    out[ps + off] = d1;
+    out[2 * ps + off] = d2;
+}
+
+// out_p = sum_t ct_t[p] (.) pt_t, pt in Montgomery form (result canonical).
+__global__ void __launch_bounds__(kTB) k_pmult_sum(uint64_t *__restrict__ out, PtrList PT, PtrList CT, int n,
+                                                   KTables kt, uint32_t level, int accumulate)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t r = blockIdx.y;
+    const uint64_t q = kt.q[r], qi = kt.qinv_neg[r];
+    const size_t ps = (size_t)(level + 1) * kt.n;
+    const size_t off = (size_t)r * kt.n + k;
+    uint64_t s0 = 0, s1 = 0;
+    int t = 0;
+    while (t < n) {
+        U128 c0{0, 0}, c1{0, 0};
+        const int end = min(n, t + 15);
+        for (; t < end; ++t) {
+            const uint64_t w = PT.p[t][off];
+            const uint64_t *c = CT.p[t];
+            mac128(c0, c[off], w);
+            mac128(c1, c[ps + off], w);
+        }
+        s0 = add_mod(s0, redc(c0, q, qi), q);
+        s1 = add_mod(s1, redc(c1, q, qi), q);
+    }
+    if (accumulate) {
+        s0 = add_mod(s0, out[off], q);
+        s1 = add_mod(s1, out[ps + off], q);
+    }
+    out[off] = s0;
+    out[ps + off] = s1;
+}
+
+// out_p = sum_t c_t ct_t[p] with per-limb Shoup constants consts[t*(l+1) + r].
+__global__ void __launch_bounds__(kTB) k_lincomb(uint64_t *__restrict__ out, PtrList CT, const TwPair *consts, int n,
+                                                 KTables kt, uint32_t level, int accumulate)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t r = blockIdx.y;
+    const uint64_t q = kt.q[r], q2 = 2 * q;
+    const size_t ps = (size_t)(level + 1) * kt.n;
+    const size_t off = (size_t)r * kt.n + k;
+    uint64_t s0 = 0, s1 = 0;
+    for (int t = 0; t < n; ++t) {
+        const TwPair c = consts[(size_t)t * (level + 1) + r];
+        const uint64_t *ct = CT.p[t];
+        s0 += shoup_lazy(ct[off], c.w, c.wp, q);
+        s1 += shoup_lazy(ct[ps + off], c.w, c.wp, q);
+        s0 = s0 >= q2 ? s0 - q2 : s0;
+        s1 = s1 >= q2 ? s1 - q2 : s1;
+    }
+    s0 = csub(s0, q);
+    s1 = csub(s1, q);
+    if (accumulate) {
+        s0 = add_mod(s0, out[off], q);
+        s1 = add_mod(s1, out[ps + off], q);
+    }
+    out[off] = s0;
+    out[ps + off] = s1;
+}
+
+__global__ void k_add_plain(uint64_t *__restrict__ c0, const uint64_t *__restrict__ pt, KTables kt)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t r = blockIdx.y;
+    const uint64_t q = kt.q[r];
+    const size_t off = (size_t)r * kt.n + k;
+    const uint64_t v = redc(U128{pt[off], 0}, q, kt.qinv_neg[r]);
+    c0[off] = add_mod(c0[off], v, q);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+#define LAUNCH_CHECK(c)                                                                           \
+    do {                                                                                          \
+        ++(c).launches;                                                                           \
+        CUDA_CHECK(cudaGetLastError());                                                           \
+    } while (0)
+
+void launch_addsub(Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, uint32_t rows, const PrimeMap &pm,
+                   bool sub)
+{
+    k_addsub<<<grid2(c.n, rows), kTB, 0, c.stream>>>(out, a, b, c.kt, pm, sub ? 1 : 0);
+    LAUNCH_CHECK(c);
+}
+
+void launch_to_mont(Ctx &c, uint64_t *x, uint32_t rows, const PrimeMap &pm)
+{
+    k_to_mont<<<grid2(c.n, rows), kTB, 0, c.stream>>>(x, c.kt, pm);
+    LAUNCH_CHECK(c);
+}
+
+void launch_automorph(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t rows, uint64_t g)
+{
+    k_automorph<<<grid2(c.n, rows), kTB, 0, c.stream>>>(out, in, c.log_n, g);
+    LAUNCH_CHECK(c);
+}
+
+void launch_modup_bconv(Ctx &c, uint64_t *y, const uint64_t *x_coef, uint32_t level, const std::vector<size_t> &off)
+{
+    const auto &plans = c.modup[level];
+    MMFHE_REQUIRE(plans.size() <= 16 && c.alpha <= 16, MMFHE_E_PARAMS, "dnum/alpha too large");
+    ModUpArgs a{};
+    a.level = level;
+    a.L = c.L;
+    for (size_t j = 0; j < plans.size(); ++j) {
+        const ModUpPlan &p = plans[j];
+        a.d[j].hat_inv = (const TwPair *)c.bconv_ptr(p.off_hat_inv);
+        a.d[j].hat = (const uint64_t *)c.bconv_ptr(p.off_hat);
+        a.d[j].tgt = (const uint32_t *)c.bconv_ptr(p.off_tgt);
+        a.d[j].y = y + off[j] * c.n;
+        a.d[j].lo = p.lo;
+        a.d[j].hi = p.hi;
+        a.d[j].n_tgt = p.n_tgt;
+    }
+    k_modup<<<grid2(c.n, (uint32_t)plans.size()), kTB, 0, c.stream>>>(x_coef, c.kt, a);
+    LAUNCH_CHECK(c);
+}
+
+void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, const uint64_t *y,
+                   const std::vector<size_t> &off, const uint64_t *key, uint32_t level)
+{
+    const auto &plans = c.modup[level];
+    IPArgs a{};
+    a.dnum = (uint32_t)plans.size();
+    a.level = level;
+    a.L = c.L;
+    a.K = c.K;
+    for (size_t j = 0; j < plans.size(); ++j) {
+        a.y[j] = y + off[j] * c.n;
+        a.lo[j] = plans[j].lo;
+        a.hi[j] = plans[j].hi;
+    }
+    k_key_ip<<<grid2(c.n, level + 1 + c.K), kTB, 0, c.stream>>>(accQ, accP, x_ntt, key, c.kt, a);
+    LAUNCH_CHECK(c);
+}
+
+static MDArgs md_args(Ctx &c, uint32_t level)
+{
+    MDArgs a;
+    a.phat_inv = (const TwPair *)c.bconv_ptr(c.off_pd_hat_inv);
+    a.phat = (const uint64_t *)c.bconv_ptr(c.off_pd_hat);
+    a.pinv = (const TwPair *)c.bconv_ptr(c.off_pd_pinv);
+    a.level = level;
+    a.L = c.L;
+    a.K = c.K;
+    return a;
+}
+
+void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level)
+{
+    MMFHE_REQUIRE(c.K <= 16, MMFHE_E_PARAMS, "K too large");
+    k_moddown_bconv<<<grid2(c.n, 2), kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
+    LAUNCH_CHECK(c);
+}
+
+void launch_moddown_final(Ctx &c, uint64_t *out0, uint64_t *out1, const uint64_t *accQ, const uint64_t *w,
+                          const uint64_t *add0, const uint64_t *add1, uint32_t level)
+{
+    k_moddown_final<<<grid2(c.n, 2 * (level + 1)), kTB, 0, c.stream>>>(out0, out1, accQ, w, add0, add1, c.kt,
+                                                                       md_args(c, level));
+    LAUNCH_CHECK(c);
+}
+
+static RSArgs rs_args(Ctx &c, uint32_t level)
+{
+    RSArgs a;
+    a.qlinv = (const TwPair *)c.bconv_ptr(c.off_rs) + (size_t)level * (c.L + 1);
+    a.h = (const uint64_t *)c.bconv_ptr(c.off_rs_h) + (size_t)level * (c.L + 1);
+    a.recip = (const uint64_t *)c.bconv_ptr(c.off_recip);
+    a.level = level;
+    return a;
+}
+
+void launch_rescale_prep(Ctx &c, uint64_t *v, const uint64_t *t, uint32_t level)
+{
+    k_rescale_prep<<<grid2(c.n, 2 * level), kTB, 0, c.stream>>>(v, t, c.kt, rs_args(c, level));
+    LAUNCH_CHECK(c);
+}
+
+void launch_rescale_final(Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *v, uint32_t level)
+{
+    k_rescale_final<<<grid2(c.n, 2 * level), kTB, 0, c.stream>>>(out, a, v, c.kt, rs_args(c, level));
+    LAUNCH_CHECK(c);
+}
+
+void launch_tensor_sum(Ctx &c, uint64_t *out, const PtrList &a, const PtrList &b, int n, uint32_t level,
+                       bool accumulate)
+{
+    k_tensor_sum<<<grid2(c.n, level + 1), kTB, 0, c.stream>>>(out, a, b, n, c.kt, level, accumulate ? 1 : 0);
+    LAUNCH_CHECK(c);
+}
+
+void launch_pmult_sum(Ctx &c, uint64_t *out, const PtrList &pt, const PtrList &ct, int n, uint32_t level,
+                      bool accumulate)
+{
+    k_pmult_sum<<<grid2(c.n, level + 1), kTB, 0, c.stream>>>(out, pt, ct, n, c.kt, level, accumulate ? 1 : 0);
+    LAUNCH_CHECK(c);
+}
+
+void launch_lincomb(Ctx &c, uint64_t *out, const PtrList &ct, const TwPair *consts, int n, uint32_t level,
+                    bool accumulate)
+{
+    k_lincomb<<<grid2(c.n, level + 1), kTB, 0, c.stream>>>(out, ct, consts, n, c.kt, level, accumulate ? 1 : 0);
+    LAUNCH_CHECK(c);
+}
+
+void launch_add_plain(Ctx &c, uint64_t *c0, const uint64_t *pt_mont, uint32_t level)
+{
+    k_add_plain<<<grid2(c.n, level + 1), kTB, 0, c.stream>>>(c0, pt_mont, c.kt);
+    LAUNCH_CHECK(c);
+}
+
+}  // namespace mmfhe

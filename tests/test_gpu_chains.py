@@ -1,0 +1,175 @@
+"""GPU chain parity: each mmFHE chain through mmfhe_eval_chain must reproduce
+the oracle circuit's output residues bit for bit with an identical op trace
+(north_star gate 1; Theorem P:999-1006), on seeded radar-shaped inputs
+encrypted by the oracle client.  Full-size configs: C1 (k1_energy, PS1) and
+C3 (k3_doppler_dft, PS3)."""
+import numpy as np
+import pytest
+
+from oracle import ckks as orc
+from oracle import circuits as cc
+from oracle import dsp
+from synth import radar
+from synth.params import ps1, ps3, toy
+
+from gpu_util import ct_in, ct_out, make_ctx, residues
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def m(cuda_ctx_ok):
+    from paper_2603_22437_b200 import build, mmfhe
+    build.build()
+    return mmfhe
+
+
+def _mcfg(m, cfg: cc.ChainCfg, bins=(), taps=()):
+    return m.chain_cfg(R=cfg.R, D=cfg.D, A=cfg.A, F=cfg.F, gamma=cfg.gamma, p_phi=cfg.p_phi,
+                       taylor_order=cfg.taylor_order, n_slots=cfg.n_slots, bsgs_baby=cfg.bsgs_baby,
+                       fc_dims=cfg.fc_dims, notch_width=cfg.notch_width, bands_bins=bins,
+                       n_taps=[len(t) for t in taps], fs=cfg.fs)
+
+
+def _run(m, P, keys, book, chain, cfg, cts, want, scalars=None, bins=(), taps=()):
+    ctx = make_ctx(m, P, keys, book, scalars)
+    mcfg = _mcfg(m, cfg, bins, taps)
+    levels = ctx.chain_plan(chain, mcfg, cts[0].level, len(cts))
+    assert levels == [w.level for w in want]
+    outs = [ct_out(m, P, lv) for lv in levels]
+    n = ctx.eval_chain(chain, mcfg, [ct_in(m, P, c) for c in cts], outs)
+    assert n == len(want)
+    for o, w in zip(outs, want):
+        assert np.array_equal(residues(o), np.stack(w.c)), "residues differ from the oracle"
+        assert o.scale == w.scale and o.level == w.level
+    return ctx
+
+
+def _vital_inputs(P, keys, cfg, lvl, seed):
+    z, _ = radar.vital_scene(cfg.R, cfg.F, cfg.fs, seed=seed)
+    zt = radar.preprocess_vital(z)
+    cts = []
+    for t in range(cfg.F):
+        for part in (zt[t].real, zt[t].imag):
+            cts.append(orc.encrypt_vector(P, keys, radar.pack_vital(part, cfg.n_slots), lvl, seed=seed + 1,
+                                          index=len(cts)))
+    return zt, cts
+
+
+def test_k1_energy_c1_full_size(m):
+    """C1: K1 only, N=2^13, 3 RNS limbs (2 Q + 1 P), R=64, F=32, depth 1."""
+    P = ps1()
+    cfg = cc.ChainCfg(R=64, F=32, n_slots=P.n // 2)
+    keys = orc.keygen(P, seed=3001)
+    zt, cts = _vital_inputs(P, keys, cfg, 1, 3002)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    E = cc.k1_energy(ev, cts[0::2], cts[1::2])
+    ctx = _run(m, P, keys, None, "k1_energy", cfg, cts, [E])
+    assert ctx.trace() == ev.trace
+    E_dec = orc.decrypt_vector(P, keys, E)[: cfg.R]
+    want = dsp.energy(zt)
+    assert np.max(np.abs(E_dec - want)) <= 1e-3 * np.max(np.abs(want))
+
+
+def test_vitals_v1_small(m):
+    P = toy(log_n=10, n_q=6, scale_bits=40, n_p=2, alpha=2)
+    cfg = cc.ChainCfg(R=16, F=6, gamma=2, n_slots=P.n // 2)
+    keys = orc.keygen(P, seed=3101, rotations=cc.required_rotations("vitals_v1", cfg, P.n))
+    _, cts = _vital_inputs(P, keys, cfg, 3, 3102)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    N, D = cc.vitals_v1(ev, book, cts[0::2], cts[1::2], cfg)
+    ctx = _run(m, P, keys, book, "vitals_v1", cfg, cts, [N, D])
+    assert ctx.trace() == ev.trace
+    assert sorted(ctx.required_rotations("vitals_v1", _mcfg(m, cfg))) == cc.required_rotations("vitals_v1", cfg, P.n)
+
+
+def _gesture(P, seed, F=2, A=2, R=4, D=8):
+    n = A * R * D
+    cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8))
+    Z, _ = radar.gesture_scene(A, R, D, F, seed=seed, cls=seed % 5)
+    return cfg, radar.preprocess_gesture(Z)
+
+
+def test_gesture_chain_small(m):
+    P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
+    cfg, Zt = _gesture(P, 3201)
+    keys = orc.keygen(P, seed=3202, rotations=cc.required_rotations("gesture", cfg, P.n))
+    cts = []
+    for t in range(cfg.F):
+        v = radar.pack_doppler(Zt[t])
+        for part in (v.real, v.imag):
+            cts.append(orc.encrypt_vector(P, keys, part, P.L, seed=3203, index=len(cts)))
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    feats = [cc.gesture_frame(ev, book, cts[2 * t], cts[2 * t + 1], cfg) for t in range(cfg.F)]
+    feat = cc.frame_accumulate(ev, feats)
+    dims = cfg.fc_dims
+    Ws, bs = radar.fc_weights([dims[0], dims[1], dims[2], 5], seed=3204)
+    logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
+    ctx = _run(m, P, keys, book, "gesture", cfg, cts, [logits])
+    assert ctx.trace() == ev.trace
+    assert sorted(ctx.required_rotations("gesture", _mcfg(m, cfg))) == cc.required_rotations("gesture", cfg, P.n)
+    # per-frame chain and FC chain on their own
+    ev2 = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    f0 = cc.gesture_frame(ev2, cc.PlainBook(P), cts[0], cts[1], cfg)
+    _run(m, P, keys, book, "gesture_frame", cfg, cts[:2], [f0])
+
+
+def test_k3_doppler_dft_c3_full_size(m):
+    """C3: block-diagonal Doppler DFT via slot rotations, N=2^15, A=4 x R=32 x D=32."""
+    P = ps3()
+    cfg = cc.ChainCfg(A=4, R=32, D=32, F=1, n_slots=4096)
+    keys = orc.keygen(P, seed=3301, rotations=cc.required_rotations("k3_doppler_dft", cfg, P.n))
+    Z, _ = radar.gesture_scene(4, 32, 32, 3, seed=3302, cls=2)
+    Zt = radar.preprocess_gesture(Z)
+    v = radar.pack_doppler(Zt[1])
+    cre = orc.encrypt_vector(P, keys, v.real, P.L, seed=3303, index=0)
+    cim = orc.encrypt_vector(P, keys, v.imag, P.L, seed=3303, index=1)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    dre, dim = cc.k3_doppler_dft(ev, book, cre, cim, cfg)
+    ctx = _run(m, P, keys, book, "k3_doppler_dft", cfg, [cre, cim], [dre, dim])
+    assert ctx.trace() == ev.trace
+    assert sum(1 for op in ev.trace if op[0] == "hrot") == 30
+    want = dsp.doppler_dft(v, cfg.D)
+    got = orc.decrypt_vector(P, keys, dre)
+    assert np.max(np.abs(got - want.real)) <= 1e-3 * np.max(np.abs(want.real))
+
+
+def test_vitals_v2_small(m):
+    P = toy(log_n=10, n_q=10, scale_bits=40, n_p=2, alpha=2)  # third order needs 9 levels
+    cfg = cc.ChainCfg(R=8, F=10, p_phi=2, taylor_order=3, n_slots=P.n // 2, fs=2.0,
+                      bands=((0.1, 0.6), (0.7, 1.0)))
+    keys = orc.keygen(P, seed=3401, rotations=cc.required_rotations("vitals_v2", cfg, P.n))
+    _, cts = _vital_inputs(P, keys, cfg, 9, 3402)
+    taps = [np.array([0.2, 0.3, 0.3, 0.2]), np.array([0.25, -0.5, 0.25])]
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    out = cc.vitals_v2(ev, cts[0::2], cts[1::2], taps, cfg)
+    want = out[0] + out[1]
+    scalars = {f"k5.b{b}": t for b, t in enumerate(taps)}
+    bins = []
+    for b in range(2):
+        ks = dsp.band_bins(cfg.F - 1, cfg.fs, cfg.bands[b])
+        bins.append([int(k) for k in ks])
+        for k in ks:
+            c, s = dsp.narrowband_dft_coefs(cfg.F - 1, int(k))
+            scalars[f"vp.c.{b}.{int(k)}"] = c
+            scalars[f"vp.s.{b}.{int(k)}"] = s
+    ctx = _run(m, P, keys, None, "vitals_v2", cfg, cts, want, scalars=scalars, bins=bins, taps=taps)
+    assert ctx.trace() == ev.trace
+
+
+def test_chain_shape_and_depth_errors(m):
+    P = toy(log_n=10, n_q=4, scale_bits=40, n_p=2, alpha=2)
+    ctx = make_ctx(m, P)
+    cfg = _mcfg(m, cc.ChainCfg(R=8, F=3, gamma=2, n_slots=P.n // 2))
+    with pytest.raises(m.MmfheError) as e:
+        ctx.chain_plan("vitals_v1", cfg, 3, 5)
+    assert e.value.name == "E_SHAPE"
+    with pytest.raises(m.MmfheError) as e:
+        ctx.chain_plan("vitals_v1", cfg, 2, 6)
+    assert e.value.name == "E_DEPTH"
+    with pytest.raises(m.MmfheError) as e:
+        ctx.chain_plan("no_such_chain", cfg, 3, 6)
+    assert e.value.name == "E_INVALID_ARG"
