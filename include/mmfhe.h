@@ -106,6 +106,8 @@ typedef struct {
     uint32_t n_slots;      /* packing period n */
     uint32_t bsgs_baby;    /* K3 baby steps b (0: ceil(sqrt(2D-1))) */
     uint32_t hoist;        /* 0: none (only mode in this version) */
+    uint32_t frame_batch;  /* frames evaluated together per batched launch (0: all);
+                              fixes the op order of the trace (op-major per batch) */
     uint32_t fc_dims[4];   /* n_in, h1, h2, h3 (padded logits) */
     uint32_t notch_width;  /* K6 zeroed bins around D/2 */
     uint32_t n_bands;      /* vital V2: number of FIR bands (<= 4) */
@@ -222,6 +224,13 @@ mmfhe_status mmfhe_hmult_batch(mmfhe_ctx *ctx, const mmfhe_ct *a, const mmfhe_ct
 mmfhe_status mmfhe_trace_get(mmfhe_ctx *ctx, char *buf, size_t cap, size_t *len);
 mmfhe_status mmfhe_trace_clear(mmfhe_ctx *ctx);
 mmfhe_status mmfhe_trace_enable(mmfhe_ctx *ctx, int on);
+
+/* ---- kernel profile (bench roofline) ---------------------------------------
+ * When on, CUDA events are recorded on the ctx stream around every kernel
+ * launch.  mmfhe_profile_get synchronises the stream and returns one line per
+ * kernel: "<kernel> <launches> <total_ms> <algorithmic_bytes>", then resets. */
+mmfhe_status mmfhe_profile_enable(mmfhe_ctx *ctx, int on);
+mmfhe_status mmfhe_profile_get(mmfhe_ctx *ctx, char *buf, size_t cap, size_t *len);
 
 #ifdef __cplusplus
 }

@@ -6,6 +6,12 @@ placement, rescale placement, BSGS split, overflow folds).  The CUDA library
 implements the same logical op sequence independently (csrc/chains.cpp);
 ``op trace`` equality plus bit-exact residues is the parity gate.
 
+Per-frame kernels take LISTS of frame ciphertexts and apply each op to every
+frame before the next op ("op-major" order, one list comprehension per op).
+This is only an evaluation order: each ciphertext goes through exactly the
+paper's op sequence; the order fixes the trace the GPU's batched launches
+reproduce.  Frames are processed in batches of ``cfg.frame_batch``.
+
 Kernels (PAPER.md):
   K1 Energy Integration              Eq. energy
   K2 Soft Power Attention            Eqs. soft_power_weight/soft_argmax_stats P:777-788
@@ -22,7 +28,7 @@ Table tab:depth P:914-949.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -45,6 +51,7 @@ class ChainCfg:
     notch_width: int = 1
     fs: float = 20.0
     bands: tuple = ((0.1, 0.6), (0.8, 2.5))   # RR, HR
+    frame_batch: int = 0        # frames per op-major batch (0: all frames)
 
 
 def rot(v: np.ndarray, k: int) -> np.ndarray:
@@ -54,6 +61,11 @@ def rot(v: np.ndarray, k: int) -> np.ndarray:
 
 def ceil_sqrt(x: int) -> int:
     return int(math.ceil(math.sqrt(x)))
+
+
+def chunks(n: int, size: int):
+    size = size or n
+    return [(s, min(n, s + size)) for s in range(0, n, size)]
 
 
 class PlainBook:
@@ -142,11 +154,24 @@ class CircuitEvaluator(orc.Evaluator):
         qs = self.qs(ct.level)
         return orc.Ct([orc.poly_add(qs, ct.c[0], res[: ct.level + 1]), ct.c[1]], ct.level, ct.scale, ct.n_slots)
 
-    def pmult_rescale(self, ct, pt) -> orc.Ct:
-        return self.rescale(self.pmult_sum([(pt, ct)]))
+    # ---- op-major helpers over frame lists
+    def relin_rescale_all(self, cts):
+        return [self.rescale(x) for x in [self.relin(x) for x in cts]]
 
-    def relin_rescale(self, ct) -> orc.Ct:
-        return self.rescale(self.relin(ct))
+    def square_rescale_all(self, cts):
+        return self.relin_rescale_all([self.tensor_sum([(x, x)]) for x in cts])
+
+    def rotsum_all(self, cts, count: int, stride: int):
+        """sum_{i<count} Rot(x, i*stride) for every x: log2(count) rotate-and-add
+        steps with strides stride*2^i."""
+        acc = list(cts)
+        step, c = stride, 1
+        while c < count:
+            r = [self.rotate(x, step) for x in acc]
+            acc = [self.add(x, y) for x, y in zip(acc, r)]
+            step *= 2
+            c *= 2
+        return acc
 
 
 # ------------------------------------------------------------------ K1 / K2
@@ -156,7 +181,7 @@ def k1_energy(ev: CircuitEvaluator, re_list, im_list) -> orc.Ct:
     pairs = []
     for re, im in zip(re_list, im_list):
         pairs += [(re, re), (im, im)]
-    return ev.relin_rescale(ev.tensor_sum(pairs))
+    return ev.relin_rescale_all([ev.tensor_sum(pairs)])[0]
 
 
 def k2_soft_attention(ev: CircuitEvaluator, book: PlainBook, E: orc.Ct, cfg: ChainCfg):
@@ -164,16 +189,16 @@ def k2_soft_attention(ev: CircuitEvaluator, book: PlainBook, E: orc.Ct, cfg: Cha
     D = rotsum_R(w (.) one'), ramp'_r = r/(F^2 R), one'_r = 1/(F^2 R)."""
     w = E
     for _ in range(int(math.log2(cfg.gamma))):
-        w = ev.relin_rescale(ev.tensor_sum([(w, w)]))
+        w = ev.square_rescale_all([w])[0]
     n = E.n_slots
     R, F = cfg.R, cfg.F
     ramp = np.zeros(n)
     one = np.zeros(n)
     ramp[:R] = np.arange(R) / (F * F * R)
     one[:R] = 1.0 / (F * F * R)
-    Nn = ev.pmult_rescale(w, book.vec("k2.ramp", ramp, w.level))
-    Dd = ev.pmult_rescale(w, book.vec("k2.one", one, w.level))
-    return ev.rotsum(Nn, R, 1), ev.rotsum(Dd, R, 1)
+    Nn = ev.rescale(ev.pmult_sum([(book.vec("k2.ramp", ramp, w.level), w)]))
+    Dd = ev.rescale(ev.pmult_sum([(book.vec("k2.one", one, w.level), w)]))
+    return ev.rotsum_all([Nn], R, 1)[0], ev.rotsum_all([Dd], R, 1)[0]
 
 
 def vitals_v1(ev, book, re_list, im_list, cfg):
@@ -209,16 +234,17 @@ def k3_schedule(cfg: ChainCfg):
     return b, giants
 
 
-def k3_doppler_dft(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg: ChainCfg):
-    """K3 (Eqs. dft_re/dft_im P:805-815): d_re = C~ v_re - S~ v_im, d_im = S~ v_re + C~ v_im
-    via BSGS with pre-rotated diagonals; one rescale after the giant sum (c-6)."""
-    n = v_re.n_slots
-    lvl = v_re.level
+def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg: ChainCfg):
+    """K3 (Eqs. dft_re/dft_im P:805-815) on a list of frames: d_re = C~ v_re - S~ v_im,
+    d_im = S~ v_re + C~ v_im via BSGS with pre-rotated diagonals; one rescale after
+    the giant sum (c-6)."""
+    n = v_re[0].n_slots
+    lvl = v_re[0].level
     W = dsp.dft_matrix(cfg.D)
     C, S = W.real, W.imag
     b, giants = k3_schedule(cfg)
-    xr = [v_re] + [ev.rotate(v_re, s) for s in range(1, b)]
-    xi = [v_im] + [ev.rotate(v_im, s) for s in range(1, b)]
+    xr = [list(v_re)] + [[ev.rotate(v, s) for v in v_re] for s in range(1, b)]
+    xi = [list(v_im)] + [[ev.rotate(v, s) for v in v_im] for s in range(1, b)]
     out_re = out_im = None
     for gp, G, babies in giants:
         t_re, t_im = [], []
@@ -229,46 +255,63 @@ def k3_doppler_dft(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg: Chain
             pc = book.vec(f"k3.c.{gp}.{s}", dc, lvl)
             ps = book.vec(f"k3.s.{gp}.{s}", ds, lvl)
             pns = book.vec(f"k3.ns.{gp}.{s}", -ds, lvl)
-            t_re += [(pc, xr[s]), (pns, xi[s])]
-            t_im += [(ps, xr[s]), (pc, xi[s])]
-        ir = ev.rotate(ev.pmult_sum(t_re), G)
-        ii = ev.rotate(ev.pmult_sum(t_im), G)
-        out_re = ir if out_re is None else ev.add(out_re, ir)
-        out_im = ii if out_im is None else ev.add(out_im, ii)
-    return ev.rescale(out_re), ev.rescale(out_im)
+            t_re += [(pc, s, "r"), (pns, s, "i")]
+            t_im += [(ps, s, "r"), (pc, s, "i")]
+
+        def terms(spec, f):
+            return [(pt, (xr if which == "r" else xi)[s][f]) for pt, s, which in spec]
+
+        nf = len(v_re)
+        ir = [ev.rotate(x, G) for x in [ev.pmult_sum(terms(t_re, f)) for f in range(nf)]]
+        ii = [ev.rotate(x, G) for x in [ev.pmult_sum(terms(t_im, f)) for f in range(nf)]]
+        out_re = ir if out_re is None else [ev.add(a, x) for a, x in zip(out_re, ir)]
+        out_im = ii if out_im is None else [ev.add(a, x) for a, x in zip(out_im, ii)]
+    return [ev.rescale(x) for x in out_re], [ev.rescale(x) for x in out_im]
+
+
+def k3_doppler_dft(ev, book, v_re, v_im, cfg):
+    """K3 on one frame."""
+    dre, dim = k3_doppler_dft_frames(ev, book, [v_re], [v_im], cfg)
+    return dre[0], dim[0]
 
 
 # ------------------------------------------------------------------ gesture frame
 
 def k1_power(ev, d_re, d_im):
     """K1 on the K3 output: P = rescale(relin(tensor(d_re,d_re) + tensor(d_im,d_im)))."""
-    return ev.relin_rescale(ev.tensor_sum([(d_re, d_re), (d_im, d_im)]))
+    return ev.relin_rescale_all([ev.tensor_sum([(a, a), (b, b)]) for a, b in zip(d_re, d_im)])
 
 
-def k6_notch(ev, book, P_ct, cfg):
+def k6_notch(ev, book, P_cts, cfg):
     """K6: P (.) m~ with m~[d] = m[d]/s, s = R A (sum w)^2 (P:887 fold)."""
-    n = P_ct.n_slots
+    n = P_cts[0].n_slots
     s = dsp.spectral_scale(cfg.R, cfg.A, cfg.D)
     mask = np.tile(dsp.notch_mask(cfg.D, cfg.notch_width) / s, n // cfg.D)
-    return ev.pmult_rescale(P_ct, book.vec("k6.mask", mask, P_ct.level))
+    pt = book.vec("k6.mask", mask, P_cts[0].level)
+    return [ev.rescale(x) for x in [ev.pmult_sum([(pt, p)]) for p in P_cts]]
 
 
 def k2_doppler_soft_power(ev, Pm, cfg):
     """K2b (Eq. gesture_soft_power): S = rotsum over the n/D blocks
     (stride D; every block then holds sum_{a,r}, reading #8); S^gamma by squarings;
     f = Pm (.) S^gamma (P:906 'feature weighting')."""
-    S = ev.rotsum(Pm, Pm.n_slots // cfg.D, cfg.D)
+    S = ev.rotsum_all(Pm, Pm[0].n_slots // cfg.D, cfg.D)
     for _ in range(int(math.log2(cfg.gamma))):
-        S = ev.relin_rescale(ev.tensor_sum([(S, S)]))
-    return ev.relin_rescale(ev.tensor_sum([(ev.drop_to(Pm, S.level), S)]))
+        S = ev.square_rescale_all(S)
+    Pd = [ev.drop_to(p, s.level) for p, s in zip(Pm, S)]
+    return ev.relin_rescale_all([ev.tensor_sum([(p, s)]) for p, s in zip(Pd, S)])
+
+
+def gesture_frames(ev, book, v_re, v_im, cfg):
+    """Per frame: K3 -> K1 -> K6 -> K2b -> weighting, on a list of frames."""
+    d_re, d_im = k3_doppler_dft_frames(ev, book, v_re, v_im, cfg)
+    P_cts = k1_power(ev, d_re, d_im)
+    Pm = k6_notch(ev, book, P_cts, cfg)
+    return k2_doppler_soft_power(ev, Pm, cfg)
 
 
 def gesture_frame(ev, book, v_re, v_im, cfg):
-    """Per frame: K3 -> K1 -> K6 -> K2b -> weighting."""
-    d_re, d_im = k3_doppler_dft(ev, book, v_re, v_im, cfg)
-    P_ct = k1_power(ev, d_re, d_im)
-    Pm = k6_notch(ev, book, P_ct, cfg)
-    return k2_doppler_soft_power(ev, Pm, cfg)
+    return gesture_frames(ev, book, [v_re], [v_im], cfg)[0]
 
 
 def frame_accumulate(ev, feats):
@@ -276,6 +319,16 @@ def frame_accumulate(ev, feats):
     acc = feats[0]
     for f in feats[1:]:
         acc = ev.add(acc, f)
+    return acc
+
+
+def gesture_features(ev, book, v_re, v_im, cfg):
+    """All F frames in batches of cfg.frame_batch: per batch the frame kernels, the
+    batch's features summed, batches then added in order."""
+    acc = None
+    for s, e in chunks(len(v_re), cfg.frame_batch):
+        part = frame_accumulate(ev, gesture_frames(ev, book, v_re[s:e], v_im[s:e], cfg))
+        acc = part if acc is None else ev.add(acc, part)
     return acc
 
 
@@ -312,10 +365,10 @@ def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int
             inner = ev.rotate(inner, G)
         acc = inner if acc is None else ev.add(acc, inner)
     z = ev.rescale(acc)
-    y = ev.rotsum(z, n_in // h, h)
+    y = ev.rotsum_all([z], n_in // h, h)[0]
     y = ev.add_plain(y, book.vec(f"fc{layer}.bias", np.asarray(bias, dtype=np.float64), y.level, scale=y.scale))
     if square:
-        y = ev.relin_rescale(ev.tensor_sum([(y, y)]))
+        y = ev.square_rescale_all([y])[0]
     return y
 
 
@@ -344,65 +397,65 @@ def gesture_fc(ev, book, feat, Ws, bs, cfg):
 # ------------------------------------------------------------------ vital V2
 
 def k4_soft_iq(ev, re, im, cfg):
-    """K4, P_phi = 2^k: p = |z|^2, m = p^P_phi, i = m re, q = m im,
-    I = rotsum_R(i), Q = rotsum_R(q) (slot 0 valid)."""
-    p = ev.relin_rescale(ev.tensor_sum([(re, re), (im, im)]))
-    m = p
+    """K4 on lists of frames, P_phi = 2^k: p = |z|^2, m = p^P_phi,
+    i = m re, q = m im, I = rotsum_R(i), Q = rotsum_R(q) (slot 0 valid)."""
+    m = ev.relin_rescale_all([ev.tensor_sum([(r, r), (i, i)]) for r, i in zip(re, im)])
     for _ in range(int(math.log2(cfg.p_phi))):
-        m = ev.relin_rescale(ev.tensor_sum([(m, m)]))
-    i = ev.relin_rescale(ev.tensor_sum([(m, ev.drop_to(re, m.level))]))
-    q = ev.relin_rescale(ev.tensor_sum([(m, ev.drop_to(im, m.level))]))
-    return ev.rotsum(i, cfg.R, 1), ev.rotsum(q, cfg.R, 1)
+        m = ev.square_rescale_all(m)
+    red = [ev.drop_to(r, x.level) for r, x in zip(re, m)]
+    i_ = ev.relin_rescale_all([ev.tensor_sum([(x, r)]) for x, r in zip(m, red)])
+    imd = [ev.drop_to(i, x.level) for i, x in zip(im, m)]
+    q_ = ev.relin_rescale_all([ev.tensor_sum([(x, i)]) for x, i in zip(m, imd)])
+    return ev.rotsum_all(i_, cfg.R, 1), ev.rotsum_all(q_, cfg.R, 1)
 
 
 def k5_fir(ev, xs, taps):
     """K5: x_f[t] = rescale(sum_{k <= t} h[k] x[t-k]) (causal Toeplitz)."""
-    out = []
+    lin = []
     for t in range(len(xs)):
         ks = [k for k in range(len(taps)) if t - k >= 0]
-        out.append(ev.rescale(ev.lincomb_scalar([xs[t - k] for k in ks], [taps[k] for k in ks])))
-    return out
+        lin.append(ev.lincomb_scalar([xs[t - k] for k in ks], [taps[k] for k in ks]))
+    return [ev.rescale(x) for x in lin]
 
 
 def k7_taylor_phase(ev, If, Qf, order):
     """K7: y[t] = Q_f[t] I_f[t-1] - I_f[t] Q_f[t-1]; first order y,
     third order y x^2 - y^3/3 (literal polynomial, reading #2); t = 1..F-1."""
-    out = []
-    for t in range(1, len(If)):
-        ty = ev.tensor_sum([(Qf[t], If[t - 1])])
-        ty2 = ev.tensor_sum([(If[t], Qf[t - 1])])
-        y = ev.relin_rescale(ev.sub(ty, ty2))
-        if order == 1:
-            out.append(y)
-            continue
-        x = ev.relin_rescale(ev.tensor_sum([(If[t], If[t - 1]), (Qf[t], Qf[t - 1])]))
-        x2 = ev.relin_rescale(ev.tensor_sum([(x, x)]))
-        y2 = ev.relin_rescale(ev.tensor_sum([(y, y)]))
-        yt = ev.rescale(ev.lincomb_scalar([y], [-1.0 / 3.0]))
-        yx2 = ev.relin_rescale(ev.tensor_sum([(ev.drop_to(y, x2.level), x2)]))
-        y3 = ev.relin_rescale(ev.tensor_sum([(y2, yt)]))
-        out.append(ev.add(yx2, y3))
-    return out
+    T = range(1, len(If))
+    ty = [ev.tensor_sum([(Qf[t], If[t - 1])]) for t in T]
+    ty2 = [ev.tensor_sum([(If[t], Qf[t - 1])]) for t in T]
+    y = ev.relin_rescale_all([ev.sub(a, b) for a, b in zip(ty, ty2)])
+    if order == 1:
+        return y
+    x = ev.relin_rescale_all([ev.tensor_sum([(If[t], If[t - 1]), (Qf[t], Qf[t - 1])]) for t in T])
+    x2 = ev.square_rescale_all(x)
+    y2 = ev.square_rescale_all(y)
+    yt = [ev.rescale(v) for v in [ev.lincomb_scalar([v], [-1.0 / 3.0]) for v in y]]
+    yd = [ev.drop_to(v, w.level) for v, w in zip(y, x2)]
+    yx2 = ev.relin_rescale_all([ev.tensor_sum([(v, w)]) for v, w in zip(yd, x2)])
+    y3 = ev.relin_rescale_all([ev.tensor_sum([(v, w)]) for v, w in zip(y2, yt)])
+    return [ev.add(a, b) for a, b in zip(yx2, y3)]
 
 
 def vp_band_power(ev, ys, bins):
     """VP+ (P:279-288): X[k] = sum_t c_{k,t} y[t] (+ j s_{k,t}), P_k = |X[k]|^2."""
     Fp = len(ys)
-    out = []
-    for k in bins:
-        c, s = dsp.narrowband_dft_coefs(Fp, int(k))
-        xr = ev.rescale(ev.lincomb_scalar(ys, c))
-        xi = ev.rescale(ev.lincomb_scalar(ys, s))
-        out.append(ev.relin_rescale(ev.tensor_sum([(xr, xr), (xi, xi)])))
-    return out
+    coefs = [dsp.narrowband_dft_coefs(Fp, int(k)) for k in bins]
+    xr = [ev.lincomb_scalar(ys, c) for c, _ in coefs]
+    xi = [ev.lincomb_scalar(ys, s) for _, s in coefs]
+    xr = [ev.rescale(x) for x in xr]
+    xi = [ev.rescale(x) for x in xi]
+    return ev.relin_rescale_all([ev.tensor_sum([(a, a), (b, b)]) for a, b in zip(xr, xi)])
 
 
 def vitals_v2(ev, re_list, im_list, taps_by_band, cfg):
     """Chain V2: K4 -> K5 -> K7 -> narrowband DFT -> |X|^2 per band;
     returns {band index: [P_k ciphertexts]} (sharpen/average on the client, reading #4)."""
-    IQ = [k4_soft_iq(ev, re, im, cfg) for re, im in zip(re_list, im_list)]
-    I = [a for a, _ in IQ]
-    Q = [b for _, b in IQ]
+    I, Q = [], []
+    for s, e in chunks(len(re_list), cfg.frame_batch):
+        Ib, Qb = k4_soft_iq(ev, re_list[s:e], im_list[s:e], cfg)
+        I += Ib
+        Q += Qb
     out = {}
     for bi, taps in enumerate(taps_by_band):
         If = k5_fir(ev, I, taps)

@@ -36,7 +36,7 @@ DCt input_ct(Ctx &c, const mmfhe_ct &ct)
     MMFHE_REQUIRE(ct.data != nullptr, MMFHE_E_INVALID_ARG, "null ciphertext");
     MMFHE_REQUIRE(ct.log_n == c.log_n, MMFHE_E_PARAMS, "ring dimension mismatch");
     MMFHE_REQUIRE(ct.level <= c.L, MMFHE_E_DEPTH, "level above the modulus chain");
-    if (ct.on_device && ct.form == MMFHE_FORM_EVAL) return view_ct(ct, npolys_of(ct));
+    if (ct.on_device && ct.form == MMFHE_FORM_EVAL) return view_ct(c, ct, npolys_of(ct));
     return import_ct(c, ct, npolys_of(ct));
 }
 
@@ -207,13 +207,11 @@ mmfhe_status mmfhe_eval_chain(mmfhe_ctx *ctx, const char *chain, const mmfhe_cha
     std::vector<uint32_t> lv = chain_plan(*ctx, chain, c, in[0].level, n_in);
     *n_out = lv.size();
     MMFHE_REQUIRE(lv.size() <= cap, MMFHE_E_LAYOUT, "output capacity too small");
-    std::vector<DCt> ins;
-    ins.reserve(n_in);
-    for (size_t i = 0; i < n_in; ++i) ins.push_back(input_ct(*ctx, in[i]));
-    std::vector<const DCt *> ptrs;
-    for (auto &x : ins) ptrs.push_back(&x);
-    std::vector<DCt> res = run_chain(*ctx, chain, c, ptrs);
-    for (size_t i = 0; i < res.size(); ++i) export_ct(*ctx, res[i], out[i]);
+    std::vector<DCt> res = run_chain(*ctx, chain, c, in, n_in);
+    size_t o = 0;
+    for (auto &d : res)
+        for (uint32_t b = 0; b < d.batch; ++b) export_ct(*ctx, slice(d, b, 1), out[o++]);
+    MMFHE_REQUIRE(o == lv.size(), MMFHE_E_LAYOUT, "chain produced an unexpected number of outputs");
     API_END(ctx)
 }
 
@@ -242,9 +240,9 @@ static mmfhe_status ntt_rows(mmfhe_ctx *ctx, uint64_t *d_rows, uint32_t n_rows, 
         PrimeMap pm = make_map(std::vector<uint32_t>(m.begin() + s, m.begin() + s + cnt));
         uint64_t *d = d_rows + (size_t)s * ctx->n;
         if (inv)
-            ntt_inverse(ctx->kt, d, cnt, pm, ctx->stream, ctx->launches);
+            ntt_inverse(*ctx, d, cnt, pm);
         else
-            ntt_forward(ctx->kt, d, cnt, pm, ctx->stream, ctx->launches);
+            ntt_forward(*ctx, d, cnt, pm);
     }
     API_END(ctx)
 }
@@ -339,7 +337,7 @@ mmfhe_status mmfhe_keyswitch(mmfhe_ctx *ctx, const mmfhe_ct *x, int32_t step, in
     }
     ctx->rec("keyswitch", in.level);
     DCt r = make_ct(*ctx, in.level, 2, in.n_slots, in.scale);
-    ev_keyswitch(*ctx, in.data(), in.level, *key, r.poly(0, ctx->n), r.poly(1, ctx->n), nullptr, nullptr);
+    ev_keyswitch(*ctx, in.data(), in.item_words(), in.level, 1, *key, r.data(), r.item_words(), nullptr, 0, false);
     export_ct(*ctx, r, *out);
     API_END(ctx)
 }
@@ -356,22 +354,20 @@ mmfhe_status mmfhe_mod_switch(mmfhe_ctx *ctx, const mmfhe_ct *a, uint32_t level,
 mmfhe_status mmfhe_hrot_batch(mmfhe_ctx *ctx, const mmfhe_ct *a, size_t n, int32_t step, mmfhe_ct *out)
 {
     API_BEGIN
-    MMFHE_REQUIRE(a && out, MMFHE_E_INVALID_ARG, "null argument");
-    for (size_t i = 0; i < n; ++i) {
-        DCt x = input_ct(*ctx, a[i]);
-        export_ct(*ctx, ev_rotate(*ctx, x, step), out[i]);
-    }
+    MMFHE_REQUIRE(a && out && n, MMFHE_E_INVALID_ARG, "null argument");
+    DCt x = import_batch(*ctx, a, 0, 1, n);  // one batched KS: each evk word read once for all n
+    DCt r = ev_rotate(*ctx, x, step);
+    for (size_t i = 0; i < n; ++i) export_ct(*ctx, slice(r, (uint32_t)i, 1), out[i]);
     API_END(ctx)
 }
 
 mmfhe_status mmfhe_hmult_batch(mmfhe_ctx *ctx, const mmfhe_ct *a, const mmfhe_ct *b, size_t n, mmfhe_ct *out)
 {
     API_BEGIN
-    MMFHE_REQUIRE(a && b && out, MMFHE_E_INVALID_ARG, "null argument");
-    for (size_t i = 0; i < n; ++i) {
-        DCt x = input_ct(*ctx, a[i]), y = input_ct(*ctx, b[i]);
-        export_ct(*ctx, ev_relin(*ctx, ev_tensor_sum(*ctx, {{&x, &y}})), out[i]);
-    }
+    MMFHE_REQUIRE(a && b && out && n, MMFHE_E_INVALID_ARG, "null argument");
+    DCt x = import_batch(*ctx, a, 0, 1, n), y = import_batch(*ctx, b, 0, 1, n);
+    DCt r = ev_relin(*ctx, ev_tensor_sum(*ctx, {{&x, &y}}));
+    for (size_t i = 0; i < n; ++i) export_ct(*ctx, slice(r, (uint32_t)i, 1), out[i]);
     API_END(ctx)
 }
 
@@ -403,6 +399,27 @@ mmfhe_status mmfhe_trace_enable(mmfhe_ctx *ctx, int on)
 {
     API_BEGIN
     ctx->trace_on = on != 0;
+    API_END(ctx)
+}
+
+mmfhe_status mmfhe_profile_enable(mmfhe_ctx *ctx, int on)
+{
+    API_BEGIN
+    if (!on && ctx->prof_on) ctx->profile_report();
+    ctx->prof_on = on != 0;
+    API_END(ctx)
+}
+
+mmfhe_status mmfhe_profile_get(mmfhe_ctx *ctx, char *buf, size_t cap, size_t *len)
+{
+    API_BEGIN
+    std::string s = ctx->profile_report();
+    if (len) *len = s.size();
+    if (buf && cap) {
+        size_t n = std::min(cap - 1, s.size());
+        std::memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    }
     API_END(ctx)
 }
 

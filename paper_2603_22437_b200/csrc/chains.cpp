@@ -1,8 +1,8 @@
-// chains.cpp -- the mmFHE kernel chains over the device evaluator.
+// chains.cpp -- the mmFHE kernel chains over the batched device evaluator.
 //
 // Each kernel follows the paper's circuit with the canonical op sequence of
 // SURVEY §8(c)-7 (relinearisation / rescale placement, BSGS split, overflow
-// folds), so that the op trace and every residue equal the CPU oracle's:
+// folds), so the op trace and every residue equal the CPU oracle's:
 //   K1  Eq. energy            P:767-771     K5  Eq. fir_iq
 //   K2  Eqs. soft_power_*     P:777-788     K6  Eq. notch_mask
 //   K2b Eq. gesture_soft_pow  P:128-133     K7  Eq. taylor_arctan
@@ -10,6 +10,12 @@
 //       BSGS P:164-176
 //   K4  Eqs. phase_mask/iq
 // Pipelines: vital signs P:901-902, dynamic classification P:904-907.
+//
+// Per-frame kernels run on batches of frames (cfg.frame_batch, op-major order
+// inside a batch): one launch per op covers the whole batch, so plaintext
+// diagonals and evaluation keys are streamed once per batch.  K5 (Toeplitz FIR
+// over frames) and the narrowband DFT are banded / dense scalar matrix products
+// over the frame batch (one kernel each).
 //
 // Public plaintext operands are looked up by (name, level); when absent and
 // the ctx was prepared (mmfhe_prepare_chain), they are computed from the
@@ -104,11 +110,26 @@ std::vector<uint32_t> rotsum_steps(uint32_t count, uint32_t stride)
     return out;
 }
 
+// Copy a list of batches into one contiguous batch.
+DCt concat(Ctx &c, const std::vector<DCt> &parts)
+{
+    uint32_t total = 0;
+    for (auto &p : parts) total += p.batch;
+    const DCt &p0 = parts[0];
+    DCt r = make_ct(c, p0.level, p0.npolys, p0.n_slots, p0.scale, total);
+    uint32_t at = 0;
+    for (auto &p : parts) {
+        CUDA_CHECK(cudaMemcpyAsync(r.item(at), p.data(), p.item_words() * p.batch * 8, cudaMemcpyDeviceToDevice,
+                                   c.stream));
+        at += p.batch;
+    }
+    return r;
+}
+
 class Runner {
   public:
     Runner(Ctx &c, const mmfhe_chain_cfg &cfg) : c_(c), cfg_(cfg) {}
 
-    // plaintext operand (name, level), computed + encoded lazily when the ctx is prepared
     const DPlain &plain(const std::string &name, uint32_t level, double scale,
                         const std::function<std::vector<double>()> &values)
     {
@@ -128,20 +149,25 @@ class Runner {
         return c_.scalars[name] = fn();
     }
 
+    uint32_t frame_batch(uint32_t F) const { return cfg_.frame_batch ? std::min(cfg_.frame_batch, F) : F; }
+
     // ---------------------------------------------------------- K1 / K2
-    DCt k1_energy(const std::vector<const DCt *> &re, const std::vector<const DCt *> &im)
+    DCt k1_energy(const DCt &re, const DCt &im)
     {
-        std::vector<std::pair<const DCt *, const DCt *>> pairs;
-        for (size_t t = 0; t < re.size(); ++t) {
-            pairs.push_back({re[t], re[t]});
-            pairs.push_back({im[t], im[t]});
+        std::vector<DCt> views;
+        views.reserve(2 * re.batch);
+        for (uint32_t t = 0; t < re.batch; ++t) {
+            views.push_back(slice(re, t, 1));
+            views.push_back(slice(im, t, 1));
         }
+        std::vector<std::pair<const DCt *, const DCt *>> pairs;
+        for (auto &v : views) pairs.push_back({&v, &v});
         return ev_relin_rescale(c_, ev_tensor_sum(c_, pairs));
     }
 
     std::pair<DCt, DCt> k2_soft_attention(const DCt &E)
     {
-        DCt w = ev_drop_to(c_, E, E.level);
+        DCt w = copy_ct(c_, E);
         for (uint32_t i = 0; i < ilog2(cfg_.gamma); ++i) w = ev_square_rescale(c_, w);
         const uint32_t n = E.n_slots, R = cfg_.R;
         const double FFR = (double)cfg_.F * cfg_.F * R;
@@ -157,24 +183,26 @@ class Runner {
         });
         DCt Nn = ev_rescale(c_, ev_pmult_sum(c_, {{&ramp, &w}}));
         DCt Dd = ev_rescale(c_, ev_pmult_sum(c_, {{&one, &w}}));
-        return {ev_rotsum(c_, Nn, R, 1), ev_rotsum(c_, Dd, R, 1)};
+        DCt Ns = ev_rotsum(c_, Nn, R, 1);
+        DCt Ds = ev_rotsum(c_, Dd, R, 1);
+        return {std::move(Ns), std::move(Ds)};
     }
 
-    // ---------------------------------------------------------- K3 (BSGS)
+    // ---------------------------------------------------------- K3 (BSGS), batched over frames
     std::pair<DCt, DCt> k3_doppler_dft(const DCt &vre, const DCt &vim)
     {
         const uint32_t n = vre.n_slots, D = cfg_.D, lvl = vre.level;
         Sched s = k3_schedule(cfg_);
         std::vector<DCt> xr, xi;
-        xr.push_back(ev_drop_to(c_, vre, lvl));
-        xi.push_back(ev_drop_to(c_, vim, lvl));
+        xr.push_back(copy_ct(c_, vre));
+        xi.push_back(copy_ct(c_, vim));
         for (uint32_t b = 1; b < s.b; ++b) xr.push_back(ev_rotate(c_, vre, (int32_t)b));
         for (uint32_t b = 1; b < s.b; ++b) xi.push_back(ev_rotate(c_, vim, (int32_t)b));
-        // W = hann[n] e^{-j 2 pi sigma(d) n / D}
+        // W = hann[m] e^{-j 2 pi sigma(d) m / D}, diagonal o of I (x) W, pre-rotated by -G
         auto diag = [&](bool imag, int32_t o, int32_t G, bool neg) {
             std::vector<double> w = hann(D), v(n, 0.0);
             for (uint32_t j = 0; j < n; ++j) {
-                const uint32_t col = (uint32_t)(((int64_t)j + o) % (int64_t)n + n) % n;
+                const uint32_t col = (uint32_t)((((int64_t)j + o) % (int64_t)n + n) % n);
                 if (j / D != col / D) continue;
                 const uint32_t d = j % D, m = col % D;
                 const uint32_t sig = (d + D / 2) % D;
@@ -209,10 +237,12 @@ class Runner {
                 out_im = ev_addsub(c_, out_im, ii, false);
             }
         }
-        return {ev_rescale(c_, out_re), ev_rescale(c_, out_im)};
+        DCt a = ev_rescale(c_, out_re);
+        DCt b = ev_rescale(c_, out_im);
+        return {std::move(a), std::move(b)};
     }
 
-    // ---------------------------------------------------------- gesture frame
+    // ---------------------------------------------------------- gesture frame (batched)
     DCt k1_power(const DCt &dre, const DCt &dim)
     {
         return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&dre, &dre}, {&dim, &dim}}));
@@ -266,7 +296,7 @@ class Runner {
             bias = &c_.fc_b[layer - 1];
         }
         std::vector<DCt> babies;
-        babies.push_back(ev_drop_to(c_, x, lvl));
+        babies.push_back(copy_ct(c_, x));
         for (uint32_t b = 1; b < std::min(s.b, h); ++b) babies.push_back(ev_rotate(c_, x, (int32_t)b));
         DCt acc;
         bool first = true;
@@ -311,7 +341,7 @@ class Runner {
         return fc_layer(x, 3, false);
     }
 
-    // ---------------------------------------------------------- vital V2
+    // ---------------------------------------------------------- vital V2 (batched over frames)
     std::pair<DCt, DCt> k4_soft_iq(const DCt &re, const DCt &im)
     {
         DCt p = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&re, &re}, {&im, &im}}));
@@ -320,57 +350,49 @@ class Runner {
         DCt i_ = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&p, &red}}));
         DCt imd = ev_drop_to(c_, im, p.level);
         DCt q_ = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&p, &imd}}));
-        return {ev_rotsum(c_, i_, cfg_.R, 1), ev_rotsum(c_, q_, cfg_.R, 1)};
+        DCt I = ev_rotsum(c_, i_, cfg_.R, 1);
+        DCt Q = ev_rotsum(c_, q_, cfg_.R, 1);
+        return {std::move(I), std::move(Q)};
     }
 
-    std::vector<DCt> k5_fir(const std::vector<DCt> &xs, const std::vector<double> &taps)
+    // I_f[t] = sum_{k <= t} h[k] I[t-k]: banded Toeplitz product over the frame batch, then rescale
+    DCt k5_fir(const DCt &x, const std::vector<double> &taps)
     {
-        std::vector<DCt> out;
-        for (size_t t = 0; t < xs.size(); ++t) {
-            std::vector<const DCt *> cts;
-            std::vector<double> cf;
-            for (size_t k = 0; k < taps.size() && k <= t; ++k) {
-                cts.push_back(&xs[t - k]);
-                cf.push_back(taps[k]);
-            }
-            out.push_back(ev_rescale(c_, ev_lincomb(c_, cts, cf)));
-        }
-        return out;
+        const uint32_t F = x.batch, W = (uint32_t)taps.size();
+        std::vector<double> coef((size_t)F * W);
+        for (uint32_t j = 0; j < F; ++j)
+            for (uint32_t w = 0; w < W; ++w) coef[(size_t)j * W + w] = taps[W - 1 - w];
+        return ev_rescale(c_, ev_lincomb_mat(c_, x, F, W, -(int)(W - 1), 1, coef));
     }
 
-    std::vector<DCt> k7_taylor_phase(const std::vector<DCt> &If, const std::vector<DCt> &Qf)
+    DCt k7_taylor_phase(const DCt &If, const DCt &Qf)
     {
-        std::vector<DCt> out;
-        for (size_t t = 1; t < If.size(); ++t) {
-            DCt ty = ev_tensor_sum(c_, {{&Qf[t], &If[t - 1]}});
-            DCt ty2 = ev_tensor_sum(c_, {{&If[t], &Qf[t - 1]}});
-            DCt y = ev_relin_rescale(c_, ev_addsub(c_, ty, ty2, true));
-            if (cfg_.taylor_order == 1) {
-                out.push_back(std::move(y));
-                continue;
-            }
-            DCt x = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&If[t], &If[t - 1]}, {&Qf[t], &Qf[t - 1]}}));
-            DCt x2 = ev_square_rescale(c_, x);
-            DCt y2 = ev_square_rescale(c_, y);
-            DCt yt = ev_rescale(c_, ev_lincomb(c_, {&y}, {-1.0 / 3.0}));
-            DCt yd = ev_drop_to(c_, y, x2.level);
-            DCt yx2 = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&yd, &x2}}));
-            DCt y3 = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&y2, &yt}}));
-            out.push_back(ev_addsub(c_, yx2, y3, false));
-        }
-        return out;
+        const uint32_t F = If.batch;
+        DCt I1 = slice(If, 1, F - 1), I0 = slice(If, 0, F - 1);
+        DCt Q1 = slice(Qf, 1, F - 1), Q0 = slice(Qf, 0, F - 1);
+        DCt ty = ev_tensor_sum(c_, {{&Q1, &I0}});
+        DCt ty2 = ev_tensor_sum(c_, {{&I1, &Q0}});
+        DCt y = ev_relin_rescale(c_, ev_addsub(c_, ty, ty2, true));
+        if (cfg_.taylor_order == 1) return y;
+        DCt x = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&I1, &I0}, {&Q1, &Q0}}));
+        DCt x2 = ev_square_rescale(c_, x);
+        DCt y2 = ev_square_rescale(c_, y);
+        std::vector<double> third(y.batch, -1.0 / 3.0);
+        DCt yt = ev_rescale(c_, ev_lincomb_mat(c_, y, y.batch, 1, 0, 1, third));
+        DCt yd = ev_drop_to(c_, y, x2.level);
+        DCt yx2 = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&yd, &x2}}));
+        DCt y3 = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&y2, &yt}}));
+        return ev_addsub(c_, yx2, y3, false);
     }
 
-    std::vector<DCt> vp_band_power(const std::vector<DCt> &ys, uint32_t band)
+    DCt vp_band_power(const DCt &ys, uint32_t band)
     {
-        const uint32_t Fp = (uint32_t)ys.size();
-        std::vector<const DCt *> ptrs;
-        for (auto &y : ys) ptrs.push_back(&y);
-        std::vector<DCt> out;
-        for (uint32_t bi = 0; bi < cfg_.n_bins[band]; ++bi) {
+        const uint32_t Fp = ys.batch, K = cfg_.n_bins[band];
+        std::vector<double> coef((size_t)2 * K * Fp);
+        for (uint32_t bi = 0; bi < K; ++bi) {
             const uint32_t k = cfg_.bins[band][bi];
             const std::string sfx = "." + std::to_string(band) + "." + std::to_string(k);
-            auto coefs = [&](bool imag) {
+            auto gen = [=](bool imag) {
                 return [=]() {
                     std::vector<double> w = hann(Fp), v(Fp);
                     for (uint32_t t = 0; t < Fp; ++t) {
@@ -380,33 +402,56 @@ class Runner {
                     return v;
                 };
             };
-            const std::vector<double> &cc = scalars("vp.c" + sfx, coefs(false));
-            const std::vector<double> &ss = scalars("vp.s" + sfx, coefs(true));
+            const std::vector<double> &cc = scalars("vp.c" + sfx, gen(false));
+            const std::vector<double> &ss = scalars("vp.s" + sfx, gen(true));
             MMFHE_REQUIRE(cc.size() == Fp && ss.size() == Fp, MMFHE_E_SHAPE, "DFT coefficient count");
-            DCt xr = ev_rescale(c_, ev_lincomb(c_, ptrs, cc));
-            DCt xi = ev_rescale(c_, ev_lincomb(c_, ptrs, ss));
-            out.push_back(ev_relin_rescale(c_, ev_tensor_sum(c_, {{&xr, &xr}, {&xi, &xi}})));
+            std::copy(cc.begin(), cc.end(), coef.begin() + (size_t)bi * Fp);
+            std::copy(ss.begin(), ss.end(), coef.begin() + (size_t)(K + bi) * Fp);
+        }
+        DCt X = ev_rescale(c_, ev_lincomb_mat(c_, ys, 2 * K, Fp, 0, 0, coef));
+        DCt Xr = slice(X, 0, K), Xi = slice(X, K, K);
+        return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&Xr, &Xr}, {&Xi, &Xi}}));
+    }
+
+    std::vector<DCt> vitals_v2(const mmfhe_ct *in, size_t n_in)
+    {
+        const uint32_t F = (uint32_t)(n_in / 2), fb = frame_batch(F);
+        std::vector<DCt> Is, Qs;
+        for (uint32_t t0 = 0; t0 < F; t0 += fb) {
+            const uint32_t cnt = std::min(fb, F - t0);
+            DCt re = import_batch(c_, in, 2 * (size_t)t0, 2, cnt);
+            DCt im = import_batch(c_, in, 2 * (size_t)t0 + 1, 2, cnt);
+            auto iq = k4_soft_iq(re, im);
+            Is.push_back(std::move(iq.first));
+            Qs.push_back(std::move(iq.second));
+        }
+        DCt I = Is.size() == 1 ? std::move(Is[0]) : concat(c_, Is);
+        DCt Q = Qs.size() == 1 ? std::move(Qs[0]) : concat(c_, Qs);
+        std::vector<DCt> out;
+        for (uint32_t b = 0; b < cfg_.n_bands; ++b) {
+            const std::vector<double> &taps = scalars("k5.b" + std::to_string(b), nullptr);
+            MMFHE_REQUIRE(cfg_.n_taps[b] == 0 || taps.size() == cfg_.n_taps[b], MMFHE_E_SHAPE, "FIR tap count");
+            DCt If = k5_fir(I, taps);
+            DCt Qf = k5_fir(Q, taps);
+            DCt ys = k7_taylor_phase(If, Qf);
+            out.push_back(vp_band_power(ys, b));
         }
         return out;
     }
 
-    std::vector<DCt> vitals_v2(const std::vector<const DCt *> &re, const std::vector<const DCt *> &im)
+    DCt gesture(const mmfhe_ct *in, size_t n_in)
     {
-        std::vector<DCt> I, Q;
-        for (size_t t = 0; t < re.size(); ++t) {
-            auto iq = k4_soft_iq(*re[t], *im[t]);
-            I.push_back(std::move(iq.first));
-            Q.push_back(std::move(iq.second));
+        const uint32_t F = (uint32_t)(n_in / 2), fb = frame_batch(F);
+        DCt acc;
+        for (uint32_t t0 = 0; t0 < F; t0 += fb) {
+            const uint32_t cnt = std::min(fb, F - t0);
+            DCt vre = import_batch(c_, in, 2 * (size_t)t0, 2, cnt);
+            DCt vim = import_batch(c_, in, 2 * (size_t)t0 + 1, 2, cnt);
+            DCt f = gesture_frame(vre, vim);
+            DCt part = ev_batch_sum(c_, f);
+            acc = t0 == 0 ? std::move(part) : ev_addsub(c_, acc, part, false);
         }
-        std::vector<DCt> out;
-        for (uint32_t b = 0; b < cfg_.n_bands; ++b) {
-            const std::vector<double> &taps = scalars("k5.b" + std::to_string(b), nullptr);
-            MMFHE_REQUIRE(taps.size() == cfg_.n_taps[b] || cfg_.n_taps[b] == 0, MMFHE_E_SHAPE, "FIR tap count");
-            std::vector<DCt> If = k5_fir(I, taps), Qf = k5_fir(Q, taps);
-            std::vector<DCt> ys = k7_taylor_phase(If, Qf);
-            for (auto &p : vp_band_power(ys, b)) out.push_back(std::move(p));
-        }
-        return out;
+        return gesture_fc(acc);
     }
 
   private:
@@ -463,19 +508,23 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
 std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const mmfhe_chain_cfg &cfg, uint32_t in_level,
                                  size_t n_in)
 {
+    (void)c;
     const uint32_t dep = chain_depth(chain, cfg);
     MMFHE_REQUIRE(in_level >= dep, MMFHE_E_DEPTH,
                   "chain " + chain + " needs " + std::to_string(dep) + " levels, input has " +
                       std::to_string(in_level));
     const uint32_t out = in_level - dep;
-    if (chain == "k1_energy" || chain == "vitals_v1" || chain == "vitals_v2") {
+    if (chain == "k1_energy" || chain == "vitals_v1" || chain == "vitals_v2" || chain == "gesture") {
         MMFHE_REQUIRE(n_in == 2 * (size_t)cfg.F && cfg.F > 0, MMFHE_E_SHAPE, "expected 2F input ciphertexts");
     } else if (chain == "k3_doppler_dft" || chain == "gesture_frame") {
         MMFHE_REQUIRE(n_in == 2, MMFHE_E_SHAPE, "expected (v_re, v_im)");
     } else if (chain == "gesture_fc") {
         MMFHE_REQUIRE(n_in == 1, MMFHE_E_SHAPE, "expected one feature ciphertext");
-    } else if (chain == "gesture") {
-        MMFHE_REQUIRE(n_in == 2 * (size_t)cfg.F && cfg.F > 0, MMFHE_E_SHAPE, "expected 2F input ciphertexts");
+    }
+    if (chain == "vitals_v2") {
+        MMFHE_REQUIRE(cfg.F >= 2 && cfg.n_bands <= 4, MMFHE_E_SHAPE, "vitals_v2 needs F >= 2 and <= 4 bands");
+        for (uint32_t b = 0; b < cfg.n_bands; ++b)
+            MMFHE_REQUIRE(cfg.n_bins[b] >= 1 && cfg.n_bins[b] <= 64, MMFHE_E_SHAPE, "1..64 DFT bins per band");
     }
     size_t n_out = 1;
     if (chain == "vitals_v1" || chain == "k3_doppler_dft") n_out = 2;
@@ -486,44 +535,41 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
     return std::vector<uint32_t>(n_out, out);
 }
 
-std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_cfg &cfg,
-                           const std::vector<const DCt *> &in)
+std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_cfg &cfg, const mmfhe_ct *in,
+                           size_t n_in)
 {
-    MMFHE_REQUIRE(!in.empty(), MMFHE_E_SHAPE, "no inputs");
-    chain_plan(c, chain, cfg, in[0]->level, in.size());
-    for (auto *x : in)
-        MMFHE_REQUIRE(x->level == in[0]->level && x->scale == in[0]->scale, MMFHE_E_SCALE,
-                      "inputs must share level and scale");
+    MMFHE_REQUIRE(in && n_in, MMFHE_E_SHAPE, "no inputs");
+    chain_plan(c, chain, cfg, in[0].level, n_in);
     Runner r(c, cfg);
     std::vector<DCt> out;
-    std::vector<const DCt *> re, im;
-    for (size_t i = 0; i + 1 < in.size(); i += 2) {
-        re.push_back(in[i]);
-        im.push_back(in[i + 1]);
-    }
-    if (chain == "k1_energy") {
-        out.push_back(r.k1_energy(re, im));
-    } else if (chain == "vitals_v1") {
-        auto nd = r.k2_soft_attention(r.k1_energy(re, im));
-        out.push_back(std::move(nd.first));
-        out.push_back(std::move(nd.second));
+    if (chain == "k1_energy" || chain == "vitals_v1") {
+        DCt re = import_batch(c, in, 0, 2, n_in / 2);
+        DCt im = import_batch(c, in, 1, 2, n_in / 2);
+        DCt E = r.k1_energy(re, im);
+        if (chain == "k1_energy") {
+            out.push_back(std::move(E));
+        } else {
+            auto nd = r.k2_soft_attention(E);
+            out.push_back(std::move(nd.first));
+            out.push_back(std::move(nd.second));
+        }
     } else if (chain == "vitals_v2") {
-        out = r.vitals_v2(re, im);
-    } else if (chain == "k3_doppler_dft") {
-        auto d = r.k3_doppler_dft(*in[0], *in[1]);
-        out.push_back(std::move(d.first));
-        out.push_back(std::move(d.second));
-    } else if (chain == "gesture_frame") {
-        out.push_back(r.gesture_frame(*in[0], *in[1]));
+        out = r.vitals_v2(in, n_in);
+    } else if (chain == "k3_doppler_dft" || chain == "gesture_frame") {
+        DCt vre = import_batch(c, in, 0, 1, 1);
+        DCt vim = import_batch(c, in, 1, 1, 1);
+        if (chain == "k3_doppler_dft") {
+            auto d = r.k3_doppler_dft(vre, vim);
+            out.push_back(std::move(d.first));
+            out.push_back(std::move(d.second));
+        } else {
+            out.push_back(r.gesture_frame(vre, vim));
+        }
     } else if (chain == "gesture_fc") {
-        out.push_back(r.gesture_fc(*in[0]));
+        DCt x = import_batch(c, in, 0, 1, 1);
+        out.push_back(r.gesture_fc(x));
     } else if (chain == "gesture") {
-        std::vector<DCt> feats;
-        for (size_t t = 0; t < re.size(); ++t) feats.push_back(r.gesture_frame(*re[t], *im[t]));
-        std::vector<const DCt *> fp;
-        for (auto &f : feats) fp.push_back(&f);
-        DCt acc = ev_sum(c, fp);
-        out.push_back(r.gesture_fc(acc));
+        out.push_back(r.gesture(in, n_in));
     }
     return out;
 }

@@ -1,6 +1,7 @@
 // context.cu -- ctx creation: parameter validation, NTT twiddle tables,
 // base-conversion / rescale constants, device memory pool.
 #include <algorithm>
+#include <cstdio>
 #include <set>
 
 #include "context.h"
@@ -102,6 +103,44 @@ DPlain *Ctx::find_plain(const std::string &name, uint32_t level) const
 
 void Ctx::sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
 
+cudaEvent_t Ctx::next_event()
+{
+    if (ev_used == ev_pool.size()) {
+        cudaEvent_t e;
+        CUDA_CHECK(cudaEventCreate(&e));
+        ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+}
+
+std::string Ctx::profile_report()
+{
+    sync();
+    struct Agg {
+        uint64_t count = 0;
+        double ms = 0, bytes = 0;
+    };
+    std::map<std::string, Agg> agg;
+    for (auto &r : prof) {
+        float ms = 0;
+        CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+        Agg &g = agg[r.name];
+        g.count++;
+        g.ms += ms;
+        g.bytes += r.bytes;
+    }
+    prof.clear();
+    ev_used = 0;
+    std::string out;
+    char line[256];
+    for (auto &kv : agg) {
+        snprintf(line, sizeof(line), "%s %llu %.6f %.0f\n", kv.first.c_str(), (unsigned long long)kv.second.count,
+                 kv.second.ms, kv.second.bytes);
+        out += line;
+    }
+    return out;
+}
+
 Ctx::Ctx(const mmfhe_params &p, int dev, cudaStream_t s) : device(dev), stream(s)
 {
     MMFHE_REQUIRE(p.log_n >= 4 && p.log_n <= 16, MMFHE_E_PARAMS, "log_n must be in [4, 16]");
@@ -135,6 +174,7 @@ Ctx::Ctx(const mmfhe_params &p, int dev, cudaStream_t s) : device(dev), stream(s
 Ctx::~Ctx()
 {
     cudaStreamSynchronize(stream);
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
 }
 
 namespace {

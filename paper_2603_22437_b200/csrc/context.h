@@ -43,17 +43,23 @@ class DBuf {
     cudaStream_t s_ = nullptr;
 };
 
-// Ciphertext (npolys = 2, or 3 after a tensor) in the library's NTT form.
+// A batch of `batch` ciphertexts (npolys = 2, or 3 after a tensor) in the
+// library's NTT form, laid out [batch][npolys][level+1][N] contiguously.
 struct DCt {
     DBuf buf;
-    uint64_t *ext = nullptr;  // non-owning view (caller buffer) when set
+    uint64_t *ext = nullptr;  // non-owning view (caller buffer / slice) when set
     uint32_t level = 0;
     uint32_t npolys = 2;
     uint32_t n_slots = 0;
+    uint32_t batch = 1;
+    uint32_t n = 0;  // ring dimension
     double scale = 1.0;
     uint64_t *data() const { return ext ? ext : buf.get(); }
-    uint64_t *poly(uint32_t i, uint32_t n) const { return data() + (size_t)i * (level + 1) * n; }
-    size_t limbs() const { return level + 1; }
+    size_t poly_words() const { return (size_t)(level + 1) * n; }
+    size_t item_words() const { return (size_t)npolys * poly_words(); }
+    uint64_t *item(uint32_t b) const { return data() + (size_t)b * item_words(); }
+    uint64_t *poly(uint32_t i, uint32_t b = 0) const { return item(b) + (size_t)i * poly_words(); }
+    uint32_t rows() const { return batch * npolys * (level + 1); }
 };
 
 struct DKey {
@@ -111,6 +117,19 @@ class Ctx {
     bool auto_encode = false;
     std::vector<std::vector<double>> fc_w, fc_b;  // FC layer weights (row-major) and biases
 
+    // per-kernel CUDA-event profile (bench roofline): events around each launch
+    struct ProfRec {
+        const char *name;
+        cudaEvent_t a, b;
+        double bytes;
+    };
+    bool prof_on = false;
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    cudaEvent_t next_event();
+    std::string profile_report();  // "name count total_ms bytes" lines; resets
+
     // trace (Theorem P:999-1006)
     bool trace_on = true;
     std::vector<std::string> trace;
@@ -133,10 +152,34 @@ class Ctx {
 
 std::string plain_key(const std::string &name, uint32_t level);
 
+// Records CUDA events around one kernel launch when the ctx profiler is on.
+class ProfScope {
+  public:
+    ProfScope(Ctx &c, const char *name, double bytes) : c_(c), name_(name), bytes_(bytes)
+    {
+        if (c_.prof_on) {
+            a_ = c_.next_event();
+            cudaEventRecord(a_, c_.stream);
+        }
+    }
+    ~ProfScope()
+    {
+        if (c_.prof_on) {
+            cudaEvent_t b = c_.next_event();
+            cudaEventRecord(b, c_.stream);
+            c_.prof.push_back({name_, a_, b, bytes_});
+        }
+    }
+
+  private:
+    Ctx &c_;
+    const char *name_;
+    double bytes_;
+    cudaEvent_t a_ = nullptr;
+};
+
 // ------------------------------------------------------------------ kernels (launchers)
-void ntt_forward(const KTables &kt, uint64_t *d, uint32_t rows, const PrimeMap &pm, cudaStream_t s,
-                 uint64_t &launches);
-void ntt_inverse(const KTables &kt, uint64_t *d, uint32_t rows, const PrimeMap &pm, cudaStream_t s,
-                 uint64_t &launches);
+void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm);
+void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm);
 
 }  // namespace mmfhe

@@ -1,4 +1,4 @@
-// eval.cu -- host orchestration of the CKKS evaluator ops on the ctx stream.
+// eval.cu -- host orchestration of the batched CKKS evaluator ops on the ctx stream.
 #include <algorithm>
 #include <cmath>
 
@@ -13,27 +13,82 @@ void memcpy_d2d(Ctx &c, uint64_t *dst, const uint64_t *src, size_t words)
 {
     CUDA_CHECK(cudaMemcpyAsync(dst, src, words * 8, cudaMemcpyDeviceToDevice, c.stream));
 }
+
+void rec_n(Ctx &c, const char *op, uint32_t level, uint32_t times, const std::string &arg = "")
+{
+    for (uint32_t i = 0; i < times; ++i) c.rec(op, level, arg);
+}
 }  // namespace
 
-DCt make_ct(Ctx &c, uint32_t level, uint32_t npolys, uint32_t n_slots, double scale)
+DCt make_ct(Ctx &c, uint32_t level, uint32_t npolys, uint32_t n_slots, double scale, uint32_t batch)
 {
     DCt r;
-    r.buf = DBuf((size_t)npolys * (level + 1) * c.n, c.stream);
+    r.n = c.n;
     r.level = level;
     r.npolys = npolys;
     r.n_slots = n_slots;
     r.scale = scale;
+    r.batch = batch;
+    r.buf = DBuf(r.item_words() * batch, c.stream);
     return r;
 }
 
-DCt view_ct(const mmfhe_ct &ct, uint32_t npolys)
+DCt view_ct(const Ctx &c, const mmfhe_ct &ct, uint32_t npolys)
 {
     DCt r;
     r.ext = ct.data;
+    r.n = c.n;
     r.level = ct.level;
     r.npolys = npolys;
     r.n_slots = ct.n_slots;
     r.scale = ct.scale;
+    r.batch = 1;
+    return r;
+}
+
+DCt slice(const DCt &a, uint32_t start, uint32_t count)
+{
+    MMFHE_REQUIRE(start + count <= a.batch, MMFHE_E_LAYOUT, "slice out of range");
+    DCt r;
+    r.ext = a.item(start);
+    r.n = a.n;
+    r.level = a.level;
+    r.npolys = a.npolys;
+    r.n_slots = a.n_slots;
+    r.scale = a.scale;
+    r.batch = count;
+    return r;
+}
+
+DCt copy_ct(Ctx &c, const DCt &a)
+{
+    DCt r = make_ct(c, a.level, a.npolys, a.n_slots, a.scale, a.batch);
+    memcpy_d2d(c, r.data(), a.data(), a.item_words() * a.batch);
+    return r;
+}
+
+DCt import_batch(Ctx &c, const mmfhe_ct *cts, size_t first, size_t step, size_t count)
+{
+    MMFHE_REQUIRE(count >= 1, MMFHE_E_SHAPE, "empty batch");
+    const mmfhe_ct &c0 = cts[first];
+    for (size_t i = 0; i < count; ++i) {
+        const mmfhe_ct &x = cts[first + i * step];
+        MMFHE_REQUIRE(x.data != nullptr, MMFHE_E_INVALID_ARG, "null ciphertext data");
+        MMFHE_REQUIRE(x.log_n == c.log_n, MMFHE_E_PARAMS, "ring dimension mismatch");
+        MMFHE_REQUIRE(x.level <= c.L, MMFHE_E_DEPTH, "level above the chain");
+        MMFHE_REQUIRE(x.form == c0.form && (x.form == MMFHE_FORM_COEFF || x.form == MMFHE_FORM_EVAL),
+                      MMFHE_E_FORMAT, "bad or mixed form");
+        MMFHE_REQUIRE(x.level == c0.level && x.scale == c0.scale, MMFHE_E_SCALE, "inputs must share level and scale");
+        MMFHE_REQUIRE((x.n_polys ? x.n_polys : 2) == 2, MMFHE_E_LAYOUT, "chain inputs are 2-poly ciphertexts");
+    }
+    DCt r = make_ct(c, c0.level, 2, c0.n_slots, c0.scale, (uint32_t)count);
+    const size_t words = r.item_words();
+    for (size_t i = 0; i < count; ++i) {
+        const mmfhe_ct &x = cts[first + i * step];
+        CUDA_CHECK(cudaMemcpyAsync(r.item((uint32_t)i), x.data, words * 8,
+                                   x.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    }
+    if (c0.form == MMFHE_FORM_COEFF) ntt_forward(c, r.data(), r.rows(), qmap(c, c0.level));
     return r;
 }
 
@@ -44,19 +99,18 @@ DCt import_ct(Ctx &c, const mmfhe_ct &in, uint32_t npolys)
     MMFHE_REQUIRE(in.level <= c.L, MMFHE_E_DEPTH, "level above the chain");
     MMFHE_REQUIRE(in.form == MMFHE_FORM_COEFF || in.form == MMFHE_FORM_EVAL, MMFHE_E_FORMAT, "bad form");
     DCt r = make_ct(c, in.level, npolys, in.n_slots, in.scale);
-    const size_t words = (size_t)npolys * (in.level + 1) * c.n;
-    CUDA_CHECK(cudaMemcpyAsync(r.data(), in.data, words * 8,
+    CUDA_CHECK(cudaMemcpyAsync(r.data(), in.data, r.item_words() * 8,
                                in.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
-    if (in.form == MMFHE_FORM_COEFF)
-        ntt_forward(c.kt, r.data(), npolys * (in.level + 1), qmap(c, in.level), c.stream, c.launches);
+    if (in.form == MMFHE_FORM_COEFF) ntt_forward(c, r.data(), r.rows(), qmap(c, in.level));
     return r;
 }
 
 void export_ct(Ctx &c, const DCt &in, mmfhe_ct &out)
 {
     MMFHE_REQUIRE(out.data != nullptr, MMFHE_E_INVALID_ARG, "null output buffer");
-    const uint32_t rows = in.npolys * (in.level + 1);
-    const size_t words = (size_t)rows * c.n;
+    MMFHE_REQUIRE(in.batch == 1, MMFHE_E_LAYOUT, "export one ciphertext at a time");
+    const uint32_t rows = in.rows();
+    const size_t words = in.item_words();
     out.log_n = c.log_n;
     out.level = in.level;
     out.scale = in.scale;
@@ -64,11 +118,11 @@ void export_ct(Ctx &c, const DCt &in, mmfhe_ct &out)
     out.n_polys = in.npolys;
     if (out.on_device) {
         memcpy_d2d(c, out.data, in.data(), words);
-        if (out.form == MMFHE_FORM_COEFF) ntt_inverse(c.kt, out.data, rows, qmap(c, in.level), c.stream, c.launches);
+        if (out.form == MMFHE_FORM_COEFF) ntt_inverse(c, out.data, rows, qmap(c, in.level));
     } else {
         DBuf tmp(words, c.stream);
         memcpy_d2d(c, tmp.get(), in.data(), words);
-        if (out.form == MMFHE_FORM_COEFF) ntt_inverse(c.kt, tmp.get(), rows, qmap(c, in.level), c.stream, c.launches);
+        if (out.form == MMFHE_FORM_COEFF) ntt_inverse(c, tmp.get(), rows, qmap(c, in.level));
         CUDA_CHECK(cudaMemcpyAsync(out.data, tmp.get(), words * 8, cudaMemcpyDeviceToHost, c.stream));
         CUDA_CHECK(cudaStreamSynchronize(c.stream));
     }
@@ -77,11 +131,12 @@ void export_ct(Ctx &c, const DCt &in, mmfhe_ct &out)
 // ------------------------------------------------------------------ exact ops
 DCt ev_addsub(Ctx &c, const DCt &a, const DCt &b, bool sub)
 {
-    MMFHE_REQUIRE(a.level == b.level && a.npolys == b.npolys, MMFHE_E_LAYOUT, "hadd level/size mismatch");
+    MMFHE_REQUIRE(a.level == b.level && a.npolys == b.npolys && a.batch == b.batch, MMFHE_E_LAYOUT,
+                  "hadd level/size mismatch");
     MMFHE_REQUIRE(a.scale == b.scale, MMFHE_E_SCALE, "hadd scale mismatch");
-    c.rec(sub ? "hsub" : "hadd", a.level);
-    DCt r = make_ct(c, a.level, a.npolys, a.n_slots, a.scale);
-    launch_addsub(c, r.data(), a.data(), b.data(), a.npolys * (a.level + 1), qmap(c, a.level), sub);
+    rec_n(c, sub ? "hsub" : "hadd", a.level, a.batch);
+    DCt r = make_ct(c, a.level, a.npolys, a.n_slots, a.scale, a.batch);
+    launch_addsub(c, r.data(), a.data(), b.data(), a.rows(), qmap(c, a.level), sub);
     return r;
 }
 
@@ -89,25 +144,33 @@ DCt ev_sum(Ctx &c, const std::vector<const DCt *> &cts)
 {
     MMFHE_REQUIRE(!cts.empty(), MMFHE_E_INVALID_ARG, "empty sum");
     const DCt &a0 = *cts[0];
-    DCt r = make_ct(c, a0.level, a0.npolys, a0.n_slots, a0.scale);
-    memcpy_d2d(c, r.data(), a0.data(), (size_t)a0.npolys * (a0.level + 1) * c.n);
+    DCt r = copy_ct(c, a0);
     for (size_t i = 1; i < cts.size(); ++i) {
         const DCt &b = *cts[i];
-        MMFHE_REQUIRE(b.level == a0.level && b.npolys == a0.npolys, MMFHE_E_LAYOUT, "sum level mismatch");
+        MMFHE_REQUIRE(b.level == a0.level && b.npolys == a0.npolys && b.batch == a0.batch, MMFHE_E_LAYOUT,
+                      "sum level mismatch");
         MMFHE_REQUIRE(b.scale == a0.scale, MMFHE_E_SCALE, "sum scale mismatch");
-        c.rec("hadd", a0.level);
-        launch_addsub(c, r.data(), r.data(), b.data(), a0.npolys * (a0.level + 1), qmap(c, a0.level), false);
+        rec_n(c, "hadd", a0.level, a0.batch);
+        launch_addsub(c, r.data(), r.data(), b.data(), a0.rows(), qmap(c, a0.level), false);
     }
+    return r;
+}
+
+DCt ev_batch_sum(Ctx &c, const DCt &a)
+{
+    rec_n(c, "hadd", a.level, a.batch - 1);
+    DCt r = make_ct(c, a.level, a.npolys, a.n_slots, a.scale, 1);
+    launch_batch_sum(c, r.data(), a.data(), a.batch, a.npolys, a.level);
     return r;
 }
 
 DCt ev_drop_to(Ctx &c, const DCt &a, uint32_t level)
 {
     MMFHE_REQUIRE(level <= a.level, MMFHE_E_DEPTH, "cannot raise a level");
-    DCt r = make_ct(c, level, a.npolys, a.n_slots, a.scale);
-    if (level != a.level) c.rec("modswitch", a.level, std::to_string(level));
-    CUDA_CHECK(cudaMemcpy2DAsync(r.data(), (size_t)(level + 1) * c.n * 8, a.data(), (size_t)(a.level + 1) * c.n * 8,
-                                 (size_t)(level + 1) * c.n * 8, a.npolys, cudaMemcpyDeviceToDevice, c.stream));
+    DCt r = make_ct(c, level, a.npolys, a.n_slots, a.scale, a.batch);
+    if (level != a.level) rec_n(c, "modswitch", a.level, a.batch, std::to_string(level));
+    CUDA_CHECK(cudaMemcpy2DAsync(r.data(), r.poly_words() * 8, a.data(), a.poly_words() * 8, r.poly_words() * 8,
+                                 (size_t)a.npolys * a.batch, cudaMemcpyDeviceToDevice, c.stream));
     return r;
 }
 
@@ -117,13 +180,14 @@ DCt ev_tensor_sum(Ctx &c, const std::vector<std::pair<const DCt *, const DCt *>>
     const DCt &a0 = *pairs[0].first;
     const double sc = a0.scale * pairs[0].second->scale;
     for (auto &pr : pairs) {
-        MMFHE_REQUIRE(pr.first->level == a0.level && pr.second->level == a0.level, MMFHE_E_LAYOUT,
-                      "tensor level mismatch");
-        MMFHE_REQUIRE(pr.first->npolys == 2 && pr.second->npolys == 2, MMFHE_E_LAYOUT, "tensor needs 2-poly cts");
+        for (const DCt *x : {pr.first, pr.second}) {
+            MMFHE_REQUIRE(x->level == a0.level && x->batch == a0.batch, MMFHE_E_LAYOUT, "tensor level/batch mismatch");
+            MMFHE_REQUIRE(x->npolys == 2, MMFHE_E_LAYOUT, "tensor needs 2-poly cts");
+        }
         MMFHE_REQUIRE(pr.first->scale * pr.second->scale == sc, MMFHE_E_SCALE, "tensor_sum scale mismatch");
     }
-    c.rec("tensor_sum", a0.level, std::to_string(pairs.size()));
-    DCt r = make_ct(c, a0.level, 3, a0.n_slots, sc);
+    rec_n(c, "tensor_sum", a0.level, a0.batch, std::to_string(pairs.size()));
+    DCt r = make_ct(c, a0.level, 3, a0.n_slots, sc, a0.batch);
     for (size_t s = 0; s < pairs.size(); s += kMaxTerms) {
         PtrList A{}, B{};
         int n = (int)std::min<size_t>(kMaxTerms, pairs.size() - s);
@@ -131,7 +195,7 @@ DCt ev_tensor_sum(Ctx &c, const std::vector<std::pair<const DCt *, const DCt *>>
             A.p[i] = pairs[s + i].first->data();
             B.p[i] = pairs[s + i].second->data();
         }
-        launch_tensor_sum(c, r.data(), A, B, n, a0.level, s > 0);
+        launch_tensor_sum(c, r.data(), r.item_words(), A, B, a0.item_words(), n, a0.level, s > 0, a0.batch);
     }
     return r;
 }
@@ -142,12 +206,13 @@ DCt ev_pmult_sum(Ctx &c, const std::vector<std::pair<const DPlain *, const DCt *
     const DCt &a0 = *terms[0].second;
     const double sc = a0.scale * terms[0].first->scale;
     for (auto &t : terms) {
-        MMFHE_REQUIRE(t.second->level == a0.level && t.second->npolys == 2, MMFHE_E_LAYOUT, "pmult level mismatch");
+        MMFHE_REQUIRE(t.second->level == a0.level && t.second->npolys == 2 && t.second->batch == a0.batch,
+                      MMFHE_E_LAYOUT, "pmult level/batch mismatch");
         MMFHE_REQUIRE(t.first->level == a0.level, MMFHE_E_LAYOUT, "plaintext level mismatch");
         MMFHE_REQUIRE(t.second->scale * t.first->scale == sc, MMFHE_E_SCALE, "pmult_sum scale mismatch");
     }
-    c.rec("pmult_sum", a0.level, std::to_string(terms.size()));
-    DCt r = make_ct(c, a0.level, 2, a0.n_slots, sc);
+    rec_n(c, "pmult_sum", a0.level, a0.batch, std::to_string(terms.size()));
+    DCt r = make_ct(c, a0.level, 2, a0.n_slots, sc, a0.batch);
     for (size_t s = 0; s < terms.size(); s += kMaxTerms) {
         PtrList P{}, C{};
         int n = (int)std::min<size_t>(kMaxTerms, terms.size() - s);
@@ -155,23 +220,23 @@ DCt ev_pmult_sum(Ctx &c, const std::vector<std::pair<const DPlain *, const DCt *
             P.p[i] = terms[s + i].first->buf.get();
             C.p[i] = terms[s + i].second->data();
         }
-        launch_pmult_sum(c, r.data(), P, C, n, a0.level, s > 0);
+        launch_pmult_sum(c, r.data(), r.item_words(), P, C, a0.item_words(), n, a0.level, s > 0, a0.batch);
     }
     return r;
 }
 
 uint64_t encode_scalar_mod(double v, uint64_t q_scale, uint64_t m)
 {
-    // v = mant * 2^e exactly with |mant| < 2^53; x = v * q_scale = mant * q_scale * 2^e;
-    // round half away from zero, exactly, in 128-bit integers.
+    // v = mant * 2^e exactly with mant < 2^53; |x| = mant * q_scale * 2^e rounded
+    // half away from zero, exactly, in 128-bit integers.
     typedef unsigned __int128 u128;
     if (v == 0.0) return 0;
     MMFHE_REQUIRE(std::isfinite(v), MMFHE_E_INVALID_ARG, "non-finite scalar");
     int e;
-    double f = std::frexp(std::fabs(v), &e);           // |v| = f * 2^e, f in [0.5, 1)
-    uint64_t mant = (uint64_t)std::ldexp(f, 53);       // exact
-    e -= 53;                                           // |v| = mant * 2^e
-    u128 prod = (u128)mant * q_scale;                  // < 2^113
+    double f = std::frexp(std::fabs(v), &e);  // |v| = f * 2^e, f in [0.5, 1)
+    uint64_t mant = (uint64_t)std::ldexp(f, 53);
+    e -= 53;
+    u128 prod = (u128)mant * q_scale;  // < 2^113
     u128 mag;
     if (e >= 0) {
         MMFHE_REQUIRE(e < 14, MMFHE_E_SCALE, "scalar constant overflows the encoding");
@@ -180,31 +245,36 @@ uint64_t encode_scalar_mod(double v, uint64_t q_scale, uint64_t m)
         mag = 0;
     } else {
         u128 half = (u128)1 << (-e - 1);
-        mag = (prod + half) >> (-e);                   // ties away from zero (on |x|)
+        mag = (prod + half) >> (-e);
     }
     uint64_t r = (uint64_t)(mag % m);
     return (v < 0 && r) ? m - r : r;
 }
 
-DCt ev_lincomb(Ctx &c, const std::vector<const DCt *> &cts, const std::vector<double> &coefs)
+DCt ev_lincomb_mat(Ctx &c, const DCt &in, uint32_t J, uint32_t W, int lo0, int lo_step,
+                   const std::vector<double> &coef)
 {
-    MMFHE_REQUIRE(!cts.empty() && cts.size() == coefs.size(), MMFHE_E_INVALID_ARG, "lincomb size");
-    const DCt &a0 = *cts[0];
-    for (auto *ct : cts)
-        MMFHE_REQUIRE(ct->level == a0.level && ct->scale == a0.scale && ct->npolys == 2, MMFHE_E_SCALE,
-                      "lincomb operands must share level and scale");
-    c.rec("lincomb", a0.level, std::to_string(cts.size()));
-    const uint32_t l = a0.level;
+    MMFHE_REQUIRE(in.npolys == 2 && J >= 1 && W >= 1 && coef.size() == (size_t)J * W, MMFHE_E_SHAPE,
+                  "lincomb matrix shape");
+    const uint32_t l = in.level, M = in.batch;
     const uint64_t ql = c.primes[l];
-    // constant table [n][l+1] of Shoup pairs, cached by content
-    std::string key = std::to_string(l) + ":";
-    key.append((const char *)coefs.data(), coefs.size() * sizeof(double));
+    for (uint32_t j = 0; j < J; ++j) {
+        int cnt = 0;
+        for (uint32_t w = 0; w < W; ++w) {
+            const int i = lo0 + (int)j * lo_step + (int)w;
+            cnt += (i >= 0 && i < (int)M);
+        }
+        MMFHE_REQUIRE(cnt > 0, MMFHE_E_SHAPE, "lincomb output without inputs");
+        c.rec("lincomb", l, std::to_string(cnt));
+    }
+    std::string key = "mat:" + std::to_string(l) + ":" + std::to_string(J) + ":" + std::to_string(W) + ":";
+    key.append((const char *)coef.data(), coef.size() * sizeof(double));
     auto it = c.const_cache.find(key);
     if (it == c.const_cache.end()) {
-        std::vector<TwPair> tab(coefs.size() * (l + 1));
-        for (size_t t = 0; t < coefs.size(); ++t)
+        std::vector<TwPair> tab(coef.size() * (l + 1));
+        for (size_t t = 0; t < coef.size(); ++t)
             for (uint32_t i = 0; i <= l; ++i) {
-                uint64_t v = encode_scalar_mod(coefs[t], ql, c.primes[i]);
+                uint64_t v = encode_scalar_mod(coef[t], ql, c.primes[i]);
                 tab[t * (l + 1) + i] = {v, host::shoup(v, c.primes[i])};
             }
         DBuf b((tab.size() * sizeof(TwPair) + 7) / 8, c.stream);
@@ -213,37 +283,31 @@ DCt ev_lincomb(Ctx &c, const std::vector<const DCt *> &cts, const std::vector<do
         CUDA_CHECK(cudaStreamSynchronize(c.stream));
         it = c.const_cache.emplace(key, std::move(b)).first;
     }
-    const TwPair *consts = (const TwPair *)it->second.get();
-    DCt r = make_ct(c, l, 2, a0.n_slots, a0.scale * (double)ql);
-    for (size_t s = 0; s < cts.size(); s += kMaxTerms) {
-        PtrList C{};
-        int n = (int)std::min<size_t>(kMaxTerms, cts.size() - s);
-        for (int i = 0; i < n; ++i) C.p[i] = cts[s + i]->data();
-        launch_lincomb(c, r.data(), C, consts + s * (l + 1), n, l, s > 0);
-    }
+    DCt r = make_ct(c, l, 2, in.n_slots, in.scale * (double)ql, J);
+    launch_lincomb_mat(c, r.data(), in.data(), M, J, W, lo0, lo_step, (const TwPair *)it->second.get(), l);
     return r;
 }
 
 DCt ev_add_plain(Ctx &c, const DCt &a, const DPlain &pt)
 {
-    MMFHE_REQUIRE(pt.level == a.level, MMFHE_E_LAYOUT, "plaintext level mismatch");
+    MMFHE_REQUIRE(pt.level == a.level && a.npolys == 2, MMFHE_E_LAYOUT, "plaintext level mismatch");
     MMFHE_REQUIRE(pt.scale == a.scale, MMFHE_E_SCALE, "add_plain scale mismatch");
-    c.rec("add_plain", a.level);
-    DCt r = make_ct(c, a.level, 2, a.n_slots, a.scale);
-    memcpy_d2d(c, r.data(), a.data(), (size_t)2 * (a.level + 1) * c.n);
-    launch_add_plain(c, r.data(), pt.buf.get(), a.level);
+    rec_n(c, "add_plain", a.level, a.batch);
+    DCt r = copy_ct(c, a);
+    launch_add_plain(c, r.data(), r.item_words(), pt.buf.get(), a.level, a.batch);
     return r;
 }
 
 // ------------------------------------------------------------------ key switching
-void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, uint32_t l, const DKey &key, uint64_t *out0, uint64_t *out1,
-                  const uint64_t *add0, const uint64_t *add1)
+void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t B, const DKey &key,
+                  uint64_t *out, size_t os, const uint64_t *add, size_t as, bool add_poly1)
 {
     const size_t N = c.n;
-    // 1. coefficient form of x
-    DBuf xc((size_t)(l + 1) * N, c.stream);
-    memcpy_d2d(c, xc.get(), x_ntt, (size_t)(l + 1) * N);
-    ntt_inverse(c.kt, xc.get(), l + 1, qmap(c, l), c.stream, c.launches);
+    const size_t lw = (size_t)(l + 1) * N;
+    // 1. coefficient form of every x_b
+    DBuf xc(B * lw, c.stream);
+    CUDA_CHECK(cudaMemcpy2DAsync(xc.get(), lw * 8, x_ntt, xs * 8, lw * 8, B, cudaMemcpyDeviceToDevice, c.stream));
+    ntt_inverse(c, xc.get(), B * (l + 1), qmap(c, l));
     // 2. ModUp: fast BConv of every digit, then NTT of the converted rows
     const auto &plans = c.modup[l];
     std::vector<size_t> off;
@@ -256,30 +320,30 @@ void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, uint32_t l, const DKey &key, ui
             if (r < p.lo || r >= p.hi) rowmap.push_back(basis[r]);
         T += p.n_tgt;
     }
-    DBuf y(T * N, c.stream);
-    launch_modup_bconv(c, y.get(), xc.get(), l, off);
-    ntt_forward(c.kt, y.get(), (uint32_t)T, make_map(rowmap), c.stream, c.launches);
-    // 3. key inner product (evk streamed once)
-    DBuf accQ((size_t)2 * (l + 1) * N, c.stream), accP((size_t)2 * c.K * N, c.stream);
-    launch_key_ip(c, accQ.get(), accP.get(), x_ntt, y.get(), off, key.buf.get(), l);
+    DBuf y(B * T * N, c.stream);
+    launch_modup_bconv(c, y.get(), T * N, xc.get(), lw, l, off, B);
+    ntt_forward(c, y.get(), (uint32_t)(B * T), make_map(rowmap));
+    // 3. key inner product (each evk word fetched once for the batch)
+    DBuf accQ(B * 2 * lw, c.stream), accP(B * 2 * c.K * N, c.stream);
+    launch_key_ip(c, accQ.get(), accP.get(), x_ntt, xs, y.get(), T * N, off, key.buf.get(), l, B);
     // 4. ModDown
     std::vector<uint32_t> pm;
     for (uint32_t k = 0; k < c.K; ++k) pm.push_back(c.L + 1 + k);
-    ntt_inverse(c.kt, accP.get(), 2 * c.K, make_map(pm), c.stream, c.launches);
-    DBuf w((size_t)2 * (l + 1) * N, c.stream);
-    launch_moddown_bconv(c, w.get(), accP.get(), l);
-    ntt_forward(c.kt, w.get(), 2 * (l + 1), qmap(c, l), c.stream, c.launches);
-    launch_moddown_final(c, out0, out1, accQ.get(), w.get(), add0, add1, l);
+    ntt_inverse(c, accP.get(), B * 2 * c.K, make_map(pm));
+    DBuf w(B * 2 * lw, c.stream);
+    launch_moddown_bconv(c, w.get(), accP.get(), l, B);
+    ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l));
+    launch_moddown_final(c, out, os, accQ.get(), w.get(), add, as, add_poly1, l, B);
 }
 
 DCt ev_relin(Ctx &c, const DCt &a3)
 {
     MMFHE_REQUIRE(a3.npolys == 3, MMFHE_E_LAYOUT, "relin needs a 3-poly ciphertext");
     MMFHE_REQUIRE(c.rlk != nullptr, MMFHE_E_MISSING_KEY, "missing relinearisation key");
-    c.rec("relin", a3.level);
-    DCt r = make_ct(c, a3.level, 2, a3.n_slots, a3.scale);
-    ev_keyswitch(c, a3.poly(2, c.n), a3.level, *c.rlk, r.poly(0, c.n), r.poly(1, c.n), a3.poly(0, c.n),
-                 a3.poly(1, c.n));
+    rec_n(c, "relin", a3.level, a3.batch);
+    DCt r = make_ct(c, a3.level, 2, a3.n_slots, a3.scale, a3.batch);
+    ev_keyswitch(c, a3.poly(2), a3.item_words(), a3.level, a3.batch, *c.rlk, r.data(), r.item_words(), a3.data(),
+                 a3.item_words(), true);
     return r;
 }
 
@@ -303,17 +367,14 @@ DCt ev_rotate(Ctx &c, const DCt &a, int32_t step)
     MMFHE_REQUIRE(a.npolys == 2, MMFHE_E_LAYOUT, "rotate needs a 2-poly ciphertext");
     int32_t k;
     const uint64_t g = galois_element(c, step, &k);
-    DCt r = make_ct(c, a.level, 2, a.n_slots, a.scale);
-    if (k == 0) {
-        memcpy_d2d(c, r.data(), a.data(), (size_t)2 * (a.level + 1) * c.n);
-        return r;
-    }
+    if (k == 0) return copy_ct(c, a);
     const DKey &key = find_gk(c, k);
-    c.rec("hrot", a.level, std::to_string(k));
-    DBuf sig((size_t)2 * (a.level + 1) * c.n, c.stream);
-    launch_automorph(c, sig.get(), a.data(), 2 * (a.level + 1), g);
-    const uint64_t *s0 = sig.get(), *s1 = sig.get() + (size_t)(a.level + 1) * c.n;
-    ev_keyswitch(c, s1, a.level, key, r.poly(0, c.n), r.poly(1, c.n), s0, nullptr);
+    rec_n(c, "hrot", a.level, a.batch, std::to_string(k));
+    DCt r = make_ct(c, a.level, 2, a.n_slots, a.scale, a.batch);
+    DBuf sig(a.item_words() * a.batch, c.stream);
+    launch_automorph(c, sig.get(), a.data(), a.rows(), g);
+    ev_keyswitch(c, sig.get() + a.poly_words(), a.item_words(), a.level, a.batch, key, r.data(), r.item_words(),
+                 sig.get(), a.item_words(), false);
     return r;
 }
 
@@ -321,25 +382,24 @@ DCt ev_rescale(Ctx &c, const DCt &a)
 {
     MMFHE_REQUIRE(a.npolys == 2, MMFHE_E_LAYOUT, "rescale needs a 2-poly ciphertext");
     MMFHE_REQUIRE(a.level >= 1, MMFHE_E_DEPTH, "depth exhausted");
-    const uint32_t l = a.level;
-    c.rec("rescale", l);
+    const uint32_t l = a.level, B = a.batch;
+    rec_n(c, "rescale", l, B);
     const size_t N = c.n;
-    DBuf t(2 * N, c.stream);
-    memcpy_d2d(c, t.get(), a.poly(0, c.n) + (size_t)l * N, N);
-    memcpy_d2d(c, t.get() + N, a.poly(1, c.n) + (size_t)l * N, N);
-    ntt_inverse(c.kt, t.get(), 2, make_map({l}), c.stream, c.launches);
-    DBuf v((size_t)2 * l * N, c.stream);
-    launch_rescale_prep(c, v.get(), t.get(), l);
-    ntt_forward(c.kt, v.get(), 2 * l, qmap(c, l - 1), c.stream, c.launches);
-    DCt r = make_ct(c, l - 1, 2, a.n_slots, a.scale / (double)c.primes[l]);
-    launch_rescale_final(c, r.data(), a.data(), v.get(), l);
+    DBuf t(2 * N * B, c.stream);
+    CUDA_CHECK(cudaMemcpy2DAsync(t.get(), N * 8, a.data() + (size_t)l * N, a.poly_words() * 8, N * 8, 2 * (size_t)B,
+                                 cudaMemcpyDeviceToDevice, c.stream));
+    ntt_inverse(c, t.get(), 2 * B, make_map({l}));
+    DBuf v((size_t)2 * l * N * B, c.stream);
+    launch_rescale_prep(c, v.get(), t.get(), l, B);
+    ntt_forward(c, v.get(), 2 * l * B, qmap(c, l - 1));
+    DCt r = make_ct(c, l - 1, 2, a.n_slots, a.scale / (double)c.primes[l], B);
+    launch_rescale_final(c, r.data(), a.data(), a.item_words(), v.get(), l, B);
     return r;
 }
 
 DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride)
 {
-    DCt acc = make_ct(c, a.level, 2, a.n_slots, a.scale);
-    memcpy_d2d(c, acc.data(), a.data(), (size_t)2 * (a.level + 1) * c.n);
+    DCt acc = copy_ct(c, a);
     uint32_t step = stride;
     for (uint32_t n = 1; n < count; n *= 2, step *= 2) {
         DCt r = ev_rotate(c, acc, (int32_t)step);
@@ -360,7 +420,7 @@ void load_key(Ctx &c, DKey &k, const uint64_t *words, size_t n_words, bool on_de
     for (uint32_t i = 0; i < c.L + 1 + c.K; ++i) all.push_back(i);
     const uint32_t rows = (uint32_t)(n_words / c.n);
     PrimeMap pm = make_map(all);
-    ntt_forward(c.kt, k.buf.get(), rows, pm, c.stream, c.launches);
+    ntt_forward(c, k.buf.get(), rows, pm);
     launch_to_mont(c, k.buf.get(), rows, pm);
 }
 
@@ -375,7 +435,7 @@ void load_plain(Ctx &c, const std::string &name, uint32_t level, double scale, c
     CUDA_CHECK(cudaMemcpyAsync(p->buf.get(), coef, words * 8,
                                on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
     PrimeMap pm = qmap(c, level);
-    ntt_forward(c.kt, p->buf.get(), level + 1, pm, c.stream, c.launches);
+    ntt_forward(c, p->buf.get(), level + 1, pm);
     launch_to_mont(c, p->buf.get(), level + 1, pm);
     c.plains[plain_key(name, level)] = std::move(p);
 }

@@ -1,10 +1,12 @@
-// eval.h -- the CKKS evaluator over device ciphertexts (NTT form).
+// eval.h -- the CKKS evaluator over batches of device ciphertexts (NTT form).
 //
 // Semantics follow the pinned operations of SURVEY §8(c)-4..6 (exact ring ops,
 // round-half-up rescale, hybrid key switching without BConv correction,
-// automorphism-first HRot, lazy relinearisation, exact scale bookkeeping);
-// each call records one logical op in the ctx trace.
+// automorphism-first HRot, lazy relinearisation, exact scale bookkeeping).
+// Every op works on a batch of B ciphertexts in one set of launches and records
+// one logical op per item in the ctx trace (item order).
 #pragma once
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -12,25 +14,34 @@
 
 namespace mmfhe {
 
-DCt make_ct(Ctx &c, uint32_t level, uint32_t npolys, uint32_t n_slots, double scale);
-DCt view_ct(const mmfhe_ct &ct, uint32_t npolys);  // non-owning device NTT-form view
+DCt make_ct(Ctx &c, uint32_t level, uint32_t npolys, uint32_t n_slots, double scale, uint32_t batch = 1);
+DCt view_ct(const Ctx &c, const mmfhe_ct &ct, uint32_t npolys);  // non-owning device NTT-form view
+DCt slice(const DCt &a, uint32_t start, uint32_t count);           // non-owning items [start, start+count)
+DCt copy_ct(Ctx &c, const DCt &a);
 
-// ABI boundary: coefficient/NTT form, host/device.
+// ABI boundary: coefficient/NTT form, host/device.  import_batch gathers
+// cts[first + i*step], i < count, into one contiguous batch.
 DCt import_ct(Ctx &c, const mmfhe_ct &in, uint32_t npolys);
-void export_ct(Ctx &c, const DCt &in, mmfhe_ct &out);
+DCt import_batch(Ctx &c, const mmfhe_ct *cts, size_t first, size_t step, size_t count);
+void export_ct(Ctx &c, const DCt &in, mmfhe_ct &out);  // in.batch == 1
 
-// exact ops
+// exact ops (batched)
 DCt ev_addsub(Ctx &c, const DCt &a, const DCt &b, bool sub);
 DCt ev_drop_to(Ctx &c, const DCt &a, uint32_t level);
 DCt ev_tensor_sum(Ctx &c, const std::vector<std::pair<const DCt *, const DCt *>> &pairs);
 DCt ev_pmult_sum(Ctx &c, const std::vector<std::pair<const DPlain *, const DCt *>> &terms);
-DCt ev_lincomb(Ctx &c, const std::vector<const DCt *> &cts, const std::vector<double> &coefs);
-DCt ev_add_plain(Ctx &c, const DCt &a, const DPlain &pt);
+// sum of all items of a batch (frame accumulation, depth 0)
+DCt ev_batch_sum(Ctx &c, const DCt &a);
 DCt ev_sum(Ctx &c, const std::vector<const DCt *> &cts);
+DCt ev_add_plain(Ctx &c, const DCt &a, const DPlain &pt);
+// Scalar linear maps over a batch (CK10): out[j] = sum_{w<W} coef[j][w] in[lo0 + j*lo_step + w]
+// (inputs outside [0, M) contribute nothing); coef row-major [J][W]; exact scalar encoding at q_l.
+DCt ev_lincomb_mat(Ctx &c, const DCt &in, uint32_t J, uint32_t W, int lo0, int lo_step,
+                   const std::vector<double> &coef);
 
-// key switching family
-void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, uint32_t level, const DKey &key, uint64_t *out0, uint64_t *out1,
-                  const uint64_t *add0, const uint64_t *add1);
+// key switching family (batched)
+void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t level, uint32_t B, const DKey &key,
+                  uint64_t *out, size_t os, const uint64_t *add, size_t as, bool add_poly1);
 DCt ev_relin(Ctx &c, const DCt &a3);
 DCt ev_rotate(Ctx &c, const DCt &a, int32_t step);
 DCt ev_rescale(Ctx &c, const DCt &a);
@@ -38,10 +49,7 @@ DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride);
 
 // composites
 inline DCt ev_relin_rescale(Ctx &c, const DCt &a3) { return ev_rescale(c, ev_relin(c, a3)); }
-inline DCt ev_square_rescale(Ctx &c, const DCt &a)
-{
-    return ev_relin_rescale(c, ev_tensor_sum(c, {{&a, &a}}));
-}
+inline DCt ev_square_rescale(Ctx &c, const DCt &a) { return ev_relin_rescale(c, ev_tensor_sum(c, {{&a, &a}})); }
 
 uint64_t galois_element(const Ctx &c, int32_t step, int32_t *normalised);
 const DKey &find_gk(const Ctx &c, int32_t step_norm);
@@ -54,7 +62,7 @@ void load_plain(Ctx &c, const std::string &name, uint32_t level, double scale, c
 // host encoder (canonical embedding), csrc/encoder.cpp
 std::vector<int64_t> encode_real(const Ctx &c, const std::vector<double> &v, double scale);
 void encode_plain(Ctx &c, const std::string &name, const std::vector<double> &v, uint32_t level, double scale);
-// exact round-half-away(v * q) as a signed 128-bit integer reduced mod m
+// exact round-half-away(v * q_scale) reduced mod m
 uint64_t encode_scalar_mod(double v, uint64_t q_scale, uint64_t m);
 
 }  // namespace mmfhe

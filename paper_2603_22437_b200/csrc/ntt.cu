@@ -6,24 +6,27 @@
 // Inverse: Gentleman-Sande with psi^{-bitrev}, bit-reversed in, natural out,
 // times N^{-1}.  Harvey lazy butterflies: values stay in [0, 4q) (q < 2^60).
 //
-// B200 mapping: a limb of N = 2^16 words (512 KiB) does not fit one SM's
-// shared memory, so the transform runs as two passes over HBM:
-//   pass "col"  -- the first L1 stages on 2^L2 columns of 2^L1 strided words
-//                  (G consecutive columns per CTA -> coalesced G*8-byte runs);
-//   pass "row"  -- the last L2 stages on contiguous blocks of 2^L2 words.
-// Each pass stages its tile in shared memory and runs the stages there; all
-// limbs of all polynomials of a batch go in one launch (grid.y = rows).
+// B200 mapping.  A limb of N = 2^16 words (512 KiB) exceeds one SM's shared
+// memory, so the transform is two passes over HBM (logN = L1 + L2):
+//   col pass -- stages 0..L1-1 on 2^L2 strided columns of 2^L1 words; a warp
+//               spans G consecutive columns (G*8-byte sector-aligned runs);
+//   row pass -- stages L1..logN-1 on contiguous blocks of 2^L2 words; one warp
+//               per block, consecutive lanes on consecutive words.
+// Inside a pass each thread holds E = 2^ELOG = 8 words in registers and runs
+// ELOG butterfly stages there (radix-8); rounds exchange data through
+// double-buffered shared memory (one __syncthreads per exchange).  All index
+// arithmetic is shifts/masks of compile-time widths.  Every limb of every
+// polynomial of a batch goes in one launch (grid.y = rows, prime per row).
 #include <algorithm>
 
-#include "common.h"
+#include "context.h"
 #include "modarith.cuh"
 
 namespace mmfhe {
 
 namespace {
 
-constexpr int kTileWords = 4096;  // 32 KiB of shared memory per CTA
-constexpr int kThreads = 256;
+constexpr int kCtaThreads = 256;
 
 __device__ __forceinline__ uint64_t reduce4q(uint64_t x, uint64_t q)
 {
@@ -31,203 +34,240 @@ __device__ __forceinline__ uint64_t reduce4q(uint64_t x, uint64_t q)
     return x >= q ? x - q : x;
 }
 
-// ---------------------------------------------------------------- forward
-// Columns: element (k, c) at a[(k << L2) + c], k < 2^LOGS; stages 0..LOGS-1.
-template <int LOGS>
-__global__ void __launch_bounds__(kThreads) ntt_fwd_col(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
-                                                         int G)
+// Local index of register e of thread t in a round that owns bits [lo, lo+w):
+// y = top w bits of e -> bits lo..lo+w-1; z = (t, low ELOG-w bits of e) fills
+// the free bit positions [0, lo) and [lo+w, LOGS) in ascending order.
+template <int ELOG>
+__device__ __forceinline__ int kmap(int lo, int w, int t, int e)
 {
-    constexpr int S = 1 << LOGS;
-    extern __shared__ uint64_t sm[];
-    const int row = blockIdx.y;
-    const int p = pm.idx[row % pm.period];
-    const uint64_t q = kt.q[p];
-    const uint64_t q2 = 2 * q;
-    const TwPair *tw = kt.tw_fwd + (size_t)p * kt.n;
-    uint64_t *a = data + (size_t)row * kt.n;
-    const int L2 = kt.log_n - LOGS;
-    const int c0 = blockIdx.x * G;
-    const int tot = S * G;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        int k = e / G, cc = e - k * G;
-        sm[e] = a[((size_t)k << L2) + c0 + cc];
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int l = 0; l < LOGS; ++l) {
-        const int half = S >> (l + 1);
-        for (int b = threadIdx.x; b < (S / 2) * G; b += blockDim.x) {
-            int pi = b / G, cc = b - pi * G;
-            int grp = pi / half, off = pi - grp * half;
-            int k = grp * 2 * half + off;
-            TwPair w = tw[(1 << l) + grp];
-            uint64_t U = sm[k * G + cc];
-            uint64_t V = sm[(k + half) * G + cc];
-            U = U >= q2 ? U - q2 : U;
-            V = shoup_lazy(V, w.w, w.wp, q);
-            sm[k * G + cc] = U + V;
-            sm[(k + half) * G + cc] = U - V + q2;
-        }
-        __syncthreads();
-    }
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        int k = e / G, cc = e - k * G;
-        a[((size_t)k << L2) + c0 + cc] = sm[e];
-    }
+    const int y = e >> (ELOG - w);
+    const int z = (t << (ELOG - w)) | (e & ((1 << (ELOG - w)) - 1));
+    return (z & ((1 << lo) - 1)) | (y << lo) | ((z >> lo) << (lo + w));
 }
 
-// Rows: blocks of 2^LOGS contiguous words, stages L1..logN-1; output reduced to [0, q).
-template <int LOGS>
-__global__ void __launch_bounds__(kThreads) ntt_fwd_row(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
-                                                         int G)
+// Global word offset (within the row) of local element k of group gi.
+template <bool COL>
+__device__ __forceinline__ size_t gaddr(int k, int gi, int L2, int LOGS)
 {
-    constexpr int S = 1 << LOGS;
+    return COL ? (((size_t)k << L2) + gi) : (((size_t)gi << LOGS) + k);
+}
+
+// ---------------------------------------------------------------- forward
+template <int LOGS, int ELOG, bool COL>
+__global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
+                                                            int log_g)
+{
+    constexpr int S = 1 << LOGS, E = 1 << ELOG, T = S >> ELOG, R = (LOGS + ELOG - 1) / ELOG;
     extern __shared__ uint64_t sm[];
+    const int G = 1 << log_g;
     const int row = blockIdx.y;
     const int p = pm.idx[row % pm.period];
-    const uint64_t q = kt.q[p];
-    const uint64_t q2 = 2 * q;
+    const uint64_t q = kt.q[p], q2 = 2 * q;
     const TwPair *tw = kt.tw_fwd + (size_t)p * kt.n;
-    const int L1 = kt.log_n - LOGS;
-    const int blk0 = blockIdx.x * G;
-    uint64_t *a = data + (size_t)row * kt.n + (size_t)blk0 * S;
-    const int tot = S * G;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) sm[e] = a[e];
-    __syncthreads();
-#pragma unroll 1
-    for (int l = 0; l < LOGS; ++l) {
-        const int half = S >> (l + 1);
-        const int m = 1 << (L1 + l);
-        for (int b = threadIdx.x; b < (S / 2) * G; b += blockDim.x) {
-            int g = b / (S / 2), pi = b - g * (S / 2);
-            int grp = pi / half, off = pi - grp * half;
-            int k = g * S + grp * 2 * half + off;
-            TwPair w = tw[m + ((blk0 + g) << l) + grp];
-            uint64_t U = sm[k];
-            uint64_t V = sm[k + half];
-            U = U >= q2 ? U - q2 : U;
-            V = shoup_lazy(V, w.w, w.wp, q);
-            sm[k] = U + V;
-            sm[k + half] = U - V + q2;
-        }
-        __syncthreads();
+    uint64_t *a = data + (size_t)row * kt.n;
+    const int logn = kt.log_n;
+    const int L2 = logn - LOGS;  // col pass: 2^L2 columns
+    const int tid = threadIdx.x;
+    int g, t;
+    if (COL) {
+        g = tid & (G - 1);
+        t = tid >> log_g;
+    } else {
+        t = tid & (T - 1);
+        g = tid / T;
     }
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) a[e] = reduce4q(sm[e], q);
+    const int gi = blockIdx.x * G + g;        // global column / block index
+    const int lbase = COL ? 0 : logn - LOGS;  // global stage of local stage 0
+    const int prefix = COL ? 0 : gi;
+    uint64_t *buf0 = sm, *buf1 = sm + S * G;
+    uint64_t v[E];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int hi = LOGS - 1 - r * ELOG;
+        const int w = (LOGS - r * ELOG) < ELOG ? (LOGS - r * ELOG) : ELOG;
+        const int lo = hi - w + 1;
+        if (r == 0) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)];
+        } else {
+            const uint64_t *b = ((r - 1) & 1) ? buf1 : buf0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int k = kmap<ELOG>(lo, w, t, e);
+                v[e] = COL ? b[k * G + g] : b[g * S + k];
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < w; ++s) {
+            const int lp = r * ELOG + s;   // local stage
+            const int bit = ELOG - 1 - s;  // register bit paired in this stage
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                if (e & (1 << bit)) continue;
+                const int k = kmap<ELOG>(lo, w, t, e);
+                const TwPair wt = tw[(1 << (lbase + lp)) + (prefix << lp) + (k >> (LOGS - lp))];
+                uint64_t U = v[e];
+                uint64_t V = v[e | (1 << bit)];
+                U = U >= q2 ? U - q2 : U;
+                V = shoup_lazy(V, wt.w, wt.wp, q);
+                v[e] = U + V;
+                v[e | (1 << bit)] = U - V + q2;
+            }
+        }
+        if (r == R - 1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const uint64_t x = COL ? v[e] : reduce4q(v[e], q);
+                a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)] = x;
+            }
+        } else {
+            uint64_t *b = (r & 1) ? buf1 : buf0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int k = kmap<ELOG>(lo, w, t, e);
+                if (COL)
+                    b[k * G + g] = v[e];
+                else
+                    b[g * S + k] = v[e];
+            }
+            __syncthreads();
+        }
+    }
 }
 
 // ---------------------------------------------------------------- inverse
-// Rows first: stages logN-1 .. L1 (reverse order) on contiguous blocks.
-template <int LOGS>
-__global__ void __launch_bounds__(kThreads) ntt_inv_row(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
-                                                         int G)
+// Stages in reverse: local stage lp = LOGS-1 .. 0 operates on bit LOGS-1-lp, so
+// rounds own bits from the bottom up.  The col pass (last) multiplies by N^{-1}.
+template <int LOGS, int ELOG, bool COL>
+__global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
+                                                            int log_g)
 {
-    constexpr int S = 1 << LOGS;
+    constexpr int S = 1 << LOGS, E = 1 << ELOG, T = S >> ELOG, R = (LOGS + ELOG - 1) / ELOG;
     extern __shared__ uint64_t sm[];
+    const int G = 1 << log_g;
     const int row = blockIdx.y;
     const int p = pm.idx[row % pm.period];
-    const uint64_t q = kt.q[p];
-    const uint64_t q2 = 2 * q;
+    const uint64_t q = kt.q[p], q2 = 2 * q;
     const TwPair *tw = kt.tw_inv + (size_t)p * kt.n;
-    const int L1 = kt.log_n - LOGS;
-    const int blk0 = blockIdx.x * G;
-    uint64_t *a = data + (size_t)row * kt.n + (size_t)blk0 * S;
-    const int tot = S * G;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) sm[e] = a[e];
-    __syncthreads();
-#pragma unroll 1
-    for (int l = LOGS - 1; l >= 0; --l) {
-        const int half = S >> (l + 1);
-        const int m = 1 << (L1 + l);
-        for (int b = threadIdx.x; b < (S / 2) * G; b += blockDim.x) {
-            int g = b / (S / 2), pi = b - g * (S / 2);
-            int grp = pi / half, off = pi - grp * half;
-            int k = g * S + grp * 2 * half + off;
-            TwPair w = tw[m + ((blk0 + g) << l) + grp];
-            uint64_t X = sm[k];
-            uint64_t Y = sm[k + half];
-            uint64_t s = X + Y;
-            sm[k] = s >= q2 ? s - q2 : s;
-            sm[k + half] = shoup_lazy(X - Y + q2, w.w, w.wp, q);
-        }
-        __syncthreads();
-    }
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) a[e] = sm[e];
-}
-
-// Columns last: stages L1-1 .. 0, then times N^{-1}, output in [0, q).
-template <int LOGS>
-__global__ void __launch_bounds__(kThreads) ntt_inv_col(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
-                                                         int G)
-{
-    constexpr int S = 1 << LOGS;
-    extern __shared__ uint64_t sm[];
-    const int row = blockIdx.y;
-    const int p = pm.idx[row % pm.period];
-    const uint64_t q = kt.q[p];
-    const uint64_t q2 = 2 * q;
-    const TwPair *tw = kt.tw_inv + (size_t)p * kt.n;
-    const TwPair ninv = kt.n_inv[p];
     uint64_t *a = data + (size_t)row * kt.n;
-    const int L2 = kt.log_n - LOGS;
-    const int c0 = blockIdx.x * G;
-    const int tot = S * G;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        int k = e / G, cc = e - k * G;
-        sm[e] = a[((size_t)k << L2) + c0 + cc];
+    const int logn = kt.log_n;
+    const int L2 = logn - LOGS;
+    const int tid = threadIdx.x;
+    int g, t;
+    if (COL) {
+        g = tid & (G - 1);
+        t = tid >> log_g;
+    } else {
+        t = tid & (T - 1);
+        g = tid / T;
     }
-    __syncthreads();
-#pragma unroll 1
-    for (int l = LOGS - 1; l >= 0; --l) {
-        const int half = S >> (l + 1);
-        for (int b = threadIdx.x; b < (S / 2) * G; b += blockDim.x) {
-            int pi = b / G, cc = b - pi * G;
-            int grp = pi / half, off = pi - grp * half;
-            int k = grp * 2 * half + off;
-            TwPair w = tw[(1 << l) + grp];
-            uint64_t X = sm[k * G + cc];
-            uint64_t Y = sm[(k + half) * G + cc];
-            uint64_t s = X + Y;
-            sm[k * G + cc] = s >= q2 ? s - q2 : s;
-            sm[(k + half) * G + cc] = shoup_lazy(X - Y + q2, w.w, w.wp, q);
+    const int gi = blockIdx.x * G + g;
+    const int lbase = COL ? 0 : logn - LOGS;
+    const int prefix = COL ? 0 : gi;
+    uint64_t *buf0 = sm, *buf1 = sm + S * G;
+    uint64_t v[E];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int lo = r * ELOG;
+        const int w = (LOGS - lo) < ELOG ? (LOGS - lo) : ELOG;
+        if (r == 0) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)];
+        } else {
+            const uint64_t *b = ((r - 1) & 1) ? buf1 : buf0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int k = kmap<ELOG>(lo, w, t, e);
+                v[e] = COL ? b[k * G + g] : b[g * S + k];
+            }
         }
-        __syncthreads();
-    }
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        int k = e / G, cc = e - k * G;
-        a[((size_t)k << L2) + c0 + cc] = shoup(sm[e], ninv.w, ninv.wp, q);
+#pragma unroll
+        for (int s = 0; s < w; ++s) {
+            const int lp = LOGS - 1 - (lo + s);  // local stage of bit lo+s
+            const int bit = ELOG - w + s;        // register bit of k-bit lo+s
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                if (e & (1 << bit)) continue;
+                const int k = kmap<ELOG>(lo, w, t, e);
+                const TwPair wt = tw[(1 << (lbase + lp)) + (prefix << lp) + (k >> (LOGS - lp))];
+                const uint64_t X = v[e];
+                const uint64_t Y = v[e | (1 << bit)];
+                const uint64_t sum = X + Y;
+                v[e] = sum >= q2 ? sum - q2 : sum;
+                v[e | (1 << bit)] = shoup_lazy(X - Y + q2, wt.w, wt.wp, q);
+            }
+        }
+        if (r == R - 1) {
+            TwPair ninv{0, 0};
+            if (COL) ninv = kt.n_inv[p];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const uint64_t x = COL ? shoup(v[e], ninv.w, ninv.wp, q) : v[e];
+                a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)] = x;
+            }
+        } else {
+            uint64_t *b = (r & 1) ? buf1 : buf0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int k = kmap<ELOG>(lo, w, t, e);
+                if (COL)
+                    b[k * G + g] = v[e];
+                else
+                    b[g * S + k] = v[e];
+            }
+            __syncthreads();
+        }
     }
 }
 
-#define MMFHE_NTT_DISPATCH(FN)                                                                    \
-    template <int LOGS>                                                                           \
-    struct FN##_k {                                                                               \
-        static void run(dim3 g, size_t smem, cudaStream_t s, uint64_t *d, const KTables &kt,      \
-                        const PrimeMap &pm, int G)                                                \
-        {                                                                                         \
-            FN<LOGS><<<g, kThreads, smem, s>>>(d, kt, pm, G);                                     \
-        }                                                                                         \
-    };
+struct Launch {
+    dim3 grid;
+    int threads;
+    size_t smem;
+    int log_g;
+};
 
-MMFHE_NTT_DISPATCH(ntt_fwd_col)
-MMFHE_NTT_DISPATCH(ntt_fwd_row)
-MMFHE_NTT_DISPATCH(ntt_inv_col)
-MMFHE_NTT_DISPATCH(ntt_inv_row)
-
-template <template <int> class K>
-void launch_logs(int logs, dim3 g, size_t smem, cudaStream_t s, uint64_t *d, const KTables &kt,
-                 const PrimeMap &pm, int G)
+// Groups per CTA: as many as fit kCtaThreads threads (and exist).
+Launch plan(int LOGS, int ELOG, int n_groups, uint32_t rows)
 {
-    switch (logs) {
-    case 1: K<1>::run(g, smem, s, d, kt, pm, G); break;
-    case 2: K<2>::run(g, smem, s, d, kt, pm, G); break;
-    case 3: K<3>::run(g, smem, s, d, kt, pm, G); break;
-    case 4: K<4>::run(g, smem, s, d, kt, pm, G); break;
-    case 5: K<5>::run(g, smem, s, d, kt, pm, G); break;
-    case 6: K<6>::run(g, smem, s, d, kt, pm, G); break;
-    case 7: K<7>::run(g, smem, s, d, kt, pm, G); break;
-    case 8: K<8>::run(g, smem, s, d, kt, pm, G); break;
-    default: throw Error(MMFHE_E_PARAMS, "unsupported NTT split");
+    const int T = 1 << (LOGS - ELOG);
+    int log_g = 0;
+    while ((T << (log_g + 1)) <= kCtaThreads && (1 << (log_g + 1)) <= n_groups) ++log_g;
+    const int G = 1 << log_g;
+    Launch l;
+    l.log_g = log_g;
+    l.threads = T * G;
+    l.grid = dim3(n_groups / G, rows);
+    l.smem = (LOGS > ELOG) ? 2 * sizeof(uint64_t) * ((size_t)G << LOGS) : 0;
+    return l;
+}
+
+template <bool FWD, bool COL>
+void launch_pass(int LOGS, uint32_t log_n, uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm,
+                 cudaStream_t s)
+{
+    const int ELOG = LOGS < 3 ? LOGS : 3;
+    const int n_groups = 1 << (log_n - LOGS);
+    Launch l = plan(LOGS, ELOG, n_groups, rows);
+#define MMFHE_NTT_CASE(LS, EL)                                                                    \
+    case LS:                                                                                      \
+        if (FWD)                                                                                  \
+            ntt_fwd_pass<LS, EL, COL><<<l.grid, l.threads, l.smem, s>>>(d, kt, pm, l.log_g);      \
+        else                                                                                      \
+            ntt_inv_pass<LS, EL, COL><<<l.grid, l.threads, l.smem, s>>>(d, kt, pm, l.log_g);      \
+        break;
+    switch (LOGS) {
+        MMFHE_NTT_CASE(2, 2)
+        MMFHE_NTT_CASE(3, 3)
+        MMFHE_NTT_CASE(4, 3)
+        MMFHE_NTT_CASE(5, 3)
+        MMFHE_NTT_CASE(6, 3)
+        MMFHE_NTT_CASE(7, 3)
+        MMFHE_NTT_CASE(8, 3)
+    default:
+        throw Error(MMFHE_E_PARAMS, "unsupported NTT split");
     }
+#undef MMFHE_NTT_CASE
 }
 
 void split(uint32_t log_n, int &L1, int &L2)
@@ -238,33 +278,39 @@ void split(uint32_t log_n, int &L1, int &L2)
 
 }  // namespace
 
-void ntt_forward(const KTables &kt, uint64_t *d, uint32_t rows, const PrimeMap &pm, cudaStream_t s,
-                 uint64_t &launches)
+void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm)
 {
     if (!rows) return;
     int L1, L2;
-    split(kt.log_n, L1, L2);
-    int S1 = 1 << L1, S2 = 1 << L2;
-    int G1 = std::max(1, std::min(kTileWords / S1, S2));
-    int G2 = std::max(1, std::min(kTileWords / S2, S1));
-    launch_logs<ntt_fwd_col_k>(L1, dim3(S2 / G1, rows), (size_t)S1 * G1 * 8, s, d, kt, pm, G1);
-    launch_logs<ntt_fwd_row_k>(L2, dim3(S1 / G2, rows), (size_t)S2 * G2 * 8, s, d, kt, pm, G2);
-    launches += 2;
+    split(c.log_n, L1, L2);
+    const double bytes = 16.0 * rows * c.n;  // one read + one write of every word per pass
+    {
+        ProfScope ps(c, "ntt_fwd_col", bytes);
+        launch_pass<true, true>(L1, c.log_n, d, rows, c.kt, pm, c.stream);
+    }
+    {
+        ProfScope ps(c, "ntt_fwd_row", bytes);
+        launch_pass<true, false>(L2, c.log_n, d, rows, c.kt, pm, c.stream);
+    }
+    c.launches += 2;
     CUDA_CHECK(cudaGetLastError());
 }
 
-void ntt_inverse(const KTables &kt, uint64_t *d, uint32_t rows, const PrimeMap &pm, cudaStream_t s,
-                 uint64_t &launches)
+void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm)
 {
     if (!rows) return;
     int L1, L2;
-    split(kt.log_n, L1, L2);
-    int S1 = 1 << L1, S2 = 1 << L2;
-    int G1 = std::max(1, std::min(kTileWords / S1, S2));
-    int G2 = std::max(1, std::min(kTileWords / S2, S1));
-    launch_logs<ntt_inv_row_k>(L2, dim3(S1 / G2, rows), (size_t)S2 * G2 * 8, s, d, kt, pm, G2);
-    launch_logs<ntt_inv_col_k>(L1, dim3(S2 / G1, rows), (size_t)S1 * G1 * 8, s, d, kt, pm, G1);
-    launches += 2;
+    split(c.log_n, L1, L2);
+    const double bytes = 16.0 * rows * c.n;
+    {
+        ProfScope ps(c, "ntt_inv_row", bytes);
+        launch_pass<false, false>(L2, c.log_n, d, rows, c.kt, pm, c.stream);
+    }
+    {
+        ProfScope ps(c, "ntt_inv_col", bytes);
+        launch_pass<false, true>(L1, c.log_n, d, rows, c.kt, pm, c.stream);
+    }
+    c.launches += 2;
     CUDA_CHECK(cudaGetLastError());
 }
 

@@ -1,5 +1,9 @@
-// ops.h -- launchers of the RNS polynomial kernels (poly.cu).  All device
-// buffers are limb-major [rows][N]; "pm" maps a row to its prime.
+// ops.h -- launchers of the RNS polynomial kernels (poly.cu).
+//
+// All device buffers are limb-major [rows][N].  Batched launchers take B
+// items laid out at a fixed item stride (in words); every kernel covers the
+// whole batch in one launch so a key, plaintext or twiddle word fetched once
+// serves B ciphertexts.
 #pragma once
 #include "context.h"
 
@@ -11,38 +15,49 @@ struct PtrList {
     const uint64_t *p[kMaxTerms];
 };
 
-// out = a + b (sub=false) or a - b (sub=true), rows x N words.
+// out = a (+/-) b over `rows` rows (contiguous); pm maps row -> prime.
 void launch_addsub(Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, uint32_t rows, const PrimeMap &pm,
                    bool sub);
 // x -> x * 2^64 mod q (Montgomery form), in place.
 void launch_to_mont(Ctx &c, uint64_t *x, uint32_t rows, const PrimeMap &pm);
-// NTT-domain automorphism sigma_g: out[j] = in[perm_g(j)] (all rows).
+// NTT-domain automorphism sigma_g on every row: out[j] = in[perm_g(j)].
 void launch_automorph(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t rows, uint64_t g);
-// ModUp base conversion of all digits at `level` from coefficient-form x [level+1][N] into
-// y (digit j's n_tgt rows at y + off_j*N, coefficient form).
-void launch_modup_bconv(Ctx &c, uint64_t *y, const uint64_t *x_coef, uint32_t level, const std::vector<size_t> &off);
-// Key inner product: accQ [2][l+1][N], accP [2][K][N] = sum_j y_j (.) evk_j (Montgomery MAC).
-void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, const uint64_t *y,
-                   const std::vector<size_t> &off, const uint64_t *key, uint32_t level);
-// ModDown base conversion: w [2][l+1][N] = BConv_{P->Q}(zP [2][K][N], coefficient form).
-void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level);
-// out_p = (accQ_p - w_p) * P^{-1} (+ addend_p if given), p = 0, 1; NTT form.
-void launch_moddown_final(Ctx &c, uint64_t *out0, uint64_t *out1, const uint64_t *accQ, const uint64_t *w,
-                          const uint64_t *add0, const uint64_t *add1, uint32_t level);
-// Rescale helper: v [2][l][N] = (t - h) mod q_i from t [2][N] (coefficient form mod q_l).
-void launch_rescale_prep(Ctx &c, uint64_t *v, const uint64_t *t, uint32_t level);
-// out [2][l][N] = (a_i - v_i) * q_l^{-1} mod q_i from a [2][l+1][N] (NTT form).
-void launch_rescale_final(Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *v, uint32_t level);
-// Fused tensor sum over <= kMaxTerms pairs: out [3][l+1][N] (+)= sum_p a_p (x) b_p.
-void launch_tensor_sum(Ctx &c, uint64_t *out, const PtrList &a, const PtrList &b, int n, uint32_t level,
-                       bool accumulate);
-// out [2][l+1][N] (+)= sum_t pt_t (.) ct_t, pt in Montgomery form [l+1][N].
-void launch_pmult_sum(Ctx &c, uint64_t *out, const PtrList &pt, const PtrList &ct, int n, uint32_t level,
-                      bool accumulate);
-// out [2][l+1][N] (+)= sum_t c_t ct_t with scalar constants consts[t][l+1] (Shoup pairs).
-void launch_lincomb(Ctx &c, uint64_t *out, const PtrList &ct, const TwPair *consts, int n, uint32_t level,
-                    bool accumulate);
-// c0 [l+1][N] += pt (pt in Montgomery form).
-void launch_add_plain(Ctx &c, uint64_t *c0, const uint64_t *pt_mont, uint32_t level);
+
+// ---- hybrid key switching (batched over B polynomials x_b, each [l+1][N])
+// ModUp BConv of every digit: x_coef item stride xs; y item stride ys; digit j rows at y + off_j*N.
+void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, size_t xs, uint32_t level,
+                        const std::vector<size_t> &off, uint32_t B);
+// accQ [B][2][l+1][N], accP [B][2][K][N] = sum_j y_j (.) evk_j; each key word is loaded once for all B.
+void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, size_t xs, const uint64_t *y,
+                   size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B);
+// w [B][2][l+1][N] = BConv_{P->Q}(zP [B][2][K][N]) (coefficient form).
+void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B);
+// out_{b,p} = (accQ_{b,p} - w_{b,p}) * P^{-1} (+ add_{b,p}); out/add item strides os/as,
+// poly 1 of an item at +(l+1)N; add may be null, add1 (poly 1 addend) selectable.
+void launch_moddown_final(Ctx &c, uint64_t *out, size_t os, const uint64_t *accQ, const uint64_t *w,
+                          const uint64_t *add, size_t as, bool add_poly1, uint32_t level, uint32_t B);
+
+// ---- rescale (batched): t [B][2][N] coefficient-form last limbs; v [B][2][l][N]
+void launch_rescale_prep(Ctx &c, uint64_t *v, const uint64_t *t, uint32_t level, uint32_t B);
+// out [B][2][l][N] = (a_i - v_i) * q_l^{-1}; a item stride as.
+void launch_rescale_final(Ctx &c, uint64_t *out, const uint64_t *a, size_t as, const uint64_t *v, uint32_t level,
+                          uint32_t B);
+
+// ---- fused sums (batched: operand item stride is, output item stride os)
+// out (+)= sum_p a_p (x) b_p (3 polys), <= kMaxTerms pairs.
+void launch_tensor_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &a, const PtrList &b, size_t is, int n,
+                       uint32_t level, bool accumulate, uint32_t B);
+// out (+)= sum_t pt_t (.) ct_t; pt shared by the batch (Montgomery form).
+void launch_pmult_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &pt, const PtrList &ct, size_t is, int n,
+                      uint32_t level, bool accumulate, uint32_t B);
+// Scalar "modular matrix product" over a batch of 2-poly cts (CK10):
+//   out[j] = sum_{w < W} C[j][w] in[lo_j + w],  j < J,  lo_j = lo0 + j*lo_step,
+// C given as Shoup pairs [J][W][l+1]; inputs outside [0, M) contribute nothing.
+void launch_lincomb_mat(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, uint32_t J, uint32_t W, int lo0,
+                        int lo_step, const TwPair *C, uint32_t level);
+// out = sum_b in_b over a batch of B items of `words` words each (rows of level l).
+void launch_batch_sum(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t B, uint32_t npolys, uint32_t level);
+// c0 of every item (item stride s) += pt (pt in Montgomery form).
+void launch_add_plain(Ctx &c, uint64_t *c0, size_t s, const uint64_t *pt_mont, uint32_t level, uint32_t B);
 
 }  // namespace mmfhe

@@ -1,13 +1,13 @@
 // poly.cu -- RNS polynomial kernels of the CKKS evaluator (SURVEY §8(a)
-// a4-a10, §2.7 CK4-CK9): elementwise add/sub, Montgomery conversion, the
+// a4-a10, §2.7 CK4-CK10): elementwise add/sub, Montgomery conversion, the
 // NTT-domain automorphism, ModUp / ModDown fast base conversion, the key inner
 // product, rescale pre/post steps, and fused multi-operand sums (tensor sums,
-// plaintext inner products, scalar linear combinations).
+// plaintext inner products, scalar modular matrix products).
 //
 // All outputs are canonical residues in [0, q).  Thread mapping: one thread per
-// coefficient index (consecutive threads = consecutive words, coalesced
-// 256-byte warp accesses), grid.y over limbs/rows; per-prime constants are
-// warp-uniform loads (L1 broadcast).
+// coefficient index (consecutive threads = consecutive words: coalesced
+// 256-byte warp accesses), grid.y over limbs/rows, grid.z over batch items;
+// per-prime constants are warp-uniform loads (L1 broadcast).
 #include <algorithm>
 
 #include "modarith.cuh"
@@ -21,7 +21,7 @@ constexpr int kTB = 256;
 
 __device__ __forceinline__ uint32_t bitrev(uint32_t x, uint32_t log_n) { return __brev(x) >> (32 - log_n); }
 
-inline dim3 grid2(uint32_t n, uint32_t rows) { return dim3((n + kTB - 1) / kTB, rows); }
+inline dim3 grid3(uint32_t n, uint32_t rows, uint32_t batch = 1) { return dim3((n + kTB - 1) / kTB, rows, batch); }
 
 // ------------------------------------------------------------------ elementwise
 __global__ void k_addsub(uint64_t *__restrict__ out, const uint64_t *__restrict__ a, const uint64_t *__restrict__ b,
@@ -64,11 +64,12 @@ struct ModUpDigit {
     const TwPair *hat_inv;
     const uint64_t *hat;
     const uint32_t *tgt;
-    uint64_t *y;
+    size_t y_off;  // words
     uint32_t lo, hi, n_tgt;
 };
 struct ModUpArgs {
     ModUpDigit d[16];
+    size_t xs, ys;  // item strides (words)
     uint32_t level, L;
 };
 
@@ -78,43 +79,47 @@ __device__ __forceinline__ uint32_t ext_prime(uint32_t r, uint32_t level, uint32
 }
 
 // y_{j,t} = sum_{i in I_j} [x_i [Qhat_i^{-1}]_{q_i}]_{q_i} [Qhat_i]_t mod t
-__global__ void __launch_bounds__(kTB) k_modup(const uint64_t *__restrict__ x, KTables kt, ModUpArgs args)
+__global__ void __launch_bounds__(kTB) k_modup(uint64_t *__restrict__ y_base, const uint64_t *__restrict__ x_base,
+                                               KTables kt, ModUpArgs args)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
     const ModUpDigit &dg = args.d[blockIdx.y];
+    const uint64_t *x = x_base + (size_t)blockIdx.z * args.xs;
+    uint64_t *y = y_base + (size_t)blockIdx.z * args.ys + dg.y_off;
     const uint32_t na = dg.hi - dg.lo;
     uint64_t v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         if (i < (int)na) {
             const uint32_t pi = dg.lo + i;
-            const uint64_t q = kt.q[pi];
             const TwPair h = dg.hat_inv[i];
-            v[i] = shoup(x[(size_t)pi * kt.n + k], h.w, h.wp, q);
+            v[i] = shoup(x[(size_t)pi * kt.n + k], h.w, h.wp, kt.q[pi]);
         }
     }
     for (uint32_t ti = 0; ti < dg.n_tgt; ++ti) {
         const uint32_t pt = ext_prime(dg.tgt[ti], args.level, args.L);
-        const uint64_t t = kt.q[pt];
         U128 acc{0, 0};
 #pragma unroll
         for (int i = 0; i < 16; ++i)
             if (i < (int)na) mac128(acc, v[i], dg.hat[(size_t)i * dg.n_tgt + ti]);
-        dg.y[(size_t)ti * kt.n + k] = redc(acc, t, kt.qinv_neg[pt]);
+        y[(size_t)ti * kt.n + k] = redc(acc, kt.q[pt], kt.qinv_neg[pt]);
     }
 }
 
 struct IPArgs {
-    const uint64_t *y[16];
+    size_t y_off[16];
     uint32_t lo[16], hi[16];
-    uint32_t dnum, level, L, K;
+    size_t xs, ys;
+    uint32_t dnum, level, L, K, B;
 };
 
-// (accQ|accP)_p[r] = sum_j src_j[r] (.) evk_j[p][r]; src_j[r] = x[r] for r in I_j, else ModUp'd row.
+// For every batch item b: (accQ|accP)_{b,p}[r] = sum_j src_{b,j}[r] (.) evk_j[p][r] with
+// src = x_b[r] for r in I_j, else the ModUp'd row.  The 2*dnum key words of (r, k) are
+// loaded once and reused for all B items (the key is streamed once per batch).
 __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
-                                                const uint64_t *__restrict__ x, const uint64_t *__restrict__ key,
-                                                KTables kt, IPArgs a)
+                                                const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
+                                                const uint64_t *__restrict__ key, KTables kt, IPArgs a)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
@@ -122,30 +127,39 @@ __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uin
     const uint32_t pr = ext_prime(r, a.level, a.L);
     const uint64_t q = kt.q[pr], qi = kt.qinv_neg[pr];
     const size_t key_rows = a.L + 1 + a.K;
-    U128 acc0{0, 0}, acc1{0, 0};
-    for (uint32_t j = 0; j < a.dnum; ++j) {
-        uint64_t s;
-        if (r >= a.lo[j] && r < a.hi[j]) {
-            s = x[(size_t)r * kt.n + k];
-        } else {
-            const uint32_t row = r < a.lo[j] ? r : r - (a.hi[j] - a.lo[j]);
-            s = a.y[j][(size_t)row * kt.n + k];
+    uint64_t kb[16], ka[16];
+    const uint64_t *src[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (j < (int)a.dnum) {
+            kb[j] = __ldg(key + ((size_t)(2 * j) * key_rows + pr) * kt.n + k);
+            ka[j] = __ldg(key + ((size_t)(2 * j + 1) * key_rows + pr) * kt.n + k);
+            if (r >= a.lo[j] && r < a.hi[j]) {
+                src[j] = x + (size_t)r * kt.n + k;
+            } else {
+                const uint32_t row = r < a.lo[j] ? r : r - (a.hi[j] - a.lo[j]);
+                src[j] = y + a.y_off[j] + (size_t)row * kt.n + k;
+            }
         }
-        const uint64_t *kb = key + ((size_t)(2 * j) * key_rows + pr) * kt.n;
-        const uint64_t *ka = key + ((size_t)(2 * j + 1) * key_rows + pr) * kt.n;
-        mac128(acc0, s, __ldg(kb + k));
-        mac128(acc1, s, __ldg(ka + k));
     }
-    const uint64_t r0 = redc(acc0, q, qi), r1 = redc(acc1, q, qi);
-    if (r <= a.level) {
-        const size_t stride = (size_t)(a.level + 1) * kt.n;
-        accQ[(size_t)r * kt.n + k] = r0;
-        accQ[stride + (size_t)r * kt.n + k] = r1;
-    } else {
-        const uint32_t rr = r - a.level - 1;
-        const size_t stride = (size_t)a.K * kt.n;
-        accP[(size_t)rr * kt.n + k] = r0;
-        accP[stride + (size_t)rr * kt.n + k] = r1;
+    const bool isq = r <= a.level;
+    const size_t qs = (size_t)2 * (a.level + 1) * kt.n, ps = (size_t)2 * a.K * kt.n;
+    uint64_t *o = isq ? accQ + (size_t)r * kt.n + k : accP + (size_t)(r - a.level - 1) * kt.n + k;
+    const size_t ostride = isq ? qs : ps;
+    const size_t opoly = isq ? (size_t)(a.level + 1) * kt.n : (size_t)a.K * kt.n;
+    for (uint32_t b = 0; b < a.B; ++b) {
+        U128 acc0{0, 0}, acc1{0, 0};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (j < (int)a.dnum) {
+                const bool in_digit = r >= a.lo[j] && r < a.hi[j];
+                const uint64_t s = src[j][(size_t)b * (in_digit ? a.xs : a.ys)];
+                mac128(acc0, s, kb[j]);
+                mac128(acc1, s, ka[j]);
+            }
+        }
+        o[(size_t)b * ostride] = redc(acc0, q, qi);
+        o[(size_t)b * ostride + opoly] = redc(acc1, q, qi);
     }
 }
 
@@ -156,20 +170,20 @@ struct MDArgs {
     uint32_t level, L, K;
 };
 
-// w_i = sum_k [z_k [Phat_k^{-1}]_{p_k}]_{p_k} [Phat_k]_{q_i} mod q_i
+// w_i = sum_k [z_k [Phat_k^{-1}]_{p_k}]_{p_k} [Phat_k]_{q_i} mod q_i; grid.y = item*2 + poly
 __global__ void __launch_bounds__(kTB) k_moddown_bconv(uint64_t *__restrict__ w, const uint64_t *__restrict__ zP,
                                                        KTables kt, MDArgs a)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
-    const uint32_t poly = blockIdx.y;
+    const uint32_t ip = blockIdx.y;  // item * 2 + poly
     uint64_t v[16];
 #pragma unroll
     for (int kk = 0; kk < 16; ++kk) {
         if (kk < (int)a.K) {
             const uint32_t pi = a.L + 1 + kk;
             const TwPair h = a.phat_inv[kk];
-            v[kk] = shoup(zP[((size_t)poly * a.K + kk) * kt.n + k], h.w, h.wp, kt.q[pi]);
+            v[kk] = shoup(zP[((size_t)ip * a.K + kk) * kt.n + k], h.w, h.wp, kt.q[pi]);
         }
     }
     for (uint32_t i = 0; i <= a.level; ++i) {
@@ -177,73 +191,75 @@ __global__ void __launch_bounds__(kTB) k_moddown_bconv(uint64_t *__restrict__ w,
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk)
             if (kk < (int)a.K) mac128(acc, v[kk], a.phat[(size_t)kk * (a.L + 1) + i]);
-        w[((size_t)poly * (a.level + 1) + i) * kt.n + k] = redc(acc, kt.q[i], kt.qinv_neg[i]);
+        w[((size_t)ip * (a.level + 1) + i) * kt.n + k] = redc(acc, kt.q[i], kt.qinv_neg[i]);
     }
 }
 
-__global__ void k_moddown_final(uint64_t *__restrict__ out0, uint64_t *__restrict__ out1,
-                                const uint64_t *__restrict__ accQ, const uint64_t *__restrict__ w,
-                                const uint64_t *__restrict__ add0, const uint64_t *__restrict__ add1, KTables kt,
-                                MDArgs a)
+// grid.y = poly*(l+1) + i, grid.z = item
+__global__ void k_moddown_final(uint64_t *__restrict__ out, size_t os, const uint64_t *__restrict__ accQ,
+                                const uint64_t *__restrict__ w, const uint64_t *__restrict__ add, size_t as,
+                                int add_poly1, KTables kt, MDArgs a)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
-    const uint32_t r = blockIdx.y;  // 0 .. 2(l+1)-1
+    const uint32_t r = blockIdx.y, b = blockIdx.z;
     const uint32_t poly = r / (a.level + 1), i = r - poly * (a.level + 1);
     const uint64_t q = kt.q[i];
     const TwPair pv = a.pinv[i];
-    const size_t idx = (size_t)r * kt.n + k;
+    const size_t idx = ((size_t)b * 2 * (a.level + 1) + r) * kt.n + k;
     uint64_t d = shoup(accQ[idx] + q - w[idx], pv.w, pv.wp, q);
-    const uint64_t *add = poly ? add1 : add0;
-    const size_t li = (size_t)i * kt.n + k;
-    if (add) d = add_mod(d, add[li], q);
-    (poly ? out1 : out0)[li] = d;
+    const size_t li = (size_t)r * kt.n + k;
+    if (add && (poly == 0 || add_poly1)) d = add_mod(d, add[(size_t)b * as + li], q);
+    out[(size_t)b * os + li] = d;
 }
 
 // ------------------------------------------------------------------ rescale
 struct RSArgs {
-    const TwPair *qlinv;  // row l of [L+1][L+1]
-    const uint64_t *h;    // row l: floor(q_l/2) mod q_i
+    const TwPair *qlinv;    // row l of [L+1][L+1]
+    const uint64_t *h;      // row l: floor(q_l/2) mod q_i
     const uint64_t *recip;  // floor(2^64 / q_i)
     uint32_t level;
 };
 
-// v_i = ([t]_{q_i} - [h]_{q_i}) mod q_i, t = [a_l + h]_{q_l} in coefficient form
+// v_i = ([t]_{q_i} - [h]_{q_i}) mod q_i, t = [a_l + h]_{q_l} (coefficient form); grid.z = item
 __global__ void k_rescale_prep(uint64_t *__restrict__ v, const uint64_t *__restrict__ t, KTables kt, RSArgs a)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
-    const uint32_t r = blockIdx.y;  // 0 .. 2l-1
+    const uint32_t r = blockIdx.y, b = blockIdx.z;  // r: 0 .. 2l-1
     const uint32_t poly = r / a.level, i = r - poly * a.level;
     const uint64_t ql = kt.q[a.level];
     const uint64_t hl = ql >> 1;
-    const uint64_t tl = add_mod(t[(size_t)poly * kt.n + k], hl, ql);
+    const uint64_t tl = add_mod(t[((size_t)b * 2 + poly) * kt.n + k], hl, ql);
     const uint64_t q = kt.q[i];
     const uint64_t tm = shoup(tl, 1, a.recip[i], q);
-    v[(size_t)r * kt.n + k] = sub_mod(tm, a.h[i], q);
+    v[((size_t)b * 2 * a.level + r) * kt.n + k] = sub_mod(tm, a.h[i], q);
 }
 
-__global__ void k_rescale_final(uint64_t *__restrict__ out, const uint64_t *__restrict__ in,
+__global__ void k_rescale_final(uint64_t *__restrict__ out, const uint64_t *__restrict__ in, size_t is,
                                 const uint64_t *__restrict__ v, KTables kt, RSArgs a)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
-    const uint32_t r = blockIdx.y;
+    const uint32_t r = blockIdx.y, b = blockIdx.z;
     const uint32_t poly = r / a.level, i = r - poly * a.level;
     const uint64_t q = kt.q[i];
     const TwPair w = a.qlinv[i];
-    const uint64_t x = in[((size_t)poly * (a.level + 1) + i) * kt.n + k];
-    out[(size_t)r * kt.n + k] = shoup(x + q - v[(size_t)r * kt.n + k], w.w, w.wp, q);
+    const uint64_t x = in[(size_t)b * is + ((size_t)poly * (a.level + 1) + i) * kt.n + k];
+    const size_t o = ((size_t)b * 2 * a.level + r) * kt.n + k;
+    out[o] = shoup(x + q - v[o], w.w, w.wp, q);
 }
 
 // ------------------------------------------------------------------ fused sums
-// d0 = sum a0 b0, d1 = sum a0 b1 + a1 b0, d2 = sum a1 b1 over n pairs (<= kMaxTerms).
-__global__ void __launch_bounds__(kTB) k_tensor_sum(uint64_t *__restrict__ out, PtrList A, PtrList B, int n,
-                                                    KTables kt, uint32_t level, int accumulate)
+// d0 = sum a0 b0, d1 = sum a0 b1 + a1 b0, d2 = sum a1 b1 over n pairs; grid.z = item.
+__global__ void __launch_bounds__(kTB) k_tensor_sum(uint64_t *__restrict__ out_base, size_t os, PtrList A, PtrList B,
+                                                    size_t is, int n, KTables kt, uint32_t level, int accumulate)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
     const uint32_t r = blockIdx.y;
+    const size_t boff = (size_t)blockIdx.z * is;
+    uint64_t *out = out_base + (size_t)blockIdx.z * os;
     const uint64_t q = kt.q[r], qi = kt.qinv_neg[r];
     const size_t ps = (size_t)(level + 1) * kt.n;
     const size_t off = (size_t)r * kt.n + k;
@@ -253,7 +269,7 @@ __global__ void __launch_bounds__(kTB) k_tensor_sum(uint64_t *__restrict__ out, 
         U128 a0c{0, 0}, a1c{0, 0}, a2c{0, 0};
         const int end = min(n, p + 7);  // <= 14 products < q*2^60 each in acc1
         for (; p < end; ++p) {
-            const uint64_t *pa = A.p[p], *pb = B.p[p];
+            const uint64_t *pa = A.p[p] + boff, *pb = B.p[p] + boff;
             const uint64_t a0 = pa[off], a1 = pa[ps + off];
             if (pa == pb) {
                 mac128(a0c, a0, a0);
@@ -286,13 +302,16 @@ __global__ void __launch_bounds__(kTB) k_tensor_sum(uint64_t *__restrict__ out, 
     out[2 * ps + off] = d2;
 }
 
-// out_p = sum_t ct_t[p] (.) pt_t, pt in Montgomery form (result canonical).
-__global__ void __launch_bounds__(kTB) k_pmult_sum(uint64_t *__restrict__ out, PtrList PT, PtrList CT, int n,
-                                                   KTables kt, uint32_t level, int accumulate)
+// out_p = sum_t ct_t[p] (.) pt_t, pt in Montgomery form shared by the batch.
+__global__ void __launch_bounds__(kTB) k_pmult_sum(uint64_t *__restrict__ out_base, size_t os, PtrList PT,
+                                                   PtrList CT, size_t is, int n, KTables kt, uint32_t level,
+                                                   int accumulate)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
     const uint32_t r = blockIdx.y;
+    const size_t boff = (size_t)blockIdx.z * is;
+    uint64_t *out = out_base + (size_t)blockIdx.z * os;
     const uint64_t q = kt.q[r], qi = kt.qinv_neg[r];
     const size_t ps = (size_t)(level + 1) * kt.n;
     const size_t off = (size_t)r * kt.n + k;
@@ -302,8 +321,8 @@ __global__ void __launch_bounds__(kTB) k_pmult_sum(uint64_t *__restrict__ out, P
         U128 c0{0, 0}, c1{0, 0};
         const int end = min(n, t + 15);
         for (; t < end; ++t) {
-            const uint64_t w = PT.p[t][off];
-            const uint64_t *c = CT.p[t];
+            const uint64_t w = __ldg(PT.p[t] + off);
+            const uint64_t *c = CT.p[t] + boff;
             mac128(c0, c[off], w);
             mac128(c1, c[ps + off], w);
         }
@@ -318,36 +337,72 @@ __global__ void __launch_bounds__(kTB) k_pmult_sum(uint64_t *__restrict__ out, P
     out[ps + off] = s1;
 }
 
-// out_p = sum_t c_t ct_t[p] with per-limb Shoup constants consts[t*(l+1) + r].
-__global__ void __launch_bounds__(kTB) k_lincomb(uint64_t *__restrict__ out, PtrList CT, const TwPair *consts, int n,
-                                                 KTables kt, uint32_t level, int accumulate)
+constexpr int kJG = 8;  // outputs per thread in the modular matrix product
+
+// out[j] = sum_w C[j][w] in[lo_j + w] for j in this CTA's group of kJG outputs.
+__global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out, const uint64_t *__restrict__ in,
+                                                     uint32_t M, uint32_t J, uint32_t W, int lo0, int lo_step,
+                                                     const TwPair *__restrict__ C, KTables kt, uint32_t level)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
     const uint32_t r = blockIdx.y;
+    const uint32_t j0 = blockIdx.z * kJG;
+    const uint32_t jn = min((uint32_t)kJG, J - j0);
     const uint64_t q = kt.q[r], q2 = 2 * q;
-    const size_t ps = (size_t)(level + 1) * kt.n;
+    const uint32_t L1 = level + 1;
+    const size_t ps = (size_t)L1 * kt.n, item = 2 * ps;
     const size_t off = (size_t)r * kt.n + k;
-    uint64_t s0 = 0, s1 = 0;
-    for (int t = 0; t < n; ++t) {
-        const TwPair c = consts[(size_t)t * (level + 1) + r];
-        const uint64_t *ct = CT.p[t];
-        s0 += shoup_lazy(ct[off], c.w, c.wp, q);
-        s1 += shoup_lazy(ct[ps + off], c.w, c.wp, q);
-        s0 = s0 >= q2 ? s0 - q2 : s0;
-        s1 = s1 >= q2 ? s1 - q2 : s1;
+    int ilo = lo0 + (int)j0 * lo_step, ihi = lo0 + (int)(j0 + jn - 1) * lo_step + (int)W;
+    if (lo_step < 0) {
+        const int tmp = lo0 + (int)(j0 + jn - 1) * lo_step;
+        ihi = lo0 + (int)j0 * lo_step + (int)W;
+        ilo = tmp;
     }
-    s0 = csub(s0, q);
-    s1 = csub(s1, q);
-    if (accumulate) {
-        s0 = add_mod(s0, out[off], q);
-        s1 = add_mod(s1, out[ps + off], q);
+    ilo = max(ilo, 0);
+    ihi = min(ihi, (int)M);
+    uint64_t a0[kJG], a1[kJG];
+#pragma unroll
+    for (int jj = 0; jj < kJG; ++jj) a0[jj] = a1[jj] = 0;
+    for (int i = ilo; i < ihi; ++i) {
+        const uint64_t x0 = in[(size_t)i * item + off], x1 = in[(size_t)i * item + ps + off];
+#pragma unroll
+        for (int jj = 0; jj < kJG; ++jj) {
+            if (jj < (int)jn) {
+                const int w = i - (lo0 + (int)(j0 + jj) * lo_step);
+                if (w >= 0 && w < (int)W) {
+                    const TwPair c = C[((size_t)(j0 + jj) * W + w) * L1 + r];
+                    uint64_t s0 = a0[jj] + shoup_lazy(x0, c.w, c.wp, q);
+                    uint64_t s1 = a1[jj] + shoup_lazy(x1, c.w, c.wp, q);
+                    a0[jj] = s0 >= q2 ? s0 - q2 : s0;
+                    a1[jj] = s1 >= q2 ? s1 - q2 : s1;
+                }
+            }
+        }
     }
-    out[off] = s0;
-    out[ps + off] = s1;
+#pragma unroll
+    for (int jj = 0; jj < kJG; ++jj) {
+        if (jj < (int)jn) {
+            out[(size_t)(j0 + jj) * item + off] = csub(a0[jj], q);
+            out[(size_t)(j0 + jj) * item + ps + off] = csub(a1[jj], q);
+        }
+    }
 }
 
-__global__ void k_add_plain(uint64_t *__restrict__ c0, const uint64_t *__restrict__ pt, KTables kt)
+__global__ void k_batch_sum(uint64_t *__restrict__ out, const uint64_t *__restrict__ in, uint32_t B, size_t item,
+                            KTables kt, uint32_t level)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t r = blockIdx.y;
+    const uint64_t q = kt.q[r % (level + 1)];
+    const size_t off = (size_t)r * kt.n + k;
+    uint64_t s = 0;
+    for (uint32_t b = 0; b < B; ++b) s = add_mod(s, in[(size_t)b * item + off], q);
+    out[off] = s;
+}
+
+__global__ void k_add_plain(uint64_t *__restrict__ c0, size_t s, const uint64_t *__restrict__ pt, KTables kt)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
@@ -355,7 +410,8 @@ __global__ void k_add_plain(uint64_t *__restrict__ c0, const uint64_t *__restric
     const uint64_t q = kt.q[r];
     const size_t off = (size_t)r * kt.n + k;
     const uint64_t v = redc(U128{pt[off], 0}, q, kt.qinv_neg[r]);
-    c0[off] = add_mod(c0[off], v, q);
+    uint64_t *c = c0 + (size_t)blockIdx.z * s;
+    c[off] = add_mod(c[off], v, q);
 }
 
 }  // namespace
@@ -370,45 +426,54 @@ __global__ void k_add_plain(uint64_t *__restrict__ c0, const uint64_t *__restric
 void launch_addsub(Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, uint32_t rows, const PrimeMap &pm,
                    bool sub)
 {
-    k_addsub<<<grid2(c.n, rows), kTB, 0, c.stream>>>(out, a, b, c.kt, pm, sub ? 1 : 0);
+    ProfScope ps(c, "addsub", 24.0 * rows * c.n);
+    k_addsub<<<grid3(c.n, rows), kTB, 0, c.stream>>>(out, a, b, c.kt, pm, sub ? 1 : 0);
     LAUNCH_CHECK(c);
 }
 
 void launch_to_mont(Ctx &c, uint64_t *x, uint32_t rows, const PrimeMap &pm)
 {
-    k_to_mont<<<grid2(c.n, rows), kTB, 0, c.stream>>>(x, c.kt, pm);
+    ProfScope ps(c, "to_mont", 16.0 * rows * c.n);
+    k_to_mont<<<grid3(c.n, rows), kTB, 0, c.stream>>>(x, c.kt, pm);
     LAUNCH_CHECK(c);
 }
 
 void launch_automorph(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t rows, uint64_t g)
 {
-    k_automorph<<<grid2(c.n, rows), kTB, 0, c.stream>>>(out, in, c.log_n, g);
+    ProfScope ps(c, "automorph", 16.0 * rows * c.n);
+    k_automorph<<<grid3(c.n, rows), kTB, 0, c.stream>>>(out, in, c.log_n, g);
     LAUNCH_CHECK(c);
 }
 
-void launch_modup_bconv(Ctx &c, uint64_t *y, const uint64_t *x_coef, uint32_t level, const std::vector<size_t> &off)
+void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, size_t xs, uint32_t level,
+                        const std::vector<size_t> &off, uint32_t B)
 {
     const auto &plans = c.modup[level];
     MMFHE_REQUIRE(plans.size() <= 16 && c.alpha <= 16, MMFHE_E_PARAMS, "dnum/alpha too large");
     ModUpArgs a{};
     a.level = level;
     a.L = c.L;
+    a.xs = xs;
+    a.ys = ys;
+    double words = 0;
+    for (const auto &p : plans) words += (double)(p.hi - p.lo) + p.n_tgt;
+    ProfScope ps(c, "modup_bconv", 8.0 * words * c.n * B);
     for (size_t j = 0; j < plans.size(); ++j) {
         const ModUpPlan &p = plans[j];
         a.d[j].hat_inv = (const TwPair *)c.bconv_ptr(p.off_hat_inv);
         a.d[j].hat = (const uint64_t *)c.bconv_ptr(p.off_hat);
         a.d[j].tgt = (const uint32_t *)c.bconv_ptr(p.off_tgt);
-        a.d[j].y = y + off[j] * c.n;
+        a.d[j].y_off = off[j] * c.n;
         a.d[j].lo = p.lo;
         a.d[j].hi = p.hi;
         a.d[j].n_tgt = p.n_tgt;
     }
-    k_modup<<<grid2(c.n, (uint32_t)plans.size()), kTB, 0, c.stream>>>(x_coef, c.kt, a);
+    k_modup<<<grid3(c.n, (uint32_t)plans.size(), B), kTB, 0, c.stream>>>(y, x_coef, c.kt, a);
     LAUNCH_CHECK(c);
 }
 
-void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, const uint64_t *y,
-                   const std::vector<size_t> &off, const uint64_t *key, uint32_t level)
+void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, size_t xs, const uint64_t *y,
+                   size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B)
 {
     const auto &plans = c.modup[level];
     IPArgs a{};
@@ -416,12 +481,17 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
     a.level = level;
     a.L = c.L;
     a.K = c.K;
+    a.B = B;
+    a.xs = xs;
+    a.ys = ys;
     for (size_t j = 0; j < plans.size(); ++j) {
-        a.y[j] = y + off[j] * c.n;
+        a.y_off[j] = off[j] * c.n;
         a.lo[j] = plans[j].lo;
         a.hi[j] = plans[j].hi;
     }
-    k_key_ip<<<grid2(c.n, level + 1 + c.K), kTB, 0, c.stream>>>(accQ, accP, x_ntt, key, c.kt, a);
+    const double rows = level + 1 + c.K;  // per row: key 2 dnum words once; per item dnum in + 2 out
+    ProfScope ps(c, "key_ip", 8.0 * rows * c.n * (2.0 * a.dnum + B * (a.dnum + 2.0)));
+    k_key_ip<<<grid3(c.n, level + 1 + c.K), kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
     LAUNCH_CHECK(c);
 }
 
@@ -437,18 +507,20 @@ static MDArgs md_args(Ctx &c, uint32_t level)
     return a;
 }
 
-void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level)
+void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B)
 {
     MMFHE_REQUIRE(c.K <= 16, MMFHE_E_PARAMS, "K too large");
-    k_moddown_bconv<<<grid2(c.n, 2), kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
+    ProfScope ps(c, "moddown_bconv", 16.0 * (c.K + level + 1) * c.n * B);
+    k_moddown_bconv<<<grid3(c.n, 2 * B), kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
     LAUNCH_CHECK(c);
 }
 
-void launch_moddown_final(Ctx &c, uint64_t *out0, uint64_t *out1, const uint64_t *accQ, const uint64_t *w,
-                          const uint64_t *add0, const uint64_t *add1, uint32_t level)
+void launch_moddown_final(Ctx &c, uint64_t *out, size_t os, const uint64_t *accQ, const uint64_t *w,
+                          const uint64_t *add, size_t as, bool add_poly1, uint32_t level, uint32_t B)
 {
-    k_moddown_final<<<grid2(c.n, 2 * (level + 1)), kTB, 0, c.stream>>>(out0, out1, accQ, w, add0, add1, c.kt,
-                                                                       md_args(c, level));
+    ProfScope ps(c, "moddown_final", 8.0 * 2 * (level + 1) * c.n * B * (add ? (add_poly1 ? 4.0 : 3.5) : 3.0));
+    k_moddown_final<<<grid3(c.n, 2 * (level + 1), B), kTB, 0, c.stream>>>(out, os, accQ, w, add, as,
+                                                                          add_poly1 ? 1 : 0, c.kt, md_args(c, level));
     LAUNCH_CHECK(c);
 }
 
@@ -462,42 +534,63 @@ static RSArgs rs_args(Ctx &c, uint32_t level)
     return a;
 }
 
-void launch_rescale_prep(Ctx &c, uint64_t *v, const uint64_t *t, uint32_t level)
+void launch_rescale_prep(Ctx &c, uint64_t *v, const uint64_t *t, uint32_t level, uint32_t B)
 {
-    k_rescale_prep<<<grid2(c.n, 2 * level), kTB, 0, c.stream>>>(v, t, c.kt, rs_args(c, level));
+    ProfScope ps(c, "rescale_prep", 8.0 * (2.0 + 2.0 * level) * c.n * B);
+    k_rescale_prep<<<grid3(c.n, 2 * level, B), kTB, 0, c.stream>>>(v, t, c.kt, rs_args(c, level));
     LAUNCH_CHECK(c);
 }
 
-void launch_rescale_final(Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *v, uint32_t level)
+void launch_rescale_final(Ctx &c, uint64_t *out, const uint64_t *a, size_t as, const uint64_t *v, uint32_t level,
+                          uint32_t B)
 {
-    k_rescale_final<<<grid2(c.n, 2 * level), kTB, 0, c.stream>>>(out, a, v, c.kt, rs_args(c, level));
+    ProfScope ps(c, "rescale_final", 8.0 * 6.0 * level * c.n * B);
+    k_rescale_final<<<grid3(c.n, 2 * level, B), kTB, 0, c.stream>>>(out, a, as, v, c.kt, rs_args(c, level));
     LAUNCH_CHECK(c);
 }
 
-void launch_tensor_sum(Ctx &c, uint64_t *out, const PtrList &a, const PtrList &b, int n, uint32_t level,
-                       bool accumulate)
+void launch_tensor_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &a, const PtrList &b, size_t is, int n,
+                       uint32_t level, bool accumulate, uint32_t B)
 {
-    k_tensor_sum<<<grid2(c.n, level + 1), kTB, 0, c.stream>>>(out, a, b, n, c.kt, level, accumulate ? 1 : 0);
+    double in_words = 0;
+    for (int i = 0; i < n; ++i) in_words += (a.p[i] == b.p[i]) ? 2.0 : 4.0;
+    ProfScope ps(c, "tensor_sum", 8.0 * (level + 1) * c.n * B * (in_words + 3.0 + (accumulate ? 3.0 : 0.0)));
+    k_tensor_sum<<<grid3(c.n, level + 1, B), kTB, 0, c.stream>>>(out, os, a, b, is, n, c.kt, level,
+                                                                 accumulate ? 1 : 0);
     LAUNCH_CHECK(c);
 }
 
-void launch_pmult_sum(Ctx &c, uint64_t *out, const PtrList &pt, const PtrList &ct, int n, uint32_t level,
-                      bool accumulate)
+void launch_pmult_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &pt, const PtrList &ct, size_t is, int n,
+                      uint32_t level, bool accumulate, uint32_t B)
 {
-    k_pmult_sum<<<grid2(c.n, level + 1), kTB, 0, c.stream>>>(out, pt, ct, n, c.kt, level, accumulate ? 1 : 0);
+    ProfScope ps(c, "pmult_sum",
+                 8.0 * (level + 1) * c.n * ((double)n + B * (2.0 * n + 2.0 + (accumulate ? 2.0 : 0.0))));
+    k_pmult_sum<<<grid3(c.n, level + 1, B), kTB, 0, c.stream>>>(out, os, pt, ct, is, n, c.kt, level,
+                                                                accumulate ? 1 : 0);
     LAUNCH_CHECK(c);
 }
 
-void launch_lincomb(Ctx &c, uint64_t *out, const PtrList &ct, const TwPair *consts, int n, uint32_t level,
-                    bool accumulate)
+void launch_lincomb_mat(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, uint32_t J, uint32_t W, int lo0,
+                        int lo_step, const TwPair *C, uint32_t level)
 {
-    k_lincomb<<<grid2(c.n, level + 1), kTB, 0, c.stream>>>(out, ct, consts, n, c.kt, level, accumulate ? 1 : 0);
+    ProfScope ps(c, "lincomb_mat", 8.0 * 2.0 * (level + 1) * c.n * ((double)M + J));
+    k_lincomb_mat<<<grid3(c.n, level + 1, (J + kJG - 1) / kJG), kTB, 0, c.stream>>>(out, in, M, J, W, lo0, lo_step,
+                                                                                   C, c.kt, level);
     LAUNCH_CHECK(c);
 }
 
-void launch_add_plain(Ctx &c, uint64_t *c0, const uint64_t *pt_mont, uint32_t level)
+void launch_batch_sum(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t B, uint32_t npolys, uint32_t level)
 {
-    k_add_plain<<<grid2(c.n, level + 1), kTB, 0, c.stream>>>(c0, pt_mont, c.kt);
+    const uint32_t rows = npolys * (level + 1);
+    ProfScope ps(c, "batch_sum", 8.0 * rows * c.n * (B + 1.0));
+    k_batch_sum<<<grid3(c.n, rows), kTB, 0, c.stream>>>(out, in, B, (size_t)rows * c.n, c.kt, level);
+    LAUNCH_CHECK(c);
+}
+
+void launch_add_plain(Ctx &c, uint64_t *c0, size_t s, const uint64_t *pt_mont, uint32_t level, uint32_t B)
+{
+    ProfScope ps(c, "add_plain", 8.0 * (level + 1) * c.n * (1.0 + 2.0 * B));
+    k_add_plain<<<grid3(c.n, level + 1, B), kTB, 0, c.stream>>>(c0, s, pt_mont, c.kt);
     LAUNCH_CHECK(c);
 }
 

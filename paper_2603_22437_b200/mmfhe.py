@@ -47,16 +47,17 @@ class ChainCfg(ctypes.Structure):
     _fields_ = [("R", ctypes.c_uint32), ("D", ctypes.c_uint32), ("A", ctypes.c_uint32), ("F", ctypes.c_uint32),
                 ("gamma", ctypes.c_uint32), ("p_phi", ctypes.c_uint32), ("taylor_order", ctypes.c_uint32),
                 ("n_slots", ctypes.c_uint32), ("bsgs_baby", ctypes.c_uint32), ("hoist", ctypes.c_uint32),
-                ("fc_dims", ctypes.c_uint32 * 4), ("notch_width", ctypes.c_uint32), ("n_bands", ctypes.c_uint32),
+                ("frame_batch", ctypes.c_uint32), ("fc_dims", ctypes.c_uint32 * 4), ("notch_width", ctypes.c_uint32), ("n_bands", ctypes.c_uint32),
                 ("n_taps", ctypes.c_uint32 * 4), ("n_bins", ctypes.c_uint32 * 4),
                 ("bins", (ctypes.c_uint32 * 64) * 4), ("fs", ctypes.c_double)]
 
 
 def chain_cfg(R=0, D=0, A=0, F=0, gamma=1, p_phi=1, taylor_order=1, n_slots=0, bsgs_baby=0,
-              fc_dims=(0, 0, 0, 0), notch_width=1, bands_bins=(), n_taps=(), fs=0.0) -> ChainCfg:
+              fc_dims=(0, 0, 0, 0), notch_width=1, bands_bins=(), n_taps=(), fs=0.0, frame_batch=0) -> ChainCfg:
     c = ChainCfg()
     c.R, c.D, c.A, c.F = R, D, A, F
     c.gamma, c.p_phi, c.taylor_order, c.n_slots, c.bsgs_baby = gamma, p_phi, taylor_order, n_slots, bsgs_baby
+    c.frame_batch = frame_batch
     for i, v in enumerate(fc_dims):
         c.fc_dims[i] = int(v)
     c.notch_width = notch_width
@@ -115,6 +116,8 @@ def lib():
             "mmfhe_trace_get": [V, ctypes.c_char_p, S, P(S)],
             "mmfhe_trace_clear": [V],
             "mmfhe_trace_enable": [V, ctypes.c_int],
+            "mmfhe_profile_enable": [V, ctypes.c_int],
+            "mmfhe_profile_get": [V, ctypes.c_char_p, S, P(S)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -133,7 +136,8 @@ EXPORTED = [
     "mmfhe_encode_plain", "mmfhe_prepare_chain", "mmfhe_load_scalars", "mmfhe_chain_plan", "mmfhe_eval_chain",
     "mmfhe_sum_partials", "mmfhe_ntt", "mmfhe_intt", "mmfhe_hadd", "mmfhe_hsub", "mmfhe_pmult", "mmfhe_hmult",
     "mmfhe_relin", "mmfhe_hrot", "mmfhe_rescale", "mmfhe_keyswitch", "mmfhe_mod_switch", "mmfhe_hrot_batch",
-    "mmfhe_hmult_batch", "mmfhe_trace_get", "mmfhe_trace_clear", "mmfhe_trace_enable",
+    "mmfhe_hmult_batch", "mmfhe_trace_get", "mmfhe_trace_clear", "mmfhe_trace_enable", "mmfhe_profile_enable",
+    "mmfhe_profile_get",
 ]
 
 
@@ -350,6 +354,20 @@ class Context:
 
     def trace_enable(self, on=True):
         self._check(self._lib.mmfhe_trace_enable(self.h, 1 if on else 0))
+
+    def profile_enable(self, on=True):
+        self._check(self._lib.mmfhe_profile_enable(self.h, 1 if on else 0))
+
+    def profile(self):
+        """{kernel: (launches, total_ms, algorithmic_bytes)} since the last call (resets)."""
+        n = ctypes.c_size_t()
+        buf = ctypes.create_string_buffer(1 << 16)
+        self._check(self._lib.mmfhe_profile_get(self.h, buf, 1 << 16, ctypes.byref(n)))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            k, c, ms, b = line.split()
+            out[k] = (int(c), float(ms), float(b))
+        return out
 
     def launch_count(self):
         c = ctypes.c_uint64()

@@ -28,7 +28,7 @@ def _mcfg(m, cfg: cc.ChainCfg, bins=(), taps=()):
     return m.chain_cfg(R=cfg.R, D=cfg.D, A=cfg.A, F=cfg.F, gamma=cfg.gamma, p_phi=cfg.p_phi,
                        taylor_order=cfg.taylor_order, n_slots=cfg.n_slots, bsgs_baby=cfg.bsgs_baby,
                        fc_dims=cfg.fc_dims, notch_width=cfg.notch_width, bands_bins=bins,
-                       n_taps=[len(t) for t in taps], fs=cfg.fs)
+                       n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch)
 
 
 def _run(m, P, keys, book, chain, cfg, cts, want, scalars=None, bins=(), taps=()):
@@ -84,16 +84,17 @@ def test_vitals_v1_small(m):
     assert sorted(ctx.required_rotations("vitals_v1", _mcfg(m, cfg))) == cc.required_rotations("vitals_v1", cfg, P.n)
 
 
-def _gesture(P, seed, F=2, A=2, R=4, D=8):
+def _gesture(P, seed, F=2, A=2, R=4, D=8, frame_batch=0):
     n = A * R * D
-    cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8))
+    cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8), frame_batch=frame_batch)
     Z, _ = radar.gesture_scene(A, R, D, F, seed=seed, cls=seed % 5)
     return cfg, radar.preprocess_gesture(Z)
 
 
-def test_gesture_chain_small(m):
+@pytest.mark.parametrize("F,fb", [(2, 0), (3, 2)])
+def test_gesture_chain_small(m, F, fb):
     P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
-    cfg, Zt = _gesture(P, 3201)
+    cfg, Zt = _gesture(P, 3201, F=F, frame_batch=fb)
     keys = orc.keygen(P, seed=3202, rotations=cc.required_rotations("gesture", cfg, P.n))
     cts = []
     for t in range(cfg.F):
@@ -102,8 +103,7 @@ def test_gesture_chain_small(m):
             cts.append(orc.encrypt_vector(P, keys, part, P.L, seed=3203, index=len(cts)))
     ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
     book = cc.PlainBook(P)
-    feats = [cc.gesture_frame(ev, book, cts[2 * t], cts[2 * t + 1], cfg) for t in range(cfg.F)]
-    feat = cc.frame_accumulate(ev, feats)
+    feat = cc.gesture_features(ev, book, cts[0::2], cts[1::2], cfg)
     dims = cfg.fc_dims
     Ws, bs = radar.fc_weights([dims[0], dims[1], dims[2], 5], seed=3204)
     logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
@@ -140,7 +140,7 @@ def test_k3_doppler_dft_c3_full_size(m):
 def test_vitals_v2_small(m):
     P = toy(log_n=10, n_q=10, scale_bits=40, n_p=2, alpha=2)  # third order needs 9 levels
     cfg = cc.ChainCfg(R=8, F=10, p_phi=2, taylor_order=3, n_slots=P.n // 2, fs=2.0,
-                      bands=((0.1, 0.6), (0.7, 1.0)))
+                      bands=((0.1, 0.6), (0.7, 1.0)), frame_batch=4)
     keys = orc.keygen(P, seed=3401, rotations=cc.required_rotations("vitals_v2", cfg, P.n))
     _, cts = _vital_inputs(P, keys, cfg, 9, 3402)
     taps = [np.array([0.2, 0.3, 0.3, 0.2]), np.array([0.25, -0.5, 0.25])]
