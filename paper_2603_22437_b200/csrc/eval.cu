@@ -83,10 +83,22 @@ DCt import_batch(Ctx &c, const mmfhe_ct *cts, size_t first, size_t step, size_t 
     }
     DCt r = make_ct(c, c0.level, 2, c0.n_slots, c0.scale, (uint32_t)count);
     const size_t words = r.item_words();
-    for (size_t i = 0; i < count; ++i) {
-        const mmfhe_ct &x = cts[first + i * step];
-        CUDA_CHECK(cudaMemcpyAsync(r.item((uint32_t)i), x.data, words * 8,
-                                   x.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+    bool all_dev = true;
+    for (size_t i = 0; i < count; ++i)
+        all_dev = all_dev && cts[first + i * step].on_device && ((uintptr_t)cts[first + i * step].data % 16 == 0);
+    if (all_dev) {  // one gather launch per 64 device items
+        for (size_t s = 0; s < count; s += kMaxTerms) {
+            PtrList P{};
+            const int n = (int)std::min<size_t>(kMaxTerms, count - s);
+            for (int i = 0; i < n; ++i) P.p[i] = cts[first + (s + i) * step].data;
+            launch_gather(c, r.item((uint32_t)s), P, n, words);
+        }
+    } else {
+        for (size_t i = 0; i < count; ++i) {
+            const mmfhe_ct &x = cts[first + i * step];
+            CUDA_CHECK(cudaMemcpyAsync(r.item((uint32_t)i), x.data, words * 8,
+                                       x.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
+        }
     }
     if (c0.form == MMFHE_FORM_COEFF) ntt_forward(c, r.data(), r.rows(), qmap(c, c0.level));
     return r;

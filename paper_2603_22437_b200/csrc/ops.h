@@ -57,6 +57,9 @@ void launch_lincomb_mat(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, u
                         int lo_step, const TwPair *C, uint32_t level);
 // out = sum_b in_b over a batch of B items of `words` words each (rows of level l).
 void launch_batch_sum(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t B, uint32_t npolys, uint32_t level);
+// out[b] = copy of src.p[b] (n <= kMaxTerms items of `words` words each; device pointers,
+// 16-byte aligned).
+void launch_gather(Ctx &c, uint64_t *out, const PtrList &src, int n, size_t words);
 // c0 of every item (item stride s) += pt (pt in Montgomery form).
 void launch_add_plain(Ctx &c, uint64_t *c0, size_t s, const uint64_t *pt_mont, uint32_t level, uint32_t B);
 

@@ -402,6 +402,20 @@ __global__ void k_batch_sum(uint64_t *__restrict__ out, const uint64_t *__restri
     out[off] = s;
 }
 
+// out[b] = *src[b] for n items of `words` words (16-byte vector copies).
+__global__ void k_gather(uint64_t *__restrict__ out, PtrList src, size_t words)
+{
+    const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (i >= words) return;
+    const uint64_t *s = src.p[blockIdx.y];
+    uint64_t *o = out + (size_t)blockIdx.y * words;
+    if (i + 1 < words) {
+        *(ulonglong2 *)(o + i) = *(const ulonglong2 *)(s + i);
+    } else {
+        o[i] = s[i];
+    }
+}
+
 __global__ void k_add_plain(uint64_t *__restrict__ c0, size_t s, const uint64_t *__restrict__ pt, KTables kt)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -584,6 +598,14 @@ void launch_batch_sum(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t B, uin
     const uint32_t rows = npolys * (level + 1);
     ProfScope ps(c, "batch_sum", 8.0 * rows * c.n * (B + 1.0));
     k_batch_sum<<<grid3(c.n, rows), kTB, 0, c.stream>>>(out, in, B, (size_t)rows * c.n, c.kt, level);
+    LAUNCH_CHECK(c);
+}
+
+void launch_gather(Ctx &c, uint64_t *out, const PtrList &src, int n, size_t words)
+{
+    ProfScope ps(c, "gather", 16.0 * words * n);
+    const size_t threads = (words + 1) / 2;
+    k_gather<<<dim3((unsigned)((threads + kTB - 1) / kTB), n), kTB, 0, c.stream>>>(out, src, words);
     LAUNCH_CHECK(c);
 }
 
