@@ -101,17 +101,26 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict
         for (int s = 0; s < w; ++s) {
             const int lp = r * ELOG + s;   // local stage
             const int bit = ELOG - 1 - s;  // register bit paired in this stage
+            // In a full-width round the twiddle depends only on the top s register bits: load
+            // each distinct one once.  In the (last, lo = 0) partial round the spare register
+            // bits map ABOVE the round's bits, so every butterfly has its own twiddle.
+            const int tb = (w == ELOG) ? s : ELOG;  // ELOG: one twiddle per register
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                if (e & (1 << bit)) continue;
-                const int k = kmap<ELOG>(lo, w, t, e);
-                const TwPair wt = tw[(1 << (lbase + lp)) + (prefix << lp) + (k >> (LOGS - lp))];
-                uint64_t U = v[e];
-                uint64_t V = v[e | (1 << bit)];
-                U = U >= q2 ? U - q2 : U;
-                V = shoup_lazy(V, wt.w, wt.wp, q);
-                v[e] = U + V;
-                v[e | (1 << bit)] = U - V + q2;
+            for (int m = 0; m < (1 << tb); ++m) {
+                const int erep = m << (ELOG - tb);
+                if (erep & (1 << bit)) continue;  // per-register case: pair leaders only
+                const int krep = kmap<ELOG>(lo, w, t, erep);
+                const TwPair wt = tw[(1 << (lbase + lp)) + (prefix << lp) + (krep >> (LOGS - lp))];
+#pragma unroll
+                for (int e = erep; e < erep + (1 << (ELOG - tb)); ++e) {
+                    if (e & (1 << bit)) continue;
+                    uint64_t U = v[e];
+                    uint64_t V = v[e | (1 << bit)];
+                    U = U >= q2 ? U - q2 : U;
+                    V = shoup_lazy(V, wt.w, wt.wp, q);
+                    v[e] = U + V;
+                    v[e | (1 << bit)] = U - V + q2;
+                }
             }
         }
         if (r == R - 1) {
@@ -185,16 +194,21 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict
         for (int s = 0; s < w; ++s) {
             const int lp = LOGS - 1 - (lo + s);  // local stage of bit lo+s
             const int bit = ELOG - w + s;        // register bit of k-bit lo+s
+            const int ntop = w - 1 - s;          // register bits above: the twiddle depends on these only
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                if (e & (1 << bit)) continue;
-                const int k = kmap<ELOG>(lo, w, t, e);
-                const TwPair wt = tw[(1 << (lbase + lp)) + (prefix << lp) + (k >> (LOGS - lp))];
-                const uint64_t X = v[e];
-                const uint64_t Y = v[e | (1 << bit)];
-                const uint64_t sum = X + Y;
-                v[e] = sum >= q2 ? sum - q2 : sum;
-                v[e | (1 << bit)] = shoup_lazy(X - Y + q2, wt.w, wt.wp, q);
+            for (int m = 0; m < (1 << ntop); ++m) {
+                const int erep = m << (ELOG - ntop);
+                const int krep = kmap<ELOG>(lo, w, t, erep);
+                const TwPair wt = tw[(1 << (lbase + lp)) + (prefix << lp) + (krep >> (LOGS - lp))];
+#pragma unroll
+                for (int e = erep; e < erep + (1 << (ELOG - ntop)); ++e) {
+                    if (e & (1 << bit)) continue;
+                    const uint64_t X = v[e];
+                    const uint64_t Y = v[e | (1 << bit)];
+                    const uint64_t sum = X + Y;
+                    v[e] = sum >= q2 ? sum - q2 : sum;
+                    v[e | (1 << bit)] = shoup_lazy(X - Y + q2, wt.w, wt.wp, q);
+                }
             }
         }
         if (r == R - 1) {

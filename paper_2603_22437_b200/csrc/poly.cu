@@ -79,6 +79,8 @@ __device__ __forceinline__ uint32_t ext_prime(uint32_t r, uint32_t level, uint32
 }
 
 // y_{j,t} = sum_{i in I_j} [x_i [Qhat_i^{-1}]_{q_i}]_{q_i} [Qhat_i]_t mod t
+// AMAX >= digit width (compile-time bound keeps v[] in registers).
+template <int AMAX>
 __global__ void __launch_bounds__(kTB) k_modup(uint64_t *__restrict__ y_base, const uint64_t *__restrict__ x_base,
                                                KTables kt, ModUpArgs args)
 {
@@ -88,9 +90,9 @@ __global__ void __launch_bounds__(kTB) k_modup(uint64_t *__restrict__ y_base, co
     const uint64_t *x = x_base + (size_t)blockIdx.z * args.xs;
     uint64_t *y = y_base + (size_t)blockIdx.z * args.ys + dg.y_off;
     const uint32_t na = dg.hi - dg.lo;
-    uint64_t v[16];
+    uint64_t v[AMAX];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < AMAX; ++i) {
         if (i < (int)na) {
             const uint32_t pi = dg.lo + i;
             const TwPair h = dg.hat_inv[i];
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(kTB) k_modup(uint64_t *__restrict__ y_base, co
         const uint32_t pt = ext_prime(dg.tgt[ti], args.level, args.L);
         U128 acc{0, 0};
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
+        for (int i = 0; i < AMAX; ++i)
             if (i < (int)na) mac128(acc, v[i], dg.hat[(size_t)i * dg.n_tgt + ti]);
         y[(size_t)ti * kt.n + k] = redc(acc, kt.q[pt], kt.qinv_neg[pt]);
     }
@@ -111,12 +113,13 @@ struct IPArgs {
     size_t y_off[16];
     uint32_t lo[16], hi[16];
     size_t xs, ys;
-    uint32_t dnum, level, L, K, B;
+    uint32_t dnum, level, L, K, B, per_z;
 };
 
 // For every batch item b: (accQ|accP)_{b,p}[r] = sum_j src_{b,j}[r] (.) evk_j[p][r] with
 // src = x_b[r] for r in I_j, else the ModUp'd row.  The 2*dnum key words of (r, k) are
-// loaded once and reused for all B items (the key is streamed once per batch).
+// loaded once per thread and reused for its per_z items (grid.z splits the batch).
+template <int DMAX>
 __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
                                                 const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
                                                 const uint64_t *__restrict__ key, KTables kt, IPArgs a)
@@ -124,21 +127,25 @@ __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uin
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
     const uint32_t r = blockIdx.y;
+    const uint32_t b0 = blockIdx.z * a.per_z, b1 = min(a.B, b0 + a.per_z);
     const uint32_t pr = ext_prime(r, a.level, a.L);
     const uint64_t q = kt.q[pr], qi = kt.qinv_neg[pr];
     const size_t key_rows = a.L + 1 + a.K;
-    uint64_t kb[16], ka[16];
-    const uint64_t *src[16];
+    uint64_t kb[DMAX], ka[DMAX];
+    const uint64_t *src[DMAX];
+    size_t sstr[DMAX];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < DMAX; ++j) {
         if (j < (int)a.dnum) {
             kb[j] = __ldg(key + ((size_t)(2 * j) * key_rows + pr) * kt.n + k);
             ka[j] = __ldg(key + ((size_t)(2 * j + 1) * key_rows + pr) * kt.n + k);
             if (r >= a.lo[j] && r < a.hi[j]) {
                 src[j] = x + (size_t)r * kt.n + k;
+                sstr[j] = a.xs;
             } else {
                 const uint32_t row = r < a.lo[j] ? r : r - (a.hi[j] - a.lo[j]);
                 src[j] = y + a.y_off[j] + (size_t)row * kt.n + k;
+                sstr[j] = a.ys;
             }
         }
     }
@@ -147,15 +154,17 @@ __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uin
     uint64_t *o = isq ? accQ + (size_t)r * kt.n + k : accP + (size_t)(r - a.level - 1) * kt.n + k;
     const size_t ostride = isq ? qs : ps;
     const size_t opoly = isq ? (size_t)(a.level + 1) * kt.n : (size_t)a.K * kt.n;
-    for (uint32_t b = 0; b < a.B; ++b) {
+    for (uint32_t b = b0; b < b1; ++b) {
+        uint64_t s[DMAX];
+#pragma unroll
+        for (int j = 0; j < DMAX; ++j)
+            if (j < (int)a.dnum) s[j] = src[j][(size_t)b * sstr[j]];
         U128 acc0{0, 0}, acc1{0, 0};
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < DMAX; ++j) {
             if (j < (int)a.dnum) {
-                const bool in_digit = r >= a.lo[j] && r < a.hi[j];
-                const uint64_t s = src[j][(size_t)b * (in_digit ? a.xs : a.ys)];
-                mac128(acc0, s, kb[j]);
-                mac128(acc1, s, ka[j]);
+                mac128(acc0, s[j], kb[j]);
+                mac128(acc1, s[j], ka[j]);
             }
         }
         o[(size_t)b * ostride] = redc(acc0, q, qi);
@@ -171,15 +180,16 @@ struct MDArgs {
 };
 
 // w_i = sum_k [z_k [Phat_k^{-1}]_{p_k}]_{p_k} [Phat_k]_{q_i} mod q_i; grid.y = item*2 + poly
+template <int KMAX>
 __global__ void __launch_bounds__(kTB) k_moddown_bconv(uint64_t *__restrict__ w, const uint64_t *__restrict__ zP,
                                                        KTables kt, MDArgs a)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
     const uint32_t ip = blockIdx.y;  // item * 2 + poly
-    uint64_t v[16];
+    uint64_t v[KMAX];
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
+    for (int kk = 0; kk < KMAX; ++kk) {
         if (kk < (int)a.K) {
             const uint32_t pi = a.L + 1 + kk;
             const TwPair h = a.phat_inv[kk];
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(kTB) k_moddown_bconv(uint64_t *__restrict__ w,
     for (uint32_t i = 0; i <= a.level; ++i) {
         U128 acc{0, 0};
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk)
+        for (int kk = 0; kk < KMAX; ++kk)
             if (kk < (int)a.K) mac128(acc, v[kk], a.phat[(size_t)kk * (a.L + 1) + i]);
         w[((size_t)ip * (a.level + 1) + i) * kt.n + k] = redc(acc, kt.q[i], kt.qinv_neg[i]);
     }
@@ -482,7 +492,15 @@ void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, 
         a.d[j].hi = p.hi;
         a.d[j].n_tgt = p.n_tgt;
     }
-    k_modup<<<grid3(c.n, (uint32_t)plans.size(), B), kTB, 0, c.stream>>>(y, x_coef, c.kt, a);
+    const dim3 g = grid3(c.n, (uint32_t)plans.size(), B);
+    if (c.alpha <= 1)
+        k_modup<1><<<g, kTB, 0, c.stream>>>(y, x_coef, c.kt, a);
+    else if (c.alpha <= 4)
+        k_modup<4><<<g, kTB, 0, c.stream>>>(y, x_coef, c.kt, a);
+    else if (c.alpha <= 8)
+        k_modup<8><<<g, kTB, 0, c.stream>>>(y, x_coef, c.kt, a);
+    else
+        k_modup<16><<<g, kTB, 0, c.stream>>>(y, x_coef, c.kt, a);
     LAUNCH_CHECK(c);
 }
 
@@ -505,7 +523,19 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
     }
     const double rows = level + 1 + c.K;  // per row: key 2 dnum words once; per item dnum in + 2 out
     ProfScope ps(c, "key_ip", 8.0 * rows * c.n * (2.0 * a.dnum + B * (a.dnum + 2.0)));
-    k_key_ip<<<grid3(c.n, level + 1 + c.K), kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
+    // split the batch over grid.z so that >= ~8 CTAs per SM are in flight; the key words
+    // are then re-read once per z-chunk (negligible next to the per-item traffic)
+    const uint32_t ctas_xy = ((c.n + kTB - 1) / kTB) * (level + 1 + c.K);
+    uint32_t nz = std::max<uint32_t>(1, std::min<uint32_t>(B, (148 * 8 + ctas_xy - 1) / ctas_xy));
+    a.per_z = (B + nz - 1) / nz;
+    nz = (B + a.per_z - 1) / a.per_z;
+    const dim3 g = grid3(c.n, level + 1 + c.K, nz);
+    if (a.dnum <= 4)
+        k_key_ip<4><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
+    else if (a.dnum <= 8)
+        k_key_ip<8><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
+    else
+        k_key_ip<16><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
     LAUNCH_CHECK(c);
 }
 
@@ -525,7 +555,15 @@ void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t leve
 {
     MMFHE_REQUIRE(c.K <= 16, MMFHE_E_PARAMS, "K too large");
     ProfScope ps(c, "moddown_bconv", 16.0 * (c.K + level + 1) * c.n * B);
-    k_moddown_bconv<<<grid3(c.n, 2 * B), kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
+    const dim3 g = grid3(c.n, 2 * B);
+    if (c.K <= 1)
+        k_moddown_bconv<1><<<g, kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
+    else if (c.K <= 4)
+        k_moddown_bconv<4><<<g, kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
+    else if (c.K <= 8)
+        k_moddown_bconv<8><<<g, kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
+    else
+        k_moddown_bconv<16><<<g, kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
     LAUNCH_CHECK(c);
 }
 
