@@ -232,6 +232,12 @@ mmfhe_status mmfhe_trace_enable(mmfhe_ctx *ctx, int on);
 mmfhe_status mmfhe_profile_enable(mmfhe_ctx *ctx, int on);
 mmfhe_status mmfhe_profile_get(mmfhe_ctx *ctx, char *buf, size_t cap, size_t *len);
 
+/* Integer roofline microbenchmark (synchronous): whole-GPU rate of one
+ * register-resident operation, in operations per second.
+ * kind 0: Harvey CT butterfly (lazy Shoup), 1: GS butterfly, 2: 64x64->128 MAC,
+ * 3: fully reduced Shoup modular product. */
+mmfhe_status mmfhe_microbench(mmfhe_ctx *ctx, int kind, double *ops_per_s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -410,6 +410,14 @@ mmfhe_status mmfhe_profile_enable(mmfhe_ctx *ctx, int on)
     API_END(ctx)
 }
 
+mmfhe_status mmfhe_microbench(mmfhe_ctx *ctx, int kind, double *ops_per_s)
+{
+    API_BEGIN
+    MMFHE_REQUIRE(ops_per_s && kind >= 0 && kind <= 3, MMFHE_E_INVALID_ARG, "bad microbench kind");
+    *ops_per_s = microbench_ops_per_s(*ctx, kind);
+    API_END(ctx)
+}
+
 mmfhe_status mmfhe_profile_get(mmfhe_ctx *ctx, char *buf, size_t cap, size_t *len)
 {
     API_BEGIN

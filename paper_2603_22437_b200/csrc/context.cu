@@ -118,7 +118,7 @@ std::string Ctx::profile_report()
     sync();
     struct Agg {
         uint64_t count = 0;
-        double ms = 0, bytes = 0;
+        double ms = 0, bytes = 0, ops = 0;
     };
     std::map<std::string, Agg> agg;
     for (auto &r : prof) {
@@ -128,14 +128,15 @@ std::string Ctx::profile_report()
         g.count++;
         g.ms += ms;
         g.bytes += r.bytes;
+        g.ops += r.ops;
     }
     prof.clear();
     ev_used = 0;
     std::string out;
     char line[256];
     for (auto &kv : agg) {
-        snprintf(line, sizeof(line), "%s %llu %.6f %.0f\n", kv.first.c_str(), (unsigned long long)kv.second.count,
-                 kv.second.ms, kv.second.bytes);
+        snprintf(line, sizeof(line), "%s %llu %.6f %.0f %.0f\n", kv.first.c_str(), (unsigned long long)kv.second.count,
+                 kv.second.ms, kv.second.bytes, kv.second.ops);
         out += line;
     }
     return out;

@@ -121,7 +121,7 @@ class Ctx {
     struct ProfRec {
         const char *name;
         cudaEvent_t a, b;
-        double bytes;
+        double bytes, ops;  // algorithmic bytes and butterflies (NTT) of the launch
     };
     bool prof_on = false;
     std::vector<ProfRec> prof;
@@ -155,7 +155,7 @@ std::string plain_key(const std::string &name, uint32_t level);
 // Records CUDA events around one kernel launch when the ctx profiler is on.
 class ProfScope {
   public:
-    ProfScope(Ctx &c, const char *name, double bytes) : c_(c), name_(name), bytes_(bytes)
+    ProfScope(Ctx &c, const char *name, double bytes, double ops = 0) : c_(c), name_(name), bytes_(bytes), ops_(ops)
     {
         if (c_.prof_on) {
             a_ = c_.next_event();
@@ -167,14 +167,14 @@ class ProfScope {
         if (c_.prof_on) {
             cudaEvent_t b = c_.next_event();
             cudaEventRecord(b, c_.stream);
-            c_.prof.push_back({name_, a_, b, bytes_});
+            c_.prof.push_back({name_, a_, b, bytes_, ops_});
         }
     }
 
   private:
     Ctx &c_;
     const char *name_;
-    double bytes_;
+    double bytes_, ops_;
     cudaEvent_t a_ = nullptr;
 };
 

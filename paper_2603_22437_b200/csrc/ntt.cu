@@ -299,11 +299,11 @@ void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm)
     split(c.log_n, L1, L2);
     const double bytes = 16.0 * rows * c.n;  // one read + one write of every word per pass
     {
-        ProfScope ps(c, "ntt_fwd_col", bytes);
+        ProfScope ps(c, "ntt_fwd_col", bytes, 0.5 * rows * c.n * L1);
         launch_pass<true, true>(L1, c.log_n, d, rows, c.kt, pm, c.stream);
     }
     {
-        ProfScope ps(c, "ntt_fwd_row", bytes);
+        ProfScope ps(c, "ntt_fwd_row", bytes, 0.5 * rows * c.n * L2);
         launch_pass<true, false>(L2, c.log_n, d, rows, c.kt, pm, c.stream);
     }
     c.launches += 2;
@@ -317,11 +317,11 @@ void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm)
     split(c.log_n, L1, L2);
     const double bytes = 16.0 * rows * c.n;
     {
-        ProfScope ps(c, "ntt_inv_row", bytes);
+        ProfScope ps(c, "ntt_inv_row", bytes, 0.5 * rows * c.n * L2);
         launch_pass<false, false>(L2, c.log_n, d, rows, c.kt, pm, c.stream);
     }
     {
-        ProfScope ps(c, "ntt_inv_col", bytes);
+        ProfScope ps(c, "ntt_inv_col", bytes, 0.5 * rows * c.n * L1);
         launch_pass<false, true>(L1, c.log_n, d, rows, c.kt, pm, c.stream);
     }
     c.launches += 2;

@@ -118,6 +118,7 @@ def lib():
             "mmfhe_trace_enable": [V, ctypes.c_int],
             "mmfhe_profile_enable": [V, ctypes.c_int],
             "mmfhe_profile_get": [V, ctypes.c_char_p, S, P(S)],
+            "mmfhe_microbench": [V, ctypes.c_int, P(ctypes.c_double)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -137,7 +138,7 @@ EXPORTED = [
     "mmfhe_sum_partials", "mmfhe_ntt", "mmfhe_intt", "mmfhe_hadd", "mmfhe_hsub", "mmfhe_pmult", "mmfhe_hmult",
     "mmfhe_relin", "mmfhe_hrot", "mmfhe_rescale", "mmfhe_keyswitch", "mmfhe_mod_switch", "mmfhe_hrot_batch",
     "mmfhe_hmult_batch", "mmfhe_trace_get", "mmfhe_trace_clear", "mmfhe_trace_enable", "mmfhe_profile_enable",
-    "mmfhe_profile_get",
+    "mmfhe_profile_get", "mmfhe_microbench",
 ]
 
 
@@ -365,9 +366,16 @@ class Context:
         self._check(self._lib.mmfhe_profile_get(self.h, buf, 1 << 16, ctypes.byref(n)))
         out = {}
         for line in buf.value.decode().splitlines():
-            k, c, ms, b = line.split()
-            out[k] = (int(c), float(ms), float(b))
+            k, c, ms, b, ops = line.split()
+            out[k] = (int(c), float(ms), float(b), float(ops))
         return out
+
+    def microbench(self, kind):
+        """Whole-GPU ops/s of one register-resident op: 0 CT butterfly, 1 GS butterfly,
+        2 64x64->128 MAC, 3 Shoup modular product."""
+        v = ctypes.c_double()
+        self._check(self._lib.mmfhe_microbench(self.h, int(kind), ctypes.byref(v)))
+        return v.value
 
     def launch_count(self):
         c = ctypes.c_uint64()
