@@ -45,6 +45,28 @@ __device__ __forceinline__ int kmap(int lo, int w, int t, int e)
     return (z & ((1 << lo) - 1)) | (y << lo) | ((z >> lo) << (lo + w));
 }
 
+// Shared-memory word of local element k in the row pass.  One warp spans
+// 32/T groups; in rounds 1-2 its lanes step k by 2-16 words, which would hit only
+// 2-4 of the 16 64-bit bank pairs.  XOR-ing the low 4 bits with a function of
+// the high bits makes every round's lane pattern cover all 16 bank pairs
+// (derived for LOGS = 7 and 8, both directions; identity otherwise).
+template <int LOGS>
+__device__ __forceinline__ int swz(int k)
+{
+    if (LOGS == 8) return k ^ (((k >> 4) & 7) ^ (((k >> 5) & 3) << 2));
+    if (LOGS == 7) return k ^ ((((k >> 4) & 7) << 1) ^ ((k >> 6) & 1));
+    return k;
+}
+
+// Column pass (word a = k*G + g): conflict-free for LOGS <= 7; for LOGS = 8 (G = 8)
+// rounds 2 would leave bit 3 constant across a warp -- flip it with a parity of bits 4, 6.
+template <int LOGS>
+__device__ __forceinline__ int colswz(int a)
+{
+    if (LOGS == 8) return a ^ ((((a >> 4) ^ (a >> 6)) & 1) << 3);
+    return a;
+}
+
 // Global word offset (within the row) of local element k of group gi.
 template <bool COL>
 __device__ __forceinline__ size_t gaddr(int k, int gi, int L2, int LOGS)
@@ -94,7 +116,7 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const int k = kmap<ELOG>(lo, w, t, e);
-                v[e] = COL ? b[k * G + g] : b[g * S + k];
+                v[e] = COL ? b[colswz<LOGS>(k * G + g)] : b[g * S + swz<LOGS>(k)];
             }
         }
 #pragma unroll
@@ -135,9 +157,9 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict
             for (int e = 0; e < E; ++e) {
                 const int k = kmap<ELOG>(lo, w, t, e);
                 if (COL)
-                    b[k * G + g] = v[e];
+                    b[colswz<LOGS>(k * G + g)] = v[e];
                 else
-                    b[g * S + k] = v[e];
+                    b[g * S + swz<LOGS>(k)] = v[e];
             }
             __syncthreads();
         }
@@ -187,7 +209,7 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const int k = kmap<ELOG>(lo, w, t, e);
-                v[e] = COL ? b[k * G + g] : b[g * S + k];
+                v[e] = COL ? b[colswz<LOGS>(k * G + g)] : b[g * S + swz<LOGS>(k)];
             }
         }
 #pragma unroll
@@ -225,9 +247,9 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict
             for (int e = 0; e < E; ++e) {
                 const int k = kmap<ELOG>(lo, w, t, e);
                 if (COL)
-                    b[k * G + g] = v[e];
+                    b[colswz<LOGS>(k * G + g)] = v[e];
                 else
-                    b[g * S + k] = v[e];
+                    b[g * S + swz<LOGS>(k)] = v[e];
             }
             __syncthreads();
         }
