@@ -207,6 +207,11 @@ mmfhe_status mmfhe_hmult(mmfhe_ctx *ctx, const mmfhe_ct *a, const mmfhe_ct *b, m
 mmfhe_status mmfhe_relin(mmfhe_ctx *ctx, const mmfhe_ct *a3, mmfhe_ct *out);
 /* HRot by step k: (sigma_g c0 + d0, d1), (d0, d1) = KS(sigma_g c1; gk_k). */
 mmfhe_status mmfhe_hrot(mmfhe_ctx *ctx, const mmfhe_ct *a, int32_t step, mmfhe_ct *out);
+/* Hoisted HRot: one ModUp of c1 shared by n_steps rotations (a
+ * separate op -- sigma_g acts on the ModUp'd digits, residues differ from
+ * mmfhe_hrot, decryption is the same rotation).  out[i] receives step i. */
+mmfhe_status mmfhe_hrot_hoisted(mmfhe_ctx *ctx, const mmfhe_ct *a, const int32_t *steps, size_t n_steps,
+                                mmfhe_ct *out);
 /* Rescale by q_level, round-half-up. */
 mmfhe_status mmfhe_rescale(mmfhe_ctx *ctx, const mmfhe_ct *a, mmfhe_ct *out);
 /* Hybrid key switching of one polynomial x (n_polys = 1, level l) with the

@@ -52,6 +52,7 @@ class ChainCfg:
     fs: float = 20.0
     bands: tuple = ((0.1, 0.6), (0.8, 2.5))   # RR, HR
     frame_batch: int = 0        # frames per op-major batch (0: all frames)
+    hoist: int = 0              # 1: baby-step rotations of K3 / FC share one ModUp (hoisted HRot)
 
 
 def rot(v: np.ndarray, k: int) -> np.ndarray:
@@ -234,6 +235,15 @@ def k3_schedule(cfg: ChainCfg):
     return b, giants
 
 
+def baby_steps(ev, cts, steps, hoist):
+    """[[Rot(x, s) for x in cts] for s in steps]: plain HRots, or hoisted HRots that
+    share one ModUp per ciphertext (SURVEY §8(c)-5 'Hoisted HRot is a different op')."""
+    if not hoist:
+        return [[ev.rotate(x, s) for x in cts] for s in steps]
+    ys = [ev.hoist_modup(x) for x in cts]
+    return [[ev.hoisted_step(x, y, s) for x, y in zip(cts, ys)] for s in steps]
+
+
 def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg: ChainCfg):
     """K3 (Eqs. dft_re/dft_im P:805-815) on a list of frames: d_re = C~ v_re - S~ v_im,
     d_im = S~ v_re + C~ v_im via BSGS with pre-rotated diagonals; one rescale after
@@ -243,8 +253,8 @@ def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg
     W = dsp.dft_matrix(cfg.D)
     C, S = W.real, W.imag
     b, giants = k3_schedule(cfg)
-    xr = [list(v_re)] + [[ev.rotate(v, s) for v in v_re] for s in range(1, b)]
-    xi = [list(v_im)] + [[ev.rotate(v, s) for v in v_im] for s in range(1, b)]
+    xr = [list(v_re)] + baby_steps(ev, v_re, range(1, b), cfg.hoist)
+    xi = [list(v_im)] + baby_steps(ev, v_im, range(1, b), cfg.hoist)
     out_re = out_im = None
     for gp, G, babies in giants:
         t_re, t_im = [], []
@@ -347,13 +357,13 @@ def fc_schedule(h: int):
     return b, [(gp, gp * b, [s for s in range(b) if gp * b + s < h]) for gp in range(g)]
 
 
-def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int, square: bool):
+def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int, square: bool, hoist: int = 0):
     """One layer of Eq. mlp_forward: z = sum_i diag_i (.) Rot(x, i) by BSGS,
     y = rotsum_{n_in/h}(z, stride h) (h-periodic W x), + b, then (.)^2 unless last."""
     h = W.shape[0]
     lvl = x.level
     b, giants = fc_schedule(h)
-    babies = [x] + [ev.rotate(x, s) for s in range(1, min(b, h))]
+    babies = [x] + [r[0] for r in baby_steps(ev, [x], range(1, min(b, h)), hoist)]
     acc = None
     for gp, G, ss in giants:
         terms = []
@@ -390,7 +400,7 @@ def gesture_fc(ev, book, feat, Ws, bs, cfg):
     Ws, bs = pad_fc(Ws, bs, dims)
     x = feat
     for layer in range(len(Ws)):
-        x = fc_layer(ev, book, x, Ws[layer], bs[layer], dims[layer], layer + 1, layer < len(Ws) - 1)
+        x = fc_layer(ev, book, x, Ws[layer], bs[layer], dims[layer], layer + 1, layer < len(Ws) - 1, cfg.hoist)
     return x
 
 

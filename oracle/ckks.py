@@ -453,6 +453,54 @@ class Evaluator:
         d0, d1 = self.keyswitch(c1, a.level, self.gk[kn])
         return Ct([poly_add(qs, c0, d0), d1], a.level, a.scale, a.n_slots)
 
+    def rotate_hoisted(self, a: Ct, ks) -> list:
+        """Hoisted HRot (a separate op): ModUp(c1) once, then per step
+        (sigma_g c0 + d0, d1) with (d0, d1) = ModDown(sum_j sigma_g(y_j) (.) evk_g,j).
+        sigma_g acts on the ModUp'd digits over Q_l u P, so residues differ from
+        rotate() (BConv does not commute with sigma_g's sign flips)."""
+        ys = self.hoist_modup(a)
+        return [self.hoisted_step(a, ys, k) for k in ks]
+
+    def hoist_modup(self, a: Ct) -> list:
+        """ModUp of every digit of c1 (coefficient form over Q_l u P), shared by the
+        hoisted rotations of `a`."""
+        P = self.P
+        l = a.level
+        ys = []
+        for j in range(-(-(l + 1) // P.alpha)):
+            y = np.empty((l + 1 + P.K, P.n), dtype=np.uint64)
+            lib().or_modup(P.n, l, _arr(P.q), P.K, _arr(P.p), P.alpha, j, _arr(a.c[1]), y)
+            ys.append(y)
+        return ys
+
+    def hoisted_step(self, a: Ct, ys: list, k: int) -> Ct:
+        P = self.P
+        l = a.level
+        kn = k % (P.n // 2)
+        if kn == 0:
+            return a
+        if kn not in self.gk:
+            raise KeyError(f"missing Galois key for rotation {kn}")
+        self._rec("hrot_hoisted", l, str(kn))
+        basis = list(P.q[: l + 1]) + list(P.p)
+        nkey = P.L + 1 + P.K
+        g = galois_element(P, kn)
+        evk = self.gk[kn]
+        acc0 = np.zeros((l + 1 + P.K, P.n), dtype=np.uint64)
+        acc1 = np.zeros_like(acc0)
+        for j, y in enumerate(ys):
+            sy = automorphism(basis, y, g)
+            kb = np.concatenate([evk[j, 0, : l + 1], evk[j, 0, P.L + 1: nkey]])
+            ka = np.concatenate([evk[j, 1, : l + 1], evk[j, 1, P.L + 1: nkey]])
+            acc0 = poly_add(basis, acc0, poly_mul(basis, sy, kb))
+            acc1 = poly_add(basis, acc1, poly_mul(basis, sy, ka))
+        d0 = np.empty((l + 1, P.n), dtype=np.uint64)
+        d1 = np.empty_like(d0)
+        lib().or_moddown(P.n, l, _arr(P.q), P.K, _arr(P.p), _arr(acc0), d0)
+        lib().or_moddown(P.n, l, _arr(P.q), P.K, _arr(P.p), _arr(acc1), d1)
+        qs = self.qs(l)
+        return Ct([poly_add(qs, automorphism(qs, a.c[0], g), d0), d1], l, a.scale, a.n_slots)
+
     def rescale(self, a: Ct) -> Ct:
         """Divide by q_level with the pinned round-half-up rule (c-5)."""
         if len(a.c) != 2:

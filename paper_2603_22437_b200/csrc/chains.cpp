@@ -151,6 +151,22 @@ class Runner {
 
     uint32_t frame_batch(uint32_t F) const { return cfg_.frame_batch ? std::min(cfg_.frame_batch, F) : F; }
 
+    // [x, Rot(x,1), ..., Rot(x,nb-1)]: plain HRots, or (cfg.hoist) hoisted HRots sharing one ModUp
+    std::vector<DCt> baby_steps(const DCt &x, uint32_t nb)
+    {
+        std::vector<DCt> out;
+        out.push_back(copy_ct(c_, x));
+        if (cfg_.hoist) {
+            std::vector<int32_t> st;
+            for (uint32_t b = 1; b < nb; ++b) st.push_back((int32_t)b);
+            if (!st.empty())
+                for (auto &r : ev_rotate_hoisted(c_, x, st)) out.push_back(std::move(r));
+        } else {
+            for (uint32_t b = 1; b < nb; ++b) out.push_back(ev_rotate(c_, x, (int32_t)b));
+        }
+        return out;
+    }
+
     // ---------------------------------------------------------- K1 / K2
     DCt k1_energy(const DCt &re, const DCt &im)
     {
@@ -193,11 +209,7 @@ class Runner {
     {
         const uint32_t n = vre.n_slots, D = cfg_.D, lvl = vre.level;
         Sched s = k3_schedule(cfg_);
-        std::vector<DCt> xr, xi;
-        xr.push_back(copy_ct(c_, vre));
-        xi.push_back(copy_ct(c_, vim));
-        for (uint32_t b = 1; b < s.b; ++b) xr.push_back(ev_rotate(c_, vre, (int32_t)b));
-        for (uint32_t b = 1; b < s.b; ++b) xi.push_back(ev_rotate(c_, vim, (int32_t)b));
+        std::vector<DCt> xr = baby_steps(vre, s.b), xi = baby_steps(vim, s.b);
         // W = hann[m] e^{-j 2 pi sigma(d) m / D}, diagonal o of I (x) W, pre-rotated by -G
         auto diag = [&](bool imag, int32_t o, int32_t G, bool neg) {
             std::vector<double> w = hann(D), v(n, 0.0);
@@ -295,9 +307,7 @@ class Runner {
             W = &c_.fc_w[layer - 1];
             bias = &c_.fc_b[layer - 1];
         }
-        std::vector<DCt> babies;
-        babies.push_back(copy_ct(c_, x));
-        for (uint32_t b = 1; b < std::min(s.b, h); ++b) babies.push_back(ev_rotate(c_, x, (int32_t)b));
+        std::vector<DCt> babies = baby_steps(x, std::min(s.b, h));
         DCt acc;
         bool first = true;
         for (auto &g : s.giants) {

@@ -311,34 +311,49 @@ DCt ev_add_plain(Ctx &c, const DCt &a, const DPlain &pt)
 }
 
 // ------------------------------------------------------------------ key switching
-void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t B, const DKey &key,
-                  uint64_t *out, size_t os, const uint64_t *add, size_t as, bool add_poly1)
+namespace {
+// ModUp of B polynomials x_b (NTT form, item stride xs): y [B][T][N] in NTT form,
+// digit j's n_tgt rows at offset off[j] (rows inside I_j are x itself and not stored).
+struct ModUpOut {
+    DBuf y;
+    std::vector<size_t> off;
+    std::vector<uint32_t> rowmap;
+    size_t T = 0;
+};
+
+ModUpOut ks_modup(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t B)
 {
     const size_t N = c.n;
     const size_t lw = (size_t)(l + 1) * N;
-    // 1. coefficient form of every x_b
+    ModUpOut m;
+    // coefficient form of every x_b
     DBuf xc(B * lw, c.stream);
     CUDA_CHECK(cudaMemcpy2DAsync(xc.get(), lw * 8, x_ntt, xs * 8, lw * 8, B, cudaMemcpyDeviceToDevice, c.stream));
     ntt_inverse(c, xc.get(), B * (l + 1), qmap(c, l));
-    // 2. ModUp: fast BConv of every digit, then NTT of the converted rows
+    // fast BConv of every digit, then NTT of the converted rows
     const auto &plans = c.modup[l];
-    std::vector<size_t> off;
-    std::vector<uint32_t> rowmap;
     const std::vector<uint32_t> basis = c.ext_basis(l);
-    size_t T = 0;
     for (const auto &p : plans) {
-        off.push_back(T);
+        m.off.push_back(m.T);
         for (uint32_t r = 0; r < basis.size(); ++r)
-            if (r < p.lo || r >= p.hi) rowmap.push_back(basis[r]);
-        T += p.n_tgt;
+            if (r < p.lo || r >= p.hi) m.rowmap.push_back(basis[r]);
+        m.T += p.n_tgt;
     }
-    DBuf y(B * T * N, c.stream);
-    launch_modup_bconv(c, y.get(), T * N, xc.get(), lw, l, off, B);
-    ntt_forward(c, y.get(), (uint32_t)(B * T), make_map(rowmap));
-    // 3. key inner product (each evk word fetched once for the batch)
+    m.y = DBuf(B * m.T * N, c.stream);
+    launch_modup_bconv(c, m.y.get(), m.T * N, xc.get(), lw, l, m.off, B);
+    ntt_forward(c, m.y.get(), (uint32_t)(B * m.T), make_map(m.rowmap));
+    return m;
+}
+
+// Key inner product (each evk word fetched once per batch split) + ModDown.
+void ks_ip_moddown(Ctx &c, const uint64_t *x_ntt, size_t xs, const uint64_t *y, const ModUpOut &m, uint32_t l,
+                   uint32_t B, const DKey &key, uint64_t *out, size_t os, const uint64_t *add, size_t as,
+                   bool add_poly1)
+{
+    const size_t N = c.n;
+    const size_t lw = (size_t)(l + 1) * N;
     DBuf accQ(B * 2 * lw, c.stream), accP(B * 2 * c.K * N, c.stream);
-    launch_key_ip(c, accQ.get(), accP.get(), x_ntt, xs, y.get(), T * N, off, key.buf.get(), l, B);
-    // 4. ModDown
+    launch_key_ip(c, accQ.get(), accP.get(), x_ntt, xs, y, m.T * N, m.off, key.buf.get(), l, B);
     std::vector<uint32_t> pm;
     for (uint32_t k = 0; k < c.K; ++k) pm.push_back(c.L + 1 + k);
     ntt_inverse(c, accP.get(), B * 2 * c.K, make_map(pm));
@@ -346,6 +361,51 @@ void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t
     launch_moddown_bconv(c, w.get(), accP.get(), l, B);
     ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l));
     launch_moddown_final(c, out, os, accQ.get(), w.get(), add, as, add_poly1, l, B);
+}
+}  // namespace
+
+void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t B, const DKey &key,
+                  uint64_t *out, size_t os, const uint64_t *add, size_t as, bool add_poly1)
+{
+    ModUpOut m = ks_modup(c, x_ntt, xs, l, B);
+    ks_ip_moddown(c, x_ntt, xs, m.y.get(), m, l, B, key, out, os, add, as, add_poly1);
+}
+
+std::vector<DCt> ev_rotate_hoisted(Ctx &c, const DCt &a, const std::vector<int32_t> &steps)
+{
+    MMFHE_REQUIRE(a.npolys == 2, MMFHE_E_LAYOUT, "rotate needs a 2-poly ciphertext");
+    const uint32_t l = a.level, B = a.batch;
+    std::vector<DCt> out;
+    bool need = false;
+    for (int32_t s : steps) {
+        int32_t k;
+        galois_element(c, s, &k);
+        if (k) {
+            find_gk(c, k);  // fail before any work on a missing key
+            need = true;
+        }
+    }
+    ModUpOut m;
+    if (need) m = ks_modup(c, a.poly(1), a.item_words(), l, B);
+    for (int32_t s : steps) {
+        int32_t k;
+        const uint64_t g = galois_element(c, s, &k);
+        if (k == 0) {
+            out.push_back(copy_ct(c, a));
+            continue;
+        }
+        const DKey &key = find_gk(c, k);
+        rec_n(c, "hrot_hoisted", l, B, std::to_string(k));
+        // sigma_g on (c0, c1) and on the ModUp'd digits: an NTT-domain permutation of every row
+        DBuf sig(a.item_words() * B, c.stream), sy(B * m.T * c.n, c.stream);
+        launch_automorph(c, sig.get(), a.data(), a.rows(), g);
+        launch_automorph(c, sy.get(), m.y.get(), (uint32_t)(B * m.T), g);
+        DCt r = make_ct(c, l, 2, a.n_slots, a.scale, B);
+        ks_ip_moddown(c, sig.get() + a.poly_words(), a.item_words(), sy.get(), m, l, B, key, r.data(),
+                      r.item_words(), sig.get(), a.item_words(), false);
+        out.push_back(std::move(r));
+    }
+    return out;
 }
 
 DCt ev_relin(Ctx &c, const DCt &a3)

@@ -44,6 +44,10 @@ void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t level, uint
                   uint64_t *out, size_t os, const uint64_t *add, size_t as, bool add_poly1);
 DCt ev_relin(Ctx &c, const DCt &a3);
 DCt ev_rotate(Ctx &c, const DCt &a, int32_t step);
+// Hoisted HRot: one ModUp of c1 shared by every step; per step the
+// ModUp'd digits are permuted by sigma_g, then IP + ModDown.  A separate op from
+// ev_rotate (different residues, same decryption).
+std::vector<DCt> ev_rotate_hoisted(Ctx &c, const DCt &a, const std::vector<int32_t> &steps);
 DCt ev_rescale(Ctx &c, const DCt &a);
 DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride);
 

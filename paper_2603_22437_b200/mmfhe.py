@@ -53,11 +53,12 @@ class ChainCfg(ctypes.Structure):
 
 
 def chain_cfg(R=0, D=0, A=0, F=0, gamma=1, p_phi=1, taylor_order=1, n_slots=0, bsgs_baby=0,
-              fc_dims=(0, 0, 0, 0), notch_width=1, bands_bins=(), n_taps=(), fs=0.0, frame_batch=0) -> ChainCfg:
+              fc_dims=(0, 0, 0, 0), notch_width=1, bands_bins=(), n_taps=(), fs=0.0, frame_batch=0,
+              hoist=0) -> ChainCfg:
     c = ChainCfg()
     c.R, c.D, c.A, c.F = R, D, A, F
     c.gamma, c.p_phi, c.taylor_order, c.n_slots, c.bsgs_baby = gamma, p_phi, taylor_order, n_slots, bsgs_baby
-    c.frame_batch = frame_batch
+    c.frame_batch, c.hoist = frame_batch, hoist
     for i, v in enumerate(fc_dims):
         c.fc_dims[i] = int(v)
     c.notch_width = notch_width
@@ -108,6 +109,7 @@ def lib():
             "mmfhe_hmult": [V, CTP, CTP, CTP],
             "mmfhe_relin": [V, CTP, CTP],
             "mmfhe_hrot": [V, CTP, I32, CTP],
+            "mmfhe_hrot_hoisted": [V, CTP, P(I32), S, CTP],
             "mmfhe_rescale": [V, CTP, CTP],
             "mmfhe_keyswitch": [V, CTP, I32, ctypes.c_int, CTP],
             "mmfhe_mod_switch": [V, CTP, U32, CTP],
@@ -136,7 +138,7 @@ EXPORTED = [
     "mmfhe_chain_required_rotations", "mmfhe_load_relin_key", "mmfhe_load_galois_key", "mmfhe_load_plain",
     "mmfhe_encode_plain", "mmfhe_prepare_chain", "mmfhe_load_scalars", "mmfhe_chain_plan", "mmfhe_eval_chain",
     "mmfhe_sum_partials", "mmfhe_ntt", "mmfhe_intt", "mmfhe_hadd", "mmfhe_hsub", "mmfhe_pmult", "mmfhe_hmult",
-    "mmfhe_relin", "mmfhe_hrot", "mmfhe_rescale", "mmfhe_keyswitch", "mmfhe_mod_switch", "mmfhe_hrot_batch",
+    "mmfhe_relin", "mmfhe_hrot", "mmfhe_hrot_hoisted", "mmfhe_rescale", "mmfhe_keyswitch", "mmfhe_mod_switch", "mmfhe_hrot_batch",
     "mmfhe_hmult_batch", "mmfhe_trace_get", "mmfhe_trace_clear", "mmfhe_trace_enable", "mmfhe_profile_enable",
     "mmfhe_profile_get", "mmfhe_microbench",
 ]
@@ -314,6 +316,15 @@ class Context:
 
     def hrot(self, a, step, out):
         return self._unary("mmfhe_hrot", a, out, int(step))
+
+    def hrot_hoisted(self, a, steps, outs):
+        sa = a.struct()
+        st = (ctypes.c_int32 * len(steps))(*[int(s) for s in steps])
+        o = (CT * len(outs))(*[c.struct() for c in outs])
+        self._check(self._lib.mmfhe_hrot_hoisted(self.h, ctypes.byref(sa), st, len(steps), o))
+        for c, s in zip(outs, o):
+            c.level, c.scale, c.n_slots = s.level, s.scale, s.n_slots
+        return outs
 
     def rescale(self, a, out):
         return self._unary("mmfhe_rescale", a, out)

@@ -28,7 +28,7 @@ def _mcfg(m, cfg: cc.ChainCfg, bins=(), taps=()):
     return m.chain_cfg(R=cfg.R, D=cfg.D, A=cfg.A, F=cfg.F, gamma=cfg.gamma, p_phi=cfg.p_phi,
                        taylor_order=cfg.taylor_order, n_slots=cfg.n_slots, bsgs_baby=cfg.bsgs_baby,
                        fc_dims=cfg.fc_dims, notch_width=cfg.notch_width, bands_bins=bins,
-                       n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch)
+                       n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch, hoist=cfg.hoist)
 
 
 def _run(m, P, keys, book, chain, cfg, cts, want, scalars=None, bins=(), taps=()):
@@ -84,17 +84,18 @@ def test_vitals_v1_small(m):
     assert sorted(ctx.required_rotations("vitals_v1", _mcfg(m, cfg))) == cc.required_rotations("vitals_v1", cfg, P.n)
 
 
-def _gesture(P, seed, F=2, A=2, R=4, D=8, frame_batch=0):
+def _gesture(P, seed, F=2, A=2, R=4, D=8, frame_batch=0, hoist=0):
     n = A * R * D
-    cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8), frame_batch=frame_batch)
+    cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8), frame_batch=frame_batch,
+                      hoist=hoist)
     Z, _ = radar.gesture_scene(A, R, D, F, seed=seed, cls=seed % 5)
     return cfg, radar.preprocess_gesture(Z)
 
 
-@pytest.mark.parametrize("F,fb", [(2, 0), (3, 2)])
-def test_gesture_chain_small(m, F, fb):
+@pytest.mark.parametrize("F,fb,hoist", [(2, 0, 0), (3, 2, 0), (3, 2, 1)])
+def test_gesture_chain_small(m, F, fb, hoist):
     P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
-    cfg, Zt = _gesture(P, 3201, F=F, frame_batch=fb)
+    cfg, Zt = _gesture(P, 3201, F=F, frame_batch=fb, hoist=hoist)
     keys = orc.keygen(P, seed=3202, rotations=cc.required_rotations("gesture", cfg, P.n))
     cts = []
     for t in range(cfg.F):

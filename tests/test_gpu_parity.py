@@ -112,6 +112,21 @@ def test_hrot_parity(m, toy_keys, step, level):
     assert ctx.trace() == ev.trace
 
 
+@pytest.mark.parametrize("level", [5, 3, 0])
+def test_hrot_hoisted_parity(m, toy_keys, level):
+    P, keys = toy_keys
+    ctx = make_ctx(m, P, keys)
+    a = _rand_ct(P, level, 65 + level)
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    steps = [1, 3, -1, 100, 0]
+    want = ev.rotate_hoisted(a, steps)
+    outs = [ct_out(m, P, level) for _ in steps]
+    ctx.hrot_hoisted(ct_in(m, P, a), steps, outs)
+    for o, w in zip(outs, want):
+        assert np.array_equal(residues(o), np.stack(w.c))
+    assert ctx.trace() == ev.trace
+
+
 @pytest.mark.parametrize("level", [5, 2])
 def test_hmult_relin_parity(m, toy_keys, level):
     P, keys = toy_keys

@@ -138,9 +138,11 @@ def _gesture_setup(P, A=2, R=4, D=8, F=2, seed=5):
     return cfg, Zt
 
 
-def test_gesture_frame_and_fc(Pg):
+@pytest.mark.parametrize("hoist", [0, 1])
+def test_gesture_frame_and_fc(Pg, hoist):
     P = Pg
     cfg, Zt = _gesture_setup(P)
+    cfg.hoist = hoist
     keys = orc.keygen(P, seed=2002, rotations=cc.required_rotations("gesture", cfg, P.n))
     ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
     book = cc.PlainBook(P)

@@ -88,6 +88,28 @@ def test_hadd_hmult_rotate(P, keys):
     assert np.max(np.abs(orc.decrypt_vector(P, keys, ev.rotate(cr, 1)) - np.roll(ramp, -1))) < 2 ** -20
 
 
+def test_hoisted_rotation(P, keys):
+    # hoisted HRot decrypts to the rotation, but is a different op:
+    # BConv does not commute with sigma_g's sign flips, so residues differ from rotate()
+    rng = np.random.default_rng(9)
+    n = 128
+    a = rng.uniform(-1, 1, n)
+    ca = orc.encrypt_vector(P, keys, a, P.L, seed=8, index=0)
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    outs = ev.rotate_hoisted(ca, [1, 3, -1, 64, 0])
+    for k, c in zip([1, 3, -1, 64], outs):
+        assert np.max(np.abs(orc.decrypt_vector(P, keys, c) - np.roll(a, -k))) < 2 ** -20
+    assert outs[4] is ca
+    plain = ev.rotate(ca, 3)
+    assert not np.array_equal(np.stack(plain.c), np.stack(outs[1].c))
+    assert [t for t in ev.trace if t[0] == "hrot_hoisted"] == [("hrot_hoisted", P.L, s) for s in
+                                                               ("1", "3", str(P.n // 2 - 1), "64")]
+    # lower level: digits truncated at level l (SURVEY c-5 "Keys")
+    low = orc.Ct([x[:3].copy() for x in ca.c], 2, ca.scale, ca.n_slots)
+    r = ev.rotate_hoisted(low, [5])[0]
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, r) - np.roll(a, -5))) < 2 ** -20
+
+
 def test_plain_mult_and_scalar(P, keys):
     rng = np.random.default_rng(4)
     n = 128
