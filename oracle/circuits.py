@@ -185,6 +185,17 @@ def k1_energy(ev: CircuitEvaluator, re_list, im_list) -> orc.Ct:
     return ev.relin_rescale_all([ev.tensor_sum(pairs)])[0]
 
 
+def k1_energy_sessions(ev: CircuitEvaluator, sessions):
+    """K1 for several independent sessions [(re_list, im_list), ...], op-major."""
+    ts = []
+    for re_list, im_list in sessions:
+        pairs = []
+        for re, im in zip(re_list, im_list):
+            pairs += [(re, re), (im, im)]
+        ts.append(ev.tensor_sum(pairs))
+    return ev.relin_rescale_all(ts)
+
+
 def k2_soft_attention(ev: CircuitEvaluator, book: PlainBook, E: orc.Ct, cfg: ChainCfg):
     """K2a: w = E^gamma by log2(gamma) squarings; N = rotsum_R(w (.) ramp'),
     D = rotsum_R(w (.) one'), ramp'_r = r/(F^2 R), one'_r = 1/(F^2 R)."""

@@ -181,6 +181,17 @@ class Runner {
         return ev_relin_rescale(c_, ev_tensor_sum(c_, pairs));
     }
 
+    // K1 for S sessions at once: re[t], im[t] are batches over the sessions
+    DCt k1_energy_sessions(const std::vector<DCt> &re, const std::vector<DCt> &im)
+    {
+        std::vector<std::pair<const DCt *, const DCt *>> pairs;
+        for (size_t t = 0; t < re.size(); ++t) {
+            pairs.push_back({&re[t], &re[t]});
+            pairs.push_back({&im[t], &im[t]});
+        }
+        return ev_relin_rescale(c_, ev_tensor_sum(c_, pairs));
+    }
+
     std::pair<DCt, DCt> k2_soft_attention(const DCt &E)
     {
         DCt w = copy_ct(c_, E);
@@ -524,10 +535,17 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
                   "chain " + chain + " needs " + std::to_string(dep) + " levels, input has " +
                       std::to_string(in_level));
     const uint32_t out = in_level - dep;
-    if (chain == "k1_energy" || chain == "vitals_v1" || chain == "vitals_v2" || chain == "gesture") {
+    size_t n_out = 1;
+    if (chain == "k1_energy") {
+        // S independent sessions of F frames: inputs session-major, (re_t, im_t) per frame
+        MMFHE_REQUIRE(cfg.F > 0 && n_in % (2 * (size_t)cfg.F) == 0, MMFHE_E_SHAPE,
+                      "expected 2F input ciphertexts per session");
+        n_out = n_in / (2 * (size_t)cfg.F);
+    } else if (chain == "vitals_v1" || chain == "vitals_v2" || chain == "gesture") {
         MMFHE_REQUIRE(n_in == 2 * (size_t)cfg.F && cfg.F > 0, MMFHE_E_SHAPE, "expected 2F input ciphertexts");
     } else if (chain == "k3_doppler_dft" || chain == "gesture_frame") {
-        MMFHE_REQUIRE(n_in == 2, MMFHE_E_SHAPE, "expected (v_re, v_im)");
+        MMFHE_REQUIRE(n_in >= 2 && n_in % 2 == 0, MMFHE_E_SHAPE, "expected (v_re, v_im) per frame");
+        n_out = chain == "k3_doppler_dft" ? n_in : n_in / 2;
     } else if (chain == "gesture_fc") {
         MMFHE_REQUIRE(n_in == 1, MMFHE_E_SHAPE, "expected one feature ciphertext");
     }
@@ -536,8 +554,7 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
         for (uint32_t b = 0; b < cfg.n_bands; ++b)
             MMFHE_REQUIRE(cfg.n_bins[b] >= 1 && cfg.n_bins[b] <= 64, MMFHE_E_SHAPE, "1..64 DFT bins per band");
     }
-    size_t n_out = 1;
-    if (chain == "vitals_v1" || chain == "k3_doppler_dft") n_out = 2;
+    if (chain == "vitals_v1") n_out = 2;
     if (chain == "vitals_v2") {
         n_out = 0;
         for (uint32_t b = 0; b < cfg.n_bands; ++b) n_out += cfg.n_bins[b];
@@ -552,28 +569,37 @@ std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_c
     chain_plan(c, chain, cfg, in[0].level, n_in);
     Runner r(c, cfg);
     std::vector<DCt> out;
-    if (chain == "k1_energy" || chain == "vitals_v1") {
+    if (chain == "k1_energy") {
+        // sessions batched: frame t of every session forms one batch (one launch per op)
+        const uint32_t F = cfg.F, S = (uint32_t)(n_in / (2 * (size_t)F));
+        std::vector<DCt> re, im;
+        for (uint32_t t = 0; t < F; ++t) {
+            re.push_back(import_batch(c, in, 2 * (size_t)t, 2 * (size_t)F, S));
+            im.push_back(import_batch(c, in, 2 * (size_t)t + 1, 2 * (size_t)F, S));
+        }
+        out.push_back(r.k1_energy_sessions(re, im));
+    } else if (chain == "vitals_v1") {
         DCt re = import_batch(c, in, 0, 2, n_in / 2);
         DCt im = import_batch(c, in, 1, 2, n_in / 2);
-        DCt E = r.k1_energy(re, im);
-        if (chain == "k1_energy") {
-            out.push_back(std::move(E));
-        } else {
-            auto nd = r.k2_soft_attention(E);
-            out.push_back(std::move(nd.first));
-            out.push_back(std::move(nd.second));
-        }
+        auto nd = r.k2_soft_attention(r.k1_energy(re, im));
+        out.push_back(std::move(nd.first));
+        out.push_back(std::move(nd.second));
     } else if (chain == "vitals_v2") {
         out = r.vitals_v2(in, n_in);
     } else if (chain == "k3_doppler_dft" || chain == "gesture_frame") {
-        DCt vre = import_batch(c, in, 0, 1, 1);
-        DCt vim = import_batch(c, in, 1, 1, 1);
-        if (chain == "k3_doppler_dft") {
-            auto d = r.k3_doppler_dft(vre, vim);
-            out.push_back(std::move(d.first));
-            out.push_back(std::move(d.second));
-        } else {
-            out.push_back(r.gesture_frame(vre, vim));
+        // frames in batches of cfg.frame_batch; k3 outputs per batch: its d_re items, then its d_im items
+        const uint32_t F = (uint32_t)(n_in / 2), fb = r.frame_batch(F);
+        for (uint32_t t0 = 0; t0 < F; t0 += fb) {
+            const uint32_t cnt = std::min(fb, F - t0);
+            DCt vre = import_batch(c, in, 2 * (size_t)t0, 2, cnt);
+            DCt vim = import_batch(c, in, 2 * (size_t)t0 + 1, 2, cnt);
+            if (chain == "k3_doppler_dft") {
+                auto d = r.k3_doppler_dft(vre, vim);
+                out.push_back(std::move(d.first));
+                out.push_back(std::move(d.second));
+            } else {
+                out.push_back(r.gesture_frame(vre, vim));
+            }
         }
     } else if (chain == "gesture_fc") {
         DCt x = import_batch(c, in, 0, 1, 1);

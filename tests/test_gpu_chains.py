@@ -71,6 +71,38 @@ def test_k1_energy_c1_full_size(m):
     assert np.max(np.abs(E_dec - want)) <= 1e-3 * np.max(np.abs(want))
 
 
+def test_k1_energy_multi_session(m):
+    """C1/C5 serving shape: S sessions in one call, batched over sessions."""
+    P = toy(log_n=11, n_q=3, scale_bits=40, n_p=1, alpha=1)
+    cfg = cc.ChainCfg(R=16, F=4, n_slots=P.n // 2)
+    keys = orc.keygen(P, seed=3011)
+    sessions, cts = [], []
+    for s in range(3):
+        _, c = _vital_inputs(P, keys, cfg, 1, 3020 + 10 * s)
+        sessions.append((c[0::2], c[1::2]))
+        cts += c
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    want = cc.k1_energy_sessions(ev, sessions)
+    ctx = _run(m, P, keys, None, "k1_energy", cfg, cts, want)
+    assert ctx.trace() == ev.trace
+
+
+def test_k3_multi_frame_batches(m):
+    P = toy(log_n=10, n_q=4, scale_bits=40, n_p=2, alpha=2)
+    cfg = cc.ChainCfg(A=2, R=4, D=8, F=3, n_slots=64, frame_batch=2, hoist=1)
+    keys = orc.keygen(P, seed=3031, rotations=cc.required_rotations("k3_doppler_dft", cfg, P.n))
+    rng = np.random.default_rng(3)
+    cts = [orc.encrypt_vector(P, keys, rng.uniform(-1, 1, 64), P.L, seed=3032, index=i) for i in range(6)]
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    want = []
+    for s, e in cc.chunks(3, 2):
+        dre, dim = cc.k3_doppler_dft_frames(ev, book, cts[2 * s:2 * e:2], cts[2 * s + 1:2 * e:2], cfg)
+        want += dre + dim
+    ctx = _run(m, P, keys, book, "k3_doppler_dft", cfg, cts, want)
+    assert ctx.trace() == ev.trace
+
+
 def test_vitals_v1_small(m):
     P = toy(log_n=10, n_q=6, scale_bits=40, n_p=2, alpha=2)
     cfg = cc.ChainCfg(R=16, F=6, gamma=2, n_slots=P.n // 2)
