@@ -250,10 +250,80 @@ def run_gpu(args, rank, world, device):
         e2e = {"value": cfg["F"] * world / e_s, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_s * 1e3, "clock": "host wall, per rank"}
 
-    extras = {} if args.no_extras else extras_n16(args, m, torch, device)
+    extras = {}
+    if not args.no_extras:
+        extras = extras_n16(args, m, torch, device)
+        for wl in ("C1", "C3", "C4"):
+            try:
+                extras[wl] = bench_workload(wl, m, torch, device)
+            except Exception as e:  # report, do not hide
+                extras[wl] = {"error": f"{type(e).__name__}: {e}"}
     return dict(value=value, ms=ms_max / args.steps, launches=launches, clocks=clk.summary(), prof=prof,
                 prof_steps=prof_steps, prof_ms=prof_ms / prof_steps, e2e=e2e, extras=extras, cfg=cfg, P=P,
                 int_peaks=int_peaks)
+
+
+def bench_workload(name, m, torch, device, steps=2, warmup=1):
+    """Encrypted frames/s of the other BASELINE.json configs (SURVEY §8(d) definitions),
+    device-resident coefficient-form inputs, CUDA events on the library stream:
+      C1: K1 energy, N=2^13 (PS1), R=64, F=32, 256 sessions per step (frames = sessions*F);
+      C3: K3 Doppler DFT, N=2^15 (PS3), A=4 x R=32 x D=32, 32 frames per step, hoisted baby steps;
+      C4: gesture session, N=2^16 (PS4, entry level 19), F=100 frames + FC 4096->64->32->5."""
+    from synth import radar
+    from synth.params import ps1, ps3, ps4
+    stream = torch.cuda.current_stream(device)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(7000 + ord(name[1]))
+    if name == "C1":
+        P = ps1()
+        cfg = m.chain_cfg(R=64, F=32, n_slots=P.n // 2)
+        chain, lvl, n_in, frames, info = "k1_energy", 1, 2 * 32 * 256, 32 * 256, "256 sessions x F=32"
+    elif name == "C3":
+        P = ps3()
+        cfg = m.chain_cfg(A=4, R=32, D=32, n_slots=4096, frame_batch=32, hoist=1)
+        chain, lvl, n_in, frames, info = "k3_doppler_dft", P.L, 64, 32, "32 frames, frame_batch 32, hoisted"
+    else:
+        P = ps4()
+        cfg = m.chain_cfg(A=4, R=32, D=32, F=100, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8),
+                          frame_batch=25, hoist=1)
+        chain, lvl, n_in, frames, info = "gesture", 19, 200, 100, "F=100 frames, frame_batch 25, hoisted"
+    ctx = m.Context.from_params(P, device=device.index or 0, stream=stream.cuda_stream)
+    basis = list(P.q) + list(P.p)
+    key_shape = (P.dnum(), 2, len(basis))
+    ctx.load_relin_key(uniform_dev(torch, gen, key_shape, basis, P.n, device))
+    for k in ctx.required_rotations(chain, cfg):
+        ctx.load_galois_key(k, uniform_dev(torch, gen, key_shape, basis, P.n, device))
+    fc_w = fc_b = None
+    if chain == "gesture":
+        Ws, bs = radar.fc_weights([4096, 64, 32, 5], seed=11)
+        Ws[-1] = np.vstack([Ws[-1], np.zeros((3, 32))])
+        bs[-1] = np.concatenate([bs[-1], np.zeros(3)])
+        fc_w, fc_b = Ws, bs
+    ctx.prepare_chain(chain, cfg, lvl, fc_w=fc_w, fc_b=fc_b)
+    scale = float(2 ** P.scale_bits)
+    data = uniform_dev(torch, gen, (n_in, 2, lvl + 1), list(P.q[: lvl + 1]), P.n, device)
+    ins = [m.Ct(data[i], lvl, scale, cfg.n_slots, P.log_n) for i in range(n_in)]
+    outs = [m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=device), lv, 0.0, 0, P.log_n)
+            for lv in ctx.chain_plan(chain, cfg, lvl, n_in)]
+    ctx.trace_enable(False)
+    for _ in range(warmup):
+        ctx.eval_chain(chain, cfg, ins, outs)
+    torch.cuda.synchronize(device)
+    l0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        ctx.eval_chain(chain, cfg, ins, outs)
+    e1.record(stream)
+    torch.cuda.synchronize(device)
+    ms = e0.elapsed_time(e1) / steps
+    res = {"frames_per_s": frames / (ms / 1e3), "ms_per_step": ms, "frames_per_step": frames,
+           "gpu_launches_per_step": (ctx.launch_count() - l0) // steps,
+           "config": f"{chain} at N=2^{P.log_n} ({len(P.q)} Q + {len(P.p)} P limbs, entry level {lvl}), {info}"}
+    ctx.close()
+    del data, ins, outs
+    torch.cuda.empty_cache()
+    return res
 
 
 def extras_n16(args, m, torch, device, batch=8, reps=3):
