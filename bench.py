@@ -125,7 +125,7 @@ def make_ctx_c2(m, torch, P, cfg, device, seed):
     key_shape = (P.dnum(), 2, len(basis))
     ctx.load_relin_key(uniform_dev(torch, gen, key_shape, basis, P.n, device))
     mcfg = chain_cfg_c2(m, cfg)
-    for k in ctx.required_rotations("vitals_v1", mcfg) + ctx.required_rotations("vitals_v2", mcfg):
+    for k in sorted(set(ctx.required_rotations("vitals_v1", mcfg) + ctx.required_rotations("vitals_v2", mcfg))):
         ctx.load_galois_key(k, uniform_dev(torch, gen, key_shape, basis, P.n, device))
     from synth.radar import fir_taps
     taps = [fir_taps(cfg["n_taps"], b, cfg["fs"]) for b in BANDS]
