@@ -258,6 +258,8 @@ def run_gpu(args, rank, world, device):
                 extras[wl] = bench_workload(wl, m, torch, device)
             except Exception as e:  # report, do not hide
                 extras[wl] = {"error": f"{type(e).__name__}: {e}"}
+    if not args.no_c5:
+        extras["C5"] = bench_c5(m, torch, device, rank, world)
     return dict(value=value, ms=ms_max / args.steps, launches=launches, clocks=clk.summary(), prof=prof,
                 prof_steps=prof_steps, prof_ms=prof_ms / prof_steps, e2e=e2e, extras=extras, cfg=cfg, P=P,
                 int_peaks=int_peaks)
@@ -317,13 +319,102 @@ def bench_workload(name, m, torch, device, steps=2, warmup=1):
     e1.record(stream)
     torch.cuda.synchronize(device)
     ms = e0.elapsed_time(e1) / steps
+    launches = (ctx.launch_count() - l0) // steps
+    ctx.profile_enable(True)
+    ctx.eval_chain(chain, cfg, ins, outs)
+    prof = ctx.profile()
+    ctx.profile_enable(False)
+    top = sorted(prof.items(), key=lambda kv: -kv[1][1])[:6]
     res = {"frames_per_s": frames / (ms / 1e3), "ms_per_step": ms, "frames_per_step": frames,
-           "gpu_launches_per_step": (ctx.launch_count() - l0) // steps,
+           "gpu_launches_per_step": launches,
+           "kernel_ms_top": {k: round(v[1], 3) for k, v in top},
+           "kernel_ms_total": round(sum(v[1] for v in prof.values()), 3),
            "config": f"{chain} at N=2^{P.log_n} ({len(P.q)} Q + {len(P.p)} P limbs, entry level {lvl}), {info}"}
     ctx.close()
     del data, ins, outs
     torch.cuda.empty_cache()
     return res
+
+
+def bench_c5(m, torch, device, rank, world, sessions_per_rank=1, F=100, steps=2, warmup=1):
+    """C5 batched multi-session gesture serving (BASELINE configs[4]) with the method's one
+    exchange step: G = sessions_per_rank * world sessions per step; every session's F
+    frames are sharded over the ranks (paper_2603_22437_b200.dist.shard); each rank runs
+    gesture_features on its shard of every session, the per-rank partial feature
+    ciphertexts are all-gathered over NCCL, and the owner of each session sums them in the
+    library (mmfhe_sum_partials) and runs the FC head.  Weak scaling: per-rank work is
+    fixed (F frames + sessions_per_rank FC heads per step)."""
+    from paper_2603_22437_b200 import dist as mdist
+    from synth import radar
+    from synth.params import ps4
+    import torch.distributed as tdist
+    distributed = tdist.is_available() and tdist.is_initialized()
+    P = ps4()
+    lvl = 19
+    stream = torch.cuda.current_stream(device)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(9100)  # same keys on every rank (the client's key set, replicated)
+    cfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25,
+                      hoist=1)
+    ctx = m.Context.from_params(P, device=device.index or 0, stream=stream.cuda_stream)
+    basis = list(P.q) + list(P.p)
+    key_shape = (P.dnum(), 2, len(basis))
+    ctx.load_relin_key(uniform_dev(torch, gen, key_shape, basis, P.n, device))
+    for k in ctx.required_rotations("gesture", cfg):
+        ctx.load_galois_key(k, uniform_dev(torch, gen, key_shape, basis, P.n, device))
+    Ws, bs = radar.fc_weights([4096, 64, 32, 5], seed=11)
+    Ws[-1] = np.vstack([Ws[-1], np.zeros((3, 32))])
+    bs[-1] = np.concatenate([bs[-1], np.zeros(3)])
+    ctx.prepare_chain("gesture", cfg, lvl, fc_w=Ws, fc_b=bs)
+    G = sessions_per_rank * world
+    lo, hi = mdist.shard(F, rank, world)
+    gen_in = torch.Generator(device=device)
+    gen_in.manual_seed(9200 + rank)
+    scale = float(2 ** P.scale_bits)
+    data = uniform_dev(torch, gen_in, (G, 2 * (hi - lo), 2, lvl + 1), list(P.q[: lvl + 1]), P.n, device)
+    frames_by_session = [[m.Ct(data[s, i], lvl, scale, 4096, P.log_n) for i in range(2 * (hi - lo))]
+                         for s in range(G)]
+    mine = [s for s in range(G) if mdist.owner(s, world) == rank]
+    ctx.trace_enable(False)
+
+    def step():
+        partials, lv, sc = mdist.sessions_features(ctx, m, cfg, frames_by_session, lvl, scale, 4096, P.log_n, device)
+        gathered = mdist.allgather_partials(partials)
+        logits = []
+        for s in mine:
+            total = mdist.reduce_partials(ctx, m, gathered, s, lv, sc, 4096, P.log_n)
+            lvo = ctx.chain_plan("gesture_fc", cfg, lv, 1)[0]
+            o = m.Ct(torch.empty((2, lvo + 1, P.n), dtype=torch.int64, device=device), lvo, 0.0, 0, P.log_n,
+                     m.FORM_EVAL)
+            ctx.eval_chain("gesture_fc", cfg, [total], [o])
+            logits.append(o)
+        return partials.numel() * 8
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(device)
+    if distributed:
+        tdist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        xbytes = step()
+    e1.record(stream)
+    torch.cuda.synchronize(device)
+    if distributed:
+        tdist.barrier()
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if distributed:
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    ctx.close()
+    del data, frames_by_session
+    torch.cuda.empty_cache()
+    return {"frames_per_s": G * F / (ms / 1e3), "ms_per_step": ms, "sessions_per_step": G, "frames_per_session": F,
+            "n_gpus": world, "allgather_bytes_per_rank_per_step": xbytes,
+            "config": "PS4 gesture sessions, frames sharded over ranks, NCCL all-gather of partial feature "
+                      "ciphertexts + library mod-q sum + FC on the owning rank; weak scaling in sessions"}
 
 
 def extras_n16(args, m, torch, device, batch=8, reps=3):
@@ -492,6 +583,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["mmfhe", "reference"], default="mmfhe")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the multi-GPU C5 exchange workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-frames", type=int, default=4)
     ap.add_argument("--profile-out", default="")

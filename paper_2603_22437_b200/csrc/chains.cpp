@@ -460,7 +460,8 @@ class Runner {
         return out;
     }
 
-    DCt gesture(const mmfhe_ct *in, size_t n_in)
+    // per frame batch: frame kernels, batch sum; batches added in order
+    DCt gesture_features(const mmfhe_ct *in, size_t n_in)
     {
         const uint32_t F = (uint32_t)(n_in / 2), fb = frame_batch(F);
         DCt acc;
@@ -472,8 +473,10 @@ class Runner {
             DCt part = ev_batch_sum(c_, f);
             acc = t0 == 0 ? std::move(part) : ev_addsub(c_, acc, part, false);
         }
-        return gesture_fc(acc);
+        return acc;
     }
+
+    DCt gesture(const mmfhe_ct *in, size_t n_in) { return gesture_fc(gesture_features(in, n_in)); }
 
   private:
     Ctx &c_;
@@ -492,6 +495,7 @@ uint32_t chain_depth(const std::string &chain, const mmfhe_chain_cfg &cfg)
     if (chain == "gesture_frame") return gf;
     if (chain == "gesture_fc") return fc;
     if (chain == "gesture") return gf + fc;
+    if (chain == "gesture_features") return gf;
     throw Error(MMFHE_E_INVALID_ARG, "unknown chain " + chain);
 }
 
@@ -508,12 +512,13 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
     chain_depth(chain, cfg);  // validates the name
     if (chain == "vitals_v1" || chain == "vitals_v2")
         for (uint32_t s : rotsum_steps(cfg.R, 1)) add(s);
-    if (chain == "k3_doppler_dft" || chain == "gesture_frame" || chain == "gesture") {
+    const bool frames = chain == "gesture_frame" || chain == "gesture" || chain == "gesture_features";
+    if (chain == "k3_doppler_dft" || frames) {
         Sched s = k3_schedule(cfg);
         for (uint32_t b = 1; b < s.b; ++b) add(b);
         for (auto &g : s.giants) add(g.G);
     }
-    if (chain == "gesture_frame" || chain == "gesture")
+    if (frames)
         for (uint32_t s : rotsum_steps(cfg.n_slots / cfg.D, cfg.D)) add(s);
     if (chain == "gesture_fc" || chain == "gesture")
         for (int layer = 0; layer < 3; ++layer) {
@@ -543,9 +548,9 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
         n_out = n_in / (2 * (size_t)cfg.F);
     } else if (chain == "vitals_v1" || chain == "vitals_v2" || chain == "gesture") {
         MMFHE_REQUIRE(n_in == 2 * (size_t)cfg.F && cfg.F > 0, MMFHE_E_SHAPE, "expected 2F input ciphertexts");
-    } else if (chain == "k3_doppler_dft" || chain == "gesture_frame") {
+    } else if (chain == "k3_doppler_dft" || chain == "gesture_frame" || chain == "gesture_features") {
         MMFHE_REQUIRE(n_in >= 2 && n_in % 2 == 0, MMFHE_E_SHAPE, "expected (v_re, v_im) per frame");
-        n_out = chain == "k3_doppler_dft" ? n_in : n_in / 2;
+        n_out = chain == "k3_doppler_dft" ? n_in : chain == "gesture_frame" ? n_in / 2 : 1;
     } else if (chain == "gesture_fc") {
         MMFHE_REQUIRE(n_in == 1, MMFHE_E_SHAPE, "expected one feature ciphertext");
     }
@@ -606,6 +611,8 @@ std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_c
         out.push_back(r.gesture_fc(x));
     } else if (chain == "gesture") {
         out.push_back(r.gesture(in, n_in));
+    } else if (chain == "gesture_features") {
+        out.push_back(r.gesture_features(in, n_in));
     }
     return out;
 }

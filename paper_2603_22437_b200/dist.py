@@ -1,0 +1,67 @@
+"""Multi-GPU plumbing for the mmFHE hot path.
+
+Units are independent (sessions, frames); the method's only exchange step is the
+cross-frame homomorphic sum ("accumulate across frames via addition",
+P:943) when one session's frames are spread over GPUs: each rank evaluates the
+frame kernels on its frame shard and sums them locally (chain
+``gesture_features``), the per-rank partial ciphertexts are all-gathered over
+NCCL/NVLink, and the modular sum of the gathered parts runs in the library
+(``mmfhe_sum_partials``) before the FC head.
+
+torch.distributed only moves bytes (NCCL on GPUs, gloo in the CPU tests); no
+arithmetic of the method happens here.
+"""
+from __future__ import annotations
+
+
+def shard(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced [start, stop) share of n units for `rank` (sizes differ by <= 1)."""
+    base, extra = divmod(n, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def owner(unit: int, world: int) -> int:
+    """Rank that finishes unit (session) `unit` after the exchange (round-robin)."""
+    return unit % world
+
+
+def allgather_partials(local, group=None):
+    """[k, ...] 64-bit tensor of per-rank partial ciphertexts -> [world, k, ...] on every
+    rank (rank order).  A no-op stack when torch.distributed is not initialised."""
+    import torch
+    import torch.distributed as dist
+
+    local = local.contiguous()
+    if not (dist.is_available() and dist.is_initialized()):
+        return local.unsqueeze(0)
+    world = dist.get_world_size(group)
+    k = local.shape[0]
+    out = torch.empty((world * k,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(out, local, group=group)  # rank-major concatenation
+    return out.view((world, k) + tuple(local.shape[1:]))
+
+
+def sessions_features(ctx, m, cfg, frames_by_session, level, scale, n_slots, log_n, device):
+    """Partial features of this rank's frame shard for every session: one ciphertext per
+    session, stacked [S, 2, level_out+1, N] (device, int64 view of the residues)."""
+    import torch
+
+    outs = []
+    for ins in frames_by_session:
+        lv = ctx.chain_plan("gesture_features", cfg, level, len(ins))[0]
+        o = m.Ct(torch.empty((2, lv + 1, 1 << log_n), dtype=torch.int64, device=device), lv, 0.0, 0, log_n,
+                 m.FORM_EVAL)
+        ctx.eval_chain("gesture_features", cfg, ins, [o])
+        outs.append(o)
+    return torch.stack([o.data for o in outs]), outs[0].level, outs[0].scale
+
+
+def reduce_partials(ctx, m, gathered, session, level, scale, n_slots, log_n):
+    """Library-side modular sum of session `session`'s partials from every rank."""
+    import torch
+
+    parts = [m.Ct(gathered[r, session], level, scale, n_slots, log_n, m.FORM_EVAL) for r in range(gathered.shape[0])]
+    out = m.Ct(torch.empty_like(gathered[0, session]), level, 0.0, 0, log_n, m.FORM_EVAL)
+    ctx.sum_partials(parts, out)
+    return out

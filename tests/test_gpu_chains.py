@@ -149,6 +149,41 @@ def test_gesture_chain_small(m, F, fb, hoist):
     _run(m, P, keys, book, "gesture_frame", cfg, cts[:2], [f0])
 
 
+def test_frame_sharded_gesture_exchange(m):
+    """frames of one session split over 'ranks' (here 3 shards on one GPU),
+    per-shard gesture_features, library sum of the partials, FC head -- equals the
+    oracle's single-device gesture pipeline residue for residue (sums are exact mod q)."""
+    from paper_2603_22437_b200.dist import shard
+    P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
+    cfg, Zt = _gesture(P, 3211, F=5, frame_batch=2, hoist=1)
+    keys = orc.keygen(P, seed=3212, rotations=cc.required_rotations("gesture", cfg, P.n))
+    cts = []
+    for t in range(cfg.F):
+        v = radar.pack_doppler(Zt[t])
+        for part in (v.real, v.imag):
+            cts.append(orc.encrypt_vector(P, keys, part, P.L, seed=3213, index=len(cts)))
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    feat = cc.gesture_features(ev, book, cts[0::2], cts[1::2], cfg)
+    dims = cfg.fc_dims
+    Ws, bs = radar.fc_weights([dims[0], dims[1], dims[2], 5], seed=3214)
+    logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
+    ctx = make_ctx(m, P, keys, book)
+    mcfg = _mcfg(m, cfg)
+    parts = []
+    for r in range(3):
+        lo, hi = shard(cfg.F, r, 3)
+        o = ct_out(m, P, feat.level)
+        ctx.eval_chain("gesture_features", mcfg, [ct_in(m, P, c) for c in cts[2 * lo:2 * hi]], [o])
+        parts.append(o)
+    total = ct_out(m, P, feat.level)
+    ctx.sum_partials(parts, total)
+    assert np.array_equal(residues(total), np.stack(feat.c)) and total.scale == feat.scale
+    out = ct_out(m, P, logits.level)
+    ctx.eval_chain("gesture_fc", mcfg, [total], [out])
+    assert np.array_equal(residues(out), np.stack(logits.c))
+
+
 def test_k3_doppler_dft_c3_full_size(m):
     """C3: block-diagonal Doppler DFT via slot rotations, N=2^15, A=4 x R=32 x D=32."""
     P = ps3()
