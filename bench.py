@@ -91,8 +91,13 @@ class ClockSampler:
                         pass
                     self._stop.wait(self.interval)
 
+            # first NVML queries cost ~0.3 s of process time: pay them before the timed region
+            for _ in range(3):
+                pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
             self._thread = threading.Thread(target=run, daemon=True)
             self._thread.start()
+            time.sleep(0.5)
         except Exception:
             self._thread = None
         return self
@@ -176,10 +181,12 @@ def run_gpu(args, rank, world, device):
     ins = session_inputs(m, torch, gen, P, cfg, device)
     outs = {c: outputs_for(m, torch, ctx, P, mcfg, c, ins[c], device) for c in ins}
     stream = torch.cuda.current_stream(device)
+    ins_a = {c: m.CtArray(ins[c]) for c in ins}      # marshalled once (binding-side cost only)
+    outs_a = {c: m.CtArray(outs[c]) for c in outs}
 
     def step():
         for chain in ("vitals_v1", "vitals_v2"):
-            ctx.eval_chain(chain, mcfg, ins[chain], outs[chain])
+            ctx.eval_chain(chain, mcfg, ins_a[chain], outs_a[chain])
 
     ctx.trace_enable(False)
     for _ in range(args.warmup):
@@ -192,6 +199,7 @@ def run_gpu(args, rank, world, device):
     launches0 = ctx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(device.index or 0) as clk:
+        torch.cuda.synchronize(device)
         ev0.record(stream)
         for _ in range(args.steps):
             step()
@@ -237,6 +245,8 @@ def run_gpu(args, rank, world, device):
             hout[c] = outs_h
         h2d = sum(x.data.numel() * 8 for c in hin for x in hin[c])
         d2h = sum(x.data.numel() * 8 for c in hout for x in hout[c])
+        hin = {c: m.CtArray(hin[c]) for c in hin}
+        hout = {c: m.CtArray(hout[c]) for c in hout}
         for chain in hin:  # warm host path
             ctx.eval_chain(chain, mcfg, hin[chain], hout[chain])
         torch.cuda.synchronize(device)
@@ -265,7 +275,7 @@ def run_gpu(args, rank, world, device):
                 int_peaks=int_peaks)
 
 
-def bench_workload(name, m, torch, device, steps=2, warmup=1):
+def bench_workload(name, m, torch, device, steps=2, warmup=2):
     """Encrypted frames/s of the other BASELINE.json configs (SURVEY §8(d) definitions),
     device-resident coefficient-form inputs, CUDA events on the library stream:
       C1: K1 energy, N=2^13 (PS1), R=64, F=32, 256 sessions per step (frames = sessions*F);
@@ -304,9 +314,9 @@ def bench_workload(name, m, torch, device, steps=2, warmup=1):
     ctx.prepare_chain(chain, cfg, lvl, fc_w=fc_w, fc_b=fc_b)
     scale = float(2 ** P.scale_bits)
     data = uniform_dev(torch, gen, (n_in, 2, lvl + 1), list(P.q[: lvl + 1]), P.n, device)
-    ins = [m.Ct(data[i], lvl, scale, cfg.n_slots, P.log_n) for i in range(n_in)]
-    outs = [m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=device), lv, 0.0, 0, P.log_n)
-            for lv in ctx.chain_plan(chain, cfg, lvl, n_in)]
+    ins = m.CtArray([m.Ct(data[i], lvl, scale, cfg.n_slots, P.log_n) for i in range(n_in)])
+    outs = m.CtArray([m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=device), lv, 0.0, 0, P.log_n)
+                      for lv in ctx.chain_plan(chain, cfg, lvl, n_in)])
     ctx.trace_enable(False)
     for _ in range(warmup):
         ctx.eval_chain(chain, cfg, ins, outs)
@@ -372,7 +382,7 @@ def bench_c5(m, torch, device, rank, world, sessions_per_rank=1, F=100, steps=2,
     gen_in.manual_seed(9200 + rank)
     scale = float(2 ** P.scale_bits)
     data = uniform_dev(torch, gen_in, (G, 2 * (hi - lo), 2, lvl + 1), list(P.q[: lvl + 1]), P.n, device)
-    frames_by_session = [[m.Ct(data[s, i], lvl, scale, 4096, P.log_n) for i in range(2 * (hi - lo))]
+    frames_by_session = [m.CtArray([m.Ct(data[s, i], lvl, scale, 4096, P.log_n) for i in range(2 * (hi - lo))])
                          for s in range(G)]
     mine = [s for s in range(G) if mdist.owner(s, world) == rank]
     ctx.trace_enable(False)

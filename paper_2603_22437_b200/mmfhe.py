@@ -178,6 +178,22 @@ class Ct:
         return CT(self.log_n, self.level, self.n_slots, self.form, float(self.scale), addr, dev, self.n_polys)
 
 
+class CtArray:
+    """A marshalled mmfhe_ct[] built once from a list of Ct (the buffers must stay alive);
+    passing it to eval_chain avoids rebuilding thousands of structs per call."""
+
+    def __init__(self, cts):
+        self.cts = list(cts)
+        self.arr = (CT * len(self.cts))(*[c.struct() for c in self.cts])
+
+    def __len__(self):
+        return len(self.cts)
+
+    def sync_back(self):
+        for c, s in zip(self.cts, self.arr):
+            c.level, c.scale, c.n_slots = s.level, s.scale, s.n_slots
+
+
 class Context:
     def __init__(self, log_n, q, p, alpha, scale_bits, device=0, stream=None):
         self._lib = lib()
@@ -270,13 +286,13 @@ class Context:
         return [buf[i] for i in range(n.value)]
 
     def eval_chain(self, chain, cfg, ins, outs):
-        arr_in = (CT * len(ins))(*[c.struct() for c in ins])
-        arr_out = (CT * len(outs))(*[c.struct() for c in outs])
+        """ins / outs: lists of Ct, or CtArray (pre-marshalled, reused across calls)."""
+        arr_in = ins if isinstance(ins, CtArray) else CtArray(ins)
+        arr_out = outs if isinstance(outs, CtArray) else CtArray(outs)
         n = ctypes.c_size_t()
-        self._check(self._lib.mmfhe_eval_chain(self.h, chain.encode(), ctypes.byref(cfg), arr_in, len(ins), arr_out,
-                                               len(outs), ctypes.byref(n)))
-        for c, s in zip(outs, arr_out):
-            c.level, c.scale, c.n_slots = s.level, s.scale, s.n_slots
+        self._check(self._lib.mmfhe_eval_chain(self.h, chain.encode(), ctypes.byref(cfg), arr_in.arr, len(arr_in),
+                                               arr_out.arr, len(arr_out), ctypes.byref(n)))
+        arr_out.sync_back()
         return n.value
 
     # ---- primitives
