@@ -10,13 +10,15 @@
 // memory, so the transform is two passes over HBM (logN = L1 + L2):
 //   col pass -- stages 0..L1-1 on 2^L2 strided columns of 2^L1 words; a warp
 //               spans G consecutive columns (G*8-byte sector-aligned runs);
-//   row pass -- stages L1..logN-1 on contiguous blocks of 2^L2 words; one warp
-//               per block, consecutive lanes on consecutive words.
-// Inside a pass each thread holds E = 2^ELOG = 8 words in registers and runs
-// ELOG butterfly stages there (radix-8); rounds exchange data through
-// double-buffered shared memory (one __syncthreads per exchange).  All index
-// arithmetic is shifts/masks of compile-time widths.  Every limb of every
-// polynomial of a batch goes in one launch (grid.y = rows, prime per row).
+//   row pass -- stages L1..logN-1 on contiguous blocks of 2^L2 words; lanes
+//               of a group on consecutive words.
+// Inside a pass each thread holds E = 2^ELOG = 8 words in registers (radix-8)
+// and runs up to ELOG butterfly stages there per round; rounds exchange through double-buffered, XOR-swizzled shared memory
+// (one __syncthreads per exchange, bank-conflict-free).  Forward rounds put the
+// narrow round FIRST (top bits) and inverse rounds LAST, so that in every round a
+// stage's twiddle depends only on register bits above it: each distinct twiddle
+// is loaded once per stage.  All index math is compile-time shifts and masks.
+// Every limb of every polynomial of a batch goes in one launch (grid.y = rows).
 #include <algorithm>
 
 #include "context.h"
@@ -45,26 +47,26 @@ __device__ __forceinline__ int kmap(int lo, int w, int t, int e)
     return (z & ((1 << lo) - 1)) | (y << lo) | ((z >> lo) << (lo + w));
 }
 
-// Shared-memory word of local element k in the row pass.  One warp spans
-// 32/T groups; in rounds 1-2 its lanes step k by 2-16 words, which would hit only
-// 2-4 of the 16 64-bit bank pairs.  XOR-ing the low 4 bits with a function of
-// the high bits makes every round's lane pattern cover all 16 bank pairs
-// (derived for LOGS = 7 and 8, both directions; identity otherwise).
-template <int LOGS>
-__device__ __forceinline__ int swz(int k)
+// XOR swizzle of a shared-memory word index: low bit b ^= parity((x >> 4) & M_b).
+// Masks found by exhaustive bank simulation of every round's lane pattern (both
+// directions); identity where the plain layout is already conflict-free.
+template <int M0, int M1, int M2, int M3>
+__device__ __forceinline__ int pswz(int x)
 {
-    if (LOGS == 8) return k ^ (((k >> 4) & 7) ^ (((k >> 5) & 3) << 2));
-    if (LOGS == 7) return k ^ ((((k >> 4) & 7) << 1) ^ ((k >> 6) & 1));
-    return k;
+    const int h = x >> 4;
+    return x ^ ((__popc(h & M0) & 1) | ((__popc(h & M1) & 1) << 1) | ((__popc(h & M2) & 1) << 2) |
+                ((__popc(h & M3) & 1) << 3));
 }
 
-// Column pass (word a = k*G + g): conflict-free for LOGS <= 7; for LOGS = 8 (G = 8)
-// rounds 2 would leave bit 3 constant across a warp -- flip it with a parity of bits 4, 6.
-template <int LOGS>
-__device__ __forceinline__ int colswz(int a)
+template <int LOGS, int ELOG, bool COL>
+__device__ __forceinline__ int swz(int x)
 {
-    if (LOGS == 8) return a ^ ((((a >> 4) ^ (a >> 6)) & 1) << 3);
-    return a;
+    if (!COL && LOGS == 8 && ELOG == 4) return pswz<4, 2, 3, 14>(x);
+    if (!COL && LOGS == 8 && ELOG == 3) return pswz<7, 11, 13, 6>(x);
+    if (!COL && LOGS == 7 && ELOG == 3) return pswz<3, 1, 7, 4>(x);
+    if (!COL && LOGS == 6 && ELOG == 3) return pswz<1, 2, 1, 1>(x);
+    if (COL && LOGS == 8 && ELOG == 3) return pswz<49, 27, 49, 6>(x);
+    return x;
 }
 
 // Global word offset (within the row) of local element k of group gi.
@@ -74,12 +76,20 @@ __device__ __forceinline__ size_t gaddr(int k, int gi, int L2, int LOGS)
     return COL ? (((size_t)k << L2) + gi) : (((size_t)gi << LOGS) + k);
 }
 
+template <int LOGS, int ELOG, bool COL>
+__device__ __forceinline__ int smem_index(int k, int g, int G)
+{
+    return COL ? swz<LOGS, ELOG, true>(k * G + g) : g * (1 << LOGS) + swz<LOGS, ELOG, false>(k);
+}
+
 // ---------------------------------------------------------------- forward
+// Round widths: the first (top) round takes LOGS - (R-1)*ELOG bits, the others ELOG.
 template <int LOGS, int ELOG, bool COL>
 __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
                                                             int log_g)
 {
     constexpr int S = 1 << LOGS, E = 1 << ELOG, T = S >> ELOG, R = (LOGS + ELOG - 1) / ELOG;
+    constexpr int W0 = LOGS - (R - 1) * ELOG;
     extern __shared__ uint64_t sm[];
     const int G = 1 << log_g;
     const int row = blockIdx.y;
@@ -105,36 +115,31 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict
     uint64_t v[E];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int hi = LOGS - 1 - r * ELOG;
-        const int w = (LOGS - r * ELOG) < ELOG ? (LOGS - r * ELOG) : ELOG;
+        const int w = r == 0 ? W0 : ELOG;
+        const int hi = LOGS - 1 - (r == 0 ? 0 : W0 + (r - 1) * ELOG);
         const int lo = hi - w + 1;
+        const int lp0 = LOGS - 1 - hi;  // local stage of this round's first stage
         if (r == 0) {
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)];
         } else {
             const uint64_t *b = ((r - 1) & 1) ? buf1 : buf0;
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int k = kmap<ELOG>(lo, w, t, e);
-                v[e] = COL ? b[colswz<LOGS>(k * G + g)] : b[g * S + swz<LOGS>(k)];
-            }
+            for (int e = 0; e < E; ++e) v[e] = b[smem_index<LOGS, ELOG, COL>(kmap<ELOG>(lo, w, t, e), g, G)];
         }
 #pragma unroll
         for (int s = 0; s < w; ++s) {
-            const int lp = r * ELOG + s;   // local stage
+            const int lp = lp0 + s;        // local stage
             const int bit = ELOG - 1 - s;  // register bit paired in this stage
-            // In a full-width round the twiddle depends only on the top s register bits: load
-            // each distinct one once.  In the (last, lo = 0) partial round the spare register
-            // bits map ABOVE the round's bits, so every butterfly has its own twiddle.
-            const int tb = (w == ELOG) ? s : ELOG;  // ELOG: one twiddle per register
+            // the twiddle depends only on the top s register bits (spare register bits
+            // map below lo): load each of the 2^s distinct ones once
 #pragma unroll
-            for (int m = 0; m < (1 << tb); ++m) {
-                const int erep = m << (ELOG - tb);
-                if (erep & (1 << bit)) continue;  // per-register case: pair leaders only
+            for (int mm = 0; mm < (1 << s); ++mm) {
+                const int erep = mm << (ELOG - s);
                 const int krep = kmap<ELOG>(lo, w, t, erep);
                 const TwPair wt = tw[(1 << (lbase + lp)) + (prefix << lp) + (krep >> (LOGS - lp))];
 #pragma unroll
-                for (int e = erep; e < erep + (1 << (ELOG - tb)); ++e) {
+                for (int e = erep; e < erep + (1 << (ELOG - s)); ++e) {
                     if (e & (1 << bit)) continue;
                     uint64_t U = v[e];
                     uint64_t V = v[e | (1 << bit)];
@@ -154,13 +159,7 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict
         } else {
             uint64_t *b = (r & 1) ? buf1 : buf0;
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int k = kmap<ELOG>(lo, w, t, e);
-                if (COL)
-                    b[colswz<LOGS>(k * G + g)] = v[e];
-                else
-                    b[g * S + swz<LOGS>(k)] = v[e];
-            }
+            for (int e = 0; e < E; ++e) b[smem_index<LOGS, ELOG, COL>(kmap<ELOG>(lo, w, t, e), g, G)] = v[e];
             __syncthreads();
         }
     }
@@ -168,7 +167,8 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict
 
 // ---------------------------------------------------------------- inverse
 // Stages in reverse: local stage lp = LOGS-1 .. 0 operates on bit LOGS-1-lp, so
-// rounds own bits from the bottom up.  The col pass (last) multiplies by N^{-1}.
+// rounds own bits from the bottom up (the narrow round last, at the top).  The
+// col pass (last) multiplies by N^{-1}.
 template <int LOGS, int ELOG, bool COL>
 __global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
                                                             int log_g)
@@ -207,10 +207,7 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict
         } else {
             const uint64_t *b = ((r - 1) & 1) ? buf1 : buf0;
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int k = kmap<ELOG>(lo, w, t, e);
-                v[e] = COL ? b[colswz<LOGS>(k * G + g)] : b[g * S + swz<LOGS>(k)];
-            }
+            for (int e = 0; e < E; ++e) v[e] = b[smem_index<LOGS, ELOG, COL>(kmap<ELOG>(lo, w, t, e), g, G)];
         }
 #pragma unroll
         for (int s = 0; s < w; ++s) {
@@ -218,8 +215,8 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict
             const int bit = ELOG - w + s;        // register bit of k-bit lo+s
             const int ntop = w - 1 - s;          // register bits above: the twiddle depends on these only
 #pragma unroll
-            for (int m = 0; m < (1 << ntop); ++m) {
-                const int erep = m << (ELOG - ntop);
+            for (int mm = 0; mm < (1 << ntop); ++mm) {
+                const int erep = mm << (ELOG - ntop);
                 const int krep = kmap<ELOG>(lo, w, t, erep);
                 const TwPair wt = tw[(1 << (lbase + lp)) + (prefix << lp) + (krep >> (LOGS - lp))];
 #pragma unroll
@@ -244,13 +241,7 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict
         } else {
             uint64_t *b = (r & 1) ? buf1 : buf0;
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int k = kmap<ELOG>(lo, w, t, e);
-                if (COL)
-                    b[colswz<LOGS>(k * G + g)] = v[e];
-                else
-                    b[g * S + swz<LOGS>(k)] = v[e];
-            }
+            for (int e = 0; e < E; ++e) b[smem_index<LOGS, ELOG, COL>(kmap<ELOG>(lo, w, t, e), g, G)] = v[e];
             __syncthreads();
         }
     }
@@ -278,20 +269,30 @@ Launch plan(int LOGS, int ELOG, int n_groups, uint32_t rows)
     return l;
 }
 
+// Radix-8 everywhere: radix-16 (ELOG = 4) halves the exchanges but its 64 KiB CTAs and
+// 16 live words per thread halved occupancy and ran 2x slower on B200 (measured).
+int elog_for(int LOGS) { return LOGS < 3 ? LOGS : 3; }
+
 template <bool FWD, bool COL>
 void launch_pass(int LOGS, uint32_t log_n, uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm,
                  cudaStream_t s)
 {
-    const int ELOG = LOGS < 3 ? LOGS : 3;
+    const int ELOG = elog_for(LOGS);
     const int n_groups = 1 << (log_n - LOGS);
     Launch l = plan(LOGS, ELOG, n_groups, rows);
+    // > 48 KiB of dynamic shared memory (radix-16 passes) needs an explicit opt-in, once
 #define MMFHE_NTT_CASE(LS, EL)                                                                    \
-    case LS:                                                                                      \
-        if (FWD)                                                                                  \
-            ntt_fwd_pass<LS, EL, COL><<<l.grid, l.threads, l.smem, s>>>(d, kt, pm, l.log_g);      \
-        else                                                                                      \
-            ntt_inv_pass<LS, EL, COL><<<l.grid, l.threads, l.smem, s>>>(d, kt, pm, l.log_g);      \
-        break;
+    case LS: {                                                                                    \
+        auto kern = FWD ? ntt_fwd_pass<LS, EL, COL> : ntt_inv_pass<LS, EL, COL>;                  \
+        static bool attr_set = false;                                                             \
+        if (!attr_set) {                                                                          \
+            CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                            96 * 1024));                                          \
+            attr_set = true;                                                                      \
+        }                                                                                         \
+        kern<<<l.grid, l.threads, l.smem, s>>>(d, kt, pm, l.log_g);                               \
+        break;                                                                                    \
+    }
     switch (LOGS) {
         MMFHE_NTT_CASE(2, 2)
         MMFHE_NTT_CASE(3, 3)
