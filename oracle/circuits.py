@@ -267,6 +267,13 @@ def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg
     xr = [list(v_re)] + baby_steps(ev, v_re, range(1, b), cfg.hoist)
     xi = [list(v_im)] + baby_steps(ev, v_im, range(1, b), cfg.hoist)
     out_re = out_im = None
+    nf = len(v_re)
+
+    def terms(spec, f):
+        return [(pt, (xr if which == "r" else xi)[s][f]) for pt, s, which in spec]
+
+    # all giant steps' inner sums first (one pass over the baby steps), then the giant rotations
+    inner = []
     for gp, G, babies in giants:
         t_re, t_im = [], []
         for s in babies:
@@ -278,13 +285,11 @@ def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg
             pns = book.vec(f"k3.ns.{gp}.{s}", -ds, lvl)
             t_re += [(pc, s, "r"), (pns, s, "i")]
             t_im += [(ps, s, "r"), (pc, s, "i")]
-
-        def terms(spec, f):
-            return [(pt, (xr if which == "r" else xi)[s][f]) for pt, s, which in spec]
-
-        nf = len(v_re)
-        ir = [ev.rotate(x, G) for x in [ev.pmult_sum(terms(t_re, f)) for f in range(nf)]]
-        ii = [ev.rotate(x, G) for x in [ev.pmult_sum(terms(t_im, f)) for f in range(nf)]]
+        inner.append(([ev.pmult_sum(terms(t_re, f)) for f in range(nf)],
+                      [ev.pmult_sum(terms(t_im, f)) for f in range(nf)]))
+    for (gp, G, babies), (pr, pi) in zip(giants, inner):
+        ir = [ev.rotate(x, G) for x in pr]
+        ii = [ev.rotate(x, G) for x in pi]
         out_re = ir if out_re is None else [ev.add(a, x) for a, x in zip(out_re, ir)]
         out_im = ii if out_im is None else [ev.add(a, x) for a, x in zip(out_im, ii)]
     return [ev.rescale(x) for x in out_re], [ev.rescale(x) for x in out_im]
@@ -376,12 +381,14 @@ def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int
     b, giants = fc_schedule(h)
     babies = [x] + [r[0] for r in baby_steps(ev, [x], range(1, min(b, h)), hoist)]
     acc = None
+    inners = []  # all giant steps' inner sums first, then the giant rotations
     for gp, G, ss in giants:
         terms = []
         for s in ss:
             dg = rot(fc_diagonal(W, n_in, G + s), -G)
             terms.append((book.vec(f"fc{layer}.d.{gp}.{s}", dg, lvl), babies[s]))
-        inner = ev.pmult_sum(terms)
+        inners.append(ev.pmult_sum(terms))
+    for (gp, G, ss), inner in zip(giants, inners):
         if G:
             inner = ev.rotate(inner, G)
         acc = inner if acc is None else ev.add(acc, inner)

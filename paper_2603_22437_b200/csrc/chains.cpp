@@ -234,23 +234,35 @@ class Runner {
             }
             return rot(v, -G);
         };
-        DCt out_re, out_im;
-        bool first = true;
+        // inner sums of every giant step in one pass over the 2b baby steps (fused diagonal
+        // MAC: babies read once, each diagonal once per frame batch), then the giant rotations
+        std::vector<const DCt *> cts;
+        for (uint32_t b = 0; b < s.b; ++b) cts.push_back(&xr[b]);
+        for (uint32_t b = 0; b < s.b; ++b) cts.push_back(&xi[b]);
+        std::vector<std::vector<const DPlain *>> rows;
         for (auto &g : s.giants) {
-            std::vector<std::pair<const DPlain *, const DCt *>> tre, tim;
+            std::vector<const DPlain *> re(2 * s.b, nullptr), im(2 * s.b, nullptr);
             for (uint32_t b : g.babies) {
                 const int32_t o = g.G + (int32_t)b;
                 const std::string sfx = "." + std::to_string(g.gp) + "." + std::to_string(b);
                 const DPlain &pc = plain("k3.c" + sfx, lvl, qscale(lvl), [&] { return diag(false, o, g.G, false); });
                 const DPlain &ps = plain("k3.s" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, false); });
                 const DPlain &pn = plain("k3.ns" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, true); });
-                tre.push_back({&pc, &xr[b]});
-                tre.push_back({&pn, &xi[b]});
-                tim.push_back({&ps, &xr[b]});
-                tim.push_back({&pc, &xi[b]});
+                re[b] = &pc;
+                re[s.b + b] = &pn;
+                im[b] = &ps;
+                im[s.b + b] = &pc;
             }
-            DCt ir = ev_rotate(c_, ev_pmult_sum(c_, tre), g.G);
-            DCt ii = ev_rotate(c_, ev_pmult_sum(c_, tim), g.G);
+            rows.push_back(re);
+            rows.push_back(im);
+        }
+        std::vector<DCt> inner = ev_diag_mac(c_, cts, rows);
+        DCt out_re, out_im;
+        bool first = true;
+        for (size_t gi = 0; gi < s.giants.size(); ++gi) {
+            const auto &g = s.giants[gi];
+            DCt ir = ev_rotate(c_, inner[2 * gi], g.G);
+            DCt ii = ev_rotate(c_, inner[2 * gi + 1], g.G);
             if (first) {
                 out_re = std::move(ir);
                 out_im = std::move(ii);
@@ -319,23 +331,30 @@ class Runner {
             bias = &c_.fc_b[layer - 1];
         }
         std::vector<DCt> babies = baby_steps(x, std::min(s.b, h));
-        DCt acc;
-        bool first = true;
+        std::vector<const DCt *> cts;
+        for (auto &bb : babies) cts.push_back(&bb);
+        std::vector<std::vector<const DPlain *>> rows;
         for (auto &g : s.giants) {
-            std::vector<std::pair<const DPlain *, const DCt *>> terms;
+            std::vector<const DPlain *> row(babies.size(), nullptr);
             for (uint32_t b : g.babies) {
                 const uint32_t i = (uint32_t)g.G + b;
                 const std::string name = "fc" + std::to_string(layer) + ".d." + std::to_string(g.gp) + "." +
                                          std::to_string(b);
-                const DPlain &p = plain(name, lvl, qscale(lvl), [&] {
+                row[b] = &plain(name, lvl, qscale(lvl), [&] {
                     MMFHE_REQUIRE(W != nullptr, MMFHE_E_MISSING_PLAIN, "FC weights not prepared");
                     std::vector<double> v(n_in);
                     for (uint32_t j = 0; j < n_in; ++j) v[j] = (*W)[(size_t)(j % h) * n_in + (j + i) % n_in];
                     return rot(v, -g.G);
                 });
-                terms.push_back({&p, &babies[b]});
             }
-            DCt inner = ev_pmult_sum(c_, terms);
+            rows.push_back(row);
+        }
+        std::vector<DCt> inners = ev_diag_mac(c_, cts, rows);
+        DCt acc;
+        bool first = true;
+        for (size_t gi = 0; gi < s.giants.size(); ++gi) {
+            const auto &g = s.giants[gi];
+            DCt inner = std::move(inners[gi]);
             if (g.G) inner = ev_rotate(c_, inner, g.G);
             if (first) {
                 acc = std::move(inner);

@@ -237,6 +237,51 @@ DCt ev_pmult_sum(Ctx &c, const std::vector<std::pair<const DPlain *, const DCt *
     return r;
 }
 
+std::vector<DCt> ev_diag_mac(Ctx &c, const std::vector<const DCt *> &cts,
+                             const std::vector<std::vector<const DPlain *>> &pts)
+{
+    MMFHE_REQUIRE(!cts.empty() && !pts.empty(), MMFHE_E_INVALID_ARG, "empty diagonal MAC");
+    const DCt &a0 = *cts[0];
+    for (auto *x : cts)
+        MMFHE_REQUIRE(x->level == a0.level && x->batch == a0.batch && x->npolys == 2 && x->scale == a0.scale,
+                      MMFHE_E_LAYOUT, "diag MAC operands must share level, batch and scale");
+    std::vector<DCt> out;
+    const bool fused = cts.size() <= (size_t)kDiagMax && pts.size() <= (size_t)kDiagMax;
+    std::vector<const uint64_t *> ctp;
+    for (auto *x : cts) ctp.push_back(x->data());
+    std::vector<std::vector<const uint64_t *>> ptp;
+    std::vector<uint64_t *> outp;
+    for (const auto &row : pts) {
+        MMFHE_REQUIRE(row.size() == cts.size(), MMFHE_E_LAYOUT, "diag MAC row size");
+        double sc = 0;
+        int cnt = 0;
+        std::vector<const uint64_t *> rp;
+        std::vector<std::pair<const DPlain *, const DCt *>> terms;
+        for (size_t i = 0; i < row.size(); ++i) {
+            const DPlain *p = row[i];
+            rp.push_back(p ? p->buf.get() : nullptr);
+            if (!p) continue;
+            MMFHE_REQUIRE(p->level == a0.level, MMFHE_E_LAYOUT, "plaintext level mismatch");
+            const double s = a0.scale * p->scale;
+            MMFHE_REQUIRE(cnt == 0 || s == sc, MMFHE_E_SCALE, "diag MAC scale mismatch");
+            sc = s;
+            ++cnt;
+            terms.push_back({p, cts[i]});
+        }
+        MMFHE_REQUIRE(cnt > 0, MMFHE_E_INVALID_ARG, "diag MAC output without terms");
+        if (!fused) {  // more than kDiagMax babies or outputs: one plaintext inner product per output
+            out.push_back(ev_pmult_sum(c, terms));
+            continue;
+        }
+        rec_n(c, "pmult_sum", a0.level, a0.batch, std::to_string(cnt));
+        out.push_back(make_ct(c, a0.level, 2, a0.n_slots, sc, a0.batch));
+        ptp.push_back(rp);
+        outp.push_back(out.back().data());
+    }
+    if (fused) launch_diag_mac(c, ctp, a0.item_words(), ptp, outp, out[0].item_words(), a0.level, a0.batch);
+    return out;
+}
+
 uint64_t encode_scalar_mod(double v, uint64_t q_scale, uint64_t m)
 {
     // v = mant * 2^e exactly with mant < 2^53; |x| = mant * q_scale * 2^e rounded

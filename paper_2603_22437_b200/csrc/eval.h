@@ -30,6 +30,10 @@ DCt ev_addsub(Ctx &c, const DCt &a, const DCt &b, bool sub);
 DCt ev_drop_to(Ctx &c, const DCt &a, uint32_t level);
 DCt ev_tensor_sum(Ctx &c, const std::vector<std::pair<const DCt *, const DCt *>> &pairs);
 DCt ev_pmult_sum(Ctx &c, const std::vector<std::pair<const DPlain *, const DCt *>> &terms);
+// BSGS inner sums of every giant step in one pass over the baby steps:
+// out[o] = sum_c pts[o][c] (.) cts[c] (pts[o][c] may be null); records one pmult_sum per output.
+std::vector<DCt> ev_diag_mac(Ctx &c, const std::vector<const DCt *> &cts,
+                             const std::vector<std::vector<const DPlain *>> &pts);
 // sum of all items of a batch (frame accumulation, depth 0)
 DCt ev_batch_sum(Ctx &c, const DCt &a);
 DCt ev_sum(Ctx &c, const std::vector<const DCt *> &cts);

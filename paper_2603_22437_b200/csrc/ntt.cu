@@ -119,7 +119,19 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict
         const int hi = LOGS - 1 - (r == 0 ? 0 : W0 + (r - 1) * ELOG);
         const int lo = hi - w + 1;
         const int lp0 = LOGS - 1 - hi;  // local stage of this round's first stage
-        if (r == 0) {
+        if (r == 0 && !COL) {
+            // row pass: the CTA's G blocks are one contiguous tile -- load it coalesced
+            // into shared memory, then read the round's register pattern from there
+            const uint64_t *tile = data + (size_t)row * kt.n + ((size_t)blockIdx.x * G << LOGS);
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+                const int idx = tid + i * (T << log_g);
+                buf1[smem_index<LOGS, ELOG, false>(idx & (S - 1), idx >> LOGS, G)] = tile[idx];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = buf1[smem_index<LOGS, ELOG, false>(kmap<ELOG>(lo, w, t, e), g, G)];
+        } else if (r == 0) {
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)];
         } else {
@@ -127,17 +139,26 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = b[smem_index<LOGS, ELOG, COL>(kmap<ELOG>(lo, w, t, e), g, G)];
         }
+        // The twiddle of stage s depends only on the top s register bits (spare register
+        // bits map below lo): 2^s distinct ones per stage.  Issue all of the round's
+        // twiddle loads before the first butterfly so their L2 latency overlaps.
+        TwPair tws[E];
 #pragma unroll
         for (int s = 0; s < w; ++s) {
-            const int lp = lp0 + s;        // local stage
+            const int lp = lp0 + s;
+#pragma unroll
+            for (int mm = 0; mm < (1 << s); ++mm) {
+                const int krep = kmap<ELOG>(lo, w, t, mm << (ELOG - s));
+                tws[(1 << s) - 1 + mm] = tw[(1 << (lbase + lp)) + (prefix << lp) + (krep >> (LOGS - lp))];
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < w; ++s) {
             const int bit = ELOG - 1 - s;  // register bit paired in this stage
-            // the twiddle depends only on the top s register bits (spare register bits
-            // map below lo): load each of the 2^s distinct ones once
 #pragma unroll
             for (int mm = 0; mm < (1 << s); ++mm) {
                 const int erep = mm << (ELOG - s);
-                const int krep = kmap<ELOG>(lo, w, t, erep);
-                const TwPair wt = tw[(1 << (lbase + lp)) + (prefix << lp) + (krep >> (LOGS - lp))];
+                const TwPair wt = tws[(1 << s) - 1 + mm];
 #pragma unroll
                 for (int e = erep; e < erep + (1 << (ELOG - s)); ++e) {
                     if (e & (1 << bit)) continue;
@@ -150,12 +171,21 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict
                 }
             }
         }
-        if (r == R - 1) {
+        if (r == R - 1 && !COL) {
+            // row pass: through shared memory back to a coalesced store of the tile
+            uint64_t *b = (r & 1) ? buf1 : buf0;
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const uint64_t x = COL ? v[e] : reduce4q(v[e], q);
-                a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)] = x;
+            for (int e = 0; e < E; ++e) b[smem_index<LOGS, ELOG, false>(kmap<ELOG>(lo, w, t, e), g, G)] = reduce4q(v[e], q);
+            __syncthreads();
+            uint64_t *tile = data + (size_t)row * kt.n + ((size_t)blockIdx.x * G << LOGS);
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+                const int idx = tid + i * (T << log_g);
+                tile[idx] = b[smem_index<LOGS, ELOG, false>(idx & (S - 1), idx >> LOGS, G)];
             }
+        } else if (r == R - 1) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)] = v[e];
         } else {
             uint64_t *b = (r & 1) ? buf1 : buf0;
 #pragma unroll
@@ -201,7 +231,18 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict
     for (int r = 0; r < R; ++r) {
         const int lo = r * ELOG;
         const int w = (LOGS - lo) < ELOG ? (LOGS - lo) : ELOG;
-        if (r == 0) {
+        if (r == 0 && !COL) {
+            // row pass: coalesced load of the CTA's contiguous tile through shared memory
+            const uint64_t *tile = data + (size_t)row * kt.n + ((size_t)blockIdx.x * G << LOGS);
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+                const int idx = tid + i * (T << log_g);
+                buf1[smem_index<LOGS, ELOG, false>(idx & (S - 1), idx >> LOGS, G)] = tile[idx];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = buf1[smem_index<LOGS, ELOG, false>(kmap<ELOG>(lo, w, t, e), g, G)];
+        } else if (r == 0) {
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)];
         } else {
@@ -209,16 +250,27 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = b[smem_index<LOGS, ELOG, COL>(kmap<ELOG>(lo, w, t, e), g, G)];
         }
+        // stage s needs 2^(w-1-s) distinct twiddles (register bits above it); load the
+        // whole round's set up front
+        TwPair tws[E];
 #pragma unroll
         for (int s = 0; s < w; ++s) {
-            const int lp = LOGS - 1 - (lo + s);  // local stage of bit lo+s
-            const int bit = ELOG - w + s;        // register bit of k-bit lo+s
-            const int ntop = w - 1 - s;          // register bits above: the twiddle depends on these only
+            const int lp = LOGS - 1 - (lo + s);
+            const int ntop = w - 1 - s;
+#pragma unroll
+            for (int mm = 0; mm < (1 << ntop); ++mm) {
+                const int krep = kmap<ELOG>(lo, w, t, mm << (ELOG - ntop));
+                tws[(1 << ntop) - 1 + mm] = tw[(1 << (lbase + lp)) + (prefix << lp) + (krep >> (LOGS - lp))];
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < w; ++s) {
+            const int bit = ELOG - w + s;  // register bit of k-bit lo+s
+            const int ntop = w - 1 - s;    // register bits above: the twiddle depends on these only
 #pragma unroll
             for (int mm = 0; mm < (1 << ntop); ++mm) {
                 const int erep = mm << (ELOG - ntop);
-                const int krep = kmap<ELOG>(lo, w, t, erep);
-                const TwPair wt = tw[(1 << (lbase + lp)) + (prefix << lp) + (krep >> (LOGS - lp))];
+                const TwPair wt = tws[(1 << ntop) - 1 + mm];
 #pragma unroll
                 for (int e = erep; e < erep + (1 << (ELOG - ntop)); ++e) {
                     if (e & (1 << bit)) continue;
@@ -230,14 +282,22 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict
                 }
             }
         }
-        if (r == R - 1) {
-            TwPair ninv{0, 0};
-            if (COL) ninv = kt.n_inv[p];
+        if (r == R - 1 && !COL) {
+            // row pass: through shared memory back to a coalesced store of the tile
+            uint64_t *b = (r & 1) ? buf1 : buf0;
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const uint64_t x = COL ? shoup(v[e], ninv.w, ninv.wp, q) : v[e];
-                a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)] = x;
+            for (int e = 0; e < E; ++e) b[smem_index<LOGS, ELOG, false>(kmap<ELOG>(lo, w, t, e), g, G)] = v[e];
+            __syncthreads();
+            uint64_t *tile = data + (size_t)row * kt.n + ((size_t)blockIdx.x * G << LOGS);
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+                const int idx = tid + i * (T << log_g);
+                tile[idx] = b[smem_index<LOGS, ELOG, false>(idx & (S - 1), idx >> LOGS, G)];
             }
+        } else if (r == R - 1) {
+            const TwPair ninv = kt.n_inv[p];
+#pragma unroll
+            for (int e = 0; e < E; ++e) a[gaddr<COL>(kmap<ELOG>(lo, w, t, e), gi, L2, LOGS)] = shoup(v[e], ninv.w, ninv.wp, q);
         } else {
             uint64_t *b = (r & 1) ? buf1 : buf0;
 #pragma unroll
@@ -265,7 +325,7 @@ Launch plan(int LOGS, int ELOG, int n_groups, uint32_t rows)
     l.log_g = log_g;
     l.threads = T * G;
     l.grid = dim3(n_groups / G, rows);
-    l.smem = (LOGS > ELOG) ? 2 * sizeof(uint64_t) * ((size_t)G << LOGS) : 0;
+    l.smem = 2 * sizeof(uint64_t) * ((size_t)G << LOGS);  // exchanges + the row pass's I/O staging
     return l;
 }
 

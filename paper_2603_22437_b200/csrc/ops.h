@@ -10,6 +10,7 @@
 namespace mmfhe {
 
 constexpr int kMaxTerms = 64;  // operands per fused-sum launch (chunked above)
+constexpr int kDiagMax = 16;   // baby steps / outputs of one fused BSGS diagonal MAC
 
 struct PtrList {
     const uint64_t *p[kMaxTerms];
@@ -50,6 +51,11 @@ void launch_tensor_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &a, const
 // out (+)= sum_t pt_t (.) ct_t; pt shared by the batch (Montgomery form).
 void launch_pmult_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &pt, const PtrList &ct, size_t is, int n,
                       uint32_t level, bool accumulate, uint32_t B);
+// Fused BSGS inner sums (CK9): out_o (+0) = sum_c pts[o][c] (.) cts[c] for a batch of B
+// (cts item stride is, outs item stride os); pts[o][c] may be null; <= kDiagMax each.
+void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is,
+                     const std::vector<std::vector<const uint64_t *>> &pts, const std::vector<uint64_t *> &outs,
+                     size_t os, uint32_t level, uint32_t B);
 // Scalar "modular matrix product" over a batch of 2-poly cts (CK10):
 //   out[j] = sum_{w < W} C[j][w] in[lo_j + w],  j < J,  lo_j = lo0 + j*lo_step,
 // C given as Shoup pairs [J][W][l+1]; inputs outside [0, M) contribute nothing.

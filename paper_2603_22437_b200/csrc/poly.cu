@@ -347,6 +347,54 @@ __global__ void __launch_bounds__(kTB) k_pmult_sum(uint64_t *__restrict__ out_ba
     out[ps + off] = s1;
 }
 
+// BSGS inner sums of all giant steps in one pass:
+//   out_o = sum_c pt[o][c] (.) ct_c   (pt[o][c] == nullptr: no term),
+// every thread loads its coefficient of the NC baby-step ciphertexts once and
+// produces all NO outputs; plaintext words are shared by the batch (grid.z).
+struct DiagMacArgs {
+    const uint64_t *ct[kDiagMax];
+    const uint64_t *pt[kDiagMax][kDiagMax];
+    uint64_t *out[kDiagMax];
+    size_t is, os;
+    int nc, no;
+    uint32_t level;
+};
+
+// grid.x = tile * B + item: the B CTAs that share a tile's plaintext words run together,
+// so each diagonal word is fetched from HBM once and served to the batch from L2.
+// grid.y = poly * (l+1) + limb (one polynomial per thread keeps ~60 registers); the
+// next output's diagonal words are prefetched while the current one accumulates.
+template <int NCMAX>
+__global__ void __launch_bounds__(kTB) k_diag_mac(DiagMacArgs a, KTables kt, uint32_t B)
+{
+    const uint32_t item = blockIdx.x % B, tile = blockIdx.x / B;
+    const uint32_t k = tile * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t L1 = a.level + 1;
+    const uint32_t poly = blockIdx.y / L1, r = blockIdx.y - poly * L1;
+    const size_t off = (size_t)r * kt.n + k;
+    const size_t poff = (size_t)poly * L1 * kt.n + off;
+    const size_t boff = (size_t)item * a.is + poff;
+    const uint64_t q = kt.q[r], qi = kt.qinv_neg[r];
+    uint64_t x[NCMAX], w[NCMAX];
+#pragma unroll
+    for (int c = 0; c < NCMAX; ++c) x[c] = c < a.nc ? a.ct[c][boff] : 0;
+#pragma unroll
+    for (int c = 0; c < NCMAX; ++c) w[c] = (c < a.nc && a.pt[0][c]) ? __ldg(a.pt[0][c] + off) : 0;
+    for (int o = 0; o < a.no; ++o) {
+        uint64_t wn[NCMAX];
+        const bool more = o + 1 < a.no;
+#pragma unroll
+        for (int c = 0; c < NCMAX; ++c) wn[c] = (more && c < a.nc && a.pt[o + 1][c]) ? __ldg(a.pt[o + 1][c] + off) : 0;
+        U128 acc{0, 0};  // <= 16 terms < q*2^60 each: < q*2^64 for q < 2^60; absent terms are 0
+#pragma unroll
+        for (int c = 0; c < NCMAX; ++c) mac128(acc, x[c], w[c]);
+        a.out[o][(size_t)item * a.os + poff] = redc(acc, q, qi);
+#pragma unroll
+        for (int c = 0; c < NCMAX; ++c) w[c] = wn[c];
+    }
+}
+
 constexpr int kJG = 8;  // outputs per thread in the modular matrix product
 
 // out[j] = sum_w C[j][w] in[lo_j + w] for j in this CTA's group of kJG outputs.
@@ -619,6 +667,39 @@ void launch_pmult_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &pt, const
                  8.0 * (level + 1) * c.n * ((double)n + B * (2.0 * n + 2.0 + (accumulate ? 2.0 : 0.0))));
     k_pmult_sum<<<grid3(c.n, level + 1, B), kTB, 0, c.stream>>>(out, os, pt, ct, is, n, c.kt, level,
                                                                 accumulate ? 1 : 0);
+    LAUNCH_CHECK(c);
+}
+
+void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is,
+                     const std::vector<std::vector<const uint64_t *>> &pts, const std::vector<uint64_t *> &outs,
+                     size_t os, uint32_t level, uint32_t B)
+{
+    MMFHE_REQUIRE(cts.size() <= (size_t)kDiagMax && outs.size() <= (size_t)kDiagMax && pts.size() == outs.size(),
+                  MMFHE_E_LAYOUT, "diag_mac shape");
+    DiagMacArgs a{};
+    a.nc = (int)cts.size();
+    a.no = (int)outs.size();
+    a.is = is;
+    a.os = os;
+    a.level = level;
+    double terms = 0;
+    for (size_t i = 0; i < cts.size(); ++i) a.ct[i] = cts[i];
+    for (size_t o = 0; o < outs.size(); ++o) {
+        a.out[o] = outs[o];
+        for (size_t i = 0; i < cts.size(); ++i) {
+            a.pt[o][i] = pts[o][i];
+            terms += pts[o][i] != nullptr;
+        }
+    }
+    // algorithmic: babies read once, plaintexts once per batch, outputs written once
+    ProfScope ps(c, "diag_mac", 8.0 * (level + 1) * c.n * (terms + B * 2.0 * (a.nc + a.no)));
+    const dim3 g(((c.n + kTB - 1) / kTB) * B, 2 * (level + 1));
+    if (a.nc <= 4)
+        k_diag_mac<4><<<g, kTB, 0, c.stream>>>(a, c.kt, B);
+    else if (a.nc <= 8)
+        k_diag_mac<8><<<g, kTB, 0, c.stream>>>(a, c.kt, B);
+    else
+        k_diag_mac<16><<<g, kTB, 0, c.stream>>>(a, c.kt, B);
     LAUNCH_CHECK(c);
 }
 
