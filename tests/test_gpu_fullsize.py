@@ -1,0 +1,118 @@
+"""Full-size correctness at the benchmarked configurations (north_star gate 2):
+the GPU chains on real encryptions (oracle client) at BASELINE sizes, decrypted
+outputs against the O-DSP closed forms (normwise 1e-3, reading R9), HR/RR within
+1 BPM, target bin exact, argmax agreement.  Bit-exact residue parity at these
+sizes is covered where the oracle can afford it (C1, C3, PS4 HRot/HMult in the
+other GPU test files); here the full pipelines are checked through decryption."""
+import numpy as np
+import pytest
+
+from oracle import ckks as orc
+from oracle import circuits as cc
+from oracle import dsp
+from synth import radar
+from synth.params import ps2, ps4
+
+from gpu_util import ct_in, ct_out, make_ctx, residues
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def m(cuda_ctx_ok):
+    from paper_2603_22437_b200 import build, mmfhe
+    build.build()
+    return mmfhe
+
+
+def _dec(P, keys, o):
+    ct = orc.Ct([residues(o)[0], residues(o)[1]], o.level, o.scale, o.n_slots)
+    return orc.decrypt_vector(P, keys, ct)
+
+
+def test_c2_vital_pipeline_full_size(m):
+    """configs[1]: N=2^14 (PS2), R=128, F=256 frames at 20 Hz -- vitals_v1 (entry 3) and
+    vitals_v2 (entry 7, through |X|^2) on one encrypted session, as bench.py times it."""
+    P = ps2()
+    R, F, fs = 128, 256, 20.0
+    bands = ((0.1, 0.6), (0.8, 2.5))
+    cfg = cc.ChainCfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=fs, bands=bands)
+    z, truth = radar.vital_scene(R, F, fs, seed=5001)
+    zt = radar.preprocess_vital(z)
+    rots = sorted(set(cc.required_rotations("vitals_v1", cfg, P.n)))
+    keys = orc.keygen(P, seed=5002, rotations=rots)
+    v1, v2 = [], []
+    for t in range(F):
+        for part in (zt[t].real, zt[t].imag):
+            vec = radar.pack_vital(part, cfg.n_slots)
+            pt = orc.encode(P, vec, float(2 ** P.scale_bits), P.L)
+            ct = orc.encrypt(P, keys, pt, P.L, float(2 ** P.scale_bits), cfg.n_slots, seed=5003, index=len(v2))
+            v2.append(ct)
+            v1.append(orc.Ct([c[:4].copy() for c in ct.c], 3, ct.scale, ct.n_slots))
+    taps = [radar.fir_taps(41, b, fs) for b in bands]
+    bins = [[int(k) for k in dsp.band_bins(F - 1, fs, b)] for b in bands]
+    ctx = make_ctx(m, P, keys)
+    mcfg = m.chain_cfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=cfg.n_slots, bands_bins=bins,
+                       n_taps=[41, 41], fs=fs)
+    ctx.prepare_chain("vitals_v1", mcfg, 3)
+    ctx.prepare_chain("vitals_v2", mcfg, 7, taps=taps)
+    # V1: N, D -> target bin
+    outs = [ct_out(m, P, lv) for lv in ctx.chain_plan("vitals_v1", mcfg, 3, 2 * F)]
+    ctx.eval_chain("vitals_v1", mcfg, [ct_in(m, P, c) for c in v1], outs)
+    N, D = _dec(P, keys, outs[0])[0], _dec(P, keys, outs[1])[0]
+    Np, Dp, rp = dsp.soft_attention(dsp.energy(zt), 2, F)
+    assert abs(N - Np) <= 1e-3 * abs(Np) and abs(D - Dp) <= 1e-3 * abs(Dp)
+    assert round(N / D) == round(rp)
+    # V2: |X[k]|^2 per band -> BPM
+    lv2 = ctx.chain_plan("vitals_v2", mcfg, 7, 2 * F)
+    outs2 = [ct_out(m, P, lv) for lv in lv2]
+    ctx.eval_chain("vitals_v2", mcfg, [ct_in(m, P, c) for c in v2], outs2)
+    I = np.array([dsp.soft_iq(zt[t], 2)[0] for t in range(F)])
+    Q = np.array([dsp.soft_iq(zt[t], 2)[1] for t in range(F)])
+    at = 0
+    for b, h in enumerate(taps):
+        y = dsp.taylor_phase(dsp.fir(I, h), dsp.fir(Q, h), 1)
+        want = dsp.narrowband_power(y, bins[b])
+        got = np.array([_dec(P, keys, o)[0] for o in outs2[at:at + len(bins[b])]])
+        at += len(bins[b])
+        assert np.max(np.abs(got - want)) <= 1e-3 * np.max(np.abs(want))
+        bpm_enc = dsp.bpm_from_power(got, bins[b], fs, F - 1)
+        bpm_plain = dsp.bpm_from_power(want, bins[b], fs, F - 1)
+        assert abs(bpm_enc - bpm_plain) < 1.0
+
+
+def test_c4_gesture_full_size(m):
+    """configs[3] shape: N=2^16 (PS4, 20 Q limbs, entry level 19), A=4 x R=32 x D=32
+    (4096 active slots), per-frame K3->K1->K6->K2b, frame sum, FC 4096->64->32->5;
+    4 frames to bound the oracle client's encryption/keygen time."""
+    P = ps4()
+    A, R, D, F = 4, 32, 32, 4
+    cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=4,
+                      hoist=1)
+    Z, info = radar.gesture_scene(A, R, D, F, seed=5101, cls=3)
+    Zt = radar.preprocess_gesture(Z)
+    keys = orc.keygen(P, seed=5102, rotations=cc.required_rotations("gesture", cfg, P.n))
+    cts, feats = [], []
+    for t in range(F):
+        v = radar.pack_doppler(Zt[t])
+        feats.append(dsp.gesture_frame_features(v, A, R, D, 4))
+        for part in (v.real, v.imag):
+            cts.append(orc.encrypt_vector(P, keys, part, 19, seed=5103, index=len(cts)))
+    xp = np.sum(feats, axis=0)
+    Ws, bs = radar.fc_weights([4096, 64, 32, 5], seed=5104)
+    # the normalised features are ~1e-5 (P:886-887 folding caveat, SURVEY c-7): scale W1 up
+    # towards O(1) pre-activations, but keep every diagonal entry encodable at
+    # Delta_pt = q_l ~ 2^50 (|w| q_l < 2^62)
+    gain = min(0.8 / max(np.max(np.abs(Ws[0] @ xp)), 1e-30), 2000.0 / np.max(np.abs(Ws[0])))
+    Ws[0] = Ws[0] * gain
+    want = dsp.mlp_forward(xp, Ws, bs)
+    Wp, bp = cc.pad_fc(Ws, bs, cfg.fc_dims)
+    ctx = make_ctx(m, P, keys)
+    mcfg = m.chain_cfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=4, hoist=1)
+    ctx.prepare_chain("gesture", mcfg, 19, fc_w=Wp, fc_b=bp)
+    outs = [ct_out(m, P, lv) for lv in ctx.chain_plan("gesture", mcfg, 19, 2 * F)]
+    ctx.eval_chain("gesture", mcfg, [ct_in(m, P, c) for c in cts], outs)
+    assert outs[0].level == 19 - 11
+    got = _dec(P, keys, outs[0])[:5]
+    assert np.max(np.abs(got - want)) <= 1e-3 * np.max(np.abs(want)), (got, want)
+    assert int(np.argmax(got)) == int(np.argmax(want))
