@@ -29,6 +29,8 @@ namespace mmfhe {
 namespace {
 
 constexpr int kCtaThreads = 256;
+// min CTAs/SM for __launch_bounds__: forcing 5 (<= 51 registers) spilled and ran slower
+constexpr int kMinCtas = 1;
 
 __device__ __forceinline__ uint64_t reduce4q(uint64_t x, uint64_t q)
 {
@@ -85,7 +87,7 @@ __device__ __forceinline__ int smem_index(int k, int g, int G)
 // ---------------------------------------------------------------- forward
 // Round widths: the first (top) round takes LOGS - (R-1)*ELOG bits, the others ELOG.
 template <int LOGS, int ELOG, bool COL>
-__global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
+__global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
                                                             int log_g)
 {
     constexpr int S = 1 << LOGS, E = 1 << ELOG, T = S >> ELOG, R = (LOGS + ELOG - 1) / ELOG;
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(kCtaThreads) ntt_fwd_pass(uint64_t *__restrict
 // rounds own bits from the bottom up (the narrow round last, at the top).  The
 // col pass (last) multiplies by N^{-1}.
 template <int LOGS, int ELOG, bool COL>
-__global__ void __launch_bounds__(kCtaThreads) ntt_inv_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
+__global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm,
                                                             int log_g)
 {
     constexpr int S = 1 << LOGS, E = 1 << ELOG, T = S >> ELOG, R = (LOGS + ELOG - 1) / ELOG;
