@@ -178,7 +178,12 @@ mmfhe_status mmfhe_load_scalars(mmfhe_ctx *ctx, const char *name, const double *
  * §2): k1/vitals: re_0, im_0, re_1, im_1, ...; gesture*: v_re_t, v_im_t per frame.
  * out: caller buffers; mmfhe_chain_plan tells their count and levels.
  * MMFHE_E_SHAPE on a frame-count mismatch, MMFHE_E_DEPTH if in_level is too
- * low, MMFHE_E_MISSING_KEY / MMFHE_E_MISSING_PLAIN for absent operands. */
+ * low, MMFHE_E_MISSING_KEY / MMFHE_E_MISSING_PLAIN for absent operands.
+ * Graph replay: when every input and output is device-resident and trace and
+ * profile are off, the second call with the same chain, cfg, buffer addresses
+ * and layouts is captured into a CUDA graph and later identical calls replay it
+ * (same results, one graph launch; inputs are re-read each call).  Any key,
+ * plaintext, scalar or prepare_chain load invalidates the captured graphs. */
 mmfhe_status mmfhe_chain_plan(mmfhe_ctx *ctx, const char *chain, const mmfhe_chain_cfg *cfg, uint32_t in_level,
                               size_t n_in, uint32_t *out_levels, size_t cap, size_t *n_out);
 mmfhe_status mmfhe_eval_chain(mmfhe_ctx *ctx, const char *chain, const mmfhe_chain_cfg *cfg, const mmfhe_ct *in,
@@ -229,6 +234,12 @@ mmfhe_status mmfhe_hmult_batch(mmfhe_ctx *ctx, const mmfhe_ct *a, const mmfhe_ct
 mmfhe_status mmfhe_trace_get(mmfhe_ctx *ctx, char *buf, size_t cap, size_t *len);
 mmfhe_status mmfhe_trace_clear(mmfhe_ctx *ctx);
 mmfhe_status mmfhe_trace_enable(mmfhe_ctx *ctx, int on);
+
+/* ---- CUDA-graph replay of repeated mmfhe_eval_chain calls (default on) ----
+ * on = 0 disables it and releases the captured graphs (their memory). */
+mmfhe_status mmfhe_graph_enable(mmfhe_ctx *ctx, int on);
+/* n_graphs: captured graphs held; replays: graph launches since ctx creation. */
+mmfhe_status mmfhe_graph_stats(mmfhe_ctx *ctx, size_t *n_graphs, uint64_t *replays);
 
 /* ---- kernel profile (bench roofline) ---------------------------------------
  * When on, CUDA events are recorded on the ctx stream around every kernel

@@ -40,6 +40,101 @@ DCt input_ct(Ctx &c, const mmfhe_ct &ct)
     return import_ct(c, ct, npolys_of(ct));
 }
 
+// Operand stores changed: cached chain graphs may bake in stale operands.
+void state_changed(Ctx &c)
+{
+    c.drop_graphs();
+    ++c.state_gen;
+}
+
+bool all_device(const mmfhe_ct *v, size_t n)
+{
+    for (size_t i = 0; i < n; ++i)
+        if (!v[i].on_device) return false;
+    return true;
+}
+
+template <class T>
+void put(std::string &k, const T &x)
+{
+    k.append((const char *)&x, sizeof(T));
+}
+
+// Everything a captured chain graph depends on: chain, cfg, every buffer address and
+// layout, and the operand-store generation.
+std::string chain_key(const Ctx &c, const char *chain, const mmfhe_chain_cfg &cfg, const mmfhe_ct *in, size_t n_in,
+                      const mmfhe_ct *out, size_t n_out)
+{
+    std::string k(chain);
+    k.push_back('\0');
+    put(k, cfg);
+    put(k, c.state_gen);
+    put(k, n_in);
+    for (size_t i = 0; i < n_in; ++i) {
+        put(k, in[i].data);
+        put(k, in[i].level);
+        put(k, in[i].scale);
+        put(k, in[i].n_slots);
+        put(k, in[i].form);
+        put(k, in[i].n_polys);
+        put(k, in[i].log_n);
+    }
+    put(k, n_out);
+    for (size_t i = 0; i < n_out; ++i) {
+        put(k, out[i].data);
+        put(k, out[i].form);
+    }
+    return k;
+}
+
+void run_and_export(Ctx &c, const char *chain, const mmfhe_chain_cfg &cfg, const mmfhe_ct *in, size_t n_in,
+                    mmfhe_ct *out, size_t n_out)
+{
+    std::vector<DCt> res = run_chain(c, chain, cfg, in, n_in);
+    size_t o = 0;
+    for (auto &d : res)
+        for (uint32_t b = 0; b < d.batch; ++b) {
+            MMFHE_REQUIRE(o < n_out, MMFHE_E_LAYOUT, "chain produced an unexpected number of outputs");
+            export_ct(c, slice(d, b, 1), out[o++]);
+        }
+    MMFHE_REQUIRE(o == n_out, MMFHE_E_LAYOUT, "chain produced an unexpected number of outputs");
+}
+
+// Capture one chain call on a private stream; false if the call is not capturable (the
+// caller then runs it eagerly).  Validation errors surface in that eager run.
+bool capture_chain(Ctx &c, Ctx::ChainGraph &g, const char *chain, const mmfhe_chain_cfg &cfg, const mmfhe_ct *in,
+                   size_t n_in, mmfhe_ct *out, size_t n_out)
+{
+    if (!c.cap_stream) CUDA_CHECK(cudaStreamCreateWithFlags(&c.cap_stream, cudaStreamNonBlocking));
+    const cudaStream_t saved = c.stream;
+    const uint64_t l0 = c.launches;
+    c.stream = c.cap_stream;
+    cudaGraph_t graph = nullptr;
+    bool ok = cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+        try {
+            run_and_export(c, chain, cfg, in, n_in, out, n_out);
+        } catch (...) {
+            ok = false;
+        }
+        ok = cudaStreamEndCapture(c.stream, &graph) == cudaSuccess && ok;
+    }
+    c.stream = saved;
+    g.launches = c.launches - l0;
+    c.launches = l0;
+    cudaGraphExec_t exec = nullptr;
+    ok = ok && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {
+        (void)cudaGetLastError();
+        g.seen = -1;
+        return false;
+    }
+    g.exec = exec;
+    g.out_meta.assign(out, out + n_out);
+    return true;
+}
+
 mmfhe_chain_cfg cfg_or_default(const mmfhe_chain_cfg *cfg)
 {
     mmfhe_chain_cfg d{};
@@ -107,6 +202,7 @@ mmfhe_status mmfhe_chain_required_rotations(mmfhe_ctx *ctx, const char *chain, c
 mmfhe_status mmfhe_load_relin_key(mmfhe_ctx *ctx, const uint64_t *words, size_t n_words, int on_device)
 {
     API_BEGIN
+    state_changed(*ctx);
     MMFHE_REQUIRE(words, MMFHE_E_INVALID_ARG, "null key");
     auto k = std::make_unique<DKey>();
     load_key(*ctx, *k, words, n_words, on_device != 0);
@@ -119,6 +215,7 @@ mmfhe_status mmfhe_load_galois_key(mmfhe_ctx *ctx, int32_t step, const uint64_t 
                                    int on_device)
 {
     API_BEGIN
+    state_changed(*ctx);
     MMFHE_REQUIRE(words, MMFHE_E_INVALID_ARG, "null key");
     int32_t k;
     galois_element(*ctx, step, &k);
@@ -133,6 +230,7 @@ mmfhe_status mmfhe_load_galois_key(mmfhe_ctx *ctx, int32_t step, const uint64_t 
 mmfhe_status mmfhe_load_plain(mmfhe_ctx *ctx, const char *name, const mmfhe_ct *pt)
 {
     API_BEGIN
+    state_changed(*ctx);
     MMFHE_REQUIRE(name && pt && pt->data, MMFHE_E_INVALID_ARG, "null argument");
     MMFHE_REQUIRE(pt->log_n == ctx->log_n, MMFHE_E_PARAMS, "ring dimension mismatch");
     MMFHE_REQUIRE(pt->form == MMFHE_FORM_COEFF, MMFHE_E_FORMAT, "plaintexts are imported in coefficient form");
@@ -145,6 +243,7 @@ mmfhe_status mmfhe_encode_plain(mmfhe_ctx *ctx, const char *name, const double *
                                 double scale)
 {
     API_BEGIN
+    state_changed(*ctx);
     MMFHE_REQUIRE(name && v && n, MMFHE_E_INVALID_ARG, "null argument");
     encode_plain(*ctx, name, std::vector<double>(v, v + n), level, scale);
     API_END(ctx)
@@ -153,6 +252,7 @@ mmfhe_status mmfhe_encode_plain(mmfhe_ctx *ctx, const char *name, const double *
 mmfhe_status mmfhe_load_scalars(mmfhe_ctx *ctx, const char *name, const double *v, size_t n)
 {
     API_BEGIN
+    state_changed(*ctx);
     MMFHE_REQUIRE(name && (v || !n), MMFHE_E_INVALID_ARG, "null argument");
     ctx->scalars[name] = std::vector<double>(v, v + n);
     API_END(ctx)
@@ -162,6 +262,7 @@ mmfhe_status mmfhe_prepare_chain(mmfhe_ctx *ctx, const char *chain, const mmfhe_
                                  const double *const *fc_w, const double *const *fc_b, const double *const *taps)
 {
     API_BEGIN
+    state_changed(*ctx);
     MMFHE_REQUIRE(chain && cfg, MMFHE_E_INVALID_ARG, "null argument");
     mmfhe_chain_cfg c = cfg_or_default(cfg);
     chain_rotations(*ctx, chain, c);  // validates the name
@@ -207,11 +308,28 @@ mmfhe_status mmfhe_eval_chain(mmfhe_ctx *ctx, const char *chain, const mmfhe_cha
     std::vector<uint32_t> lv = chain_plan(*ctx, chain, c, in[0].level, n_in);
     *n_out = lv.size();
     MMFHE_REQUIRE(lv.size() <= cap, MMFHE_E_LAYOUT, "output capacity too small");
-    std::vector<DCt> res = run_chain(*ctx, chain, c, in, n_in);
-    size_t o = 0;
-    for (auto &d : res)
-        for (uint32_t b = 0; b < d.batch; ++b) export_ct(*ctx, slice(d, b, 1), out[o++]);
-    MMFHE_REQUIRE(o == lv.size(), MMFHE_E_LAYOUT, "chain produced an unexpected number of outputs");
+    const size_t n = lv.size();
+    // repeated device-resident calls replay a captured CUDA graph (trace / profile off)
+    if (ctx->graphs_on && !ctx->trace_on && !ctx->prof_on && all_device(in, n_in) && all_device(out, n)) {
+        if (ctx->graphs.size() >= 64) ctx->drop_graphs();
+        Ctx::ChainGraph &g = ctx->graphs[chain_key(*ctx, chain, c, in, n_in, out, n)];
+        if (!g.exec && g.seen >= 1) capture_chain(*ctx, g, chain, c, in, n_in, out, n);
+        if (g.exec) {
+            CUDA_CHECK(cudaGraphLaunch(g.exec, ctx->stream));
+            ctx->launches += g.launches;
+            ++ctx->graph_replays;
+            for (size_t i = 0; i < n; ++i) {
+                out[i].log_n = g.out_meta[i].log_n;
+                out[i].level = g.out_meta[i].level;
+                out[i].scale = g.out_meta[i].scale;
+                out[i].n_slots = g.out_meta[i].n_slots;
+                out[i].n_polys = g.out_meta[i].n_polys;
+            }
+            return MMFHE_OK;
+        }
+        if (g.seen >= 0) ++g.seen;
+    }
+    run_and_export(*ctx, chain, c, in, n_in, out, n);
     API_END(ctx)
 }
 
@@ -235,6 +353,19 @@ static mmfhe_status ntt_rows(mmfhe_ctx *ctx, uint64_t *d_rows, uint32_t n_rows, 
     MMFHE_REQUIRE(d_rows && prime_idx && n_rows, MMFHE_E_INVALID_ARG, "null argument");
     std::vector<uint32_t> m(prime_idx, prime_idx + n_rows);
     for (uint32_t p : m) MMFHE_REQUIRE(p < ctx->primes.size(), MMFHE_E_INVALID_ARG, "prime index out of range");
+    // a periodic prime list (a batch of items with the same limbs) goes in one launch
+    for (uint32_t per = 1; per <= std::min<uint32_t>(kMapCap, n_rows); ++per) {
+        if (n_rows % per) continue;
+        bool ok = true;
+        for (uint32_t i = per; i < n_rows && ok; ++i) ok = m[i] == m[i - per];
+        if (!ok) continue;
+        PrimeMap pm = make_map(std::vector<uint32_t>(m.begin(), m.begin() + per));
+        if (inv)
+            ntt_inverse(*ctx, d_rows, n_rows, pm);
+        else
+            ntt_forward(*ctx, d_rows, n_rows, pm);
+        return MMFHE_OK;
+    }
     for (uint32_t s = 0; s < n_rows; s += kMapCap) {
         uint32_t cnt = std::min<uint32_t>(kMapCap, n_rows - s);
         PrimeMap pm = make_map(std::vector<uint32_t>(m.begin() + s, m.begin() + s + cnt));
@@ -411,6 +542,25 @@ mmfhe_status mmfhe_trace_enable(mmfhe_ctx *ctx, int on)
     API_BEGIN
     ctx->trace_on = on != 0;
     API_END(ctx)
+}
+
+mmfhe_status mmfhe_graph_enable(mmfhe_ctx *ctx, int on)
+{
+    if (!ctx) return fail(ctx, MMFHE_E_INVALID_ARG, "null argument");
+    API_BEGIN
+    ctx->graphs_on = on != 0;
+    if (!ctx->graphs_on) ctx->drop_graphs();
+    API_END(ctx)
+}
+
+mmfhe_status mmfhe_graph_stats(mmfhe_ctx *ctx, size_t *n_graphs, uint64_t *replays)
+{
+    if (!ctx || !n_graphs || !replays) return fail(ctx, MMFHE_E_INVALID_ARG, "null argument");
+    size_t n = 0;
+    for (const auto &kv : ctx->graphs) n += kv.second.exec != nullptr;
+    *n_graphs = n;
+    *replays = ctx->graph_replays;
+    return MMFHE_OK;
 }
 
 mmfhe_status mmfhe_profile_enable(mmfhe_ctx *ctx, int on)

@@ -175,7 +175,18 @@ Ctx::Ctx(const mmfhe_params &p, int dev, cudaStream_t s) : device(dev), stream(s
 Ctx::~Ctx()
 {
     cudaStreamSynchronize(stream);
+    drop_graphs();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+}
+
+void Ctx::drop_graphs()
+{
+    if (graphs.empty()) return;
+    cudaStreamSynchronize(stream);
+    for (auto &kv : graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
 }
 
 namespace {

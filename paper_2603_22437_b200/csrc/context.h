@@ -2,6 +2,7 @@
 // stores, stream, device memory pool, op trace.
 #pragma once
 #include <map>
+#include <unordered_map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -129,6 +130,22 @@ class Ctx {
     size_t ev_used = 0;
     cudaEvent_t next_event();
     std::string profile_report();  // "name count total_ms bytes" lines; resets
+
+    // CUDA-graph replay of repeated device-resident chain calls (mmfhe_eval_chain): the
+    // second identical call is captured, later ones replay the graph, so the host-side
+    // op dispatch (hundreds of launches, allocations, plan lookups) leaves the step.
+    // Any operand-store change bumps state_gen, which is part of the key.
+    struct ChainGraph {
+        cudaGraphExec_t exec = nullptr;
+        uint64_t launches = 0;           // kernel launches inside the graph
+        std::vector<mmfhe_ct> out_meta;  // output level / scale / n_slots / n_polys
+        int seen = 0;                    // < 0: capture failed, never retry
+    };
+    bool graphs_on = true;
+    uint64_t state_gen = 0, graph_replays = 0;
+    std::unordered_map<std::string, ChainGraph> graphs;
+    cudaStream_t cap_stream = nullptr;
+    void drop_graphs();
 
     // trace (Theorem P:999-1006)
     bool trace_on = true;

@@ -32,7 +32,7 @@
 // transform corrects U >= 8q only at global stages s = 3 mod 4 (bounds: input < 2q,
 // then < 10q after each corrected stage, never above 16q), and the row pass fully
 // reduces its output to [0, q).  Inputs of ntt_forward must be < 2q.
-// Every limb of every polynomial of a batch goes in one launch (grid.y = rows).
+// Every limb of every polynomial of a batch goes in one launch.
 #include <algorithm>
 
 #include "context.h"
@@ -131,27 +131,65 @@ __device__ __forceinline__ int soff(int sb, int ke)
 
 __device__ __forceinline__ uint64_t csub64(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
 
+// x < 16q -> x mod q.  k = floor(x * fl(1/q) - 2^-14) in fp32 is floor(x/q) or one less
+// (relative error of the estimate < 2^-21, so |error| < 2^-17 < margin < 1), leaving
+// x - kq in [0, 2q) for one conditional subtraction: ~12 instructions instead of four
+// 64-bit conditional subtractions.
+__device__ __forceinline__ uint64_t reduce16q(uint64_t x, uint64_t q, float qinv)
+{
+    const float y = fmaxf(__fmaf_rn(__ull2float_rn(x), qinv, -0x1p-14f), 0.0f);
+    const uint32_t k = __float2uint_rz(y);
+    return csub64(x - (uint64_t)k * q, q);
+}
+
+// Batch structure of the rows: row = item * rstride + ri, ri < rstride, n_items items.
+struct RowMap {
+    uint32_t n_items, rstride;
+};
+
+// Which row / block / group / lane this thread works on.
+//   col pass: CTA (x, y) = G consecutive columns of row y (coalesced strided columns).
+//   row pass: groups are enumerated item-fastest, z -> (item, block, ri), so the groups of
+//   a CTA are mostly the same block of the same residue row of different batch items:
+//   their twiddles coincide (warp-broadcast loads) and need no per-CTA tail padding.
+template <class Gm, int LOGS, int OTHER, bool COL>
+__device__ __forceinline__ void locate(RowMap rm, size_t &row, int &gi, int &g, int &t)
+{
+    const int tid = threadIdx.x;
+    if (COL) {
+        g = tid & (Gm::G - 1);
+        t = tid >> Gm::LOGG;
+        gi = blockIdx.x * Gm::G + g;
+        row = blockIdx.y;
+    } else {
+        g = tid >> Gm::LOGT;
+        t = tid & (Gm::T - 1);
+        const uint32_t z = blockIdx.x * Gm::G + g;
+        const uint32_t item = z % rm.n_items, rest = z / rm.n_items;
+        gi = rest & ((1u << OTHER) - 1);
+        row = (size_t)item * rm.rstride + (rest >> OTHER);
+    }
+}
+
 // ---------------------------------------------------------------- forward
 // Round widths: the first (top) round takes LOGS - (R-1)*ELOG bits, the others ELOG.
 template <int LOGS, int OTHER, bool COL>
-__global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm)
+__global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm, RowMap rm)
 {
     using Gm = Geo<LOGS, OTHER, COL>;
-    constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, T = Gm::T, G = Gm::G, R = Gm::R, NT = Gm::THREADS;
+    constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, T = Gm::T, G = Gm::G, R = Gm::R;
     constexpr int W0 = LOGS - (R - 1) * ELOG;
     constexpr int LOGN = LOGS + OTHER;
     extern __shared__ uint64_t sm[];
-    const int row = blockIdx.y;
+    size_t row;
+    int gi, g, t;
+    locate<Gm, LOGS, OTHER, COL>(rm, row, gi, g, t);
     const int p = pm.idx[row % pm.period];
     const uint64_t q = kt.q[p], q2 = 2 * q, q8 = 8 * q;
     const TwPair *tw = kt.tw_fwd + ((size_t)p << LOGN);
     uint64_t *a = data + ((size_t)row << LOGN);
-    const int tid = threadIdx.x;
-    const int g = COL ? (tid & (G - 1)) : (tid >> Gm::LOGT);
-    const int t = COL ? (tid >> Gm::LOGG) : (tid & (T - 1));
-    const int gi = blockIdx.x * G + g;  // global column / block index
     uint64_t *buf0 = sm, *buf1 = sm + S * G;
-    uint64_t *tile = a + ((size_t)blockIdx.x * G << LOGS);  // row pass: the CTA's contiguous tile
+    uint64_t *blk = a + ((size_t)gi << LOGS);  // row pass: this group's block
     uint64_t v[E];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -164,9 +202,10 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
         if (r == 0 && !COL) {
             // row pass: load the CTA's tile coalesced into shared memory, then read the
             // round's register pattern from there
-            const int sio = sbase<Gm, LOGS, false>(tid & (S - 1), tid >> LOGS);
+            // the group's T lanes read 8 runs of T consecutive words (coalesced)
+            const int sio = sbase<Gm, LOGS, false>(t, g);
 #pragma unroll
-            for (int i = 0; i < E; ++i) buf1[sio + i * NT] = tile[tid + i * NT];
+            for (int i = 0; i < E; ++i) buf1[soff<Gm, LOGS, false>(sio, i * T)] = blk[t + i * T];
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = buf1[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))];
@@ -215,17 +254,13 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
             // row pass: full reduction (< 16q -> [0, q)), then through shared memory
             // back to a coalesced store of the tile
             uint64_t *b = (r & 1) ? buf1 : buf0;
+            const float qinv = __frcp_rn(__ull2float_rn(q));
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                uint64_t x = csub64(v[e], q8);
-                x = csub64(x, 4 * q);
-                x = csub64(x, q2);
-                b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))] = csub64(x, q);
-            }
+            for (int e = 0; e < E; ++e) b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))] = reduce16q(v[e], q, qinv);
             __syncthreads();
-            const int sio = sbase<Gm, LOGS, false>(tid & (S - 1), tid >> LOGS);
+            const int sio = sbase<Gm, LOGS, false>(t, g);
 #pragma unroll
-            for (int i = 0; i < E; ++i) tile[tid + i * NT] = b[sio + i * NT];
+            for (int i = 0; i < E; ++i) blk[t + i * T] = b[soff<Gm, LOGS, false>(sio, i * T)];
         } else if (r == R - 1) {
             uint64_t *col = a + gi + ((size_t)ktr << OTHER);
 #pragma unroll
@@ -244,23 +279,21 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
 // rounds own bits from the bottom up (the narrow round last, at the top).  Harvey
 // GS butterflies keep words in [0, 2q); the col pass (last) multiplies by N^{-1}.
 template <int LOGS, int OTHER, bool COL>
-__global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm)
+__global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm, RowMap rm)
 {
     using Gm = Geo<LOGS, OTHER, COL>;
-    constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, T = Gm::T, G = Gm::G, R = Gm::R, NT = Gm::THREADS;
+    constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, T = Gm::T, G = Gm::G, R = Gm::R;
     constexpr int LOGN = LOGS + OTHER;
     extern __shared__ uint64_t sm[];
-    const int row = blockIdx.y;
+    size_t row;
+    int gi, g, t;
+    locate<Gm, LOGS, OTHER, COL>(rm, row, gi, g, t);
     const int p = pm.idx[row % pm.period];
     const uint64_t q = kt.q[p], q2 = 2 * q;
     const TwPair *tw = kt.tw_inv + ((size_t)p << LOGN);
     uint64_t *a = data + ((size_t)row << LOGN);
-    const int tid = threadIdx.x;
-    const int g = COL ? (tid & (G - 1)) : (tid >> Gm::LOGT);
-    const int t = COL ? (tid >> Gm::LOGG) : (tid & (T - 1));
-    const int gi = blockIdx.x * G + g;
     uint64_t *buf0 = sm, *buf1 = sm + S * G;
-    uint64_t *tile = a + ((size_t)blockIdx.x * G << LOGS);
+    uint64_t *blk = a + ((size_t)gi << LOGS);  // row pass: this group's block
     uint64_t v[E];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -269,9 +302,10 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
         const int ktr = kmap(ELOG, lo, w, t, 0);
         const int sb = sbase<Gm, LOGS, COL>(ktr, g);
         if (r == 0 && !COL) {
-            const int sio = sbase<Gm, LOGS, false>(tid & (S - 1), tid >> LOGS);
+            // the group's T lanes read 8 runs of T consecutive words (coalesced)
+            const int sio = sbase<Gm, LOGS, false>(t, g);
 #pragma unroll
-            for (int i = 0; i < E; ++i) buf1[sio + i * NT] = tile[tid + i * NT];
+            for (int i = 0; i < E; ++i) buf1[soff<Gm, LOGS, false>(sio, i * T)] = blk[t + i * T];
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = buf1[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))];
@@ -319,9 +353,9 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
 #pragma unroll
             for (int e = 0; e < E; ++e) b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))] = v[e];
             __syncthreads();
-            const int sio = sbase<Gm, LOGS, false>(tid & (S - 1), tid >> LOGS);
+            const int sio = sbase<Gm, LOGS, false>(t, g);
 #pragma unroll
-            for (int i = 0; i < E; ++i) tile[tid + i * NT] = b[sio + i * NT];
+            for (int i = 0; i < E; ++i) blk[t + i * T] = b[soff<Gm, LOGS, false>(sio, i * T)];
         } else if (r == R - 1) {
             const TwPair ninv = kt.n_inv[p];
             uint64_t *col = a + gi + ((size_t)ktr << OTHER);
@@ -349,7 +383,18 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
         return true;
     }();
     (void)attr;
-    kern<<<dim3((1u << OTHER) / Gm::G, rows), Gm::THREADS, Gm::SMEM, s>>>(d, kt, pm);
+    if (COL) {
+        // grid.y <= 65535: chunks of whole periods keep row % period aligned
+        const uint32_t chunk = 65535u / pm.period * pm.period;
+        for (uint32_t r0 = 0; r0 < rows; r0 += chunk)
+            kern<<<dim3((1u << OTHER) / Gm::G, std::min(chunk, rows - r0)), Gm::THREADS, Gm::SMEM, s>>>(
+                d + ((size_t)r0 << (LOGS + OTHER)), kt, pm, RowMap{rows, 1});
+    } else {
+        // rows are items of pm.period residue rows each whenever that divides
+        const uint32_t stride = rows % pm.period == 0 ? pm.period : 1;
+        const RowMap rm{rows / stride, stride};
+        kern<<<dim3((uint32_t)(((size_t)rows << OTHER) / Gm::G)), Gm::THREADS, Gm::SMEM, s>>>(d, kt, pm, rm);
+    }
 }
 
 // Radix-8 everywhere: radix-16 (ELOG = 4) halves the exchanges but its 64 KiB CTAs and

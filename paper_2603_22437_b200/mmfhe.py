@@ -118,6 +118,8 @@ def lib():
             "mmfhe_trace_get": [V, ctypes.c_char_p, S, P(S)],
             "mmfhe_trace_clear": [V],
             "mmfhe_trace_enable": [V, ctypes.c_int],
+            "mmfhe_graph_enable": [V, ctypes.c_int],
+            "mmfhe_graph_stats": [V, P(S), P(ctypes.c_uint64)],
             "mmfhe_profile_enable": [V, ctypes.c_int],
             "mmfhe_profile_get": [V, ctypes.c_char_p, S, P(S)],
             "mmfhe_microbench": [V, ctypes.c_int, P(ctypes.c_double)],
@@ -140,7 +142,7 @@ EXPORTED = [
     "mmfhe_sum_partials", "mmfhe_ntt", "mmfhe_intt", "mmfhe_hadd", "mmfhe_hsub", "mmfhe_pmult", "mmfhe_hmult",
     "mmfhe_relin", "mmfhe_hrot", "mmfhe_hrot_hoisted", "mmfhe_rescale", "mmfhe_keyswitch", "mmfhe_mod_switch", "mmfhe_hrot_batch",
     "mmfhe_hmult_batch", "mmfhe_trace_get", "mmfhe_trace_clear", "mmfhe_trace_enable", "mmfhe_profile_enable",
-    "mmfhe_profile_get", "mmfhe_microbench",
+    "mmfhe_profile_get", "mmfhe_microbench", "mmfhe_graph_enable", "mmfhe_graph_stats",
 ]
 
 
@@ -382,6 +384,16 @@ class Context:
 
     def trace_enable(self, on=True):
         self._check(self._lib.mmfhe_trace_enable(self.h, 1 if on else 0))
+
+    def graph_enable(self, on=True):
+        """CUDA-graph replay of repeated device-resident eval_chain calls (default on)."""
+        self._check(self._lib.mmfhe_graph_enable(self.h, 1 if on else 0))
+
+    def graph_stats(self):
+        """(captured graphs held, graph replays so far)."""
+        n, r = ctypes.c_size_t(), ctypes.c_uint64()
+        self._check(self._lib.mmfhe_graph_stats(self.h, ctypes.byref(n), ctypes.byref(r)))
+        return n.value, r.value
 
     def profile_enable(self, on=True):
         self._check(self._lib.mmfhe_profile_enable(self.h, 1 if on else 0))

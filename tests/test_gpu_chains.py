@@ -116,6 +116,68 @@ def test_vitals_v1_small(m):
     assert sorted(ctx.required_rotations("vitals_v1", _mcfg(m, cfg))) == cc.required_rotations("vitals_v1", cfg, P.n)
 
 
+def test_graph_replay_matches_eager(m):
+    """Repeated device-resident eval_chain calls (trace off) are captured once and replayed
+    as a CUDA graph: residues stay bit-exact with the oracle on every call, the launch
+    count per call is unchanged, replays re-read new input contents, and an operand-store
+    change invalidates the captured graph."""
+    import torch
+    P = toy(log_n=10, n_q=6, scale_bits=40, n_p=2, alpha=2)
+    cfg = cc.ChainCfg(R=16, F=6, gamma=2, n_slots=P.n // 2)
+    keys = orc.keygen(P, seed=3151, rotations=cc.required_rotations("vitals_v1", cfg, P.n))
+    book = cc.PlainBook(P)
+    wants = []
+    inputs = []
+    for seed in (3152, 3153):
+        _, cts = _vital_inputs(P, keys, cfg, 3, seed)
+        ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+        wants.append(cc.vitals_v1(ev, book, cts[0::2], cts[1::2], cfg))
+        inputs.append(cts)
+    ctx = make_ctx(m, P, keys, book)
+    ctx.trace_enable(False)
+    mcfg = _mcfg(m, cfg)
+    ins = [ct_in(m, P, c) for c in inputs[0]]
+    outs = [ct_out(m, P, lv) for lv in ctx.chain_plan("vitals_v1", mcfg, 3, len(ins))]
+
+    def check(want):
+        for o, w in zip(outs, want):
+            assert np.array_equal(residues(o), np.stack(w.c))
+            assert o.level == w.level and o.scale == w.scale
+
+    deltas = []
+    for _ in range(4):
+        l0 = ctx.launch_count()
+        ctx.eval_chain("vitals_v1", mcfg, ins, outs)
+        torch.cuda.synchronize()
+        deltas.append(ctx.launch_count() - l0)
+        check(wants[0])
+    assert len(set(deltas)) == 1 and deltas[0] > 0
+    n_graphs, replays = ctx.graph_stats()
+    assert n_graphs == 1 and replays == 3  # call 2 captured + launched, calls 3-4 replayed
+    # same buffers, new contents: the replay reads them
+    for x, c in zip(ins, inputs[1]):
+        x.data.copy_(ct_in(m, P, c).data)
+    ctx.eval_chain("vitals_v1", mcfg, ins, outs)
+    torch.cuda.synchronize()
+    assert ctx.graph_stats()[1] == 4
+    check(wants[1])
+    # an operand-store change drops the graphs; the next call runs eagerly and is still exact
+    ctx.load_scalars("unused", [1.0])
+    assert ctx.graph_stats()[0] == 0
+    for o in outs:
+        o.data.zero_()
+    ctx.eval_chain("vitals_v1", mcfg, ins, outs)
+    torch.cuda.synchronize()
+    check(wants[1])
+    # graphs off: eager every call
+    ctx.graph_enable(False)
+    ctx.eval_chain("vitals_v1", mcfg, ins, outs)
+    ctx.eval_chain("vitals_v1", mcfg, ins, outs)
+    torch.cuda.synchronize()
+    assert ctx.graph_stats() == (0, 4)
+    check(wants[1])
+
+
 def _gesture(P, seed, F=2, A=2, R=4, D=8, frame_batch=0, hoist=0):
     n = A * R * D
     cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8), frame_batch=frame_batch,
