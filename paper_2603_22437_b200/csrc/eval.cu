@@ -341,7 +341,15 @@ DCt ev_lincomb_mat(Ctx &c, const DCt &in, uint32_t J, uint32_t W, int lo0, int l
         it = c.const_cache.emplace(key, std::move(b)).first;
     }
     DCt r = make_ct(c, l, 2, in.n_slots, in.scale * (double)ql, J);
-    launch_lincomb_mat(c, r.data(), in.data(), M, J, W, lo0, lo_step, (const TwPair *)it->second.get(), l);
+    // Toeplitz rows with one symmetric tap vector (linear-phase FIR): equal doubles encode to
+    // equal residues, so pairing the mirrored inputs before the product is exact
+    bool sym = lo_step == 1 && W >= 2 && W <= 129;
+    for (uint32_t w = 0; sym && w < W; ++w) sym = coef[w] == coef[W - 1 - w];
+    for (size_t t = W; sym && t < coef.size(); ++t) sym = coef[t] == coef[t % W];
+    if (sym)
+        launch_lincomb_sym(c, r.data(), in.data(), M, J, W, lo0, (const TwPair *)it->second.get(), l);
+    else
+        launch_lincomb_mat(c, r.data(), in.data(), M, J, W, lo0, lo_step, (const TwPair *)it->second.get(), l);
     return r;
 }
 

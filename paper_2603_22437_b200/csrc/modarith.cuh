@@ -40,6 +40,18 @@ __device__ __forceinline__ U128 mul128(uint64_t a, uint64_t b)
 
 __device__ __forceinline__ uint64_t csub(uint64_t a, uint64_t q) { return a >= q ? a - q : a; }
 
+// Reduction of a lazily accumulated x < 2^17 q to [0, q) by an fp32 quotient estimate:
+// qinv_est(q) = fl(1/q)(1 - 2^-18), k = floor(x qinv - 2^-14) is floor(x/q) or one less
+// (combined relative error of the three roundings and the approximate reciprocal is
+// < 2^-21 < the 2^-18 margin), so x - kq lies in [0, 2q) and one subtraction finishes.
+__device__ __forceinline__ float qinv_est(uint64_t q) { return __fdividef(1.0f, __ull2float_rn(q)) * (1.0f - 0x1p-18f); }
+__device__ __forceinline__ uint64_t reduce_est(uint64_t x, uint64_t q, float qinv)
+{
+    const float y = fmaxf(__fmaf_rn(__ull2float_rn(x), qinv, -0x1p-14f), 0.0f);
+    const uint64_t r = x - (uint64_t)__float2uint_rz(y) * q;
+    return r >= q ? r - q : r;
+}
+
 __device__ __forceinline__ uint64_t add_mod(uint64_t a, uint64_t b, uint64_t q) { return csub(a + b, q); }
 __device__ __forceinline__ uint64_t sub_mod(uint64_t a, uint64_t b, uint64_t q) { return a >= b ? a - b : a + q - b; }
 

@@ -31,7 +31,7 @@
 // bound by 2q, so instead of Harvey's per-butterfly U >= 2q correction the forward
 // transform corrects U >= 8q only at global stages s = 3 mod 4 (bounds: input < 2q,
 // then < 10q after each corrected stage, never above 16q), and the row pass fully
-// reduces its output to [0, q).  Inputs of ntt_forward must be < 2q.
+// reduces its output to [0, q) with one estimated-quotient step (reduce_est).  Inputs of ntt_forward must be < 2q.
 // Every limb of every polynomial of a batch goes in one launch.
 #include <algorithm>
 
@@ -130,17 +130,6 @@ __device__ __forceinline__ int soff(int sb, int ke)
 }
 
 __device__ __forceinline__ uint64_t csub64(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
-
-// x < 16q -> x mod q.  k = floor(x * fl(1/q) - 2^-14) in fp32 is floor(x/q) or one less
-// (relative error of the estimate < 2^-21, so |error| < 2^-17 < margin < 1), leaving
-// x - kq in [0, 2q) for one conditional subtraction: ~12 instructions instead of four
-// 64-bit conditional subtractions.
-__device__ __forceinline__ uint64_t reduce16q(uint64_t x, uint64_t q, float qinv)
-{
-    const float y = fmaxf(__fmaf_rn(__ull2float_rn(x), qinv, -0x1p-14f), 0.0f);
-    const uint32_t k = __float2uint_rz(y);
-    return csub64(x - (uint64_t)k * q, q);
-}
 
 // Batch structure of the rows: row = item * rstride + ri, ri < rstride, n_items items.
 struct RowMap {
@@ -254,9 +243,9 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
             // row pass: full reduction (< 16q -> [0, q)), then through shared memory
             // back to a coalesced store of the tile
             uint64_t *b = (r & 1) ? buf1 : buf0;
-            const float qinv = __frcp_rn(__ull2float_rn(q));
+            const float qinv = qinv_est(q);
 #pragma unroll
-            for (int e = 0; e < E; ++e) b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))] = reduce16q(v[e], q, qinv);
+            for (int e = 0; e < E; ++e) b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))] = reduce_est(v[e], q, qinv);
             __syncthreads();
             const int sio = sbase<Gm, LOGS, false>(t, g);
 #pragma unroll

@@ -61,6 +61,9 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
 // C given as Shoup pairs [J][W][l+1]; inputs outside [0, M) contribute nothing.
 void launch_lincomb_mat(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, uint32_t J, uint32_t W, int lo0,
                         int lo_step, const TwPair *C, uint32_t level);
+// symmetric Toeplitz rows (every row the same taps, c_w == c_{W-1-w}); T: TwPair[W][level+1]
+void launch_lincomb_sym(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, uint32_t J, uint32_t W, int lo0,
+                        const TwPair *T, uint32_t level);
 // out = sum_b in_b over a batch of B items of `words` words each (rows of level l).
 void launch_batch_sum(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t B, uint32_t npolys, uint32_t level);
 // out[b] = copy of src.p[b] (n <= kMaxTerms items of `words` words each; device pointers,

@@ -397,6 +397,38 @@ __global__ void __launch_bounds__(kTB) k_diag_mac(DiagMacArgs a, KTables kt, uin
 
 constexpr int kJG = 8;  // outputs per thread in the modular matrix product
 
+// One thread's term loop of k_lincomb_mat.  LAZY: every term shoup_lazy() < 2q is added
+// without correction (the caller guarantees (W + kJG) 2q < 2^63, true for every 40/50-bit
+// scaling prime); otherwise (the 60-bit q_0) each partial sum is kept in [0, 2q).
+template <bool LAZY>
+__device__ __forceinline__ void lincomb_terms(uint64_t (&a0)[kJG], uint64_t (&a1)[kJG], const uint64_t *__restrict__ in,
+                                              size_t item, size_t ps, size_t off, int ilo, int ihi, uint32_t j0,
+                                              uint32_t jn, uint32_t W, int lo0, int lo_step,
+                                              const TwPair *__restrict__ C, uint32_t L1, uint32_t r, uint64_t q)
+{
+    const uint64_t q2 = 2 * q;
+    for (int i = ilo; i < ihi; ++i) {
+        const uint64_t x0 = in[(size_t)i * item + off], x1 = in[(size_t)i * item + ps + off];
+#pragma unroll
+        for (int jj = 0; jj < kJG; ++jj) {
+            if (jj < (int)jn) {
+                const int w = i - (lo0 + (int)(j0 + jj) * lo_step);
+                if (w >= 0 && w < (int)W) {
+                    const TwPair c = C[((size_t)(j0 + jj) * W + w) * L1 + r];
+                    uint64_t s0 = a0[jj] + shoup_lazy(x0, c.w, c.wp, q);
+                    uint64_t s1 = a1[jj] + shoup_lazy(x1, c.w, c.wp, q);
+                    if (!LAZY) {
+                        s0 = s0 >= q2 ? s0 - q2 : s0;
+                        s1 = s1 >= q2 ? s1 - q2 : s1;
+                    }
+                    a0[jj] = s0;
+                    a1[jj] = s1;
+                }
+            }
+        }
+    }
+}
+
 // out[j] = sum_w C[j][w] in[lo_j + w] for j in this CTA's group of kJG outputs.
 __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out, const uint64_t *__restrict__ in,
                                                      uint32_t M, uint32_t J, uint32_t W, int lo0, int lo_step,
@@ -407,7 +439,7 @@ __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out,
     const uint32_t r = blockIdx.y;
     const uint32_t j0 = blockIdx.z * kJG;
     const uint32_t jn = min((uint32_t)kJG, J - j0);
-    const uint64_t q = kt.q[r], q2 = 2 * q;
+    const uint64_t q = kt.q[r];
     const uint32_t L1 = level + 1;
     const size_t ps = (size_t)L1 * kt.n, item = 2 * ps;
     const size_t off = (size_t)r * kt.n + k;
@@ -422,28 +454,78 @@ __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out,
     uint64_t a0[kJG], a1[kJG];
 #pragma unroll
     for (int jj = 0; jj < kJG; ++jj) a0[jj] = a1[jj] = 0;
-    for (int i = ilo; i < ihi; ++i) {
-        const uint64_t x0 = in[(size_t)i * item + off], x1 = in[(size_t)i * item + ps + off];
-#pragma unroll
-        for (int jj = 0; jj < kJG; ++jj) {
-            if (jj < (int)jn) {
-                const int w = i - (lo0 + (int)(j0 + jj) * lo_step);
-                if (w >= 0 && w < (int)W) {
-                    const TwPair c = C[((size_t)(j0 + jj) * W + w) * L1 + r];
-                    uint64_t s0 = a0[jj] + shoup_lazy(x0, c.w, c.wp, q);
-                    uint64_t s1 = a1[jj] + shoup_lazy(x1, c.w, c.wp, q);
-                    a0[jj] = s0 >= q2 ? s0 - q2 : s0;
-                    a1[jj] = s1 >= q2 ? s1 - q2 : s1;
-                }
-            }
-        }
-    }
+    // per-CTA uniform: one limb per blockIdx.y
+    if ((uint64_t)(W + kJG) * 2 * q < (1ull << 63) && W + kJG < (1u << 16))
+        lincomb_terms<true>(a0, a1, in, item, ps, off, ilo, ihi, j0, jn, W, lo0, lo_step, C, L1, r, q);
+    else
+        lincomb_terms<false>(a0, a1, in, item, ps, off, ilo, ihi, j0, jn, W, lo0, lo_step, C, L1, r, q);
+    const float qinv = qinv_est(q);
 #pragma unroll
     for (int jj = 0; jj < kJG; ++jj) {
         if (jj < (int)jn) {
-            out[(size_t)(j0 + jj) * item + off] = csub(a0[jj], q);
-            out[(size_t)(j0 + jj) * item + ps + off] = csub(a1[jj], q);
+            out[(size_t)(j0 + jj) * item + off] = reduce_est(a0[jj], q, qinv);
+            out[(size_t)(j0 + jj) * item + ps + off] = reduce_est(a1[jj], q, qinv);
         }
+    }
+}
+
+// Symmetric Toeplitz rows (K5 FIR with linear-phase taps): every output j
+// uses the same taps c_w on inputs lo0 + j + w with c_w == c_{W-1-w} as encoded integers
+// (checked on the host), so out[j] = sum_{w < W/2} c_w (x_a + x_b) + c_mid x_mid exactly
+// (mod q): half the modular products of k_lincomb_mat.  A CTA stages the input window of
+// its kSymJT outputs for kSymK coefficients of one (poly, limb) row in shared memory
+// (zeros outside [0, M)); each thread owns one coefficient and kSymJT / kSymSplit outputs.
+constexpr int kSymK = 128, kSymJT = 32, kSymSplit = 2;
+
+template <bool LAZY>
+__device__ __forceinline__ uint64_t lincomb_sym_row(const uint64_t *__restrict__ X, int b, int W,
+                                                    const TwPair *__restrict__ T, uint32_t L1, uint32_t r, uint64_t q)
+{
+    const uint64_t q2 = 2 * q;
+    uint64_t acc = 0;
+    for (int w = 0; w < W / 2; ++w) {
+        const TwPair c = T[(size_t)w * L1 + r];
+        const uint64_t x = X[(b + w) * kSymK] + X[(b + W - 1 - w) * kSymK];  // < 2q
+        acc += shoup_lazy(x, c.w, c.wp, q);
+        if (!LAZY) acc = acc >= q2 ? acc - q2 : acc;
+    }
+    if (W & 1) {
+        const TwPair c = T[(size_t)(W / 2) * L1 + r];
+        acc += shoup_lazy(X[(b + W / 2) * kSymK], c.w, c.wp, q);
+        if (!LAZY) acc = acc >= q2 ? acc - q2 : acc;
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(kSymK *kSymSplit) k_lincomb_sym(uint64_t *__restrict__ out,
+                                                                  const uint64_t *__restrict__ in, uint32_t M,
+                                                                  uint32_t J, uint32_t W, int lo0,
+                                                                  const TwPair *__restrict__ T, KTables kt,
+                                                                  uint32_t level)
+{
+    extern __shared__ uint64_t X[];  // [kSymJT + W - 1][kSymK]
+    const uint32_t L1 = level + 1;
+    const uint32_t r = blockIdx.y % L1, poly = blockIdx.y / L1;
+    const uint32_t k0 = blockIdx.x * kSymK, j0 = blockIdx.z * kSymJT;
+    const uint64_t q = kt.q[r];
+    const size_t ps = (size_t)L1 * kt.n, item = 2 * ps;
+    const size_t col = (size_t)poly * ps + (size_t)r * kt.n + k0;
+    const int rows = kSymJT + (int)W - 1;
+    for (int idx = threadIdx.x; idx < rows * kSymK; idx += blockDim.x) {
+        const int i = lo0 + (int)j0 + idx / kSymK;
+        X[idx] = (i >= 0 && i < (int)M) ? in[(size_t)i * item + col + idx % kSymK] : 0;
+    }
+    __syncthreads();
+    const int k = threadIdx.x % kSymK, part = threadIdx.x / kSymK;
+    const bool lazy = (uint64_t)(W / 2 + 2) * 2 * q < (1ull << 63);
+    const float qinv = qinv_est(q);
+    constexpr int per = kSymJT / kSymSplit;
+    for (int jj = part * per; jj < (part + 1) * per; ++jj) {
+        const uint32_t j = j0 + jj;
+        if (j >= J) break;
+        const uint64_t acc = lazy ? lincomb_sym_row<true>(X + k, jj, (int)W, T, L1, r, q)
+                                  : lincomb_sym_row<false>(X + k, jj, (int)W, T, L1, r, q);
+        out[(size_t)j * item + col + k] = reduce_est(acc, q, qinv);
     }
 }
 
@@ -709,6 +791,22 @@ void launch_lincomb_mat(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, u
     ProfScope ps(c, "lincomb_mat", 8.0 * 2.0 * (level + 1) * c.n * ((double)M + J));
     k_lincomb_mat<<<grid3(c.n, level + 1, (J + kJG - 1) / kJG), kTB, 0, c.stream>>>(out, in, M, J, W, lo0, lo_step,
                                                                                    C, c.kt, level);
+    LAUNCH_CHECK(c);
+}
+
+void launch_lincomb_sym(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, uint32_t J, uint32_t W, int lo0,
+                        const TwPair *T, uint32_t level)
+{
+    const size_t smem = sizeof(uint64_t) * (kSymJT + W - 1) * kSymK;
+    MMFHE_REQUIRE(smem <= 200 * 1024, MMFHE_E_SHAPE, "FIR too long for the staged window");
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_lincomb_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr = true;
+    }
+    ProfScope ps(c, "lincomb_mat", 8.0 * 2.0 * (level + 1) * c.n * ((double)M + J));
+    const dim3 grid(c.n / kSymK, 2 * (level + 1), (J + kSymJT - 1) / kSymJT);
+    k_lincomb_sym<<<grid, kSymK * kSymSplit, smem, c.stream>>>(out, in, M, J, W, lo0, T, c.kt, level);
     LAUNCH_CHECK(c);
 }
 

@@ -267,13 +267,19 @@ def test_k3_doppler_dft_c3_full_size(m):
     assert np.max(np.abs(got - want.real)) <= 1e-3 * np.max(np.abs(want.real))
 
 
-def test_vitals_v2_small(m):
+@pytest.mark.parametrize("taps", [
+    # linear-phase (symmetric) taps: the paired k_lincomb_sym path, even and odd length
+    ([0.2, 0.3, 0.3, 0.2], [0.25, -0.5, 0.25]),
+    # asymmetric taps: the general k_lincomb_mat path
+    ([0.1, 0.3, 0.4, 0.2], [0.25, -0.5, 0.3]),
+])
+def test_vitals_v2_small(m, taps):
     P = toy(log_n=10, n_q=10, scale_bits=40, n_p=2, alpha=2)  # third order needs 9 levels
     cfg = cc.ChainCfg(R=8, F=10, p_phi=2, taylor_order=3, n_slots=P.n // 2, fs=2.0,
                       bands=((0.1, 0.6), (0.7, 1.0)), frame_batch=4)
     keys = orc.keygen(P, seed=3401, rotations=cc.required_rotations("vitals_v2", cfg, P.n))
     _, cts = _vital_inputs(P, keys, cfg, 9, 3402)
-    taps = [np.array([0.2, 0.3, 0.3, 0.2]), np.array([0.25, -0.5, 0.25])]
+    taps = [np.array(t) for t in taps]
     ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
     out = cc.vitals_v2(ev, cts[0::2], cts[1::2], taps, cfg)
     want = out[0] + out[1]
