@@ -586,6 +586,23 @@ def roofline(prof, peaks, int_peaks):
     return out
 
 
+def kernel_table(prof, peaks, int_peaks, steps):
+    """Per kernel: ms/step, algorithmic HBM GB/s and its fraction of the measured HBM peak;
+    NTT passes also Gbutterfly/s against the in-run butterfly microbenchmark."""
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    out = {}
+    for name, (cnt, ms, by, ops) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        gbs = by / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        row = {"ms_per_step": round(ms / steps, 3), "launches_per_step": cnt // max(steps, 1),
+               "alg_gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm_peak, 3)}
+        if name.startswith("ntt_") and ops > 0 and ms > 0:
+            peak = int_peaks["ct_butterfly"] if "fwd" in name else int_peaks["gs_butterfly"]
+            row["gbfly_s"] = round(ops / (ms / 1e3) / 1e9, 1)
+            row["alu_frac"] = round(ops / (ms / 1e3) / peak, 3)
+        out[name] = row
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -646,6 +663,7 @@ def main():
             "clocks": r["clocks"], "e2e": r["e2e"], "gpu_launches": r["launches"], "roofline": rl,
             "cpu_baseline": cpu, "extras": r["extras"],
             "kernel_profile_ms_per_step": {k: round(v[1] / r["prof_steps"], 3) for k, v in r["prof"].items()},
+            "kernel_roofline": kernel_table(r["prof"], peaks, r["int_peaks"], r["prof_steps"]),
             "profiled_step_ms": r["prof_ms"],
             "int_peaks_ops_per_s": r["int_peaks"],
         }

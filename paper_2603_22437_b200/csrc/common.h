@@ -74,6 +74,7 @@ struct KTables {
     const TwPair *tw_fwd;      // [np][N]  psi^{bitrev(k)}
     const TwPair *tw_inv;      // [np][N]  psi^{-bitrev(k)}
     const TwPair *n_inv;       // [np]
+    const uint64_t *recip;     // [np] floor(2^64 / q): shoup_lazy(x, 1, recip, q) = x mod q in [0, 2q)
     uint32_t log_n;
     uint32_t n;
 };
@@ -83,6 +84,17 @@ constexpr int kMapCap = 256;
 struct PrimeMap {
     uint8_t idx[kMapCap];
     uint32_t period;
+};
+
+// Optional source of the forward NTT's col pass: row r reads
+// x + (r / period) * xs + src[r % period] * N and reduces it into [0, 2q) on load.
+// ModUp of single-limb digits (alpha = 1) is exactly y = x_j mod q_t,
+// so the base conversion fuses into the transform's first HBM read.
+struct ColSrc {
+    const uint64_t *x;  // nullptr: the pass transforms its own rows
+    size_t xs;          // item stride of x (words)
+    uint32_t period;    // == the PrimeMap period
+    uint8_t src[kMapCap];
 };
 
 inline PrimeMap make_map(const std::vector<uint32_t> &v)

@@ -343,6 +343,7 @@ void Ctx::build_tables()
     CUDA_CHECK(cudaMemcpyAsync(tab_bconv.get(), blob.bytes.data(), blob.bytes.size(), cudaMemcpyHostToDevice,
                                stream));
     CUDA_CHECK(cudaStreamSynchronize(stream));
+    kt.recip = (const uint64_t *)bconv_ptr(off_recip);
 }
 
 }  // namespace mmfhe

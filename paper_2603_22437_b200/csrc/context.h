@@ -196,7 +196,8 @@ class ProfScope {
 };
 
 // ------------------------------------------------------------------ kernels (launchers)
-void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm);
+// src: optional fused source of the col pass (ModUp of single-limb digits), see ColSrc
+void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const ColSrc *src = nullptr);
 void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm);
 
 }  // namespace mmfhe

@@ -393,8 +393,22 @@ ModUpOut ks_modup(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t
         m.T += p.n_tgt;
     }
     m.y = DBuf(B * m.T * N, c.stream);
-    launch_modup_bconv(c, m.y.get(), m.T * N, xc.get(), lw, l, m.off, B);
-    ntt_forward(c, m.y.get(), (uint32_t)(B * m.T), make_map(m.rowmap));
+    bool single = m.T <= (size_t)kMapCap;
+    for (const auto &p : plans) single = single && p.hi - p.lo == 1;
+    if (single) {
+        // single-limb digits: BConv is y = x_j mod q_t, fused into the NTT's first read
+        ColSrc src{};
+        src.x = xc.get();
+        src.xs = lw;
+        src.period = (uint32_t)m.T;
+        size_t t = 0;
+        for (const auto &p : plans)
+            for (uint32_t i = 0; i < p.n_tgt; ++i) src.src[t++] = (uint8_t)p.lo;
+        ntt_forward(c, m.y.get(), (uint32_t)(B * m.T), make_map(m.rowmap), &src);
+    } else {
+        launch_modup_bconv(c, m.y.get(), m.T * N, xc.get(), lw, l, m.off, B);
+        ntt_forward(c, m.y.get(), (uint32_t)(B * m.T), make_map(m.rowmap));
+    }
     return m;
 }
 

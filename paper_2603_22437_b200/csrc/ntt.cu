@@ -163,7 +163,8 @@ __device__ __forceinline__ void locate(RowMap rm, size_t &row, int &gi, int &g, 
 // ---------------------------------------------------------------- forward
 // Round widths: the first (top) round takes LOGS - (R-1)*ELOG bits, the others ELOG.
 template <int LOGS, int OTHER, bool COL>
-__global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm, RowMap rm)
+__global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm, RowMap rm,
+                                                                      ColSrc cs)
 {
     using Gm = Geo<LOGS, OTHER, COL>;
     constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, T = Gm::T, G = Gm::G, R = Gm::R;
@@ -198,6 +199,13 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
             __syncthreads();
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = buf1[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))];
+        } else if (r == 0 && cs.x != nullptr) {
+            // fused ModUp (alpha = 1): this row is x_j mod q of a source limb x_j
+            const uint64_t *src = cs.x + (row / cs.period) * cs.xs + ((size_t)cs.src[row % cs.period] << LOGN);
+            const uint64_t *col = src + gi + ((size_t)ktr << OTHER);
+            const uint64_t rc = kt.recip[p];
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = shoup_lazy(col[(size_t)kmap(ELOG, lo, w, 0, e) << OTHER], 1, rc, q);
         } else if (r == 0) {
             const uint64_t *col = a + gi + ((size_t)ktr << OTHER);
 #pragma unroll
@@ -360,29 +368,45 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
 }
 
 template <bool FWD, int LOGS, int OTHER, bool COL>
-void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm, cudaStream_t s)
+void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm, const ColSrc *cs, cudaStream_t s)
 {
     using Gm = Geo<LOGS, OTHER, COL>;
     static_assert(Gm::SMEM <= 48 * 1024, "NTT pass exceeds the default dynamic shared memory");
-    auto kern = FWD ? ntt_fwd_pass<LOGS, OTHER, COL> : ntt_inv_pass<LOGS, OTHER, COL>;
     // prefer the shared-memory carveout: residency is bounded by registers, not by L1
-    static const bool attr = [&] {
-        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                        cudaSharedmemCarveoutMaxShared));
+    static const bool attr = [] {
+        if (FWD)
+            CUDA_CHECK(cudaFuncSetAttribute(ntt_fwd_pass<LOGS, OTHER, COL>,
+                                            cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            cudaSharedmemCarveoutMaxShared));
+        else
+            CUDA_CHECK(cudaFuncSetAttribute(ntt_inv_pass<LOGS, OTHER, COL>,
+                                            cudaFuncAttributePreferredSharedMemoryCarveout,
+                                            cudaSharedmemCarveoutMaxShared));
         return true;
     }();
     (void)attr;
+    auto go = [&](dim3 grid, uint64_t *dd, RowMap rm, const ColSrc &src) {
+        if constexpr (FWD)
+            ntt_fwd_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm, src);
+        else
+            ntt_inv_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm);
+    };
     if (COL) {
         // grid.y <= 65535: chunks of whole periods keep row % period aligned
         const uint32_t chunk = 65535u / pm.period * pm.period;
-        for (uint32_t r0 = 0; r0 < rows; r0 += chunk)
-            kern<<<dim3((1u << OTHER) / Gm::G, std::min(chunk, rows - r0)), Gm::THREADS, Gm::SMEM, s>>>(
-                d + ((size_t)r0 << (LOGS + OTHER)), kt, pm, RowMap{rows, 1});
+        for (uint32_t r0 = 0; r0 < rows; r0 += chunk) {
+            ColSrc src{};
+            if (cs) {
+                src = *cs;
+                src.x += (size_t)(r0 / pm.period) * cs->xs;
+            }
+            go(dim3((1u << OTHER) / Gm::G, std::min(chunk, rows - r0)), d + ((size_t)r0 << (LOGS + OTHER)),
+               RowMap{rows, 1}, src);
+        }
     } else {
         // rows are items of pm.period residue rows each whenever that divides
         const uint32_t stride = rows % pm.period == 0 ? pm.period : 1;
-        const RowMap rm{rows / stride, stride};
-        kern<<<dim3((uint32_t)(((size_t)rows << OTHER) / Gm::G)), Gm::THREADS, Gm::SMEM, s>>>(d, kt, pm, rm);
+        go(dim3((uint32_t)(((size_t)rows << OTHER) / Gm::G)), d, RowMap{rows / stride, stride}, ColSrc{});
     }
 }
 
@@ -390,14 +414,15 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
 // 16 live words per thread halved occupancy and ran 2x slower on B200 (measured).
 // log N = L1 + L2, L1 = floor(log N / 2): col pass <L1, L2>, row pass <L2, L1>.
 template <bool FWD, bool COL>
-void launch_pass(uint32_t log_n, uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm, cudaStream_t s)
+void launch_pass(uint32_t log_n, uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm, const ColSrc *cs,
+                 cudaStream_t s)
 {
 #define MMFHE_NTT_CASE(LN, A, B)                                    \
     case LN:                                                        \
         if (COL)                                                    \
-            launch_one<FWD, A, B, true>(d, rows, kt, pm, s);        \
+            launch_one<FWD, A, B, true>(d, rows, kt, pm, cs, s);        \
         else                                                        \
-            launch_one<FWD, B, A, false>(d, rows, kt, pm, s);       \
+            launch_one<FWD, B, A, false>(d, rows, kt, pm, nullptr, s);       \
         break;
     switch (log_n) {
         MMFHE_NTT_CASE(4, 2, 2)
@@ -427,19 +452,20 @@ void split(uint32_t log_n, int &L1, int &L2)
 
 }  // namespace
 
-void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm)
+void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const ColSrc *src)
 {
     if (!rows) return;
+    MMFHE_REQUIRE(!src || src->period == pm.period, MMFHE_E_LAYOUT, "NTT source map period");
     int L1, L2;
     split(c.log_n, L1, L2);
     const double bytes = 16.0 * rows * c.n;  // one read + one write of every word per pass
     {
         ProfScope ps(c, "ntt_fwd_col", bytes, 0.5 * rows * c.n * L1);
-        launch_pass<true, true>(c.log_n, d, rows, c.kt, pm, c.stream);
+        launch_pass<true, true>(c.log_n, d, rows, c.kt, pm, src, c.stream);
     }
     {
         ProfScope ps(c, "ntt_fwd_row", bytes, 0.5 * rows * c.n * L2);
-        launch_pass<true, false>(c.log_n, d, rows, c.kt, pm, c.stream);
+        launch_pass<true, false>(c.log_n, d, rows, c.kt, pm, nullptr, c.stream);
     }
     c.launches += 2;
     CUDA_CHECK(cudaGetLastError());
@@ -453,11 +479,11 @@ void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm)
     const double bytes = 16.0 * rows * c.n;
     {
         ProfScope ps(c, "ntt_inv_row", bytes, 0.5 * rows * c.n * L2);
-        launch_pass<false, false>(c.log_n, d, rows, c.kt, pm, c.stream);
+        launch_pass<false, false>(c.log_n, d, rows, c.kt, pm, nullptr, c.stream);
     }
     {
         ProfScope ps(c, "ntt_inv_col", bytes, 0.5 * rows * c.n * L1);
-        launch_pass<false, true>(c.log_n, d, rows, c.kt, pm, c.stream);
+        launch_pass<false, true>(c.log_n, d, rows, c.kt, pm, nullptr, c.stream);
     }
     c.launches += 2;
     CUDA_CHECK(cudaGetLastError());
