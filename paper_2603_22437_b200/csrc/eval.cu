@@ -425,8 +425,17 @@ void ks_ip_moddown(Ctx &c, const uint64_t *x_ntt, size_t xs, const uint64_t *y, 
     for (uint32_t k = 0; k < c.K; ++k) pm.push_back(c.L + 1 + k);
     ntt_inverse(c, accP.get(), B * 2 * c.K, make_map(pm));
     DBuf w(B * 2 * lw, c.stream);
-    launch_moddown_bconv(c, w.get(), accP.get(), l, B);
-    ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l));
+    if (c.K == 1 && l + 1 <= (uint32_t)kMapCap) {
+        // one special prime: BConv_{P->Q} is w_i = accP mod q_i, fused into the NTT's first read
+        ColSrc src{};
+        src.x = accP.get();
+        src.xs = N;  // one P row per (item, poly)
+        src.period = l + 1;
+        ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l), &src);
+    } else {
+        launch_moddown_bconv(c, w.get(), accP.get(), l, B);
+        ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l));
+    }
     launch_moddown_final(c, out, os, accQ.get(), w.get(), add, as, add_poly1, l, B);
 }
 }  // namespace

@@ -132,9 +132,17 @@ __device__ __forceinline__ int soff(int sb, int ke)
 __device__ __forceinline__ uint64_t csub64(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
 
 // Batch structure of the rows: row = item * rstride + ri, ri < rstride, n_items items.
+// z / n_items by multiply-high (Granlund-Montgomery; z < 2^31): q = (umulhi(z, mul) + z) >> shift.
 struct RowMap {
-    uint32_t n_items, rstride;
+    uint32_t n_items, rstride, mul, shift;
 };
+RowMap make_rowmap(uint32_t n_items, uint32_t rstride)
+{
+    uint32_t s = 0;
+    while ((1ull << s) < n_items) ++s;
+    const uint32_t mul = (uint32_t)(((1ull << 32) * ((1ull << s) - n_items)) / n_items + 1);
+    return RowMap{n_items, rstride, mul, s};
+}
 
 // Which row / block / group / lane this thread works on.
 //   col pass: CTA (x, y) = G consecutive columns of row y (coalesced strided columns).
@@ -154,7 +162,8 @@ __device__ __forceinline__ void locate(RowMap rm, size_t &row, int &gi, int &g, 
         g = tid >> Gm::LOGT;
         t = tid & (Gm::T - 1);
         const uint32_t z = blockIdx.x * Gm::G + g;
-        const uint32_t item = z % rm.n_items, rest = z / rm.n_items;
+        const uint32_t rest = (__umulhi(z, rm.mul) + z) >> rm.shift;
+        const uint32_t item = z - rest * rm.n_items;
         gi = rest & ((1u << OTHER) - 1);
         row = (size_t)item * rm.rstride + (rest >> OTHER);
     }
@@ -401,12 +410,14 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
                 src.x += (size_t)(r0 / pm.period) * cs->xs;
             }
             go(dim3((1u << OTHER) / Gm::G, std::min(chunk, rows - r0)), d + ((size_t)r0 << (LOGS + OTHER)),
-               RowMap{rows, 1}, src);
+               make_rowmap(rows, 1), src);
         }
     } else {
         // rows are items of pm.period residue rows each whenever that divides
         const uint32_t stride = rows % pm.period == 0 ? pm.period : 1;
-        go(dim3((uint32_t)(((size_t)rows << OTHER) / Gm::G)), d, RowMap{rows / stride, stride}, ColSrc{});
+        const size_t groups = (size_t)rows << OTHER;
+        MMFHE_REQUIRE(groups < (1ull << 31), MMFHE_E_SHAPE, "NTT batch too large for one launch");
+        go(dim3((uint32_t)(groups / Gm::G)), d, make_rowmap(rows / stride, stride), ColSrc{});
     }
 }
 
