@@ -79,33 +79,61 @@ __device__ __forceinline__ uint32_t ext_prime(uint32_t r, uint32_t level, uint32
 }
 
 // y_{j,t} = sum_{i in I_j} [x_i [Qhat_i^{-1}]_{q_i}]_{q_i} [Qhat_i]_t mod t
-// AMAX >= digit width (compile-time bound keeps v[] in registers).
+// AMAX >= digit width (compile-time bound keeps v[] in registers).  The conversion is a
+// small modular matrix product (n_tgt x alpha per coefficient) and MAC-bound at PS3/PS4:
+// the digit's constants are staged in shared memory once per CTA (broadcast reads) and
+// each thread converts kBcK coefficients, so every constant feeds kBcK MAC chains.
+constexpr int kBcK = 2;
+
 template <int AMAX>
 __global__ void __launch_bounds__(kTB) k_modup(uint64_t *__restrict__ y_base, const uint64_t *__restrict__ x_base,
                                                KTables kt, ModUpArgs args)
 {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= kt.n) return;
+    extern __shared__ uint64_t sh[];  // hat [na][n_tgt], then target q and -q^{-1}
     const ModUpDigit &dg = args.d[blockIdx.y];
+    const uint32_t na = dg.hi - dg.lo, nt = dg.n_tgt;
+    uint64_t *s_hat = sh, *s_q = sh + na * nt, *s_qi = s_q + nt;
+    for (uint32_t i = threadIdx.x; i < na * nt; i += blockDim.x) s_hat[i] = dg.hat[i];
+    for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+        const uint32_t pt = ext_prime(dg.tgt[i], args.level, args.L);
+        s_q[i] = kt.q[pt];
+        s_qi[i] = kt.qinv_neg[pt];
+    }
+    __syncthreads();
     const uint64_t *x = x_base + (size_t)blockIdx.z * args.xs;
     uint64_t *y = y_base + (size_t)blockIdx.z * args.ys + dg.y_off;
-    const uint32_t na = dg.hi - dg.lo;
-    uint64_t v[AMAX];
+    const uint32_t k0 = blockIdx.x * (kBcK * kTB) + threadIdx.x;
+    uint64_t v[kBcK][AMAX];
 #pragma unroll
     for (int i = 0; i < AMAX; ++i) {
         if (i < (int)na) {
             const uint32_t pi = dg.lo + i;
             const TwPair h = dg.hat_inv[i];
-            v[i] = shoup(x[(size_t)pi * kt.n + k], h.w, h.wp, kt.q[pi]);
+            const uint64_t qp = kt.q[pi];
+#pragma unroll
+            for (int c = 0; c < kBcK; ++c) {
+                const uint32_t k = k0 + c * kTB;
+                v[c][i] = k < kt.n ? shoup(x[(size_t)pi * kt.n + k], h.w, h.wp, qp) : 0;
+            }
         }
     }
-    for (uint32_t ti = 0; ti < dg.n_tgt; ++ti) {
-        const uint32_t pt = ext_prime(dg.tgt[ti], args.level, args.L);
-        U128 acc{0, 0};
+    for (uint32_t ti = 0; ti < nt; ++ti) {
+        U128 acc[kBcK];
+#pragma unroll
+        for (int c = 0; c < kBcK; ++c) acc[c] = U128{0, 0};
 #pragma unroll
         for (int i = 0; i < AMAX; ++i)
-            if (i < (int)na) mac128(acc, v[i], dg.hat[(size_t)i * dg.n_tgt + ti]);
-        y[(size_t)ti * kt.n + k] = redc(acc, kt.q[pt], kt.qinv_neg[pt]);
+            if (i < (int)na) {
+                const uint64_t hc = s_hat[i * nt + ti];
+#pragma unroll
+                for (int c = 0; c < kBcK; ++c) mac128(acc[c], v[c][i], hc);
+            }
+        const uint64_t q = s_q[ti], qi = s_qi[ti];
+#pragma unroll
+        for (int c = 0; c < kBcK; ++c) {
+            const uint32_t k = k0 + c * kTB;
+            if (k < kt.n) y[(size_t)ti * kt.n + k] = redc(acc[c], q, qi);
+        }
     }
 }
 
@@ -239,29 +267,55 @@ struct MDArgs {
     uint32_t level, L, K;
 };
 
-// w_i = sum_k [z_k [Phat_k^{-1}]_{p_k}]_{p_k} [Phat_k]_{q_i} mod q_i; grid.y = item*2 + poly
+// w_i = sum_k [z_k [Phat_k^{-1}]_{p_k}]_{p_k} [Phat_k]_{q_i} mod q_i; grid.y = item*2 + poly.
+// Same structure as k_modup: constants in shared memory, kBcK coefficients per thread.
 template <int KMAX>
 __global__ void __launch_bounds__(kTB) k_moddown_bconv(uint64_t *__restrict__ w, const uint64_t *__restrict__ zP,
                                                        KTables kt, MDArgs a)
 {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= kt.n) return;
+    extern __shared__ uint64_t sh[];  // phat [K][level+1], then q_i and -q_i^{-1}
+    const uint32_t L1 = a.level + 1;
+    uint64_t *s_hat = sh, *s_q = sh + a.K * L1, *s_qi = s_q + L1;
+    for (uint32_t t = threadIdx.x; t < a.K * L1; t += blockDim.x)
+        s_hat[t] = a.phat[(size_t)(t / L1) * (a.L + 1) + t % L1];
+    for (uint32_t i = threadIdx.x; i < L1; i += blockDim.x) {
+        s_q[i] = kt.q[i];
+        s_qi[i] = kt.qinv_neg[i];
+    }
+    __syncthreads();
     const uint32_t ip = blockIdx.y;  // item * 2 + poly
-    uint64_t v[KMAX];
+    const uint32_t k0 = blockIdx.x * (kBcK * kTB) + threadIdx.x;
+    uint64_t v[kBcK][KMAX];
 #pragma unroll
     for (int kk = 0; kk < KMAX; ++kk) {
         if (kk < (int)a.K) {
             const uint32_t pi = a.L + 1 + kk;
             const TwPair h = a.phat_inv[kk];
-            v[kk] = shoup(zP[((size_t)ip * a.K + kk) * kt.n + k], h.w, h.wp, kt.q[pi]);
+            const uint64_t qp = kt.q[pi];
+#pragma unroll
+            for (int c = 0; c < kBcK; ++c) {
+                const uint32_t k = k0 + c * kTB;
+                v[c][kk] = k < kt.n ? shoup(zP[((size_t)ip * a.K + kk) * kt.n + k], h.w, h.wp, qp) : 0;
+            }
         }
     }
-    for (uint32_t i = 0; i <= a.level; ++i) {
-        U128 acc{0, 0};
+    for (uint32_t i = 0; i < L1; ++i) {
+        U128 acc[kBcK];
+#pragma unroll
+        for (int c = 0; c < kBcK; ++c) acc[c] = U128{0, 0};
 #pragma unroll
         for (int kk = 0; kk < KMAX; ++kk)
-            if (kk < (int)a.K) mac128(acc, v[kk], a.phat[(size_t)kk * (a.L + 1) + i]);
-        w[((size_t)ip * (a.level + 1) + i) * kt.n + k] = redc(acc, kt.q[i], kt.qinv_neg[i]);
+            if (kk < (int)a.K) {
+                const uint64_t hc = s_hat[kk * L1 + i];
+#pragma unroll
+                for (int c = 0; c < kBcK; ++c) mac128(acc[c], v[c][kk], hc);
+            }
+        const uint64_t q = s_q[i], qi = s_qi[i];
+#pragma unroll
+        for (int c = 0; c < kBcK; ++c) {
+            const uint32_t k = k0 + c * kTB;
+            if (k < kt.n) w[((size_t)ip * L1 + i) * kt.n + k] = redc(acc[c], q, qi);
+        }
     }
 }
 
@@ -682,15 +736,17 @@ void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, 
         a.d[j].hi = p.hi;
         a.d[j].n_tgt = p.n_tgt;
     }
-    const dim3 g = grid3(c.n, (uint32_t)plans.size(), B);
+    size_t smem = 0;
+    for (const auto &p : plans) smem = std::max(smem, 8 * ((size_t)(p.hi - p.lo) * p.n_tgt + 2 * p.n_tgt));
+    const dim3 g((c.n + kBcK * kTB - 1) / (kBcK * kTB), (uint32_t)plans.size(), B);
     if (c.alpha <= 1)
-        k_modup<1><<<g, kTB, 0, c.stream>>>(y, x_coef, c.kt, a);
+        k_modup<1><<<g, kTB, smem, c.stream>>>(y, x_coef, c.kt, a);
     else if (c.alpha <= 4)
-        k_modup<4><<<g, kTB, 0, c.stream>>>(y, x_coef, c.kt, a);
+        k_modup<4><<<g, kTB, smem, c.stream>>>(y, x_coef, c.kt, a);
     else if (c.alpha <= 8)
-        k_modup<8><<<g, kTB, 0, c.stream>>>(y, x_coef, c.kt, a);
+        k_modup<8><<<g, kTB, smem, c.stream>>>(y, x_coef, c.kt, a);
     else
-        k_modup<16><<<g, kTB, 0, c.stream>>>(y, x_coef, c.kt, a);
+        k_modup<16><<<g, kTB, smem, c.stream>>>(y, x_coef, c.kt, a);
     LAUNCH_CHECK(c);
 }
 
@@ -745,15 +801,16 @@ void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t leve
 {
     MMFHE_REQUIRE(c.K <= 16, MMFHE_E_PARAMS, "K too large");
     ProfScope ps(c, "moddown_bconv", 16.0 * (c.K + level + 1) * c.n * B);
-    const dim3 g = grid3(c.n, 2 * B);
+    const size_t smem = 8 * ((size_t)c.K * (level + 1) + 2 * (level + 1));
+    const dim3 g((c.n + kBcK * kTB - 1) / (kBcK * kTB), 2 * B);
     if (c.K <= 1)
-        k_moddown_bconv<1><<<g, kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
+        k_moddown_bconv<1><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, md_args(c, level));
     else if (c.K <= 4)
-        k_moddown_bconv<4><<<g, kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
+        k_moddown_bconv<4><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, md_args(c, level));
     else if (c.K <= 8)
-        k_moddown_bconv<8><<<g, kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
+        k_moddown_bconv<8><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, md_args(c, level));
     else
-        k_moddown_bconv<16><<<g, kTB, 0, c.stream>>>(w, zP, c.kt, md_args(c, level));
+        k_moddown_bconv<16><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, md_args(c, level));
     LAUNCH_CHECK(c);
 }
 
