@@ -86,6 +86,37 @@ DCt import_batch(Ctx &c, const mmfhe_ct *cts, size_t first, size_t step, size_t 
     bool all_dev = true;
     for (size_t i = 0; i < count; ++i)
         all_dev = all_dev && cts[first + i * step].on_device && ((uintptr_t)cts[first + i * step].data % 16 == 0);
+    if (all_dev && c0.form == MMFHE_FORM_EVAL) {
+        // device NTT-form items already back to back: use them in place (like input_ct)
+        bool contig = true;
+        for (size_t i = 1; i < count && contig; ++i)
+            contig = cts[first + i * step].data == (const uint64_t *)c0.data + i * words;
+        if (contig) {
+            DCt v = view_ct(c, c0, 2);
+            v.batch = (uint32_t)count;
+            return v;
+        }
+    }
+    if (all_dev && c0.form == MMFHE_FORM_COEFF && 2 * (c0.level + 1) <= (uint32_t)kMapCap) {
+        // uniformly strided device items: the NTT's col pass reads them in place (the
+        // fused-source Barrett step is the identity on residues < q), no gather copy
+        const ptrdiff_t S = count > 1 ? cts[first + step].data - c0.data : (ptrdiff_t)words;
+        bool uniform = S >= (ptrdiff_t)words;
+        for (size_t i = 2; i < count && uniform; ++i) uniform = cts[first + i * step].data == c0.data + i * S;
+        if (uniform) {
+            ColSrc src{};
+            src.x = c0.data;
+            src.xs = (size_t)S;
+            src.period = 2 * (c0.level + 1);
+            std::vector<uint32_t> pm;
+            for (uint32_t t = 0; t < src.period; ++t) {
+                src.src[t] = (uint8_t)t;
+                pm.push_back(t % (c0.level + 1));
+            }
+            ntt_forward(c, r.data(), r.rows(), make_map(pm), &src);
+            return r;
+        }
+    }
     if (all_dev) {  // one gather launch per 64 device items
         for (size_t s = 0; s < count; s += kMaxTerms) {
             PtrList P{};
