@@ -247,18 +247,23 @@ def run_gpu(args, rank, world, device):
         d2h = sum(x.data.numel() * 8 for c in hout for x in hout[c])
         hin = {c: m.CtArray(hin[c]) for c in hin}
         hout = {c: m.CtArray(hout[c]) for c in hout}
-        for chain in hin:  # warm host path
-            ctx.eval_chain(chain, mcfg, hin[chain], hout[chain])
-        torch.cuda.synchronize(device)
-        e_steps = max(1, min(3, args.steps))
+        # mmfhe_eval_chain_async: the upload of step i+1 (library copy stream, two device
+        # staging slots) overlaps the compute of step i; every step's H2D and D2H is
+        # inside the timed region (host wall clock around the loop + final sync)
+        for _ in range(4):  # both staging slots through eager run + graph capture
+            for chain in hin:
+                ctx.eval_chain_async(chain, mcfg, hin[chain], hout[chain])
+        ctx.sync()
+        e_steps = max(3, args.steps)
         t0 = time.perf_counter()
         for _ in range(e_steps):
             for chain in hin:
-                ctx.eval_chain(chain, mcfg, hin[chain], hout[chain])
-        torch.cuda.synchronize(device)
+                ctx.eval_chain_async(chain, mcfg, hin[chain], hout[chain])
+        ctx.sync()
         e_s = (time.perf_counter() - t0) / e_steps
         e2e = {"value": cfg["F"] * world / e_s, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_s * 1e3, "clock": "host wall, per rank"}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_s * 1e3, "clock": "host wall, per rank",
+               "api": "mmfhe_eval_chain_async (pinned host buffers, copy/compute overlap across steps)"}
 
     extras = {}
     if not args.no_extras:

@@ -189,6 +189,22 @@ mmfhe_status mmfhe_chain_plan(mmfhe_ctx *ctx, const char *chain, const mmfhe_cha
 mmfhe_status mmfhe_eval_chain(mmfhe_ctx *ctx, const char *chain, const mmfhe_chain_cfg *cfg, const mmfhe_ct *in,
                               size_t n_in, mmfhe_ct *out, size_t cap, size_t *n_out);
 
+/* Asynchronous variant for serving loops: same arguments and results as
+ * mmfhe_eval_chain, but host (ideally pinned) input/output buffers are handled
+ * without blocking.  The inputs are uploaded on the context's copy stream into
+ * one of two library-owned device staging slots (per chain and shape), the chain
+ * runs on the ctx stream (graph replay applies), and the outputs are copied back
+ * asynchronously; the call returns once everything is enqueued (output metadata
+ * is already filled in).  Successive calls alternate slots, so the upload of
+ * call i+1 overlaps the compute of call i.  The caller keeps every host buffer
+ * alive and unmodified, and reads outputs only after mmfhe_ctx_sync.  All inputs
+ * must share level, layout and form (MMFHE_E_LAYOUT otherwise).  Device-resident
+ * arguments behave exactly like mmfhe_eval_chain. */
+mmfhe_status mmfhe_eval_chain_async(mmfhe_ctx *ctx, const char *chain, const mmfhe_chain_cfg *cfg,
+                                    const mmfhe_ct *in, size_t n_in, mmfhe_ct *out, size_t cap, size_t *n_out);
+/* Wait for everything enqueued on the context (copy stream and ctx stream). */
+mmfhe_status mmfhe_ctx_sync(mmfhe_ctx *ctx);
+
 /* Sum of n partial ciphertexts mod q (cross-GPU frame accumulation after an
  * NCCL all-gather); all parts at one level and scale. */
 mmfhe_status mmfhe_sum_partials(mmfhe_ctx *ctx, const mmfhe_ct *parts, size_t n, mmfhe_ct *out);

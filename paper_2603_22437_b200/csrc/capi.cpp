@@ -135,6 +135,33 @@ bool capture_chain(Ctx &c, Ctx::ChainGraph &g, const char *chain, const mmfhe_ch
     return true;
 }
 
+// mmfhe_eval_chain's body: repeated device-resident calls (trace / profile off) replay a
+// captured CUDA graph, everything else runs eagerly.
+void eval_chain_impl(Ctx &c, const char *chain, const mmfhe_chain_cfg &cfg, const mmfhe_ct *in, size_t n_in,
+                     mmfhe_ct *out, size_t n)
+{
+    if (c.graphs_on && !c.trace_on && !c.prof_on && all_device(in, n_in) && all_device(out, n)) {
+        if (c.graphs.size() >= 64) c.drop_graphs();
+        Ctx::ChainGraph &g = c.graphs[chain_key(c, chain, cfg, in, n_in, out, n)];
+        if (!g.exec && g.seen >= 1) capture_chain(c, g, chain, cfg, in, n_in, out, n);
+        if (g.exec) {
+            CUDA_CHECK(cudaGraphLaunch(g.exec, c.stream));
+            c.launches += g.launches;
+            ++c.graph_replays;
+            for (size_t i = 0; i < n; ++i) {
+                out[i].log_n = g.out_meta[i].log_n;
+                out[i].level = g.out_meta[i].level;
+                out[i].scale = g.out_meta[i].scale;
+                out[i].n_slots = g.out_meta[i].n_slots;
+                out[i].n_polys = g.out_meta[i].n_polys;
+            }
+            return;
+        }
+        if (g.seen >= 0) ++g.seen;
+    }
+    run_and_export(c, chain, cfg, in, n_in, out, n);
+}
+
 mmfhe_chain_cfg cfg_or_default(const mmfhe_chain_cfg *cfg)
 {
     mmfhe_chain_cfg d{};
@@ -308,28 +335,95 @@ mmfhe_status mmfhe_eval_chain(mmfhe_ctx *ctx, const char *chain, const mmfhe_cha
     std::vector<uint32_t> lv = chain_plan(*ctx, chain, c, in[0].level, n_in);
     *n_out = lv.size();
     MMFHE_REQUIRE(lv.size() <= cap, MMFHE_E_LAYOUT, "output capacity too small");
+    eval_chain_impl(*ctx, chain, c, in, n_in, out, lv.size());
+    API_END(ctx)
+}
+
+mmfhe_status mmfhe_eval_chain_async(mmfhe_ctx *ctx, const char *chain, const mmfhe_chain_cfg *cfg,
+                                    const mmfhe_ct *in, size_t n_in, mmfhe_ct *out, size_t cap, size_t *n_out)
+{
+    API_BEGIN
+    MMFHE_REQUIRE(chain && in && n_in && out && n_out, MMFHE_E_INVALID_ARG, "null argument");
+    mmfhe_chain_cfg c = cfg_or_default(cfg);
+    std::vector<uint32_t> lv = chain_plan(*ctx, chain, c, in[0].level, n_in);
+    *n_out = lv.size();
+    MMFHE_REQUIRE(lv.size() <= cap, MMFHE_E_LAYOUT, "output capacity too small");
     const size_t n = lv.size();
-    // repeated device-resident calls replay a captured CUDA graph (trace / profile off)
-    if (ctx->graphs_on && !ctx->trace_on && !ctx->prof_on && all_device(in, n_in) && all_device(out, n)) {
-        if (ctx->graphs.size() >= 64) ctx->drop_graphs();
-        Ctx::ChainGraph &g = ctx->graphs[chain_key(*ctx, chain, c, in, n_in, out, n)];
-        if (!g.exec && g.seen >= 1) capture_chain(*ctx, g, chain, c, in, n_in, out, n);
-        if (g.exec) {
-            CUDA_CHECK(cudaGraphLaunch(g.exec, ctx->stream));
-            ctx->launches += g.launches;
-            ++ctx->graph_replays;
-            for (size_t i = 0; i < n; ++i) {
-                out[i].log_n = g.out_meta[i].log_n;
-                out[i].level = g.out_meta[i].level;
-                out[i].scale = g.out_meta[i].scale;
-                out[i].n_slots = g.out_meta[i].n_slots;
-                out[i].n_polys = g.out_meta[i].n_polys;
-            }
-            return MMFHE_OK;
-        }
-        if (g.seen >= 0) ++g.seen;
+    if (all_device(in, n_in) && all_device(out, n)) {  // already asynchronous
+        eval_chain_impl(*ctx, chain, c, in, n_in, out, n);
+        return MMFHE_OK;
     }
-    run_and_export(*ctx, chain, c, in, n_in, out, n);
+    Ctx &x = *ctx;
+    const mmfhe_ct &c0 = in[0];
+    const size_t iw = (size_t)npolys_of(c0) * (c0.level + 1) * x.n;
+    for (size_t i = 0; i < n_in; ++i)
+        MMFHE_REQUIRE(in[i].data && in[i].level == c0.level && npolys_of(in[i]) == npolys_of(c0) &&
+                          in[i].form == c0.form,
+                      MMFHE_E_LAYOUT, "async chain inputs must share level, layout and form");
+    std::vector<size_t> ooff(n + 1, 0);
+    for (size_t i = 0; i < n; ++i) {
+        MMFHE_REQUIRE(out[i].data, MMFHE_E_INVALID_ARG, "null output buffer");
+        ooff[i + 1] = ooff[i] + (size_t)2 * (lv[i] + 1) * x.n;
+    }
+    std::string key(chain);
+    key.push_back('\0');
+    put(key, n_in);
+    put(key, iw);
+    put(key, ooff[n]);
+    Ctx::Staging &st = x.staging[key];
+    if (!x.copy_stream) CUDA_CHECK(cudaStreamCreateWithFlags(&x.copy_stream, cudaStreamNonBlocking));
+    Ctx::StageSlot &sl = st.slot[st.next];
+    st.next ^= 1;
+    if (!sl.ready) {
+        sl.in = DBuf(n_in * iw, x.stream);
+        sl.out = DBuf(ooff[n], x.stream);
+        CUDA_CHECK(cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreateWithFlags(&sl.free, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventRecord(sl.free, x.stream));
+    }
+    // upload on the copy stream once the compute that last read this slot is done
+    CUDA_CHECK(cudaStreamWaitEvent(x.copy_stream, sl.free, 0));
+    bool contig = true;
+    for (size_t i = 1; i < n_in && contig; ++i) contig = in[i].data == c0.data + i * iw && !in[i].on_device;
+    if (contig && !c0.on_device) {
+        CUDA_CHECK(cudaMemcpyAsync(sl.in.get(), c0.data, n_in * iw * 8, cudaMemcpyHostToDevice, x.copy_stream));
+    } else {
+        for (size_t i = 0; i < n_in; ++i)
+            CUDA_CHECK(cudaMemcpyAsync(sl.in.get() + i * iw, in[i].data, iw * 8,
+                                       in[i].on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                       x.copy_stream));
+    }
+    CUDA_CHECK(cudaEventRecord(sl.ready, x.copy_stream));
+    CUDA_CHECK(cudaStreamWaitEvent(x.stream, sl.ready, 0));
+    std::vector<mmfhe_ct> din(in, in + n_in), dout(out, out + n);
+    for (size_t i = 0; i < n_in; ++i) {
+        din[i].data = sl.in.get() + i * iw;
+        din[i].on_device = 1;
+    }
+    for (size_t i = 0; i < n; ++i) {
+        dout[i].data = sl.out.get() + ooff[i];
+        dout[i].on_device = 1;
+    }
+    eval_chain_impl(x, chain, c, din.data(), n_in, dout.data(), n);
+    CUDA_CHECK(cudaEventRecord(sl.free, x.stream));
+    for (size_t i = 0; i < n; ++i) {
+        out[i].log_n = dout[i].log_n;
+        out[i].level = dout[i].level;
+        out[i].scale = dout[i].scale;
+        out[i].n_slots = dout[i].n_slots;
+        out[i].n_polys = dout[i].n_polys;
+        CUDA_CHECK(cudaMemcpyAsync(out[i].data, dout[i].data, (ooff[i + 1] - ooff[i]) * 8,
+                                   out[i].on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, x.stream));
+    }
+    API_END(ctx)
+}
+
+mmfhe_status mmfhe_ctx_sync(mmfhe_ctx *ctx)
+{
+    if (!ctx) return fail(ctx, MMFHE_E_INVALID_ARG, "null argument");
+    API_BEGIN
+    if (ctx->copy_stream) CUDA_CHECK(cudaStreamSynchronize(ctx->copy_stream));
+    CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     API_END(ctx)
 }
 

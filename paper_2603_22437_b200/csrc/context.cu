@@ -176,6 +176,14 @@ Ctx::~Ctx()
 {
     cudaStreamSynchronize(stream);
     drop_graphs();
+    if (copy_stream) cudaStreamSynchronize(copy_stream);
+    for (auto &kv : staging)
+        for (auto &sl : kv.second.slot) {
+            if (sl.ready) cudaEventDestroy(sl.ready);
+            if (sl.free) cudaEventDestroy(sl.free);
+        }
+    staging.clear();
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
 }

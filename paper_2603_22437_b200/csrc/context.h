@@ -147,6 +147,19 @@ class Ctx {
     cudaStream_t cap_stream = nullptr;
     void drop_graphs();
 
+    // mmfhe_eval_chain_async: two device staging slots per (chain, shape) so that the
+    // upload of call i+1 (copy_stream) overlaps the compute of call i (stream)
+    struct StageSlot {
+        DBuf in, out;
+        cudaEvent_t ready = nullptr, free = nullptr;
+    };
+    struct Staging {
+        StageSlot slot[2];
+        int next = 0;
+    };
+    std::unordered_map<std::string, Staging> staging;
+    cudaStream_t copy_stream = nullptr;
+
     // trace (Theorem P:999-1006)
     bool trace_on = true;
     std::vector<std::string> trace;

@@ -100,6 +100,8 @@ def lib():
             "mmfhe_load_scalars": [V, ctypes.c_char_p, P(ctypes.c_double), S],
             "mmfhe_chain_plan": [V, ctypes.c_char_p, P(ChainCfg), U32, S, P(U32), S, P(S)],
             "mmfhe_eval_chain": [V, ctypes.c_char_p, P(ChainCfg), CTP, S, CTP, S, P(S)],
+            "mmfhe_eval_chain_async": [V, ctypes.c_char_p, P(ChainCfg), CTP, S, CTP, S, P(S)],
+            "mmfhe_ctx_sync": [V],
             "mmfhe_sum_partials": [V, CTP, S, CTP],
             "mmfhe_ntt": [V, V, U32, P(U32)],
             "mmfhe_intt": [V, V, U32, P(U32)],
@@ -142,7 +144,8 @@ EXPORTED = [
     "mmfhe_sum_partials", "mmfhe_ntt", "mmfhe_intt", "mmfhe_hadd", "mmfhe_hsub", "mmfhe_pmult", "mmfhe_hmult",
     "mmfhe_relin", "mmfhe_hrot", "mmfhe_hrot_hoisted", "mmfhe_rescale", "mmfhe_keyswitch", "mmfhe_mod_switch", "mmfhe_hrot_batch",
     "mmfhe_hmult_batch", "mmfhe_trace_get", "mmfhe_trace_clear", "mmfhe_trace_enable", "mmfhe_profile_enable",
-    "mmfhe_profile_get", "mmfhe_microbench", "mmfhe_graph_enable", "mmfhe_graph_stats",
+    "mmfhe_profile_get", "mmfhe_microbench", "mmfhe_graph_enable", "mmfhe_graph_stats", "mmfhe_eval_chain_async",
+    "mmfhe_ctx_sync",
 ]
 
 
@@ -296,6 +299,21 @@ class Context:
                                                arr_out.arr, len(arr_out), ctypes.byref(n)))
         arr_out.sync_back()
         return n.value
+
+    def eval_chain_async(self, chain, cfg, ins, outs):
+        """Non-blocking eval_chain for host (pinned) buffers: upload of call i+1 overlaps
+        the compute of call i.  Keep the buffers alive; read outputs after sync()."""
+        arr_in = ins if isinstance(ins, CtArray) else CtArray(ins)
+        arr_out = outs if isinstance(outs, CtArray) else CtArray(outs)
+        n = ctypes.c_size_t()
+        self._check(self._lib.mmfhe_eval_chain_async(self.h, chain.encode(), ctypes.byref(cfg), arr_in.arr,
+                                                     len(arr_in), arr_out.arr, len(arr_out), ctypes.byref(n)))
+        arr_out.sync_back()
+        return n.value
+
+    def sync(self):
+        """Wait for all work enqueued on this context (copy and compute streams)."""
+        self._check(self._lib.mmfhe_ctx_sync(self.h))
 
     # ---- primitives
     def ntt(self, rows, prime_idx, inverse=False):
