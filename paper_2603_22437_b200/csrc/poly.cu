@@ -319,6 +319,52 @@ __global__ void __launch_bounds__(kTB) k_moddown_bconv(uint64_t *__restrict__ w,
     }
 }
 
+// One pair (the common case: squarings, K7 products): d0 = a0 b0, d1 = a0 b1 + a1 b0,
+// d2 = a1 b1.  The two a-inputs are taken to Montgomery form once (a R = mont(a, R^2))
+// so each output is a single REDC of a product sum (two corrections instead of three
+// output fix-ups), and each thread handles two coefficients to keep more loads in flight.
+__global__ void __launch_bounds__(kTB) k_tensor1(uint64_t *__restrict__ out_base, size_t os,
+                                                 const uint64_t *__restrict__ A, const uint64_t *__restrict__ Bp,
+                                                 size_t is, KTables kt, uint32_t level, int accumulate)
+{
+    const uint32_t r = blockIdx.y;
+    const size_t boff = (size_t)blockIdx.z * is;
+    uint64_t *out = out_base + (size_t)blockIdx.z * os;
+    const uint64_t q = kt.q[r], qi = kt.qinv_neg[r], r2 = kt.r2[r];
+    const size_t ps = (size_t)(level + 1) * kt.n;
+    const uint32_t k0 = blockIdx.x * (2 * kTB) + threadIdx.x;
+    uint64_t a0[2], a1[2], b0[2], b1[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const uint32_t k = min(k0 + c * kTB, kt.n - 1);
+        const size_t off = boff + (size_t)r * kt.n + k;
+        a0[c] = A[off];
+        a1[c] = A[ps + off];
+        b0[c] = Bp[off];
+        b1[c] = Bp[ps + off];
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const uint32_t k = k0 + c * kTB;
+        if (k >= kt.n) break;
+        const uint64_t x0 = mont_mul(a0[c], r2, q, qi), x1 = mont_mul(a1[c], r2, q, qi);
+        U128 m1 = mul128(x0, b1[c]);
+        const U128 m2 = mul128(x1, b0[c]);
+        m1.lo += m2.lo;
+        m1.hi += m2.hi + (m1.lo < m2.lo);
+        uint64_t d0 = redc(mul128(x0, b0[c]), q, qi), d1 = redc(m1, q, qi), d2 = redc(mul128(x1, b1[c]), q, qi);
+        const size_t off = (size_t)r * kt.n + k;
+        if (accumulate) {
+            d0 = add_mod(d0, out[off], q);
+            d1 = add_mod(d1, out[ps + off], q);
+            d2 = add_mod(d2, out[2 * ps + off], q);
+        }
+        out[off] = d0;
+        out[ps + off] = d1;
+        out[2 * ps + off] = d2;
+    }
+}
+
 // grid.y = poly*(l+1) + i, grid.z = item
 __global__ void k_moddown_final(uint64_t *__restrict__ out, size_t os, const uint64_t *__restrict__ accQ,
                                 const uint64_t *__restrict__ w, const uint64_t *__restrict__ add, size_t as,
@@ -854,8 +900,12 @@ void launch_tensor_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &a, const
     double in_words = 0;
     for (int i = 0; i < n; ++i) in_words += (a.p[i] == b.p[i]) ? 2.0 : 4.0;
     ProfScope ps(c, "tensor_sum", 8.0 * (level + 1) * c.n * B * (in_words + 3.0 + (accumulate ? 3.0 : 0.0)));
-    k_tensor_sum<<<grid3(c.n, level + 1, B), kTB, 0, c.stream>>>(out, os, a, b, is, n, c.kt, level,
-                                                                 accumulate ? 1 : 0);
+    if (n == 1)
+        k_tensor1<<<dim3((c.n + 2 * kTB - 1) / (2 * kTB), level + 1, B), kTB, 0, c.stream>>>(
+            out, os, a.p[0], b.p[0], is, c.kt, level, accumulate ? 1 : 0);
+    else
+        k_tensor_sum<<<grid3(c.n, level + 1, B), kTB, 0, c.stream>>>(out, os, a, b, is, n, c.kt, level,
+                                                                     accumulate ? 1 : 0);
     LAUNCH_CHECK(c);
 }
 
