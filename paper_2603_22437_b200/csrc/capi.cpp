@@ -573,7 +573,7 @@ mmfhe_status mmfhe_keyswitch(mmfhe_ctx *ctx, const mmfhe_ct *x, int32_t step, in
     }
     ctx->rec("keyswitch", in.level);
     DCt r = make_ct(*ctx, in.level, 2, in.n_slots, in.scale);
-    ev_keyswitch(*ctx, in.data(), in.item_words(), in.level, 1, *key, r.data(), r.item_words(), nullptr, 0, false);
+    ev_keyswitch(*ctx, in.data(), in.item_words(), in.level, 1, *key, r.data(), r.item_words(), nullptr, nullptr, 0);
     export_ct(*ctx, r, *out);
     API_END(ctx)
 }

@@ -445,8 +445,8 @@ ModUpOut ks_modup(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t
 
 // Key inner product (each evk word fetched once per batch split) + ModDown.
 void ks_ip_moddown(Ctx &c, const uint64_t *x_ntt, size_t xs, const uint64_t *y, const ModUpOut &m, uint32_t l,
-                   uint32_t B, const DKey &key, uint64_t *out, size_t os, const uint64_t *add, size_t as,
-                   bool add_poly1)
+                   uint32_t B, const DKey &key, uint64_t *out, size_t os, const uint64_t *add0,
+                   const uint64_t *add1, size_t as)
 {
     const size_t N = c.n;
     const size_t lw = (size_t)(l + 1) * N;
@@ -467,15 +467,15 @@ void ks_ip_moddown(Ctx &c, const uint64_t *x_ntt, size_t xs, const uint64_t *y, 
         launch_moddown_bconv(c, w.get(), accP.get(), l, B);
         ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l));
     }
-    launch_moddown_final(c, out, os, accQ.get(), w.get(), add, as, add_poly1, l, B);
+    launch_moddown_final(c, out, os, accQ.get(), w.get(), add0, add1, as, l, B);
 }
 }  // namespace
 
 void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t B, const DKey &key,
-                  uint64_t *out, size_t os, const uint64_t *add, size_t as, bool add_poly1)
+                  uint64_t *out, size_t os, const uint64_t *add0, const uint64_t *add1, size_t as)
 {
     ModUpOut m = ks_modup(c, x_ntt, xs, l, B);
-    ks_ip_moddown(c, x_ntt, xs, m.y.get(), m, l, B, key, out, os, add, as, add_poly1);
+    ks_ip_moddown(c, x_ntt, xs, m.y.get(), m, l, B, key, out, os, add0, add1, as);
 }
 
 std::vector<DCt> ev_rotate_hoisted(Ctx &c, const DCt &a, const std::vector<int32_t> &steps)
@@ -509,7 +509,7 @@ std::vector<DCt> ev_rotate_hoisted(Ctx &c, const DCt &a, const std::vector<int32
         launch_automorph(c, sy.get(), m.y.get(), (uint32_t)(B * m.T), g);
         DCt r = make_ct(c, l, 2, a.n_slots, a.scale, B);
         ks_ip_moddown(c, sig.get() + a.poly_words(), a.item_words(), sy.get(), m, l, B, key, r.data(),
-                      r.item_words(), sig.get(), a.item_words(), false);
+                      r.item_words(), sig.get(), nullptr, a.item_words());
         out.push_back(std::move(r));
     }
     return out;
@@ -522,7 +522,7 @@ DCt ev_relin(Ctx &c, const DCt &a3)
     rec_n(c, "relin", a3.level, a3.batch);
     DCt r = make_ct(c, a3.level, 2, a3.n_slots, a3.scale, a3.batch);
     ev_keyswitch(c, a3.poly(2), a3.item_words(), a3.level, a3.batch, *c.rlk, r.data(), r.item_words(), a3.data(),
-                 a3.item_words(), true);
+                 a3.poly(1), a3.item_words());
     return r;
 }
 
@@ -553,7 +553,7 @@ DCt ev_rotate(Ctx &c, const DCt &a, int32_t step)
     DBuf sig(a.item_words() * a.batch, c.stream);
     launch_automorph(c, sig.get(), a.data(), a.rows(), g);
     ev_keyswitch(c, sig.get() + a.poly_words(), a.item_words(), a.level, a.batch, key, r.data(), r.item_words(),
-                 sig.get(), a.item_words(), false);
+                 sig.get(), nullptr, a.item_words());
     return r;
 }
 
@@ -576,14 +576,31 @@ DCt ev_rescale(Ctx &c, const DCt &a)
     return r;
 }
 
+// acc + HRot(acc, step) with the HAdd fused: the automorph writes sigma(c0) + c0 for poly 0
+// and ModDown adds c1 to poly 1 (records "hrot" then "hadd", as the two ops it replaces).
+DCt ev_rot_add(Ctx &c, const DCt &a, int32_t step)
+{
+    MMFHE_REQUIRE(a.npolys == 2, MMFHE_E_LAYOUT, "rotate needs a 2-poly ciphertext");
+    int32_t k;
+    const uint64_t g = galois_element(c, step, &k);
+    if (k == 0) return ev_addsub(c, a, a, false);
+    const DKey &key = find_gk(c, k);
+    rec_n(c, "hrot", a.level, a.batch, std::to_string(k));
+    rec_n(c, "hadd", a.level, a.batch);
+    DCt r = make_ct(c, a.level, 2, a.n_slots, a.scale, a.batch);
+    DBuf sig(a.item_words() * a.batch, c.stream);
+    launch_automorph_acc(c, sig.get(), a.data(), a.rows(), g, a.level);
+    ev_keyswitch(c, sig.get() + a.poly_words(), a.item_words(), a.level, a.batch, key, r.data(), r.item_words(),
+                 sig.get(), a.poly(1), a.item_words());
+    return r;
+}
+
 DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride)
 {
-    DCt acc = copy_ct(c, a);
-    uint32_t step = stride;
-    for (uint32_t n = 1; n < count; n *= 2, step *= 2) {
-        DCt r = ev_rotate(c, acc, (int32_t)step);
-        acc = ev_addsub(c, acc, r, false);
-    }
+    if (count <= 1) return copy_ct(c, a);
+    DCt acc = ev_rot_add(c, a, (int32_t)stride);
+    uint32_t step = 2 * stride;
+    for (uint32_t n = 2; n < count; n *= 2, step *= 2) acc = ev_rot_add(c, acc, (int32_t)step);
     return acc;
 }
 

@@ -45,7 +45,7 @@ DCt ev_lincomb_mat(Ctx &c, const DCt &in, uint32_t J, uint32_t W, int lo0, int l
 
 // key switching family (batched)
 void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t level, uint32_t B, const DKey &key,
-                  uint64_t *out, size_t os, const uint64_t *add, size_t as, bool add_poly1);
+                  uint64_t *out, size_t os, const uint64_t *add0, const uint64_t *add1, size_t as);
 DCt ev_relin(Ctx &c, const DCt &a3);
 DCt ev_rotate(Ctx &c, const DCt &a, int32_t step);
 // Hoisted HRot: one ModUp of c1 shared by every step; per step the
@@ -53,6 +53,8 @@ DCt ev_rotate(Ctx &c, const DCt &a, int32_t step);
 // ev_rotate (different residues, same decryption).
 std::vector<DCt> ev_rotate_hoisted(Ctx &c, const DCt &a, const std::vector<int32_t> &steps);
 DCt ev_rescale(Ctx &c, const DCt &a);
+// a + HRot(a, step) in one key switch (the rotsum step)
+DCt ev_rot_add(Ctx &c, const DCt &a, int32_t step);
 DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride);
 
 // composites

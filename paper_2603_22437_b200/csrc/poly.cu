@@ -59,6 +59,24 @@ __global__ void k_automorph(uint64_t *__restrict__ out, const uint64_t *__restri
     out[(size_t)r * n + j] = in[(size_t)r * n + src];
 }
 
+// Rotate-and-accumulate input of a rotsum step: poly 0 rows get sigma_g(a) + a (the
+// step's HAdd folded in), poly 1 rows sigma_g(a) (the key-switch input).
+__global__ void k_automorph_acc(uint64_t *__restrict__ out, const uint64_t *__restrict__ in, uint32_t log_n,
+                                uint64_t g, KTables kt, uint32_t level)
+{
+    const uint32_t n = 1u << log_n;
+    const uint32_t r = blockIdx.y;
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const uint64_t two_n = 2ull * n;
+    const uint64_t e = ((2ull * bitrev(j, log_n) + 1) * g) & (two_n - 1);
+    const uint32_t src = bitrev((uint32_t)((e - 1) >> 1), log_n);
+    const uint32_t rr = r % (2 * (level + 1));
+    uint64_t v = in[(size_t)r * n + src];
+    if (rr <= level) v = add_mod(v, in[(size_t)r * n + j], kt.q[rr]);
+    out[(size_t)r * n + j] = v;
+}
+
 // ------------------------------------------------------------------ base conversion
 struct ModUpDigit {
     const TwPair *hat_inv;
@@ -367,8 +385,8 @@ __global__ void __launch_bounds__(kTB) k_tensor1(uint64_t *__restrict__ out_base
 
 // grid.y = poly*(l+1) + i, grid.z = item
 __global__ void k_moddown_final(uint64_t *__restrict__ out, size_t os, const uint64_t *__restrict__ accQ,
-                                const uint64_t *__restrict__ w, const uint64_t *__restrict__ add, size_t as,
-                                int add_poly1, KTables kt, MDArgs a)
+                                const uint64_t *__restrict__ w, const uint64_t *__restrict__ add0,
+                                const uint64_t *__restrict__ add1, size_t as, KTables kt, MDArgs a)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
@@ -378,9 +396,9 @@ __global__ void k_moddown_final(uint64_t *__restrict__ out, size_t os, const uin
     const TwPair pv = a.pinv[i];
     const size_t idx = ((size_t)b * 2 * (a.level + 1) + r) * kt.n + k;
     uint64_t d = shoup(accQ[idx] + q - w[idx], pv.w, pv.wp, q);
-    const size_t li = (size_t)r * kt.n + k;
-    if (add && (poly == 0 || add_poly1)) d = add_mod(d, add[(size_t)b * as + li], q);
-    out[(size_t)b * os + li] = d;
+    const uint64_t *add = poly == 0 ? add0 : add1;  // per-poly fused additions (may be null)
+    if (add) d = add_mod(d, add[(size_t)b * as + (size_t)i * kt.n + k], q);
+    out[(size_t)b * os + (size_t)r * kt.n + k] = d;
 }
 
 // ------------------------------------------------------------------ rescale
@@ -752,6 +770,13 @@ void launch_to_mont(Ctx &c, uint64_t *x, uint32_t rows, const PrimeMap &pm)
     LAUNCH_CHECK(c);
 }
 
+void launch_automorph_acc(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t rows, uint64_t g, uint32_t level)
+{
+    ProfScope ps(c, "automorph", 8.0 * rows * c.n * 2.5);  // read all rows, re-read poly 0, write all
+    k_automorph_acc<<<grid3(c.n, rows), kTB, 0, c.stream>>>(out, in, c.log_n, g, c.kt, level);
+    LAUNCH_CHECK(c);
+}
+
 void launch_automorph(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t rows, uint64_t g)
 {
     ProfScope ps(c, "automorph", 16.0 * rows * c.n);
@@ -861,11 +886,12 @@ void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t leve
 }
 
 void launch_moddown_final(Ctx &c, uint64_t *out, size_t os, const uint64_t *accQ, const uint64_t *w,
-                          const uint64_t *add, size_t as, bool add_poly1, uint32_t level, uint32_t B)
+                          const uint64_t *add0, const uint64_t *add1, size_t as, uint32_t level, uint32_t B)
 {
-    ProfScope ps(c, "moddown_final", 8.0 * 2 * (level + 1) * c.n * B * (add ? (add_poly1 ? 4.0 : 3.5) : 3.0));
-    k_moddown_final<<<grid3(c.n, 2 * (level + 1), B), kTB, 0, c.stream>>>(out, os, accQ, w, add, as,
-                                                                          add_poly1 ? 1 : 0, c.kt, md_args(c, level));
+    ProfScope ps(c, "moddown_final",
+                 8.0 * (level + 1) * c.n * B * (6.0 + (add0 ? 1.0 : 0.0) + (add1 ? 1.0 : 0.0)));
+    k_moddown_final<<<grid3(c.n, 2 * (level + 1), B), kTB, 0, c.stream>>>(out, os, accQ, w, add0, add1, as, c.kt,
+                                                                          md_args(c, level));
     LAUNCH_CHECK(c);
 }
 
