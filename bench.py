@@ -588,6 +588,15 @@ def roofline(prof, peaks, int_peaks):
     else:
         out.update({"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
                     "peak_source": hbm_src})
+    # DRAM traffic from the committed ncu --set full capture of this kernel (dram read +
+    # write per launch / algorithmic bytes of that launch), applied to this run's launches
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        tr = json.load(open(tpath))
+        if tr.get("kernel") == name:
+            out["traffic"] = tr["ratio"] * by / max(cnt, 1)
+            out["traffic_source"] = (f"{tr['capture']}: {tr['dram_bytes']} B DRAM for {tr['alg_bytes']} B algorithmic "
+                                     f"({tr['launch']}); ratio {tr['ratio']} x this run's bytes per launch")
     return out
 
 
