@@ -169,6 +169,103 @@ __device__ __forceinline__ void locate(RowMap rm, size_t &row, int &gi, int &g, 
     }
 }
 
+// ---------------------------------------------------------------- round bodies
+// Forward round r: bits [lo, lo+w) with the narrow round first.  Loads the round's
+// distinct twiddles (the twiddle of stage s depends only on the top s register bits:
+// 2^s per stage, issued before the first butterfly so their latency overlaps) and runs
+// its CT butterflies with the lazy 16q schedule (U >= 8q corrected at global stages
+// = 3 mod 4).
+template <class Gm, int LOGS>
+struct FwdGeo {
+    static constexpr int W0 = LOGS - (Gm::R - 1) * Gm::ELOG;
+    __device__ static constexpr int w(int r) { return r == 0 ? W0 : Gm::ELOG; }
+    __device__ static constexpr int hi(int r) { return LOGS - 1 - (r == 0 ? 0 : W0 + (r - 1) * Gm::ELOG); }
+    __device__ static constexpr int lo(int r) { return hi(r) - w(r) + 1; }
+};
+
+template <class Gm, int LOGS>
+__device__ __forceinline__ void fwd_bfly(uint64_t (&v)[Gm::E], int r, int ktr, int prefix, const TwPair *tw, uint64_t q)
+{
+    using F = FwdGeo<Gm, LOGS>;
+    constexpr int ELOG = Gm::ELOG, E = Gm::E;
+    const int w = F::w(r), lo = F::lo(r), lp0 = LOGS - 1 - F::hi(r);
+    const uint64_t q2 = 2 * q, q8 = 8 * q;
+    TwPair tws[E];
+#pragma unroll
+    for (int s = 0; s < w; ++s) {
+        const int lp = lp0 + s;
+        const TwPair *tb = tw + (1 << (Gm::LBASE + lp)) + (prefix << lp) + (ktr >> (LOGS - lp));
+#pragma unroll
+        for (int mm = 0; mm < (1 << s); ++mm)
+            tws[(1 << s) - 1 + mm] = tb[kmap(ELOG, lo, w, 0, mm << (ELOG - s)) >> (LOGS - lp)];
+    }
+#pragma unroll
+    for (int s = 0; s < w; ++s) {
+        const int bit = ELOG - 1 - s;  // register bit paired in this stage
+        const bool corr = ((Gm::LBASE + lp0 + s) & 3) == 3;
+#pragma unroll
+        for (int mm = 0; mm < (1 << s); ++mm) {
+            const int erep = mm << (ELOG - s);
+            const TwPair wt = tws[(1 << s) - 1 + mm];
+#pragma unroll
+            for (int e = erep; e < erep + (1 << (ELOG - s)); ++e) {
+                if (e & (1 << bit)) continue;
+                uint64_t U = v[e];
+                uint64_t V = v[e | (1 << bit)];
+                if (corr) U = csub64(U, q8);
+                V = shoup_lazy(V, wt.w, wt.wp, q);
+                v[e] = U + V;
+                v[e | (1 << bit)] = U - V + q2;
+            }
+        }
+    }
+}
+
+// Inverse round r: bits [lo, lo+w) from the bottom up (the narrow round last); stage s
+// needs 2^(w-1-s) distinct twiddles (register bits above it).  Harvey GS butterflies.
+template <class Gm, int LOGS>
+struct InvGeo {
+    __device__ static constexpr int lo(int r) { return r * Gm::ELOG; }
+    __device__ static constexpr int w(int r) { return (LOGS - lo(r)) < Gm::ELOG ? (LOGS - lo(r)) : Gm::ELOG; }
+};
+
+template <class Gm, int LOGS>
+__device__ __forceinline__ void inv_bfly(uint64_t (&v)[Gm::E], int r, int ktr, int prefix, const TwPair *tw, uint64_t q)
+{
+    using I = InvGeo<Gm, LOGS>;
+    constexpr int ELOG = Gm::ELOG, E = Gm::E;
+    const int lo = I::lo(r), w = I::w(r);
+    const uint64_t q2 = 2 * q;
+    TwPair tws[E];
+#pragma unroll
+    for (int s = 0; s < w; ++s) {
+        const int lp = LOGS - 1 - (lo + s);
+        const int ntop = w - 1 - s;
+        const TwPair *tb = tw + (1 << (Gm::LBASE + lp)) + (prefix << lp) + (ktr >> (LOGS - lp));
+#pragma unroll
+        for (int mm = 0; mm < (1 << ntop); ++mm)
+            tws[(1 << ntop) - 1 + mm] = tb[kmap(ELOG, lo, w, 0, mm << (ELOG - ntop)) >> (LOGS - lp)];
+    }
+#pragma unroll
+    for (int s = 0; s < w; ++s) {
+        const int bit = ELOG - w + s;  // register bit of k-bit lo+s
+        const int ntop = w - 1 - s;    // register bits above: the twiddle depends on these only
+#pragma unroll
+        for (int mm = 0; mm < (1 << ntop); ++mm) {
+            const int erep = mm << (ELOG - ntop);
+            const TwPair wt = tws[(1 << ntop) - 1 + mm];
+#pragma unroll
+            for (int e = erep; e < erep + (1 << (ELOG - ntop)); ++e) {
+                if (e & (1 << bit)) continue;
+                const uint64_t X = v[e];
+                const uint64_t Y = v[e | (1 << bit)];
+                v[e] = csub64(X + Y, q2);
+                v[e | (1 << bit)] = shoup_lazy(X - Y + q2, wt.w, wt.wp, q);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- forward
 // Round widths: the first (top) round takes LOGS - (R-1)*ELOG bits, the others ELOG.
 template <int LOGS, int OTHER, bool COL>
@@ -177,14 +274,13 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
 {
     using Gm = Geo<LOGS, OTHER, COL>;
     constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, T = Gm::T, G = Gm::G, R = Gm::R;
-    constexpr int W0 = LOGS - (R - 1) * ELOG;
     constexpr int LOGN = LOGS + OTHER;
     extern __shared__ uint64_t sm[];
     size_t row;
     int gi, g, t;
     locate<Gm, LOGS, OTHER, COL>(rm, row, gi, g, t);
     const int p = pm.idx[row % pm.period];
-    const uint64_t q = kt.q[p], q2 = 2 * q, q8 = 8 * q;
+    const uint64_t q = kt.q[p];
     const TwPair *tw = kt.tw_fwd + ((size_t)p << LOGN);
     uint64_t *a = data + ((size_t)row << LOGN);
     uint64_t *buf0 = sm, *buf1 = sm + S * G;
@@ -192,10 +288,7 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
     uint64_t v[E];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int w = r == 0 ? W0 : ELOG;
-        const int hi = LOGS - 1 - (r == 0 ? 0 : W0 + (r - 1) * ELOG);
-        const int lo = hi - w + 1;
-        const int lp0 = LOGS - 1 - hi;  // local stage of this round's first stage
+        const int w = FwdGeo<Gm, LOGS>::w(r), lo = FwdGeo<Gm, LOGS>::lo(r);
         const int ktr = kmap(ELOG, lo, w, t, 0);
         const int sb = sbase<Gm, LOGS, COL>(ktr, g);
         if (r == 0 && !COL) {
@@ -224,38 +317,7 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))];
         }
-        // The twiddle of stage s depends only on the top s register bits (spare register
-        // bits map below lo): 2^s distinct ones per stage.  Issue all of the round's
-        // twiddle loads before the first butterfly so their L2 latency overlaps.
-        TwPair tws[E];
-#pragma unroll
-        for (int s = 0; s < w; ++s) {
-            const int lp = lp0 + s;
-            const TwPair *tb = tw + (1 << (Gm::LBASE + lp)) + (COL ? 0 : (gi << lp)) + (ktr >> (LOGS - lp));
-#pragma unroll
-            for (int mm = 0; mm < (1 << s); ++mm)
-                tws[(1 << s) - 1 + mm] = tb[kmap(ELOG, lo, w, 0, mm << (ELOG - s)) >> (LOGS - lp)];
-        }
-#pragma unroll
-        for (int s = 0; s < w; ++s) {
-            const int bit = ELOG - 1 - s;  // register bit paired in this stage
-            const bool corr = ((Gm::LBASE + lp0 + s) & 3) == 3;
-#pragma unroll
-            for (int mm = 0; mm < (1 << s); ++mm) {
-                const int erep = mm << (ELOG - s);
-                const TwPair wt = tws[(1 << s) - 1 + mm];
-#pragma unroll
-                for (int e = erep; e < erep + (1 << (ELOG - s)); ++e) {
-                    if (e & (1 << bit)) continue;
-                    uint64_t U = v[e];
-                    uint64_t V = v[e | (1 << bit)];
-                    if (corr) U = csub64(U, q8);
-                    V = shoup_lazy(V, wt.w, wt.wp, q);
-                    v[e] = U + V;
-                    v[e | (1 << bit)] = U - V + q2;
-                }
-            }
-        }
+        fwd_bfly<Gm, LOGS>(v, r, ktr, COL ? 0 : gi, tw, q);
         if (r == R - 1 && !COL) {
             // row pass: full reduction (< 16q -> [0, q)), then through shared memory
             // back to a coalesced store of the tile
@@ -295,7 +357,7 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
     int gi, g, t;
     locate<Gm, LOGS, OTHER, COL>(rm, row, gi, g, t);
     const int p = pm.idx[row % pm.period];
-    const uint64_t q = kt.q[p], q2 = 2 * q;
+    const uint64_t q = kt.q[p];
     const TwPair *tw = kt.tw_inv + ((size_t)p << LOGN);
     uint64_t *a = data + ((size_t)row << LOGN);
     uint64_t *buf0 = sm, *buf1 = sm + S * G;
@@ -324,36 +386,7 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))];
         }
-        // stage s needs 2^(w-1-s) distinct twiddles (register bits above it); load the
-        // whole round's set up front
-        TwPair tws[E];
-#pragma unroll
-        for (int s = 0; s < w; ++s) {
-            const int lp = LOGS - 1 - (lo + s);
-            const int ntop = w - 1 - s;
-            const TwPair *tb = tw + (1 << (Gm::LBASE + lp)) + (COL ? 0 : (gi << lp)) + (ktr >> (LOGS - lp));
-#pragma unroll
-            for (int mm = 0; mm < (1 << ntop); ++mm)
-                tws[(1 << ntop) - 1 + mm] = tb[kmap(ELOG, lo, w, 0, mm << (ELOG - ntop)) >> (LOGS - lp)];
-        }
-#pragma unroll
-        for (int s = 0; s < w; ++s) {
-            const int bit = ELOG - w + s;  // register bit of k-bit lo+s
-            const int ntop = w - 1 - s;    // register bits above: the twiddle depends on these only
-#pragma unroll
-            for (int mm = 0; mm < (1 << ntop); ++mm) {
-                const int erep = mm << (ELOG - ntop);
-                const TwPair wt = tws[(1 << ntop) - 1 + mm];
-#pragma unroll
-                for (int e = erep; e < erep + (1 << (ELOG - ntop)); ++e) {
-                    if (e & (1 << bit)) continue;
-                    const uint64_t X = v[e];
-                    const uint64_t Y = v[e | (1 << bit)];
-                    v[e] = csub64(X + Y, q2);
-                    v[e | (1 << bit)] = shoup_lazy(X - Y + q2, wt.w, wt.wp, q);
-                }
-            }
-        }
+        inv_bfly<Gm, LOGS>(v, r, ktr, COL ? 0 : gi, tw, q);
         if (r == R - 1 && !COL) {
             uint64_t *b = (r & 1) ? buf1 : buf0;
 #pragma unroll
