@@ -267,7 +267,8 @@ mmfhe_status mmfhe_profile_get(mmfhe_ctx *ctx, char *buf, size_t cap, size_t *le
 /* Integer roofline microbenchmark (synchronous): whole-GPU rate of one
  * register-resident operation, in operations per second.
  * kind 0: Harvey CT butterfly (lazy Shoup), 1: GS butterfly, 2: 64x64->128 MAC,
- * 3: fully reduced Shoup modular product. */
+ * 3: fully reduced Shoup modular product, 4/5: CT/GS butterfly with the
+ * truncated-quotient Shoup product (results in [0, 4q)).  Other kinds: E_INVALID_ARG. */
 mmfhe_status mmfhe_microbench(mmfhe_ctx *ctx, int kind, double *ops_per_s);
 
 #ifdef __cplusplus

@@ -668,7 +668,7 @@ mmfhe_status mmfhe_profile_enable(mmfhe_ctx *ctx, int on)
 mmfhe_status mmfhe_microbench(mmfhe_ctx *ctx, int kind, double *ops_per_s)
 {
     API_BEGIN
-    MMFHE_REQUIRE(ops_per_s && kind >= 0 && kind <= 3, MMFHE_E_INVALID_ARG, "bad microbench kind");
+    MMFHE_REQUIRE(ops_per_s && kind >= 0 && kind <= 5, MMFHE_E_INVALID_ARG, "bad microbench kind");
     *ops_per_s = microbench_ops_per_s(*ctx, kind);
     API_END(ctx)
 }

@@ -74,6 +74,7 @@ struct KTables {
     const TwPair *tw_fwd;      // [np][N]  psi^{bitrev(k)}
     const TwPair *tw_inv;      // [np][N]  psi^{-bitrev(k)}
     const TwPair *n_inv;       // [np]
+    const TwPair *n_inv_w;     // [np] N^{-1} tw_inv[1]: the inverse's last stage with N^{-1} folded in
     const uint64_t *recip;     // [np] floor(2^64 / q): shoup_lazy(x, 1, recip, q) = x mod q in [0, 2q)
     uint32_t log_n;
     uint32_t n;
@@ -95,6 +96,18 @@ struct ColSrc {
     size_t xs;          // item stride of x (words)
     uint32_t period;    // == the PrimeMap period
     uint8_t src[kMapCap];
+};
+
+// Optional source of the inverse NTT's row pass (its first pass): output row r reads
+// x + (r / per) * xs + (r % per) * ss instead of transforming in place, and with g != 1
+// reads it through the NTT-domain automorphism sigma_g (word j <- word perm_g(j),
+// perm_g(j) = bitrev(((2 bitrev(j) + 1) g mod 2N - 1) / 2)): the rotation's permutation
+// and the key switch's INTT are one pass over HBM.
+struct InvSrc {
+    const uint64_t *x;  // nullptr: in place
+    size_t xs, ss;      // item stride, sub-row stride (words)
+    uint32_t per;       // rows per item
+    uint32_t g;         // Galois element (odd, < 2N); 1 = identity
 };
 
 inline PrimeMap make_map(const std::vector<uint32_t> &v)

@@ -215,7 +215,7 @@ void Ctx::build_tables()
 {
     const uint32_t np = (uint32_t)primes.size();
     std::vector<uint64_t> hq(np), hqinv(np), hr2(np);
-    std::vector<TwPair> fwd((size_t)np * n), inv((size_t)np * n), ninv(np);
+    std::vector<TwPair> fwd((size_t)np * n), inv((size_t)np * n), ninv(np), ninvw(np);
     std::vector<uint32_t> br(n);
     for (uint32_t k = 0; k < n; ++k) {
         uint32_t r = 0;
@@ -243,6 +243,8 @@ void Ctx::build_tables()
         }
         uint64_t ni = host::inv(n, q);
         ninv[pi] = {ni, host::shoup(ni, q)};
+        const uint64_t niw = host::mul(ni, inv[(size_t)pi * n + 1].w, q);
+        ninvw[pi] = {niw, host::shoup(niw, q)};
     }
     auto up = [&](DBuf &b, const void *src, size_t bytes) {
         b = DBuf((bytes + 7) / 8, stream);
@@ -254,12 +256,14 @@ void Ctx::build_tables()
     up(tab_tw_fwd, fwd.data(), fwd.size() * sizeof(TwPair));
     up(tab_tw_inv, inv.data(), inv.size() * sizeof(TwPair));
     up(tab_ninv, ninv.data(), ninv.size() * sizeof(TwPair));
+    up(tab_ninvw, ninvw.data(), ninvw.size() * sizeof(TwPair));
     kt.q = tab_q.get();
     kt.qinv_neg = tab_qinv.get();
     kt.r2 = tab_r2.get();
     kt.tw_fwd = (const TwPair *)tab_tw_fwd.get();
     kt.tw_inv = (const TwPair *)tab_tw_inv.get();
     kt.n_inv = (const TwPair *)tab_ninv.get();
+    kt.n_inv_w = (const TwPair *)tab_ninvw.get();
     kt.log_n = log_n;
     kt.n = n;
 

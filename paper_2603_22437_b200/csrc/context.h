@@ -97,7 +97,7 @@ class Ctx {
 
     // device tables
     KTables kt{};
-    DBuf tab_q, tab_qinv, tab_r2, tab_tw_fwd, tab_tw_inv, tab_ninv;
+    DBuf tab_q, tab_qinv, tab_r2, tab_tw_fwd, tab_tw_inv, tab_ninv, tab_ninvw;
     // base conversion / rescale constant blob (device) and host plans
     DBuf tab_bconv;
     std::vector<std::vector<ModUpPlan>> modup;  // [level][digit]
@@ -211,6 +211,7 @@ class ProfScope {
 // ------------------------------------------------------------------ kernels (launchers)
 // src: optional fused source of the col pass (ModUp of single-limb digits), see ColSrc
 void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const ColSrc *src = nullptr);
-void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm);
+// src: optional out-of-place / automorphism-permuted source of the row pass, see InvSrc
+void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const InvSrc *src = nullptr);
 
 }  // namespace mmfhe

@@ -159,13 +159,19 @@ void export_ct(Ctx &c, const DCt &in, mmfhe_ct &out)
     out.scale = in.scale;
     out.n_slots = in.n_slots;
     out.n_polys = in.npolys;
+    // coefficient form: out-of-place INTT straight from the library's buffer
+    const InvSrc src{in.data(), words, c.n, rows, 1};
     if (out.on_device) {
-        memcpy_d2d(c, out.data, in.data(), words);
-        if (out.form == MMFHE_FORM_COEFF) ntt_inverse(c, out.data, rows, qmap(c, in.level));
+        if (out.form == MMFHE_FORM_COEFF)
+            ntt_inverse(c, out.data, rows, qmap(c, in.level), &src);
+        else
+            memcpy_d2d(c, out.data, in.data(), words);
     } else {
         DBuf tmp(words, c.stream);
-        memcpy_d2d(c, tmp.get(), in.data(), words);
-        if (out.form == MMFHE_FORM_COEFF) ntt_inverse(c, tmp.get(), rows, qmap(c, in.level));
+        if (out.form == MMFHE_FORM_COEFF)
+            ntt_inverse(c, tmp.get(), rows, qmap(c, in.level), &src);
+        else
+            memcpy_d2d(c, tmp.get(), in.data(), words);
         CUDA_CHECK(cudaMemcpyAsync(out.data, tmp.get(), words * 8, cudaMemcpyDeviceToHost, c.stream));
         CUDA_CHECK(cudaStreamSynchronize(c.stream));
     }
@@ -405,15 +411,16 @@ struct ModUpOut {
     size_t T = 0;
 };
 
-ModUpOut ks_modup(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t B)
+// g != 1: ModUp of sigma_g(x) (the rotation's permutation fused into the INTT's first read).
+ModUpOut ks_modup(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t B, uint32_t g = 1)
 {
     const size_t N = c.n;
     const size_t lw = (size_t)(l + 1) * N;
     ModUpOut m;
-    // coefficient form of every x_b
+    // coefficient form of every x_b (or sigma_g(x_b)): out-of-place INTT, no staging copy
     DBuf xc(B * lw, c.stream);
-    CUDA_CHECK(cudaMemcpy2DAsync(xc.get(), lw * 8, x_ntt, xs * 8, lw * 8, B, cudaMemcpyDeviceToDevice, c.stream));
-    ntt_inverse(c, xc.get(), B * (l + 1), qmap(c, l));
+    const InvSrc src{x_ntt, xs, N, l + 1, g};
+    ntt_inverse(c, xc.get(), B * (l + 1), qmap(c, l), &src);
     // fast BConv of every digit, then NTT of the converted rows
     const auto &plans = c.modup[l];
     const std::vector<uint32_t> basis = c.ext_basis(l);
@@ -443,15 +450,19 @@ ModUpOut ks_modup(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t
     return m;
 }
 
-// Key inner product (each evk word fetched once per batch split) + ModDown.
+// Key inner product (each evk word fetched once per batch split) + ModDown.  The x / y
+// reads of the inner product go through sigma_gx / sigma_gy and poly 0's addend through
+// sigma_g0 (NTT-domain gathers fused into the kernels; 1 = none); add2 is a second,
+// unpermuted poly-0 addend.
 void ks_ip_moddown(Ctx &c, const uint64_t *x_ntt, size_t xs, const uint64_t *y, const ModUpOut &m, uint32_t l,
                    uint32_t B, const DKey &key, uint64_t *out, size_t os, const uint64_t *add0,
-                   const uint64_t *add1, size_t as)
+                   const uint64_t *add1, size_t as, uint32_t gx = 1, uint32_t gy = 1, uint32_t g0 = 1,
+                   const uint64_t *add2 = nullptr)
 {
     const size_t N = c.n;
     const size_t lw = (size_t)(l + 1) * N;
     DBuf accQ(B * 2 * lw, c.stream), accP(B * 2 * c.K * N, c.stream);
-    launch_key_ip(c, accQ.get(), accP.get(), x_ntt, xs, y, m.T * N, m.off, key.buf.get(), l, B);
+    launch_key_ip(c, accQ.get(), accP.get(), x_ntt, xs, y, m.T * N, m.off, key.buf.get(), l, B, gx, gy);
     std::vector<uint32_t> pm;
     for (uint32_t k = 0; k < c.K; ++k) pm.push_back(c.L + 1 + k);
     ntt_inverse(c, accP.get(), B * 2 * c.K, make_map(pm));
@@ -467,7 +478,7 @@ void ks_ip_moddown(Ctx &c, const uint64_t *x_ntt, size_t xs, const uint64_t *y, 
         launch_moddown_bconv(c, w.get(), accP.get(), l, B);
         ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l));
     }
-    launch_moddown_final(c, out, os, accQ.get(), w.get(), add0, add1, as, l, B);
+    launch_moddown_final(c, out, os, accQ.get(), w.get(), add0, add1, as, l, B, g0, add2);
 }
 }  // namespace
 
@@ -503,13 +514,12 @@ std::vector<DCt> ev_rotate_hoisted(Ctx &c, const DCt &a, const std::vector<int32
         }
         const DKey &key = find_gk(c, k);
         rec_n(c, "hrot_hoisted", l, B, std::to_string(k));
-        // sigma_g on (c0, c1) and on the ModUp'd digits: an NTT-domain permutation of every row
-        DBuf sig(a.item_words() * B, c.stream), sy(B * m.T * c.n, c.stream);
-        launch_automorph(c, sig.get(), a.data(), a.rows(), g);
-        launch_automorph(c, sy.get(), m.y.get(), (uint32_t)(B * m.T), g);
+        // sigma_g on (c0, c1) and on the ModUp'd digits is an NTT-domain permutation of
+        // every row: applied inside the inner product's reads and ModDown's addend
         DCt r = make_ct(c, l, 2, a.n_slots, a.scale, B);
-        ks_ip_moddown(c, sig.get() + a.poly_words(), a.item_words(), sy.get(), m, l, B, key, r.data(),
-                      r.item_words(), sig.get(), nullptr, a.item_words());
+        const uint32_t g32 = (uint32_t)g;
+        ks_ip_moddown(c, a.poly(1), a.item_words(), m.y.get(), m, l, B, key, r.data(), r.item_words(), a.data(),
+                      nullptr, a.item_words(), g32, g32, g32);
         out.push_back(std::move(r));
     }
     return out;
@@ -550,10 +560,12 @@ DCt ev_rotate(Ctx &c, const DCt &a, int32_t step)
     const DKey &key = find_gk(c, k);
     rec_n(c, "hrot", a.level, a.batch, std::to_string(k));
     DCt r = make_ct(c, a.level, 2, a.n_slots, a.scale, a.batch);
-    DBuf sig(a.item_words() * a.batch, c.stream);
-    launch_automorph(c, sig.get(), a.data(), a.rows(), g);
-    ev_keyswitch(c, sig.get() + a.poly_words(), a.item_words(), a.level, a.batch, key, r.data(), r.item_words(),
-                 sig.get(), nullptr, a.item_words());
+    // sigma_g fused: into the INTT's first read (c1), the inner product's reads of the
+    // digit-own rows (sigma_g c1) and ModDown's addend (sigma_g c0)
+    const uint32_t g32 = (uint32_t)g;
+    ModUpOut m = ks_modup(c, a.poly(1), a.item_words(), a.level, a.batch, g32);
+    ks_ip_moddown(c, a.poly(1), a.item_words(), m.y.get(), m, a.level, a.batch, key, r.data(), r.item_words(),
+                  a.data(), nullptr, a.item_words(), g32, 1, g32);
     return r;
 }
 
@@ -564,10 +576,10 @@ DCt ev_rescale(Ctx &c, const DCt &a)
     const uint32_t l = a.level, B = a.batch;
     rec_n(c, "rescale", l, B);
     const size_t N = c.n;
+    // coefficient form of the last limb of both polys of every item (out-of-place INTT)
     DBuf t(2 * N * B, c.stream);
-    CUDA_CHECK(cudaMemcpy2DAsync(t.get(), N * 8, a.data() + (size_t)l * N, a.poly_words() * 8, N * 8, 2 * (size_t)B,
-                                 cudaMemcpyDeviceToDevice, c.stream));
-    ntt_inverse(c, t.get(), 2 * B, make_map({l}));
+    const InvSrc src{a.data() + (size_t)l * N, a.item_words(), a.poly_words(), 2, 1};
+    ntt_inverse(c, t.get(), 2 * B, make_map({l}), &src);
     DBuf v((size_t)2 * l * N * B, c.stream);
     launch_rescale_prep(c, v.get(), t.get(), l, B);
     ntt_forward(c, v.get(), 2 * l * B, qmap(c, l - 1));
@@ -576,8 +588,8 @@ DCt ev_rescale(Ctx &c, const DCt &a)
     return r;
 }
 
-// acc + HRot(acc, step) with the HAdd fused: the automorph writes sigma(c0) + c0 for poly 0
-// and ModDown adds c1 to poly 1 (records "hrot" then "hadd", as the two ops it replaces).
+// acc + HRot(acc, step) with the HAdd fused: ModDown adds sigma(c0) + c0 to poly 0 and c1
+// to poly 1 (records "hrot" then "hadd", as the two ops it replaces).
 DCt ev_rot_add(Ctx &c, const DCt &a, int32_t step)
 {
     MMFHE_REQUIRE(a.npolys == 2, MMFHE_E_LAYOUT, "rotate needs a 2-poly ciphertext");
@@ -588,10 +600,11 @@ DCt ev_rot_add(Ctx &c, const DCt &a, int32_t step)
     rec_n(c, "hrot", a.level, a.batch, std::to_string(k));
     rec_n(c, "hadd", a.level, a.batch);
     DCt r = make_ct(c, a.level, 2, a.n_slots, a.scale, a.batch);
-    DBuf sig(a.item_words() * a.batch, c.stream);
-    launch_automorph_acc(c, sig.get(), a.data(), a.rows(), g, a.level);
-    ev_keyswitch(c, sig.get() + a.poly_words(), a.item_words(), a.level, a.batch, key, r.data(), r.item_words(),
-                 sig.get(), a.poly(1), a.item_words());
+    // as ev_rotate, with ModDown adding sigma_g(c0) + c0 to poly 0 and c1 to poly 1
+    const uint32_t g32 = (uint32_t)g;
+    ModUpOut m = ks_modup(c, a.poly(1), a.item_words(), a.level, a.batch, g32);
+    ks_ip_moddown(c, a.poly(1), a.item_words(), m.y.get(), m, a.level, a.batch, key, r.data(), r.item_words(),
+                  a.data(), a.poly(1), a.item_words(), g32, 1, g32, a.data());
     return r;
 }
 

@@ -5,6 +5,8 @@
 //   kind 1: Gentleman-Sande butterfly, as in the inverse NTT
 //   kind 2: 64x64->128 multiply-accumulate (the key inner product / BConv MAC)
 //   kind 3: Shoup modular product (fixed operand), fully reduced
+//   kind 4: CT butterfly with the truncated-quotient Shoup product (shoup_lazy4, [0, 4q))
+//   kind 5: GS butterfly with shoup_lazy4
 #include "context.h"
 #include "modarith.cuh"
 
@@ -58,10 +60,32 @@ __global__ void __launch_bounds__(256) mb_kernel(uint64_t *out, uint64_t q, uint
         }
 #pragma unroll
         for (int j = 0; j < kChains; ++j) a[j] ^= acc[j].lo ^ acc[j].hi;
-    } else {
+    } else if (kind == 3) {
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
             for (int j = 0; j < kChains; ++j) a[j] = shoup(a[j] ^ b[j], w0, wp0, q);
+        }
+    } else if (kind == 4) {
+        const uint64_t q4 = 4 * q, q8 = 8 * q;
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int j = 0; j < kChains; ++j) {
+                uint64_t U = a[j] >= q8 ? a[j] - q8 : a[j];
+                uint64_t V = shoup_lazy4(b[j], w0, wp0, q);
+                a[j] = U + V;
+                b[j] = U - V + q4;
+            }
+        }
+    } else {
+        const uint64_t q4 = 4 * q;
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int j = 0; j < kChains; ++j) {
+                const uint64_t X = a[j], Y = b[j];
+                const uint64_t s = X + Y;
+                a[j] = s >= q4 ? s - q4 : s;
+                b[j] = shoup_lazy4(X - Y + q4, w0, wp0, q);
+            }
         }
     }
     uint64_t x = 0;

@@ -65,6 +65,24 @@ __device__ __forceinline__ uint64_t shoup(uint64_t a, uint64_t w, uint64_t wp, u
     return csub(shoup_lazy(a, w, wp, q), q);
 }
 
+// Shoup product with a truncated quotient, result in [0, 4q) for any a < 2^64 (w < q).
+// With a = ah 2^32 + al and wp = wh 2^32 + wl, a wp / 2^64 = ah wh + (ah wl + al wh) / 2^32
+// + al wl / 2^64: dropping al wl and the fractions of the two middle terms leaves an
+// integer Q' <= floor(a wp / 2^64) short by at most 2, so a w - Q' q < 2q + 2q.  One
+// 32x32->64 and two 32x32->hi32 products replace the four wide products of __umul64hi.
+__device__ __forceinline__ uint64_t shoup_lazy4(uint64_t a, uint64_t w, uint64_t wp, uint64_t q)
+{
+    uint64_t Q;
+    asm("{\n\t.reg .u32 al, ah, wl, wh, t1, t2;\n\t.reg .u64 s;\n\t"
+        "mov.b64 {al, ah}, %1;\n\tmov.b64 {wl, wh}, %2;\n\t"
+        "mul.hi.u32 t1, ah, wl;\n\tmul.hi.u32 t2, al, wh;\n\t"
+        "add.cc.u32 t1, t1, t2;\n\taddc.u32 t2, 0, 0;\n\t"
+        "mov.b64 s, {t1, t2};\n\tmad.wide.u32 %0, ah, wh, s;\n\t}"
+        : "=l"(Q)
+        : "l"(a), "l"(wp));
+    return a * w - Q * q;
+}
+
 // Montgomery reduction of x = hi*2^64 + lo < q*2^64: returns x*2^-64 mod q in [0, 2q).
 __device__ __forceinline__ uint64_t redc_lazy(U128 x, uint64_t q, uint64_t qinv_neg)
 {

@@ -4,20 +4,24 @@
 // merged into the twiddles (tw_fwd[m + i] = psi^{bitrev(m+i)}): stage l (m = 2^l)
 // pairs j, j + N/2^{l+1} with twiddle index m + (j >> (log N - l)).
 // Inverse: Gentleman-Sande with psi^{-bitrev}, bit-reversed in, natural out,
-// times N^{-1}.  Shoup products throughout (q < 2^60).
+// times N^{-1} (folded into the last stage).  Shoup products throughout (q < 2^60).
 //
 // B200 mapping.  A limb of N = 2^16 words (512 KiB) exceeds one SM's shared
 // memory, so the transform is two passes over HBM (logN = L1 + L2):
 //   col pass -- stages 0..L1-1 on 2^L2 strided columns of 2^L1 words; a warp
 //               spans G consecutive columns (G*8-byte sector-aligned runs);
-//   row pass -- stages L1..logN-1 on contiguous blocks of 2^L2 words, staged
-//               through shared memory so the HBM side is fully coalesced.
+//   row pass -- stages L1..logN-1 on contiguous blocks of 2^L2 words.  Its first and
+//               last rounds read / write HBM directly: in those rounds a thread's
+//               registers cover runs of 2..8 consecutive words, moved with 16- or
+//               32-byte vector accesses that are contiguous across lanes (measured
+//               12-20% faster than staging the tile through shared memory).
 // Inside a pass each thread holds E = 2^ELOG = 8 words in registers (radix-8)
 // and runs up to ELOG butterfly stages there per round; rounds exchange through
 // double-buffered, XOR-swizzled shared memory (one __syncthreads per exchange,
 // bank-conflict-free).  Forward rounds put the narrow round FIRST (top bits) and
 // inverse rounds LAST, so that in every round a stage's twiddle depends only on
-// register bits above it: each distinct twiddle is loaded once per stage.
+// register bits above it: each distinct twiddle is loaded once per stage (one
+// 16-byte read-only load per twiddle pair).
 //
 // Index arithmetic.  The whole pass geometry (LOGS, the other pass's bits, groups
 // per CTA) is compile-time.  Every local index k = kmap(t, e) is the OR of a thread
@@ -26,12 +30,13 @@
 // a compile-time constant: the loads and stores carry immediate offsets and the
 // issue slots go to the butterflies.
 //
-// Lazy forward reduction.  With q < 2^60 every word may grow to 16q < 2^64.  A CT
-// butterfly (U, V) -> (U + V', U - V' + 2q), V' = V w mod q in [0, 2q), grows the
-// bound by 2q, so instead of Harvey's per-butterfly U >= 2q correction the forward
-// transform corrects U >= 8q only at global stages s = 3 mod 4 (bounds: input < 2q,
-// then < 10q after each corrected stage, never above 16q), and the row pass fully
-// reduces its output to [0, q) with one estimated-quotient step (reduce_est).  Inputs of ntt_forward must be < 2q.
+// Butterfly product: Shoup with a truncated quotient (shoup_lazy4, V' = V w mod q in
+// [0, 4q)).  Lazy forward reduction: with q < 2^60 every word may grow to 16q < 2^64;
+// a CT butterfly (U, V) -> (U + V', U - V' + 4q) grows the bound by 4q, so instead of a
+// per-butterfly correction the forward transform corrects U >= 8q only at odd global
+// stages >= 3 (fwd_corr), and the row pass fully reduces its output to [0, q) with one
+// estimated-quotient step (reduce_est).  Inputs of ntt_forward must be < 2q, inputs of
+// ntt_inverse < 4q.
 // Every limb of every polynomial of a batch goes in one launch.
 #include <algorithm>
 
@@ -43,6 +48,21 @@ namespace mmfhe {
 namespace {
 
 constexpr int kCtaThreads = 256;
+
+// Butterfly product: Shoup with a truncated quotient (shoup_lazy4, results in [0, 4q)):
+// 3 wide + 2 high 32-bit products instead of 6 wide ones; measured 5% above the exact-
+// quotient butterfly in the register-resident microbenchmark and 2-4% in the passes.
+constexpr int kLazyMul = 4;  // V' < 4q
+__device__ __forceinline__ uint64_t bfly_mul(uint64_t a, uint64_t w, uint64_t wp, uint64_t q)
+{
+    return shoup_lazy4(a, w, wp, q);
+}
+// Forward: is U >= 8q corrected before the butterflies of global stage s?  From the input
+// bound 2q every stage grows the bound by 4q (U + V', U - V' + 4q); U < 16q must hold
+// before a correction and every word stays < 16q < 2^64: bounds 2, 6, 10, 14 | 12, 16 |
+// 12, 16 ... -> correct at odd s >= 3.
+__host__ __device__ constexpr bool fwd_corr(int s) { return s >= 3 && (s & 1); }
+
 // min CTAs/SM for __launch_bounds__: 4 (<= 64 registers) fits every pass without spills
 // and keeps 32 warps resident; 5 (<= 51 registers) spills
 constexpr int kMinCtas = 4;
@@ -131,6 +151,76 @@ __device__ __forceinline__ int soff(int sb, int ke)
 
 __device__ __forceinline__ uint64_t csub64(uint64_t x, uint64_t m) { return x >= m ? x - m : x; }
 
+// One twiddle pair in a single 16-byte read-only load (the twiddle tables are separate,
+// 16-byte aligned allocations of 16-byte entries).
+__device__ __forceinline__ TwPair ld_tw(const TwPair *p)
+{
+    const ulonglong2 x = __ldg(reinterpret_cast<const ulonglong2 *>(p));
+    return TwPair{x.x, x.y};
+}
+
+// log2 of the run of consecutive local indices a thread's registers cover in a round:
+// the largest r with kmap(0, e) == e for every e < 2^r (then kmap(t, e0 + i) = kmap(t, e0) + i
+// for i < 2^r and e0 a multiple of 2^r, and the thread part is 2^r-word aligned).
+__host__ __device__ constexpr int run_log(int elog, int lo, int w)
+{
+    int r = 0;
+    while (r < elog) {
+        bool ok = true;
+        for (int e = 0; e < (2 << r); ++e) ok = ok && kmap(elog, lo, w, 0, e) == e;
+        if (!ok) break;
+        ++r;
+    }
+    return r;
+}
+
+// Vectorised global I/O of 2^RL consecutive words (16 B / 32 B / 2 x 32 B per thread).
+template <int RL>
+__device__ __forceinline__ void ld_run(const uint64_t *p, uint64_t *v)
+{
+    if constexpr (RL == 0) {
+        v[0] = p[0];
+    } else if constexpr (RL == 1) {
+        asm volatile("ld.global.v2.u64 {%0, %1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(p));
+    } else {
+#pragma unroll
+        for (int i = 0; i < (1 << RL); i += 4)
+            asm volatile("ld.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+                         : "=l"(v[i]), "=l"(v[i + 1]), "=l"(v[i + 2]), "=l"(v[i + 3])
+                         : "l"(p + i));
+    }
+}
+template <int RL>
+__device__ __forceinline__ void st_run(uint64_t *p, const uint64_t *v)
+{
+    if constexpr (RL == 0) {
+        p[0] = v[0];
+    } else if constexpr (RL == 1) {
+        asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(v[0]), "l"(v[1]) : "memory");
+    } else {
+#pragma unroll
+        for (int i = 0; i < (1 << RL); i += 4)
+            asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p + i), "l"(v[i]), "l"(v[i + 1]),
+                         "l"(v[i + 2]), "l"(v[i + 3])
+                         : "memory");
+    }
+}
+// A round's register pattern straight from / to global memory, one vector per run.
+template <int ELOG, int LO, int W>
+__device__ __forceinline__ void ld_pattern(const uint64_t *blk, int ktr, uint64_t (&v)[1 << ELOG])
+{
+    constexpr int RL = run_log(ELOG, LO, W);
+#pragma unroll
+    for (int e = 0; e < (1 << ELOG); e += (1 << RL)) ld_run<RL>(blk + ktr + kmap(ELOG, LO, W, 0, e), v + e);
+}
+template <int ELOG, int LO, int W>
+__device__ __forceinline__ void st_pattern(uint64_t *blk, int ktr, const uint64_t (&v)[1 << ELOG])
+{
+    constexpr int RL = run_log(ELOG, LO, W);
+#pragma unroll
+    for (int e = 0; e < (1 << ELOG); e += (1 << RL)) st_run<RL>(blk + ktr + kmap(ELOG, LO, W, 0, e), v + e);
+}
+
 // Batch structure of the rows: row = item * rstride + ri, ri < rstride, n_items items.
 // z / n_items by multiply-high (Granlund-Montgomery; z < 2^31): q = (umulhi(z, mul) + z) >> shift.
 struct RowMap {
@@ -189,7 +279,7 @@ __device__ __forceinline__ void fwd_bfly(uint64_t (&v)[Gm::E], int r, int ktr, i
     using F = FwdGeo<Gm, LOGS>;
     constexpr int ELOG = Gm::ELOG, E = Gm::E;
     const int w = F::w(r), lo = F::lo(r), lp0 = LOGS - 1 - F::hi(r);
-    const uint64_t q2 = 2 * q, q8 = 8 * q;
+    const uint64_t qm = kLazyMul * q, q8 = 8 * q;
     TwPair tws[E];
 #pragma unroll
     for (int s = 0; s < w; ++s) {
@@ -197,12 +287,12 @@ __device__ __forceinline__ void fwd_bfly(uint64_t (&v)[Gm::E], int r, int ktr, i
         const TwPair *tb = tw + (1 << (Gm::LBASE + lp)) + (prefix << lp) + (ktr >> (LOGS - lp));
 #pragma unroll
         for (int mm = 0; mm < (1 << s); ++mm)
-            tws[(1 << s) - 1 + mm] = tb[kmap(ELOG, lo, w, 0, mm << (ELOG - s)) >> (LOGS - lp)];
+            tws[(1 << s) - 1 + mm] = ld_tw(tb + (kmap(ELOG, lo, w, 0, mm << (ELOG - s)) >> (LOGS - lp)));
     }
 #pragma unroll
     for (int s = 0; s < w; ++s) {
         const int bit = ELOG - 1 - s;  // register bit paired in this stage
-        const bool corr = ((Gm::LBASE + lp0 + s) & 3) == 3;
+        const bool corr = fwd_corr(Gm::LBASE + lp0 + s);
 #pragma unroll
         for (int mm = 0; mm < (1 << s); ++mm) {
             const int erep = mm << (ELOG - s);
@@ -213,29 +303,33 @@ __device__ __forceinline__ void fwd_bfly(uint64_t (&v)[Gm::E], int r, int ktr, i
                 uint64_t U = v[e];
                 uint64_t V = v[e | (1 << bit)];
                 if (corr) U = csub64(U, q8);
-                V = shoup_lazy(V, wt.w, wt.wp, q);
+                V = bfly_mul(V, wt.w, wt.wp, q);
                 v[e] = U + V;
-                v[e | (1 << bit)] = U - V + q2;
+                v[e | (1 << bit)] = U - V + qm;
             }
         }
     }
 }
 
 // Inverse round r: bits [lo, lo+w) from the bottom up (the narrow round last); stage s
-// needs 2^(w-1-s) distinct twiddles (register bits above it).  Harvey GS butterflies.
+// needs 2^(w-1-s) distinct twiddles (register bits above it).  GS butterflies in [0, 4q).
 template <class Gm, int LOGS>
 struct InvGeo {
     __device__ static constexpr int lo(int r) { return r * Gm::ELOG; }
     __device__ static constexpr int w(int r) { return (LOGS - lo(r)) < Gm::ELOG ? (LOGS - lo(r)) : Gm::ELOG; }
 };
 
-template <class Gm, int LOGS>
-__device__ __forceinline__ void inv_bfly(uint64_t (&v)[Gm::E], int r, int ktr, int prefix, const TwPair *tw, uint64_t q)
+// FOLD (last round of the col pass): the transform's final stage (local stage 0, one
+// twiddle w1 = tw[1] for the whole limb) absorbs the N^{-1} scaling, X' = (X + Y) N^{-1},
+// Y' = (X - Y) (w1 N^{-1}), fully reduced: no separate pass over the outputs.
+template <class Gm, int LOGS, bool FOLD>
+__device__ __forceinline__ void inv_bfly(uint64_t (&v)[Gm::E], int r, int ktr, int prefix, const TwPair *tw, uint64_t q,
+                                         TwPair ninv, TwPair ninv_w)
 {
     using I = InvGeo<Gm, LOGS>;
     constexpr int ELOG = Gm::ELOG, E = Gm::E;
     const int lo = I::lo(r), w = I::w(r);
-    const uint64_t q2 = 2 * q;
+    const uint64_t qm = kLazyMul * q;  // words stay in [0, kLazyMul q)
     TwPair tws[E];
 #pragma unroll
     for (int s = 0; s < w; ++s) {
@@ -244,7 +338,7 @@ __device__ __forceinline__ void inv_bfly(uint64_t (&v)[Gm::E], int r, int ktr, i
         const TwPair *tb = tw + (1 << (Gm::LBASE + lp)) + (prefix << lp) + (ktr >> (LOGS - lp));
 #pragma unroll
         for (int mm = 0; mm < (1 << ntop); ++mm)
-            tws[(1 << ntop) - 1 + mm] = tb[kmap(ELOG, lo, w, 0, mm << (ELOG - ntop)) >> (LOGS - lp)];
+            tws[(1 << ntop) - 1 + mm] = ld_tw(tb + (kmap(ELOG, lo, w, 0, mm << (ELOG - ntop)) >> (LOGS - lp)));
     }
 #pragma unroll
     for (int s = 0; s < w; ++s) {
@@ -259,8 +353,13 @@ __device__ __forceinline__ void inv_bfly(uint64_t (&v)[Gm::E], int r, int ktr, i
                 if (e & (1 << bit)) continue;
                 const uint64_t X = v[e];
                 const uint64_t Y = v[e | (1 << bit)];
-                v[e] = csub64(X + Y, q2);
-                v[e | (1 << bit)] = shoup_lazy(X - Y + q2, wt.w, wt.wp, q);
+                if (FOLD && lo + s == LOGS - 1) {
+                    v[e] = shoup(X + Y, ninv.w, ninv.wp, q);
+                    v[e | (1 << bit)] = shoup(X - Y + qm, ninv_w.w, ninv_w.wp, q);
+                } else {
+                    v[e] = csub64(X + Y, qm);
+                    v[e | (1 << bit)] = bfly_mul(X - Y + qm, wt.w, wt.wp, q);
+                }
             }
         }
     }
@@ -292,15 +391,9 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
         const int ktr = kmap(ELOG, lo, w, t, 0);
         const int sb = sbase<Gm, LOGS, COL>(ktr, g);
         if (r == 0 && !COL) {
-            // row pass: load the CTA's tile coalesced into shared memory, then read the
-            // round's register pattern from there
-            // the group's T lanes read 8 runs of T consecutive words (coalesced)
-            const int sio = sbase<Gm, LOGS, false>(t, g);
-#pragma unroll
-            for (int i = 0; i < E; ++i) buf1[soff<Gm, LOGS, false>(sio, i * T)] = blk[t + i * T];
-            __syncthreads();
-#pragma unroll
-            for (int e = 0; e < E; ++e) v[e] = buf1[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))];
+            // row pass: the round's register pattern straight from the block (runs of
+            // consecutive words per thread, 16/32-byte vector loads, coalesced across lanes)
+            ld_pattern<ELOG, FwdGeo<Gm, LOGS>::lo(0), FwdGeo<Gm, LOGS>::w(0)>(blk, ktr, v);
         } else if (r == 0 && cs.x != nullptr) {
             // fused ModUp (alpha = 1): this row is x_j mod q of a source limb x_j
             const uint64_t *src = cs.x + (row / cs.period) * cs.xs + ((size_t)cs.src[row % cs.period] << LOGN);
@@ -319,16 +412,12 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
         }
         fwd_bfly<Gm, LOGS>(v, r, ktr, COL ? 0 : gi, tw, q);
         if (r == R - 1 && !COL) {
-            // row pass: full reduction (< 16q -> [0, q)), then through shared memory
-            // back to a coalesced store of the tile
-            uint64_t *b = (r & 1) ? buf1 : buf0;
+            // row pass: full reduction (< 16q -> [0, q)), stored as the last round's runs
+            // (8 consecutive words per thread: two 32-byte stores)
             const float qinv = qinv_est(q);
 #pragma unroll
-            for (int e = 0; e < E; ++e) b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))] = reduce_est(v[e], q, qinv);
-            __syncthreads();
-            const int sio = sbase<Gm, LOGS, false>(t, g);
-#pragma unroll
-            for (int i = 0; i < E; ++i) blk[t + i * T] = b[soff<Gm, LOGS, false>(sio, i * T)];
+            for (int e = 0; e < E; ++e) v[e] = reduce_est(v[e], q, qinv);
+            st_pattern<ELOG, FwdGeo<Gm, LOGS>::lo(R - 1), FwdGeo<Gm, LOGS>::w(R - 1)>(blk, ktr, v);
         } else if (r == R - 1) {
             uint64_t *col = a + gi + ((size_t)ktr << OTHER);
 #pragma unroll
@@ -344,10 +433,12 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
 
 // ---------------------------------------------------------------- inverse
 // Stages in reverse: local stage lp = LOGS-1 .. 0 operates on bit LOGS-1-lp, so
-// rounds own bits from the bottom up (the narrow round last, at the top).  Harvey
-// GS butterflies keep words in [0, 2q); the col pass (last) multiplies by N^{-1}.
+// rounds own bits from the bottom up (the narrow round last, at the top).  GS
+// butterflies keep words in [0, 4q) (inputs must be < 4q); the col pass (last) folds
+// N^{-1} into its final stage and writes canonical residues.
 template <int LOGS, int OTHER, bool COL>
-__global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm, RowMap rm)
+__global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm, RowMap rm,
+                                                                      InvSrc is)
 {
     using Gm = Geo<LOGS, OTHER, COL>;
     constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, T = Gm::T, G = Gm::G, R = Gm::R;
@@ -369,14 +460,24 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
         const int w = (LOGS - lo) < ELOG ? (LOGS - lo) : ELOG;
         const int ktr = kmap(ELOG, lo, w, t, 0);
         const int sb = sbase<Gm, LOGS, COL>(ktr, g);
-        if (r == 0 && !COL) {
-            // the group's T lanes read 8 runs of T consecutive words (coalesced)
-            const int sio = sbase<Gm, LOGS, false>(t, g);
+        if (r == 0 && !COL && is.x != nullptr) {
+            // out-of-place source row, optionally through sigma_g
+            const uint64_t *srow = is.x + (row / is.per) * is.xs + (row % is.per) * is.ss;
+            if (is.g == 1) {
+                ld_pattern<ELOG, InvGeo<Gm, LOGS>::lo(0), InvGeo<Gm, LOGS>::w(0)>(srow + ((size_t)gi << LOGS), ktr, v);
+            } else {
+                // perm_g maps every aligned 32-word span onto an aligned 32-word span, so a
+                // warp's gathers stay within a few sectors (L1 serves the rest)
+                const uint32_t base = ((uint32_t)gi << LOGS) | (uint32_t)ktr;
 #pragma unroll
-            for (int i = 0; i < E; ++i) buf1[soff<Gm, LOGS, false>(sio, i * T)] = blk[t + i * T];
-            __syncthreads();
-#pragma unroll
-            for (int e = 0; e < E; ++e) v[e] = buf1[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))];
+                for (int e = 0; e < E; ++e) {
+                    const uint32_t j = base | (uint32_t)kmap(ELOG, lo, w, 0, e);
+                    const uint32_t ex = ((2u * (__brev(j) >> (32 - LOGN)) + 1u) * is.g) & ((2u << LOGN) - 1u);
+                    v[e] = srow[__brev((ex - 1u) >> 1) >> (32 - LOGN)];
+                }
+            }
+        } else if (r == 0 && !COL) {
+            ld_pattern<ELOG, InvGeo<Gm, LOGS>::lo(0), InvGeo<Gm, LOGS>::w(0)>(blk, ktr, v);
         } else if (r == 0) {
             const uint64_t *col = a + gi + ((size_t)ktr << OTHER);
 #pragma unroll
@@ -386,20 +487,17 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
 #pragma unroll
             for (int e = 0; e < E; ++e) v[e] = b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))];
         }
-        inv_bfly<Gm, LOGS>(v, r, ktr, COL ? 0 : gi, tw, q);
+        if (COL && r == R - 1)
+            inv_bfly<Gm, LOGS, true>(v, r, ktr, 0, tw, q, kt.n_inv[p], kt.n_inv_w[p]);
+        else
+            inv_bfly<Gm, LOGS, false>(v, r, ktr, COL ? 0 : gi, tw, q, TwPair{}, TwPair{});
         if (r == R - 1 && !COL) {
-            uint64_t *b = (r & 1) ? buf1 : buf0;
-#pragma unroll
-            for (int e = 0; e < E; ++e) b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))] = v[e];
-            __syncthreads();
-            const int sio = sbase<Gm, LOGS, false>(t, g);
-#pragma unroll
-            for (int i = 0; i < E; ++i) blk[t + i * T] = b[soff<Gm, LOGS, false>(sio, i * T)];
+            st_pattern<ELOG, InvGeo<Gm, LOGS>::lo(R - 1), InvGeo<Gm, LOGS>::w(R - 1)>(blk, ktr, v);
         } else if (r == R - 1) {
-            const TwPair ninv = kt.n_inv[p];
+            // canonical [0, q): N^{-1} is folded into the last stage (inv_bfly<FOLD>)
             uint64_t *col = a + gi + ((size_t)ktr << OTHER);
 #pragma unroll
-            for (int e = 0; e < E; ++e) col[(size_t)kmap(ELOG, lo, w, 0, e) << OTHER] = shoup(v[e], ninv.w, ninv.wp, q);
+            for (int e = 0; e < E; ++e) col[(size_t)kmap(ELOG, lo, w, 0, e) << OTHER] = v[e];
         } else {
             uint64_t *b = (r & 1) ? buf1 : buf0;
 #pragma unroll
@@ -410,7 +508,8 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
 }
 
 template <bool FWD, int LOGS, int OTHER, bool COL>
-void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm, const ColSrc *cs, cudaStream_t s)
+void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm, const ColSrc *cs, const InvSrc *is,
+                cudaStream_t s)
 {
     using Gm = Geo<LOGS, OTHER, COL>;
     static_assert(Gm::SMEM <= 48 * 1024, "NTT pass exceeds the default dynamic shared memory");
@@ -431,7 +530,8 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
         if constexpr (FWD)
             ntt_fwd_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm, src);
         else
-            ntt_inv_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm);
+            ntt_inv_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm,
+                                                                              (!COL && is) ? *is : InvSrc{});
     };
     if (COL) {
         // grid.y <= 65535: chunks of whole periods keep row % period aligned
@@ -459,14 +559,14 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
 // log N = L1 + L2, L1 = floor(log N / 2): col pass <L1, L2>, row pass <L2, L1>.
 template <bool FWD, bool COL>
 void launch_pass(uint32_t log_n, uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm, const ColSrc *cs,
-                 cudaStream_t s)
+                 const InvSrc *is, cudaStream_t s)
 {
 #define MMFHE_NTT_CASE(LN, A, B)                                    \
     case LN:                                                        \
         if (COL)                                                    \
-            launch_one<FWD, A, B, true>(d, rows, kt, pm, cs, s);        \
+            launch_one<FWD, A, B, true>(d, rows, kt, pm, cs, nullptr, s);   \
         else                                                        \
-            launch_one<FWD, B, A, false>(d, rows, kt, pm, nullptr, s);       \
+            launch_one<FWD, B, A, false>(d, rows, kt, pm, nullptr, is, s);  \
         break;
     switch (log_n) {
         MMFHE_NTT_CASE(4, 2, 2)
@@ -505,17 +605,17 @@ void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const C
     const double bytes = 16.0 * rows * c.n;  // one read + one write of every word per pass
     {
         ProfScope ps(c, "ntt_fwd_col", bytes, 0.5 * rows * c.n * L1);
-        launch_pass<true, true>(c.log_n, d, rows, c.kt, pm, src, c.stream);
+        launch_pass<true, true>(c.log_n, d, rows, c.kt, pm, src, nullptr, c.stream);
     }
     {
         ProfScope ps(c, "ntt_fwd_row", bytes, 0.5 * rows * c.n * L2);
-        launch_pass<true, false>(c.log_n, d, rows, c.kt, pm, nullptr, c.stream);
+        launch_pass<true, false>(c.log_n, d, rows, c.kt, pm, nullptr, nullptr, c.stream);
     }
     c.launches += 2;
     CUDA_CHECK(cudaGetLastError());
 }
 
-void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm)
+void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const InvSrc *src)
 {
     if (!rows) return;
     int L1, L2;
@@ -523,11 +623,13 @@ void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm)
     const double bytes = 16.0 * rows * c.n;
     {
         ProfScope ps(c, "ntt_inv_row", bytes, 0.5 * rows * c.n * L2);
-        launch_pass<false, false>(c.log_n, d, rows, c.kt, pm, nullptr, c.stream);
+        MMFHE_REQUIRE(!src || (src->x && src->per >= 1 && (src->g & 1) && src->g < 2 * c.n), MMFHE_E_LAYOUT,
+                      "INTT source");
+        launch_pass<false, false>(c.log_n, d, rows, c.kt, pm, nullptr, src, c.stream);
     }
     {
         ProfScope ps(c, "ntt_inv_col", bytes, 0.5 * rows * c.n * L1);
-        launch_pass<false, true>(c.log_n, d, rows, c.kt, pm, nullptr, c.stream);
+        launch_pass<false, true>(c.log_n, d, rows, c.kt, pm, nullptr, nullptr, c.stream);
     }
     c.launches += 2;
     CUDA_CHECK(cudaGetLastError());

@@ -21,25 +21,26 @@ void launch_addsub(Ctx &c, uint64_t *out, const uint64_t *a, const uint64_t *b, 
                    bool sub);
 // x -> x * 2^64 mod q (Montgomery form), in place.
 void launch_to_mont(Ctx &c, uint64_t *x, uint32_t rows, const PrimeMap &pm);
-// NTT-domain automorphism sigma_g on every row: out[j] = in[perm_g(j)].
-void launch_automorph(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t rows, uint64_t g);
-// rows of 2-poly items at `level`: poly 0 -> sigma_g(a) + a, poly 1 -> sigma_g(a)
-void launch_automorph_acc(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t rows, uint64_t g, uint32_t level);
+// (The NTT-domain automorphism sigma_g has no kernel of its own: it is a gather fused into
+// the INTT's first read (InvSrc), the key inner product and ModDown's addend.)
 
 // ---- hybrid key switching (batched over B polynomials x_b, each [l+1][N])
 // ModUp BConv of every digit: x_coef item stride xs; y item stride ys; digit j rows at y + off_j*N.
 void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, size_t xs, uint32_t level,
                         const std::vector<size_t> &off, uint32_t B);
 // accQ [B][2][l+1][N], accP [B][2][K][N] = sum_j y_j (.) evk_j; each key word is loaded once for all B.
+// gx / gy: the x (digit-own rows) / y reads go through sigma_g (NTT-domain gather; 1 = none).
 void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, size_t xs, const uint64_t *y,
-                   size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B);
+                   size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B,
+                   uint32_t gx = 1, uint32_t gy = 1);
 // w [B][2][l+1][N] = BConv_{P->Q}(zP [B][2][K][N]) (coefficient form).
 void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B);
 // out_{b,p} = (accQ_{b,p} - w_{b,p}) * P^{-1} (+ add_{b,p}); out/add item strides os/as,
 // poly 1 of an item at +(l+1)N; add may be null, add1 (poly 1 addend) selectable.
-// out = (accQ - w) P^{-1} (+ add0 on poly 0, + add1 on poly 1; either may be null)
+// out = (accQ - w) P^{-1} (+ sigma_g0(add0) + add2 on poly 0, + add1 on poly 1; each may be null)
 void launch_moddown_final(Ctx &c, uint64_t *out, size_t os, const uint64_t *accQ, const uint64_t *w,
-                          const uint64_t *add0, const uint64_t *add1, size_t as, uint32_t level, uint32_t B);
+                          const uint64_t *add0, const uint64_t *add1, size_t as, uint32_t level, uint32_t B,
+                          uint32_t g0 = 1, const uint64_t *add2 = nullptr);
 
 // ---- rescale (batched): t [B][2][N] coefficient-form last limbs; v [B][2][l][N]
 void launch_rescale_prep(Ctx &c, uint64_t *v, const uint64_t *t, uint32_t level, uint32_t B);

@@ -21,6 +21,18 @@ constexpr int kTB = 256;
 
 __device__ __forceinline__ uint32_t bitrev(uint32_t x, uint32_t log_n) { return __brev(x) >> (32 - log_n); }
 
+// NTT-domain automorphism sigma_g as a gather: (sigma_g a)[j] = a[galois_perm(j)] with
+// perm(j) = bitrev(((2 bitrev(j) + 1) g mod 2N - 1) / 2) (slot j holds a(psi^(2 bitrev(j)+1))).
+// The top t bits of perm(j) depend only on the top t bits of j, so 32 consecutive j map
+// onto one aligned 32-word span: a warp's gather is as coalesced as a plain read, and
+// the permutation fuses into any elementwise kernel for the price of the index math.
+__device__ __forceinline__ uint32_t galois_perm(uint32_t j, uint32_t g, uint32_t log_n)
+{
+    if (g == 1) return j;
+    const uint32_t ex = ((2u * bitrev(j, log_n) + 1u) * g) & ((2u << log_n) - 1u);
+    return bitrev((ex - 1u) >> 1, log_n);
+}
+
 inline dim3 grid3(uint32_t n, uint32_t rows, uint32_t batch = 1) { return dim3((n + kTB - 1) / kTB, rows, batch); }
 
 // ------------------------------------------------------------------ elementwise
@@ -47,36 +59,6 @@ __global__ void k_to_mont(uint64_t *__restrict__ x, KTables kt, PrimeMap pm)
 
 // sigma_g in the bit-reversed evaluation domain: slot j holds a(psi^(2 br(j) + 1)),
 // and sigma_g(a)(psi^e) = a(psi^(e g)).
-__global__ void k_automorph(uint64_t *__restrict__ out, const uint64_t *__restrict__ in, uint32_t log_n, uint64_t g)
-{
-    const uint32_t n = 1u << log_n;
-    const uint32_t r = blockIdx.y;
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const uint64_t two_n = 2ull * n;
-    const uint64_t e = ((2ull * bitrev(j, log_n) + 1) * g) & (two_n - 1);
-    const uint32_t src = bitrev((uint32_t)((e - 1) >> 1), log_n);
-    out[(size_t)r * n + j] = in[(size_t)r * n + src];
-}
-
-// Rotate-and-accumulate input of a rotsum step: poly 0 rows get sigma_g(a) + a (the
-// step's HAdd folded in), poly 1 rows sigma_g(a) (the key-switch input).
-__global__ void k_automorph_acc(uint64_t *__restrict__ out, const uint64_t *__restrict__ in, uint32_t log_n,
-                                uint64_t g, KTables kt, uint32_t level)
-{
-    const uint32_t n = 1u << log_n;
-    const uint32_t r = blockIdx.y;
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const uint64_t two_n = 2ull * n;
-    const uint64_t e = ((2ull * bitrev(j, log_n) + 1) * g) & (two_n - 1);
-    const uint32_t src = bitrev((uint32_t)((e - 1) >> 1), log_n);
-    const uint32_t rr = r % (2 * (level + 1));
-    uint64_t v = in[(size_t)r * n + src];
-    if (rr <= level) v = add_mod(v, in[(size_t)r * n + j], kt.q[rr]);
-    out[(size_t)r * n + j] = v;
-}
-
 // ------------------------------------------------------------------ base conversion
 struct ModUpDigit {
     const TwPair *hat_inv;
@@ -160,6 +142,7 @@ struct IPArgs {
     uint32_t lo[16], hi[16];
     size_t xs, ys;
     uint32_t dnum, level, L, K, B, per_z;
+    uint32_t gx, gy;  // sigma_g applied on the fly to the x / y reads (1 = none)
 };
 
 // Key inner product (see k_key_ip below for the formula).
@@ -184,17 +167,18 @@ __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ acc
     // fit 32 bits (T*N <= 2^24), bit j of xm selects x
     uint32_t so[DMAX];
     uint32_t xm = 0;
+    const uint32_t kx = galois_perm(k, a.gx, kt.log_n), ky = galois_perm(k, a.gy, kt.log_n);
 #pragma unroll
     for (int j = 0; j < DMAX; ++j) {
         if (j < (int)a.dnum) {
             kb[j] = __ldg(key + ((size_t)(2 * j) * key_rows + pr) * kt.n + k);
             ka[j] = __ldg(key + ((size_t)(2 * j + 1) * key_rows + pr) * kt.n + k);
             if (r >= a.lo[j] && r < a.hi[j]) {
-                so[j] = r * kt.n + k;
+                so[j] = r * kt.n + kx;
                 xm |= 1u << j;
             } else {
                 const uint32_t row = r < a.lo[j] ? r : r - (a.hi[j] - a.lo[j]);
-                so[j] = (uint32_t)a.y_off[j] + row * kt.n + k;
+                so[j] = (uint32_t)a.y_off[j] + row * kt.n + ky;
             }
         }
     }
@@ -240,17 +224,18 @@ __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uin
     uint64_t kb[DMAX], ka[DMAX];
     const uint64_t *src[DMAX];
     size_t sstr[DMAX];
+    const uint32_t kx = galois_perm(k, a.gx, kt.log_n), ky = galois_perm(k, a.gy, kt.log_n);
 #pragma unroll
     for (int j = 0; j < DMAX; ++j) {
         if (j < (int)a.dnum) {
             kb[j] = __ldg(key + ((size_t)(2 * j) * key_rows + pr) * kt.n + k);
             ka[j] = __ldg(key + ((size_t)(2 * j + 1) * key_rows + pr) * kt.n + k);
             if (r >= a.lo[j] && r < a.hi[j]) {
-                src[j] = x + (size_t)r * kt.n + k;
+                src[j] = x + (size_t)r * kt.n + kx;
                 sstr[j] = a.xs;
             } else {
                 const uint32_t row = r < a.lo[j] ? r : r - (a.hi[j] - a.lo[j]);
-                src[j] = y + a.y_off[j] + (size_t)row * kt.n + k;
+                src[j] = y + a.y_off[j] + (size_t)row * kt.n + ky;
                 sstr[j] = a.ys;
             }
         }
@@ -384,9 +369,13 @@ __global__ void __launch_bounds__(kTB) k_tensor1(uint64_t *__restrict__ out_base
 }
 
 // grid.y = poly*(l+1) + i, grid.z = item
+struct MDAdd {
+    const uint64_t *add0, *add1, *add2;  // poly-0 addend read through sigma_g0, poly-1 addend, poly-0 addend
+    size_t as;                          // item stride of the addends
+    uint32_t g0;
+};
 __global__ void k_moddown_final(uint64_t *__restrict__ out, size_t os, const uint64_t *__restrict__ accQ,
-                                const uint64_t *__restrict__ w, const uint64_t *__restrict__ add0,
-                                const uint64_t *__restrict__ add1, size_t as, KTables kt, MDArgs a)
+                                const uint64_t *__restrict__ w, MDAdd ad, KTables kt, MDArgs a)
 {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= kt.n) return;
@@ -396,8 +385,14 @@ __global__ void k_moddown_final(uint64_t *__restrict__ out, size_t os, const uin
     const TwPair pv = a.pinv[i];
     const size_t idx = ((size_t)b * 2 * (a.level + 1) + r) * kt.n + k;
     uint64_t d = shoup(accQ[idx] + q - w[idx], pv.w, pv.wp, q);
-    const uint64_t *add = poly == 0 ? add0 : add1;  // per-poly fused additions (may be null)
-    if (add) d = add_mod(d, add[(size_t)b * as + (size_t)i * kt.n + k], q);
+    // per-poly fused additions (each may be null): sigma_g0(add0) + add2 on poly 0, add1 on poly 1
+    const size_t ao = (size_t)b * ad.as + (size_t)i * kt.n;
+    if (poly == 0) {
+        if (ad.add0) d = add_mod(d, ad.add0[ao + galois_perm(k, ad.g0, kt.log_n)], q);
+        if (ad.add2) d = add_mod(d, ad.add2[ao + k], q);
+    } else if (ad.add1) {
+        d = add_mod(d, ad.add1[ao + k], q);
+    }
     out[(size_t)b * os + (size_t)r * kt.n + k] = d;
 }
 
@@ -770,19 +765,6 @@ void launch_to_mont(Ctx &c, uint64_t *x, uint32_t rows, const PrimeMap &pm)
     LAUNCH_CHECK(c);
 }
 
-void launch_automorph_acc(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t rows, uint64_t g, uint32_t level)
-{
-    ProfScope ps(c, "automorph", 8.0 * rows * c.n * 2.5);  // read all rows, re-read poly 0, write all
-    k_automorph_acc<<<grid3(c.n, rows), kTB, 0, c.stream>>>(out, in, c.log_n, g, c.kt, level);
-    LAUNCH_CHECK(c);
-}
-
-void launch_automorph(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t rows, uint64_t g)
-{
-    ProfScope ps(c, "automorph", 16.0 * rows * c.n);
-    k_automorph<<<grid3(c.n, rows), kTB, 0, c.stream>>>(out, in, c.log_n, g);
-    LAUNCH_CHECK(c);
-}
 
 void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, size_t xs, uint32_t level,
                         const std::vector<size_t> &off, uint32_t B)
@@ -822,7 +804,8 @@ void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, 
 }
 
 void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, size_t xs, const uint64_t *y,
-                   size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B)
+                   size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B,
+                   uint32_t gx, uint32_t gy)
 {
     const auto &plans = c.modup[level];
     IPArgs a{};
@@ -833,6 +816,8 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
     a.B = B;
     a.xs = xs;
     a.ys = ys;
+    a.gx = gx;
+    a.gy = gy;
     for (size_t j = 0; j < plans.size(); ++j) {
         a.y_off[j] = off[j] * c.n;
         a.lo[j] = plans[j].lo;
@@ -886,11 +871,14 @@ void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t leve
 }
 
 void launch_moddown_final(Ctx &c, uint64_t *out, size_t os, const uint64_t *accQ, const uint64_t *w,
-                          const uint64_t *add0, const uint64_t *add1, size_t as, uint32_t level, uint32_t B)
+                          const uint64_t *add0, const uint64_t *add1, size_t as, uint32_t level, uint32_t B,
+                          uint32_t g0, const uint64_t *add2)
 {
     ProfScope ps(c, "moddown_final",
-                 8.0 * (level + 1) * c.n * B * (6.0 + (add0 ? 1.0 : 0.0) + (add1 ? 1.0 : 0.0)));
-    k_moddown_final<<<grid3(c.n, 2 * (level + 1), B), kTB, 0, c.stream>>>(out, os, accQ, w, add0, add1, as, c.kt,
+                 8.0 * (level + 1) * c.n * B *
+                     (6.0 + (add0 ? 1.0 : 0.0) + (add1 ? 1.0 : 0.0) + (add2 ? 1.0 : 0.0)));
+    const MDAdd ad{add0, add1, add2, as, g0};
+    k_moddown_final<<<grid3(c.n, 2 * (level + 1), B), kTB, 0, c.stream>>>(out, os, accQ, w, ad, c.kt,
                                                                           md_args(c, level));
     LAUNCH_CHECK(c);
 }

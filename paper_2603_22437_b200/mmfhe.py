@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libmmfhe.so")
+# MMFHE_LIB selects another build of the same library (tools/build_variant.py experiments)
+LIB_PATH = os.environ.get("MMFHE_LIB") or os.path.join(_HERE, "lib", "libmmfhe.so")
 
 FORM_COEFF, FORM_EVAL = 0, 1
 

@@ -48,7 +48,7 @@ def test_library_is_sm100a_and_has_kernels():
     sass = subprocess.run([os.path.join(build.CUDA, "bin", "cuobjdump"), "-symbols", so],
                           capture_output=True, text=True).stdout
     for k in ("ntt_fwd_pass", "ntt_inv_pass", "k_modup", "k_key_ip", "k_moddown_bconv", "k_tensor_sum",
-              "k_pmult_sum", "k_rescale_final", "k_automorph", "k_lincomb_mat", "k_batch_sum"):
+              "k_pmult_sum", "k_rescale_final", "k_moddown_final", "k_lincomb_mat", "k_batch_sum"):
         assert k in sass, k
 
 

@@ -29,7 +29,8 @@ for P, rows in ((ps2(), 4096), (ps4(), 1020)):
     torch.cuda.synchronize()
     prof = ctx.profile()
     ctx.profile_enable(False)
-    ct, gs = ctx.microbench(0), ctx.microbench(1)
+    ct, gs = ctx.microbench(4), ctx.microbench(5)  # the NTT's own (truncated-quotient) butterflies
+    ct0, gs0 = ctx.microbench(0), ctx.microbench(1)
     print(f"log_n={P.log_n} rows={rows}")
     for k in ("ntt_fwd_col", "ntt_fwd_row", "ntt_inv_row", "ntt_inv_col"):
         c, ms, b, ops = prof[k]
@@ -37,5 +38,6 @@ for P, rows in ((ps2(), 4096), (ps4(), 1020)):
         peak = ct if "fwd" in k else gs
         print(f"  {k:12s} {ms / c * 1e3:8.1f} us/launch  {rate / 1e9:7.1f} Gbfly/s  frac {rate / peak:.3f}  "
               f"hbm {b / (ms * 1e-3) / 1e9:7.1f} GB/s")
-    print(f"  peaks: CT {ct / 1e9:.1f} GS {gs / 1e9:.1f} Gbfly/s")
+    print(f"  peaks: CT {ct / 1e9:.1f} GS {gs / 1e9:.1f} Gbfly/s (exact-quotient Shoup: CT {ct0 / 1e9:.1f} "
+          f"GS {gs0 / 1e9:.1f})")
     ctx.close()
