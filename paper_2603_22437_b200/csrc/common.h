@@ -108,6 +108,7 @@ struct InvSrc {
     size_t xs, ss;      // item stride, sub-row stride (words)
     uint32_t per;       // rows per item
     uint32_t g;         // Galois element (odd, < 2N); 1 = identity
+    uint32_t add_half;  // 1: the col pass adds floor(q/2) mod q to every output (rescale's rounding offset)
 };
 
 inline PrimeMap make_map(const std::vector<uint32_t> &v)

@@ -576,13 +576,28 @@ DCt ev_rescale(Ctx &c, const DCt &a)
     const uint32_t l = a.level, B = a.batch;
     rec_n(c, "rescale", l, B);
     const size_t N = c.n;
-    // coefficient form of the last limb of both polys of every item (out-of-place INTT)
+    // t = [a_l + floor(q_l/2)]_{q_l} in coefficient form, both polys of every item: one
+    // out-of-place INTT whose last stage adds the rounding offset
     DBuf t(2 * N * B, c.stream);
-    const InvSrc src{a.data() + (size_t)l * N, a.item_words(), a.poly_words(), 2, 1};
+    const InvSrc src{a.data() + (size_t)l * N, a.item_words(), a.poly_words(), 2, 1, 1};
     ntt_inverse(c, t.get(), 2 * B, make_map({l}), &src);
+    // v_i = NTT_{q_i}([t]_{q_i}) for i < l: the reduction mod q_i is the forward NTT's fused
+    // first read (row (poly, i) reads t's poly row); [h]_{q_i} is subtracted in
+    // rescale_final (the NTT of a constant polynomial is that constant in every slot)
     DBuf v((size_t)2 * l * N * B, c.stream);
-    launch_rescale_prep(c, v.get(), t.get(), l, B);
-    ntt_forward(c, v.get(), 2 * l * B, qmap(c, l - 1));
+    {
+        std::vector<uint32_t> pm(2 * l);
+        ColSrc cs{};
+        cs.x = t.get();
+        cs.xs = 2 * N;
+        cs.period = 2 * l;
+        for (uint32_t r = 0; r < 2 * l; ++r) {
+            pm[r] = r % l;
+            cs.src[r] = (uint8_t)(r / l);
+        }
+        MMFHE_REQUIRE(2 * l <= (uint32_t)kMapCap, MMFHE_E_PARAMS, "too many limbs for the fused rescale");
+        ntt_forward(c, v.get(), 2 * l * B, make_map(pm), &cs);
+    }
     DCt r = make_ct(c, l - 1, 2, a.n_slots, a.scale / (double)c.primes[l], B);
     launch_rescale_final(c, r.data(), a.data(), a.item_words(), v.get(), l, B);
     return r;

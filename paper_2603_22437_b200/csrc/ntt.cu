@@ -496,6 +496,10 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
         } else if (r == R - 1) {
             // canonical [0, q): N^{-1} is folded into the last stage (inv_bfly<FOLD>)
             uint64_t *col = a + gi + ((size_t)ktr << OTHER);
+            if (is.add_half) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = add_mod(v[e], q >> 1, q);
+            }
 #pragma unroll
             for (int e = 0; e < E; ++e) col[(size_t)kmap(ELOG, lo, w, 0, e) << OTHER] = v[e];
         } else {
@@ -530,8 +534,8 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
         if constexpr (FWD)
             ntt_fwd_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm, src);
         else
-            ntt_inv_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm,
-                                                                              (!COL && is) ? *is : InvSrc{});
+            ntt_inv_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(
+                dd, kt, pm, rm, !is ? InvSrc{} : !COL ? *is : InvSrc{nullptr, 0, 0, 1, 1, is->add_half});
     };
     if (COL) {
         // grid.y <= 65535: chunks of whole periods keep row % period aligned
@@ -564,7 +568,7 @@ void launch_pass(uint32_t log_n, uint64_t *d, uint32_t rows, const KTables &kt, 
 #define MMFHE_NTT_CASE(LN, A, B)                                    \
     case LN:                                                        \
         if (COL)                                                    \
-            launch_one<FWD, A, B, true>(d, rows, kt, pm, cs, nullptr, s);   \
+            launch_one<FWD, A, B, true>(d, rows, kt, pm, cs, is, s);        \
         else                                                        \
             launch_one<FWD, B, A, false>(d, rows, kt, pm, nullptr, is, s);  \
         break;
@@ -623,13 +627,13 @@ void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const I
     const double bytes = 16.0 * rows * c.n;
     {
         ProfScope ps(c, "ntt_inv_row", bytes, 0.5 * rows * c.n * L2);
-        MMFHE_REQUIRE(!src || (src->x && src->per >= 1 && (src->g & 1) && src->g < 2 * c.n), MMFHE_E_LAYOUT,
-                      "INTT source");
+        MMFHE_REQUIRE(!src || ((src->x || src->g == 1) && src->per >= 1 && (src->g & 1) && src->g < 2 * c.n),
+                      MMFHE_E_LAYOUT, "INTT source");
         launch_pass<false, false>(c.log_n, d, rows, c.kt, pm, nullptr, src, c.stream);
     }
     {
         ProfScope ps(c, "ntt_inv_col", bytes, 0.5 * rows * c.n * L1);
-        launch_pass<false, true>(c.log_n, d, rows, c.kt, pm, nullptr, nullptr, c.stream);
+        launch_pass<false, true>(c.log_n, d, rows, c.kt, pm, nullptr, src, c.stream);
     }
     c.launches += 2;
     CUDA_CHECK(cudaGetLastError());

@@ -42,9 +42,8 @@ void launch_moddown_final(Ctx &c, uint64_t *out, size_t os, const uint64_t *accQ
                           const uint64_t *add0, const uint64_t *add1, size_t as, uint32_t level, uint32_t B,
                           uint32_t g0 = 1, const uint64_t *add2 = nullptr);
 
-// ---- rescale (batched): t [B][2][N] coefficient-form last limbs; v [B][2][l][N]
-void launch_rescale_prep(Ctx &c, uint64_t *v, const uint64_t *t, uint32_t level, uint32_t B);
-// out [B][2][l][N] = (a_i - v_i) * q_l^{-1}; a item stride as.
+// ---- rescale (batched): v [B][2][l][N] = NTT_{q_i}([t]_{q_i}), t = [a_l + floor(q_l/2)]_{q_l}
+// out [B][2][l][N] = (a_i + [floor(q_l/2)]_{q_i} - v_i) * q_l^{-1}; a item stride as.
 void launch_rescale_final(Ctx &c, uint64_t *out, const uint64_t *a, size_t as, const uint64_t *v, uint32_t level,
                           uint32_t B);
 

@@ -400,25 +400,11 @@ __global__ void k_moddown_final(uint64_t *__restrict__ out, size_t os, const uin
 struct RSArgs {
     const TwPair *qlinv;    // row l of [L+1][L+1]
     const uint64_t *h;      // row l: floor(q_l/2) mod q_i
-    const uint64_t *recip;  // floor(2^64 / q_i)
     uint32_t level;
 };
 
-// v_i = ([t]_{q_i} - [h]_{q_i}) mod q_i, t = [a_l + h]_{q_l} (coefficient form); grid.z = item
-__global__ void k_rescale_prep(uint64_t *__restrict__ v, const uint64_t *__restrict__ t, KTables kt, RSArgs a)
-{
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= kt.n) return;
-    const uint32_t r = blockIdx.y, b = blockIdx.z;  // r: 0 .. 2l-1
-    const uint32_t poly = r / a.level, i = r - poly * a.level;
-    const uint64_t ql = kt.q[a.level];
-    const uint64_t hl = ql >> 1;
-    const uint64_t tl = add_mod(t[((size_t)b * 2 + poly) * kt.n + k], hl, ql);
-    const uint64_t q = kt.q[i];
-    const uint64_t tm = shoup(tl, 1, a.recip[i], q);
-    v[((size_t)b * 2 * a.level + r) * kt.n + k] = sub_mod(tm, a.h[i], q);
-}
-
+// out_i = (a_i + [h]_{q_i} - v_i) q_l^{-1} mod q_i, v_i = NTT_{q_i}([t]_{q_i}),
+// t = [a_l + h]_{q_l}, h = floor(q_l / 2) (SURVEY §8(c)-5 rescale, round half up); grid.z = item
 __global__ void k_rescale_final(uint64_t *__restrict__ out, const uint64_t *__restrict__ in, size_t is,
                                 const uint64_t *__restrict__ v, KTables kt, RSArgs a)
 {
@@ -430,7 +416,7 @@ __global__ void k_rescale_final(uint64_t *__restrict__ out, const uint64_t *__re
     const TwPair w = a.qlinv[i];
     const uint64_t x = in[(size_t)b * is + ((size_t)poly * (a.level + 1) + i) * kt.n + k];
     const size_t o = ((size_t)b * 2 * a.level + r) * kt.n + k;
-    out[o] = shoup(x + q - v[o], w.w, w.wp, q);
+    out[o] = shoup(x + a.h[i] + q - v[o], w.w, w.wp, q);  // < 3q
 }
 
 // ------------------------------------------------------------------ fused sums
@@ -647,28 +633,12 @@ __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out,
 // (checked on the host), so out[j] = sum_{w < W/2} c_w (x_a + x_b) + c_mid x_mid exactly
 // (mod q): half the modular products of k_lincomb_mat.  A CTA stages the input window of
 // its kSymJT outputs for kSymK coefficients of one (poly, limb) row in shared memory
-// (zeros outside [0, M)); each thread owns one coefficient and kSymJT / kSymSplit outputs.
-constexpr int kSymK = 128, kSymJT = 32, kSymSplit = 2;
-
-template <bool LAZY>
-__device__ __forceinline__ uint64_t lincomb_sym_row(const uint64_t *__restrict__ X, int b, int W,
-                                                    const TwPair *__restrict__ T, uint32_t L1, uint32_t r, uint64_t q)
-{
-    const uint64_t q2 = 2 * q;
-    uint64_t acc = 0;
-    for (int w = 0; w < W / 2; ++w) {
-        const TwPair c = T[(size_t)w * L1 + r];
-        const uint64_t x = X[(b + w) * kSymK] + X[(b + W - 1 - w) * kSymK];  // < 2q
-        acc += shoup_lazy(x, c.w, c.wp, q);
-        if (!LAZY) acc = acc >= q2 ? acc - q2 : acc;
-    }
-    if (W & 1) {
-        const TwPair c = T[(size_t)(W / 2) * L1 + r];
-        acc += shoup_lazy(X[(b + W / 2) * kSymK], c.w, c.wp, q);
-        if (!LAZY) acc = acc >= q2 ? acc - q2 : acc;
-    }
-    return acc;
-}
+// (zeros outside [0, M)) together with the taps in Montgomery form; each thread owns one
+// coefficient and kSymJT / kSymSplit outputs, computed kSymJB at a time: the kSymJB
+// outputs' input pairs slide along the window (two shared-memory reads per tap for all
+// kSymJB outputs) and each tap is one 64x64->128 multiply-accumulate per output, reduced
+// once at the end (hi word brought below q, then one Montgomery reduction).
+constexpr int kSymK = 128, kSymJT = 32, kSymSplit = 2, kSymJB = 4;
 
 __global__ void __launch_bounds__(kSymK *kSymSplit) k_lincomb_sym(uint64_t *__restrict__ out,
                                                                   const uint64_t *__restrict__ in, uint32_t M,
@@ -676,29 +646,67 @@ __global__ void __launch_bounds__(kSymK *kSymSplit) k_lincomb_sym(uint64_t *__re
                                                                   const TwPair *__restrict__ T, KTables kt,
                                                                   uint32_t level)
 {
-    extern __shared__ uint64_t X[];  // [kSymJT + W - 1][kSymK]
+    extern __shared__ uint64_t X[];  // [kSymJT + W - 1][kSymK], then the taps [W / 2 + 1]
     const uint32_t L1 = level + 1;
     const uint32_t r = blockIdx.y % L1, poly = blockIdx.y / L1;
     const uint32_t k0 = blockIdx.x * kSymK, j0 = blockIdx.z * kSymJT;
-    const uint64_t q = kt.q[r];
+    const uint64_t q = kt.q[r], qi = kt.qinv_neg[r];
     const size_t ps = (size_t)L1 * kt.n, item = 2 * ps;
     const size_t col = (size_t)poly * ps + (size_t)r * kt.n + k0;
     const int rows = kSymJT + (int)W - 1;
+    uint64_t *cm = X + (size_t)rows * kSymK;
+    for (int w = threadIdx.x; w <= (int)W / 2; w += blockDim.x)
+        cm[w] = mont_mul(T[(size_t)w * L1 + r].w, kt.r2[r], q, qi);  // c 2^64 mod q
     for (int idx = threadIdx.x; idx < rows * kSymK; idx += blockDim.x) {
         const int i = lo0 + (int)j0 + idx / kSymK;
         X[idx] = (i >= 0 && i < (int)M) ? in[(size_t)i * item + col + idx % kSymK] : 0;
     }
     __syncthreads();
     const int k = threadIdx.x % kSymK, part = threadIdx.x / kSymK;
-    const bool lazy = (uint64_t)(W / 2 + 2) * 2 * q < (1ull << 63);
+    const uint64_t *Xk = X + k;
     const float qinv = qinv_est(q);
     constexpr int per = kSymJT / kSymSplit;
-    for (int jj = part * per; jj < (part + 1) * per; ++jj) {
-        const uint32_t j = j0 + jj;
-        if (j >= J) break;
-        const uint64_t acc = lazy ? lincomb_sym_row<true>(X + k, jj, (int)W, T, L1, r, q)
-                                  : lincomb_sym_row<false>(X + k, jj, (int)W, T, L1, r, q);
-        out[(size_t)j * item + col + k] = reduce_est(acc, q, qinv);
+    const int half = (int)W / 2;
+    for (int jb = part * per; jb < (part + 1) * per; jb += kSymJB) {
+        if (j0 + jb >= J) break;
+        // lo[i] = X[jb + i + w], hi[i] = X[jb + i + W - 1 - w] at tap w
+        uint64_t lo[kSymJB], hi[kSymJB];
+        U128 acc[kSymJB];
+#pragma unroll
+        for (int i = 0; i < kSymJB; ++i) {
+            lo[i] = Xk[(jb + i) * kSymK];
+            hi[i] = Xk[(jb + i + (int)W - 1) * kSymK];
+            acc[i] = U128{0, 0};
+        }
+        for (int w = 0; w < half; ++w) {
+            const uint64_t c = cm[w];
+#pragma unroll
+            for (int i = 0; i < kSymJB; ++i) mac128(acc[i], lo[i] + hi[i], c);  // (< 2q) x (< q)
+#pragma unroll
+            for (int i = 0; i < kSymJB - 1; ++i) {
+                lo[i] = lo[i + 1];
+                hi[kSymJB - 1 - i] = hi[kSymJB - 2 - i];
+            }
+            lo[kSymJB - 1] = Xk[(jb + kSymJB + w) * kSymK];
+            hi[0] = Xk[(jb + (int)W - 2 - w) * kSymK];
+        }
+        if (W & 1) {
+            // after the loop lo[i] = X[jb + i + W/2]: the middle tap
+            const uint64_t c = cm[half];
+#pragma unroll
+            for (int i = 0; i < kSymJB; ++i) mac128(acc[i], lo[i], c);
+        }
+#pragma unroll
+        for (int i = 0; i < kSymJB; ++i) {
+            const uint32_t j = j0 + jb + i;
+            if (j >= J) break;
+            // acc < (W/2 + 1) 2q^2 (<= 65 terms): hi < 2^17 q, reduced below q so that the
+            // Montgomery reduction's input is < q 2^64 (subtracting multiples of q 2^64 does
+            // not change the result mod q)
+            U128 x = acc[i];
+            x.hi = reduce_est(x.hi, q, qinv);
+            out[(size_t)j * item + col + k] = redc(x, q, qi);
+        }
     }
 }
 
@@ -888,16 +896,8 @@ static RSArgs rs_args(Ctx &c, uint32_t level)
     RSArgs a;
     a.qlinv = (const TwPair *)c.bconv_ptr(c.off_rs) + (size_t)level * (c.L + 1);
     a.h = (const uint64_t *)c.bconv_ptr(c.off_rs_h) + (size_t)level * (c.L + 1);
-    a.recip = (const uint64_t *)c.bconv_ptr(c.off_recip);
     a.level = level;
     return a;
-}
-
-void launch_rescale_prep(Ctx &c, uint64_t *v, const uint64_t *t, uint32_t level, uint32_t B)
-{
-    ProfScope ps(c, "rescale_prep", 8.0 * (2.0 + 2.0 * level) * c.n * B);
-    k_rescale_prep<<<grid3(c.n, 2 * level, B), kTB, 0, c.stream>>>(v, t, c.kt, rs_args(c, level));
-    LAUNCH_CHECK(c);
 }
 
 void launch_rescale_final(Ctx &c, uint64_t *out, const uint64_t *a, size_t as, const uint64_t *v, uint32_t level,
@@ -978,7 +978,7 @@ void launch_lincomb_mat(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, u
 void launch_lincomb_sym(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, uint32_t J, uint32_t W, int lo0,
                         const TwPair *T, uint32_t level)
 {
-    const size_t smem = sizeof(uint64_t) * (kSymJT + W - 1) * kSymK;
+    const size_t smem = sizeof(uint64_t) * ((kSymJT + W - 1) * kSymK + W / 2 + 1);
     MMFHE_REQUIRE(smem <= 200 * 1024, MMFHE_E_SHAPE, "FIR too long for the staged window");
     static bool attr = false;
     if (!attr) {
