@@ -90,12 +90,18 @@ struct PrimeMap {
 // Optional source of the forward NTT's col pass: row r reads
 // x + (r / period) * xs + src[r % period] * N and reduces it into [0, 2q) on load.
 // ModUp of single-limb digits (alpha = 1) is exactly y = x_j mod q_t,
-// so the base conversion fuses into the transform's first HBM read.
+// so the base conversion fuses into the transform's first HBM read.  With sub != nullptr
+// the loaded word is fully reduced and sub[p] (p = the row's prime index) is subtracted
+// mod q: the rescale's ([t]_{q_i} - [h]_{q_i}) mod q_i.
 struct ColSrc {
-    const uint64_t *x;  // nullptr: the pass transforms its own rows
-    size_t xs;          // item stride of x (words)
-    uint32_t period;    // == the PrimeMap period
+    const uint64_t *x;    // nullptr: the pass transforms its own rows
+    size_t xs;            // item stride of x (words)
+    uint32_t period;      // == the PrimeMap period
+    const uint64_t *sub;  // optional per-prime subtrahend (canonical), indexed by prime
     uint8_t src[kMapCap];
+    // bit r % period set: the source words are canonical residues of a prime q_s < 2q for the
+    // row's prime q, hence already < 2q: the load skips the reduction (sub == nullptr only)
+    uint32_t below2q[kMapCap / 32];
 };
 
 // Optional source of the inverse NTT's row pass (its first pass): output row r reads
@@ -109,6 +115,22 @@ struct InvSrc {
     uint32_t per;       // rows per item
     uint32_t g;         // Galois element (odd, < 2N); 1 = identity
     uint32_t add_half;  // 1: the col pass adds floor(q/2) mod q to every output (rescale's rounding offset)
+};
+
+// Optional epilogue of the forward NTT's row pass (its last pass): instead of storing the
+// transform v of row r = (item b, poly, limb i) (rows per item = 2 * per), it stores
+//   out[b os + poly ops + i N] = (X[b xs + poly xps + i N] - v) mul[i] mod q_i
+//                               (+ add0[b as + i N + perm_g0(k)] + add2[b as + i N + k] on poly 0,
+//                                + add1[b as + i N + k] on poly 1),
+// which is ModDown's final step (X = accQ, mul = P^{-1}) and the rescale's (X = a,
+// mul = q_l^{-1}): the transform's output never goes to HBM.
+struct RowEpi {
+    uint64_t *out;                       // nullptr: no epilogue
+    const uint64_t *X;
+    const TwPair *mul;                   // [per] Shoup pairs, indexed by i
+    const uint64_t *add0, *add1, *add2;  // each may be null
+    size_t os, ops, xs, xps, as;
+    uint32_t per, g0;
 };
 
 inline PrimeMap make_map(const std::vector<uint32_t> &v)

@@ -210,7 +210,10 @@ class ProfScope {
 
 // ------------------------------------------------------------------ kernels (launchers)
 // src: optional fused source of the col pass (ModUp of single-limb digits), see ColSrc
-void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const ColSrc *src = nullptr);
+// epi: optional fused epilogue of the row pass (ModDown / rescale final step), see RowEpi;
+// with epi the transform itself is not stored (d is scratch for the col pass)
+void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const ColSrc *src = nullptr,
+                 const RowEpi *epi = nullptr);
 // src: optional out-of-place / automorphism-permuted source of the row pass, see InvSrc
 void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const InvSrc *src = nullptr);
 

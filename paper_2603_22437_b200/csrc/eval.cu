@@ -368,8 +368,9 @@ DCt ev_lincomb_mat(Ctx &c, const DCt &in, uint32_t J, uint32_t W, int lo0, int l
         std::vector<TwPair> tab(coef.size() * (l + 1));
         for (size_t t = 0; t < coef.size(); ++t)
             for (uint32_t i = 0; i <= l; ++i) {
-                uint64_t v = encode_scalar_mod(coef[t], ql, c.primes[i]);
-                tab[t * (l + 1) + i] = {v, host::shoup(v, c.primes[i])};
+                // (value, Montgomery form): the lincomb kernels multiply-accumulate in 128 bits
+                const uint64_t v = encode_scalar_mod(coef[t], ql, c.primes[i]);
+                tab[t * (l + 1) + i] = {v, host::to_mont(v, c.primes[i])};
             }
         DBuf b((tab.size() * sizeof(TwPair) + 7) / 8, c.stream);
         CUDA_CHECK(cudaMemcpyAsync(b.get(), tab.data(), tab.size() * sizeof(TwPair), cudaMemcpyHostToDevice,
@@ -441,7 +442,11 @@ ModUpOut ks_modup(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t
         src.period = (uint32_t)m.T;
         size_t t = 0;
         for (const auto &p : plans)
-            for (uint32_t i = 0; i < p.n_tgt; ++i) src.src[t++] = (uint8_t)p.lo;
+            for (uint32_t i = 0; i < p.n_tgt; ++i) {
+                // x_j < q_j < 2 q_t: already a valid NTT input, no reduction on load
+                if (c.primes[p.lo] < 2 * c.primes[m.rowmap[t]]) src.below2q[t >> 5] |= 1u << (t & 31);
+                src.src[t++] = (uint8_t)p.lo;
+            }
         ntt_forward(c, m.y.get(), (uint32_t)(B * m.T), make_map(m.rowmap), &src);
     } else {
         launch_modup_bconv(c, m.y.get(), m.T * N, xc.get(), lw, l, m.off, B);
@@ -466,6 +471,22 @@ void ks_ip_moddown(Ctx &c, const uint64_t *x_ntt, size_t xs, const uint64_t *y, 
     std::vector<uint32_t> pm;
     for (uint32_t k = 0; k < c.K; ++k) pm.push_back(c.L + 1 + k);
     ntt_inverse(c, accP.get(), B * 2 * c.K, make_map(pm));
+    // ModDown's final step (accQ - w) P^{-1} + addends is the epilogue of w's forward NTT
+    // row pass: w never goes to HBM
+    RowEpi ep{};
+    ep.out = out;
+    ep.X = accQ.get();
+    ep.mul = (const TwPair *)c.bconv_ptr(c.off_pd_pinv);
+    ep.add0 = add0;
+    ep.add1 = add1;
+    ep.add2 = add2;
+    ep.os = os;
+    ep.ops = lw;
+    ep.xs = 2 * lw;
+    ep.xps = lw;
+    ep.as = as;
+    ep.per = l + 1;
+    ep.g0 = g0;
     DBuf w(B * 2 * lw, c.stream);
     if (c.K == 1 && l + 1 <= (uint32_t)kMapCap) {
         // one special prime: BConv_{P->Q} is w_i = accP mod q_i, fused into the NTT's first read
@@ -473,12 +494,13 @@ void ks_ip_moddown(Ctx &c, const uint64_t *x_ntt, size_t xs, const uint64_t *y, 
         src.x = accP.get();
         src.xs = N;  // one P row per (item, poly)
         src.period = l + 1;
-        ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l), &src);
+        for (uint32_t i = 0; i <= l; ++i)
+            if (c.primes[c.L + 1] < 2 * c.primes[i]) src.below2q[i >> 5] |= 1u << (i & 31);
+        ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l), &src, &ep);
     } else {
         launch_moddown_bconv(c, w.get(), accP.get(), l, B);
-        ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l));
+        ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l), nullptr, &ep);
     }
-    launch_moddown_final(c, out, os, accQ.get(), w.get(), add0, add1, as, l, B, g0, add2);
 }
 }  // namespace
 
@@ -581,25 +603,35 @@ DCt ev_rescale(Ctx &c, const DCt &a)
     DBuf t(2 * N * B, c.stream);
     const InvSrc src{a.data() + (size_t)l * N, a.item_words(), a.poly_words(), 2, 1, 1};
     ntt_inverse(c, t.get(), 2 * B, make_map({l}), &src);
-    // v_i = NTT_{q_i}([t]_{q_i}) for i < l: the reduction mod q_i is the forward NTT's fused
-    // first read (row (poly, i) reads t's poly row); [h]_{q_i} is subtracted in
-    // rescale_final (the NTT of a constant polynomial is that constant in every slot)
+    // v_i = NTT_{q_i}(([t]_{q_i} - [h]_{q_i}) mod q_i) for i < l: reduction and subtraction
+    // are the forward NTT's fused first read (row (poly, i) reads t's poly row)
     DBuf v((size_t)2 * l * N * B, c.stream);
+    DCt r = make_ct(c, l - 1, 2, a.n_slots, a.scale / (double)c.primes[l], B);
     {
         std::vector<uint32_t> pm(2 * l);
         ColSrc cs{};
         cs.x = t.get();
         cs.xs = 2 * N;
         cs.period = 2 * l;
+        cs.sub = (const uint64_t *)c.bconv_ptr(c.off_rs_h) + (size_t)l * (c.L + 1);  // [h]_{q_i}, h = floor(q_l/2)
         for (uint32_t r = 0; r < 2 * l; ++r) {
             pm[r] = r % l;
             cs.src[r] = (uint8_t)(r / l);
         }
         MMFHE_REQUIRE(2 * l <= (uint32_t)kMapCap, MMFHE_E_PARAMS, "too many limbs for the fused rescale");
-        ntt_forward(c, v.get(), 2 * l * B, make_map(pm), &cs);
+        // final step out_i = (a_i - v_i) q_l^{-1} as the epilogue of v's row pass
+        RowEpi ep{};
+        ep.out = r.data();
+        ep.X = a.data();
+        ep.mul = (const TwPair *)c.bconv_ptr(c.off_rs) + (size_t)l * (c.L + 1);
+        ep.os = r.item_words();
+        ep.ops = r.poly_words();
+        ep.xs = a.item_words();
+        ep.xps = a.poly_words();
+        ep.per = l;
+        ep.g0 = 1;
+        ntt_forward(c, v.get(), 2 * l * B, make_map(pm), &cs, &ep);
     }
-    DCt r = make_ct(c, l - 1, 2, a.n_slots, a.scale / (double)c.primes[l], B);
-    launch_rescale_final(c, r.data(), a.data(), a.item_words(), v.get(), l, B);
     return r;
 }
 

@@ -369,7 +369,7 @@ __device__ __forceinline__ void inv_bfly(uint64_t (&v)[Gm::E], int r, int ktr, i
 // Round widths: the first (top) round takes LOGS - (R-1)*ELOG bits, the others ELOG.
 template <int LOGS, int OTHER, bool COL>
 __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm, RowMap rm,
-                                                                      ColSrc cs)
+                                                                      ColSrc cs, RowEpi ep)
 {
     using Gm = Geo<LOGS, OTHER, COL>;
     constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, T = Gm::T, G = Gm::G, R = Gm::R;
@@ -397,10 +397,22 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
         } else if (r == 0 && cs.x != nullptr) {
             // fused ModUp (alpha = 1): this row is x_j mod q of a source limb x_j
             const uint64_t *src = cs.x + (row / cs.period) * cs.xs + ((size_t)cs.src[row % cs.period] << LOGN);
+            // (a fused BConv row of a single-limb digit: y = x_j mod q_t, reduced into [0, 2q))
             const uint64_t *col = src + gi + ((size_t)ktr << OTHER);
-            const uint64_t rc = kt.recip[p];
+            const uint32_t rr = row % cs.period;
+            if ((cs.below2q[rr >> 5] >> (rr & 31)) & 1) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) v[e] = shoup_lazy(col[(size_t)kmap(ELOG, lo, w, 0, e) << OTHER], 1, rc, q);
+                for (int e = 0; e < E; ++e) v[e] = col[(size_t)kmap(ELOG, lo, w, 0, e) << OTHER];
+            } else {
+                const uint64_t rc = kt.recip[p];
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = shoup_lazy(col[(size_t)kmap(ELOG, lo, w, 0, e) << OTHER], 1, rc, q);
+            }
+            if (cs.sub != nullptr) {
+                const uint64_t h = cs.sub[p];
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = sub_mod(csub64(v[e], q), h, q);
+            }
         } else if (r == 0) {
             const uint64_t *col = a + gi + ((size_t)ktr << OTHER);
 #pragma unroll
@@ -411,7 +423,44 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
             for (int e = 0; e < E; ++e) v[e] = b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))];
         }
         fwd_bfly<Gm, LOGS>(v, r, ktr, COL ? 0 : gi, tw, q);
-        if (r == R - 1 && !COL) {
+        if (r == R - 1 && !COL && ep.out != nullptr) {
+            // fused epilogue (RowEpi): (X - v) mul + addends, written to ep.out
+            constexpr int LOL = FwdGeo<Gm, LOGS>::lo(R - 1), WL = FwdGeo<Gm, LOGS>::w(R - 1);
+            const float qinv = qinv_est(q);
+            const size_t b = row / (2 * ep.per);
+            const uint32_t rr = (uint32_t)(row % (2 * ep.per)), poly = rr / ep.per, i = rr % ep.per;
+            const uint32_t k0 = ((uint32_t)gi << LOGS) | (uint32_t)ktr;  // this thread's first word
+            uint64_t x[E];
+            ld_pattern<ELOG, LOL, WL>(ep.X + b * ep.xs + poly * ep.xps + ((size_t)i << LOGN), k0, x);
+            const TwPair m = ep.mul[i];
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = shoup(x[e] + q - reduce_est(v[e], q, qinv), m.w, m.wp, q);
+            const size_t ao = b * ep.as + ((size_t)i << LOGN);
+            if (poly == 0) {
+                if (ep.add0) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        const uint32_t j = k0 + (uint32_t)kmap(ELOG, LOL, WL, 0, e);
+                        uint32_t src = j;
+                        if (ep.g0 != 1) {
+                            const uint32_t ex = ((2u * (__brev(j) >> (32 - LOGN)) + 1u) * ep.g0) & ((2u << LOGN) - 1u);
+                            src = __brev((ex - 1u) >> 1) >> (32 - LOGN);
+                        }
+                        v[e] = add_mod(v[e], ep.add0[ao + src], q);
+                    }
+                }
+                if (ep.add2) {
+                    ld_pattern<ELOG, LOL, WL>(ep.add2 + ao, k0, x);
+#pragma unroll
+                    for (int e = 0; e < E; ++e) v[e] = add_mod(v[e], x[e], q);
+                }
+            } else if (ep.add1) {
+                ld_pattern<ELOG, LOL, WL>(ep.add1 + ao, k0, x);
+#pragma unroll
+                for (int e = 0; e < E; ++e) v[e] = add_mod(v[e], x[e], q);
+            }
+            st_pattern<ELOG, LOL, WL>(ep.out + b * ep.os + poly * ep.ops + ((size_t)i << LOGN), k0, v);
+        } else if (r == R - 1 && !COL) {
             // row pass: full reduction (< 16q -> [0, q)), stored as the last round's runs
             // (8 consecutive words per thread: two 32-byte stores)
             const float qinv = qinv_est(q);
@@ -513,7 +562,7 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
 
 template <bool FWD, int LOGS, int OTHER, bool COL>
 void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm, const ColSrc *cs, const InvSrc *is,
-                cudaStream_t s)
+                const RowEpi *ep, cudaStream_t s)
 {
     using Gm = Geo<LOGS, OTHER, COL>;
     static_assert(Gm::SMEM <= 48 * 1024, "NTT pass exceeds the default dynamic shared memory");
@@ -532,7 +581,8 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
     (void)attr;
     auto go = [&](dim3 grid, uint64_t *dd, RowMap rm, const ColSrc &src) {
         if constexpr (FWD)
-            ntt_fwd_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm, src);
+            ntt_fwd_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm, src,
+                                                                              (!COL && ep) ? *ep : RowEpi{});
         else
             ntt_inv_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(
                 dd, kt, pm, rm, !is ? InvSrc{} : !COL ? *is : InvSrc{nullptr, 0, 0, 1, 1, is->add_half});
@@ -563,14 +613,14 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
 // log N = L1 + L2, L1 = floor(log N / 2): col pass <L1, L2>, row pass <L2, L1>.
 template <bool FWD, bool COL>
 void launch_pass(uint32_t log_n, uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &pm, const ColSrc *cs,
-                 const InvSrc *is, cudaStream_t s)
+                 const InvSrc *is, const RowEpi *ep, cudaStream_t s)
 {
 #define MMFHE_NTT_CASE(LN, A, B)                                    \
     case LN:                                                        \
         if (COL)                                                    \
-            launch_one<FWD, A, B, true>(d, rows, kt, pm, cs, is, s);        \
+            launch_one<FWD, A, B, true>(d, rows, kt, pm, cs, is, nullptr, s);  \
         else                                                        \
-            launch_one<FWD, B, A, false>(d, rows, kt, pm, nullptr, is, s);  \
+            launch_one<FWD, B, A, false>(d, rows, kt, pm, nullptr, is, ep, s); \
         break;
     switch (log_n) {
         MMFHE_NTT_CASE(4, 2, 2)
@@ -600,7 +650,7 @@ void split(uint32_t log_n, int &L1, int &L2)
 
 }  // namespace
 
-void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const ColSrc *src)
+void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const ColSrc *src, const RowEpi *epi)
 {
     if (!rows) return;
     MMFHE_REQUIRE(!src || src->period == pm.period, MMFHE_E_LAYOUT, "NTT source map period");
@@ -609,11 +659,17 @@ void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const C
     const double bytes = 16.0 * rows * c.n;  // one read + one write of every word per pass
     {
         ProfScope ps(c, "ntt_fwd_col", bytes, 0.5 * rows * c.n * L1);
-        launch_pass<true, true>(c.log_n, d, rows, c.kt, pm, src, nullptr, c.stream);
+        launch_pass<true, true>(c.log_n, d, rows, c.kt, pm, src, nullptr, nullptr, c.stream);
     }
     {
-        ProfScope ps(c, "ntt_fwd_row", bytes, 0.5 * rows * c.n * L2);
-        launch_pass<true, false>(c.log_n, d, rows, c.kt, pm, nullptr, nullptr, c.stream);
+        // with the epilogue: + X read, out written, addends read (instead of the v write)
+        const double ebytes = !epi ? 0.0
+                                   : 8.0 * rows * c.n *
+                                         (1.0 + (epi->add0 ? 0.5 : 0.0) + (epi->add1 ? 0.5 : 0.0) +
+                                          (epi->add2 ? 0.5 : 0.0));
+        MMFHE_REQUIRE(!epi || (epi->per >= 1 && rows % (2 * epi->per) == 0), MMFHE_E_LAYOUT, "NTT epilogue rows");
+        ProfScope ps(c, epi ? "ntt_fwd_row_epi" : "ntt_fwd_row", bytes + ebytes, 0.5 * rows * c.n * L2);
+        launch_pass<true, false>(c.log_n, d, rows, c.kt, pm, nullptr, nullptr, epi, c.stream);
     }
     c.launches += 2;
     CUDA_CHECK(cudaGetLastError());
@@ -629,11 +685,11 @@ void ntt_inverse(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const I
         ProfScope ps(c, "ntt_inv_row", bytes, 0.5 * rows * c.n * L2);
         MMFHE_REQUIRE(!src || ((src->x || src->g == 1) && src->per >= 1 && (src->g & 1) && src->g < 2 * c.n),
                       MMFHE_E_LAYOUT, "INTT source");
-        launch_pass<false, false>(c.log_n, d, rows, c.kt, pm, nullptr, src, c.stream);
+        launch_pass<false, false>(c.log_n, d, rows, c.kt, pm, nullptr, src, nullptr, c.stream);
     }
     {
         ProfScope ps(c, "ntt_inv_col", bytes, 0.5 * rows * c.n * L1);
-        launch_pass<false, true>(c.log_n, d, rows, c.kt, pm, nullptr, src, c.stream);
+        launch_pass<false, true>(c.log_n, d, rows, c.kt, pm, nullptr, src, nullptr, c.stream);
     }
     c.launches += 2;
     CUDA_CHECK(cudaGetLastError());

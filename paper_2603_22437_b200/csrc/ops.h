@@ -42,8 +42,8 @@ void launch_moddown_final(Ctx &c, uint64_t *out, size_t os, const uint64_t *accQ
                           const uint64_t *add0, const uint64_t *add1, size_t as, uint32_t level, uint32_t B,
                           uint32_t g0 = 1, const uint64_t *add2 = nullptr);
 
-// ---- rescale (batched): v [B][2][l][N] = NTT_{q_i}([t]_{q_i}), t = [a_l + floor(q_l/2)]_{q_l}
-// out [B][2][l][N] = (a_i + [floor(q_l/2)]_{q_i} - v_i) * q_l^{-1}; a item stride as.
+// ---- rescale (batched): v [B][2][l][N] = NTT_{q_i}([t]_{q_i} - [h]_{q_i}), t = [a_l + h]_{q_l}, h = floor(q_l/2)
+// out [B][2][l][N] = (a_i - v_i) * q_l^{-1}; a item stride as.
 void launch_rescale_final(Ctx &c, uint64_t *out, const uint64_t *a, size_t as, const uint64_t *v, uint32_t level,
                           uint32_t B);
 
@@ -61,10 +61,10 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
                      size_t os, uint32_t level, uint32_t B);
 // Scalar "modular matrix product" over a batch of 2-poly cts (CK10):
 //   out[j] = sum_{w < W} C[j][w] in[lo_j + w],  j < J,  lo_j = lo0 + j*lo_step,
-// C given as Shoup pairs [J][W][l+1]; inputs outside [0, M) contribute nothing.
+// C given as (value, Montgomery form) pairs [J][W][l+1]; inputs outside [0, M) contribute nothing.
 void launch_lincomb_mat(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, uint32_t J, uint32_t W, int lo0,
                         int lo_step, const TwPair *C, uint32_t level);
-// symmetric Toeplitz rows (every row the same taps, c_w == c_{W-1-w}); T: TwPair[W][level+1]
+// symmetric Toeplitz rows (every row the same taps, c_w == c_{W-1-w}); T: (value, Montgomery form) pairs [W][level+1]
 void launch_lincomb_sym(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, uint32_t J, uint32_t W, int lo0,
                         const TwPair *T, uint32_t level);
 // out = sum_b in_b over a batch of B items of `words` words each (rows of level l).

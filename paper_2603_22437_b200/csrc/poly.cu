@@ -403,7 +403,7 @@ struct RSArgs {
     uint32_t level;
 };
 
-// out_i = (a_i + [h]_{q_i} - v_i) q_l^{-1} mod q_i, v_i = NTT_{q_i}([t]_{q_i}),
+// out_i = (a_i - v_i) q_l^{-1} mod q_i, v_i = NTT_{q_i}([t]_{q_i} - [h]_{q_i}),
 // t = [a_l + h]_{q_l}, h = floor(q_l / 2) (SURVEY §8(c)-5 rescale, round half up); grid.z = item
 __global__ void k_rescale_final(uint64_t *__restrict__ out, const uint64_t *__restrict__ in, size_t is,
                                 const uint64_t *__restrict__ v, KTables kt, RSArgs a)
@@ -416,7 +416,7 @@ __global__ void k_rescale_final(uint64_t *__restrict__ out, const uint64_t *__re
     const TwPair w = a.qlinv[i];
     const uint64_t x = in[(size_t)b * is + ((size_t)poly * (a.level + 1) + i) * kt.n + k];
     const size_t o = ((size_t)b * 2 * a.level + r) * kt.n + k;
-    out[o] = shoup(x + a.h[i] + q - v[o], w.w, w.wp, q);  // < 3q
+    out[o] = shoup(x + q - v[o], w.w, w.wp, q);
 }
 
 // ------------------------------------------------------------------ fused sums
@@ -554,41 +554,13 @@ __global__ void __launch_bounds__(kTB) k_diag_mac(DiagMacArgs a, KTables kt, uin
     }
 }
 
-constexpr int kJG = 8;  // outputs per thread in the modular matrix product
+constexpr int kJG = 4;  // outputs per thread in the modular matrix product (2 x 128-bit accumulators each)
 
-// One thread's term loop of k_lincomb_mat.  LAZY: every term shoup_lazy() < 2q is added
-// without correction (the caller guarantees (W + kJG) 2q < 2^63, true for every 40/50-bit
-// scaling prime); otherwise (the 60-bit q_0) each partial sum is kept in [0, 2q).
-template <bool LAZY>
-__device__ __forceinline__ void lincomb_terms(uint64_t (&a0)[kJG], uint64_t (&a1)[kJG], const uint64_t *__restrict__ in,
-                                              size_t item, size_t ps, size_t off, int ilo, int ihi, uint32_t j0,
-                                              uint32_t jn, uint32_t W, int lo0, int lo_step,
-                                              const TwPair *__restrict__ C, uint32_t L1, uint32_t r, uint64_t q)
-{
-    const uint64_t q2 = 2 * q;
-    for (int i = ilo; i < ihi; ++i) {
-        const uint64_t x0 = in[(size_t)i * item + off], x1 = in[(size_t)i * item + ps + off];
-#pragma unroll
-        for (int jj = 0; jj < kJG; ++jj) {
-            if (jj < (int)jn) {
-                const int w = i - (lo0 + (int)(j0 + jj) * lo_step);
-                if (w >= 0 && w < (int)W) {
-                    const TwPair c = C[((size_t)(j0 + jj) * W + w) * L1 + r];
-                    uint64_t s0 = a0[jj] + shoup_lazy(x0, c.w, c.wp, q);
-                    uint64_t s1 = a1[jj] + shoup_lazy(x1, c.w, c.wp, q);
-                    if (!LAZY) {
-                        s0 = s0 >= q2 ? s0 - q2 : s0;
-                        s1 = s1 >= q2 ? s1 - q2 : s1;
-                    }
-                    a0[jj] = s0;
-                    a1[jj] = s1;
-                }
-            }
-        }
-    }
-}
-
-// out[j] = sum_w C[j][w] in[lo_j + w] for j in this CTA's group of kJG outputs.
+// out[j] = sum_w C[j][w] in[lo_j + w] for j in this CTA's group of kJG outputs.  Each
+// term is one 64x64->128 multiply-accumulate per poly with the coefficient in Montgomery
+// form (C[.].wp = c 2^64 mod q); every accumulator is reduced once at the end (hi word
+// brought below q, then one Montgomery reduction).  acc < W q^2, so hi < W q / 16 < 2^17 q
+// for W <= 8192 (checked by the launcher).
 __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out, const uint64_t *__restrict__ in,
                                                      uint32_t M, uint32_t J, uint32_t W, int lo0, int lo_step,
                                                      const TwPair *__restrict__ C, KTables kt, uint32_t level)
@@ -598,7 +570,7 @@ __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out,
     const uint32_t r = blockIdx.y;
     const uint32_t j0 = blockIdx.z * kJG;
     const uint32_t jn = min((uint32_t)kJG, J - j0);
-    const uint64_t q = kt.q[r];
+    const uint64_t q = kt.q[r], qi = kt.qinv_neg[r];
     const uint32_t L1 = level + 1;
     const size_t ps = (size_t)L1 * kt.n, item = 2 * ps;
     const size_t off = (size_t)r * kt.n + k;
@@ -610,20 +582,33 @@ __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out,
     }
     ilo = max(ilo, 0);
     ihi = min(ihi, (int)M);
-    uint64_t a0[kJG], a1[kJG];
+    U128 a0[kJG], a1[kJG];
 #pragma unroll
-    for (int jj = 0; jj < kJG; ++jj) a0[jj] = a1[jj] = 0;
-    // per-CTA uniform: one limb per blockIdx.y
-    if ((uint64_t)(W + kJG) * 2 * q < (1ull << 63) && W + kJG < (1u << 16))
-        lincomb_terms<true>(a0, a1, in, item, ps, off, ilo, ihi, j0, jn, W, lo0, lo_step, C, L1, r, q);
-    else
-        lincomb_terms<false>(a0, a1, in, item, ps, off, ilo, ihi, j0, jn, W, lo0, lo_step, C, L1, r, q);
+    for (int jj = 0; jj < kJG; ++jj) a0[jj] = a1[jj] = U128{0, 0};
+    for (int i = ilo; i < ihi; ++i) {
+        const uint64_t x0 = in[(size_t)i * item + off], x1 = in[(size_t)i * item + ps + off];
+#pragma unroll
+        for (int jj = 0; jj < kJG; ++jj) {
+            if (jj < (int)jn) {
+                const int w = i - (lo0 + (int)(j0 + jj) * lo_step);
+                if (w >= 0 && w < (int)W) {
+                    const uint64_t c = C[((size_t)(j0 + jj) * W + w) * L1 + r].wp;
+                    mac128(a0[jj], x0, c);
+                    mac128(a1[jj], x1, c);
+                }
+            }
+        }
+    }
     const float qinv = qinv_est(q);
 #pragma unroll
     for (int jj = 0; jj < kJG; ++jj) {
         if (jj < (int)jn) {
-            out[(size_t)(j0 + jj) * item + off] = reduce_est(a0[jj], q, qinv);
-            out[(size_t)(j0 + jj) * item + ps + off] = reduce_est(a1[jj], q, qinv);
+            U128 x = a0[jj];
+            x.hi = reduce_est(x.hi, q, qinv);
+            out[(size_t)(j0 + jj) * item + off] = redc(x, q, qi);
+            x = a1[jj];
+            x.hi = reduce_est(x.hi, q, qinv);
+            out[(size_t)(j0 + jj) * item + ps + off] = redc(x, q, qi);
         }
     }
 }
@@ -633,7 +618,7 @@ __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out,
 // (checked on the host), so out[j] = sum_{w < W/2} c_w (x_a + x_b) + c_mid x_mid exactly
 // (mod q): half the modular products of k_lincomb_mat.  A CTA stages the input window of
 // its kSymJT outputs for kSymK coefficients of one (poly, limb) row in shared memory
-// (zeros outside [0, M)) together with the taps in Montgomery form; each thread owns one
+// (zeros outside [0, M)) together with the taps (Montgomery form); each thread owns one
 // coefficient and kSymJT / kSymSplit outputs, computed kSymJB at a time: the kSymJB
 // outputs' input pairs slide along the window (two shared-memory reads per tap for all
 // kSymJB outputs) and each tap is one 64x64->128 multiply-accumulate per output, reduced
@@ -655,8 +640,7 @@ __global__ void __launch_bounds__(kSymK *kSymSplit) k_lincomb_sym(uint64_t *__re
     const size_t col = (size_t)poly * ps + (size_t)r * kt.n + k0;
     const int rows = kSymJT + (int)W - 1;
     uint64_t *cm = X + (size_t)rows * kSymK;
-    for (int w = threadIdx.x; w <= (int)W / 2; w += blockDim.x)
-        cm[w] = mont_mul(T[(size_t)w * L1 + r].w, kt.r2[r], q, qi);  // c 2^64 mod q
+    for (int w = threadIdx.x; w <= (int)W / 2; w += blockDim.x) cm[w] = T[(size_t)w * L1 + r].wp;  // c 2^64 mod q
     for (int idx = threadIdx.x; idx < rows * kSymK; idx += blockDim.x) {
         const int i = lo0 + (int)j0 + idx / kSymK;
         X[idx] = (i >= 0 && i < (int)M) ? in[(size_t)i * item + col + idx % kSymK] : 0;
@@ -969,6 +953,7 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
 void launch_lincomb_mat(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, uint32_t J, uint32_t W, int lo0,
                         int lo_step, const TwPair *C, uint32_t level)
 {
+    MMFHE_REQUIRE(W <= 8192, MMFHE_E_SHAPE, "lincomb window too long");
     ProfScope ps(c, "lincomb_mat", 8.0 * 2.0 * (level + 1) * c.n * ((double)M + J));
     k_lincomb_mat<<<grid3(c.n, level + 1, (J + kJG - 1) / kJG), kTB, 0, c.stream>>>(out, in, M, J, W, lo0, lo_step,
                                                                                    C, c.kt, level);
