@@ -476,6 +476,24 @@ def extras_n16(args, m, torch, device, batch=8, reps=3):
         res[f"{name}_per_s"] = ops
         res[f"{name}_us"] = 1e6 / ops
         res[f"{name}_alg_gbs"] = ops * alg / 1e9
+    # integer roof: the key switch's algorithmic butterflies, 128-bit MACs and
+    # modular products against the butterfly / MAC / Shoup rates measured in this run
+    Lp, K, N, logn = L + 1, P.K, P.n, P.log_n
+    bn = N // 2 * logn
+    alphas = [min(P.alpha, Lp - j * P.alpha) for j in range(P.dnum())]
+    bfly = Lp * bn + sum(Lp + K - a for a in alphas) * bn + 2 * K * bn + 2 * Lp * bn
+    mac = sum(a * (Lp + K - a + 1) for a in alphas) * N + len(alphas) * 2 * (Lp + K) * N + 2 * K * (Lp + 1) * N
+    mm = 2 * Lp * N
+    peaks = {"bfly": ctx.microbench(4), "mac": ctx.microbench(2), "mm": ctx.microbench(3)}
+    t_int = bfly / peaks["bfly"] + mac / peaks["mac"] + mm / peaks["mm"]
+    for name, extra_mac in (("hrot", 0), ("hmult", 4 * Lp * N)):
+        t = t_int + extra_mac / peaks["mac"]
+        res[f"{name}_int_model_us"] = t * 1e6
+        res[f"{name}_int_frac"] = t * res[f"{name}_per_s"]
+    res["int_model"] = (f"per key switch: {bfly / 1e6:.1f} M butterflies + {mac / 1e6:.1f} M MAC128 + {mm / 1e6:.1f} M "
+                        f"modmul (SURVEY 8(d)); HMult adds 4L'N tensor MACs; peaks measured in this run: "
+                        f"{peaks['bfly'] / 1e9:.0f} G bfly/s, {peaks['mac'] / 1e9:.0f} G MAC/s, "
+                        f"{peaks['mm'] / 1e9:.0f} G modmul/s; int_frac = model time / measured time")
     res["config"] = "PS4: N=2^16, 20 Q + 7 P limbs, dnum 3, top level, batch of 8 distinct cts, one key, eval form"
     ctx.close()
     return res
