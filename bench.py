@@ -271,7 +271,7 @@ def run_gpu(args, rank, world, device):
     extras = {}
     if not args.no_extras:
         extras = extras_n16(args, m, torch, device)
-        for wl in ("C1", "C3", "C4"):
+        for wl in ("C1", "C3", "C4", "C5v"):
             try:
                 extras[wl] = bench_workload(wl, m, torch, device)
             except Exception as e:  # report, do not hide
@@ -288,7 +288,9 @@ def bench_workload(name, m, torch, device, steps=2, warmup=2):
     device-resident coefficient-form inputs, CUDA events on the library stream:
       C1: K1 energy, N=2^13 (PS1), R=64, F=32, 256 sessions per step (frames = sessions*F);
       C3: K3 Doppler DFT, N=2^15 (PS3), A=4 x R=32 x D=32, 32 frames per step, hoisted baby steps;
-      C4: gesture session, N=2^16 (PS4, entry level 19), F=100 frames + FC 4096->64->32->5."""
+      C4: gesture session, N=2^16 (PS4, entry level 19), F=100 frames + FC 4096->64->32->5;
+      C5v: one vital session of C5 at full depth, N=2^16 (PS4), R=64, F=200 @ 20 Hz: vitals_v1
+           (entry level 3) + vitals_v2 first order with VP+ in the cloud (entry level 9, depth 9)."""
     from synth import radar
     from synth.params import ps1, ps3, ps4
     stream = torch.cuda.current_stream(device)
@@ -302,16 +304,25 @@ def bench_workload(name, m, torch, device, steps=2, warmup=2):
         P = ps3()
         cfg = m.chain_cfg(A=4, R=32, D=32, n_slots=4096, frame_batch=32, hoist=1)
         chain, lvl, n_in, frames, info = "k3_doppler_dft", P.L, 64, 32, "32 frames, frame_batch 32, hoisted"
-    else:
+    elif name == "C4":
         P = ps4()
         cfg = m.chain_cfg(A=4, R=32, D=32, F=100, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8),
                           frame_batch=25, hoist=1)
         chain, lvl, n_in, frames, info = "gesture", 19, 200, 100, "F=100 frames, frame_batch 25, hoisted"
+    else:
+        P = ps4()
+        F, fs = 200, 20.0
+        cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2,
+                          bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
+                          frame_batch=50, vp_plus=1)
+        chain, lvl, n_in, frames, info = "vitals_v2", 9, 2 * F, F, "F=200 frames, frame_batch 50, VP+ in the cloud
+    # one step = these chain calls (C5v: V1 then V2 on the same session's frames)
+    plan = [("vitals_v1", 3, n_in), (chain, lvl, n_in)] if name == "C5v" else [(chain, lvl, n_in)]
     ctx = m.Context.from_params(P, device=device.index or 0, stream=stream.cuda_stream)
     basis = list(P.q) + list(P.p)
     key_shape = (P.dnum(), 2, len(basis))
     ctx.load_relin_key(uniform_dev(torch, gen, key_shape, basis, P.n, device))
-    for k in ctx.required_rotations(chain, cfg):
+    for k in sorted({k for ch, _, _ in plan for k in ctx.required_rotations(ch, cfg)}):
         ctx.load_galois_key(k, uniform_dev(torch, gen, key_shape, basis, P.n, device))
     fc_w = fc_b = None
     if chain == "gesture":
@@ -319,27 +330,36 @@ def bench_workload(name, m, torch, device, steps=2, warmup=2):
         Ws[-1] = np.vstack([Ws[-1], np.zeros((3, 32))])
         bs[-1] = np.concatenate([bs[-1], np.zeros(3)])
         fc_w, fc_b = Ws, bs
-    ctx.prepare_chain(chain, cfg, lvl, fc_w=fc_w, fc_b=fc_b)
+    taps = [radar.fir_taps(41, b, 20.0) for b in BANDS] if chain == "vitals_v2" else None
     scale = float(2 ** P.scale_bits)
-    data = uniform_dev(torch, gen, (n_in, 2, lvl + 1), list(P.q[: lvl + 1]), P.n, device)
-    ins = m.CtArray([m.Ct(data[i], lvl, scale, cfg.n_slots, P.log_n) for i in range(n_in)])
-    outs = m.CtArray([m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=device), lv, 0.0, 0, P.log_n)
-                      for lv in ctx.chain_plan(chain, cfg, lvl, n_in)])
+    runs = []
+    for ch, lv0, n in plan:
+        ctx.prepare_chain(ch, cfg, lv0, fc_w=fc_w, fc_b=fc_b, taps=taps if ch == "vitals_v2" else None)
+        data = uniform_dev(torch, gen, (n, 2, lv0 + 1), list(P.q[: lv0 + 1]), P.n, device)
+        ins = m.CtArray([m.Ct(data[i], lv0, scale, cfg.n_slots, P.log_n) for i in range(n)])
+        outs = m.CtArray([m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=device), lv, 0.0, 0,
+                               P.log_n) for lv in ctx.chain_plan(ch, cfg, lv0, n)])
+        runs.append((ch, ins, outs, data))
+
+    def step():
+        for ch, ins, outs, _ in runs:
+            ctx.eval_chain(ch, cfg, ins, outs)
+
     ctx.trace_enable(False)
     for _ in range(warmup):
-        ctx.eval_chain(chain, cfg, ins, outs)
+        step()
     torch.cuda.synchronize(device)
     l0 = ctx.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(steps):
-        ctx.eval_chain(chain, cfg, ins, outs)
+        step()
     e1.record(stream)
     torch.cuda.synchronize(device)
     ms = e0.elapsed_time(e1) / steps
     launches = (ctx.launch_count() - l0) // steps
     ctx.profile_enable(True)
-    ctx.eval_chain(chain, cfg, ins, outs)
+    step()
     prof = ctx.profile()
     ctx.profile_enable(False)
     top = sorted(prof.items(), key=lambda kv: -kv[1][1])[:6]
@@ -347,9 +367,10 @@ def bench_workload(name, m, torch, device, steps=2, warmup=2):
            "gpu_launches_per_step": launches,
            "kernel_ms_top": {k: round(v[1], 3) for k, v in top},
            "kernel_ms_total": round(sum(v[1] for v in prof.values()), 3),
-           "config": f"{chain} at N=2^{P.log_n} ({len(P.q)} Q + {len(P.p)} P limbs, entry level {lvl}), {info}"}
+           "config": f"{' + '.join(ch for ch, _, _ in plan)} at N=2^{P.log_n} ({len(P.q)} Q + {len(P.p)} P limbs, "
+                     f"entry level {' / '.join(str(lv) for _, lv, _ in plan)}), {info}"}
     ctx.close()
-    del data, ins, outs
+    del runs
     torch.cuda.empty_cache()
     return res
 
@@ -614,8 +635,8 @@ def roofline(prof, peaks, int_peaks):
     # write per launch / algorithmic bytes of that launch), applied to this run's launches
     tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "ncu_traffic.json")
     if os.path.exists(tpath):
-        tr = json.load(open(tpath))
-        if tr.get("kernel") == name:
+        tr = json.load(open(tpath)).get("kernels", {}).get(name)
+        if tr:
             out["traffic"] = tr["ratio"] * by / max(cnt, 1)
             out["traffic_source"] = (f"{tr['capture']}: {tr['dram_bytes']} B DRAM for {tr['alg_bytes']} B algorithmic "
                                      f"({tr['launch']}); ratio {tr['ratio']} x this run's bytes per launch")

@@ -115,6 +115,10 @@ typedef struct {
     uint32_t n_bins[4];    /* vital V2: narrowband DFT bins per band */
     uint32_t bins[4][64];  /* vital V2: bin indices k per band */
     double fs;             /* frame rate (Hz) */
+    uint32_t vp_plus;      /* vital V2: 1 = sharpen P_k^2 and weighted frequency average in the cloud
+                              (VP+): per band two outputs N_f = sum_k f_k P_k^2 and
+                              D_f = sum_k P_k^2 (f_k = k fs / (F-1) Hz; the client reads
+                              BPM = 60 N_f / D_f); depth +2.  0 = outputs P_k (client finishes) */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */

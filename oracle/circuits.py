@@ -53,6 +53,7 @@ class ChainCfg:
     bands: tuple = ((0.1, 0.6), (0.8, 2.5))   # RR, HR
     frame_batch: int = 0        # frames per op-major batch (0: all frames)
     hoist: int = 0              # 1: baby-step rotations of K3 / FC share one ModUp (hoisted HRot)
+    vp_plus: int = 0            # vital V2: 1 -> sharpen + weighted frequency average in the cloud
 
 
 def rot(v: np.ndarray, k: int) -> np.ndarray:
@@ -476,9 +477,21 @@ def vp_band_power(ev, ys, bins):
     return ev.relin_rescale_all([ev.tensor_sum([(a, a), (b, b)]) for a, b in zip(xr, xi)])
 
 
+def vp_weighted_average(ev, Pk, bins, fs, Fp):
+    """VP+ sharpen and weighted frequency average:
+    S_k = P_k^2 (HMult + relin + rescale), N_f = sum_k f_k S_k, D_f = sum_k S_k with
+    f_k = k fs / Fp Hz as scalar constants (every PMult rescaled); the client reads
+    BPM = 60 N_f / D_f.  Op-major: both sums, then both rescales."""
+    S = ev.square_rescale_all(Pk)
+    f = [float(k) * fs / Fp for k in bins]
+    lin = [ev.lincomb_scalar(S, f), ev.lincomb_scalar(S, [1.0] * len(S))]
+    return [ev.rescale(x) for x in lin]
+
+
 def vitals_v2(ev, re_list, im_list, taps_by_band, cfg):
     """Chain V2: K4 -> K5 -> K7 -> narrowband DFT -> |X|^2 per band (P:901-902);
-    returns {band index: [P_k ciphertexts]} (sharpen/average on the client, reading #4)."""
+    returns {band index: [P_k ciphertexts]} (sharpen/average on the client, reading #4),
+    or with cfg.vp_plus {band index: [N_f, D_f]} (VP+ in the cloud, the full-depth chain)."""
     I, Q = [], []
     for s, e in chunks(len(re_list), cfg.frame_batch):
         Ib, Qb = k4_soft_iq(ev, re_list[s:e], im_list[s:e], cfg)
@@ -491,6 +504,8 @@ def vitals_v2(ev, re_list, im_list, taps_by_band, cfg):
         ys = k7_taylor_phase(ev, If, Qf, cfg.taylor_order)
         bins = dsp.band_bins(len(ys), cfg.fs, cfg.bands[bi])
         out[bi] = vp_band_power(ev, ys, bins)
+        if cfg.vp_plus:
+            out[bi] = vp_weighted_average(ev, out[bi], bins, cfg.fs, len(ys))
     return out
 
 

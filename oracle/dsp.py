@@ -132,6 +132,13 @@ def narrowband_power(y: np.ndarray, bins) -> np.ndarray:
     return np.array(out)
 
 
+def weighted_average(P: np.ndarray, bins, fs: float, F_phase: int):
+    """VP+ sums: N_f = sum_k f_k P_k^2, D_f = sum_k P_k^2, f_k = k fs / F_phase."""
+    f = np.asarray(bins, dtype=np.float64) * fs / F_phase
+    w = np.asarray(P, dtype=np.float64) ** 2
+    return float(np.sum(f * w)), float(np.sum(w))
+
+
 def bpm_from_power(P: np.ndarray, bins, fs: float, F_phase: int) -> float:
     """Client: sharpen (P_k^2) and weighted frequency average -> BPM."""
     f = np.asarray(bins) * fs / F_phase

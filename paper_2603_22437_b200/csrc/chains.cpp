@@ -453,6 +453,20 @@ class Runner {
         return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&Xr, &Xr}, {&Xi, &Xi}}));
     }
 
+    // VP+ (SURVEY §8(c)-7): sharpen S_k = P_k^2, then N_f = sum_k f_k S_k and
+    // D_f = sum_k S_k (f_k = k fs / Fp Hz) as one 2-output scalar matrix product + rescale
+    DCt vp_weighted_average(const DCt &Pk, uint32_t band, uint32_t Fp)
+    {
+        const uint32_t K = Pk.batch;
+        DCt S = ev_square_rescale(c_, Pk);
+        std::vector<double> coef((size_t)2 * K);
+        for (uint32_t bi = 0; bi < K; ++bi) {
+            coef[bi] = (double)cfg_.bins[band][bi] * cfg_.fs / (double)Fp;
+            coef[K + bi] = 1.0;
+        }
+        return ev_rescale(c_, ev_lincomb_mat(c_, S, 2, K, 0, 0, coef));
+    }
+
     std::vector<DCt> vitals_v2(const mmfhe_ct *in, size_t n_in)
     {
         const uint32_t F = (uint32_t)(n_in / 2), fb = frame_batch(F);
@@ -474,7 +488,8 @@ class Runner {
             DCt If = k5_fir(I, taps);
             DCt Qf = k5_fir(Q, taps);
             DCt ys = k7_taylor_phase(If, Qf);
-            out.push_back(vp_band_power(ys, b));
+            DCt Pk = vp_band_power(ys, b);
+            out.push_back(cfg_.vp_plus ? vp_weighted_average(Pk, b, ys.batch) : std::move(Pk));
         }
         return out;
     }
@@ -506,7 +521,7 @@ uint32_t chain_depth(const std::string &chain, const mmfhe_chain_cfg &cfg)
 {
     const uint32_t lg = ilog2(cfg.gamma ? cfg.gamma : 1), lp = ilog2(cfg.p_phi ? cfg.p_phi : 1);
     const uint32_t gf = 3 + lg + 1, fc = 5;
-    const uint32_t v2 = (1 + lp + 1) + 1 + (cfg.taylor_order == 3 ? 3 : 1) + 1 + 1;
+    const uint32_t v2 = (1 + lp + 1) + 1 + (cfg.taylor_order == 3 ? 3 : 1) + 1 + 1 + (cfg.vp_plus ? 2 : 0);
     if (chain == "k1_energy") return 1;
     if (chain == "vitals_v1") return 1 + lg + 1;
     if (chain == "vitals_v2") return v2;
@@ -581,7 +596,7 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
     if (chain == "vitals_v1") n_out = 2;
     if (chain == "vitals_v2") {
         n_out = 0;
-        for (uint32_t b = 0; b < cfg.n_bands; ++b) n_out += cfg.n_bins[b];
+        for (uint32_t b = 0; b < cfg.n_bands; ++b) n_out += cfg.vp_plus ? 2 : cfg.n_bins[b];
     }
     return std::vector<uint32_t>(n_out, out);
 }

@@ -35,17 +35,8 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
                    uint32_t gx = 1, uint32_t gy = 1);
 // w [B][2][l+1][N] = BConv_{P->Q}(zP [B][2][K][N]) (coefficient form).
 void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B);
-// out_{b,p} = (accQ_{b,p} - w_{b,p}) * P^{-1} (+ add_{b,p}); out/add item strides os/as,
-// poly 1 of an item at +(l+1)N; add may be null, add1 (poly 1 addend) selectable.
-// out = (accQ - w) P^{-1} (+ sigma_g0(add0) + add2 on poly 0, + add1 on poly 1; each may be null)
-void launch_moddown_final(Ctx &c, uint64_t *out, size_t os, const uint64_t *accQ, const uint64_t *w,
-                          const uint64_t *add0, const uint64_t *add1, size_t as, uint32_t level, uint32_t B,
-                          uint32_t g0 = 1, const uint64_t *add2 = nullptr);
-
-// ---- rescale (batched): v [B][2][l][N] = NTT_{q_i}([t]_{q_i} - [h]_{q_i}), t = [a_l + h]_{q_l}, h = floor(q_l/2)
-// out [B][2][l][N] = (a_i - v_i) * q_l^{-1}; a item stride as.
-void launch_rescale_final(Ctx &c, uint64_t *out, const uint64_t *a, size_t as, const uint64_t *v, uint32_t level,
-                          uint32_t B);
+// (ModDown's final step (accQ - w) P^{-1} + addends and the rescale's (a_i - v_i) q_l^{-1}
+// run as the epilogue of the forward NTT's row pass: ntt_forward(..., RowEpi).)
 
 // ---- fused sums (batched: operand item stride is, output item stride os)
 // out (+)= sum_p a_p (x) b_p (3 polys), <= kMaxTerms pairs.

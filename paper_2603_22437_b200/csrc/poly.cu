@@ -368,56 +368,7 @@ __global__ void __launch_bounds__(kTB) k_tensor1(uint64_t *__restrict__ out_base
     }
 }
 
-// grid.y = poly*(l+1) + i, grid.z = item
-struct MDAdd {
-    const uint64_t *add0, *add1, *add2;  // poly-0 addend read through sigma_g0, poly-1 addend, poly-0 addend
-    size_t as;                          // item stride of the addends
-    uint32_t g0;
-};
-__global__ void k_moddown_final(uint64_t *__restrict__ out, size_t os, const uint64_t *__restrict__ accQ,
-                                const uint64_t *__restrict__ w, MDAdd ad, KTables kt, MDArgs a)
-{
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= kt.n) return;
-    const uint32_t r = blockIdx.y, b = blockIdx.z;
-    const uint32_t poly = r / (a.level + 1), i = r - poly * (a.level + 1);
-    const uint64_t q = kt.q[i];
-    const TwPair pv = a.pinv[i];
-    const size_t idx = ((size_t)b * 2 * (a.level + 1) + r) * kt.n + k;
-    uint64_t d = shoup(accQ[idx] + q - w[idx], pv.w, pv.wp, q);
-    // per-poly fused additions (each may be null): sigma_g0(add0) + add2 on poly 0, add1 on poly 1
-    const size_t ao = (size_t)b * ad.as + (size_t)i * kt.n;
-    if (poly == 0) {
-        if (ad.add0) d = add_mod(d, ad.add0[ao + galois_perm(k, ad.g0, kt.log_n)], q);
-        if (ad.add2) d = add_mod(d, ad.add2[ao + k], q);
-    } else if (ad.add1) {
-        d = add_mod(d, ad.add1[ao + k], q);
-    }
-    out[(size_t)b * os + (size_t)r * kt.n + k] = d;
-}
-
-// ------------------------------------------------------------------ rescale
-struct RSArgs {
-    const TwPair *qlinv;    // row l of [L+1][L+1]
-    const uint64_t *h;      // row l: floor(q_l/2) mod q_i
-    uint32_t level;
-};
-
-// out_i = (a_i - v_i) q_l^{-1} mod q_i, v_i = NTT_{q_i}([t]_{q_i} - [h]_{q_i}),
-// t = [a_l + h]_{q_l}, h = floor(q_l / 2) (SURVEY §8(c)-5 rescale, round half up); grid.z = item
-__global__ void k_rescale_final(uint64_t *__restrict__ out, const uint64_t *__restrict__ in, size_t is,
-                                const uint64_t *__restrict__ v, KTables kt, RSArgs a)
-{
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= kt.n) return;
-    const uint32_t r = blockIdx.y, b = blockIdx.z;
-    const uint32_t poly = r / a.level, i = r - poly * a.level;
-    const uint64_t q = kt.q[i];
-    const TwPair w = a.qlinv[i];
-    const uint64_t x = in[(size_t)b * is + ((size_t)poly * (a.level + 1) + i) * kt.n + k];
-    const size_t o = ((size_t)b * 2 * a.level + r) * kt.n + k;
-    out[o] = shoup(x + q - v[o], w.w, w.wp, q);
-}
+// (ModDown's and the rescale's final steps are the forward NTT row pass's epilogue, RowEpi)
 
 // ------------------------------------------------------------------ fused sums
 // d0 = sum a0 b0, d1 = sum a0 b1 + a1 b0, d2 = sum a1 b1 over n pairs; grid.z = item.
@@ -862,35 +813,6 @@ void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t leve
     LAUNCH_CHECK(c);
 }
 
-void launch_moddown_final(Ctx &c, uint64_t *out, size_t os, const uint64_t *accQ, const uint64_t *w,
-                          const uint64_t *add0, const uint64_t *add1, size_t as, uint32_t level, uint32_t B,
-                          uint32_t g0, const uint64_t *add2)
-{
-    ProfScope ps(c, "moddown_final",
-                 8.0 * (level + 1) * c.n * B *
-                     (6.0 + (add0 ? 1.0 : 0.0) + (add1 ? 1.0 : 0.0) + (add2 ? 1.0 : 0.0)));
-    const MDAdd ad{add0, add1, add2, as, g0};
-    k_moddown_final<<<grid3(c.n, 2 * (level + 1), B), kTB, 0, c.stream>>>(out, os, accQ, w, ad, c.kt,
-                                                                          md_args(c, level));
-    LAUNCH_CHECK(c);
-}
-
-static RSArgs rs_args(Ctx &c, uint32_t level)
-{
-    RSArgs a;
-    a.qlinv = (const TwPair *)c.bconv_ptr(c.off_rs) + (size_t)level * (c.L + 1);
-    a.h = (const uint64_t *)c.bconv_ptr(c.off_rs_h) + (size_t)level * (c.L + 1);
-    a.level = level;
-    return a;
-}
-
-void launch_rescale_final(Ctx &c, uint64_t *out, const uint64_t *a, size_t as, const uint64_t *v, uint32_t level,
-                          uint32_t B)
-{
-    ProfScope ps(c, "rescale_final", 8.0 * 6.0 * level * c.n * B);
-    k_rescale_final<<<grid3(c.n, 2 * level, B), kTB, 0, c.stream>>>(out, a, as, v, c.kt, rs_args(c, level));
-    LAUNCH_CHECK(c);
-}
 
 void launch_tensor_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &a, const PtrList &b, size_t is, int n,
                        uint32_t level, bool accumulate, uint32_t B)

@@ -48,7 +48,7 @@ def test_library_is_sm100a_and_has_kernels():
     sass = subprocess.run([os.path.join(build.CUDA, "bin", "cuobjdump"), "-symbols", so],
                           capture_output=True, text=True).stdout
     for k in ("ntt_fwd_pass", "ntt_inv_pass", "k_modup", "k_key_ip", "k_moddown_bconv", "k_tensor_sum",
-              "k_pmult_sum", "k_rescale_final", "k_moddown_final", "k_lincomb_mat", "k_batch_sum"):
+              "k_pmult_sum", "k_tensor1", "k_lincomb_sym", "k_lincomb_mat", "k_batch_sum"):
         assert k in sass, k
 
 
@@ -62,8 +62,8 @@ def test_struct_layouts_match_header():
 #include <stdio.h>
 #include <stddef.h>
 #include "mmfhe.h"
-int main(void){printf("%zu %zu %zu %zu %zu\n", sizeof(mmfhe_ct), sizeof(mmfhe_params), sizeof(mmfhe_chain_cfg),
- offsetof(mmfhe_chain_cfg, fs), offsetof(mmfhe_ct, data));return 0;}
+int main(void){printf("%zu %zu %zu %zu %zu %zu\n", sizeof(mmfhe_ct), sizeof(mmfhe_params), sizeof(mmfhe_chain_cfg),
+ offsetof(mmfhe_chain_cfg, fs), offsetof(mmfhe_ct, data), offsetof(mmfhe_chain_cfg, vp_plus));return 0;}
 '''
     import tempfile
     with tempfile.TemporaryDirectory() as d:
@@ -76,6 +76,7 @@ int main(void){printf("%zu %zu %zu %zu %zu\n", sizeof(mmfhe_ct), sizeof(mmfhe_pa
     assert vals[1] == ctypes.sizeof(mmfhe.Params)
     assert vals[2] == ctypes.sizeof(mmfhe.ChainCfg)
     assert vals[3] == mmfhe.ChainCfg.fs.offset
+    assert vals[5] == mmfhe.ChainCfg.vp_plus.offset
     assert vals[4] == mmfhe.CT.data.offset
 
 

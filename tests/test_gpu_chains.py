@@ -28,7 +28,8 @@ def _mcfg(m, cfg: cc.ChainCfg, bins=(), taps=()):
     return m.chain_cfg(R=cfg.R, D=cfg.D, A=cfg.A, F=cfg.F, gamma=cfg.gamma, p_phi=cfg.p_phi,
                        taylor_order=cfg.taylor_order, n_slots=cfg.n_slots, bsgs_baby=cfg.bsgs_baby,
                        fc_dims=cfg.fc_dims, notch_width=cfg.notch_width, bands_bins=bins,
-                       n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch, hoist=cfg.hoist)
+                       n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch, hoist=cfg.hoist,
+                       vp_plus=cfg.vp_plus)
 
 
 def _run(m, P, keys, book, chain, cfg, cts, want, scalars=None, bins=(), taps=()):
@@ -319,6 +320,33 @@ def test_vitals_v2_small(m, taps):
     ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
     out = cc.vitals_v2(ev, cts[0::2], cts[1::2], taps, cfg)
     want = out[0] + out[1]
+    scalars = {f"k5.b{b}": t for b, t in enumerate(taps)}
+    bins = []
+    for b in range(2):
+        ks = dsp.band_bins(cfg.F - 1, cfg.fs, cfg.bands[b])
+        bins.append([int(k) for k in ks])
+        for k in ks:
+            c, s = dsp.narrowband_dft_coefs(cfg.F - 1, int(k))
+            scalars[f"vp.c.{b}.{int(k)}"] = c
+            scalars[f"vp.s.{b}.{int(k)}"] = s
+    ctx = _run(m, P, keys, None, "vitals_v2", cfg, cts, want, scalars=scalars, bins=bins, taps=taps)
+    assert ctx.trace() == ev.trace
+
+
+@pytest.mark.parametrize("taps", [([0.2, 0.3, 0.3, 0.2], [0.25, -0.5, 0.25])])
+def test_vitals_v2_vp_plus(m, taps):
+    """Full-depth V2 (VP+ sharpen + weighted frequency average in the cloud):
+    N_f, D_f residues and the op trace equal the oracle's."""
+    P = toy(log_n=10, n_q=10, scale_bits=50, n_p=2, alpha=2)
+    cfg = cc.ChainCfg(R=8, F=10, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=2.0,
+                      bands=((0.1, 0.6), (0.7, 1.0)), frame_batch=4, vp_plus=1)
+    keys = orc.keygen(P, seed=3501, rotations=cc.required_rotations("vitals_v2", cfg, P.n))
+    _, cts = _vital_inputs(P, keys, cfg, 9, 3502)
+    taps = [np.array(t) for t in taps]
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    out = cc.vitals_v2(ev, cts[0::2], cts[1::2], taps, cfg)
+    want = out[0] + out[1]
+    assert len(want) == 4 and want[0].level == 0
     scalars = {f"k5.b{b}": t for b, t in enumerate(taps)}
     bins = []
     for b in range(2):

@@ -201,6 +201,38 @@ def test_vitals_v2_small(Pg):
         assert rel_err(got, want) < 1e-3
 
 
+def test_vitals_v2_vp_plus(Pg):
+    """Full-depth V2 (SURVEY §8(c)-7 VP+): sharpen + weighted frequency
+    average in the cloud; decrypted N_f, D_f match the plaintext sums over the plaintext
+    band powers, and 60 N_f / D_f the client's BPM formula.  Depth 9 (c-6 ledger)."""
+    # Delta = 2^50 (as PS4, where the full chain runs): the sharpened powers are ~1e-9 here
+    P = toy(log_n=10, n_q=10, scale_bits=50, n_p=2, alpha=2)
+    cfg = cc.ChainCfg(R=8, F=16, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=2.0,
+                      bands=((0.1, 0.6), (0.7, 1.0)), vp_plus=1)
+    z, _ = radar.vital_scene(cfg.R, cfg.F, cfg.fs, seed=1004)
+    zt = radar.preprocess_vital(z)
+    keys = orc.keygen(P, seed=2004, rotations=cc.required_rotations("vitals_v2", cfg, P.n))
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    lvl = 9
+    re = [_enc(P, keys, radar.pack_vital(zt[t].real, cfg.n_slots), lvl, 2 * t) for t in range(cfg.F)]
+    im = [_enc(P, keys, radar.pack_vital(zt[t].imag, cfg.n_slots), lvl, 2 * t + 1) for t in range(cfg.F)]
+    taps = [np.array([0.2, 0.3, 0.3, 0.2]), np.array([0.25, -0.5, 0.25])]
+    out = cc.vitals_v2(ev, re, im, taps, cfg)
+    I = np.array([dsp.soft_iq(zt[t], cfg.p_phi)[0] for t in range(cfg.F)])
+    Q = np.array([dsp.soft_iq(zt[t], cfg.p_phi)[1] for t in range(cfg.F)])
+    for bi, h in enumerate(taps):
+        y = dsp.taylor_phase(dsp.fir(I, h), dsp.fir(Q, h), cfg.taylor_order)
+        bins = dsp.band_bins(len(y), cfg.fs, cfg.bands[bi])
+        Pk = dsp.narrowband_power(y, bins)
+        want_n, want_d = dsp.weighted_average(Pk, bins, cfg.fs, len(y))
+        assert len(out[bi]) == 2 and out[bi][0].level == 0 and out[bi][0].scale == out[bi][1].scale
+        got_n, got_d = (orc.decrypt_vector(P, keys, c)[0] for c in out[bi])
+        assert abs(got_n - want_n) <= 1e-3 * abs(want_n) and abs(got_d - want_d) <= 1e-3 * abs(want_d)
+        bpm = dsp.bpm_from_power(Pk, bins, cfg.fs, len(y))
+        assert abs(60.0 * want_n / want_d - bpm) <= 1e-9 * bpm
+        assert abs(60.0 * got_n / got_d - bpm) <= 1e-2  # BPM gate is 1 BPM (north star)
+
+
 def test_trace_is_data_oblivious(Pg):
     P = toy(log_n=10, n_q=4, scale_bits=40, n_p=2, alpha=2)
     cfg = cc.ChainCfg(R=8, F=3, gamma=2, n_slots=P.n // 2)
