@@ -315,7 +315,7 @@ def bench_workload(name, m, torch, device, steps=2, warmup=2):
         cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2,
                           bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
                           frame_batch=50, vp_plus=1)
-        chain, lvl, n_in, frames, info = "vitals_v2", 9, 2 * F, F, "F=200 frames, frame_batch 50, VP+ in the cloud
+        chain, lvl, n_in, frames, info = "vitals_v2", 9, 2 * F, F, "F=200 frames, frame_batch 50, VP+ in the cloud"
     # one step = these chain calls (C5v: V1 then V2 on the same session's frames)
     plan = [("vitals_v1", 3, n_in), (chain, lvl, n_in)] if name == "C5v" else [(chain, lvl, n_in)]
     ctx = m.Context.from_params(P, device=device.index or 0, stream=stream.cuda_stream)
