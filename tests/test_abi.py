@@ -95,3 +95,11 @@ def test_product_path_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt and "ckks_ref" not in txt, f
+
+
+def test_entry_points_compile():
+    """bench.py and __graft_entry__.py are importable Python (the driver runs both)."""
+    import py_compile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for f in ("bench.py", "__graft_entry__.py"):
+        py_compile.compile(os.path.join(root, f), doraise=True)
