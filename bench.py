@@ -54,6 +54,16 @@ def c2_config():
                    v1_level=3, v2_level=7)
 
 
+def c2_bench_config(world):
+    """The N=1 workload (BASELINE configs[1]) both arms report as `config`."""
+    return {"workload": "C2 vital-signs pipeline: vitals_v1 (K1->K2, entry level 3) + vitals_v2 "
+                        "(K4->K5->K7->narrowband DFT->|X|^2, entry level 7)",
+            "N": 2 ** 14, "R": 128, "F": 256, "params": "PS2: 8 Q limbs (60+7x40) + 1 P, alpha 1",
+            "sessions_per_step_per_gpu": 1, "parallelism": f"session-sharded x{world}",
+            "l2": "inputs larger than L2 (1.5 GiB of ciphertexts per step)",
+            "inputs": "coefficient form, device-resident; import NTT and export INTT in the step"}
+
+
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
     """SM clock and clock-event (throttle) reasons sampled during the timed region,
@@ -599,7 +609,7 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "C2 vital-signs pipeline (oracle sample)", "N": 2 ** 14, "R": 128},
+            "config": c2_bench_config(world),
             "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
@@ -711,12 +721,7 @@ def main():
             "metric": METRIC, "value": r["value"], "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": "C2 vital-signs pipeline: vitals_v1 (K1->K2, entry level 3) + vitals_v2 "
-                                   "(K4->K5->K7->narrowband DFT->|X|^2, entry level 7)",
-                       "N": P.n, "R": cfg["R"], "F": cfg["F"], "params": "PS2: 8 Q limbs (60+7x40) + 1 P, alpha 1",
-                       "sessions_per_step_per_gpu": 1, "parallelism": f"session-sharded x{world}",
-                       "l2": "inputs larger than L2 (1.5 GiB of ciphertexts per step)",
-                       "inputs": "coefficient form, device-resident; import NTT and export INTT in the step"},
+            "config": c2_bench_config(world),
             "clocks": r["clocks"], "e2e": r["e2e"], "gpu_launches": r["launches"], "roofline": rl,
             "cpu_baseline": cpu, "extras": r["extras"],
             "kernel_profile_ms_per_step": {k: round(v[1] / r["prof_steps"], 3) for k, v in r["prof"].items()},

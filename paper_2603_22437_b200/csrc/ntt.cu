@@ -65,7 +65,14 @@ __host__ __device__ constexpr bool fwd_corr(int s) { return s >= 3 && (s & 1); }
 
 // min CTAs/SM for __launch_bounds__: 4 (<= 64 registers) fits every pass without spills
 // and keeps 32 warps resident; 5 (<= 51 registers) spills
-constexpr int kMinCtas = 4;
+#ifndef MMFHE_NTT_MINCTAS
+#define MMFHE_NTT_MINCTAS 4
+#endif
+#ifndef MMFHE_NTT_TWSTAGE
+#define MMFHE_NTT_TWSTAGE 0
+#endif
+constexpr int kMinCtas = MMFHE_NTT_MINCTAS;
+constexpr bool kTwStage = MMFHE_NTT_TWSTAGE != 0;  // load each stage's twiddles just before it
 
 template <int LOGS, int OTHER, bool COL>
 struct Geo {
@@ -281,16 +288,20 @@ __device__ __forceinline__ void fwd_bfly(uint64_t (&v)[Gm::E], int r, int ktr, i
     const int w = F::w(r), lo = F::lo(r), lp0 = LOGS - 1 - F::hi(r);
     const uint64_t qm = kLazyMul * q, q8 = 8 * q;
     TwPair tws[E];
-#pragma unroll
-    for (int s = 0; s < w; ++s) {
+    auto load_stage = [&](int s) {
         const int lp = lp0 + s;
         const TwPair *tb = tw + (1 << (Gm::LBASE + lp)) + (prefix << lp) + (ktr >> (LOGS - lp));
 #pragma unroll
         for (int mm = 0; mm < (1 << s); ++mm)
             tws[(1 << s) - 1 + mm] = ld_tw(tb + (kmap(ELOG, lo, w, 0, mm << (ELOG - s)) >> (LOGS - lp)));
+    };
+    if (!kTwStage) {
+#pragma unroll
+        for (int s = 0; s < w; ++s) load_stage(s);
     }
 #pragma unroll
     for (int s = 0; s < w; ++s) {
+        if (kTwStage) load_stage(s);
         const int bit = ELOG - 1 - s;  // register bit paired in this stage
         const bool corr = fwd_corr(Gm::LBASE + lp0 + s);
 #pragma unroll
@@ -331,17 +342,21 @@ __device__ __forceinline__ void inv_bfly(uint64_t (&v)[Gm::E], int r, int ktr, i
     const int lo = I::lo(r), w = I::w(r);
     const uint64_t qm = kLazyMul * q;  // words stay in [0, kLazyMul q)
     TwPair tws[E];
-#pragma unroll
-    for (int s = 0; s < w; ++s) {
+    auto load_stage = [&](int s) {
         const int lp = LOGS - 1 - (lo + s);
         const int ntop = w - 1 - s;
         const TwPair *tb = tw + (1 << (Gm::LBASE + lp)) + (prefix << lp) + (ktr >> (LOGS - lp));
 #pragma unroll
         for (int mm = 0; mm < (1 << ntop); ++mm)
             tws[(1 << ntop) - 1 + mm] = ld_tw(tb + (kmap(ELOG, lo, w, 0, mm << (ELOG - ntop)) >> (LOGS - lp)));
+    };
+    if (!kTwStage) {
+#pragma unroll
+        for (int s = 0; s < w; ++s) load_stage(s);
     }
 #pragma unroll
     for (int s = 0; s < w; ++s) {
+        if (kTwStage) load_stage(s);
         const int bit = ELOG - w + s;  // register bit of k-bit lo+s
         const int ntop = w - 1 - s;    // register bits above: the twiddle depends on these only
 #pragma unroll
@@ -372,7 +387,7 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
                                                                       ColSrc cs, RowEpi ep)
 {
     using Gm = Geo<LOGS, OTHER, COL>;
-    constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, T = Gm::T, G = Gm::G, R = Gm::R;
+    constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, G = Gm::G, R = Gm::R;
     constexpr int LOGN = LOGS + OTHER;
     extern __shared__ uint64_t sm[];
     size_t row;
@@ -490,7 +505,7 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_inv_pass(uint64_t *
                                                                       InvSrc is)
 {
     using Gm = Geo<LOGS, OTHER, COL>;
-    constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, T = Gm::T, G = Gm::G, R = Gm::R;
+    constexpr int ELOG = Gm::ELOG, S = Gm::S, E = Gm::E, G = Gm::G, R = Gm::R;
     constexpr int LOGN = LOGS + OTHER;
     extern __shared__ uint64_t sm[];
     size_t row;
@@ -608,6 +623,9 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
     }
 }
 
+#ifndef MMFHE_NTT_L1_14
+#define MMFHE_NTT_L1_14 7
+#endif
 // Radix-8 everywhere: radix-16 (ELOG = 4) halves the exchanges but its 64 KiB CTAs and
 // 16 live words per thread halved occupancy and ran 2x slower on B200 (measured).
 // log N = L1 + L2, L1 = floor(log N / 2): col pass <L1, L2>, row pass <L2, L1>.
@@ -633,7 +651,7 @@ void launch_pass(uint32_t log_n, uint64_t *d, uint32_t rows, const KTables &kt, 
         MMFHE_NTT_CASE(11, 5, 6)
         MMFHE_NTT_CASE(12, 6, 6)
         MMFHE_NTT_CASE(13, 6, 7)
-        MMFHE_NTT_CASE(14, 7, 7)
+        MMFHE_NTT_CASE(14, MMFHE_NTT_L1_14, 14 - MMFHE_NTT_L1_14)
         MMFHE_NTT_CASE(15, 7, 8)
         MMFHE_NTT_CASE(16, 8, 8)
     default:
@@ -644,7 +662,7 @@ void launch_pass(uint32_t log_n, uint64_t *d, uint32_t rows, const KTables &kt, 
 
 void split(uint32_t log_n, int &L1, int &L2)
 {
-    L1 = (int)log_n / 2;
+    L1 = log_n == 14 ? MMFHE_NTT_L1_14 : (int)log_n / 2;
     L2 = (int)log_n - L1;
 }
 
