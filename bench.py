@@ -507,6 +507,27 @@ def extras_n16(args, m, torch, device, batch=8, reps=3):
         res[f"{name}_per_s"] = ops
         res[f"{name}_us"] = 1e6 / ops
         res[f"{name}_alg_gbs"] = ops * alg / 1e9
+    # SURVEY §8(d) variants 2 and 3: one ciphertext per op (the 81 MiB evk streamed for every
+    # rotation: the worst case) and a hoisted group of 8 rotations of one ciphertext
+    steps8 = list(range(1, 9))
+    for k in steps8[1:]:
+        ctx.load_galois_key(k, uniform_dev(torch, gen, key_shape, basis, P.n, device))
+    one, oone = cts[0], outs[0]
+    houts = [m.Ct(obuf[i], L, 0.0, 0, P.log_n, m.FORM_EVAL) for i in range(8)]
+    for name, fn, n_ops, alg in (("hrot_b1", lambda: ctx.hrot_batch([one], 1, [oone]), 1, 2 * ct_bytes + evk),
+                                 ("hrot_hoisted8", lambda: ctx.hrot_hoisted(one, steps8, houts), 8,
+                                  ct_bytes + 8 * (evk + ct_bytes))):
+        fn()
+        torch.cuda.synchronize(device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        s = e0.elapsed_time(e1) / 1e3 / reps
+        res[f"{name}_us_per_rotation"] = s / n_ops * 1e6
+        res[f"{name}_alg_gbs"] = alg / s / 1e9
     # integer roof: the key switch's algorithmic butterflies, 128-bit MACs and
     # modular products against the butterfly / MAC / Shoup rates measured in this run
     Lp, K, N, logn = L + 1, P.K, P.n, P.log_n
@@ -525,7 +546,9 @@ def extras_n16(args, m, torch, device, batch=8, reps=3):
                         f"modmul (SURVEY 8(d)); HMult adds 4L'N tensor MACs; peaks measured in this run: "
                         f"{peaks['bfly'] / 1e9:.0f} G bfly/s, {peaks['mac'] / 1e9:.0f} G MAC/s, "
                         f"{peaks['mm'] / 1e9:.0f} G modmul/s; int_frac = model time / measured time")
-    res["config"] = "PS4: N=2^16, 20 Q + 7 P limbs, dnum 3, top level, batch of 8 distinct cts, one key, eval form"
+    res["config"] = ("PS4: N=2^16, 20 Q + 7 P limbs, dnum 3, top level, eval form; hrot/hmult: batch of 8 "
+                     "distinct cts, one key; hrot_b1: one ct per call; hrot_hoisted8: steps 1..8 of one ct "
+                     "(one ModUp, 8 inner products + ModDowns, 8 keys)")
     ctx.close()
     return res
 
