@@ -51,7 +51,7 @@ def c2_config():
     R, F, fs = 128, 256, 20.0
     bins = [band_bins(F - 1, fs, b) for b in BANDS]
     return P, dict(R=R, F=F, fs=fs, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2, bins=bins, n_taps=41,
-                   v1_level=3, v2_level=7)
+                   v1_level=3, v2_level=7, iq_pack=1)
 
 
 def c2_bench_config(world):
@@ -61,7 +61,8 @@ def c2_bench_config(world):
             "N": 2 ** 14, "R": 128, "F": 256, "params": "PS2: 8 Q limbs (60+7x40) + 1 P, alpha 1",
             "sessions_per_step_per_gpu": 1, "parallelism": f"session-sharded x{world}",
             "l2": "inputs larger than L2 (1.5 GiB of ciphertexts per step)",
-            "inputs": "coefficient form, device-resident; import NTT and export INTT in the step"}
+            "inputs": "coefficient form, device-resident; import NTT and export INTT in the step",
+            "k4_rotsum": "packed I/Q rotate-and-sum (DESIGN reading R19: 2 + log2 R rotations per frame)"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -152,7 +153,7 @@ def make_ctx_c2(m, torch, P, cfg, device, seed):
 def chain_cfg_c2(m, cfg):
     return m.chain_cfg(R=cfg["R"], F=cfg["F"], gamma=cfg["gamma"], p_phi=cfg["p_phi"],
                        taylor_order=cfg["taylor_order"], n_slots=cfg["n_slots"], bands_bins=cfg["bins"],
-                       n_taps=[cfg["n_taps"]] * 2, fs=cfg["fs"])
+                       n_taps=[cfg["n_taps"]] * 2, fs=cfg["fs"], iq_pack=cfg.get("iq_pack", 0))
 
 
 def session_inputs(m, torch, gen, P, cfg, device):
@@ -324,7 +325,7 @@ def bench_workload(name, m, torch, device, steps=2, warmup=2):
         F, fs = 200, 20.0
         cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2,
                           bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
-                          frame_batch=50, vp_plus=1)
+                          frame_batch=50, vp_plus=1, iq_pack=1)
         chain, lvl, n_in, frames, info = "vitals_v2", 9, 2 * F, F, "F=200 frames, frame_batch 50, VP+ in the cloud"
     # one step = these chain calls (C5v: V1 then V2 on the same session's frames)
     plan = [("vitals_v1", 3, n_in), (chain, lvl, n_in)] if name == "C5v" else [(chain, lvl, n_in)]
@@ -576,11 +577,11 @@ def oracle_sample(frames: int, threads: int):
                     out[j, p, t] = prng.uniform_mod(rng_seed, sid + 4 * j + p, P.n, q, offset=t * P.n)
         return out
 
-    rots = sorted(set(cc.rotsum_steps(cfg["R"], 1)))
+    ccfg = cc.ChainCfg(R=cfg["R"], F=frames, gamma=2, p_phi=2, taylor_order=1, n_slots=cfg["n_slots"],
+                       fs=cfg["fs"], bands=BANDS, iq_pack=cfg.get("iq_pack", 0))
+    rots = cc.required_rotations("vitals_v2", ccfg, P.n)
     rlk = ukey(prng.SID_UNIFORM)
     gk = {k: ukey(prng.SID_UNIFORM + 100 * (i + 1)) for i, k in enumerate(rots)}
-    ccfg = cc.ChainCfg(R=cfg["R"], F=frames, gamma=2, p_phi=2, taylor_order=1, n_slots=cfg["n_slots"],
-                       fs=cfg["fs"], bands=BANDS)
 
     def uct(level, idx):
         c = [np.stack([prng.uniform_mod(rng_seed, prng.SID_UNIFORM + 10 ** 6 + 4 * idx + p, P.n, q, offset=i * P.n)

@@ -119,6 +119,10 @@ typedef struct {
                               (VP+): per band two outputs N_f = sum_k f_k P_k^2 and
                               D_f = sum_k P_k^2 (f_k = k fs / (F-1) Hz; the client reads
                               BPM = 60 N_f / D_f); depth +2.  0 = outputs P_k (client finishes) */
+    uint32_t iq_pack;      /* vital V2 / K4: 1 = one rotate-and-sum over z = i + Rot(q, -R) and
+                              Q = Rot(z, R) (2 + log2 R rotations instead of 2 log2 R; needs
+                              2R <= n and the Galois keys for R and -R, which
+                              mmfhe_chain_required_rotations lists); same decryption */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */

@@ -54,6 +54,7 @@ class ChainCfg:
     frame_batch: int = 0        # frames per op-major batch (0: all frames)
     hoist: int = 0              # 1: baby-step rotations of K3 / FC share one ModUp (hoisted HRot)
     vp_plus: int = 0            # vital V2: 1 -> sharpen + weighted frequency average in the cloud
+    iq_pack: int = 0            # K4: 1 -> one rotate-and-sum over (i | Rot(q, -R)) (reading R19)
 
 
 def rot(v: np.ndarray, k: int) -> np.ndarray:
@@ -435,6 +436,14 @@ def k4_soft_iq(ev, re, im, cfg):
     i_ = ev.relin_rescale_all([ev.tensor_sum([(x, r)]) for x, r in zip(m, red)])
     imd = [ev.drop_to(i, x.level) for i, x in zip(im, m)]
     q_ = ev.relin_rescale_all([ev.tensor_sum([(x, i)]) for x, i in zip(m, imd)])
+    if cfg.iq_pack:
+        # reading R19: i and q occupy slots 0..R-1 (zeros beyond, reading #23), so
+        # z = i + Rot(q, -R) holds q in slots R..2R-1; one rotate-and-sum puts sum(i) in
+        # slot 0 and sum(q) in slot R, and Rot(z, R) brings sum(q) to slot 0:
+        # 1 + log2 R + 1 rotations instead of 2 log2 R
+        qr = [ev.rotate(x, -cfg.R) for x in q_]
+        z = ev.rotsum_all([ev.add(a, b) for a, b in zip(i_, qr)], cfg.R, 1)
+        return z, [ev.rotate(x, cfg.R) for x in z]
     return ev.rotsum_all(i_, cfg.R, 1), ev.rotsum_all(q_, cfg.R, 1)
 
 
@@ -526,6 +535,8 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
     ks = set()
     if chain in ("k2_soft_attention", "vitals_v1", "k4_soft_iq", "vitals_v2"):
         ks |= set(rotsum_steps(cfg.R, 1))
+    if chain in ("k4_soft_iq", "vitals_v2") and cfg.iq_pack:
+        ks |= {cfg.R, -cfg.R}
     if chain in ("k3_doppler_dft", "gesture_frame", "gesture"):
         b, giants = k3_schedule(cfg)
         ks |= set(range(1, b))

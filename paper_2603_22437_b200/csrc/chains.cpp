@@ -390,6 +390,14 @@ class Runner {
         DCt i_ = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&p, &red}}));
         DCt imd = ev_drop_to(c_, im, p.level);
         DCt q_ = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&p, &imd}}));
+        if (cfg_.iq_pack) {
+            // reading R19: z = i + Rot(q, -R) (q moves to slots R..2R-1), one rotate-and-sum
+            // (sum(i) in slot 0, sum(q) in slot R), Q = Rot(z, R): 2 + log2 R key switches
+            // instead of 2 log2 R
+            DCt z = ev_rotsum(c_, ev_rot_add(c_, i_, q_, -(int32_t)cfg_.R), cfg_.R, 1);
+            DCt Q = ev_rotate(c_, z, (int32_t)cfg_.R);
+            return {std::move(z), std::move(Q)};
+        }
         DCt I = ev_rotsum(c_, i_, cfg_.R, 1);
         DCt Q = ev_rotsum(c_, q_, cfg_.R, 1);
         return {std::move(I), std::move(Q)};
@@ -546,6 +554,12 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
     chain_depth(chain, cfg);  // validates the name
     if (chain == "vitals_v1" || chain == "vitals_v2")
         for (uint32_t s : rotsum_steps(cfg.R, 1)) add(s);
+    if (chain == "vitals_v2" && cfg.iq_pack) {
+        MMFHE_REQUIRE(2 * (size_t)cfg.R <= (size_t)(cfg.n_slots ? cfg.n_slots : c.n / 2), MMFHE_E_SHAPE,
+                      "iq_pack needs 2R <= n slots");
+        add(cfg.R);
+        add(-(int64_t)cfg.R);
+    }
     const bool frames = chain == "gesture_frame" || chain == "gesture" || chain == "gesture_features";
     if (chain == "k3_doppler_dft" || frames) {
         Sched s = k3_schedule(cfg);

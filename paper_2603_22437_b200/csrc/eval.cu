@@ -637,23 +637,28 @@ DCt ev_rescale(Ctx &c, const DCt &a)
 
 // acc + HRot(acc, step) with the HAdd fused: ModDown adds sigma(c0) + c0 to poly 0 and c1
 // to poly 1 (records "hrot" then "hadd", as the two ops it replaces).
-DCt ev_rot_add(Ctx &c, const DCt &a, int32_t step)
+DCt ev_rot_add(Ctx &c, const DCt &a, const DCt &b, int32_t step)
 {
-    MMFHE_REQUIRE(a.npolys == 2, MMFHE_E_LAYOUT, "rotate needs a 2-poly ciphertext");
+    MMFHE_REQUIRE(a.npolys == 2 && b.npolys == 2, MMFHE_E_LAYOUT, "rotate needs a 2-poly ciphertext");
+    MMFHE_REQUIRE(a.level == b.level && a.batch == b.batch && a.item_words() == b.item_words(), MMFHE_E_LAYOUT,
+                  "rotate-add operands must share level and batch");
+    MMFHE_REQUIRE(a.scale == b.scale, MMFHE_E_SCALE, "hadd scale mismatch");
     int32_t k;
     const uint64_t g = galois_element(c, step, &k);
-    if (k == 0) return ev_addsub(c, a, a, false);
+    if (k == 0) return ev_addsub(c, a, b, false);
     const DKey &key = find_gk(c, k);
-    rec_n(c, "hrot", a.level, a.batch, std::to_string(k));
+    rec_n(c, "hrot", b.level, b.batch, std::to_string(k));
     rec_n(c, "hadd", a.level, a.batch);
     DCt r = make_ct(c, a.level, 2, a.n_slots, a.scale, a.batch);
-    // as ev_rotate, with ModDown adding sigma_g(c0) + c0 to poly 0 and c1 to poly 1
+    // as ev_rotate on b, with ModDown adding sigma_g(b0) + a0 to poly 0 and a1 to poly 1
     const uint32_t g32 = (uint32_t)g;
-    ModUpOut m = ks_modup(c, a.poly(1), a.item_words(), a.level, a.batch, g32);
-    ks_ip_moddown(c, a.poly(1), a.item_words(), m.y.get(), m, a.level, a.batch, key, r.data(), r.item_words(),
-                  a.data(), a.poly(1), a.item_words(), g32, 1, g32, a.data());
+    ModUpOut m = ks_modup(c, b.poly(1), b.item_words(), b.level, b.batch, g32);
+    ks_ip_moddown(c, b.poly(1), b.item_words(), m.y.get(), m, b.level, b.batch, key, r.data(), r.item_words(),
+                  b.data(), a.poly(1), a.item_words(), g32, 1, g32, a.data());
     return r;
 }
+
+DCt ev_rot_add(Ctx &c, const DCt &a, int32_t step) { return ev_rot_add(c, a, a, step); }
 
 DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride)
 {

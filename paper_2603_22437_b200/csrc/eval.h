@@ -55,6 +55,8 @@ std::vector<DCt> ev_rotate_hoisted(Ctx &c, const DCt &a, const std::vector<int32
 DCt ev_rescale(Ctx &c, const DCt &a);
 // a + HRot(a, step) in one key switch (the rotsum step)
 DCt ev_rot_add(Ctx &c, const DCt &a, int32_t step);
+// a + HRot(b, step) in one key switch (records "hrot" then "hadd")
+DCt ev_rot_add(Ctx &c, const DCt &a, const DCt &b, int32_t step);
 DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride);
 
 // composites

@@ -29,7 +29,7 @@ def _mcfg(m, cfg: cc.ChainCfg, bins=(), taps=()):
                        taylor_order=cfg.taylor_order, n_slots=cfg.n_slots, bsgs_baby=cfg.bsgs_baby,
                        fc_dims=cfg.fc_dims, notch_width=cfg.notch_width, bands_bins=bins,
                        n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch, hoist=cfg.hoist,
-                       vp_plus=cfg.vp_plus)
+                       vp_plus=cfg.vp_plus, iq_pack=cfg.iq_pack)
 
 
 def _run(m, P, keys, book, chain, cfg, cts, want, scalars=None, bins=(), taps=()):
@@ -334,12 +334,13 @@ def test_vitals_v2_small(m, taps):
 
 
 @pytest.mark.parametrize("taps", [([0.2, 0.3, 0.3, 0.2], [0.25, -0.5, 0.25])])
-def test_vitals_v2_vp_plus(m, taps):
+@pytest.mark.parametrize("iq_pack", [0, 1])
+def test_vitals_v2_vp_plus(m, taps, iq_pack):
     """Full-depth V2 (VP+ sharpen + weighted frequency average in the cloud):
     N_f, D_f residues and the op trace equal the oracle's."""
     P = toy(log_n=10, n_q=10, scale_bits=50, n_p=2, alpha=2)
     cfg = cc.ChainCfg(R=8, F=10, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=2.0,
-                      bands=((0.1, 0.6), (0.7, 1.0)), frame_batch=4, vp_plus=1)
+                      bands=((0.1, 0.6), (0.7, 1.0)), frame_batch=4, vp_plus=1, iq_pack=iq_pack)
     keys = orc.keygen(P, seed=3501, rotations=cc.required_rotations("vitals_v2", cfg, P.n))
     _, cts = _vital_inputs(P, keys, cfg, 9, 3502)
     taps = [np.array(t) for t in taps]

@@ -39,7 +39,10 @@ def test_c2_vital_pipeline_full_size(m):
     cfg = cc.ChainCfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=fs, bands=bands)
     z, truth = radar.vital_scene(R, F, fs, seed=5001)
     zt = radar.preprocess_vital(z)
-    rots = sorted(set(cc.required_rotations("vitals_v1", cfg, P.n)))
+    cfg_pack = cc.ChainCfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=fs, bands=bands,
+                           iq_pack=1)
+    rots = sorted(set(cc.required_rotations("vitals_v1", cfg, P.n)) |
+                  set(cc.required_rotations("vitals_v2", cfg_pack, P.n)))
     keys = orc.keygen(P, seed=5002, rotations=rots)
     v1, v2 = [], []
     for t in range(F):
@@ -63,22 +66,26 @@ def test_c2_vital_pipeline_full_size(m):
     Np, Dp, rp = dsp.soft_attention(dsp.energy(zt), 2, F)
     assert abs(N - Np) <= 1e-3 * abs(Np) and abs(D - Dp) <= 1e-3 * abs(Dp)
     assert round(N / D) == round(rp)
-    # V2: |X[k]|^2 per band -> BPM
-    lv2 = ctx.chain_plan("vitals_v2", mcfg, 7, 2 * F)
-    outs2 = [ct_out(m, P, lv) for lv in lv2]
-    ctx.eval_chain("vitals_v2", mcfg, [ct_in(m, P, c) for c in v2], outs2)
+    # V2: |X[k]|^2 per band -> BPM; canonical K4 and the packed rotate-and-sum (R19, bench.py)
     I = np.array([dsp.soft_iq(zt[t], 2)[0] for t in range(F)])
     Q = np.array([dsp.soft_iq(zt[t], 2)[1] for t in range(F)])
-    at = 0
-    for b, h in enumerate(taps):
-        y = dsp.taylor_phase(dsp.fir(I, h), dsp.fir(Q, h), 1)
-        want = dsp.narrowband_power(y, bins[b])
-        got = np.array([_dec(P, keys, o)[0] for o in outs2[at:at + len(bins[b])]])
-        at += len(bins[b])
-        assert np.max(np.abs(got - want)) <= 1e-3 * np.max(np.abs(want))
-        bpm_enc = dsp.bpm_from_power(got, bins[b], fs, F - 1)
-        bpm_plain = dsp.bpm_from_power(want, bins[b], fs, F - 1)
-        assert abs(bpm_enc - bpm_plain) < 1.0
+    for iq_pack in (0, 1):
+        mcfg = m.chain_cfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=cfg.n_slots, bands_bins=bins,
+                           n_taps=[41, 41], fs=fs, iq_pack=iq_pack)
+        ctx.prepare_chain("vitals_v2", mcfg, 7, taps=taps)
+        lv2 = ctx.chain_plan("vitals_v2", mcfg, 7, 2 * F)
+        outs2 = [ct_out(m, P, lv) for lv in lv2]
+        ctx.eval_chain("vitals_v2", mcfg, [ct_in(m, P, c) for c in v2], outs2)
+        at = 0
+        for b, h in enumerate(taps):
+            y = dsp.taylor_phase(dsp.fir(I, h), dsp.fir(Q, h), 1)
+            want = dsp.narrowband_power(y, bins[b])
+            got = np.array([_dec(P, keys, o)[0] for o in outs2[at:at + len(bins[b])]])
+            at += len(bins[b])
+            assert np.max(np.abs(got - want)) <= 1e-3 * np.max(np.abs(want))
+            bpm_enc = dsp.bpm_from_power(got, bins[b], fs, F - 1)
+            bpm_plain = dsp.bpm_from_power(want, bins[b], fs, F - 1)
+            assert abs(bpm_enc - bpm_plain) < 1.0
 
 
 def test_c4_gesture_full_size(m):
