@@ -31,5 +31,16 @@ for r in rows[2:]:
         if m in d:
             u = units[hdr.index(m)]
             print(f"   {m:62s} {d[m]:>12s} {u}")
-    st = {m.split('stalled_')[1].split('.')[0]: d[m] for m in METRICS[13:] if m in d}
-    print("   stalls(cycles/issue):", st)
+    # warp-state samples (--set full): share of each stall reason
+    full = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    frows = list(csv.reader(io.StringIO(full)))
+    fd = dict(zip(frows[0], frows[2 + rows.index(r) - 2])) if len(frows) > 2 else {}
+    pre = "smsp__pcsamp_warps_issue_stalled_"
+    st = {k[len(pre):]: float(v) for k, v in fd.items()
+          if k.startswith(pre) and not k.endswith("not_issued") and v.replace(".", "", 1).isdigit()}
+    tot = sum(st.values()) or 1.0
+    if "smsp__issue_active.avg.pct_of_peak_sustained_active" in fd:
+        print(f"   {'smsp__issue_active.avg.pct_of_peak_sustained_active':62s} "
+              f"{fd['smsp__issue_active.avg.pct_of_peak_sustained_active']:>12s} %")
+    top = sorted(st.items(), key=lambda kv: -kv[1])[:7]
+    print("   warp-state samples:", ", ".join(f"{k} {v / tot:.2f}" for k, v in top))
