@@ -119,10 +119,12 @@ typedef struct {
                               (VP+): per band two outputs N_f = sum_k f_k P_k^2 and
                               D_f = sum_k P_k^2 (f_k = k fs / (F-1) Hz; the client reads
                               BPM = 60 N_f / D_f); depth +2.  0 = outputs P_k (client finishes) */
-    uint32_t iq_pack;      /* vital V2 / K4: 1 = one rotate-and-sum over z = i + Rot(q, -R) and
-                              Q = Rot(z, R) (2 + log2 R rotations instead of 2 log2 R; needs
-                              2R <= n and the Galois keys for R and -R, which
-                              mmfhe_chain_required_rotations lists); same decryption */
+    uint32_t iq_pack;      /* vital V2 / K4: k >= 1 = i, q of 2^(k-1) frames packed into the slot
+                              blocks of one ciphertext, one rotate-and-sum, unpacked (DESIGN R19):
+                              per frame 2(2 - 2^(1-k)) + log2(R)/2^(k-1) rotations instead of
+                              2 log2 R; needs 2^k R <= n, a multiple of 2^(k-1) frames per frame
+                              batch (E_SHAPE) and the Galois keys for +-2^j R, j < k (listed by
+                              mmfhe_chain_required_rotations); same decryption.  0 = canonical */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */

@@ -54,7 +54,7 @@ class ChainCfg:
     frame_batch: int = 0        # frames per op-major batch (0: all frames)
     hoist: int = 0              # 1: baby-step rotations of K3 / FC share one ModUp (hoisted HRot)
     vp_plus: int = 0            # vital V2: 1 -> sharpen + weighted frequency average in the cloud
-    iq_pack: int = 0            # K4: 1 -> one rotate-and-sum over (i | Rot(q, -R)) (reading R19)
+    iq_pack: int = 0            # K4: k >= 1 -> packed rotate-and-sum over 2^k vectors (reading R19)
 
 
 def rot(v: np.ndarray, k: int) -> np.ndarray:
@@ -437,14 +437,29 @@ def k4_soft_iq(ev, re, im, cfg):
     imd = [ev.drop_to(i, x.level) for i, x in zip(im, m)]
     q_ = ev.relin_rescale_all([ev.tensor_sum([(x, i)]) for x, i in zip(m, imd)])
     if cfg.iq_pack:
-        # reading R19: i and q occupy slots 0..R-1 (zeros beyond, reading #23), so
-        # z = i + Rot(q, -R) holds q in slots R..2R-1; one rotate-and-sum puts sum(i) in
-        # slot 0 and sum(q) in slot R, and Rot(z, R) brings sum(q) to slot 0:
-        # 1 + log2 R + 1 rotations instead of 2 log2 R
-        qr = [ev.rotate(x, -cfg.R) for x in q_]
-        z = ev.rotsum_all([ev.add(a, b) for a, b in zip(i_, qr)], cfg.R, 1)
-        return z, [ev.rotate(x, cfg.R) for x in z]
+        return k4_packed_rotsum(ev, i_, q_, cfg.R, cfg.iq_pack)
     return ev.rotsum_all(i_, cfg.R, 1), ev.rotsum_all(q_, cfg.R, 1)
+
+
+def k4_packed_rotsum(ev, i_, q_, R, k):
+    """Reading R19: I = rotsum_R(i), Q = rotsum_R(q) for F frames with one rotate-and-sum per
+    2^(k-1) frames.  i and q occupy slots 0..R-1 (zeros beyond, reading #23).  Pack:
+    x = i + Rot(q, -R) (q to slots R..2R-1), then k-1 times pair the first and second half
+    of the frame list, x = x_lo + Rot(x_hi, -2^j R): 2^k vectors in slots 0..2^k R - 1.  One
+    rotsum_R leaves each vector's sum in the first slot of its block.  Unpack in reverse:
+    x <- x ++ Rot(x, 2^j R) (j = k-1..1), I = x, Q = Rot(x, R).  Per frame
+    2 (2 - 2^(1-k)) + log2(R) / 2^(k-1) rotations instead of 2 log2 R."""
+    if len(i_) % (1 << (k - 1)):
+        raise ValueError("iq_pack = k needs a multiple of 2^(k-1) frames per frame batch")
+    x = [ev.add(a, b) for a, b in zip(i_, [ev.rotate(v, -R) for v in q_])]
+    for j in range(1, k):
+        h = len(x) // 2
+        lo, hi = x[:h], x[h:]
+        x = [ev.add(a, b) for a, b in zip(lo, [ev.rotate(v, -(R << j)) for v in hi])]
+    x = ev.rotsum_all(x, R, 1)
+    for j in reversed(range(1, k)):
+        x = x + [ev.rotate(v, R << j) for v in x]
+    return x, [ev.rotate(v, R) for v in x]
 
 
 def k5_fir(ev, xs, taps):
@@ -536,7 +551,8 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
     if chain in ("k2_soft_attention", "vitals_v1", "k4_soft_iq", "vitals_v2"):
         ks |= set(rotsum_steps(cfg.R, 1))
     if chain in ("k4_soft_iq", "vitals_v2") and cfg.iq_pack:
-        ks |= {cfg.R, -cfg.R}
+        for j in range(cfg.iq_pack):
+            ks |= {cfg.R << j, -(cfg.R << j)}
     if chain in ("k3_doppler_dft", "gesture_frame", "gesture"):
         b, giants = k3_schedule(cfg)
         ks |= set(range(1, b))

@@ -391,12 +391,27 @@ class Runner {
         DCt imd = ev_drop_to(c_, im, p.level);
         DCt q_ = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&p, &imd}}));
         if (cfg_.iq_pack) {
-            // reading R19: z = i + Rot(q, -R) (q moves to slots R..2R-1), one rotate-and-sum
-            // (sum(i) in slot 0, sum(q) in slot R), Q = Rot(z, R): 2 + log2 R key switches
-            // instead of 2 log2 R
-            DCt z = ev_rotsum(c_, ev_rot_add(c_, i_, q_, -(int32_t)cfg_.R), cfg_.R, 1);
-            DCt Q = ev_rotate(c_, z, (int32_t)cfg_.R);
-            return {std::move(z), std::move(Q)};
+            // reading R19: pack i, q (and 2^(k-1) frames) into the slot blocks of one
+            // ciphertext, one rotate-and-sum, unpack (see oracle k4_packed_rotsum)
+            const int32_t R = (int32_t)cfg_.R;
+            const uint32_t k = cfg_.iq_pack;
+            MMFHE_REQUIRE(i_.batch % (1u << (k - 1)) == 0, MMFHE_E_SHAPE,
+                          "iq_pack = k needs a multiple of 2^(k-1) frames per frame batch");
+            DCt x = ev_rot_add(c_, i_, q_, -R);
+            for (uint32_t j = 1; j < k; ++j) {
+                const uint32_t h = x.batch / 2;
+                x = ev_rot_add(c_, slice(x, 0, h), slice(x, h, h), -(R << j));
+            }
+            x = ev_rotsum(c_, x, cfg_.R, 1);
+            for (uint32_t j = k - 1; j >= 1; --j) {
+                DCt hi = ev_rotate(c_, x, R << j);
+                std::vector<DCt> parts;
+                parts.push_back(std::move(x));
+                parts.push_back(std::move(hi));
+                x = concat(c_, parts);
+            }
+            DCt Q = ev_rotate(c_, x, R);
+            return {std::move(x), std::move(Q)};
         }
         DCt I = ev_rotsum(c_, i_, cfg_.R, 1);
         DCt Q = ev_rotsum(c_, q_, cfg_.R, 1);
@@ -555,10 +570,12 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
     if (chain == "vitals_v1" || chain == "vitals_v2")
         for (uint32_t s : rotsum_steps(cfg.R, 1)) add(s);
     if (chain == "vitals_v2" && cfg.iq_pack) {
-        MMFHE_REQUIRE(2 * (size_t)cfg.R <= (size_t)(cfg.n_slots ? cfg.n_slots : c.n / 2), MMFHE_E_SHAPE,
-                      "iq_pack needs 2R <= n slots");
-        add(cfg.R);
-        add(-(int64_t)cfg.R);
+        MMFHE_REQUIRE(cfg.iq_pack <= 8 && ((size_t)cfg.R << cfg.iq_pack) <= (size_t)(cfg.n_slots ? cfg.n_slots : c.n / 2),
+                      MMFHE_E_SHAPE, "iq_pack = k needs 2^k R <= n slots");
+        for (uint32_t j = 0; j < cfg.iq_pack; ++j) {
+            add((int64_t)cfg.R << j);
+            add(-((int64_t)cfg.R << j));
+        }
     }
     const bool frames = chain == "gesture_frame" || chain == "gesture" || chain == "gesture_features";
     if (chain == "k3_doppler_dft" || frames) {
