@@ -623,6 +623,14 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
         MMFHE_REQUIRE(cfg.F >= 2 && cfg.n_bands <= 4, MMFHE_E_SHAPE, "vitals_v2 needs F >= 2 and <= 4 bands");
         for (uint32_t b = 0; b < cfg.n_bands; ++b)
             MMFHE_REQUIRE(cfg.n_bins[b] >= 1 && cfg.n_bins[b] <= 64, MMFHE_E_SHAPE, "1..64 DFT bins per band");
+        if (cfg.iq_pack) {
+            // every K4 frame batch (the last one may be short) must hold whole packing groups
+            const uint32_t g = 1u << (cfg.iq_pack - 1), fb = cfg.frame_batch ? std::min(cfg.frame_batch, cfg.F) : cfg.F;
+            MMFHE_REQUIRE(cfg.iq_pack <= 8 && fb % g == 0 && (cfg.F % fb) % g == 0, MMFHE_E_SHAPE,
+                          "iq_pack = k needs a multiple of 2^(k-1) frames in every frame batch");
+            MMFHE_REQUIRE(((size_t)cfg.R << cfg.iq_pack) <= (size_t)(cfg.n_slots ? cfg.n_slots : c.n / 2),
+                          MMFHE_E_SHAPE, "iq_pack = k needs 2^k R <= n slots");
+        }
     }
     if (chain == "vitals_v1") n_out = 2;
     if (chain == "vitals_v2") {

@@ -149,7 +149,8 @@ struct IPArgs {
 // Low-register variant for 5..8 digits: 32-bit in-item source offsets instead of
 // per-digit pointers and strides, held to 3 CTAs/SM (78 registers, no spills; the
 // pointer version needs 121 and fits 2).  Measured on C2: 9.6 -> 8.9 ms/step.  For
-// <= 4 digits the pointer version (k_key_ip, no min-blocks bound) is faster.
+// <= 4 digits the pointer version (k_key_ip, no min-blocks bound) is faster.  Re-reading
+// the key words per item from L2 instead (64 registers, 4 CTAs/SM) measured 12% slower.
 template <int DMAX>
 __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
                                                 const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
@@ -199,64 +200,6 @@ __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ acc
             if (j < (int)a.dnum) {
                 mac128(acc0, s[j], kb[j]);
                 mac128(acc1, s[j], ka[j]);
-            }
-        }
-        o[(size_t)b * ostride] = redc(acc0, q, qi);
-        o[(size_t)b * ostride + opoly] = redc(acc1, q, qi);
-    }
-}
-
-#ifndef MMFHE_KEYIP_STREAM
-#define MMFHE_KEYIP_STREAM 0
-#endif
-// Streaming-key variant of k_key_ip_lr: the 2*dnum key words are re-read per item (L2-resident:
-// the whole key of a launch is < 20 MiB) instead of held in registers, so 4 CTAs/SM fit.
-template <int DMAX>
-__global__ void __launch_bounds__(kTB, 4) k_key_ip_st(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
-                                                     const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
-                                                     const uint64_t *__restrict__ key, KTables kt, IPArgs a)
-{
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= kt.n) return;
-    const uint32_t r = blockIdx.y;
-    const uint32_t b0 = blockIdx.z * a.per_z, b1 = min(a.B, b0 + a.per_z);
-    const uint32_t pr = ext_prime(r, a.level, a.L);
-    const uint64_t q = kt.q[pr], qi = kt.qinv_neg[pr];
-    const size_t key_rows = a.L + 1 + a.K;
-    const uint64_t *kp = key + (size_t)pr * kt.n + k;
-    const size_t kstride = key_rows * kt.n;  // between the b / a halves and the digits
-    uint32_t so[DMAX];
-    uint32_t xm = 0;
-    const uint32_t kx = galois_perm(k, a.gx, kt.log_n), ky = galois_perm(k, a.gy, kt.log_n);
-#pragma unroll
-    for (int j = 0; j < DMAX; ++j) {
-        if (j < (int)a.dnum) {
-            if (r >= a.lo[j] && r < a.hi[j]) {
-                so[j] = r * kt.n + kx;
-                xm |= 1u << j;
-            } else {
-                const uint32_t row = r < a.lo[j] ? r : r - (a.hi[j] - a.lo[j]);
-                so[j] = (uint32_t)a.y_off[j] + row * kt.n + ky;
-            }
-        }
-    }
-    const bool isq = r <= a.level;
-    const size_t qs = (size_t)2 * (a.level + 1) * kt.n, ps = (size_t)2 * a.K * kt.n;
-    uint64_t *o = isq ? accQ + (size_t)r * kt.n + k : accP + (size_t)(r - a.level - 1) * kt.n + k;
-    const size_t ostride = isq ? qs : ps;
-    const size_t opoly = isq ? (size_t)(a.level + 1) * kt.n : (size_t)a.K * kt.n;
-    for (uint32_t b = b0; b < b1; ++b) {
-        const uint64_t *xb = x + (size_t)b * a.xs, *yb = y + (size_t)b * a.ys;
-        uint64_t s[DMAX];
-#pragma unroll
-        for (int j = 0; j < DMAX; ++j)
-            if (j < (int)a.dnum) s[j] = ((xm >> j) & 1 ? xb : yb)[so[j]];
-        U128 acc0{0, 0}, acc1{0, 0};
-#pragma unroll
-        for (int j = 0; j < DMAX; ++j) {
-            if (j < (int)a.dnum) {
-                mac128(acc0, s[j], __ldg(kp + (size_t)(2 * j) * kstride));
-                mac128(acc1, s[j], __ldg(kp + (size_t)(2 * j + 1) * kstride));
             }
         }
         o[(size_t)b * ostride] = redc(acc0, q, qi);
@@ -836,10 +779,7 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
     if (a.dnum <= 4)
         k_key_ip<4><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
     else if (a.dnum <= 8)
-        if (MMFHE_KEYIP_STREAM)
-            k_key_ip_st<8><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
-        else
-            k_key_ip_lr<8><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
+        k_key_ip_lr<8><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
     else
         k_key_ip<16><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
     LAUNCH_CHECK(c);

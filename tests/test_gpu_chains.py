@@ -375,3 +375,17 @@ def test_chain_shape_and_depth_errors(m):
     with pytest.raises(m.MmfheError) as e:
         ctx.chain_plan("no_such_chain", cfg, 3, 6)
     assert e.value.name == "E_INVALID_ARG"
+    # packed K4 rotate-and-sum (R19): frame batches must hold whole packing groups, and the
+    # client is told every key the packing needs
+    bins = [[1], [2]]
+    P8 = toy(log_n=10, n_q=8, scale_bits=40, n_p=2, alpha=2)
+    ctx8 = make_ctx(m, P8)
+    c3 = m.chain_cfg(R=8, F=6, p_phi=2, n_slots=P.n // 2, bands_bins=bins, n_taps=[3, 3], fs=2.0, iq_pack=3)
+    with pytest.raises(m.MmfheError) as e:
+        ctx8.chain_plan("vitals_v2", c3, 7, 12)
+    assert e.value.name == "E_SHAPE"
+    c3 = m.chain_cfg(R=8, F=8, p_phi=2, n_slots=P.n // 2, bands_bins=bins, n_taps=[3, 3], fs=2.0, iq_pack=3)
+    assert len(ctx8.chain_plan("vitals_v2", c3, 7, 16)) == 2
+    rots = ctx.required_rotations("vitals_v2", c3)
+    assert all((8 << j) in rots and (P.n // 2 - (8 << j)) in rots for j in range(3))
+    assert rots == cc.required_rotations("vitals_v2", cc.ChainCfg(R=8, F=8, n_slots=P.n // 2, iq_pack=3), P.n)
