@@ -51,7 +51,7 @@ def c2_config():
     R, F, fs = 128, 256, 20.0
     bins = [band_bins(F - 1, fs, b) for b in BANDS]
     return P, dict(R=R, F=F, fs=fs, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2, bins=bins, n_taps=41,
-                   v1_level=3, v2_level=7, iq_pack=3)
+                   v1_level=3, v2_level=7, iq_pack=3, hoist=1)
 
 
 def c2_bench_config(world):
@@ -62,8 +62,9 @@ def c2_bench_config(world):
             "sessions_per_step_per_gpu": 1, "parallelism": f"session-sharded x{world}",
             "l2": "inputs larger than L2 (1.5 GiB of ciphertexts per step)",
             "inputs": "coefficient form, device-resident; import NTT and export INTT in the step",
-            "k4_rotsum": "packed I/Q rotate-and-sum over 4 frames (DESIGN reading R19, iq_pack = 3: "
-                         "2(2 - 1/4) + 7/4 = 5.25 rotations per frame instead of 14)"}
+            "k4_rotsum": "packed I/Q rotate-and-sum over 4 frames (DESIGN reading R19, iq_pack = 3, hoist = 1: "
+                         "per frame 1.75 packing + 1.75 rotate-and-sum rotations + 1.75 hoisted unpacking "
+                         "rotations sharing one ModUp per 4 frames, instead of 14 rotations)"}
 
 
 # ---------------------------------------------------------------- clocks
@@ -154,7 +155,8 @@ def make_ctx_c2(m, torch, P, cfg, device, seed):
 def chain_cfg_c2(m, cfg):
     return m.chain_cfg(R=cfg["R"], F=cfg["F"], gamma=cfg["gamma"], p_phi=cfg["p_phi"],
                        taylor_order=cfg["taylor_order"], n_slots=cfg["n_slots"], bands_bins=cfg["bins"],
-                       n_taps=[cfg["n_taps"]] * 2, fs=cfg["fs"], iq_pack=cfg.get("iq_pack", 0))
+                       n_taps=[cfg["n_taps"]] * 2, fs=cfg["fs"], iq_pack=cfg.get("iq_pack", 0),
+                       hoist=cfg.get("hoist", 0))
 
 
 def session_inputs(m, torch, gen, P, cfg, device):
@@ -326,7 +328,7 @@ def bench_workload(name, m, torch, device, steps=2, warmup=2):
         F, fs = 200, 20.0
         cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2,
                           bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
-                          frame_batch=40, vp_plus=1, iq_pack=3)
+                          frame_batch=40, vp_plus=1, iq_pack=3, hoist=1)
         chain, lvl, n_in, frames, info = "vitals_v2", 9, 2 * F, F, "F=200 frames, frame_batch 40, VP+ in the cloud"
     # one step = these chain calls (C5v: V1 then V2 on the same session's frames)
     plan = [("vitals_v1", 3, n_in), (chain, lvl, n_in)] if name == "C5v" else [(chain, lvl, n_in)]
@@ -579,7 +581,7 @@ def oracle_sample(frames: int, threads: int):
         return out
 
     ccfg = cc.ChainCfg(R=cfg["R"], F=frames, gamma=2, p_phi=2, taylor_order=1, n_slots=cfg["n_slots"],
-                       fs=cfg["fs"], bands=BANDS, iq_pack=cfg.get("iq_pack", 0))
+                       fs=cfg["fs"], bands=BANDS, iq_pack=cfg.get("iq_pack", 0), hoist=cfg.get("hoist", 0))
     rots = cc.required_rotations("vitals_v2", ccfg, P.n)
     rlk = ukey(prng.SID_UNIFORM)
     gk = {k: ukey(prng.SID_UNIFORM + 100 * (i + 1)) for i, k in enumerate(rots)}

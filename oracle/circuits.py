@@ -437,11 +437,20 @@ def k4_soft_iq(ev, re, im, cfg):
     imd = [ev.drop_to(i, x.level) for i, x in zip(im, m)]
     q_ = ev.relin_rescale_all([ev.tensor_sum([(x, i)]) for x, i in zip(m, imd)])
     if cfg.iq_pack:
-        return k4_packed_rotsum(ev, i_, q_, cfg.R, cfg.iq_pack)
+        return k4_packed_rotsum(ev, i_, q_, cfg.R, cfg.iq_pack, cfg.hoist)
     return ev.rotsum_all(i_, cfg.R, 1), ev.rotsum_all(q_, cfg.R, 1)
 
 
-def k4_packed_rotsum(ev, i_, q_, R, k):
+def unpack_shifts(k):
+    """Block order (in units of R) of the unpacked I list: [0] then, for j = k-1..1,
+    seq ++ [s + 2^j for s in seq] (the order x <- x ++ Rot(x, 2^j R) produces)."""
+    seq = [0]
+    for j in reversed(range(1, k)):
+        seq = seq + [s + (1 << j) for s in seq]
+    return seq
+
+
+def k4_packed_rotsum(ev, i_, q_, R, k, hoist=0):
     """Reading R19: I = rotsum_R(i), Q = rotsum_R(q) for F frames with one rotate-and-sum per
     2^(k-1) frames.  i and q occupy slots 0..R-1 (zeros beyond, reading #23).  Pack:
     x = i + Rot(q, -R) (q to slots R..2R-1), then k-1 times pair the first and second half
@@ -457,6 +466,12 @@ def k4_packed_rotsum(ev, i_, q_, R, k):
         lo, hi = x[:h], x[h:]
         x = [ev.add(a, b) for a, b in zip(lo, [ev.rotate(v, -(R << j)) for v in hi])]
     x = ev.rotsum_all(x, R, 1)
+    if hoist:
+        # every unpacking rotation acts on the packed x: one hoisted group Rot(x, mR),
+        # m = 1..2^k - 1, sharing one ModUp (SURVEY §8(c)-5 hoisted HRot)
+        blocks = [list(x)] + baby_steps(ev, x, [m * R for m in range(1, 1 << k)], 1)
+        seq = unpack_shifts(k)
+        return ([v for s in seq for v in blocks[s]], [v for s in seq for v in blocks[s + 1]])
     for j in reversed(range(1, k)):
         x = x + [ev.rotate(v, R << j) for v in x]
     return x, [ev.rotate(v, R) for v in x]
@@ -553,6 +568,8 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
     if chain in ("k4_soft_iq", "vitals_v2") and cfg.iq_pack:
         for j in range(cfg.iq_pack):
             ks |= {cfg.R << j, -(cfg.R << j)}
+        if cfg.hoist:
+            ks |= {m * cfg.R for m in range(1, 1 << cfg.iq_pack)}
     if chain in ("k3_doppler_dft", "gesture_frame", "gesture"):
         b, giants = k3_schedule(cfg)
         ks |= set(range(1, b))

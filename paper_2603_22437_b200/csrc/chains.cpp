@@ -403,6 +403,27 @@ class Runner {
                 x = ev_rot_add(c_, slice(x, 0, h), slice(x, h, h), -(R << j));
             }
             x = ev_rotsum(c_, x, cfg_.R, 1);
+            if (cfg_.hoist) {
+                // every unpacking rotation acts on the packed x: one hoisted group
+                // Rot(x, mR), m = 1..2^k - 1, sharing one ModUp (oracle k4_packed_rotsum)
+                std::vector<int32_t> st;
+                for (uint32_t mm = 1; mm < (1u << k); ++mm) st.push_back((int32_t)mm * R);
+                std::vector<DCt> blocks;
+                blocks.push_back(std::move(x));
+                for (auto &r : ev_rotate_hoisted(c_, blocks[0], st)) blocks.push_back(std::move(r));
+                std::vector<uint32_t> seq{0};
+                for (uint32_t j = k - 1; j >= 1; --j) {
+                    const size_t n0 = seq.size();
+                    for (size_t i = 0; i < n0; ++i) seq.push_back(seq[i] + (1u << j));
+                }
+                std::vector<DCt> ip, qp;
+                for (uint32_t sft : seq) {
+                    ip.push_back(slice(blocks[sft], 0, blocks[sft].batch));
+                    qp.push_back(slice(blocks[sft + 1], 0, blocks[sft + 1].batch));
+                }
+                DCt I = concat(c_, ip), Q = concat(c_, qp);
+                return {std::move(I), std::move(Q)};
+            }
             for (uint32_t j = k - 1; j >= 1; --j) {
                 DCt hi = ev_rotate(c_, x, R << j);
                 std::vector<DCt> parts;
@@ -576,6 +597,8 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
             add((int64_t)cfg.R << j);
             add(-((int64_t)cfg.R << j));
         }
+        if (cfg.hoist)
+            for (uint32_t mm = 1; mm < (1u << cfg.iq_pack); ++mm) add((int64_t)mm * cfg.R);
     }
     const bool frames = chain == "gesture_frame" || chain == "gesture" || chain == "gesture_features";
     if (chain == "k3_doppler_dft" || frames) {

@@ -334,14 +334,14 @@ def test_vitals_v2_small(m, taps):
 
 
 @pytest.mark.parametrize("taps", [([0.2, 0.3, 0.3, 0.2], [0.25, -0.5, 0.25])])
-@pytest.mark.parametrize("iq_pack", [0, 1, 3])
-def test_vitals_v2_vp_plus(m, taps, iq_pack):
+@pytest.mark.parametrize("iq_pack,hoist", [(0, 0), (1, 0), (3, 0), (3, 1)])
+def test_vitals_v2_vp_plus(m, taps, iq_pack, hoist):
     """Full-depth V2 (VP+ sharpen + weighted frequency average in the cloud):
     N_f, D_f residues and the op trace equal the oracle's."""
     P = toy(log_n=10, n_q=10, scale_bits=50, n_p=2, alpha=2)
     # iq_pack = 3 packs 4 frames: every frame batch a multiple of 4
     cfg = cc.ChainCfg(R=8, F=12 if iq_pack == 3 else 10, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=2.0,
-                      bands=((0.1, 0.6), (0.7, 1.0)), frame_batch=4, vp_plus=1, iq_pack=iq_pack)
+                      bands=((0.1, 0.6), (0.7, 1.0)), frame_batch=4, vp_plus=1, iq_pack=iq_pack, hoist=hoist)
     keys = orc.keygen(P, seed=3501, rotations=cc.required_rotations("vitals_v2", cfg, P.n))
     _, cts = _vital_inputs(P, keys, cfg, 9, 3502)
     taps = [np.array(t) for t in taps]

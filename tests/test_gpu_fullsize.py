@@ -40,7 +40,7 @@ def test_c2_vital_pipeline_full_size(m):
     z, truth = radar.vital_scene(R, F, fs, seed=5001)
     zt = radar.preprocess_vital(z)
     cfg_pack = cc.ChainCfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=fs, bands=bands,
-                           iq_pack=3)
+                           iq_pack=3, hoist=1)
     rots = sorted(set(cc.required_rotations("vitals_v1", cfg, P.n)) |
                   set(cc.required_rotations("vitals_v2", cfg_pack, P.n)))
     keys = orc.keygen(P, seed=5002, rotations=rots)
@@ -69,9 +69,9 @@ def test_c2_vital_pipeline_full_size(m):
     # V2: |X[k]|^2 per band -> BPM; canonical K4 and the packed rotate-and-sum (R19, bench.py)
     I = np.array([dsp.soft_iq(zt[t], 2)[0] for t in range(F)])
     Q = np.array([dsp.soft_iq(zt[t], 2)[1] for t in range(F)])
-    for iq_pack in (0, 3):
+    for iq_pack, hoist in ((0, 0), (3, 1)):
         mcfg = m.chain_cfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=cfg.n_slots, bands_bins=bins,
-                           n_taps=[41, 41], fs=fs, iq_pack=iq_pack)
+                           n_taps=[41, 41], fs=fs, iq_pack=iq_pack, hoist=hoist)
         ctx.prepare_chain("vitals_v2", mcfg, 7, taps=taps)
         lv2 = ctx.chain_plan("vitals_v2", mcfg, 7, 2 * F)
         outs2 = [ct_out(m, P, lv) for lv in lv2]

@@ -233,8 +233,8 @@ def test_vitals_v2_vp_plus(Pg):
         assert abs(60.0 * got_n / got_d - bpm) <= 1e-2  # BPM gate is 1 BPM (north star)
 
 
-@pytest.mark.parametrize("k", [1, 2, 3])
-def test_k4_iq_pack_matches_canonical(Pg, k):
+@pytest.mark.parametrize("k,hoist", [(1, 0), (2, 0), (3, 0), (1, 1), (3, 1)])
+def test_k4_iq_pack_matches_canonical(Pg, k, hoist):
     """Reading R19: K4's packed rotate-and-sum (i, q of 2^(k-1) frames packed into slot blocks,
     one rotsum, unpacked) decrypts to the same I, Q in slot 0 as the two canonical rotsums
      with 2(2 - 2^(1-k)) + log2(R) / 2^(k-1) rotations per frame."""
@@ -243,20 +243,26 @@ def test_k4_iq_pack_matches_canonical(Pg, k):
     cfg = cc.ChainCfg(R=R, F=F, p_phi=2, n_slots=P.n // 2)
     z, _ = radar.vital_scene(R, F, 20.0, seed=1005)
     zt = radar.preprocess_vital(z)
-    cfgp = cc.ChainCfg(R=R, F=F, p_phi=2, n_slots=P.n // 2, iq_pack=k)
+    cfgp = cc.ChainCfg(R=R, F=F, p_phi=2, n_slots=P.n // 2, iq_pack=k, hoist=hoist)
     rots = cc.required_rotations("vitals_v2", cfgp, P.n)
     assert all((R << j) in rots and (P.n // 2 - (R << j)) in rots for j in range(k))
     keys = orc.keygen(P, seed=2005, rotations=rots)
     re = [_enc(P, keys, radar.pack_vital(zt[t].real, cfg.n_slots), 5, 2 * t) for t in range(F)]
     im = [_enc(P, keys, radar.pack_vital(zt[t].imag, cfg.n_slots), 5, 2 * t + 1) for t in range(F)]
     want = np.array([dsp.soft_iq(zt[t], cfg.p_phi) for t in range(F)])
-    for c, n_rot in ((cfg, 2 * 3 * F), (cfgp, int(round(F * (2 * (2 - 2.0 ** (1 - k)) + 3 / 2 ** (k - 1)))))):
+    # rotations per frame: pack 2 - 2^(1-k), rotsum log2(R) / 2^(k-1), unpack 2 - 2^(1-k)
+    # (plain) or (2^k - 1) / 2^(k-1) hoisted rotations sharing one ModUp per group
+    packed = F * ((2 - 2.0 ** (1 - k)) + 3 / 2 ** (k - 1)) + F * (((1 << k) - 1) / 2 ** (k - 1) if hoist
+                                                                  else 2 - 2.0 ** (1 - k))
+    for c, n_rot in ((cfg, 2 * 3 * F), (cfgp, int(round(packed)))):
         ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
         I, Q = cc.k4_soft_iq(ev, re, im, c)
         got_i = np.array([orc.decrypt_vector(P, keys, x)[0] for x in I])
         got_q = np.array([orc.decrypt_vector(P, keys, x)[0] for x in Q])
         assert rel_err(got_i, want[:, 0]) < 1e-3 and rel_err(got_q, want[:, 1]) < 1e-3
-        assert sum(1 for op in ev.trace if op[0] == "hrot") == n_rot
+        assert sum(1 for op in ev.trace if op[0] in ("hrot", "hrot_hoisted")) == n_rot
+        assert sum(1 for op in ev.trace if op[0] == "hrot_hoisted") == (F * ((1 << k) - 1) // (1 << (k - 1))
+                                                                      if c.hoist else 0)
 
 
 def test_trace_is_data_oblivious(Pg):
