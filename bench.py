@@ -272,14 +272,20 @@ def run_gpu(args, rank, world, device):
                 ctx.eval_chain_async(chain, mcfg, hin[chain], hout[chain])
         ctx.sync()
         e_steps = max(3, args.steps)
+        if dist:
+            tdist.barrier()
         t0 = time.perf_counter()
         for _ in range(e_steps):
             for chain in hin:
                 ctx.eval_chain_async(chain, mcfg, hin[chain], hout[chain])
         ctx.sync()
         e_s = (time.perf_counter() - t0) / e_steps
+        if dist:  # the slowest rank's wall clock
+            te = torch.tensor([e_s], dtype=torch.float64, device=device)
+            tdist.all_reduce(te, op=tdist.ReduceOp.MAX)
+            e_s = float(te.item())
         e2e = {"value": cfg["F"] * world / e_s, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_s * 1e3, "clock": "host wall, per rank",
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_s * 1e3, "clock": "host wall, max over ranks",
                "api": "mmfhe_eval_chain_async (pinned host buffers, copy/compute overlap across steps)"}
 
     extras = {}
@@ -727,10 +733,14 @@ def main():
         return
 
     import torch
+    # one process per GPU; MMFHE_BENCH_BACKEND=gloo (ranks sharing a GPU) only checks the
+    # multi-rank logic on a one-GPU box -- its timings are not a scaling measurement
+    backend = os.environ.get("MMFHE_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend == "gloo" else local
     if world > 1:
         import torch.distributed as tdist
         torch.cuda.set_device(local)
-        tdist.init_process_group("nccl")
+        tdist.init_process_group(backend)
     device = torch.device("cuda", local)
     r = run_gpu(args, rank, world, device)
     peaks = {}

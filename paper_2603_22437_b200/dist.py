@@ -37,6 +37,11 @@ def allgather_partials(local, group=None):
         return local.unsqueeze(0)
     world = dist.get_world_size(group)
     k = local.shape[0]
+    if dist.get_backend(group) == "gloo" and local.is_cuda:
+        # gloo (multi-process checks on one GPU) gathers host tensors; NCCL gathers in HBM
+        parts = [torch.empty_like(local, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, local.cpu(), group=group)
+        return torch.stack(parts).to(local.device)
     out = torch.empty((world * k,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, local, group=group)  # rank-major concatenation
     return out.view((world, k) + tuple(local.shape[1:]))
