@@ -92,11 +92,11 @@ void run_and_export(Ctx &c, const char *chain, const mmfhe_chain_cfg &cfg, const
 {
     std::vector<DCt> res = run_chain(c, chain, cfg, in, n_in);
     size_t o = 0;
-    for (auto &d : res)
-        for (uint32_t b = 0; b < d.batch; ++b) {
-            MMFHE_REQUIRE(o < n_out, MMFHE_E_LAYOUT, "chain produced an unexpected number of outputs");
-            export_ct(c, slice(d, b, 1), out[o++]);
-        }
+    for (auto &d : res) {
+        MMFHE_REQUIRE(o + d.batch <= n_out, MMFHE_E_LAYOUT, "chain produced an unexpected number of outputs");
+        export_batch(c, d, out + o);
+        o += d.batch;
+    }
     MMFHE_REQUIRE(o == n_out, MMFHE_E_LAYOUT, "chain produced an unexpected number of outputs");
 }
 
@@ -593,7 +593,7 @@ mmfhe_status mmfhe_hrot_batch(mmfhe_ctx *ctx, const mmfhe_ct *a, size_t n, int32
     MMFHE_REQUIRE(a && out && n, MMFHE_E_INVALID_ARG, "null argument");
     DCt x = import_batch(*ctx, a, 0, 1, n);  // one batched KS: each evk word read once for all n
     DCt r = ev_rotate(*ctx, x, step);
-    for (size_t i = 0; i < n; ++i) export_ct(*ctx, slice(r, (uint32_t)i, 1), out[i]);
+    export_batch(*ctx, r, out);
     API_END(ctx)
 }
 
@@ -603,7 +603,7 @@ mmfhe_status mmfhe_hmult_batch(mmfhe_ctx *ctx, const mmfhe_ct *a, const mmfhe_ct
     MMFHE_REQUIRE(a && b && out && n, MMFHE_E_INVALID_ARG, "null argument");
     DCt x = import_batch(*ctx, a, 0, 1, n), y = import_batch(*ctx, b, 0, 1, n);
     DCt r = ev_relin(*ctx, ev_tensor_sum(*ctx, {{&x, &y}}));
-    for (size_t i = 0; i < n; ++i) export_ct(*ctx, slice(r, (uint32_t)i, 1), out[i]);
+    export_batch(*ctx, r, out);
     API_END(ctx)
 }
 

@@ -177,6 +177,55 @@ void export_ct(Ctx &c, const DCt &in, mmfhe_ct &out)
     }
 }
 
+// Every item of a batch to its own output: one out-of-place INTT of the whole batch into a
+// staging buffer (coefficient-form outputs), then one scatter launch per 64 device outputs
+// or one D2H copy per host output -- instead of two INTT launches per ciphertext.
+void export_batch(Ctx &c, const DCt &in, mmfhe_ct *outs)
+{
+    const uint32_t B = in.batch;
+    bool uniform = B > 1;
+    for (uint32_t b = 0; uniform && b < B; ++b) {
+        const mmfhe_ct &o = outs[b];
+        uniform = o.data != nullptr && o.form == outs[0].form && o.on_device == outs[0].on_device &&
+                  (!o.on_device || ((uintptr_t)o.data & 15) == 0);
+    }
+    if (!uniform) {
+        for (uint32_t b = 0; b < B; ++b) export_ct(c, slice(in, b, 1), outs[b]);
+        return;
+    }
+    const size_t words = in.item_words();
+    const uint32_t rows = in.rows() / B;  // per item
+    const uint64_t *src = in.data();
+    DBuf tmp;
+    if (outs[0].form == MMFHE_FORM_COEFF) {
+        tmp = DBuf(words * B, c.stream);
+        const InvSrc is{in.data(), words, c.n, rows, 1};
+        ntt_inverse(c, tmp.get(), rows * B, qmap(c, in.level), &is);
+        src = tmp.get();
+    }
+    for (uint32_t b = 0; b < B; ++b) {
+        mmfhe_ct &o = outs[b];
+        o.log_n = c.log_n;
+        o.level = in.level;
+        o.scale = in.scale;
+        o.n_slots = in.n_slots;
+        o.n_polys = in.npolys;
+    }
+    if (outs[0].on_device) {
+        for (uint32_t b0 = 0; b0 < B; b0 += kMaxTerms) {
+            const int n = (int)std::min<uint32_t>(kMaxTerms, B - b0);
+            PtrList dst{};
+            for (int i = 0; i < n; ++i) dst.p[i] = outs[b0 + i].data;
+            launch_scatter(c, dst, src + (size_t)b0 * words, n, words);
+        }
+    } else {
+        for (uint32_t b = 0; b < B; ++b)
+            CUDA_CHECK(cudaMemcpyAsync(outs[b].data, src + (size_t)b * words, words * 8, cudaMemcpyDeviceToHost,
+                                       c.stream));
+        CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    }
+}
+
 // ------------------------------------------------------------------ exact ops
 DCt ev_addsub(Ctx &c, const DCt &a, const DCt &b, bool sub)
 {

@@ -63,6 +63,8 @@ void launch_batch_sum(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t B, uin
 // out[b] = copy of src.p[b] (n <= kMaxTerms items of `words` words each; device pointers,
 // 16-byte aligned).
 void launch_gather(Ctx &c, uint64_t *out, const PtrList &src, int n, size_t words);
+// dst.p[b] (written through) = in + b*words, b < n <= kMaxTerms (16-byte aligned destinations).
+void launch_scatter(Ctx &c, const PtrList &dst, const uint64_t *in, int n, size_t words);
 // c0 of every item (item stride s) += pt (pt in Montgomery form).
 void launch_add_plain(Ctx &c, uint64_t *c0, size_t s, const uint64_t *pt_mont, uint32_t level, uint32_t B);
 

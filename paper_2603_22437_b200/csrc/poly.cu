@@ -915,6 +915,28 @@ void launch_gather(Ctx &c, uint64_t *out, const PtrList &src, int n, size_t word
     LAUNCH_CHECK(c);
 }
 
+// dst.p[b] (as writable) = in + b * words, b < n (16-byte aligned destinations)
+__global__ void k_scatter(PtrList dst, const uint64_t *__restrict__ in, size_t words)
+{
+    const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+    if (i >= words) return;
+    uint64_t *o = const_cast<uint64_t *>(dst.p[blockIdx.y]);
+    const uint64_t *s = in + (size_t)blockIdx.y * words;
+    if (i + 1 < words) {
+        *(ulonglong2 *)(o + i) = *(const ulonglong2 *)(s + i);
+    } else {
+        o[i] = s[i];
+    }
+}
+
+void launch_scatter(Ctx &c, const PtrList &dst, const uint64_t *in, int n, size_t words)
+{
+    ProfScope ps(c, "scatter", 16.0 * words * n);
+    const size_t threads = (words + 1) / 2;
+    k_scatter<<<dim3((unsigned)((threads + kTB - 1) / kTB), n), kTB, 0, c.stream>>>(dst, in, words);
+    LAUNCH_CHECK(c);
+}
+
 void launch_add_plain(Ctx &c, uint64_t *c0, size_t s, const uint64_t *pt_mont, uint32_t level, uint32_t B)
 {
     ProfScope ps(c, "add_plain", 8.0 * (level + 1) * c.n * (1.0 + 2.0 * B));
