@@ -182,16 +182,6 @@ class Runner {
     }
 
     // K1 for S sessions at once: re[t], im[t] are batches over the sessions
-    DCt k1_energy_sessions(const std::vector<DCt> &re, const std::vector<DCt> &im)
-    {
-        std::vector<std::pair<const DCt *, const DCt *>> pairs;
-        for (size_t t = 0; t < re.size(); ++t) {
-            pairs.push_back({&re[t], &re[t]});
-            pairs.push_back({&im[t], &im[t]});
-        }
-        return ev_relin_rescale(c_, ev_tensor_sum(c_, pairs));
-    }
-
     std::pair<DCt, DCt> k2_soft_attention(const DCt &E)
     {
         DCt w = copy_ct(c_, E);
@@ -672,13 +662,12 @@ std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_c
     std::vector<DCt> out;
     if (chain == "k1_energy") {
         // sessions batched: frame t of every session forms one batch (one launch per op)
+        // one import of every session's frames (session-major), then the per-session sum of
+        // squares reads frame t of every session at item stride 2F: the same op sequence as
+        // k1_energy_sessions on per-frame batches, without 2F separate imports
         const uint32_t F = cfg.F, S = (uint32_t)(n_in / (2 * (size_t)F));
-        std::vector<DCt> re, im;
-        for (uint32_t t = 0; t < F; ++t) {
-            re.push_back(import_batch(c, in, 2 * (size_t)t, 2 * (size_t)F, S));
-            im.push_back(import_batch(c, in, 2 * (size_t)t + 1, 2 * (size_t)F, S));
-        }
-        out.push_back(r.k1_energy_sessions(re, im));
+        DCt all = import_batch(c, in, 0, 1, n_in);
+        out.push_back(ev_relin_rescale(c, ev_square_sum_items(c, all, 2 * F, S)));
     } else if (chain == "vitals_v1") {
         DCt re = import_batch(c, in, 0, 2, n_in / 2);
         DCt im = import_batch(c, in, 1, 2, n_in / 2);

@@ -298,6 +298,23 @@ DCt ev_tensor_sum(Ctx &c, const std::vector<std::pair<const DCt *, const DCt *>>
     return r;
 }
 
+// K1 over session-major inputs: all = [S][m] contiguous items; out_s = sum_{t<m} x_{s,t} (x) x_{s,t}
+// (the same op and trace as ev_tensor_sum over the m per-frame batches of S sessions, without
+// gathering those batches: operand t is at item offset t with item stride m)
+DCt ev_square_sum_items(Ctx &c, const DCt &all, uint32_t m, uint32_t S)
+{
+    MMFHE_REQUIRE(all.npolys == 2 && m >= 1 && all.batch == m * S, MMFHE_E_LAYOUT, "square sum layout");
+    rec_n(c, "tensor_sum", all.level, S, std::to_string(m));
+    DCt r = make_ct(c, all.level, 3, all.n_slots, all.scale * all.scale, S);
+    for (uint32_t s0 = 0; s0 < m; s0 += kMaxTerms) {
+        PtrList A{};
+        const int n = (int)std::min<uint32_t>(kMaxTerms, m - s0);
+        for (int i = 0; i < n; ++i) A.p[i] = all.item(s0 + i);
+        launch_tensor_sum(c, r.data(), r.item_words(), A, A, (size_t)m * all.item_words(), n, all.level, s0 > 0, S);
+    }
+    return r;
+}
+
 DCt ev_pmult_sum(Ctx &c, const std::vector<std::pair<const DPlain *, const DCt *>> &terms)
 {
     MMFHE_REQUIRE(!terms.empty(), MMFHE_E_INVALID_ARG, "empty pmult sum");

@@ -49,6 +49,8 @@ void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t level, uint
                   uint64_t *out, size_t os, const uint64_t *add0, const uint64_t *add1, size_t as);
 DCt ev_relin(Ctx &c, const DCt &a3);
 DCt ev_rotate(Ctx &c, const DCt &a, int32_t step);
+// sum over the m items of each of S sessions (all = [S][m] items) of x (x) x
+DCt ev_square_sum_items(Ctx &c, const DCt &all, uint32_t m, uint32_t S);
 // Hoisted HRot: one ModUp of c1 shared by every step; per step the
 // ModUp'd digits are permuted by sigma_g, then IP + ModDown.  A separate op from
 // ev_rotate (different residues, same decryption).
