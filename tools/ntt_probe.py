@@ -1,5 +1,5 @@
-"""NTT probe: per-pass throughput of the batched forward/inverse NTT at N = 2^14 (PS2)
-and N = 2^16 (PS4) on cuda:0, against the in-run CT/GS butterfly microbenchmarks.
+"""NTT probe: per-pass throughput of the batched forward/inverse NTT at N = 2^13 (PS1),
+2^14 (PS2), 2^15 (PS3) and 2^16 (PS4) on cuda:0, against the in-run CT/GS butterfly microbenchmarks.
 Usage: python tools/ntt_probe.py [iters]   (also the target for ncu captures)."""
 import os
 import sys
@@ -8,10 +8,10 @@ sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", os.path.dirname(os.path.dir
 import torch  # noqa: E402
 
 from paper_2603_22437_b200 import mmfhe as m  # noqa: E402
-from synth.params import ps2, ps4  # noqa: E402
+from synth.params import ps1, ps2, ps3, ps4  # noqa: E402
 
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-for P, rows in ((ps2(), 4096), (ps4(), 1020)):
+for P, rows in ((ps1(), 8192), (ps2(), 4096), (ps3(), 2048), (ps4(), 1020)):
     ctx = m.Context.from_params(P)
     primes = list(P.q)
     idx = [i % len(primes) for i in range(rows)]
