@@ -149,7 +149,11 @@ struct IPArgs {
 // Low-register variant for 5..8 digits: 32-bit in-item source offsets instead of
 // per-digit pointers and strides, held to 3 CTAs/SM (78 registers, no spills; the
 // pointer version needs 121 and fits 2).  Measured on C2: 9.6 -> 8.9 ms/step.  For
-// <= 4 digits the pointer version (k_key_ip, no min-blocks bound) is faster.  Re-reading
+// <= 4 digits the pointer version (k_key_ip, no min-blocks bound) is faster.  Measured and
+// not kept: re-reading the key words per item from L2 (64 registers, 4 CTAs/SM: 12% slower
+// on C2) and one output pair per thread with 4 items per CTA sharing the key words through
+// L1 (C2 5.3 -> 7.3 ms/step, C4 66 -> 99 ms): holding a coefficient's key words in
+// registers across the batch items is what makes this kernel cheap.  Re-reading
 // the key words per item from L2 instead (64 registers, 4 CTAs/SM) measured 12% slower.
 template <int DMAX>
 __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
