@@ -153,8 +153,7 @@ struct IPArgs {
 // not kept: re-reading the key words per item from L2 (64 registers, 4 CTAs/SM: 12% slower
 // on C2) and one output pair per thread with 4 items per CTA sharing the key words through
 // L1 (C2 5.3 -> 7.3 ms/step, C4 66 -> 99 ms): holding a coefficient's key words in
-// registers across the batch items is what makes this kernel cheap.  Re-reading
-// the key words per item from L2 instead (64 registers, 4 CTAs/SM) measured 12% slower.
+// registers across the batch items is what makes this kernel cheap.
 template <int DMAX>
 __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
                                                 const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
