@@ -395,7 +395,7 @@ def bench_workload(name, m, torch, device, steps=2, warmup=2):
     return res
 
 
-def bench_c5(m, torch, device, rank, world, sessions_per_rank=1, F=100, steps=2, warmup=1):
+def bench_c5(m, torch, device, rank, world, sessions_per_rank=1, F=100, steps=2, warmup=2):
     """C5 batched multi-session gesture serving (BASELINE configs[4]) with the method's one
     exchange step: G = sessions_per_rank * world sessions per step; every session's F
     frames are sharded over the ranks (paper_2603_22437_b200.dist.shard); each rank runs
@@ -435,18 +435,22 @@ def bench_c5(m, torch, device, rank, world, sessions_per_rank=1, F=100, steps=2,
                          for s in range(G)]
     mine = [s for s in range(G) if mdist.owner(s, world) == rank]
     ctx.trace_enable(False)
+    # persistent chain output buffers: stable addresses, so the library's chain graphs are
+    # captured during warm-up and replayed in the timed steps (never captured inside them)
+    lvf = ctx.chain_plan("gesture_features", cfg, lvl, len(frames_by_session[0]))[0]
+    lvo = ctx.chain_plan("gesture_fc", cfg, lvf, 1)[0]
+    feat_bufs = torch.empty((G, 2, lvf + 1, P.n), dtype=torch.int64, device=device)
+    sum_bufs = {s: torch.empty((2, lvf + 1, P.n), dtype=torch.int64, device=device) for s in mine}
+    fc_outs = {s: m.Ct(torch.empty((2, lvo + 1, P.n), dtype=torch.int64, device=device), lvo, 0.0, 0, P.log_n,
+                       m.FORM_EVAL) for s in mine}
 
     def step():
-        partials, lv, sc = mdist.sessions_features(ctx, m, cfg, frames_by_session, lvl, scale, 4096, P.log_n, device)
+        partials, lv, sc = mdist.sessions_features(ctx, m, cfg, frames_by_session, lvl, scale, 4096, P.log_n, device,
+                                                   bufs=feat_bufs)
         gathered = mdist.allgather_partials(partials)
-        logits = []
         for s in mine:
-            total = mdist.reduce_partials(ctx, m, gathered, s, lv, sc, 4096, P.log_n)
-            lvo = ctx.chain_plan("gesture_fc", cfg, lv, 1)[0]
-            o = m.Ct(torch.empty((2, lvo + 1, P.n), dtype=torch.int64, device=device), lvo, 0.0, 0, P.log_n,
-                     m.FORM_EVAL)
-            ctx.eval_chain("gesture_fc", cfg, [total], [o])
-            logits.append(o)
+            total = mdist.reduce_partials(ctx, m, gathered, s, lv, sc, 4096, P.log_n, buf=sum_bufs[s])
+            ctx.eval_chain("gesture_fc", cfg, [total], [fc_outs[s]])
         return partials.numel() * 8
 
     for _ in range(warmup):

@@ -47,26 +47,32 @@ def allgather_partials(local, group=None):
     return out.view((world, k) + tuple(local.shape[1:]))
 
 
-def sessions_features(ctx, m, cfg, frames_by_session, level, scale, n_slots, log_n, device):
+def sessions_features(ctx, m, cfg, frames_by_session, level, scale, n_slots, log_n, device, bufs=None):
     """Partial features of this rank's frame shard for every session: one ciphertext per
-    session, stacked [S, 2, level_out+1, N] (device, int64 view of the residues)."""
+    session, stacked [S, 2, level_out+1, N] (device, int64 view of the residues).  `bufs`:
+    optional persistent [S, 2, level_out+1, N] output tensor (stable buffer addresses let the
+    library replay its captured chain graphs from call to call)."""
     import torch
 
     outs = []
-    for ins in frames_by_session:
+    for s, ins in enumerate(frames_by_session):
         lv = ctx.chain_plan("gesture_features", cfg, level, len(ins))[0]
-        o = m.Ct(torch.empty((2, lv + 1, 1 << log_n), dtype=torch.int64, device=device), lv, 0.0, 0, log_n,
-                 m.FORM_EVAL)
+        data = bufs[s] if bufs is not None else torch.empty((2, lv + 1, 1 << log_n), dtype=torch.int64,
+                                                            device=device)
+        o = m.Ct(data, lv, 0.0, 0, log_n, m.FORM_EVAL)
         ctx.eval_chain("gesture_features", cfg, ins, [o])
         outs.append(o)
-    return torch.stack([o.data for o in outs]), outs[0].level, outs[0].scale
+    stacked = bufs if bufs is not None else torch.stack([o.data for o in outs])
+    return stacked, outs[0].level, outs[0].scale
 
 
-def reduce_partials(ctx, m, gathered, session, level, scale, n_slots, log_n):
-    """Library-side modular sum of session `session`'s partials from every rank."""
+def reduce_partials(ctx, m, gathered, session, level, scale, n_slots, log_n, buf=None):
+    """Library-side modular sum of session `session`'s partials from every rank (into the
+    optional persistent tensor `buf`)."""
     import torch
 
     parts = [m.Ct(gathered[r, session], level, scale, n_slots, log_n, m.FORM_EVAL) for r in range(gathered.shape[0])]
-    out = m.Ct(torch.empty_like(gathered[0, session]), level, 0.0, 0, log_n, m.FORM_EVAL)
+    out = m.Ct(buf if buf is not None else torch.empty_like(gathered[0, session]), level, 0.0, 0, log_n,
+               m.FORM_EVAL)
     ctx.sum_partials(parts, out)
     return out

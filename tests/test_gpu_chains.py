@@ -88,6 +88,39 @@ def test_k1_energy_multi_session(m):
     assert ctx.trace() == ev.trace
 
 
+def test_k1_energy_multi_session_host_outputs(m):
+    """Batched export (one INTT per output batch) into host and device output buffers, and
+    NTT-form outputs: the same residues as the oracle (coefficient form) in every case."""
+    P = toy(log_n=11, n_q=3, scale_bits=40, n_p=1, alpha=1)
+    cfg = cc.ChainCfg(R=16, F=2, n_slots=P.n // 2)
+    keys = orc.keygen(P, seed=3041)
+    sessions, cts = [], []
+    for s in range(4):
+        _, c = _vital_inputs(P, keys, cfg, 1, 3050 + 10 * s)
+        sessions.append((c[0::2], c[1::2]))
+        cts += c
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    want = cc.k1_energy_sessions(ev, sessions)
+    ctx = make_ctx(m, P, keys)
+    mcfg = _mcfg(m, cfg)
+    levels = ctx.chain_plan("k1_energy", mcfg, 1, len(cts))
+    ins = [ct_in(m, P, c) for c in cts]
+    for device in (False, True):
+        outs = [ct_out(m, P, lv, device=device) for lv in levels]
+        assert ctx.eval_chain("k1_energy", mcfg, ins, outs) == len(want)
+        for o, w in zip(outs, want):
+            assert np.array_equal(residues(o), np.stack(w.c))
+            assert o.scale == w.scale and o.level == w.level
+    # NTT-form device outputs, converted back through the library's own INTT
+    outs = [ct_out(m, P, lv) for lv in levels]
+    for o in outs:
+        o.form = m.FORM_EVAL
+    ctx.eval_chain("k1_energy", mcfg, ins, outs)
+    for o, w in zip(outs, want):
+        ctx.ntt(o.data.view(-1, P.n), [i % (o.level + 1) for i in range(2 * (o.level + 1))], inverse=True)
+        assert np.array_equal(residues(o), np.stack(w.c))
+
+
 def test_k3_multi_frame_batches(m):
     P = toy(log_n=10, n_q=4, scale_bits=40, n_p=2, alpha=2)
     cfg = cc.ChainCfg(A=2, R=4, D=8, F=3, n_slots=64, frame_batch=2, hoist=1)
