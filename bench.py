@@ -523,6 +523,22 @@ def extras_n16(args, m, torch, device, batch=8, reps=3):
         res[f"{name}_alg_gbs"] = ops * alg / 1e9
     # SURVEY §8(d) variants 2 and 3: one ciphertext per op (the 81 MiB evk streamed for every
     # rotation: the worst case) and a hoisted group of 8 rotations of one ciphertext
+    # batch 64 sharing the key (SURVEY §8(d) metric 2: "batch 1 and batch 64 sharing a key")
+    data64 = uniform_dev(torch, gen, (64, 2, L + 1), list(P.q), P.n, device)
+    cts64 = [m.Ct(data64[i], L, scale, P.n // 2, P.log_n, m.FORM_EVAL) for i in range(64)]
+    obuf64 = torch.empty((64, 2, L + 1, P.n), dtype=torch.int64, device=device)
+    outs64 = [m.Ct(obuf64[i], L, 0.0, 0, P.log_n, m.FORM_EVAL) for i in range(64)]
+    ctx.hrot_batch(cts64, 1, outs64)
+    torch.cuda.synchronize(device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.hrot_batch(cts64, 1, outs64)
+    e1.record(stream)
+    torch.cuda.synchronize(device)
+    s64 = e0.elapsed_time(e1) / 1e3
+    res["hrot_b64_us"] = s64 / 64 * 1e6
+    res["hrot_b64_alg_gbs"] = (64 * 2 * ct_bytes + evk) / s64 / 1e9
+    del data64, obuf64, cts64, outs64
     steps8 = list(range(1, 9))
     for k in steps8[1:]:
         ctx.load_galois_key(k, uniform_dev(torch, gen, key_shape, basis, P.n, device))
@@ -561,7 +577,7 @@ def extras_n16(args, m, torch, device, batch=8, reps=3):
                         f"{peaks['bfly'] / 1e9:.0f} G bfly/s, {peaks['mac'] / 1e9:.0f} G MAC/s, "
                         f"{peaks['mm'] / 1e9:.0f} G modmul/s; int_frac = model time / measured time")
     res["config"] = ("PS4: N=2^16, 20 Q + 7 P limbs, dnum 3, top level, eval form; hrot/hmult: batch of 8 "
-                     "distinct cts, one key; hrot_b1: one ct per call; hrot_hoisted8: steps 1..8 of one ct "
+                     "distinct cts, one key; hrot_b64: batch of 64 sharing the key; hrot_b1: one ct per call; hrot_hoisted8: steps 1..8 of one ct "
                      "(one ModUp, 8 inner products + ModDowns, 8 keys)")
     ctx.close()
     return res
