@@ -22,6 +22,7 @@ session per step; no collective on the data path (weak scaling).
 from __future__ import annotations
 
 import argparse
+import math
 import json
 import os
 import statistics
@@ -296,6 +297,17 @@ def run_gpu(args, rank, world, device):
                 extras[wl] = bench_workload(wl, m, torch, device)
             except Exception as e:  # report, do not hide
                 extras[wl] = {"error": f"{type(e).__name__}: {e}"}
+        if dist:
+            # C5's vital half: one full-depth session per rank (session sharding, no exchange);
+            # aggregate over ranks with the slowest rank's device time (every rank joins the
+            # reduction, a failed rank contributes +inf)
+            t5 = torch.tensor([extras.get("C5v", {}).get("ms_per_step", float("inf"))], dtype=torch.float64,
+                              device=device)
+            tdist.all_reduce(t5, op=tdist.ReduceOp.MAX)
+            if math.isfinite(float(t5.item())):
+                extras["C5v"]["n_gpus"] = world
+                extras["C5v"]["frames_per_s_all_ranks"] = (world * extras["C5v"]["frames_per_step"] /
+                                                           (float(t5.item()) / 1e3))
     if not args.no_c5:
         extras["C5"] = bench_c5(m, torch, device, rank, world)
     return dict(value=value, ms=ms_max / args.steps, launches=launches, clocks=clk.summary(), prof=prof,
