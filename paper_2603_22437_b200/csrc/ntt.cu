@@ -382,7 +382,9 @@ __device__ __forceinline__ void inv_bfly(uint64_t (&v)[Gm::E], int r, int ktr, i
 
 // ---------------------------------------------------------------- forward
 // Round widths: the first (top) round takes LOGS - (R-1)*ELOG bits, the others ELOG.
-template <int LOGS, int OTHER, bool COL>
+// EPI (row pass only): the RowEpi epilogue replaces the plain store; a separate instantiation
+// so that the plain pass carries none of its code or registers
+template <int LOGS, int OTHER, bool COL, bool EPI = false>
 __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *__restrict__ data, KTables kt, PrimeMap pm, RowMap rm,
                                                                       ColSrc cs, RowEpi ep)
 {
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
             for (int e = 0; e < E; ++e) v[e] = b[soff<Gm, LOGS, COL>(sb, kmap(ELOG, lo, w, 0, e))];
         }
         fwd_bfly<Gm, LOGS>(v, r, ktr, COL ? 0 : gi, tw, q);
-        if (r == R - 1 && !COL && ep.out != nullptr) {
+        if (r == R - 1 && !COL && EPI) {
             // fused epilogue (RowEpi): (X - v) mul + addends, written to ep.out
             constexpr int LOL = FwdGeo<Gm, LOGS>::lo(R - 1), WL = FwdGeo<Gm, LOGS>::w(R - 1);
             const float qinv = qinv_est(q);
@@ -584,10 +586,15 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
     // prefer the shared-memory carveout: residency is bounded by registers, not by L1
     static const bool attr = [] {
         if (FWD)
-            CUDA_CHECK(cudaFuncSetAttribute(ntt_fwd_pass<LOGS, OTHER, COL>,
+        {
+            CUDA_CHECK(cudaFuncSetAttribute(ntt_fwd_pass<LOGS, OTHER, COL, false>,
                                             cudaFuncAttributePreferredSharedMemoryCarveout,
                                             cudaSharedmemCarveoutMaxShared));
-        else
+            if (!COL)
+                CUDA_CHECK(cudaFuncSetAttribute(ntt_fwd_pass<LOGS, OTHER, COL, true>,
+                                                cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                cudaSharedmemCarveoutMaxShared));
+        } else
             CUDA_CHECK(cudaFuncSetAttribute(ntt_inv_pass<LOGS, OTHER, COL>,
                                             cudaFuncAttributePreferredSharedMemoryCarveout,
                                             cudaSharedmemCarveoutMaxShared));
@@ -595,9 +602,13 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
     }();
     (void)attr;
     auto go = [&](dim3 grid, uint64_t *dd, RowMap rm, const ColSrc &src) {
-        if constexpr (FWD)
-            ntt_fwd_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm, src,
-                                                                              (!COL && ep) ? *ep : RowEpi{});
+        if constexpr (FWD) {
+            if (!COL && ep)
+                ntt_fwd_pass<LOGS, OTHER, COL, true><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm, src, *ep);
+            else
+                ntt_fwd_pass<LOGS, OTHER, COL, false><<<grid, Gm::THREADS, Gm::SMEM, s>>>(dd, kt, pm, rm, src,
+                                                                                         RowEpi{});
+        }
         else
             ntt_inv_pass<LOGS, OTHER, COL><<<grid, Gm::THREADS, Gm::SMEM, s>>>(
                 dd, kt, pm, rm, !is ? InvSrc{} : !COL ? *is : InvSrc{nullptr, 0, 0, 1, 1, is->add_half});
