@@ -761,7 +761,7 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the multi-GPU C5 exchange workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-frames", type=int, default=4)
+    ap.add_argument("--ref-frames", type=int, default=16)
     ap.add_argument("--profile-out", default="")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "mmfhe" else args.warmup
