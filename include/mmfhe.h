@@ -186,7 +186,13 @@ mmfhe_status mmfhe_load_scalars(mmfhe_ctx *ctx, const char *name, const double *
  * "gesture_frame", "gesture_fc", "gesture" (frames + accumulate + FC).
  * in[0..n_in): input ciphertexts in the order the chain documents (DESIGN.md
  * §2): k1/vitals: re_0, im_0, re_1, im_1, ...; gesture*: v_re_t, v_im_t per frame.
- * out: caller buffers; mmfhe_chain_plan tells their count and levels.
+ * Outputs: k1_energy one E per session; vitals_v1 (N, D); vitals_v2 the P_k of every
+ * band's bins in band order, or with cfg.vp_plus (N_f, D_f) per band; k3_doppler_dft
+ * per frame batch its d_re items then its d_im items; gesture_frame one f per frame;
+ * gesture / gesture_fc the logits.  Every output is valid in slot 0 (or the documented
+ * slots); other slots may hold partial sums.
+ * out: caller buffers; mmfhe_chain_plan tells their count and levels.  Outputs leave
+ * through one batched INTT (coefficient form) per output batch.
  * MMFHE_E_SHAPE on a frame-count mismatch, MMFHE_E_DEPTH if in_level is too
  * low, MMFHE_E_MISSING_KEY / MMFHE_E_MISSING_PLAIN for absent operands.
  * Graph replay: when every input and output is device-resident and trace and
