@@ -153,7 +153,10 @@ struct IPArgs {
 // not kept: re-reading the key words per item from L2 (64 registers, 4 CTAs/SM: 12% slower
 // on C2) and one output pair per thread with 4 items per CTA sharing the key words through
 // L1 (C2 5.3 -> 7.3 ms/step, C4 66 -> 99 ms): holding a coefficient's key words in
-// registers across the batch items is what makes this kernel cheap.
+// registers across the batch items is what makes this kernel cheap.  Also not kept: two
+// items per loop iteration (both items' source loads in flight before the MACs) spills
+// 396 B at 3 CTAs/SM (C2 5194 -> 5000 frames/s) and at 2 CTAs/SM (no spills) is 0.6%
+// slower (5165): the kernel already has enough loads in flight at 3 CTAs/SM.
 template <int DMAX>
 __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
                                                 const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
