@@ -581,7 +581,16 @@ __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out,
 // outputs' input pairs slide along the window (two shared-memory reads per tap for all
 // kSymJB outputs) and each tap is one 64x64->128 multiply-accumulate per output, reduced
 // once at the end (hi word brought below q, then one Montgomery reduction).
-constexpr int kSymK = 128, kSymJT = 32, kSymSplit = 2, kSymJB = 4;
+// Tile sweep on C2 (profiles/r01/sym_variants*_r01p.log, parity green for each): JB 4 /
+// split 2 (kept) 5194 frames/s; JB 8: 5073; split 4: 4975; split 1 with JB 4 / 8 / 16:
+// 5172-5182 / 5172-5191 / 5095 -- the defaults are at the optimum within run-to-run noise.
+#ifndef MMFHE_SYM_JB
+#define MMFHE_SYM_JB 4
+#endif
+#ifndef MMFHE_SYM_SPLIT
+#define MMFHE_SYM_SPLIT 2
+#endif
+constexpr int kSymK = 128, kSymJT = 32, kSymSplit = MMFHE_SYM_SPLIT, kSymJB = MMFHE_SYM_JB;
 
 __global__ void __launch_bounds__(kSymK *kSymSplit) k_lincomb_sym(uint64_t *__restrict__ out,
                                                                   const uint64_t *__restrict__ in, uint32_t M,
