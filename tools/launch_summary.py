@@ -14,9 +14,13 @@ def family(name):
         return None  # not a library kernel (torch RNG, copies, ...)
     base = m.group(1) or m.group(2)
     if base in ("ntt_fwd_pass", "ntt_inv_pass"):
-        col = re.search(r"\(bool\)(\d)>|, (true|false)>|,\s*(\d)>\(", name)
-        is_col = col and (col.group(1) == "1" or col.group(2) == "true" or col.group(3) == "1")
-        return base.replace("_pass", "_col" if is_col else "_row")
+        # template arguments <LA, LB, COL[, EPI]> (EPI: forward row pass with its epilogue)
+        targs = re.search(base + r"<([^>]*)>", name)
+        args = [a.strip().replace("(bool)", "").replace("true", "1").replace("false", "0")
+                for a in targs.group(1).split(",")] if targs else []
+        is_col = len(args) >= 3 and args[2] == "1"
+        epi = len(args) >= 4 and args[3] == "1"
+        return base.replace("_pass", "_col" if is_col else ("_row_epi" if epi else "_row"))
     return base
 
 
