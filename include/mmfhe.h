@@ -105,7 +105,9 @@ typedef struct {
     uint32_t taylor_order; /* K7: 1 or 3 */
     uint32_t n_slots;      /* packing period n */
     uint32_t bsgs_baby;    /* K3 baby steps b (0: ceil(sqrt(2D-1))) */
-    uint32_t hoist;        /* 0: none (only mode in this version) */
+    uint32_t hoist;        /* 1: rotations of one ciphertext by several amounts share one ModUp
+                              (hoisted HRot: K3 / FC baby steps, K4's packed unpack);
+                              0: every rotation is a full HRot.  Different residues, same decryption */
     uint32_t frame_batch;  /* frames evaluated together per batched launch (0: all);
                               fixes the op order of the trace (op-major per batch) */
     uint32_t fc_dims[4];   /* n_in, h1, h2, h3 (padded logits) */
@@ -125,6 +127,14 @@ typedef struct {
                               2 log2 R; needs 2^k R <= n, a multiple of 2^(k-1) frames per frame
                               batch (E_SHAPE) and the Galois keys for +-2^j R, j < k (listed by
                               mmfhe_chain_required_rotations); same decryption.  0 = canonical */
+    uint32_t lanes;        /* gesture / k3 / K2b / K6 / FC chains: L = frames interleaved per ciphertext
+                              (SIMD-dense packing, DESIGN R20); 0 or 1 = one frame per
+                              ciphertext (the paper's layout).  Slot L*i + f holds element i of
+                              frame f: every rotation amount is scaled by L, public vectors are
+                              lane-repeated, frames' features are lane-summed at the start of the FC
+                              head, logits sit in slots L*c.  Inputs: ceil(F/L) ciphertext pairs
+                              (n_slots = L*n; unused lanes of the last pair zero); frame_batch then
+                              counts ciphertext pairs.  L a power of two with L*n <= N/2 (E_SHAPE) */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */

@@ -55,11 +55,57 @@ class ChainCfg:
     hoist: int = 0              # 1: baby-step rotations of K3 / FC share one ModUp (hoisted HRot)
     vp_plus: int = 0            # vital V2: 1 -> sharpen + weighted frequency average in the cloud
     iq_pack: int = 0            # K4: k >= 1 -> packed rotate-and-sum over 2^k vectors (reading R19)
+    lanes: int = 1              # gesture / K3: frames interleaved per ciphertext (reading R20)
+
+
+def log2_exact(x: int, name: str) -> int:
+    """log2 of a power-of-two public exponent (the number of squarings, P:777-788,
+    P:821-829); anything else is rejected rather than rounded."""
+    if x < 1 or x & (x - 1):
+        raise ValueError(f"{name} must be a power of two, got {x}")
+    return x.bit_length() - 1
 
 
 def rot(v: np.ndarray, k: int) -> np.ndarray:
     """Rot(v, k)[j] = v[(j + k) mod n] (left rotation)."""
     return np.roll(v, -k)
+
+
+# ------------------------------------------------------------------ SIMD-dense lanes (reading R20)
+# With cfg.lanes = L > 1, one ciphertext carries L frames interleaved: slot L*i + f holds
+# element i (< n) of frame f (< L).  Rot(x, L k)[L i + f] = x[L (i + k) + f] (mod n L), so
+# every per-frame rotation by k becomes a slot rotation by L k, every public plaintext
+# vector p (period n) becomes p repeated L times per entry, and lanes never mix.  The
+# frames' features are summed across lanes (rotate-and-sum, strides 1 .. L/2) before the
+# classifier's first nonlinearity; the logits then sit in slots L c.  SURVEY §8(f)-3.
+
+def lanes_of(cfg) -> int:
+    L = int(getattr(cfg, "lanes", 1) or 1)
+    log2_exact(L, "lanes")
+    return L
+
+
+def lane_vec(v: np.ndarray, L: int) -> np.ndarray:
+    """A per-frame public vector in the lane-interleaved layout (entry i in slots L i .. L i + L-1)."""
+    v = np.asarray(v)
+    return np.repeat(v, L) if L > 1 else v
+
+
+def interleave(frames, L: int, n: int) -> np.ndarray:
+    """Client packing: up to L frame vectors of length n into one slot vector (unused lanes 0)."""
+    out = np.zeros(n * L)
+    for f, v in enumerate(frames):
+        out[f::L] = v
+    return out
+
+
+def n_packed(F: int, L: int) -> int:
+    """Ciphertext pairs holding F frames at L frames per ciphertext."""
+    return -(-F // L)
+
+
+def logit_slots(n_classes: int, L: int) -> list:
+    return [c * L for c in range(n_classes)]
 
 
 def ceil_sqrt(x: int) -> int:
@@ -202,7 +248,7 @@ def k2_soft_attention(ev: CircuitEvaluator, book: PlainBook, E: orc.Ct, cfg: Cha
     """K2a: w = E^gamma by log2(gamma) squarings; N = rotsum_R(w (.) ramp'),
     D = rotsum_R(w (.) one'), ramp'_r = r/(F^2 R), one'_r = 1/(F^2 R)."""
     w = E
-    for _ in range(int(math.log2(cfg.gamma))):
+    for _ in range(log2_exact(cfg.gamma, "gamma")):
         w = ev.square_rescale_all([w])[0]
     n = E.n_slots
     R, F = cfg.R, cfg.F
@@ -261,13 +307,14 @@ def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg
     """K3 (Eqs. dft_re/dft_im P:805-815) on a list of frames: d_re = C~ v_re - S~ v_im,
     d_im = S~ v_re + C~ v_im via BSGS with pre-rotated diagonals; one rescale after
     the giant sum (c-6)."""
-    n = v_re[0].n_slots
+    L = lanes_of(cfg)
+    n = v_re[0].n_slots // L
     lvl = v_re[0].level
     W = dsp.dft_matrix(cfg.D)
     C, S = W.real, W.imag
     b, giants = k3_schedule(cfg)
-    xr = [list(v_re)] + baby_steps(ev, v_re, range(1, b), cfg.hoist)
-    xi = [list(v_im)] + baby_steps(ev, v_im, range(1, b), cfg.hoist)
+    xr = [list(v_re)] + baby_steps(ev, v_re, [s * L for s in range(1, b)], cfg.hoist)
+    xi = [list(v_im)] + baby_steps(ev, v_im, [s * L for s in range(1, b)], cfg.hoist)
     out_re = out_im = None
     nf = len(v_re)
 
@@ -280,8 +327,8 @@ def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg
         t_re, t_im = [], []
         for s in babies:
             o = G + s
-            dc = rot(block_diag_diagonal(C, n, o), -G)
-            ds = rot(block_diag_diagonal(S, n, o), -G)
+            dc = lane_vec(rot(block_diag_diagonal(C, n, o), -G), L)
+            ds = lane_vec(rot(block_diag_diagonal(S, n, o), -G), L)
             pc = book.vec(f"k3.c.{gp}.{s}", dc, lvl)
             ps = book.vec(f"k3.s.{gp}.{s}", ds, lvl)
             pns = book.vec(f"k3.ns.{gp}.{s}", -ds, lvl)
@@ -290,8 +337,8 @@ def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg
         inner.append(([ev.pmult_sum(terms(t_re, f)) for f in range(nf)],
                       [ev.pmult_sum(terms(t_im, f)) for f in range(nf)]))
     for (gp, G, babies), (pr, pi) in zip(giants, inner):
-        ir = [ev.rotate(x, G) for x in pr]
-        ii = [ev.rotate(x, G) for x in pi]
+        ir = [ev.rotate(x, G * L) for x in pr]
+        ii = [ev.rotate(x, G * L) for x in pi]
         out_re = ir if out_re is None else [ev.add(a, x) for a, x in zip(out_re, ir)]
         out_im = ii if out_im is None else [ev.add(a, x) for a, x in zip(out_im, ii)]
     return [ev.rescale(x) for x in out_re], [ev.rescale(x) for x in out_im]
@@ -312,9 +359,10 @@ def k1_power(ev, d_re, d_im):
 
 def k6_notch(ev, book, P_cts, cfg):
     """K6: P (.) m~ with m~[d] = m[d]/s, s = R A (sum w)^2 (P:887 fold)."""
-    n = P_cts[0].n_slots
+    L = lanes_of(cfg)
+    n = P_cts[0].n_slots // L
     s = dsp.spectral_scale(cfg.R, cfg.A, cfg.D)
-    mask = np.tile(dsp.notch_mask(cfg.D, cfg.notch_width) / s, n // cfg.D)
+    mask = lane_vec(np.tile(dsp.notch_mask(cfg.D, cfg.notch_width) / s, n // cfg.D), L)
     pt = book.vec("k6.mask", mask, P_cts[0].level)
     return [ev.rescale(x) for x in [ev.pmult_sum([(pt, p)]) for p in P_cts]]
 
@@ -323,8 +371,9 @@ def k2_doppler_soft_power(ev, Pm, cfg):
     """K2b (Eq. gesture_soft_power): S = rotsum over the n/D blocks
     (stride D; every block then holds sum_{a,r}, reading #8); S^gamma by squarings;
     f = Pm (.) S^gamma (P:906 'feature weighting')."""
-    S = ev.rotsum_all(Pm, Pm[0].n_slots // cfg.D, cfg.D)
-    for _ in range(int(math.log2(cfg.gamma))):
+    L = lanes_of(cfg)
+    S = ev.rotsum_all(Pm, Pm[0].n_slots // L // cfg.D, cfg.D * L)
+    for _ in range(log2_exact(cfg.gamma, "gamma")):
         S = ev.square_rescale_all(S)
     Pd = [ev.drop_to(p, s.level) for p, s in zip(Pm, S)]
     return ev.relin_rescale_all([ev.tensor_sum([(p, s)]) for p, s in zip(Pd, S)])
@@ -375,28 +424,31 @@ def fc_schedule(h: int):
     return b, [(gp, gp * b, [s for s in range(b) if gp * b + s < h]) for gp in range(g)]
 
 
-def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int, square: bool, hoist: int = 0):
+def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int, square: bool, hoist: int = 0,
+             L: int = 1):
     """One layer of Eq. mlp_forward: z = sum_i diag_i (.) Rot(x, i) by BSGS,
-    y = rotsum_{n_in/h}(z, stride h) (h-periodic W x), + b, then (.)^2 unless last."""
+    y = rotsum_{n_in/h}(z, stride h) (h-periodic W x), + b, then (.)^2 unless last.
+    L lanes: rotations by L i, lane-interleaved diagonals and bias (reading R20)."""
     h = W.shape[0]
     lvl = x.level
     b, giants = fc_schedule(h)
-    babies = [x] + [r[0] for r in baby_steps(ev, [x], range(1, min(b, h)), hoist)]
+    babies = [x] + [r[0] for r in baby_steps(ev, [x], [s * L for s in range(1, min(b, h))], hoist)]
     acc = None
     inners = []  # all giant steps' inner sums first, then the giant rotations
     for gp, G, ss in giants:
         terms = []
         for s in ss:
-            dg = rot(fc_diagonal(W, n_in, G + s), -G)
+            dg = lane_vec(rot(fc_diagonal(W, n_in, G + s), -G), L)
             terms.append((book.vec(f"fc{layer}.d.{gp}.{s}", dg, lvl), babies[s]))
         inners.append(ev.pmult_sum(terms))
     for (gp, G, ss), inner in zip(giants, inners):
         if G:
-            inner = ev.rotate(inner, G)
+            inner = ev.rotate(inner, G * L)
         acc = inner if acc is None else ev.add(acc, inner)
     z = ev.rescale(acc)
-    y = ev.rotsum_all([z], n_in // h, h)[0]
-    y = ev.add_plain(y, book.vec(f"fc{layer}.bias", np.asarray(bias, dtype=np.float64), y.level, scale=y.scale))
+    y = ev.rotsum_all([z], n_in // h, h * L)[0]
+    bv = lane_vec(np.asarray(bias, dtype=np.float64), L)
+    y = ev.add_plain(y, book.vec(f"fc{layer}.bias", bv, y.level, scale=y.scale))
     if square:
         y = ev.square_rescale_all([y])[0]
     return y
@@ -415,12 +467,16 @@ def pad_fc(Ws, bs, dims):
 
 
 def gesture_fc(ev, book, feat, Ws, bs, cfg):
-    """FC1 -> x^2 -> FC2 -> x^2 -> FC3 (P:906-907)."""
+    """FC1 -> x^2 -> FC2 -> x^2 -> FC3.  With L lanes the frame features are
+    first summed across lanes (rotate-and-sum, strides 1 .. L/2; lane 0 then holds the
+    session's feature vector, reading R20) -- here rather than per partial sum, so that
+    frame sharding stays an exact modular sum."""
     dims = cfg.fc_dims
     Ws, bs = pad_fc(Ws, bs, dims)
-    x = feat
+    L = lanes_of(cfg)
+    x = ev.rotsum_all([feat], L, 1)[0] if L > 1 else feat
     for layer in range(len(Ws)):
-        x = fc_layer(ev, book, x, Ws[layer], bs[layer], dims[layer], layer + 1, layer < len(Ws) - 1, cfg.hoist)
+        x = fc_layer(ev, book, x, Ws[layer], bs[layer], dims[layer], layer + 1, layer < len(Ws) - 1, cfg.hoist, L)
     return x
 
 
@@ -430,7 +486,7 @@ def k4_soft_iq(ev, re, im, cfg):
     """K4 on lists of frames, P_phi = 2^k: p = |z|^2, m = p^P_phi,
     i = m re, q = m im, I = rotsum_R(i), Q = rotsum_R(q) (slot 0 valid)."""
     m = ev.relin_rescale_all([ev.tensor_sum([(r, r), (i, i)]) for r, i in zip(re, im)])
-    for _ in range(int(math.log2(cfg.p_phi))):
+    for _ in range(log2_exact(cfg.p_phi, "p_phi")):
         m = ev.square_rescale_all(m)
     red = [ev.drop_to(r, x.level) for r, x in zip(re, m)]
     i_ = ev.relin_rescale_all([ev.tensor_sum([(x, r)]) for x, r in zip(m, red)])
@@ -460,6 +516,9 @@ def k4_packed_rotsum(ev, i_, q_, R, k, hoist=0):
     2 (2 - 2^(1-k)) + log2(R) / 2^(k-1) rotations instead of 2 log2 R."""
     if len(i_) % (1 << (k - 1)):
         raise ValueError("iq_pack = k needs a multiple of 2^(k-1) frames per frame batch")
+    # blocks sit at multiples of R and rotsum_R adds 2^ceil(log2 R) slots: R must be 2^m,
+    # or a block's sum would pick up the next block's values
+    log2_exact(R, "R (iq_pack)")
     x = [ev.add(a, b) for a, b in zip(i_, [ev.rotate(v, -R) for v in q_])]
     for j in range(1, k):
         h = len(x) // 2
@@ -489,6 +548,8 @@ def k5_fir(ev, xs, taps):
 def k7_taylor_phase(ev, If, Qf, order):
     """K7: y[t] = Q_f[t] I_f[t-1] - I_f[t] Q_f[t-1]; first order y,
     third order y x^2 - y^3/3 (literal polynomial, reading #2); t = 1..F-1."""
+    if order not in (1, 3):
+        raise ValueError(f"taylor order must be 1 or 3, got {order}")
     T = range(1, len(If))
     ty = [ev.tensor_sum([(Qf[t], If[t - 1])]) for t in T]
     ty2 = [ev.tensor_sum([(If[t], Qf[t - 1])]) for t in T]
@@ -566,22 +627,25 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
     if chain in ("k2_soft_attention", "vitals_v1", "k4_soft_iq", "vitals_v2"):
         ks |= set(rotsum_steps(cfg.R, 1))
     if chain in ("k4_soft_iq", "vitals_v2") and cfg.iq_pack:
+        log2_exact(cfg.R, "R (iq_pack)")
         for j in range(cfg.iq_pack):
             ks |= {cfg.R << j, -(cfg.R << j)}
         if cfg.hoist:
             ks |= {m * cfg.R for m in range(1, 1 << cfg.iq_pack)}
+    L = lanes_of(cfg)
     if chain in ("k3_doppler_dft", "gesture_frame", "gesture"):
         b, giants = k3_schedule(cfg)
-        ks |= set(range(1, b))
-        ks |= {G for _, G, _ in giants if G != 0}
+        ks |= {s * L for s in range(1, b)}
+        ks |= {G * L for _, G, _ in giants if G != 0}
     if chain in ("k2_doppler_soft_power", "gesture_frame", "gesture"):
-        ks |= set(rotsum_steps(cfg.n_slots // cfg.D, cfg.D))
-    if chain in ("gesture_fc", "gesture"):
+        ks |= set(rotsum_steps(cfg.n_slots // cfg.D, cfg.D * L))
+    if chain in ("gesture_fc", "gesture", "fc_forward"):
+        ks |= set(rotsum_steps(L, 1))
         dims = cfg.fc_dims
         for layer in range(len(dims) - 1):
             h = dims[layer + 1]
             b, giants = fc_schedule(h)
-            ks |= set(range(1, min(b, h)))
-            ks |= {G for _, G, _ in giants if G != 0}
-            ks |= set(rotsum_steps(dims[layer] // h, h))
+            ks |= {s * L for s in range(1, min(b, h))}
+            ks |= {G * L for _, G, _ in giants if G != 0}
+            ks |= set(rotsum_steps(dims[layer] // h, h * L))
     return sorted({k % half for k in ks} - {0})

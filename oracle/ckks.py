@@ -38,12 +38,13 @@ u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
 
 
 def build(force: bool = False) -> str:
-    """Compile ckks_ref.c (plain C, -O2) into oracle/_build/libckks_ref.so."""
+    """Compile ckks_ref.c (plain C, -O2, OpenMP across independent limbs) into
+    oracle/_build/libckks_ref.so."""
     src = os.path.join(_HERE, "ckks_ref.c")
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
         os.makedirs(os.path.dirname(_SO), exist_ok=True)
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", src, "-o", tmp])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fopenmp", "-shared", "-fPIC", src, "-o", tmp])
         os.replace(tmp, _SO)
     return _SO
 

@@ -10,7 +10,10 @@
  * textbook one: (a*b) mod q through unsigned __int128 and '%'; ring products
  * through the textbook iterative negacyclic NTT (psi-twist, bit reversal,
  * radix-2 Cooley-Tukey).  No lazy reduction, no fusion, no precomputed
- * tables shared across calls.
+ * tables shared across calls.  Limbs (and base-conversion targets) are
+ * independent residue computations, so their loops are spread over the host's
+ * cores with OpenMP (`#pragma omp parallel for`): each limb's arithmetic is
+ * exactly the sequential one, only different limbs run at the same time.
  *
  * Citations (PAPER.md line, section) -- the paper names these operations only
  * through its libraries ("RNS-CKKS backends"; HMult/HRot/rescale in the
@@ -114,10 +117,11 @@ int or_ntt_inverse(uint32_t n, uint64_t q, uint64_t *a)
 int or_poly_mul(uint32_t n, uint32_t n_limbs, const uint64_t *qs,
                 const uint64_t *a, const uint64_t *b, uint64_t *out)
 {
-    uint64_t *ta = (uint64_t *)malloc(sizeof(uint64_t) * n);
-    uint64_t *tb = (uint64_t *)malloc(sizeof(uint64_t) * n);
     int rc = 0;
-    for (uint32_t l = 0; l < n_limbs && !rc; ++l) {
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : rc)
+    for (uint32_t l = 0; l < n_limbs; ++l) {
+        uint64_t *ta = (uint64_t *)malloc(sizeof(uint64_t) * n);
+        uint64_t *tb = (uint64_t *)malloc(sizeof(uint64_t) * n);
         uint64_t q = qs[l];
         memcpy(ta, a + (size_t)l * n, sizeof(uint64_t) * n);
         memcpy(tb, b + (size_t)l * n, sizeof(uint64_t) * n);
@@ -126,14 +130,15 @@ int or_poly_mul(uint32_t n, uint32_t n_limbs, const uint64_t *qs,
         for (uint32_t i = 0; i < n; ++i) ta[i] = mulmod(ta[i], tb[i], q);
         rc |= or_ntt_inverse(n, q, ta);
         memcpy(out + (size_t)l * n, ta, sizeof(uint64_t) * n);
+        free(ta);
+        free(tb);
     }
-    free(ta);
-    free(tb);
     return rc;
 }
 
 void or_add(uint32_t n, uint32_t n_limbs, const uint64_t *qs, const uint64_t *a, const uint64_t *b, uint64_t *out)
 {
+#pragma omp parallel for
     for (uint32_t l = 0; l < n_limbs; ++l)
         for (uint32_t i = 0; i < n; ++i) {
             size_t k = (size_t)l * n + i;
@@ -143,6 +148,7 @@ void or_add(uint32_t n, uint32_t n_limbs, const uint64_t *qs, const uint64_t *a,
 
 void or_sub(uint32_t n, uint32_t n_limbs, const uint64_t *qs, const uint64_t *a, const uint64_t *b, uint64_t *out)
 {
+#pragma omp parallel for
     for (uint32_t l = 0; l < n_limbs; ++l)
         for (uint32_t i = 0; i < n; ++i) {
             size_t k = (size_t)l * n + i;
@@ -153,6 +159,7 @@ void or_sub(uint32_t n, uint32_t n_limbs, const uint64_t *qs, const uint64_t *a,
 /* out_l = a_l * c_l mod q_l for one scalar residue c_l per limb. */
 void or_scalar_mul(uint32_t n, uint32_t n_limbs, const uint64_t *qs, const uint64_t *a, const uint64_t *c, uint64_t *out)
 {
+#pragma omp parallel for
     for (uint32_t l = 0; l < n_limbs; ++l)
         for (uint32_t i = 0; i < n; ++i) {
             size_t k = (size_t)l * n + i;
@@ -166,6 +173,7 @@ void or_scalar_mul(uint32_t n, uint32_t n_limbs, const uint64_t *qs, const uint6
 void or_automorphism(uint32_t n, uint32_t n_limbs, const uint64_t *qs, const uint64_t *a, uint64_t g, uint64_t *out)
 {
     uint64_t two_n = 2ull * n;
+#pragma omp parallel for
     for (uint32_t l = 0; l < n_limbs; ++l) {
         const uint64_t *al = a + (size_t)l * n;
         uint64_t *ol = out + (size_t)l * n;
@@ -186,6 +194,7 @@ void or_rescale(uint32_t n, uint32_t l, const uint64_t *qs, const uint64_t *a, u
     uint64_t ql = qs[l];
     uint64_t h = ql >> 1;
     const uint64_t *al = a + (size_t)l * n;
+#pragma omp parallel for
     for (uint32_t i = 0; i < l; ++i) {
         uint64_t qi = qs[i];
         uint64_t ql_inv = invmod(ql % qi, qi);
@@ -214,14 +223,17 @@ static void bconv(uint32_t n, const uint64_t *src, uint32_t ns, const uint64_t *
                   const uint64_t *dst, uint32_t nd, uint64_t *y)
 {
     uint64_t *hat_inv = (uint64_t *)malloc(sizeof(uint64_t) * ns);
-    uint64_t *hat_t = (uint64_t *)malloc(sizeof(uint64_t) * ns);
     uint64_t *others = (uint64_t *)malloc(sizeof(uint64_t) * (ns ? ns : 1));
     for (uint32_t i = 0; i < ns; ++i) {
         uint32_t c = 0;
         for (uint32_t k = 0; k < ns; ++k) if (k != i) others[c++] = src[k];
         hat_inv[i] = invmod(prod_mod(others, c, src[i]), src[i]);
     }
+    free(others);
+#pragma omp parallel for schedule(dynamic, 1)
     for (uint32_t d = 0; d < nd; ++d) {
+        uint64_t *hat_t = (uint64_t *)malloc(sizeof(uint64_t) * ns);
+        uint64_t *others = (uint64_t *)malloc(sizeof(uint64_t) * (ns ? ns : 1));
         uint64_t t = dst[d];
         for (uint32_t i = 0; i < ns; ++i) {
             uint32_t c = 0;
@@ -236,10 +248,10 @@ static void bconv(uint32_t n, const uint64_t *src, uint32_t ns, const uint64_t *
             }
             y[(size_t)d * n + k] = acc;
         }
+        free(hat_t);
+        free(others);
     }
     free(hat_inv);
-    free(hat_t);
-    free(others);
 }
 
 /* ModUp of digit j at level l:
@@ -253,6 +265,7 @@ void or_modup(uint32_t n, uint32_t l, const uint64_t *qs, uint32_t k_p, const ui
     if (hi > l + 1) hi = l + 1;
     uint32_t ns = hi - lo;
     uint32_t nb = l + 1 + k_p;
+#pragma omp parallel for schedule(dynamic, 1)
     for (uint32_t t = 0; t < nb; ++t) {
         uint64_t pt = t <= l ? qs[t] : ps[t - l - 1];
         uint64_t *yt = out + (size_t)t * n;
@@ -271,6 +284,7 @@ void or_moddown(uint32_t n, uint32_t l, const uint64_t *qs, uint32_t k_p, const 
 {
     uint64_t *w = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(l + 1) * n);
     bconv(n, ps, k_p, c + (size_t)(l + 1) * n, qs, l + 1, w);
+#pragma omp parallel for
     for (uint32_t i = 0; i <= l; ++i) {
         uint64_t qi = qs[i];
         uint64_t p_inv = invmod(prod_mod(ps, k_p, qi), qi);

@@ -20,7 +20,12 @@ mmfhe_status fail(mmfhe_ctx *c, mmfhe_status s, const char *msg)
     return s;
 }
 
-#define API_BEGIN try {
+// every entry point with a ctx allocates from that ctx's pool (PoolScope)
+#define API_BEGIN                                                                                 \
+    try {                                                                                         \
+        DeviceScope dev_scope_(ctx ? ctx->device : -1);                                           \
+        PoolScope pool_scope_(ctx ? ctx->mem.pool : nullptr);
+#define API_BEGIN0 try {
 #define API_END(C)                                                                                \
     }                                                                                             \
     catch (const Error &e) { return fail((C), e.status, e.what()); }                              \
@@ -179,7 +184,7 @@ mmfhe_status mmfhe_ctx_create(const mmfhe_params *params, int cuda_device, void 
 {
     if (!params || !out) return fail(nullptr, MMFHE_E_INVALID_ARG, "null argument");
     *out = nullptr;
-    API_BEGIN
+    API_BEGIN0
     *out = new mmfhe_ctx(*params, cuda_device, (cudaStream_t)cuda_stream);
     API_END(nullptr)
 }
@@ -187,7 +192,7 @@ mmfhe_status mmfhe_ctx_create(const mmfhe_params *params, int cuda_device, void 
 mmfhe_status mmfhe_ctx_destroy(mmfhe_ctx *ctx)
 {
     if (!ctx) return MMFHE_OK;
-    API_BEGIN
+    API_BEGIN0
     cudaStreamSynchronize(ctx->stream);
     delete ctx;
     API_END(nullptr)
@@ -198,10 +203,9 @@ const char *mmfhe_last_error(const mmfhe_ctx *ctx) { return ctx ? ctx->last_erro
 mmfhe_status mmfhe_ctx_memory(mmfhe_ctx *ctx, size_t *bytes)
 {
     API_BEGIN
-    cudaMemPool_t pool;
-    CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
-    uint64_t used = 0;
-    CUDA_CHECK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+    MMFHE_REQUIRE(bytes != nullptr, MMFHE_E_INVALID_ARG, "null argument");
+    uint64_t used = 0;  // this ctx's own pool only
+    CUDA_CHECK(cudaMemPoolGetAttribute(ctx->mem.pool, cudaMemPoolAttrUsedMemCurrent, &used));
     *bytes = (size_t)used;
     API_END(ctx)
 }

@@ -64,6 +64,19 @@ std::vector<double> rot(const std::vector<double> &v, int64_t k)
     return o;
 }
 
+// Lane-interleaved layout (DESIGN R20): a per-frame public vector with every
+// entry repeated L times (slot L i + f holds entry i for every frame lane f).
+std::vector<double> lane_rep(const std::vector<double> &v, uint32_t L)
+{
+    if (L <= 1) return v;
+    std::vector<double> o(v.size() * L);
+    for (size_t i = 0; i < v.size(); ++i)
+        for (uint32_t f = 0; f < L; ++f) o[i * L + f] = v[i];
+    return o;
+}
+
+uint32_t lanes_of(const mmfhe_chain_cfg &cfg) { return cfg.lanes ? cfg.lanes : 1; }
+
 struct Sched {
     uint32_t b;
     struct G {
@@ -151,18 +164,21 @@ class Runner {
 
     uint32_t frame_batch(uint32_t F) const { return cfg_.frame_batch ? std::min(cfg_.frame_batch, F) : F; }
 
-    // [x, Rot(x,1), ..., Rot(x,nb-1)]: plain HRots, or (cfg.hoist) hoisted HRots sharing one ModUp
+    uint32_t L() const { return lanes_of(cfg_); }
+
+    // [x, Rot(x,L), ..., Rot(x,(nb-1)L)] (L = lanes): plain HRots, or (cfg.hoist) hoisted HRots
+    // sharing one ModUp
     std::vector<DCt> baby_steps(const DCt &x, uint32_t nb)
     {
         std::vector<DCt> out;
         out.push_back(copy_ct(c_, x));
         if (cfg_.hoist) {
             std::vector<int32_t> st;
-            for (uint32_t b = 1; b < nb; ++b) st.push_back((int32_t)b);
+            for (uint32_t b = 1; b < nb; ++b) st.push_back((int32_t)(b * L()));
             if (!st.empty())
                 for (auto &r : ev_rotate_hoisted(c_, x, st)) out.push_back(std::move(r));
         } else {
-            for (uint32_t b = 1; b < nb; ++b) out.push_back(ev_rotate(c_, x, (int32_t)b));
+            for (uint32_t b = 1; b < nb; ++b) out.push_back(ev_rotate(c_, x, (int32_t)(b * L())));
         }
         return out;
     }
@@ -208,7 +224,7 @@ class Runner {
     // ---------------------------------------------------------- K3 (BSGS), batched over frames
     std::pair<DCt, DCt> k3_doppler_dft(const DCt &vre, const DCt &vim)
     {
-        const uint32_t n = vre.n_slots, D = cfg_.D, lvl = vre.level;
+        const uint32_t n = vre.n_slots / L(), D = cfg_.D, lvl = vre.level;
         Sched s = k3_schedule(cfg_);
         std::vector<DCt> xr = baby_steps(vre, s.b), xi = baby_steps(vim, s.b);
         // W = hann[m] e^{-j 2 pi sigma(d) m / D}, diagonal o of I (x) W, pre-rotated by -G
@@ -222,7 +238,7 @@ class Runner {
                 const double ang = -2.0 * M_PI * (double)sig * (double)m / (double)D;
                 v[j] = w[m] * (imag ? std::sin(ang) : std::cos(ang)) * (neg ? -1.0 : 1.0);
             }
-            return rot(v, -G);
+            return lane_rep(rot(v, -G), L());
         };
         // inner sums of every giant step in one pass over the 2b baby steps (fused diagonal
         // MAC: babies read once, each diagonal once per frame batch), then the giant rotations
@@ -251,8 +267,8 @@ class Runner {
         bool first = true;
         for (size_t gi = 0; gi < s.giants.size(); ++gi) {
             const auto &g = s.giants[gi];
-            DCt ir = ev_rotate(c_, inner[2 * gi], g.G);
-            DCt ii = ev_rotate(c_, inner[2 * gi + 1], g.G);
+            DCt ir = ev_rotate(c_, inner[2 * gi], g.G * (int32_t)L());
+            DCt ii = ev_rotate(c_, inner[2 * gi + 1], g.G * (int32_t)L());
             if (first) {
                 out_re = std::move(ir);
                 out_im = std::move(ii);
@@ -275,7 +291,7 @@ class Runner {
 
     DCt k6_notch(const DCt &P)
     {
-        const uint32_t D = cfg_.D, n = P.n_slots;
+        const uint32_t D = cfg_.D, n = P.n_slots / L();
         const DPlain &m = plain("k6.mask", P.level, qscale(P.level), [&] {
             std::vector<double> w = hann(D);
             double sw = 0;
@@ -288,14 +304,14 @@ class Runner {
                 const uint32_t d = j % D;
                 v[j] = (d >= lo && d < lo + width) ? 0.0 : 1.0 / s;
             }
-            return v;
+            return lane_rep(v, L());
         });
         return ev_rescale(c_, ev_pmult_sum(c_, {{&m, &P}}));
     }
 
     DCt k2_doppler_soft_power(const DCt &Pm)
     {
-        DCt S = ev_rotsum(c_, Pm, Pm.n_slots / cfg_.D, cfg_.D);
+        DCt S = ev_rotsum(c_, Pm, Pm.n_slots / L() / cfg_.D, cfg_.D * L());
         for (uint32_t i = 0; i < ilog2(cfg_.gamma); ++i) S = ev_square_rescale(c_, S);
         DCt Pd = ev_drop_to(c_, Pm, S.level);
         return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&Pd, &S}}));
@@ -334,7 +350,7 @@ class Runner {
                     MMFHE_REQUIRE(W != nullptr, MMFHE_E_MISSING_PLAIN, "FC weights not prepared");
                     std::vector<double> v(n_in);
                     for (uint32_t j = 0; j < n_in; ++j) v[j] = (*W)[(size_t)(j % h) * n_in + (j + i) % n_in];
-                    return rot(v, -g.G);
+                    return lane_rep(rot(v, -g.G), L());
                 });
             }
             rows.push_back(row);
@@ -345,7 +361,7 @@ class Runner {
         for (size_t gi = 0; gi < s.giants.size(); ++gi) {
             const auto &g = s.giants[gi];
             DCt inner = std::move(inners[gi]);
-            if (g.G) inner = ev_rotate(c_, inner, g.G);
+            if (g.G) inner = ev_rotate(c_, inner, g.G * (int32_t)L());
             if (first) {
                 acc = std::move(inner);
                 first = false;
@@ -354,19 +370,22 @@ class Runner {
             }
         }
         DCt z = ev_rescale(c_, acc);
-        DCt y = ev_rotsum(c_, z, n_in / h, h);
+        DCt y = ev_rotsum(c_, z, n_in / h, h * L());
         const DPlain &bp = plain("fc" + std::to_string(layer) + ".bias", y.level, y.scale, [&] {
             MMFHE_REQUIRE(bias != nullptr, MMFHE_E_MISSING_PLAIN, "FC bias not prepared");
-            return *bias;
+            return lane_rep(*bias, L());
         });
         y = ev_add_plain(c_, y, bp);
         if (square) y = ev_square_rescale(c_, y);
         return y;
     }
 
+    // With L lanes the frames' features are first summed across lanes (lane 0 then holds the
+    // session's features; oracle gesture_fc): before the first nonlinearity, after the frame
+    // sum, so frame-sharded partial sums stay exact modular sums
     DCt gesture_fc(const DCt &feat)
     {
-        DCt x = fc_layer(feat, 1, true);
+        DCt x = L() > 1 ? fc_layer(ev_rotsum(c_, feat, L(), 1), 1, true) : fc_layer(feat, 1, true);
         x = fc_layer(x, 2, true);
         return fc_layer(x, 3, false);
     }
@@ -551,8 +570,27 @@ class Runner {
     const mmfhe_chain_cfg &cfg_;
 };
 
+bool pow2_or_zero(uint32_t x) { return (x & (x - 1)) == 0; }
+
+// Public-parameter checks shared by chain_plan and chain_rotations (the oracle raises on
+// the same inputs): exponents are powers of two (log2 squarings),
+// K7 is first or third order, and the packed K4 rotate-and-sum needs R a power
+// of two (its blocks sit at multiples of R and one rotsum adds 2^ceil(log2 R) slots).
+void validate_cfg(const std::string &chain, const mmfhe_chain_cfg &cfg)
+{
+    MMFHE_REQUIRE(pow2_or_zero(cfg.gamma), MMFHE_E_INVALID_ARG, "gamma must be a power of two");
+    MMFHE_REQUIRE(pow2_or_zero(cfg.p_phi), MMFHE_E_INVALID_ARG, "p_phi must be a power of two");
+    if (chain == "vitals_v2" || chain == "k7_taylor_phase")
+        MMFHE_REQUIRE(cfg.taylor_order == 1 || cfg.taylor_order == 3, MMFHE_E_INVALID_ARG,
+                      "taylor_order must be 1 or 3");
+    if ((chain == "vitals_v2" || chain == "k4_soft_iq") && cfg.iq_pack)
+        MMFHE_REQUIRE(cfg.R >= 1 && pow2_or_zero(cfg.R), MMFHE_E_SHAPE, "iq_pack needs R a power of two");
+    MMFHE_REQUIRE(pow2_or_zero(cfg.lanes), MMFHE_E_SHAPE, "lanes must be a power of two");
+}
+
 uint32_t chain_depth(const std::string &chain, const mmfhe_chain_cfg &cfg)
 {
+    validate_cfg(chain, cfg);
     const uint32_t lg = ilog2(cfg.gamma ? cfg.gamma : 1), lp = ilog2(cfg.p_phi ? cfg.p_phi : 1);
     const uint32_t gf = 3 + lg + 1, fc = 5;
     const uint32_t v2 = (1 + lp + 1) + 1 + (cfg.taylor_order == 3 ? 3 : 1) + 1 + 1 + (cfg.vp_plus ? 2 : 0);
@@ -591,28 +629,30 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
             for (uint32_t mm = 1; mm < (1u << cfg.iq_pack); ++mm) add((int64_t)mm * cfg.R);
     }
     const bool frames = chain == "gesture_frame" || chain == "gesture" || chain == "gesture_features";
+    const int64_t L = lanes_of(cfg);
     if (chain == "k3_doppler_dft" || frames) {
         Sched s = k3_schedule(cfg);
-        for (uint32_t b = 1; b < s.b; ++b) add(b);
-        for (auto &g : s.giants) add(g.G);
+        for (uint32_t b = 1; b < s.b; ++b) add(b * L);
+        for (auto &g : s.giants) add(g.G * L);
     }
     if (frames)
-        for (uint32_t s : rotsum_steps(cfg.n_slots / cfg.D, cfg.D)) add(s);
-    if (chain == "gesture_fc" || chain == "gesture")
+        for (uint32_t s : rotsum_steps(cfg.n_slots / cfg.D, cfg.D * (uint32_t)L)) add(s);
+    if (chain == "gesture_fc" || chain == "gesture") {
+        for (uint32_t s : rotsum_steps((uint32_t)L, 1)) add(s);
         for (int layer = 0; layer < 3; ++layer) {
             const uint32_t h = cfg.fc_dims[layer + 1], n_in = cfg.fc_dims[layer];
             Sched s = fc_schedule(h);
-            for (uint32_t b = 1; b < std::min(s.b, h); ++b) add(b);
-            for (auto &g : s.giants) add(g.G);
-            for (uint32_t st : rotsum_steps(n_in / h, h)) add(st);
+            for (uint32_t b = 1; b < std::min(s.b, h); ++b) add(b * L);
+            for (auto &g : s.giants) add(g.G * L);
+            for (uint32_t st : rotsum_steps(n_in / h, h * (uint32_t)L)) add(st);
         }
+    }
     return std::vector<int32_t>(ks.begin(), ks.end());
 }
 
 std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const mmfhe_chain_cfg &cfg, uint32_t in_level,
                                  size_t n_in)
 {
-    (void)c;
     const uint32_t dep = chain_depth(chain, cfg);
     MMFHE_REQUIRE(in_level >= dep, MMFHE_E_DEPTH,
                   "chain " + chain + " needs " + std::to_string(dep) + " levels, input has " +
@@ -624,8 +664,12 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
         MMFHE_REQUIRE(cfg.F > 0 && n_in % (2 * (size_t)cfg.F) == 0, MMFHE_E_SHAPE,
                       "expected 2F input ciphertexts per session");
         n_out = n_in / (2 * (size_t)cfg.F);
-    } else if (chain == "vitals_v1" || chain == "vitals_v2" || chain == "gesture") {
+    } else if (chain == "vitals_v1" || chain == "vitals_v2") {
         MMFHE_REQUIRE(n_in == 2 * (size_t)cfg.F && cfg.F > 0, MMFHE_E_SHAPE, "expected 2F input ciphertexts");
+    } else if (chain == "gesture") {
+        const size_t L = lanes_of(cfg);
+        MMFHE_REQUIRE(cfg.F > 0 && n_in == 2 * ((cfg.F + L - 1) / L), MMFHE_E_SHAPE,
+                      "expected 2 ceil(F / lanes) input ciphertexts");
     } else if (chain == "k3_doppler_dft" || chain == "gesture_frame" || chain == "gesture_features") {
         MMFHE_REQUIRE(n_in >= 2 && n_in % 2 == 0, MMFHE_E_SHAPE, "expected (v_re, v_im) per frame");
         n_out = chain == "k3_doppler_dft" ? n_in : chain == "gesture_frame" ? n_in / 2 : 1;
@@ -644,6 +688,13 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
             MMFHE_REQUIRE(((size_t)cfg.R << cfg.iq_pack) <= (size_t)(cfg.n_slots ? cfg.n_slots : c.n / 2),
                           MMFHE_E_SHAPE, "iq_pack = k needs 2^k R <= n slots");
         }
+    }
+    if (lanes_of(cfg) > 1) {
+        const bool lane_chain = chain == "gesture" || chain == "gesture_frame" || chain == "gesture_features" ||
+                                chain == "gesture_fc" || chain == "k3_doppler_dft";
+        MMFHE_REQUIRE(lane_chain, MMFHE_E_SHAPE, "lanes > 1 applies to the gesture / K3 chains only");
+        MMFHE_REQUIRE((size_t)lanes_of(cfg) * (cfg.n_slots ? cfg.n_slots : 1) <= c.n / 2, MMFHE_E_SHAPE,
+                      "lanes * n_slots must not exceed N/2");
     }
     if (chain == "vitals_v1") n_out = 2;
     if (chain == "vitals_v2") {

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -30,6 +31,41 @@ struct Error : std::runtime_error {
             throw ::mmfhe::Error(e_ == cudaErrorMemoryAllocation ? MMFHE_E_OOM : MMFHE_E_CUDA,    \
                                  std::string(#expr) + ": " + cudaGetErrorString(e_));             \
     } while (0)
+
+// cudaFuncSetAttribute applies to the current device only: run fn once per device (the
+// attribute set is idempotent, so a concurrent first call on two threads is harmless).
+template <class F>
+void once_per_device(std::atomic<uint64_t> &done, F &&fn)
+{
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    fn();
+    done.fetch_or(bit, std::memory_order_acq_rel);
+}
+
+// Makes `device` current for the scope of one C-ABI call (kernels launch on the ctx's
+// stream, which belongs to that device) and restores the caller's device afterwards.
+struct DeviceScope {
+    explicit DeviceScope(int device)
+    {
+        if (device < 0 || cudaGetDevice(&saved_) != cudaSuccess || saved_ == device) {
+            saved_ = -1;
+            return;
+        }
+        CUDA_CHECK(cudaSetDevice(device));
+    }
+    ~DeviceScope()
+    {
+        if (saved_ >= 0) cudaSetDevice(saved_);
+    }
+    DeviceScope(const DeviceScope &) = delete;
+    DeviceScope &operator=(const DeviceScope &) = delete;
+
+  private:
+    int saved_ = -1;
+};
 
 // ---------------------------------------------------------------- host modular math
 // (own implementation; the oracle's is separate and never linked)

@@ -58,9 +58,25 @@ static uint64_t min_psi(uint64_t q, uint32_t n)
 }
 }  // namespace host
 
+namespace {
+thread_local cudaMemPool_t g_pool = nullptr;
+}
+PoolScope::PoolScope(cudaMemPool_t p) : saved_(g_pool) { g_pool = p; }
+PoolScope::~PoolScope() { g_pool = saved_; }
+cudaMemPool_t PoolScope::current() { return g_pool; }
+
+PoolHolder::~PoolHolder()
+{
+    if (pool) cudaMemPoolDestroy(pool);
+}
+
 DBuf::DBuf(size_t words, cudaStream_t s) : n_(words), s_(s)
 {
-    if (words) CUDA_CHECK(cudaMallocAsync((void **)&p_, words * sizeof(uint64_t), s));
+    if (!words) return;
+    if (g_pool)
+        CUDA_CHECK(cudaMallocFromPoolAsync((void **)&p_, words * sizeof(uint64_t), g_pool, s));
+    else
+        CUDA_CHECK(cudaMallocAsync((void **)&p_, words * sizeof(uint64_t), s));
 }
 DBuf::~DBuf() { release(); }
 void DBuf::release()
@@ -165,10 +181,16 @@ Ctx::Ctx(const mmfhe_params &p, int dev, cudaStream_t s) : device(dev), stream(s
         MMFHE_REQUIRE(seen.insert(q).second, MMFHE_E_PARAMS, "duplicate prime");
     }
     CUDA_CHECK(cudaSetDevice(device));
-    cudaMemPool_t pool;
-    CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+    // the ctx's own stream-ordered pool (steady-state steps never touch the OS allocator:
+    // release threshold = max); destroyed with the ctx, the device's default pool untouched
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    CUDA_CHECK(cudaMemPoolCreate(&mem.pool, &props));
     uint64_t thr = UINT64_MAX;
-    CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    CUDA_CHECK(cudaMemPoolSetAttribute(mem.pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    PoolScope scope(mem.pool);
     build_tables();
 }
 

@@ -11,7 +11,21 @@
 
 namespace mmfhe {
 
-// Stream-ordered device buffer from the ctx's memory pool (cudaMallocAsync).
+// The memory pool DBufs allocate from on this thread: set for the duration of every C-ABI
+// call (and the ctx constructor) to the ctx's own pool, so each ctx's allocations are its
+// own, reported per ctx and released with it (never the device's default pool).
+struct PoolScope {
+    explicit PoolScope(cudaMemPool_t p);
+    ~PoolScope();
+    PoolScope(const PoolScope &) = delete;
+    PoolScope &operator=(const PoolScope &) = delete;
+    static cudaMemPool_t current();
+
+  private:
+    cudaMemPool_t saved_;
+};
+
+// Stream-ordered device buffer from the current ctx's memory pool (cudaMallocFromPoolAsync).
 class DBuf {
   public:
     DBuf() = default;
@@ -82,10 +96,19 @@ struct ModUpPlan {
     size_t off_tgt;            // uint32 [n_tgt] target row index in the l+1+K basis
 };
 
+// Owns the ctx's device memory pool; declared first in Ctx so that it is destroyed after
+// every DBuf member has been released (cudaMemPoolDestroy then frees the pool's memory).
+struct PoolHolder {
+    cudaMemPool_t pool = nullptr;
+    ~PoolHolder();
+};
+
 class Ctx {
   public:
     Ctx(const mmfhe_params &p, int device, cudaStream_t stream);
     ~Ctx();
+
+    PoolHolder mem;  // first member: destroyed last
 
     // parameters
     uint32_t log_n, n, L, K, alpha, scale_bits;

@@ -584,7 +584,8 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
     using Gm = Geo<LOGS, OTHER, COL>;
     static_assert(Gm::SMEM <= 48 * 1024, "NTT pass exceeds the default dynamic shared memory");
     // prefer the shared-memory carveout: residency is bounded by registers, not by L1
-    static const bool attr = [] {
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, [] {
         if (FWD)
         {
             CUDA_CHECK(cudaFuncSetAttribute(ntt_fwd_pass<LOGS, OTHER, COL, false>,
@@ -598,9 +599,7 @@ void launch_one(uint64_t *d, uint32_t rows, const KTables &kt, const PrimeMap &p
             CUDA_CHECK(cudaFuncSetAttribute(ntt_inv_pass<LOGS, OTHER, COL>,
                                             cudaFuncAttributePreferredSharedMemoryCarveout,
                                             cudaSharedmemCarveoutMaxShared));
-        return true;
-    }();
-    (void)attr;
+    });
     auto go = [&](dim3 grid, uint64_t *dd, RowMap rm, const ColSrc &src) {
         if constexpr (FWD) {
             if (!COL && ep)

@@ -513,12 +513,15 @@ __global__ void __launch_bounds__(kTB) k_diag_mac(DiagMacArgs a, KTables kt, uin
 }
 
 constexpr int kJG = 4;  // outputs per thread in the modular matrix product (2 x 128-bit accumulators each)
+constexpr int kFold = 128;  // input rows between hi-word folds in k_lincomb_mat
 
 // out[j] = sum_w C[j][w] in[lo_j + w] for j in this CTA's group of kJG outputs.  Each
 // term is one 64x64->128 multiply-accumulate per poly with the coefficient in Montgomery
 // form (C[.].wp = c 2^64 mod q); every accumulator is reduced once at the end (hi word
-// brought below q, then one Montgomery reduction).  acc < W q^2, so hi < W q / 16 < 2^17 q
-// for W <= 8192 (checked by the launcher).
+// brought below q, then one Montgomery reduction).  Each term is < q^2 < 2^120, so a
+// 128-bit sum of more than 256 terms could wrap: every kFold input rows the hi words are
+// folded below q (subtracting multiples of q 2^64 leaves the Montgomery result unchanged),
+// which keeps hi < q + kFold q / 16 < 2^17 q (the reduce_est precondition) for any W.
 __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out, const uint64_t *__restrict__ in,
                                                      uint32_t M, uint32_t J, uint32_t W, int lo0, int lo_step,
                                                      const TwPair *__restrict__ C, KTables kt, uint32_t level)
@@ -543,7 +546,15 @@ __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out,
     U128 a0[kJG], a1[kJG];
 #pragma unroll
     for (int jj = 0; jj < kJG; ++jj) a0[jj] = a1[jj] = U128{0, 0};
+    const float qinv = qinv_est(q);
     for (int i = ilo; i < ihi; ++i) {
+        if (((i - ilo) & (kFold - 1)) == kFold - 1) {
+#pragma unroll
+            for (int jj = 0; jj < kJG; ++jj) {
+                a0[jj].hi = reduce_est(a0[jj].hi, q, qinv);
+                a1[jj].hi = reduce_est(a1[jj].hi, q, qinv);
+            }
+        }
         const uint64_t x0 = in[(size_t)i * item + off], x1 = in[(size_t)i * item + ps + off];
 #pragma unroll
         for (int jj = 0; jj < kJG; ++jj) {
@@ -557,7 +568,6 @@ __global__ void __launch_bounds__(kTB) k_lincomb_mat(uint64_t *__restrict__ out,
             }
         }
     }
-    const float qinv = qinv_est(q);
 #pragma unroll
     for (int jj = 0; jj < kJG; ++jj) {
         if (jj < (int)jn) {
@@ -903,11 +913,10 @@ void launch_lincomb_sym(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, u
 {
     const size_t smem = sizeof(uint64_t) * ((kSymJT + W - 1) * kSymK + W / 2 + 1);
     MMFHE_REQUIRE(smem <= 200 * 1024, MMFHE_E_SHAPE, "FIR too long for the staged window");
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, [] {
         CUDA_CHECK(cudaFuncSetAttribute(k_lincomb_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr = true;
-    }
+    });
     ProfScope ps(c, "lincomb_mat", 8.0 * 2.0 * (level + 1) * c.n * ((double)M + J));
     const dim3 grid(c.n / kSymK, 2 * (level + 1), (J + kSymJT - 1) / kSymJT);
     k_lincomb_sym<<<grid, kSymK * kSymSplit, smem, c.stream>>>(out, in, M, J, W, lo0, T, c.kt, level);

@@ -1,0 +1,184 @@
+"""Residue-level GPU <-> oracle parity at the exact parameters bench.py times
+(VERDICT r01 "weak" #3): the same parameter sets, packing, hoisting and kernel
+variants, on fewer frames than a full session so the oracle finishes.
+
+* C2 (PS2: N=2^14, 8 Q limbs + 1 P, alpha 1 / K 1, dnum = l+1): vitals_v1 at entry
+  level 3 and vitals_v2 at entry level 7 with R=128, 41-tap linear-phase FIR
+  (k_lincomb_sym), packed I/Q rotate-and-sum over 4 frames with the hoisted unpack
+  (iq_pack = 3, hoist = 1, DESIGN R19) -- 16 of the session's 256 frames.
+* C4 (PS4: N=2^16, 20 Q + 7 P limbs, alpha 7, dnum 3, entry level 19): the gesture
+  chain (K3 hoisted BSGS -> K1 -> K6 -> K2b per frame, frame sum, FC 4096->64->32->8
+  hoisted), both in the paper's one-frame-per-ciphertext layout and SIMD-dense with
+  8 frames per ciphertext (cfg.lanes, DESIGN R20).
+* The library's own encoder: against the oracle's encoding,
+  |coefficient difference| <= 1 and decode error <= 2^-30, at N = 2^14 and 2^16.
+
+Every comparison is residue for residue with an identical op trace; decryption is
+checked against the plaintext DSP as well (north-star gate 2)."""
+import numpy as np
+import pytest
+
+from oracle import ckks as orc
+from oracle import circuits as cc
+from oracle import dsp
+from synth import radar
+from synth.params import ps2, ps4
+
+from gpu_util import ct_in, ct_out, make_ctx, residues
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+BANDS = ((0.1, 0.6), (0.8, 2.5))  # the bench's FIR bands
+
+
+@pytest.fixture(scope="module")
+def m(cuda_ctx_ok):
+    from paper_2603_22437_b200 import build, mmfhe
+    build.build()
+    return mmfhe
+
+
+def _check(outs, want):
+    assert len(outs) == len(want)
+    for o, w in zip(outs, want):
+        assert o.level == w.level and o.scale == w.scale
+        assert np.array_equal(residues(o), np.stack(w.c)), "residues differ from the oracle"
+
+
+@pytest.mark.parametrize("P_name", ["ps2", "ps4"])
+def test_library_encoder_matches_oracle(m, P_name):
+    """mmfhe_encode_plain vs the oracle's canonical-embedding encoder: the library's
+    plaintext is read back as pt (.) 1 (a PMult of the constant ciphertext (1, 0))."""
+    import torch
+    P = ps2() if P_name == "ps2" else ps4()
+    n = P.n // 2 if P_name == "ps2" else 4096
+    rng = np.random.default_rng(41)
+    v = rng.uniform(-1, 1, n)
+    lvl = 1
+    scale = float(P.q[lvl])  # Delta_pt = q_l, as every PMult operand (c-6)
+    ctx = make_ctx(m, P)
+    ctx.encode_plain("enc.test", v, lvl, scale)
+    one = np.zeros((2, lvl + 1, P.n), dtype=np.uint64)
+    one[0, :, 0] = 1
+    x = m.Ct(torch.from_numpy(one.view(np.int64)).cuda(), lvl, 1.0, n, P.log_n)
+    out = ct_out(m, P, lvl)
+    ctx.pmult(x, "enc.test", out)
+    torch.cuda.synchronize()
+    got = residues(out)[0]
+    assert not residues(out)[1].any()
+    want = orc.encode(P, v, scale, lvl)
+    qs = list(P.q[: lvl + 1])
+    diff = orc.crt_centered(orc.poly_sub(qs, got, want), qs)
+    assert max(abs(int(d)) for d in diff) <= 1
+    dec = orc.decode(P, got, lvl, scale, n)
+    assert np.max(np.abs(dec - v)) <= 2.0 ** -30
+
+
+# ------------------------------------------------------------------ C2 (bench configs[1])
+
+def test_c2_bench_params_residue_parity(m):
+    P = ps2()
+    R, F, fs = 128, 16, 20.0
+    # the bench's chain config; bins chosen inside the 16-frame DFT grid (k fs / (F-1))
+    bands_for_bins = ((1.0, 1.4), (2.0, 4.0))
+    cfg = cc.ChainCfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=fs, bands=bands_for_bins,
+                      iq_pack=3, hoist=1)
+    rots = sorted(set(cc.required_rotations("vitals_v1", cfg, P.n)) | set(cc.required_rotations("vitals_v2", cfg, P.n)))
+    keys = orc.keygen(P, seed=6001, rotations=rots)
+    z, _ = radar.vital_scene(R, F, fs, seed=6002)
+    zt = radar.preprocess_vital(z)
+    v1, v2 = [], []
+    for t in range(F):
+        for part in (zt[t].real, zt[t].imag):
+            vec = radar.pack_vital(part, cfg.n_slots)
+            pt = orc.encode(P, vec, float(2 ** P.scale_bits), 7)
+            ct = orc.encrypt(P, keys, pt, 7, float(2 ** P.scale_bits), cfg.n_slots, seed=6003, index=len(v2))
+            v2.append(ct)
+            v1.append(orc.Ct([c[:4].copy() for c in ct.c], 3, ct.scale, ct.n_slots))
+    taps = [radar.fir_taps(41, b, fs) for b in BANDS]
+    bins = [[int(k) for k in dsp.band_bins(F - 1, fs, b)] for b in bands_for_bins]
+    assert all(bins)
+    # oracle
+    ev1 = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    want1 = list(cc.vitals_v1(ev1, book, v1[0::2], v1[1::2], cfg))
+    ev2 = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    out2 = cc.vitals_v2(ev2, v2[0::2], v2[1::2], taps, cfg)
+    want2 = out2[0] + out2[1]
+    scalars = {f"k5.b{b}": t for b, t in enumerate(taps)}
+    for b in range(2):
+        for k in bins[b]:
+            c, s = dsp.narrowband_dft_coefs(F - 1, k)
+            scalars[f"vp.c.{b}.{k}"] = c
+            scalars[f"vp.s.{b}.{k}"] = s
+    ctx = make_ctx(m, P, keys, book, scalars)
+    mcfg = m.chain_cfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=cfg.n_slots, bands_bins=bins,
+                       n_taps=[41, 41], fs=fs, iq_pack=3, hoist=1)
+    for chain, ins, want, ev in (("vitals_v1", v1, want1, ev1), ("vitals_v2", v2, want2, ev2)):
+        ctx.trace_clear()
+        levels = ctx.chain_plan(chain, mcfg, ins[0].level, len(ins))
+        assert levels == [w.level for w in want]
+        outs = [ct_out(m, P, lv) for lv in levels]
+        assert ctx.eval_chain(chain, mcfg, [ct_in(m, P, c) for c in ins], outs) == len(want)
+        _check(outs, want)
+        assert ctx.trace() == ev.trace
+    # decryption gate on the |X|^2 outputs
+    I = np.array([dsp.soft_iq(zt[t], 2)[0] for t in range(F)])
+    Q = np.array([dsp.soft_iq(zt[t], 2)[1] for t in range(F)])
+    at = 0
+    for b, h in enumerate(taps):
+        y = dsp.taylor_phase(dsp.fir(I, h), dsp.fir(Q, h), 1)
+        wantp = dsp.narrowband_power(y, bins[b])
+        got = np.array([orc.decrypt_vector(P, keys, w)[0] for w in want2[at:at + len(bins[b])]])
+        at += len(bins[b])
+        assert np.max(np.abs(got - wantp)) <= 1e-3 * np.max(np.abs(wantp))
+
+
+# ------------------------------------------------------------------ C4 (bench configs[3])
+
+def _c4_case(lanes, F, seed):
+    P = ps4()
+    A, R, D = 4, 32, 32
+    cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25,
+                      hoist=1, lanes=lanes)
+    Z, _ = radar.gesture_scene(A, R, D, F, seed=seed, cls=seed % 5)
+    Zt = radar.preprocess_gesture(Z)
+    keys = orc.keygen(P, seed=seed + 1, rotations=cc.required_rotations("gesture", cfg, P.n))
+    vs = [radar.pack_doppler(Zt[t]) for t in range(F)]
+    cts = []
+    for g in range(cc.n_packed(F, lanes)):
+        group = vs[g * lanes:(g + 1) * lanes]
+        for part in ("real", "imag"):
+            vec = cc.interleave([getattr(v, part) for v in group], lanes, 4096)
+            cts.append(orc.encrypt_vector(P, keys, vec, 19, seed=seed + 2, index=len(cts)))
+    feats = [dsp.gesture_frame_features(v, A, R, D, 4) for v in vs]
+    return P, cfg, keys, cts, np.sum(feats, axis=0)
+
+
+@pytest.mark.parametrize("lanes,F", [(1, 2), (8, 16)])
+def test_c4_bench_params_residue_parity(m, lanes, F):
+    """PS4 gesture at entry level 19 with hoisted BSGS and the FC head (bench C4), bit-exact:
+    canonical (one frame per ciphertext, 2 frames) and SIMD-dense (8 frames per ciphertext,
+    2 packed ciphertext pairs = 16 frames, the bench's headline packing)."""
+    P, cfg, keys, cts, xp = _c4_case(lanes, F, 6100 + lanes)
+    Ws, bs = radar.fc_weights([4096, 64, 32, 5], seed=6200)
+    gain = min(0.8 / max(np.max(np.abs(Ws[0] @ xp)), 1e-30), 2000.0 / np.max(np.abs(Ws[0])))
+    Ws[0] = Ws[0] * gain
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    feat = cc.gesture_features(ev, book, cts[0::2], cts[1::2], cfg)
+    logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
+    ctx = make_ctx(m, P, keys, book)
+    mcfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25,
+                       hoist=1, lanes=lanes)
+    assert sorted(ctx.required_rotations("gesture", mcfg)) == cc.required_rotations("gesture", cfg, P.n)
+    levels = ctx.chain_plan("gesture", mcfg, 19, len(cts))
+    assert levels == [logits.level] == [19 - 11]
+    outs = [ct_out(m, P, logits.level)]
+    ctx.eval_chain("gesture", mcfg, [ct_in(m, P, c) for c in cts], outs)
+    _check(outs, [logits])
+    assert ctx.trace() == ev.trace
+    got = orc.decrypt_vector(P, keys, logits)[cc.logit_slots(5, lanes)]
+    want = dsp.mlp_forward(xp, Ws, bs)
+    assert np.max(np.abs(got - want)) <= 1e-3 * np.max(np.abs(want))
+    assert int(np.argmax(got)) == int(np.argmax(want))

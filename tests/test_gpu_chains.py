@@ -29,7 +29,7 @@ def _mcfg(m, cfg: cc.ChainCfg, bins=(), taps=()):
                        taylor_order=cfg.taylor_order, n_slots=cfg.n_slots, bsgs_baby=cfg.bsgs_baby,
                        fc_dims=cfg.fc_dims, notch_width=cfg.notch_width, bands_bins=bins,
                        n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch, hoist=cfg.hoist,
-                       vp_plus=cfg.vp_plus, iq_pack=cfg.iq_pack)
+                       vp_plus=cfg.vp_plus, iq_pack=cfg.iq_pack, lanes=cfg.lanes)
 
 
 def _run(m, P, keys, book, chain, cfg, cts, want, scalars=None, bins=(), taps=()):
@@ -279,6 +279,38 @@ def test_gesture_chain_small(m, F, fb, hoist):
     ev2 = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
     f0 = cc.gesture_frame(ev2, cc.PlainBook(P), cts[0], cts[1], cfg)
     _run(m, P, keys, book, "gesture_frame", cfg, cts[:2], [f0])
+
+
+@pytest.mark.parametrize("lanes,F,fb", [(4, 6, 0), (2, 5, 2), (8, 8, 0)])
+def test_gesture_chain_lanes_small(m, lanes, F, fb):
+    """SIMD-dense gesture pipeline (DESIGN R20): `lanes` frames interleaved per ciphertext,
+    ceil(F / lanes) ciphertext pairs (the last one partly empty), hoisted BSGS, FC head with
+    the lane sum: residues and trace equal the oracle's; the per-frame chain and K3 alone too."""
+    P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
+    cfg, Zt = _gesture(P, 3221, F=F, frame_batch=fb, hoist=1)
+    cfg.lanes = lanes
+    keys = orc.keygen(P, seed=3222, rotations=cc.required_rotations("gesture", cfg, P.n))
+    n = cfg.n_slots
+    cts = []
+    vs = [radar.pack_doppler(Zt[t]) for t in range(F)]
+    for g in range(cc.n_packed(F, lanes)):
+        grp = vs[g * lanes:(g + 1) * lanes]
+        for part in ("real", "imag"):
+            cts.append(orc.encrypt_vector(P, keys, cc.interleave([getattr(v, part) for v in grp], lanes, n), P.L,
+                                          seed=3223, index=len(cts)))
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    feat = cc.gesture_features(ev, book, cts[0::2], cts[1::2], cfg)
+    dims = cfg.fc_dims
+    Ws, bs = radar.fc_weights([dims[0], dims[1], dims[2], 5], seed=3224)
+    logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
+    ctx = _run(m, P, keys, book, "gesture", cfg, cts, [logits])
+    assert ctx.trace() == ev.trace
+    assert sorted(ctx.required_rotations("gesture", _mcfg(m, cfg))) == cc.required_rotations("gesture", cfg, P.n)
+    ev2 = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book2 = cc.PlainBook(P)
+    dre, dim = cc.k3_doppler_dft_frames(ev2, book2, cts[0:2:2], cts[1:2:2], cfg)
+    _run(m, P, keys, book2, "k3_doppler_dft", cfg, cts[:2], dre + dim)
 
 
 def test_frame_sharded_gesture_exchange(m):

@@ -290,3 +290,148 @@ def test_required_rotation_counts():
     assert (n_ring // 2 - 31) in k3 and 25 in k3
     vital = cc.required_rotations("vitals_v1", cc.ChainCfg(R=128), n_ring)
     assert vital == [1, 2, 4, 8, 16, 32, 64]
+
+
+# ------------------------------------------------------------------ K7 third order (pins)
+
+def test_taylor_phase_polynomial_closed_forms():
+    """Eq. taylor_arctan through angles, not the code's formula: for unit
+    phasors z_t = e^{j th_t}, y = sin(dth) and x = cos(dth), so the third-order value is
+    sin(dth) cos^2(dth) - sin^3(dth)/3 and the first-order value sin(dth); equal samples
+    give y = 0, x = 1 and a zero phase step; and y x^2 - y^3/3 = x^3 (t - t^3/3),
+    t = y/x, the cubic Taylor polynomial of x^3 arctan(t) (error <= |x|^3 |t|^5 / 5)."""
+    rng = np.random.default_rng(11)
+    th = np.cumsum(rng.uniform(-0.6, 0.6, 64))
+    I, Q = np.cos(th), np.sin(th)
+    d = np.diff(th)
+    assert np.allclose(dsp.taylor_phase(I, Q, 1), np.sin(d), atol=1e-14)
+    want3 = np.sin(d) * np.cos(d) ** 2 - np.sin(d) ** 3 / 3.0
+    assert np.allclose(dsp.taylor_phase(I, Q, 3), want3, atol=1e-14)
+    # equal consecutive samples: zero phase step at both orders
+    Ie, Qe = np.full(4, 0.6), np.full(4, 0.8)
+    assert np.allclose(dsp.taylor_phase(Ie, Qe, 1), 0.0) and np.allclose(dsp.taylor_phase(Ie, Qe, 3), 0.0)
+    # arbitrary magnitudes: within the Taylor remainder of x^3 arctan(y/x)
+    a = rng.uniform(0.3, 1.0, 65)
+    I2, Q2 = a * np.cos(np.concatenate([[0], th])), a * np.sin(np.concatenate([[0], th]))
+    y = Q2[1:] * I2[:-1] - I2[1:] * Q2[:-1]
+    x = I2[1:] * I2[:-1] + Q2[1:] * Q2[:-1]
+    t = y / x
+    got = dsp.taylor_phase(I2, Q2, 3)
+    assert np.all(np.abs(got - x ** 3 * np.arctan(t)) <= np.abs(x) ** 3 * np.abs(t) ** 5 / 5 + 1e-15)
+
+
+@pytest.mark.parametrize("order", [1, 3])
+def test_k7_taylor_phase_decrypts_to_polynomial(order):
+    """The oracle's K7 circuit (c-7: y by one lazy relin; third order x, x^2, y^2, -y/3 as an
+    exact scalar at q_l, y x^2 + y^2 (-y/3)) decrypts to the literal polynomial of the
+    plaintext I_f, Q_f slot by slot, including a slot with equal consecutive samples."""
+    P = toy(log_n=10, n_q=5, scale_bits=40, n_p=2, alpha=2)
+    F, n = 5, P.n // 2
+    rng = np.random.default_rng(order)
+    th = np.cumsum(rng.uniform(-0.5, 0.5, (F, n)), axis=0)
+    amp = rng.uniform(0.4, 1.0, (F, n))
+    I, Q = amp * np.cos(th), amp * np.sin(th)
+    I[:, 7], Q[:, 7] = 0.6, 0.8  # equal samples in slot 7: y = 0, x = 1
+    keys = orc.keygen(P, seed=2101)
+    lvl = 4
+    Ie = [_enc(P, keys, I[t], lvl, 2 * t, seed=2102) for t in range(F)]
+    Qe = [_enc(P, keys, Q[t], lvl, 2 * t + 1, seed=2102) for t in range(F)]
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    out = cc.k7_taylor_phase(ev, Ie, Qe, order)
+    assert len(out) == F - 1
+    assert out[0].level == lvl - (3 if order == 3 else 1)  # Table tab:depth: K7 depth 3 / 1
+    got = np.array([orc.decrypt_vector(P, keys, c) for c in out])
+    want = np.stack([dsp.taylor_phase(I[:, j], Q[:, j], order) for j in range(n)], axis=1)
+    assert rel_err(got, want) < 1e-3
+    assert np.max(np.abs(got[:, 7])) < 1e-6
+    # third order differs from first order (a dropped term would make them agree)
+    if order == 3:
+        y1 = np.stack([dsp.taylor_phase(I[:, j], Q[:, j], 1) for j in range(n)], axis=1)
+        assert rel_err(got, y1) > 1e-2
+
+
+def test_k7_rejects_other_orders():
+    P = toy(log_n=10, n_q=5, scale_bits=40, n_p=2, alpha=2)
+    ev = cc.CircuitEvaluator(P)
+    with pytest.raises(ValueError):
+        cc.k7_taylor_phase(ev, [], [], 2)
+
+
+def test_public_exponents_must_be_powers_of_two():
+    """gamma / p_phi are numbers of squarings (log2), never rounded; the packed
+    K4 rotate-and-sum rejects a non-power-of-two R (its blocks would overlap)."""
+    with pytest.raises(ValueError):
+        cc.log2_exact(3, "gamma")
+    assert cc.log2_exact(4, "gamma") == 2
+    with pytest.raises(ValueError):
+        cc.required_rotations("vitals_v2", cc.ChainCfg(R=100, iq_pack=1, n_slots=4096), 1 << 13)
+
+
+# ------------------------------------------------------------------ SIMD-dense lanes (R20)
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_lane_interleaved_k3_schedule_on_plain_slots(L):
+    """Reading R20 on plaintext slot vectors: with L frames interleaved (slot L i + f), the
+    K3 BSGS schedule with rotations scaled by L and lane-repeated diagonals computes every
+    frame's block-diagonal DFT exactly, and lanes never mix."""
+    D, n = 8, 32
+    cfg = cc.ChainCfg(D=D)
+    rng = np.random.default_rng(L)
+    M = rng.normal(size=(D, D))
+    frames = [rng.normal(size=n) for _ in range(L)]
+    x = cc.interleave(frames, L, n)
+    bb, giants = cc.k3_schedule(cfg)
+    babies = [cc.rot(x, s * L) for s in range(bb)]
+    y = np.zeros(n * L)
+    for gp, G, ss in giants:
+        inner = sum(cc.lane_vec(cc.rot(cc.block_diag_diagonal(M, n, G + s), -G), L) * babies[s] for s in ss)
+        y += cc.rot(inner, G * L)
+    for f in range(L):
+        assert np.allclose(y[f::L], np.kron(np.eye(n // D), M) @ frames[f])
+    # lane rotate-and-sum: lane 0 holds the sum over the L frames
+    z = y.copy()
+    s = 1
+    while s < L:
+        z = z + cc.rot(z, s)
+        s *= 2
+    assert np.allclose(z[0::L], sum(np.kron(np.eye(n // D), M) @ v for v in frames))
+
+
+def test_gesture_lanes_decrypt_like_canonical(Pg):
+    """The SIMD-dense gesture pipeline (4 frames per ciphertext, 6 frames -> 2 ciphertext
+    pairs, the last half empty) decrypts to the same logits as the plaintext DSP and the
+    same per-frame features (lane by lane) as the one-frame-per-ciphertext layout."""
+    P = Pg
+    F, L = 6, 4
+    cfg, Zt = _gesture_setup(P, F=F)
+    cfg.hoist, cfg.lanes = 1, L
+    n = cfg.n_slots
+    rots = cc.required_rotations("gesture", cfg, P.n)
+    assert 1 in rots and (cfg.D * L) in rots
+    keys = orc.keygen(P, seed=2011, rotations=rots)
+    vs = [radar.pack_doppler(Zt[t]) for t in range(F)]
+    re, im = [], []
+    for g in range(cc.n_packed(F, L)):
+        grp = vs[g * L:(g + 1) * L]
+        re.append(_enc(P, keys, cc.interleave([v.real for v in grp], L, n), P.L, 4 * g))
+        im.append(_enc(P, keys, cc.interleave([v.imag for v in grp], L, n), P.L, 4 * g + 1))
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    fr = cc.gesture_frames(ev, book, re, im, cfg)
+    fp = [dsp.gesture_frame_features(v, cfg.A, cfg.R, cfg.D, cfg.gamma) for v in vs]
+    for g, c in enumerate(fr):
+        dec = orc.decrypt_vector(P, keys, c)
+        for f in range(L):
+            want = fp[g * L + f] if g * L + f < F else np.zeros(n)
+            assert np.max(np.abs(dec[f::L] - want)) <= 1e-3 * max(np.max(np.abs(fp)), 1e-30)
+    feat = cc.frame_accumulate(ev, fr)
+    xp = np.sum(fp, axis=0)
+    dims = cfg.fc_dims
+    Ws, bs = radar.fc_weights([dims[0], dims[1], dims[2], 5], seed=7)
+    Ws[0] = Ws[0] / max(np.max(np.abs(Ws[0] @ xp)), 1e-30) * 0.8
+    logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
+    assert logits.level == P.L - 11  # lanes add rotations only, no depth
+    got = orc.decrypt_vector(P, keys, logits)[cc.logit_slots(5, L)]
+    want = dsp.mlp_forward(xp, Ws, bs)
+    assert rel_err(got, want) < 1e-3
+    assert int(np.argmax(got)) == int(np.argmax(want))

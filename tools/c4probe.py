@@ -1,0 +1,61 @@
+"""C4 gesture step at N = 2^16 (PS4, entry level 19) on uniform-residue inputs, for ncu
+captures and per-kernel CUDA-event profiles.  Usage:
+    python tools/c4probe.py [--frames 25] [--steps 1] [--profile]"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2603_22437_b200 import mmfhe as m  # noqa: E402
+from synth import radar  # noqa: E402
+from synth.params import ps4  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--frames", type=int, default=25)
+ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--profile", action="store_true")
+ap.add_argument("--lanes", type=int, default=1)
+args = ap.parse_args()
+
+dev = torch.device("cuda", 0)
+P = ps4()
+F = args.frames
+stream = torch.cuda.current_stream(dev)
+cfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25, hoist=1,
+                  lanes=args.lanes) if args.lanes > 1 else \
+    m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25, hoist=1)
+ctx = m.Context.from_params(P, device=0, stream=stream.cuda_stream)
+gen = torch.Generator(device=dev)
+gen.manual_seed(77)
+basis = list(P.q) + list(P.p)
+key_shape = (P.dnum(), 2, len(basis))
+ctx.load_relin_key(bench.uniform_dev(torch, gen, key_shape, basis, P.n, dev))
+for k in ctx.required_rotations("gesture", cfg):
+    ctx.load_galois_key(k, bench.uniform_dev(torch, gen, key_shape, basis, P.n, dev))
+Ws, bs = radar.fc_weights([4096, 64, 32, 5], seed=11)
+Ws[-1] = np.vstack([Ws[-1], np.zeros((3, 32))])
+bs[-1] = np.concatenate([bs[-1], np.zeros(3)])
+ctx.prepare_chain("gesture", cfg, 19, fc_w=Ws, fc_b=bs)
+n_in = 2 * F // max(args.lanes, 1)
+data = bench.uniform_dev(torch, gen, (n_in, 2, 20), list(P.q[:20]), P.n, dev)
+ins = m.CtArray([m.Ct(data[i], 19, 2.0 ** P.scale_bits, cfg.n_slots, P.log_n) for i in range(n_in)])
+outs = m.CtArray([m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=dev), lv, 0.0, 0, P.log_n)
+                  for lv in ctx.chain_plan("gesture", cfg, 19, n_in)])
+ctx.trace_enable(False)
+ctx.graph_enable(False)
+for _ in range(args.steps):
+    ctx.eval_chain("gesture", cfg, ins, outs)
+torch.cuda.synchronize()
+if args.profile:
+    ctx.profile_enable(True)
+    ctx.profile()
+    ctx.eval_chain("gesture", cfg, ins, outs)
+    prof = ctx.profile()
+    tot = sum(v[1] for v in prof.values())
+    print(f"gesture F={F}: kernel sum {tot:.2f} ms ({tot / F:.3f} ms/frame)")
+    for k, (c, ms, by, ops) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        print(f"   {k:16s} {ms:8.2f} ms {ms / tot:6.3f}  {c:5d} launches  {by / (ms * 1e-3) / 1e9:7.1f} GB/s")
