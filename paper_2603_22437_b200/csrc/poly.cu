@@ -745,9 +745,12 @@ void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, 
     a.L = c.L;
     a.xs = xs;
     a.ys = ys;
-    double words = 0;
-    for (const auto &p : plans) words += (double)(p.hi - p.lo) + p.n_tgt;
-    ProfScope ps(c, "modup_bconv", 8.0 * words * c.n * B);
+    double words = 0, macs = 0;
+    for (const auto &p : plans) {
+        words += (double)(p.hi - p.lo) + p.n_tgt;
+        macs += (double)(p.hi - p.lo) * p.n_tgt;  // 64x64->128 MACs per coefficient
+    }
+    ProfScope ps(c, "modup_bconv", 8.0 * words * c.n * B, macs * c.n * B);
     for (size_t j = 0; j < plans.size(); ++j) {
         const ModUpPlan &p = plans[j];
         a.d[j].hat_inv = (const TwPair *)c.bconv_ptr(p.off_hat_inv);
@@ -793,7 +796,7 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
         a.hi[j] = plans[j].hi;
     }
     const double rows = level + 1 + c.K;  // per row: key 2 dnum words once; per item dnum in + 2 out
-    ProfScope ps(c, "key_ip", 8.0 * rows * c.n * (2.0 * a.dnum + B * (a.dnum + 2.0)));
+    ProfScope ps(c, "key_ip", 8.0 * rows * c.n * (2.0 * a.dnum + B * (a.dnum + 2.0)), 2.0 * a.dnum * rows * c.n * B);
     // split the batch over grid.z so that >= ~8 CTAs per SM are in flight; the key words
     // are then re-read once per z-chunk (negligible next to the per-item traffic)
     const uint32_t ctas_xy = ((c.n + kTB - 1) / kTB) * (level + 1 + c.K);
@@ -825,7 +828,7 @@ static MDArgs md_args(Ctx &c, uint32_t level)
 void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B)
 {
     MMFHE_REQUIRE(c.K <= 16, MMFHE_E_PARAMS, "K too large");
-    ProfScope ps(c, "moddown_bconv", 16.0 * (c.K + level + 1) * c.n * B);
+    ProfScope ps(c, "moddown_bconv", 16.0 * (c.K + level + 1) * c.n * B, 2.0 * c.K * (level + 1) * c.n * B);
     const size_t smem = 8 * ((size_t)c.K * (level + 1) + 2 * (level + 1));
     const dim3 g((c.n + kBcK * kTB - 1) / (kBcK * kTB), 2 * B);
     if (c.K <= 1)
@@ -887,7 +890,8 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
         }
     }
     // algorithmic: babies read once, plaintexts once per batch, outputs written once
-    ProfScope ps(c, "diag_mac", 8.0 * (level + 1) * c.n * (terms + B * 2.0 * (a.nc + a.no)));
+    ProfScope ps(c, "diag_mac", 8.0 * (level + 1) * c.n * (terms + B * 2.0 * (a.nc + a.no)),
+                 2.0 * terms * (level + 1) * c.n * B);
     const dim3 g(((c.n + kTB - 1) / kTB) * B, 2 * (level + 1));
     if (a.nc <= 4)
         k_diag_mac<4><<<g, kTB, 0, c.stream>>>(a, c.kt, B);
@@ -902,7 +906,8 @@ void launch_lincomb_mat(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, u
                         int lo_step, const TwPair *C, uint32_t level)
 {
     MMFHE_REQUIRE(W <= 8192, MMFHE_E_SHAPE, "lincomb window too long");
-    ProfScope ps(c, "lincomb_mat", 8.0 * 2.0 * (level + 1) * c.n * ((double)M + J));
+    ProfScope ps(c, "lincomb_mat", 8.0 * 2.0 * (level + 1) * c.n * ((double)M + J),
+                 2.0 * (level + 1) * c.n * (double)J * std::min<uint32_t>(W, M));
     k_lincomb_mat<<<grid3(c.n, level + 1, (J + kJG - 1) / kJG), kTB, 0, c.stream>>>(out, in, M, J, W, lo0, lo_step,
                                                                                    C, c.kt, level);
     LAUNCH_CHECK(c);
@@ -917,7 +922,8 @@ void launch_lincomb_sym(Ctx &c, uint64_t *out, const uint64_t *in, uint32_t M, u
     once_per_device(attr, [] {
         CUDA_CHECK(cudaFuncSetAttribute(k_lincomb_sym, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     });
-    ProfScope ps(c, "lincomb_mat", 8.0 * 2.0 * (level + 1) * c.n * ((double)M + J));
+    ProfScope ps(c, "lincomb_mat", 8.0 * 2.0 * (level + 1) * c.n * ((double)M + J),
+                 2.0 * (level + 1) * c.n * (double)J * (W / 2 + (W & 1)));
     const dim3 grid(c.n / kSymK, 2 * (level + 1), (J + kSymJT - 1) / kSymJT);
     k_lincomb_sym<<<grid, kSymK * kSymSplit, smem, c.stream>>>(out, in, M, J, W, lo0, T, c.kt, level);
     LAUNCH_CHECK(c);

