@@ -28,6 +28,7 @@ Table tab:depth P:914-949.
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -125,12 +126,15 @@ class PlainBook:
     def __init__(self, P):
         self.P = P
         self.entries: dict = {}
+        self.encode_s = 0.0  # seconds spent encoding (setup work; bench.py excludes it)
 
     def vec(self, name: str, values: np.ndarray, level: int, scale: float | None = None):
         key = (name, level)
         if key not in self.entries:
+            t0 = time.perf_counter()
             sc = float(self.P.q[level]) if scale is None else float(scale)
             self.entries[key] = (orc.encode(self.P, values, sc, level), sc, np.asarray(values))
+            self.encode_s += time.perf_counter() - t0
         res, sc, _ = self.entries[key]
         return res, sc
 
@@ -303,25 +307,31 @@ def baby_steps(ev, cts, steps, hoist):
     return [[ev.hoisted_step(x, y, s) for x, y in zip(cts, ys)] for s in steps]
 
 
-def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg: ChainCfg):
-    """K3 (Eqs. dft_re/dft_im P:805-815) on a list of frames: d_re = C~ v_re - S~ v_im,
-    d_im = S~ v_re + C~ v_im via BSGS with pre-rotated diagonals; one rescale after
-    the giant sum (c-6)."""
+def k3_baby_steps(ev: CircuitEvaluator, v_re, v_im, cfg: ChainCfg):
+    """K3 BSGS baby steps: [x, Rot(x, s)] for s < b, for v_re and v_im."""
     L = lanes_of(cfg)
-    n = v_re[0].n_slots // L
-    lvl = v_re[0].level
-    W = dsp.dft_matrix(cfg.D)
-    C, S = W.real, W.imag
-    b, giants = k3_schedule(cfg)
+    b, _ = k3_schedule(cfg)
     xr = [list(v_re)] + baby_steps(ev, v_re, [s * L for s in range(1, b)], cfg.hoist)
     xi = [list(v_im)] + baby_steps(ev, v_im, [s * L for s in range(1, b)], cfg.hoist)
-    out_re = out_im = None
-    nf = len(v_re)
+    return xr, xi
+
+
+def k3_inner_sums(ev: CircuitEvaluator, book: PlainBook, xr, xi, cfg: ChainCfg):
+    """Every giant step's inner sums (one pass over the baby steps): for giant g',
+    d_re part sum_s C~'_{g',s} Rot(v_re, s) - S~'_{g',s} Rot(v_im, s) and the d_im part
+    sum_s S~'_{g',s} Rot(v_re, s) + C~'_{g',s} Rot(v_im, s), with the diagonals of
+    Eqs. dft_re / dft_im pre-rotated by -G (Halevi-Shoup)."""
+    L = lanes_of(cfg)
+    n = xr[0][0].n_slots // L
+    lvl = xr[0][0].level
+    W = dsp.dft_matrix(cfg.D)
+    C, S = W.real, W.imag
+    _, giants = k3_schedule(cfg)
+    nf = len(xr[0])
 
     def terms(spec, f):
         return [(pt, (xr if which == "r" else xi)[s][f]) for pt, s, which in spec]
 
-    # all giant steps' inner sums first (one pass over the baby steps), then the giant rotations
     inner = []
     for gp, G, babies in giants:
         t_re, t_im = [], []
@@ -336,12 +346,28 @@ def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg
             t_im += [(ps, s, "r"), (pc, s, "i")]
         inner.append(([ev.pmult_sum(terms(t_re, f)) for f in range(nf)],
                       [ev.pmult_sum(terms(t_im, f)) for f in range(nf)]))
+    return inner
+
+
+def k3_giant_steps(ev: CircuitEvaluator, inner, cfg: ChainCfg):
+    """Giant rotations Rot(inner_g', G) summed over g', one rescale after the sum (c-6)."""
+    L = lanes_of(cfg)
+    _, giants = k3_schedule(cfg)
+    out_re = out_im = None
     for (gp, G, babies), (pr, pi) in zip(giants, inner):
         ir = [ev.rotate(x, G * L) for x in pr]
         ii = [ev.rotate(x, G * L) for x in pi]
         out_re = ir if out_re is None else [ev.add(a, x) for a, x in zip(out_re, ir)]
         out_im = ii if out_im is None else [ev.add(a, x) for a, x in zip(out_im, ii)]
     return [ev.rescale(x) for x in out_re], [ev.rescale(x) for x in out_im]
+
+
+def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg: ChainCfg):
+    """K3 (Eqs. dft_re/dft_im P:805-815) on a list of frames: d_re = C~ v_re - S~ v_im,
+    d_im = S~ v_re + C~ v_im via BSGS with pre-rotated diagonals: baby steps, all giant
+    steps' inner sums, then the giant rotations; one rescale after the giant sum (c-6)."""
+    xr, xi = k3_baby_steps(ev, v_re, v_im, cfg)
+    return k3_giant_steps(ev, k3_inner_sums(ev, book, xr, xi, cfg), cfg)
 
 
 def k3_doppler_dft(ev, book, v_re, v_im, cfg):

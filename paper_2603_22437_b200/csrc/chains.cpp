@@ -520,7 +520,8 @@ class Runner {
         return ev_rescale(c_, ev_lincomb_mat(c_, S, 2, K, 0, 0, coef));
     }
 
-    std::vector<DCt> vitals_v2(const mmfhe_ct *in, size_t n_in)
+    // K4 over every frame batch of (re_t, im_t) inputs: (I, Q) each a batch of F items
+    std::pair<DCt, DCt> k4_all_frames(const mmfhe_ct *in, size_t n_in)
     {
         const uint32_t F = (uint32_t)(n_in / 2), fb = frame_batch(F);
         std::vector<DCt> Is, Qs;
@@ -534,10 +535,23 @@ class Runner {
         }
         DCt I = Is.size() == 1 ? std::move(Is[0]) : concat(c_, Is);
         DCt Q = Qs.size() == 1 ? std::move(Qs[0]) : concat(c_, Qs);
+        return {std::move(I), std::move(Q)};
+    }
+
+    const std::vector<double> &band_taps(uint32_t b)
+    {
+        const std::vector<double> &taps = scalars("k5.b" + std::to_string(b), nullptr);
+        MMFHE_REQUIRE(cfg_.n_taps[b] == 0 || taps.size() == cfg_.n_taps[b], MMFHE_E_SHAPE, "FIR tap count");
+        return taps;
+    }
+
+    std::vector<DCt> vitals_v2(const mmfhe_ct *in, size_t n_in)
+    {
+        auto iq = k4_all_frames(in, n_in);
+        const DCt &I = iq.first, &Q = iq.second;
         std::vector<DCt> out;
         for (uint32_t b = 0; b < cfg_.n_bands; ++b) {
-            const std::vector<double> &taps = scalars("k5.b" + std::to_string(b), nullptr);
-            MMFHE_REQUIRE(cfg_.n_taps[b] == 0 || taps.size() == cfg_.n_taps[b], MMFHE_E_SHAPE, "FIR tap count");
+            const std::vector<double> &taps = band_taps(b);
             DCt If = k5_fir(I, taps);
             DCt Qf = k5_fir(Q, taps);
             DCt ys = k7_taylor_phase(If, Qf);
@@ -602,6 +616,14 @@ uint32_t chain_depth(const std::string &chain, const mmfhe_chain_cfg &cfg)
     if (chain == "gesture_fc") return fc;
     if (chain == "gesture") return gf + fc;
     if (chain == "gesture_features") return gf;
+    // the paper's kernels on their own ("can be used individually or composed")
+    if (chain == "k2_soft_attention") return lg + 1;
+    if (chain == "k2_doppler_soft_power") return lg + 1;
+    if (chain == "k4_soft_iq") return 1 + lp + 1;
+    if (chain == "k5_fir") return 1;
+    if (chain == "k6_notch") return 1;
+    if (chain == "k7_taylor_phase") return cfg.taylor_order == 3 ? 3 : 1;
+    if (chain == "fc_forward") return fc;
     throw Error(MMFHE_E_INVALID_ARG, "unknown chain " + chain);
 }
 
@@ -616,9 +638,9 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
         if (v) ks.insert(v);
     };
     chain_depth(chain, cfg);  // validates the name
-    if (chain == "vitals_v1" || chain == "vitals_v2")
+    if (chain == "vitals_v1" || chain == "vitals_v2" || chain == "k2_soft_attention" || chain == "k4_soft_iq")
         for (uint32_t s : rotsum_steps(cfg.R, 1)) add(s);
-    if (chain == "vitals_v2" && cfg.iq_pack) {
+    if ((chain == "vitals_v2" || chain == "k4_soft_iq") && cfg.iq_pack) {
         MMFHE_REQUIRE(cfg.iq_pack <= 8 && ((size_t)cfg.R << cfg.iq_pack) <= (size_t)(cfg.n_slots ? cfg.n_slots : c.n / 2),
                       MMFHE_E_SHAPE, "iq_pack = k needs 2^k R <= n slots");
         for (uint32_t j = 0; j < cfg.iq_pack; ++j) {
@@ -635,9 +657,9 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
         for (uint32_t b = 1; b < s.b; ++b) add(b * L);
         for (auto &g : s.giants) add(g.G * L);
     }
-    if (frames)
+    if (frames || chain == "k2_doppler_soft_power")
         for (uint32_t s : rotsum_steps(cfg.n_slots / cfg.D, cfg.D * (uint32_t)L)) add(s);
-    if (chain == "gesture_fc" || chain == "gesture") {
+    if (chain == "gesture_fc" || chain == "gesture" || chain == "fc_forward") {
         for (uint32_t s : rotsum_steps((uint32_t)L, 1)) add(s);
         for (int layer = 0; layer < 3; ++layer) {
             const uint32_t h = cfg.fc_dims[layer + 1], n_in = cfg.fc_dims[layer];
@@ -673,8 +695,31 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
     } else if (chain == "k3_doppler_dft" || chain == "gesture_frame" || chain == "gesture_features") {
         MMFHE_REQUIRE(n_in >= 2 && n_in % 2 == 0, MMFHE_E_SHAPE, "expected (v_re, v_im) per frame");
         n_out = chain == "k3_doppler_dft" ? n_in : chain == "gesture_frame" ? n_in / 2 : 1;
-    } else if (chain == "gesture_fc") {
+    } else if (chain == "gesture_fc" || chain == "fc_forward") {
         MMFHE_REQUIRE(n_in == 1, MMFHE_E_SHAPE, "expected one feature ciphertext");
+    } else if (chain == "k2_soft_attention") {
+        MMFHE_REQUIRE(n_in == 1 && cfg.F > 0, MMFHE_E_SHAPE, "expected one energy ciphertext E (and cfg.F)");
+        n_out = 2;
+    } else if (chain == "k2_doppler_soft_power" || chain == "k6_notch") {
+        MMFHE_REQUIRE(cfg.D > 0 && cfg.n_slots % cfg.D == 0, MMFHE_E_SHAPE, "D must divide the packing period");
+        n_out = n_in;
+    } else if (chain == "k4_soft_iq") {
+        MMFHE_REQUIRE(n_in == 2 * (size_t)cfg.F && cfg.F > 0, MMFHE_E_SHAPE, "expected 2F input ciphertexts");
+        n_out = n_in;
+        if (cfg.iq_pack) {
+            const uint32_t g = 1u << (cfg.iq_pack - 1), fb = cfg.frame_batch ? std::min(cfg.frame_batch, cfg.F) : cfg.F;
+            MMFHE_REQUIRE(cfg.iq_pack <= 8 && fb % g == 0 && (cfg.F % fb) % g == 0, MMFHE_E_SHAPE,
+                          "iq_pack = k needs a multiple of 2^(k-1) frames in every frame batch");
+            MMFHE_REQUIRE(((size_t)cfg.R << cfg.iq_pack) <= (size_t)(cfg.n_slots ? cfg.n_slots : c.n / 2),
+                          MMFHE_E_SHAPE, "iq_pack = k needs 2^k R <= n slots");
+        }
+    } else if (chain == "k5_fir") {
+        MMFHE_REQUIRE(n_in >= 1 && cfg.n_bands >= 1 && cfg.n_bands <= 4, MMFHE_E_SHAPE,
+                      "expected a frame sequence and 1..4 FIR bands");
+        n_out = n_in * cfg.n_bands;
+    } else if (chain == "k7_taylor_phase") {
+        MMFHE_REQUIRE(n_in >= 4 && n_in % 2 == 0, MMFHE_E_SHAPE, "expected (I_f, Q_f) per frame, F >= 2");
+        n_out = n_in / 2 - 1;
     }
     if (chain == "vitals_v2") {
         MMFHE_REQUIRE(cfg.F >= 2 && cfg.n_bands <= 4, MMFHE_E_SHAPE, "vitals_v2 needs F >= 2 and <= 4 bands");
@@ -691,7 +736,8 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
     }
     if (lanes_of(cfg) > 1) {
         const bool lane_chain = chain == "gesture" || chain == "gesture_frame" || chain == "gesture_features" ||
-                                chain == "gesture_fc" || chain == "k3_doppler_dft";
+                                chain == "gesture_fc" || chain == "k3_doppler_dft" || chain == "fc_forward" ||
+                                chain == "k2_doppler_soft_power" || chain == "k6_notch";
         MMFHE_REQUIRE(lane_chain, MMFHE_E_SHAPE, "lanes > 1 applies to the gesture / K3 chains only");
         MMFHE_REQUIRE((size_t)lanes_of(cfg) * (cfg.n_slots ? cfg.n_slots : 1) <= c.n / 2, MMFHE_E_SHAPE,
                       "lanes * n_slots must not exceed N/2");
@@ -749,6 +795,27 @@ std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_c
         out.push_back(r.gesture(in, n_in));
     } else if (chain == "gesture_features") {
         out.push_back(r.gesture_features(in, n_in));
+    } else if (chain == "fc_forward") {
+        DCt x = import_batch(c, in, 0, 1, 1);
+        out.push_back(r.gesture_fc(x));
+    } else if (chain == "k2_soft_attention") {
+        auto nd = r.k2_soft_attention(import_batch(c, in, 0, 1, 1));
+        out.push_back(std::move(nd.first));
+        out.push_back(std::move(nd.second));
+    } else if (chain == "k2_doppler_soft_power" || chain == "k6_notch") {
+        DCt x = import_batch(c, in, 0, 1, n_in);
+        out.push_back(chain == "k6_notch" ? r.k6_notch(x) : r.k2_doppler_soft_power(x));
+    } else if (chain == "k4_soft_iq") {
+        auto iq = r.k4_all_frames(in, n_in);
+        out.push_back(std::move(iq.first));
+        out.push_back(std::move(iq.second));
+    } else if (chain == "k5_fir") {
+        DCt x = import_batch(c, in, 0, 1, n_in);
+        for (uint32_t b = 0; b < cfg.n_bands; ++b) out.push_back(r.k5_fir(x, r.band_taps(b)));
+    } else if (chain == "k7_taylor_phase") {
+        DCt If = import_batch(c, in, 0, 2, n_in / 2);
+        DCt Qf = import_batch(c, in, 1, 2, n_in / 2);
+        out.push_back(r.k7_taylor_phase(If, Qf));
     }
     return out;
 }

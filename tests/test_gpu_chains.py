@@ -454,3 +454,110 @@ def test_chain_shape_and_depth_errors(m):
     rots = ctx.required_rotations("vitals_v2", c3)
     assert all((8 << j) in rots and (P.n // 2 - (8 << j)) in rots for j in range(3))
     assert rots == cc.required_rotations("vitals_v2", cc.ChainCfg(R=8, F=8, n_slots=P.n // 2, iq_pack=3), P.n)
+
+
+# ------------------------------------------------------------------ the kernels on their own
+
+def _enc_list(P, keys, vals, level, seed):
+    return [orc.encrypt_vector(P, keys, v, level, seed=seed, index=i) for i, v in enumerate(vals)]
+
+
+def test_standalone_k2_k4_k7_chains(m):
+    """k2_soft_attention, k4_soft_iq (canonical and packed), k7_taylor_phase (first and
+    third order) as chains of their own: residues and trace equal the oracle kernels'."""
+    P = toy(log_n=10, n_q=6, scale_bits=40, n_p=2, alpha=2)
+    rng = np.random.default_rng(71)
+    cfg = cc.ChainCfg(R=8, F=8, gamma=2, p_phi=2, n_slots=P.n // 2, frame_batch=4)
+    cfgp = cc.ChainCfg(R=8, F=8, gamma=2, p_phi=2, n_slots=P.n // 2, frame_batch=4, iq_pack=3, hoist=1)
+    rots = sorted(set(cc.required_rotations("k2_soft_attention", cfg, P.n)) |
+                  set(cc.required_rotations("k4_soft_iq", cfgp, P.n)))
+    keys = orc.keygen(P, seed=3601, rotations=rots)
+    # K2a on an energy ciphertext E (values in [0, F] in the first R slots)
+    E = orc.encrypt_vector(P, keys, radar.pack_vital(rng.uniform(0, 8, 8), cfg.n_slots), 3, seed=3602, index=0)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    N, D = cc.k2_soft_attention(ev, book, E, cfg)
+    ctx = _run(m, P, keys, book, "k2_soft_attention", cfg, [E], [N, D])
+    assert ctx.trace() == ev.trace
+    # K4 per frame batch (frame_batch 4), outputs I_0..I_{F-1}, Q_0..Q_{F-1}
+    z = rng.uniform(-0.5, 0.5, (8, 8)) + 1j * rng.uniform(-0.5, 0.5, (8, 8))
+    cts = []
+    for t in range(8):
+        for part in (z[t].real, z[t].imag):
+            cts.append(orc.encrypt_vector(P, keys, radar.pack_vital(part, cfg.n_slots), 4, seed=3603,
+                                          index=len(cts)))
+    for c in (cfg, cfgp):
+        ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+        I, Q = [], []
+        for s, e in cc.chunks(8, c.frame_batch):
+            Ib, Qb = cc.k4_soft_iq(ev, cts[2 * s:2 * e:2], cts[2 * s + 1:2 * e:2], c)
+            I += Ib
+            Q += Qb
+        ctx = _run(m, P, keys, None, "k4_soft_iq", c, cts, I + Q)
+        assert ctx.trace() == ev.trace
+    # K7 on (I_f, Q_f) pairs
+    P7 = toy(log_n=10, n_q=5, scale_bits=40, n_p=2, alpha=2)
+    keys7 = orc.keygen(P7, seed=3604)
+    th = np.cumsum(rng.uniform(-0.4, 0.4, (5, P7.n // 2)), axis=0)
+    If = _enc_list(P7, keys7, np.cos(th), 4, 3605)
+    Qf = _enc_list(P7, keys7, np.sin(th), 4, 3606)
+    pairs = [x for t in range(5) for x in (If[t], Qf[t])]
+    for order in (1, 3):
+        c7 = cc.ChainCfg(taylor_order=order, n_slots=P7.n // 2)
+        ev = cc.CircuitEvaluator(P7, keys7.rlk, keys7.gk)
+        ys = cc.k7_taylor_phase(ev, If, Qf, order)
+        ctx = _run(m, P7, keys7, None, "k7_taylor_phase", c7, pairs, ys)
+        assert ctx.trace() == ev.trace
+
+
+def test_standalone_k5_fir_long_window(m):
+    """k5_fir on its own with an asymmetric 300-tap filter over 300 frames (the general
+    k_lincomb_mat path, window > 256: the 128-bit accumulator's hi-word fold)
+    and a symmetric 41-tap band (k_lincomb_sym): two bands, outputs band-major."""
+    P = toy(log_n=10, n_q=3, scale_bits=40, n_p=1, alpha=1)
+    rng = np.random.default_rng(72)
+    F = 300
+    keys = orc.keygen(P, seed=3611)
+    xs = _enc_list(P, keys, rng.uniform(-1, 1, (F, P.n // 2)), 2, 3612)
+    taps = [rng.uniform(-1, 1, 300), radar.fir_taps(41, (0.8, 2.5), 20.0)]
+    cfg = cc.ChainCfg(F=F, n_slots=P.n // 2)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    want = []
+    for h in taps:
+        want += cc.k5_fir(ev, xs, h)
+    scalars = {f"k5.b{b}": t for b, t in enumerate(taps)}
+    ctx = _run(m, P, keys, None, "k5_fir", cfg, xs, want, scalars=scalars, bins=([1], [1]), taps=taps)
+    assert ctx.trace() == ev.trace
+
+
+@pytest.mark.parametrize("lanes", [1, 4])
+def test_standalone_k6_k2b_fc_chains(m, lanes):
+    """k6_notch, k2_doppler_soft_power and fc_forward as chains of their own (with and
+    without SIMD-dense lanes): residues and trace equal the oracle kernels'."""
+    P = toy(log_n=10, n_q=8, scale_bits=40, n_p=2, alpha=2)
+    n = 64
+    cfg = cc.ChainCfg(A=2, R=4, D=8, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8), hoist=1, lanes=lanes)
+    rots = sorted(set(cc.required_rotations("k2_doppler_soft_power", cfg, P.n)) |
+                  set(cc.required_rotations("fc_forward", cfg, P.n)))
+    keys = orc.keygen(P, seed=3621, rotations=rots)
+    rng = np.random.default_rng(73)
+    vals = [cc.interleave([rng.uniform(0, 1, n) for _ in range(lanes)], lanes, n) for _ in range(3)]
+    Ps = _enc_list(P, keys, vals, 7, 3622)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    want = cc.k6_notch(ev, book, Ps, cfg)
+    ctx = _run(m, P, keys, book, "k6_notch", cfg, Ps, want)
+    assert ctx.trace() == ev.trace
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    want = cc.k2_doppler_soft_power(ev, Ps, cfg)
+    ctx = _run(m, P, keys, None, "k2_doppler_soft_power", cfg, Ps, want)
+    assert ctx.trace() == ev.trace
+    feat = Ps[0]
+    Ws, bs = radar.fc_weights([n, 16, 8, 5], seed=3623)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    logits = cc.gesture_fc(ev, book, orc.Ct([c[:6].copy() for c in feat.c], 5, feat.scale, feat.n_slots),
+                           Ws, bs, cfg)
+    feat5 = orc.Ct([c[:6].copy() for c in feat.c], 5, feat.scale, feat.n_slots)
+    ctx = _run(m, P, keys, book, "fc_forward", cfg, [feat5], [logits])
+    assert ctx.trace() == ev.trace
