@@ -193,7 +193,14 @@ mmfhe_status mmfhe_load_scalars(mmfhe_ctx *ctx, const char *name, const double *
 /* ---- chains -------------------------------------------------- */
 
 /* Chains: "k1_energy", "vitals_v1", "vitals_v2", "k3_doppler_dft",
- * "gesture_frame", "gesture_fc", "gesture" (frames + accumulate + FC).
+ * "gesture_frame", "gesture_fc", "gesture" (frames + accumulate + FC), "gesture_features"
+ * (frames + accumulate: the per-rank partial of a frame-sharded session), and the kernels
+ * on their own ("used individually or composed"): "k2_soft_attention" (in: E;
+ * out: N, D), "k2_doppler_soft_power" (in: K6 outputs Pm_t; out: f_t), "k4_soft_iq" (in:
+ * re_t, im_t per frame; out: I_0..I_{F-1}, Q_0..Q_{F-1}), "k5_fir" (in: x_0..x_{F-1}; out:
+ * per band b the filtered sequence with taps "k5.b<b>", band-major), "k6_notch" (in: P_t;
+ * out: Pm_t), "k7_taylor_phase" (in: I_f,t, Q_f,t per frame; out: dphi_1..dphi_{F-1}),
+ * "fc_forward" (in: features; out: logits; = gesture_fc).
  * in[0..n_in): input ciphertexts in the order the chain documents (DESIGN.md
  * §2): k1/vitals: re_0, im_0, re_1, im_1, ...; gesture*: v_re_t, v_im_t per frame.
  * Outputs: k1_energy one E per session; vitals_v1 (N, D); vitals_v2 the P_k of every
@@ -270,6 +277,42 @@ mmfhe_status mmfhe_mod_switch(mmfhe_ctx *ctx, const mmfhe_ct *a, uint32_t level,
 /* ---- batched ops (throughput benches): n independent ciphertexts ---------- */
 mmfhe_status mmfhe_hrot_batch(mmfhe_ctx *ctx, const mmfhe_ct *a, size_t n, int32_t step, mmfhe_ct *out);
 mmfhe_status mmfhe_hmult_batch(mmfhe_ctx *ctx, const mmfhe_ct *a, const mmfhe_ct *b, size_t n, mmfhe_ct *out);
+
+/* ---- serialisation ("versioned little-endian binary (magic, params
+ * digest, per-prime residue arrays)"; keys are sent once and cached) ----
+ * Blob layout, every field little-endian:
+ *    0  char[8]  magic "MMFHEBLB"
+ *    8  u32      version (1)
+ *   12  u32      kind: MMFHE_SER_CT (ciphertext / plaintext), MMFHE_SER_RELIN_KEY,
+ *                MMFHE_SER_GALOIS_KEY
+ *   16  u64      params digest (mmfhe_params_digest: FNV-1a 64 over "mmfhe-params-v1",
+ *                u32 log_n, u32 n_q, u64 q[n_q], u32 n_p, u64 p[n_p], u32 alpha, all LE)
+ *   24  u32      log_n
+ *   28  u32      level (ct) / L (key)
+ *   32  u32      n_polys (ct) / dnum_L (key)
+ *   36  u32      n_slots (ct) / K (key)
+ *   40  f64      scale (ct) / 0
+ *   48  i32      rotation step normalised to [0, N/2) (Galois key) / 0
+ *   52  u32      n_rows: number of residue arrays
+ *   56  u64      payload bytes = n_rows * N * 8
+ *   64  u8[n_rows] prime index of each array (0..L: q_i, L+1..L+K: p_k), zero-padded to 8
+ *   ..  u64[n_rows][N] residues in COEFFICIENT form, each < its prime
+ * Arrays are in the ABI layouts: ct [n_polys][level+1], key [dnum][2][L+1+K].  Any other
+ * magic, version, digest, size, prime order or an unreduced residue: MMFHE_E_FORMAT. */
+enum { MMFHE_SER_CT = 0, MMFHE_SER_RELIN_KEY = 1, MMFHE_SER_GALOIS_KEY = 2 };
+mmfhe_status mmfhe_params_digest(mmfhe_ctx *ctx, uint64_t *digest);
+/* ct (host or device, coefficient or evaluation form; evaluation form is converted) into
+ * buf[0..cap); *len = blob size (buf == NULL: size query only; cap too small: E_LAYOUT). */
+mmfhe_status mmfhe_serialize_ct(mmfhe_ctx *ctx, const mmfhe_ct *ct, void *buf, size_t cap, size_t *len);
+/* Blob -> caller buffer out->data (host or device per out->on_device, holding n_polys *
+ * (level+1) * N words); writes out's level, scale, n_slots, n_polys, form = COEFF. */
+mmfhe_status mmfhe_deserialize_ct(mmfhe_ctx *ctx, const void *buf, size_t len, mmfhe_ct *out);
+/* Package client key words ([dnum][2][L+1+K][N] coefficient form, as mmfhe_load_*_key)
+ * into a blob (the packaging only; the library never holds a secret key). */
+mmfhe_status mmfhe_serialize_key(mmfhe_ctx *ctx, int kind, int32_t step, const uint64_t *words, size_t n_words,
+                                 int on_device, void *buf, size_t cap, size_t *len);
+/* Load a relinearisation or Galois key blob into the ctx's key store. */
+mmfhe_status mmfhe_load_key_serialized(mmfhe_ctx *ctx, const void *buf, size_t len);
 
 /* ---- op trace (Theorem P:999-1006: data-oblivious execution) -------------- */
 /* One logical op per line: "<op> <level> <arg>".  mmfhe_trace_clear resets. */

@@ -130,6 +130,11 @@ def lib():
             "mmfhe_profile_enable": [V, ctypes.c_int],
             "mmfhe_profile_get": [V, ctypes.c_char_p, S, P(S)],
             "mmfhe_microbench": [V, ctypes.c_int, P(ctypes.c_double)],
+            "mmfhe_params_digest": [V, P(U64)],
+            "mmfhe_serialize_ct": [V, CTP, V, S, P(S)],
+            "mmfhe_deserialize_ct": [V, V, S, CTP],
+            "mmfhe_serialize_key": [V, ctypes.c_int, I32, V, S, ctypes.c_int, V, S, P(S)],
+            "mmfhe_load_key_serialized": [V, V, S],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -150,8 +155,11 @@ EXPORTED = [
     "mmfhe_relin", "mmfhe_hrot", "mmfhe_hrot_hoisted", "mmfhe_rescale", "mmfhe_keyswitch", "mmfhe_mod_switch", "mmfhe_hrot_batch",
     "mmfhe_hmult_batch", "mmfhe_trace_get", "mmfhe_trace_clear", "mmfhe_trace_enable", "mmfhe_profile_enable",
     "mmfhe_profile_get", "mmfhe_microbench", "mmfhe_graph_enable", "mmfhe_graph_stats", "mmfhe_eval_chain_async",
-    "mmfhe_ctx_sync",
+    "mmfhe_ctx_sync", "mmfhe_params_digest", "mmfhe_serialize_ct", "mmfhe_deserialize_ct", "mmfhe_serialize_key",
+    "mmfhe_load_key_serialized",
 ]
+
+SER_CT, SER_RELIN_KEY, SER_GALOIS_KEY = 0, 1, 2
 
 
 def _u64_array(vals):
@@ -431,6 +439,39 @@ class Context:
             k, c, ms, b, ops = line.split()
             out[k] = (int(c), float(ms), float(b), float(ops))
         return out
+
+    # ---- serialisation (include/mmfhe.h documents the blob layout)
+    def params_digest(self):
+        d = ctypes.c_uint64()
+        self._check(self._lib.mmfhe_params_digest(self.h, ctypes.byref(d)))
+        return int(d.value)
+
+    def serialize_ct(self, ct) -> bytes:
+        s = ct.struct()
+        n = ctypes.c_size_t()
+        self._check(self._lib.mmfhe_serialize_ct(self.h, ctypes.byref(s), None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        self._check(self._lib.mmfhe_serialize_ct(self.h, ctypes.byref(s), buf, n.value, ctypes.byref(n)))
+        return buf.raw[: n.value]
+
+    def deserialize_ct(self, blob: bytes, out):
+        s = out.struct()
+        self._check(self._lib.mmfhe_deserialize_ct(self.h, blob, len(blob), ctypes.byref(s)))
+        out.level, out.scale, out.n_slots, out.n_polys, out.form = s.level, s.scale, s.n_slots, s.n_polys, s.form
+        return out
+
+    def serialize_key(self, kind, step, words) -> bytes:
+        addr, dev = _ptr(words)
+        n = ctypes.c_size_t()
+        self._check(self._lib.mmfhe_serialize_key(self.h, kind, int(step), addr, _numel(words), dev, None, 0,
+                                                  ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        self._check(self._lib.mmfhe_serialize_key(self.h, kind, int(step), addr, _numel(words), dev, buf, n.value,
+                                                  ctypes.byref(n)))
+        return buf.raw[: n.value]
+
+    def load_key_serialized(self, blob: bytes):
+        self._check(self._lib.mmfhe_load_key_serialized(self.h, blob, len(blob)))
 
     def microbench(self, kind):
         """Whole-GPU ops/s of one register-resident op: 0 CT butterfly, 1 GS butterfly,
