@@ -305,7 +305,7 @@ def run_gpu(args, rank, world, device):
             except Exception as e:  # report, do not hide
                 extras[wl] = {"error": f"{type(e).__name__}: {e}"}
     if not args.no_c5:
-        extras["C5"] = bench_c5(m, torch, device, rank, world)
+        extras["C5"] = bench_c5(args, m, torch, device, rank, world)
     return dict(value=value, ms=ms_max / args.steps, launches=launches, clocks=clk.summary(), prof=prof,
                 prof_steps=prof_steps, prof_ms=prof_ms / prof_steps, e2e=e2e, extras=extras, cfg=cfg, P=P,
                 int_peaks=int_peaks)
@@ -419,89 +419,178 @@ def bench_workload(name, m, torch, device, steps=3, warmup=2):
     return res
 
 
-def bench_c5(m, torch, device, rank, world, sessions_per_rank=1, F=100, steps=2, warmup=2):
-    """C5 batched multi-session gesture serving (BASELINE configs[4]) with the method's one
-    exchange step: G = sessions_per_rank * world sessions per step; every session's F
-    frames are sharded over the ranks (paper_2603_22437_b200.dist.shard); each rank runs
-    gesture_features on its shard of every session, the per-rank partial feature
-    ciphertexts are all-gathered over NCCL, and the owner of each session sums them in the
-    library (mmfhe_sum_partials) and runs the FC head.  Weak scaling: per-rank work is
-    fixed (F frames + sessions_per_rank FC heads per step)."""
-    from paper_2603_22437_b200 import dist as mdist
+def c5_vital_cfg(m):
+    """C5's vital session (the paper's config): R=64, F=200 @ 20 Hz at PS4,
+    vitals_v1 (entry 3) + vitals_v2 first order with VP+ in the cloud (entry 9, depth 9)."""
+    F, fs = 200, 20.0
     from synth import radar
-    from synth.params import ps4
+    cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=1 << 15,
+                      bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
+                      frame_batch=40, vp_plus=1, iq_pack=3, hoist=1)
+    return cfg, F, [radar.fir_taps(41, b, fs) for b in BANDS]
+
+
+def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=1):
+    """C5 batched multi-session serving (BASELINE configs[4]): per step Gv vital
+    + Gg gesture sessions spread over the ranks, one shared key set (SURVEY §8(d) C5 assumption):
+      * vital sessions are session-sharded (no exchange): each rank runs vitals_v1 + vitals_v2
+        (full depth, VP+, PS4) on its share of the sessions;
+      * every gesture session's ciphertext pairs (8 frames each) are frame-sharded over the ranks
+        (paper_2603_22437_b200.dist.shard): each rank computes gesture_features of its pairs of
+        EVERY gesture session, the partial feature ciphertexts are all-gathered over NCCL, and the
+        session's owner sums them in the library (mmfhe_sum_partials) and runs gesture_fc -- the
+        method's one exchange step.
+    Device-resident: inputs from a pool of `pool` distinct encrypted sessions per rank and type,
+    cycled (disclosed).  H2D-included: every session's inputs uploaded from pinned host memory
+    inside the timed region, in waves (mmfhe_eval_chain_async: the upload of session i+1 on the
+    library's copy stream overlaps the compute of session i).  Weak scaling: Gv = Gg = sessions
+    per rank x world unless --c5-sessions fixes the totals.  Frames/s = (Gv F_v + Gg F_g) / time
+    (max over ranks), also per type."""
+    from paper_2603_22437_b200 import dist as mdist
     import torch.distributed as tdist
     distributed = tdist.is_available() and tdist.is_initialized()
-    P = ps4()
-    lvl = 19
+    P, gcfg = c4_config(LANES)
+    per_rank = args.c5_per_rank
+    Gv = Gg = args.c5_sessions // 2 if args.c5_sessions else per_rank * world
     stream = torch.cuda.current_stream(device)
+    vcfg, Fv, taps = c5_vital_cfg(m)
+    # one shared key set: every rotation of both pipelines (same seed on every rank)
+    ctx, gm = make_gesture_ctx(m, torch, P, gcfg, device, seed=9100, chains=("gesture",))
     gen = torch.Generator(device=device)
-    gen.manual_seed(9100)  # same keys on every rank (the client's key set, replicated)
-    cfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25,
-                      hoist=1)
-    ctx = m.Context.from_params(P, device=device.index or 0, stream=stream.cuda_stream)
+    gen.manual_seed(9101)
     basis = list(P.q) + list(P.p)
     key_shape = (P.dnum(), 2, len(basis))
-    ctx.load_relin_key(uniform_dev(torch, gen, key_shape, basis, P.n, device))
-    for k in ctx.required_rotations("gesture", cfg):
+    have = set(ctx.required_rotations("gesture", gm))
+    for k in sorted((set(ctx.required_rotations("vitals_v1", vcfg)) | set(ctx.required_rotations("vitals_v2", vcfg)))
+                    - have):
         ctx.load_galois_key(k, uniform_dev(torch, gen, key_shape, basis, P.n, device))
-    Ws, bs = radar.fc_weights([4096, 64, 32, 5], seed=11)
-    Ws[-1] = np.vstack([Ws[-1], np.zeros((3, 32))])
-    bs[-1] = np.concatenate([bs[-1], np.zeros(3)])
-    ctx.prepare_chain("gesture", cfg, lvl, fc_w=Ws, fc_b=bs)
-    G = sessions_per_rank * world
-    lo, hi = mdist.shard(F, rank, world)
-    gen_in = torch.Generator(device=device)
-    gen_in.manual_seed(9200 + rank)
+    ctx.prepare_chain("vitals_v2", vcfg, 9, taps=taps)
+    ctx.prepare_chain("vitals_v1", vcfg, 3)
+    pool = args.c5_pool
     scale = float(2 ** P.scale_bits)
-    data = uniform_dev(torch, gen_in, (G, 2 * (hi - lo), 2, lvl + 1), list(P.q[: lvl + 1]), P.n, device)
-    frames_by_session = [m.CtArray([m.Ct(data[s, i], lvl, scale, 4096, P.log_n) for i in range(2 * (hi - lo))])
-                         for s in range(G)]
-    mine = [s for s in range(G) if mdist.owner(s, world) == rank]
-    ctx.trace_enable(False)
-    # persistent chain output buffers: stable addresses, so the library's chain graphs are
-    # captured during warm-up and replayed in the timed steps (never captured inside them)
-    lvf = ctx.chain_plan("gesture_features", cfg, lvl, len(frames_by_session[0]))[0]
-    lvo = ctx.chain_plan("gesture_fc", cfg, lvf, 1)[0]
-    feat_bufs = torch.empty((G, 2, lvf + 1, P.n), dtype=torch.int64, device=device)
+    # vital pool: V1 inputs at level 3, V2 at level 9 (the client encrypts at the entry levels)
+    vpool = []
+    for i in range(pool):
+        d1 = uniform_dev(torch, gen, (2 * Fv, 2, 4), list(P.q[:4]), P.n, device)
+        d2 = uniform_dev(torch, gen, (2 * Fv, 2, 10), list(P.q[:10]), P.n, device)
+        vpool.append((d1, d2, m.CtArray([m.Ct(d1[j], 3, scale, vcfg.n_slots, P.log_n) for j in range(2 * Fv)]),
+                      m.CtArray([m.Ct(d2[j], 9, scale, vcfg.n_slots, P.log_n) for j in range(2 * Fv)])))
+    lv1 = ctx.chain_plan("vitals_v1", vcfg, 3, 2 * Fv)
+    lv2 = ctx.chain_plan("vitals_v2", vcfg, 9, 2 * Fv)
+    vouts = (m.CtArray([m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=device), lv, 0.0, 0, P.log_n)
+                        for lv in lv1]),
+             m.CtArray([m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=device), lv, 0.0, 0, P.log_n)
+                        for lv in lv2]))
+    my_vital = list(range(*mdist.shard(Gv, rank, world)))
+    # gesture pool: this rank's pair shard of a session
+    npair = n_pairs(gcfg)
+    plo, phi = mdist.shard(npair, rank, world)
+    gdata, gsess = gesture_inputs(m, torch, P, gcfg, device, seed=9200 + rank, sessions=pool)
+    gpool = [m.CtArray(s[2 * plo:2 * phi]) for s in gsess]
+    lvf = ctx.chain_plan("gesture_features", gm, gcfg["level"], max(2 * (phi - plo), 2))[0]
+    lvo = ctx.chain_plan("gesture_fc", gm, lvf, 1)[0]
+    feat_bufs = torch.empty((Gg, 2, lvf + 1, P.n), dtype=torch.int64, device=device)
+    mine = [s for s in range(Gg) if mdist.owner(s, world) == rank]
     sum_bufs = {s: torch.empty((2, lvf + 1, P.n), dtype=torch.int64, device=device) for s in mine}
     fc_outs = {s: m.Ct(torch.empty((2, lvo + 1, P.n), dtype=torch.int64, device=device), lvo, 0.0, 0, P.log_n,
                        m.FORM_EVAL) for s in mine}
+    ctx.trace_enable(False)
+    xbytes = [0]
 
-    def step():
-        partials, lv, sc = mdist.sessions_features(ctx, m, cfg, frames_by_session, lvl, scale, 4096, P.log_n, device,
-                                                   bufs=feat_bufs)
-        gathered = mdist.allgather_partials(partials)
+    def gesture_phase(frames_of):
+        if phi > plo:
+            mdist.sessions_features(ctx, m, gm, [frames_of(s) for s in range(Gg)], gcfg["level"], scale,
+                                    gcfg["n_slots"] * LANES, P.log_n, device, bufs=feat_bufs)
+        else:  # more ranks than pairs: this rank contributes zero partials
+            feat_bufs.zero_()
+        gathered = mdist.allgather_partials(feat_bufs)
+        xbytes[0] = feat_bufs.numel() * 8
         for s in mine:
-            total = mdist.reduce_partials(ctx, m, gathered, s, lv, sc, 4096, P.log_n, buf=sum_bufs[s])
-            ctx.eval_chain("gesture_fc", cfg, [total], [fc_outs[s]])
-        return partials.numel() * 8
+            total = mdist.reduce_partials(ctx, m, gathered, s, lvf, scale_f[0], gcfg["n_slots"] * LANES, P.log_n,
+                                          buf=sum_bufs[s])
+            ctx.eval_chain("gesture_fc", gm, [total], [fc_outs[s]])
 
-    for _ in range(warmup):
-        step()
-    torch.cuda.synchronize(device)
-    if distributed:
-        tdist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        xbytes = step()
-    e1.record(stream)
-    torch.cuda.synchronize(device)
-    if distributed:
-        tdist.barrier()
-    ms = e0.elapsed_time(e1) / steps
-    t = torch.tensor([ms], dtype=torch.float64, device=device)
-    if distributed:
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    ms = float(t.item())
+    # the features' scale (the reduce needs it before the first gather)
+    probe = m.Ct(torch.empty((2, lvf + 1, P.n), dtype=torch.int64, device=device), lvf, 0.0, 0, P.log_n, m.FORM_EVAL)
+    ctx.eval_chain("gesture_features", gm, gpool[0] if phi > plo else gsess[0][:2], [probe])
+    scale_f = [probe.scale]
+
+    def step_dev():
+        for i, s in enumerate(my_vital):
+            _, _, a1, a2 = vpool[i % pool]
+            ctx.eval_chain("vitals_v1", vcfg, a1, vouts[0])
+            ctx.eval_chain("vitals_v2", vcfg, a2, vouts[1])
+        gesture_phase(lambda s: gpool[s % pool])
+
+    def timed(fn):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize(device)
+        if distributed:
+            tdist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        wall = (time.perf_counter() - t0) / steps
+        if distributed:
+            tdist.barrier()
+        t = torch.tensor([e0.elapsed_time(e1) / steps, wall * 1e3], dtype=torch.float64, device=device)
+        if distributed:
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t[0].item()), float(t[1].item())
+
+    ms_dev, _ = timed(step_dev)
+    # H2D-included: pinned host copies of one vital and one gesture session (the uplink), every
+    # session's inputs uploaded inside the timed region through mmfhe_eval_chain_async
+    hv1 = vpool[0][0].cpu().pin_memory()
+    hv2 = vpool[0][1].cpu().pin_memory()
+    hg = gdata[0].cpu().pin_memory()
+    hv1a = m.CtArray([m.Ct(hv1[j], 3, scale, vcfg.n_slots, P.log_n) for j in range(2 * Fv)])
+    hv2a = m.CtArray([m.Ct(hv2[j], 9, scale, vcfg.n_slots, P.log_n) for j in range(2 * Fv)])
+    hga = m.CtArray([m.Ct(hg[j], gcfg["level"], scale, gcfg["n_slots"] * LANES, P.log_n)
+                     for j in range(2 * plo, 2 * phi)]) if phi > plo else None
+    h2d = [0]
+
+    def sessions_features_async():
+        for s in range(Gg):
+            o = m.Ct(feat_bufs[s], lvf, 0.0, 0, P.log_n, m.FORM_EVAL)
+            ctx.eval_chain_async("gesture_features", gm, hga, m.CtArray([o]))
+
+    def step_h2d():
+        for s in my_vital:
+            ctx.eval_chain_async("vitals_v1", vcfg, hv1a, vouts[0])
+            ctx.eval_chain_async("vitals_v2", vcfg, hv2a, vouts[1])
+        if hga is not None:
+            sessions_features_async()
+        ctx.sync()
+        gathered = mdist.allgather_partials(feat_bufs)
+        for s in mine:
+            total = mdist.reduce_partials(ctx, m, gathered, s, lvf, scale_f[0], gcfg["n_slots"] * LANES, P.log_n,
+                                          buf=sum_bufs[s])
+            ctx.eval_chain("gesture_fc", gm, [total], [fc_outs[s]])
+        h2d[0] = len(my_vital) * (hv1.numel() + hv2.numel()) * 8 + (Gg * hg[2 * plo:2 * phi].numel() * 8)
+
+    _, ms_h2d = timed(step_h2d)
     ctx.close()
-    del data, frames_by_session
+    del vpool, gdata, gsess, gpool, feat_bufs, hv1, hv2, hg
     torch.cuda.empty_cache()
-    return {"frames_per_s": G * F / (ms / 1e3), "ms_per_step": ms, "sessions_per_step": G, "frames_per_session": F,
-            "n_gpus": world, "allgather_bytes_per_rank_per_step": xbytes,
-            "config": "PS4 gesture sessions, frames sharded over ranks, NCCL all-gather of partial feature "
-                      "ciphertexts + library mod-q sum + FC on the owning rank; weak scaling in sessions"}
+    fv, fg = Gv * Fv, Gg * gcfg["F"]
+    return {"frames_per_s": (fv + fg) / (ms_dev / 1e3), "vital_frames_per_s": fv / (ms_dev / 1e3),
+            "gesture_frames_per_s": fg / (ms_dev / 1e3), "ms_per_step": ms_dev,
+            "h2d_included": {"frames_per_s": (fv + fg) / (ms_h2d / 1e3), "ms_per_step": ms_h2d,
+                             "h2d_bytes_per_step_rank0": h2d[0], "clock": "host wall, max over ranks"},
+            "sessions_per_step": {"vital": Gv, "gesture": Gg}, "n_gpus": world,
+            "allgather_bytes_per_rank_per_step": xbytes[0], "device_pool_sessions_per_type": pool,
+            "config": (f"{Gv} vital sessions (R=64, F=200 @ 20 Hz, V1 + full-depth V2 with VP+, session-sharded) + "
+                       f"{Gg} gesture sessions (C4, 8 frames per ciphertext, {npair} pairs frame-sharded over the "
+                       f"ranks, NCCL all-gather of partial feature ciphertexts, library mod-q sum + FC on the owner) "
+                       f"per step at PS4 (N=2^16), one shared key set; device-resident inputs cycle a pool of {pool} "
+                       f"distinct sessions per type; h2d_included uploads every session from pinned host memory "
+                       f"inside the timed region (copy-stream waves)")}
 
 
 def extras_n16(args, m, torch, device, batch=8, reps=3):
@@ -887,6 +976,10 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the multi-GPU C5 exchange workload")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--c5-per-rank", type=int, default=8, help="C5: vital and gesture sessions per rank (weak scaling)")
+    ap.add_argument("--c5-sessions", type=int, default=0,
+                    help="C5: total sessions per step (half vital, half gesture; 1024 = SURVEY's full C5)")
+    ap.add_argument("--c5-pool", type=int, default=2, help="C5: distinct device-resident sessions per type")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-out", default="")
     args = ap.parse_args()
