@@ -212,12 +212,6 @@ __device__ __forceinline__ void st_run(uint64_t *p, const uint64_t *v)
                          : "memory");
     }
 }
-// TMA bulk prefetch of a contiguous range into L2 (one instruction, no registers held).
-__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes)
-{
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
 // A round's register pattern straight from / to global memory, one vector per run.
 template <int ELOG, int LO, int W>
 __device__ __forceinline__ void ld_pattern(const uint64_t *blk, int ktr, uint64_t (&v)[1 << ELOG])
@@ -407,36 +401,6 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
     uint64_t *a = data + ((size_t)row << LOGN);
     uint64_t *buf0 = sm, *buf1 = sm + S * G;
     uint64_t *blk = a + ((size_t)gi << LOGS);  // row pass: this group's block
-    if constexpr (EPI && !COL) {
-        // The epilogue's operands (ModDown's / the rescale's minuend X and the addends) are
-        // read only after the last round: one TMA bulk prefetch per group and operand pulls
-        // their 2^LOGS-word blocks into L2 now, so those loads hit L2 instead of exposing
-        // DRAM latency at the end of the pass (the sigma_g-permuted addend's words of an
-        // aligned block lie in one aligned block: perm_g keeps the top bits' dependence)
-        if (t == 0) {
-            constexpr uint32_t BY = 8u << LOGS;
-            const size_t b = row / (2 * ep.per);
-            const uint32_t rr = (uint32_t)(row % (2 * ep.per)), poly = rr / ep.per, i = rr % ep.per;
-            const size_t boff = ((size_t)i << LOGN) + ((size_t)gi << LOGS);
-            prefetch_l2(ep.X + b * ep.xs + poly * ep.xps + boff, BY);
-            const size_t ao = b * ep.as + boff;
-            if (poly == 0) {
-                if (ep.add0) {
-                    size_t src = boff;
-                    if (ep.g0 != 1) {
-                        const uint32_t j = (uint32_t)gi << LOGS;
-                        const uint32_t ex = ((2u * (__brev(j) >> (32 - LOGN)) + 1u) * ep.g0) & ((2u << LOGN) - 1u);
-                        const uint32_t pj = __brev((ex - 1u) >> 1) >> (32 - LOGN);
-                        src = ((size_t)i << LOGN) + (pj & ~((1u << LOGS) - 1u));
-                    }
-                    prefetch_l2(ep.add0 + b * ep.as + src, BY);
-                }
-                if (ep.add2) prefetch_l2(ep.add2 + ao, BY);
-            } else if (ep.add1) {
-                prefetch_l2(ep.add1 + ao, BY);
-            }
-        }
-    }
     uint64_t v[E];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
