@@ -430,7 +430,7 @@ def c5_vital_cfg(m):
     return cfg, F, [radar.fir_taps(41, b, fs) for b in BANDS]
 
 
-def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=1):
+def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
     """C5 batched multi-session serving (BASELINE configs[4]): per step Gv vital
     + Gg gesture sessions spread over the ranks, one shared key set (SURVEY §8(d) C5 assumption):
       * vital sessions are session-sharded (no exchange): each rank runs vitals_v1 + vitals_v2
