@@ -107,6 +107,9 @@ typedef struct {
     uint32_t bsgs_baby;    /* K3 baby steps b (0: ceil(sqrt(2D-1))) */
     uint32_t hoist;        /* 1: rotations of one ciphertext by several amounts share one ModUp
                               (hoisted HRot: K3 / FC baby steps, K4's packed unpack);
+                              2: double-hoisted BSGS for K3 and FC (baby steps kept over Q_l u P, diagonals
+                              encoded over Q_l u P, each giant step ModDowns only its inner sum's c1 and
+                              keeps its key switch over Q_l u P, one ModDown per output; K4's unpack as 1);
                               0: every rotation is a full HRot.  Different residues, same decryption */
     uint32_t frame_batch;  /* frames evaluated together per batched launch (0: all);
                               fixes the op order of the trace (op-major per batch) */
@@ -174,6 +177,9 @@ mmfhe_status mmfhe_load_galois_key(mmfhe_ctx *ctx, int32_t step, const uint64_t 
 /* Import a pre-encoded plaintext (n_polys = 1, form COEFF) under (name, level).
  * pt->scale is its scale (q_level for multiplicative operands). */
 mmfhe_status mmfhe_load_plain(mmfhe_ctx *ctx, const char *name, const mmfhe_ct *pt);
+/* The same for a plaintext over Q_level u P (double-hoisted BSGS diagonals):
+ * pt->data holds [level+1+K][N] (q_0..q_level, then p_0..p_{K-1}); stored as "<name>.pq". */
+mmfhe_status mmfhe_load_plain_pq(mmfhe_ctx *ctx, const char *name, const mmfhe_ct *pt);
 /* Encode v[0..n) (period n, replicated to N/2 slots) at (level, scale) with the
  * library's own canonical-embedding encoder and store it under (name, level). */
 mmfhe_status mmfhe_encode_plain(mmfhe_ctx *ctx, const char *name, const double *v, size_t n, uint32_t level,

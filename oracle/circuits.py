@@ -138,6 +138,18 @@ class PlainBook:
         res, sc, _ = self.entries[key]
         return res, sc
 
+    def vec_pq(self, name: str, values: np.ndarray, level: int):
+        """The same encoding over Q_level u P (double-hoisted BSGS diagonals), stored under
+        (name + ".pq", level); Delta_pt = q_level."""
+        key = (name + ".pq", level)
+        if key not in self.entries:
+            t0 = time.perf_counter()
+            sc = float(self.P.q[level])
+            self.entries[key] = (orc.encode_pq(self.P, values, sc, level), sc, np.asarray(values))
+            self.encode_s += time.perf_counter() - t0
+        res, sc, _ = self.entries[key]
+        return res, sc
+
 
 # ------------------------------------------------------------------ evaluator ext
 
@@ -181,6 +193,23 @@ class CircuitEvaluator(orc.Evaluator):
                 sc = s
             elif s != sc:
                 raise orc.ScaleError("pmult_sum scale mismatch")
+        return orc.Ct(acc, ct0.level, sc, ct0.n_slots)
+
+    def pmult_sum_pq(self, terms) -> orc.Ct:
+        """sum_i pt_i (.) ct_i over Q_l u P (PQ ciphertexts and PQ-encoded plaintexts)."""
+        ct0 = terms[0][1]
+        self._rec("pmult_sum_pq", ct0.level, str(len(terms)))
+        basis = self.pq_basis(ct0.level)
+        acc = None
+        sc = None
+        for (pt, pts), ct in terms:
+            t = [orc.poly_mul(basis, x, pt) for x in ct.c]
+            acc = t if acc is None else [orc.poly_add(basis, x, y) for x, y in zip(acc, t)]
+            s = ct.scale * pts
+            if sc is None:
+                sc = s
+            elif s != sc:
+                raise orc.ScaleError("pmult_sum_pq scale mismatch")
         return orc.Ct(acc, ct0.level, sc, ct0.n_slots)
 
     def lincomb_scalar(self, cts, coefs) -> orc.Ct:
@@ -300,17 +329,32 @@ def k3_schedule(cfg: ChainCfg):
 
 def baby_steps(ev, cts, steps, hoist):
     """[[Rot(x, s) for x in cts] for s in steps]: plain HRots, or hoisted HRots that
-    share one ModUp per ciphertext (SURVEY §8(c)-5 'Hoisted HRot is a different op')."""
+    share one ModUp per ciphertext (SURVEY §8(c)-5 'Hoisted HRot is a different op'),
+    or (hoist = 2, double hoisting) hoisted rotations left over Q_l u P."""
     if not hoist:
         return [[ev.rotate(x, s) for x in cts] for s in steps]
     ys = [ev.hoist_modup(x) for x in cts]
+    if hoist == 2:
+        return [[ev.hoisted_step_pq(x, y, s) for x, y in zip(cts, ys)] for s in steps]
     return [[ev.hoisted_step(x, y, s) for x, y in zip(cts, ys)] for s in steps]
+
+
+def dh(cfg) -> bool:
+    """Double-hoisted BSGS (cfg.hoist = 2): baby steps stay over
+    Q_l u P (no ModDown), the inner sums multiply PQ-encoded diagonals, every giant step
+    ModDowns only its inner sum's second polynomial before its key switch and keeps the
+    result over Q_l u P, and one ModDown per output ends the giant sum."""
+    return getattr(cfg, "hoist", 0) == 2
 
 
 def k3_baby_steps(ev: CircuitEvaluator, v_re, v_im, cfg: ChainCfg):
     """K3 BSGS baby steps: [x, Rot(x, s)] for s < b, for v_re and v_im."""
     L = lanes_of(cfg)
     b, _ = k3_schedule(cfg)
+    if dh(cfg):
+        xr = [[ev.lift_pq(x) for x in v_re]] + baby_steps(ev, v_re, [s * L for s in range(1, b)], 2)
+        xi = [[ev.lift_pq(x) for x in v_im]] + baby_steps(ev, v_im, [s * L for s in range(1, b)], 2)
+        return xr, xi
     xr = [list(v_re)] + baby_steps(ev, v_re, [s * L for s in range(1, b)], cfg.hoist)
     xi = [list(v_im)] + baby_steps(ev, v_im, [s * L for s in range(1, b)], cfg.hoist)
     return xr, xi
@@ -339,13 +383,15 @@ def k3_inner_sums(ev: CircuitEvaluator, book: PlainBook, xr, xi, cfg: ChainCfg):
             o = G + s
             dc = lane_vec(rot(block_diag_diagonal(C, n, o), -G), L)
             ds = lane_vec(rot(block_diag_diagonal(S, n, o), -G), L)
-            pc = book.vec(f"k3.c.{gp}.{s}", dc, lvl)
-            ps = book.vec(f"k3.s.{gp}.{s}", ds, lvl)
-            pns = book.vec(f"k3.ns.{gp}.{s}", -ds, lvl)
+            vec = book.vec_pq if dh(cfg) else book.vec
+            pc = vec(f"k3.c.{gp}.{s}", dc, lvl)
+            ps = vec(f"k3.s.{gp}.{s}", ds, lvl)
+            pns = vec(f"k3.ns.{gp}.{s}", -ds, lvl)
             t_re += [(pc, s, "r"), (pns, s, "i")]
             t_im += [(ps, s, "r"), (pc, s, "i")]
-        inner.append(([ev.pmult_sum(terms(t_re, f)) for f in range(nf)],
-                      [ev.pmult_sum(terms(t_im, f)) for f in range(nf)]))
+        psum = ev.pmult_sum_pq if dh(cfg) else ev.pmult_sum
+        inner.append(([psum(terms(t_re, f)) for f in range(nf)],
+                      [psum(terms(t_im, f)) for f in range(nf)]))
     return inner
 
 
@@ -354,11 +400,15 @@ def k3_giant_steps(ev: CircuitEvaluator, inner, cfg: ChainCfg):
     L = lanes_of(cfg)
     _, giants = k3_schedule(cfg)
     out_re = out_im = None
+    rot, add = (ev.rotate_pq, ev.add_pq) if dh(cfg) else (ev.rotate, ev.add)
     for (gp, G, babies), (pr, pi) in zip(giants, inner):
-        ir = [ev.rotate(x, G * L) for x in pr]
-        ii = [ev.rotate(x, G * L) for x in pi]
-        out_re = ir if out_re is None else [ev.add(a, x) for a, x in zip(out_re, ir)]
-        out_im = ii if out_im is None else [ev.add(a, x) for a, x in zip(out_im, ii)]
+        ir = [rot(x, G * L) for x in pr]
+        ii = [rot(x, G * L) for x in pi]
+        out_re = ir if out_re is None else [add(a, x) for a, x in zip(out_re, ir)]
+        out_im = ii if out_im is None else [add(a, x) for a, x in zip(out_im, ii)]
+    if dh(cfg):
+        out_re = [ev.moddown_ct(x) for x in out_re]
+        out_im = [ev.moddown_ct(x) for x in out_im]
     return [ev.rescale(x) for x in out_re], [ev.rescale(x) for x in out_im]
 
 
@@ -458,20 +508,23 @@ def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int
     h = W.shape[0]
     lvl = x.level
     b, giants = fc_schedule(h)
-    babies = [x] + [r[0] for r in baby_steps(ev, [x], [s * L for s in range(1, min(b, h))], hoist)]
+    pq = hoist == 2  # double-hoisted BSGS (see dh())
+    babies = ([ev.lift_pq(x)] if pq else [x]) + [r[0] for r in baby_steps(ev, [x], [s * L for s in range(1, min(b, h))],
+                                                                           hoist)]
     acc = None
     inners = []  # all giant steps' inner sums first, then the giant rotations
+    vec = book.vec_pq if pq else book.vec
     for gp, G, ss in giants:
         terms = []
         for s in ss:
             dg = lane_vec(rot(fc_diagonal(W, n_in, G + s), -G), L)
-            terms.append((book.vec(f"fc{layer}.d.{gp}.{s}", dg, lvl), babies[s]))
-        inners.append(ev.pmult_sum(terms))
+            terms.append((vec(f"fc{layer}.d.{gp}.{s}", dg, lvl), babies[s]))
+        inners.append(ev.pmult_sum_pq(terms) if pq else ev.pmult_sum(terms))
     for (gp, G, ss), inner in zip(giants, inners):
         if G:
-            inner = ev.rotate(inner, G * L)
-        acc = inner if acc is None else ev.add(acc, inner)
-    z = ev.rescale(acc)
+            inner = ev.rotate_pq(inner, G * L) if pq else ev.rotate(inner, G * L)
+        acc = inner if acc is None else (ev.add_pq(acc, inner) if pq else ev.add(acc, inner))
+    z = ev.rescale(ev.moddown_ct(acc) if pq else acc)
     y = ev.rotsum_all([z], n_in // h, h * L)[0]
     bv = lane_vec(np.asarray(bias, dtype=np.float64), L)
     y = ev.add_plain(y, book.vec(f"fc{layer}.bias", bv, y.level, scale=y.scale))

@@ -202,6 +202,14 @@ def encode(P: ParamSet, v, scale: float, level: int) -> np.ndarray:
     return small_to_rns(mi, P.q[: level + 1])
 
 
+def encode_pq(P: ParamSet, v, scale: float, level: int) -> np.ndarray:
+    """The same integer encoding as encode(), reduced mod q_0..q_level, p_0..p_{K-1}: the
+    form in which double-hoisted BSGS multiplies its diagonals."""
+    m = np.rint(embed_inverse(replicate(v, P.n), P.n) * float(scale))
+    assert np.max(np.abs(m)) < 2.0 ** 62, "encoding overflow"
+    return small_to_rns(m.astype(np.int64), list(P.q[: level + 1]) + list(P.p))
+
+
 def decode(P: ParamSet, res: np.ndarray, level: int, scale: float, n_slots: int) -> np.ndarray:
     ints = crt_centered(res, P.q[: level + 1])
     m = np.array([float(x) for x in ints]) / float(scale)
@@ -501,6 +509,108 @@ class Evaluator:
         lib().or_moddown(P.n, l, _arr(P.q), P.K, _arr(P.p), _arr(acc1), d1)
         qs = self.qs(l)
         return Ct([poly_add(qs, automorphism(qs, a.c[0], g), d0), d1], l, a.scale, a.n_slots)
+
+    # --- double hoisting ("baby steps in PQ with P sigma(c0) lift,
+    # diagonals encoded in PQ, one ModDown per giant group" -- a third op, pinned here).
+    # A PQ ciphertext holds P * (a ciphertext) over the extended basis Q_l u P: rows
+    # q_0..q_l then p_0..p_{K-1} per polynomial (level = l).
+    def pq_basis(self, level):
+        return list(self.P.q[: level + 1]) + list(self.P.p)
+
+    def _p_mod(self, basis):
+        Pm = 1
+        for p in self.P.p:
+            Pm *= int(p)
+        return np.array([Pm % int(t) for t in basis], dtype=np.uint64)
+
+    def lift_pq(self, a: Ct) -> Ct:
+        """(P c0, P c1) over Q_l u P (zero mod every p_k): the identity baby step."""
+        self._rec("lift_pq", a.level)
+        basis = self.pq_basis(a.level)
+        pm = self._p_mod(basis)
+        l1 = a.level + 1
+        out = []
+        for x in a.c:
+            y = np.zeros((len(basis), self.P.n), dtype=np.uint64)
+            y[:l1] = poly_scalar(basis[:l1], x, pm[:l1])
+            out.append(y)
+        return Ct(out, a.level, a.scale, a.n_slots)
+
+    def hoisted_step_pq(self, a: Ct, ys: list, k: int) -> Ct:
+        """A hoisted rotation left in PQ: (P sigma_g(c0) + sum_j sigma_g(y_j) (.) b_j,
+        sum_j sigma_g(y_j) (.) a_j) over Q_l u P -- the hoisted HRot without its ModDown."""
+        P = self.P
+        l = a.level
+        kn = k % (P.n // 2)
+        if kn == 0:
+            return self.lift_pq(a)
+        if kn not in self.gk:
+            raise KeyError(f"missing Galois key for rotation {kn}")
+        self._rec("hrot_hoisted_pq", l, str(kn))
+        basis = self.pq_basis(l)
+        nkey = P.L + 1 + P.K
+        g = galois_element(P, kn)
+        evk = self.gk[kn]
+        acc0 = np.zeros((l + 1 + P.K, P.n), dtype=np.uint64)
+        acc1 = np.zeros_like(acc0)
+        for j, y in enumerate(ys):
+            sy = automorphism(basis, y, g)
+            kb = np.concatenate([evk[j, 0, : l + 1], evk[j, 0, P.L + 1: nkey]])
+            ka = np.concatenate([evk[j, 1, : l + 1], evk[j, 1, P.L + 1: nkey]])
+            acc0 = poly_add(basis, acc0, poly_mul(basis, sy, kb))
+            acc1 = poly_add(basis, acc1, poly_mul(basis, sy, ka))
+        pm = self._p_mod(basis)
+        c0 = np.zeros_like(acc0)
+        c0[: l + 1] = poly_scalar(basis[: l + 1], automorphism(self.qs(l), a.c[0], g), pm[: l + 1])
+        return Ct([poly_add(basis, acc0, c0), acc1], l, a.scale, a.n_slots)
+
+    def moddown_poly(self, x: np.ndarray, level: int) -> np.ndarray:
+        """ModDown of one polynomial over Q_l u P to Q_l."""
+        P = self.P
+        out = np.empty((level + 1, P.n), dtype=np.uint64)
+        lib().or_moddown(P.n, level, _arr(P.q), P.K, _arr(P.p), _arr(x), out)
+        return out
+
+    def rotate_pq(self, a: Ct, k: int) -> Ct:
+        """Giant step of double-hoisted BSGS on a PQ ciphertext a = (a0, a1):
+        a1' = ModDown(a1) (to Q_l), then the rotation's key switch without ModDown:
+        (sigma_g(a0) + sum_j y_j (.) b_j, sum_j y_j (.) a_j) over Q_l u P with
+        y_j = ModUp_j(sigma_g(a1')) -- ModDown first, then the automorphism (BConv does not
+        commute with sigma_g's sign flips, so the order is pinned)."""
+        P = self.P
+        l = a.level
+        kn = k % (P.n // 2)
+        if kn == 0:
+            return a
+        if kn not in self.gk:
+            raise KeyError(f"missing Galois key for rotation {kn}")
+        self._rec("hrot_pq", l, str(kn))
+        basis = self.pq_basis(l)
+        nkey = P.L + 1 + P.K
+        g = galois_element(P, kn)
+        evk = self.gk[kn]
+        x = automorphism(self.qs(l), self.moddown_poly(a.c[1], l), g)
+        acc0 = np.zeros((l + 1 + P.K, P.n), dtype=np.uint64)
+        acc1 = np.zeros_like(acc0)
+        for j in range(-(-(l + 1) // P.alpha)):
+            y = np.empty((l + 1 + P.K, P.n), dtype=np.uint64)
+            lib().or_modup(P.n, l, _arr(P.q), P.K, _arr(P.p), P.alpha, j, _arr(x), y)
+            kb = np.concatenate([evk[j, 0, : l + 1], evk[j, 0, P.L + 1: nkey]])
+            ka = np.concatenate([evk[j, 1, : l + 1], evk[j, 1, P.L + 1: nkey]])
+            acc0 = poly_add(basis, acc0, poly_mul(basis, y, kb))
+            acc1 = poly_add(basis, acc1, poly_mul(basis, y, ka))
+        return Ct([poly_add(basis, automorphism(basis, a.c[0], g), acc0), acc1], l, a.scale, a.n_slots)
+
+    def add_pq(self, a: Ct, b: Ct) -> Ct:
+        self._check_pair(a, b)
+        self._rec("hadd_pq", a.level)
+        basis = self.pq_basis(a.level)
+        return Ct([poly_add(basis, x, y) for x, y in zip(a.c, b.c)], a.level, a.scale, a.n_slots)
+
+    def moddown_ct(self, a: Ct) -> Ct:
+        """Both polynomials of a PQ ciphertext back to Q_l (divides out P)."""
+        self._rec("moddown", a.level)
+        return Ct([self.moddown_poly(x, a.level) for x in a.c], a.level, a.scale, a.n_slots)
 
     def rescale(self, a: Ct) -> Ct:
         """Divide by q_level with the pinned round-half-up rule (c-5)."""

@@ -270,6 +270,18 @@ mmfhe_status mmfhe_load_plain(mmfhe_ctx *ctx, const char *name, const mmfhe_ct *
     API_END(ctx)
 }
 
+mmfhe_status mmfhe_load_plain_pq(mmfhe_ctx *ctx, const char *name, const mmfhe_ct *pt)
+{
+    API_BEGIN
+    state_changed(*ctx);
+    MMFHE_REQUIRE(name && pt && pt->data, MMFHE_E_INVALID_ARG, "null argument");
+    MMFHE_REQUIRE(pt->log_n == ctx->log_n, MMFHE_E_PARAMS, "ring dimension mismatch");
+    MMFHE_REQUIRE(pt->form == MMFHE_FORM_COEFF, MMFHE_E_FORMAT, "plaintexts are imported in coefficient form");
+    load_plain(*ctx, name, pt->level, pt->scale, pt->data, pt->on_device != 0, true);
+    ctx->sync();
+    API_END(ctx)
+}
+
 mmfhe_status mmfhe_encode_plain(mmfhe_ctx *ctx, const char *name, const double *v, size_t n, uint32_t level,
                                 double scale)
 {

@@ -144,14 +144,16 @@ class Runner {
     Runner(Ctx &c, const mmfhe_chain_cfg &cfg) : c_(c), cfg_(cfg) {}
 
     const DPlain &plain(const std::string &name, uint32_t level, double scale,
-                        const std::function<std::vector<double>()> &values)
+                        const std::function<std::vector<double>()> &values, bool pq = false)
     {
-        DPlain *p = c_.find_plain(name, level);
+        const std::string key = pq ? name + ".pq" : name;
+        DPlain *p = c_.find_plain(key, level);
         if (p) return *p;
-        MMFHE_REQUIRE(c_.auto_encode, MMFHE_E_MISSING_PLAIN, "missing plaintext operand " + plain_key(name, level));
-        encode_plain(c_, name, values(), level, scale);
-        return *c_.find_plain(name, level);
+        MMFHE_REQUIRE(c_.auto_encode, MMFHE_E_MISSING_PLAIN, "missing plaintext operand " + plain_key(key, level));
+        encode_plain(c_, name, values(), level, scale, pq);
+        return *c_.find_plain(key, level);
     }
+    bool dh() const { return cfg_.hoist == 2; }
     double qscale(uint32_t level) const { return (double)c_.primes[level]; }
 
     const std::vector<double> &scalars(const std::string &name, const std::function<std::vector<double>()> &fn)
@@ -171,6 +173,15 @@ class Runner {
     std::vector<DCt> baby_steps(const DCt &x, uint32_t nb)
     {
         std::vector<DCt> out;
+        if (dh()) {
+            // double hoisting: the baby steps stay over Q_l u P (identity: the P lift)
+            out.push_back(ev_lift_pq(c_, x));
+            std::vector<int32_t> st;
+            for (uint32_t b = 1; b < nb; ++b) st.push_back((int32_t)(b * L()));
+            if (!st.empty())
+                for (auto &r : ev_rotate_hoisted_pq(c_, x, st)) out.push_back(std::move(r));
+            return out;
+        }
         out.push_back(copy_ct(c_, x));
         if (cfg_.hoist) {
             std::vector<int32_t> st;
@@ -251,9 +262,9 @@ class Runner {
             for (uint32_t b : g.babies) {
                 const int32_t o = g.G + (int32_t)b;
                 const std::string sfx = "." + std::to_string(g.gp) + "." + std::to_string(b);
-                const DPlain &pc = plain("k3.c" + sfx, lvl, qscale(lvl), [&] { return diag(false, o, g.G, false); });
-                const DPlain &ps = plain("k3.s" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, false); });
-                const DPlain &pn = plain("k3.ns" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, true); });
+                const DPlain &pc = plain("k3.c" + sfx, lvl, qscale(lvl), [&] { return diag(false, o, g.G, false); }, dh());
+                const DPlain &ps = plain("k3.s" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, false); }, dh());
+                const DPlain &pn = plain("k3.ns" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, true); }, dh());
                 re[b] = &pc;
                 re[s.b + b] = &pn;
                 im[b] = &ps;
@@ -267,8 +278,9 @@ class Runner {
         bool first = true;
         for (size_t gi = 0; gi < s.giants.size(); ++gi) {
             const auto &g = s.giants[gi];
-            DCt ir = ev_rotate(c_, inner[2 * gi], g.G * (int32_t)L());
-            DCt ii = ev_rotate(c_, inner[2 * gi + 1], g.G * (int32_t)L());
+            const int32_t step = g.G * (int32_t)L();
+            DCt ir = dh() ? ev_rotate_pq(c_, inner[2 * gi], step) : ev_rotate(c_, inner[2 * gi], step);
+            DCt ii = dh() ? ev_rotate_pq(c_, inner[2 * gi + 1], step) : ev_rotate(c_, inner[2 * gi + 1], step);
             if (first) {
                 out_re = std::move(ir);
                 out_im = std::move(ii);
@@ -277,6 +289,10 @@ class Runner {
                 out_re = ev_addsub(c_, out_re, ir, false);
                 out_im = ev_addsub(c_, out_im, ii, false);
             }
+        }
+        if (dh()) {  // one ModDown per output ends the double-hoisted giant sum
+            out_re = ev_moddown_ct(c_, out_re);
+            out_im = ev_moddown_ct(c_, out_im);
         }
         DCt a = ev_rescale(c_, out_re);
         DCt b = ev_rescale(c_, out_im);
@@ -351,7 +367,7 @@ class Runner {
                     std::vector<double> v(n_in);
                     for (uint32_t j = 0; j < n_in; ++j) v[j] = (*W)[(size_t)(j % h) * n_in + (j + i) % n_in];
                     return lane_rep(rot(v, -g.G), L());
-                });
+                }, dh());
             }
             rows.push_back(row);
         }
@@ -361,7 +377,10 @@ class Runner {
         for (size_t gi = 0; gi < s.giants.size(); ++gi) {
             const auto &g = s.giants[gi];
             DCt inner = std::move(inners[gi]);
-            if (g.G) inner = ev_rotate(c_, inner, g.G * (int32_t)L());
+            if (g.G) {
+                const int32_t step = g.G * (int32_t)L();
+                inner = dh() ? ev_rotate_pq(c_, inner, step) : ev_rotate(c_, inner, step);
+            }
             if (first) {
                 acc = std::move(inner);
                 first = false;
@@ -369,6 +388,7 @@ class Runner {
                 acc = ev_addsub(c_, acc, inner, false);
             }
         }
+        if (dh()) acc = ev_moddown_ct(c_, acc);
         DCt z = ev_rescale(c_, acc);
         DCt y = ev_rotsum(c_, z, n_in / h, h * L());
         const DPlain &bp = plain("fc" + std::to_string(layer) + ".bias", y.level, y.scale, [&] {
@@ -600,6 +620,7 @@ void validate_cfg(const std::string &chain, const mmfhe_chain_cfg &cfg)
     if ((chain == "vitals_v2" || chain == "k4_soft_iq") && cfg.iq_pack)
         MMFHE_REQUIRE(cfg.R >= 1 && pow2_or_zero(cfg.R), MMFHE_E_SHAPE, "iq_pack needs R a power of two");
     MMFHE_REQUIRE(pow2_or_zero(cfg.lanes), MMFHE_E_SHAPE, "lanes must be a power of two");
+    MMFHE_REQUIRE(cfg.hoist <= 2, MMFHE_E_INVALID_ARG, "hoist must be 0, 1 or 2");
 }
 
 uint32_t chain_depth(const std::string &chain, const mmfhe_chain_cfg &cfg)

@@ -167,6 +167,7 @@ struct RowEpi {
     const uint64_t *add0, *add1, *add2;  // each may be null
     size_t os, ops, xs, xps, as;
     uint32_t per, g0;
+    uint32_t npoly;  // polynomials per item (0 is read as 2)
 };
 
 inline PrimeMap make_map(const std::vector<uint32_t> &v)

@@ -344,16 +344,19 @@ void Ctx::build_tables()
                 phat[(size_t)k * (L + 1) + i] = host::to_mont(pr, qi);
             }
         }
+        std::vector<TwPair> pmod(L + 1);
         for (uint32_t i = 0; i <= L; ++i) {
             uint64_t qi = primes[i];
             uint64_t P = 1;
             for (uint32_t m = 0; m < K; ++m) P = host::mul(P, primes[L + 1 + m] % qi, qi);
             uint64_t v = host::inv(P, qi);
             pinv[i] = {v, host::shoup(v, qi)};
+            pmod[i] = {P, host::shoup(P, qi)};
         }
         off_pd_hat_inv = blob.push(phinv);
         off_pd_hat = blob.push(phat);
         off_pd_pinv = blob.push(pinv);
+        off_pd_pmod = blob.push(pmod);
     }
     {
         std::vector<TwPair> rs((size_t)(L + 1) * (L + 1), TwPair{0, 0});

@@ -68,13 +68,21 @@ struct DCt {
     uint32_t n_slots = 0;
     uint32_t batch = 1;
     uint32_t n = 0;  // ring dimension
+    // PQ ciphertexts (double-hoisted BSGS): pk = K extra limbs p_0..p_{K-1} per polynomial.
+    // Item layout: [npolys][level+1][N] (the Q part, as a plain ciphertext), then
+    // [npolys][pk][N] (the P part).
+    uint32_t pk = 0;
     double scale = 1.0;
     uint64_t *data() const { return ext ? ext : buf.get(); }
     size_t poly_words() const { return (size_t)(level + 1) * n; }
-    size_t item_words() const { return (size_t)npolys * poly_words(); }
+    size_t item_words() const { return (size_t)npolys * (level + 1 + pk) * n; }
     uint64_t *item(uint32_t b) const { return data() + (size_t)b * item_words(); }
     uint64_t *poly(uint32_t i, uint32_t b = 0) const { return item(b) + (size_t)i * poly_words(); }
-    uint32_t rows() const { return batch * npolys * (level + 1); }
+    uint64_t *ppoly(uint32_t i, uint32_t b = 0) const
+    {
+        return item(b) + (size_t)npolys * poly_words() + (size_t)i * pk * n;
+    }
+    uint32_t rows() const { return batch * npolys * (level + 1 + pk); }
 };
 
 struct DKey {
@@ -82,8 +90,9 @@ struct DKey {
 };
 
 struct DPlain {
-    DBuf buf;  // [level+1][N], NTT form, Montgomery form (x 2^64 mod q)
+    DBuf buf;  // [level+1 (+pk)][N], NTT form, Montgomery form (x 2^64 mod q)
     uint32_t level = 0;
+    uint32_t pk = 0;  // K: also reduced mod p_0..p_{K-1} (rows level+1..), double hoisting
     double scale = 1.0;
 };
 
@@ -127,6 +136,7 @@ class Ctx {
     size_t off_pd_hat_inv = 0;   // TwPair[K]            [Phat_k^{-1}]_{p_k}
     size_t off_pd_hat = 0;       // uint64[K][L+1]       [Phat_k]_{q_i} * 2^64 mod q_i
     size_t off_pd_pinv = 0;      // TwPair[L+1]          [P^{-1}]_{q_i}
+    size_t off_pd_pmod = 0;      // TwPair[L+1]          [P]_{q_i} (double hoisting's P lift)
     size_t off_rs = 0;           // TwPair[L+1][L+1]     [q_l^{-1}]_{q_i} (row l)
     size_t off_rs_h = 0;         // uint64[L+1][L+1]     floor(q_l/2) mod q_i (row l)
     size_t off_recip = 0;        // uint64[np]           floor(2^64 / prime)

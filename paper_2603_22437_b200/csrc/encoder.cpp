@@ -61,19 +61,21 @@ std::vector<int64_t> encode_real(const Ctx &c, const std::vector<double> &v, dou
     return m;
 }
 
-void encode_plain(Ctx &c, const std::string &name, const std::vector<double> &v, uint32_t level, double scale)
+void encode_plain(Ctx &c, const std::string &name, const std::vector<double> &v, uint32_t level, double scale,
+                  bool pq)
 {
     MMFHE_REQUIRE(level <= c.L, MMFHE_E_DEPTH, "plaintext level above the chain");
     std::vector<int64_t> m = encode_real(c, v, scale);
-    std::vector<uint64_t> res((size_t)(level + 1) * c.n);
-    for (uint32_t i = 0; i <= level; ++i) {
-        const int64_t q = (int64_t)c.primes[i];
+    std::vector<uint32_t> basis = pq ? c.ext_basis(level) : c.q_basis(level);
+    std::vector<uint64_t> res(basis.size() * c.n);
+    for (size_t i = 0; i < basis.size(); ++i) {
+        const int64_t q = (int64_t)c.primes[basis[i]];
         for (uint32_t k = 0; k < c.n; ++k) {
             int64_t r = m[k] % q;
-            res[(size_t)i * c.n + k] = (uint64_t)(r < 0 ? r + q : r);
+            res[i * c.n + k] = (uint64_t)(r < 0 ? r + q : r);
         }
     }
-    load_plain(c, name, level, scale, res.data(), false);
+    load_plain(c, name, level, scale, res.data(), false, pq);
     CUDA_CHECK(cudaStreamSynchronize(c.stream));
 }
 

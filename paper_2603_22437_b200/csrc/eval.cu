@@ -227,11 +227,21 @@ void export_batch(Ctx &c, const DCt &in, mmfhe_ct *outs)
 }
 
 // ------------------------------------------------------------------ exact ops
+DCt make_pq(Ctx &c, uint32_t level, uint32_t n_slots, double scale, uint32_t batch);
+PrimeMap pq_item_map(const Ctx &c, uint32_t l);
+
 DCt ev_addsub(Ctx &c, const DCt &a, const DCt &b, bool sub)
 {
-    MMFHE_REQUIRE(a.level == b.level && a.npolys == b.npolys && a.batch == b.batch, MMFHE_E_LAYOUT,
+    MMFHE_REQUIRE(a.level == b.level && a.npolys == b.npolys && a.batch == b.batch && a.pk == b.pk, MMFHE_E_LAYOUT,
                   "hadd level/size mismatch");
     MMFHE_REQUIRE(a.scale == b.scale, MMFHE_E_SCALE, "hadd scale mismatch");
+    if (a.pk) {  // PQ ciphertexts (double hoisting)
+        MMFHE_REQUIRE(!sub && a.npolys == 2, MMFHE_E_LAYOUT, "PQ ciphertexts: 2-poly sums only");
+        rec_n(c, "hadd_pq", a.level, a.batch);
+        DCt r = make_pq(c, a.level, a.n_slots, a.scale, a.batch);
+        launch_addsub(c, r.data(), a.data(), b.data(), a.rows(), pq_item_map(c, a.level), false);
+        return r;
+    }
     rec_n(c, sub ? "hsub" : "hadd", a.level, a.batch);
     DCt r = make_ct(c, a.level, a.npolys, a.n_slots, a.scale, a.batch);
     launch_addsub(c, r.data(), a.data(), b.data(), a.rows(), qmap(c, a.level), sub);
@@ -346,10 +356,12 @@ std::vector<DCt> ev_diag_mac(Ctx &c, const std::vector<const DCt *> &cts,
     MMFHE_REQUIRE(!cts.empty() && !pts.empty(), MMFHE_E_INVALID_ARG, "empty diagonal MAC");
     const DCt &a0 = *cts[0];
     for (auto *x : cts)
-        MMFHE_REQUIRE(x->level == a0.level && x->batch == a0.batch && x->npolys == 2 && x->scale == a0.scale,
-                      MMFHE_E_LAYOUT, "diag MAC operands must share level, batch and scale");
+        MMFHE_REQUIRE(x->level == a0.level && x->batch == a0.batch && x->npolys == 2 && x->scale == a0.scale &&
+                          x->pk == a0.pk,
+                      MMFHE_E_LAYOUT, "diag MAC operands must share level, batch, basis and scale");
     std::vector<DCt> out;
     const bool fused = cts.size() <= (size_t)kDiagMax && pts.size() <= (size_t)kDiagMax;
+    MMFHE_REQUIRE(fused || !a0.pk, MMFHE_E_LAYOUT, "PQ diagonal MAC: at most 16 baby steps and outputs");
     std::vector<const uint64_t *> ctp;
     for (auto *x : cts) ctp.push_back(x->data());
     std::vector<std::vector<const uint64_t *>> ptp;
@@ -364,7 +376,7 @@ std::vector<DCt> ev_diag_mac(Ctx &c, const std::vector<const DCt *> &cts,
             const DPlain *p = row[i];
             rp.push_back(p ? p->buf.get() : nullptr);
             if (!p) continue;
-            MMFHE_REQUIRE(p->level == a0.level, MMFHE_E_LAYOUT, "plaintext level mismatch");
+            MMFHE_REQUIRE(p->level == a0.level && p->pk == a0.pk, MMFHE_E_LAYOUT, "plaintext level / basis mismatch");
             const double s = a0.scale * p->scale;
             MMFHE_REQUIRE(cnt == 0 || s == sc, MMFHE_E_SCALE, "diag MAC scale mismatch");
             sc = s;
@@ -376,12 +388,14 @@ std::vector<DCt> ev_diag_mac(Ctx &c, const std::vector<const DCt *> &cts,
             out.push_back(ev_pmult_sum(c, terms));
             continue;
         }
-        rec_n(c, "pmult_sum", a0.level, a0.batch, std::to_string(cnt));
-        out.push_back(make_ct(c, a0.level, 2, a0.n_slots, sc, a0.batch));
+        rec_n(c, a0.pk ? "pmult_sum_pq" : "pmult_sum", a0.level, a0.batch, std::to_string(cnt));
+        out.push_back(a0.pk ? make_pq(c, a0.level, a0.n_slots, sc, a0.batch)
+                            : make_ct(c, a0.level, 2, a0.n_slots, sc, a0.batch));
         ptp.push_back(rp);
         outp.push_back(out.back().data());
     }
-    if (fused) launch_diag_mac(c, ctp, a0.item_words(), ptp, outp, out[0].item_words(), a0.level, a0.batch);
+    if (fused)
+        launch_diag_mac(c, ctp, a0.item_words(), ptp, outp, out[0].item_words(), a0.level, a0.batch, a0.pk);
     return out;
 }
 
@@ -521,6 +535,53 @@ ModUpOut ks_modup(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t
     return m;
 }
 
+// ModDown of npoly polynomials per item, NTT form in and out:
+//   out = (X - NTT(BConv_{P->Q}(INTT(Pr)))) P^{-1} (+ addends)
+// X: the Q rows (item stride xs, poly stride xps); Pr: the P rows (item stride prs, the
+// item's npoly*K rows contiguous).  The final step (X - w) P^{-1} + addends is the epilogue
+// of w's forward NTT row pass: w never goes to HBM.  Poly 0's addend add0 is read through
+// sigma_g0 (NTT-domain gather; 1 = none); add2 is a second, unpermuted poly-0 addend.
+void moddown(Ctx &c, const uint64_t *X, size_t xs, size_t xps, const uint64_t *Pr, size_t prs, uint32_t l, uint32_t B,
+             uint32_t npoly, uint64_t *out, size_t os, size_t ops, const uint64_t *add0 = nullptr,
+             const uint64_t *add1 = nullptr, size_t as = 0, uint32_t g0 = 1, const uint64_t *add2 = nullptr)
+{
+    const size_t N = c.n;
+    std::vector<uint32_t> pm;
+    for (uint32_t k = 0; k < c.K; ++k) pm.push_back(c.L + 1 + k);
+    DBuf zP((size_t)B * npoly * c.K * N, c.stream);
+    const InvSrc isrc{Pr, prs, N, npoly * c.K, 1};
+    ntt_inverse(c, zP.get(), B * npoly * c.K, make_map(pm), &isrc);
+    RowEpi ep{};
+    ep.out = out;
+    ep.X = X;
+    ep.mul = (const TwPair *)c.bconv_ptr(c.off_pd_pinv);
+    ep.add0 = add0;
+    ep.add1 = add1;
+    ep.add2 = add2;
+    ep.os = os;
+    ep.ops = ops;
+    ep.xs = xs;
+    ep.xps = xps;
+    ep.as = as;
+    ep.per = l + 1;
+    ep.g0 = g0;
+    ep.npoly = npoly;
+    DBuf w((size_t)B * npoly * (l + 1) * N, c.stream);
+    if (c.K == 1 && l + 1 <= (uint32_t)kMapCap) {
+        // one special prime: BConv_{P->Q} is w_i = zP mod q_i, fused into the NTT's first read
+        ColSrc src{};
+        src.x = zP.get();
+        src.xs = N;  // one P row per (item, poly)
+        src.period = l + 1;
+        for (uint32_t i = 0; i <= l; ++i)
+            if (c.primes[c.L + 1] < 2 * c.primes[i]) src.below2q[i >> 5] |= 1u << (i & 31);
+        ntt_forward(c, w.get(), B * npoly * (l + 1), qmap(c, l), &src, &ep);
+    } else {
+        launch_moddown_bconv(c, w.get(), zP.get(), l, B, npoly);
+        ntt_forward(c, w.get(), B * npoly * (l + 1), qmap(c, l), nullptr, &ep);
+    }
+}
+
 // Key inner product (each evk word fetched once per batch split) + ModDown.  The x / y
 // reads of the inner product go through sigma_gx / sigma_gy and poly 0's addend through
 // sigma_g0 (NTT-domain gathers fused into the kernels; 1 = none); add2 is a second,
@@ -534,41 +595,35 @@ void ks_ip_moddown(Ctx &c, const uint64_t *x_ntt, size_t xs, const uint64_t *y, 
     const size_t lw = (size_t)(l + 1) * N;
     DBuf accQ(B * 2 * lw, c.stream), accP(B * 2 * c.K * N, c.stream);
     launch_key_ip(c, accQ.get(), accP.get(), x_ntt, xs, y, m.T * N, m.off, key.buf.get(), l, B, gx, gy);
-    std::vector<uint32_t> pm;
-    for (uint32_t k = 0; k < c.K; ++k) pm.push_back(c.L + 1 + k);
-    ntt_inverse(c, accP.get(), B * 2 * c.K, make_map(pm));
-    // ModDown's final step (accQ - w) P^{-1} + addends is the epilogue of w's forward NTT
-    // row pass: w never goes to HBM
-    RowEpi ep{};
-    ep.out = out;
-    ep.X = accQ.get();
-    ep.mul = (const TwPair *)c.bconv_ptr(c.off_pd_pinv);
-    ep.add0 = add0;
-    ep.add1 = add1;
-    ep.add2 = add2;
-    ep.os = os;
-    ep.ops = lw;
-    ep.xs = 2 * lw;
-    ep.xps = lw;
-    ep.as = as;
-    ep.per = l + 1;
-    ep.g0 = g0;
-    DBuf w(B * 2 * lw, c.stream);
-    if (c.K == 1 && l + 1 <= (uint32_t)kMapCap) {
-        // one special prime: BConv_{P->Q} is w_i = accP mod q_i, fused into the NTT's first read
-        ColSrc src{};
-        src.x = accP.get();
-        src.xs = N;  // one P row per (item, poly)
-        src.period = l + 1;
-        for (uint32_t i = 0; i <= l; ++i)
-            if (c.primes[c.L + 1] < 2 * c.primes[i]) src.below2q[i >> 5] |= 1u << (i & 31);
-        ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l), &src, &ep);
-    } else {
-        launch_moddown_bconv(c, w.get(), accP.get(), l, B);
-        ntt_forward(c, w.get(), B * 2 * (l + 1), qmap(c, l), nullptr, &ep);
-    }
+    moddown(c, accQ.get(), 2 * lw, lw, accP.get(), 2 * c.K * N, l, B, 2, out, os, lw, add0, add1, as, g0, add2);
 }
 }  // namespace
+
+// PQ ciphertext batch (double hoisting): [2][l+1] Q rows then [2][K] P rows per item
+DCt make_pq(Ctx &c, uint32_t level, uint32_t n_slots, double scale, uint32_t batch)
+{
+    DCt r;
+    r.n = c.n;
+    r.level = level;
+    r.npolys = 2;
+    r.pk = c.K;
+    r.n_slots = n_slots;
+    r.scale = scale;
+    r.batch = batch;
+    r.buf = DBuf(r.item_words() * batch, c.stream);
+    return r;
+}
+
+// row -> prime map of one PQ item: Q rows of both polys, then P rows of both polys
+PrimeMap pq_item_map(const Ctx &c, uint32_t l)
+{
+    std::vector<uint32_t> v;
+    for (int p = 0; p < 2; ++p)
+        for (uint32_t i = 0; i <= l; ++i) v.push_back(i);
+    for (int p = 0; p < 2; ++p)
+        for (uint32_t k = 0; k < c.K; ++k) v.push_back(c.L + 1 + k);
+    return make_map(v);
+}
 
 void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t l, uint32_t B, const DKey &key,
                   uint64_t *out, size_t os, const uint64_t *add0, const uint64_t *add1, size_t as)
@@ -735,6 +790,91 @@ DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride)
     return acc;
 }
 
+// ------------------------------------------------------------------ double hoisting
+// (SURVEY §8(c)-5 "a third op"; oracle Evaluator.lift_pq / hoisted_step_pq / rotate_pq /
+// add_pq / moddown_ct, pmult_sum_pq)
+DCt ev_lift_pq(Ctx &c, const DCt &a)
+{
+    MMFHE_REQUIRE(a.npolys == 2 && !a.pk, MMFHE_E_LAYOUT, "lift needs a 2-poly Q ciphertext");
+    rec_n(c, "lift_pq", a.level, a.batch);
+    DCt r = make_pq(c, a.level, a.n_slots, a.scale, a.batch);
+    launch_pq_lift(c, r.data(), r.item_words(), r.poly_words(), a.data(), a.item_words(), a.poly_words(), a.level, 2,
+                   a.batch, 1, false);
+    CUDA_CHECK(cudaMemset2DAsync(r.ppoly(0), r.item_words() * 8, 0, (size_t)2 * c.K * c.n * 8, a.batch, c.stream));
+    return r;
+}
+
+std::vector<DCt> ev_rotate_hoisted_pq(Ctx &c, const DCt &a, const std::vector<int32_t> &steps)
+{
+    MMFHE_REQUIRE(a.npolys == 2 && !a.pk, MMFHE_E_LAYOUT, "rotate needs a 2-poly Q ciphertext");
+    const uint32_t l = a.level, B = a.batch;
+    bool need = false;
+    for (int32_t s : steps) {
+        int32_t k;
+        galois_element(c, s, &k);
+        if (k) {
+            find_gk(c, k);
+            need = true;
+        }
+    }
+    ModUpOut m;
+    if (need) m = ks_modup(c, a.poly(1), a.item_words(), l, B);
+    std::vector<DCt> out;
+    for (int32_t s : steps) {
+        int32_t k;
+        const uint32_t g = (uint32_t)galois_element(c, s, &k);
+        if (k == 0) {
+            out.push_back(ev_lift_pq(c, a));
+            continue;
+        }
+        const DKey &key = find_gk(c, k);
+        rec_n(c, "hrot_hoisted_pq", l, B, std::to_string(k));
+        DCt r = make_pq(c, l, a.n_slots, a.scale, B);
+        const IPOut os{r.item_words(), r.poly_words(), r.item_words(), (size_t)c.K * c.n};
+        launch_key_ip(c, r.data(), r.ppoly(0), a.poly(1), a.item_words(), m.y.get(), m.T * c.n, m.off, key.buf.get(),
+                      l, B, g, g, &os);
+        // (P sigma_g(c0) + IP0, IP1): the P lift of sigma_g(c0) into poly 0's Q rows
+        launch_pq_lift(c, r.data(), r.item_words(), r.poly_words(), a.data(), a.item_words(), a.poly_words(), l, 1, B,
+                       g, true);
+        out.push_back(std::move(r));
+    }
+    return out;
+}
+
+DCt ev_rotate_pq(Ctx &c, const DCt &a, int32_t step)
+{
+    MMFHE_REQUIRE(a.pk == c.K && a.npolys == 2, MMFHE_E_LAYOUT, "PQ rotation needs a PQ ciphertext");
+    int32_t k;
+    const uint32_t g = (uint32_t)galois_element(c, step, &k);
+    const uint32_t l = a.level, B = a.batch;
+    DCt r = make_pq(c, l, a.n_slots, a.scale, B);
+    if (k == 0) {
+        CUDA_CHECK(cudaMemcpyAsync(r.data(), a.data(), a.item_words() * B * 8, cudaMemcpyDeviceToDevice, c.stream));
+        return r;
+    }
+    const DKey &key = find_gk(c, k);
+    rec_n(c, "hrot_pq", l, B, std::to_string(k));
+    // a1' = ModDown(a1) to Q_l (NTT form), then the rotation's key switch without ModDown
+    const size_t lw = (size_t)(l + 1) * c.n;
+    DBuf a1(lw * B, c.stream);
+    moddown(c, a.poly(1), a.item_words(), 0, a.ppoly(1), a.item_words(), l, B, 1, a1.get(), lw, 0);
+    ModUpOut m = ks_modup(c, a1.get(), lw, l, B, g);
+    const IPOut os{r.item_words(), r.poly_words(), r.item_words(), (size_t)c.K * c.n};
+    launch_key_ip(c, r.data(), r.ppoly(0), a1.get(), lw, m.y.get(), m.T * c.n, m.off, key.buf.get(), l, B, g, 1, &os);
+    launch_pq_add_perm(c, r.data(), a.data(), a.item_words(), l, B, g);
+    return r;
+}
+
+DCt ev_moddown_ct(Ctx &c, const DCt &a)
+{
+    MMFHE_REQUIRE(a.pk == c.K && a.npolys == 2, MMFHE_E_LAYOUT, "ModDown needs a PQ ciphertext");
+    rec_n(c, "moddown", a.level, a.batch);
+    DCt r = make_ct(c, a.level, 2, a.n_slots, a.scale, a.batch);
+    moddown(c, a.data(), a.item_words(), a.poly_words(), a.ppoly(0), a.item_words(), a.level, a.batch, 2, r.data(),
+            r.item_words(), r.poly_words());
+    return r;
+}
+
 // ------------------------------------------------------------------ stores
 void load_key(Ctx &c, DKey &k, const uint64_t *words, size_t n_words, bool on_device)
 {
@@ -751,20 +891,23 @@ void load_key(Ctx &c, DKey &k, const uint64_t *words, size_t n_words, bool on_de
     launch_to_mont(c, k.buf.get(), rows, pm);
 }
 
-void load_plain(Ctx &c, const std::string &name, uint32_t level, double scale, const uint64_t *coef, bool on_device)
+void load_plain(Ctx &c, const std::string &name, uint32_t level, double scale, const uint64_t *coef, bool on_device,
+                bool pq)
 {
     MMFHE_REQUIRE(level <= c.L, MMFHE_E_DEPTH, "plaintext level above the chain");
     auto p = std::make_unique<DPlain>();
     p->level = level;
+    p->pk = pq ? c.K : 0;
     p->scale = scale;
-    const size_t words = (size_t)(level + 1) * c.n;
+    const uint32_t rows = level + 1 + p->pk;
+    const size_t words = (size_t)rows * c.n;
     p->buf = DBuf(words, c.stream);
     CUDA_CHECK(cudaMemcpyAsync(p->buf.get(), coef, words * 8,
                                on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c.stream));
-    PrimeMap pm = qmap(c, level);
-    ntt_forward(c, p->buf.get(), level + 1, pm);
-    launch_to_mont(c, p->buf.get(), level + 1, pm);
-    c.plains[plain_key(name, level)] = std::move(p);
+    PrimeMap pm = pq ? make_map(c.ext_basis(level)) : qmap(c, level);
+    ntt_forward(c, p->buf.get(), rows, pm);
+    launch_to_mont(c, p->buf.get(), rows, pm);
+    c.plains[plain_key(pq ? name + ".pq" : name, level)] = std::move(p);
 }
 
 const DPlain &need_plain(const Ctx &c, const std::string &name, uint32_t level)

@@ -62,6 +62,12 @@ DCt ev_rot_add(Ctx &c, const DCt &a, int32_t step);
 DCt ev_rot_add(Ctx &c, const DCt &a, const DCt &b, int32_t step);
 DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride);
 
+// double-hoisted BSGS (SURVEY §8(c)-5 third op): ciphertexts over Q_l u P (DCt::pk = K)
+DCt ev_lift_pq(Ctx &c, const DCt &a);                                                    // (P c0, P c1)
+std::vector<DCt> ev_rotate_hoisted_pq(Ctx &c, const DCt &a, const std::vector<int32_t> &steps);  // no ModDown
+DCt ev_rotate_pq(Ctx &c, const DCt &a, int32_t step);  // ModDown(a1), sigma_g, key switch kept over Q_l u P
+DCt ev_moddown_ct(Ctx &c, const DCt &a);               // both polys back to Q_l
+
 // composites
 inline DCt ev_relin_rescale(Ctx &c, const DCt &a3) { return ev_rescale(c, ev_relin(c, a3)); }
 inline DCt ev_square_rescale(Ctx &c, const DCt &a) { return ev_relin_rescale(c, ev_tensor_sum(c, {{&a, &a}})); }
@@ -72,11 +78,13 @@ const DPlain &need_plain(const Ctx &c, const std::string &name, uint32_t level);
 
 // key / plaintext stores
 void load_key(Ctx &c, DKey &k, const uint64_t *words, size_t n_words, bool on_device);
+// pq: coef holds [level+1+K][N] (q_0..q_level then p_0..p_{K-1}); stored as "name.pq@level"
 void load_plain(Ctx &c, const std::string &name, uint32_t level, double scale, const uint64_t *coef,
-                bool on_device);
+                bool on_device, bool pq = false);
 // host encoder (canonical embedding), csrc/encoder.cpp
 std::vector<int64_t> encode_real(const Ctx &c, const std::vector<double> &v, double scale);
-void encode_plain(Ctx &c, const std::string &name, const std::vector<double> &v, uint32_t level, double scale);
+void encode_plain(Ctx &c, const std::string &name, const std::vector<double> &v, uint32_t level, double scale,
+                  bool pq = false);
 // exact round-half-away(v * q_scale) reduced mod m
 uint64_t encode_scalar_mod(double v, uint64_t q_scale, uint64_t m);
 

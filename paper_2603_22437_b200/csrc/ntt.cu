@@ -444,8 +444,9 @@ __global__ void __launch_bounds__(kCtaThreads, kMinCtas) ntt_fwd_pass(uint64_t *
             // fused epilogue (RowEpi): (X - v) mul + addends, written to ep.out
             constexpr int LOL = FwdGeo<Gm, LOGS>::lo(R - 1), WL = FwdGeo<Gm, LOGS>::w(R - 1);
             const float qinv = qinv_est(q);
-            const size_t b = row / (2 * ep.per);
-            const uint32_t rr = (uint32_t)(row % (2 * ep.per)), poly = rr / ep.per, i = rr % ep.per;
+            const uint32_t np = ep.npoly ? ep.npoly : 2;
+            const size_t b = row / (np * ep.per);
+            const uint32_t rr = (uint32_t)(row % (np * ep.per)), poly = rr / ep.per, i = rr % ep.per;
             const uint32_t k0 = ((uint32_t)gi << LOGS) | (uint32_t)ktr;  // this thread's first word
             uint64_t x[E];
             ld_pattern<ELOG, LOL, WL>(ep.X + b * ep.xs + poly * ep.xps + ((size_t)i << LOGN), k0, x);

@@ -30,11 +30,22 @@ void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, 
                         const std::vector<size_t> &off, uint32_t B);
 // accQ [B][2][l+1][N], accP [B][2][K][N] = sum_j y_j (.) evk_j; each key word is loaded once for all B.
 // gx / gy: the x (digit-own rows) / y reads go through sigma_g (NTT-domain gather; 1 = none).
+// os: output item / poly strides of the Q and P rows (nullptr: compact accQ / accP as above).
+struct IPOut {
+    size_t qs, qp, ps, pp;
+};
 void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, size_t xs, const uint64_t *y,
                    size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B,
-                   uint32_t gx = 1, uint32_t gy = 1);
-// w [B][2][l+1][N] = BConv_{P->Q}(zP [B][2][K][N]) (coefficient form).
-void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B);
+                   uint32_t gx = 1, uint32_t gy = 1, const IPOut *os = nullptr);
+// w [B*npoly][l+1][N] = BConv_{P->Q}(zP [B*npoly][K][N]) (coefficient form).
+void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B, uint32_t npoly = 2);
+// double hoisting: Q rows of out (+)= [P]_{q_i} sigma_g(src) for npoly polys per
+// item (out / src item strides os / ss, poly strides ops / sps); and poly 0 of a PQ ciphertext
+// out (+)= sigma_g(poly 0 of src) over Q_l u P (item stride is, PQ item layout).
+void launch_pq_lift(Ctx &c, uint64_t *out, size_t os, size_t ops, const uint64_t *src, size_t ss, size_t sps,
+                    uint32_t level, uint32_t npoly, uint32_t B, uint32_t g, bool accumulate);
+void launch_pq_add_perm(Ctx &c, uint64_t *out, const uint64_t *src, size_t is, uint32_t level, uint32_t B,
+                        uint32_t g);
 // (ModDown's final step (accQ - w) P^{-1} + addends and the rescale's (a_i - v_i) q_l^{-1}
 // run as the epilogue of the forward NTT's row pass: ntt_forward(..., RowEpi).)
 
@@ -47,9 +58,10 @@ void launch_pmult_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &pt, const
                       uint32_t level, bool accumulate, uint32_t B);
 // Fused BSGS inner sums (CK9): out_o (+0) = sum_c pts[o][c] (.) cts[c] for a batch of B
 // (cts item stride is, outs item stride os); pts[o][c] may be null; <= kDiagMax each.
+// pk = K: the operands are PQ ciphertexts / plaintexts (rows over Q_l u P, double hoisting).
 void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is,
                      const std::vector<std::vector<const uint64_t *>> &pts, const std::vector<uint64_t *> &outs,
-                     size_t os, uint32_t level, uint32_t B);
+                     size_t os, uint32_t level, uint32_t B, uint32_t pk = 0);
 // Scalar "modular matrix product" over a batch of 2-poly cts (CK10):
 //   out[j] = sum_{w < W} C[j][w] in[lo_j + w],  j < J,  lo_j = lo0 + j*lo_step,
 // C given as (value, Montgomery form) pairs [J][W][l+1]; inputs outside [0, M) contribute nothing.

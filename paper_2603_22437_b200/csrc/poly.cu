@@ -141,6 +141,7 @@ struct IPArgs {
     size_t y_off[16];
     uint32_t lo[16], hi[16];
     size_t xs, ys;
+    size_t oqs, oqp, ops, opp;  // output item / poly strides of the Q rows (accQ) and P rows (accP)
     uint32_t dnum, level, L, K, B, per_z;
     uint32_t gx, gy;  // sigma_g applied on the fly to the x / y reads (1 = none)
 };
@@ -190,10 +191,9 @@ __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ acc
         }
     }
     const bool isq = r <= a.level;
-    const size_t qs = (size_t)2 * (a.level + 1) * kt.n, ps = (size_t)2 * a.K * kt.n;
     uint64_t *o = isq ? accQ + (size_t)r * kt.n + k : accP + (size_t)(r - a.level - 1) * kt.n + k;
-    const size_t ostride = isq ? qs : ps;
-    const size_t opoly = isq ? (size_t)(a.level + 1) * kt.n : (size_t)a.K * kt.n;
+    const size_t ostride = isq ? a.oqs : a.ops;
+    const size_t opoly = isq ? a.oqp : a.opp;
     for (uint32_t b = b0; b < b1; ++b) {
         const uint64_t *xb = x + (size_t)b * a.xs, *yb = y + (size_t)b * a.ys;
         uint64_t s[DMAX];
@@ -248,10 +248,9 @@ __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uin
         }
     }
     const bool isq = r <= a.level;
-    const size_t qs = (size_t)2 * (a.level + 1) * kt.n, ps = (size_t)2 * a.K * kt.n;
     uint64_t *o = isq ? accQ + (size_t)r * kt.n + k : accP + (size_t)(r - a.level - 1) * kt.n + k;
-    const size_t ostride = isq ? qs : ps;
-    const size_t opoly = isq ? (size_t)(a.level + 1) * kt.n : (size_t)a.K * kt.n;
+    const size_t ostride = isq ? a.oqs : a.ops;
+    const size_t opoly = isq ? a.oqp : a.opp;
     for (uint32_t b = b0; b < b1; ++b) {
         uint64_t s[DMAX];
 #pragma unroll
@@ -464,51 +463,61 @@ __global__ void __launch_bounds__(kTB) k_pmult_sum(uint64_t *__restrict__ out_ba
     out[ps + off] = s1;
 }
 
-// BSGS inner sums of all giant steps in one pass:
-//   out_o = sum_c pt[o][c] (.) ct_c   (pt[o][c] == nullptr: no term),
-// every thread loads its coefficient of the NC baby-step ciphertexts once and
-// produces all NO outputs; plaintext words are shared by the batch (grid.z).
+// BSGS inner sums of all giant steps in one pass, plaintext-stationary:
+//   out_o = sum_c pt[o][c] (.) ct_c   (pt[o][c] == nullptr: no term)
+// for every item of a batch.  A CTA owns kDmTK = 32 coefficients of one residue row: it stages
+// that tile's word of every (o, c) plaintext in shared memory once (the plaintexts are read
+// from HBM once per launch, not once per item), then its warps walk the batch items: each
+// lane loads its coefficient of the nc baby steps into registers and produces all no outputs
+// (nc 64x64->128 MACs from shared memory + one Montgomery reduction each).  Rows of PQ
+// operands (double hoisting: pk = K extra limbs) map to the special primes.
+constexpr int kDmTK = 32;
 struct DiagMacArgs {
     const uint64_t *ct[kDiagMax];
     const uint64_t *pt[kDiagMax][kDiagMax];
     uint64_t *out[kDiagMax];
     size_t is, os;
     int nc, no;
-    uint32_t level;
+    uint32_t level, L, pk, B;
 };
 
-// grid.x = tile * B + item: the B CTAs that share a tile's plaintext words run together,
-// so each diagonal word is fetched from HBM once and served to the batch from L2.
-// grid.y = poly * (l+1) + limb (one polynomial per thread keeps ~60 registers); the
-// next output's diagonal words are prefetched while the current one accumulates.
 template <int NCMAX>
-__global__ void __launch_bounds__(kTB) k_diag_mac(DiagMacArgs a, KTables kt, uint32_t B)
+__global__ void __launch_bounds__(256) k_diag_mac(DiagMacArgs a, KTables kt)
 {
-    const uint32_t item = blockIdx.x % B, tile = blockIdx.x / B;
-    const uint32_t k = tile * blockDim.x + threadIdx.x;
-    if (k >= kt.n) return;
+    extern __shared__ uint64_t spt[];  // [no][nc][kDmTK]
     const uint32_t L1 = a.level + 1;
-    const uint32_t poly = blockIdx.y / L1, r = blockIdx.y - poly * L1;
-    const size_t off = (size_t)r * kt.n + k;
-    const size_t poff = (size_t)poly * L1 * kt.n + off;
-    const size_t boff = (size_t)item * a.is + poff;
-    const uint64_t q = kt.q[r], qi = kt.qinv_neg[r];
-    uint64_t x[NCMAX], w[NCMAX];
+    const uint32_t ry = blockIdx.y;  // row inside an item: [2][L1] Q rows, then [2][pk] P rows
+    uint32_t prow, prime;
+    if (ry < 2 * L1) {
+        prow = ry % L1;
+        prime = prow;
+    } else {
+        const uint32_t kk = (ry - 2 * L1) % a.pk;
+        prow = L1 + kk;
+        prime = a.L + 1 + kk;
+    }
+    const uint32_t k0 = blockIdx.x * kDmTK;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nt = a.no * a.nc;
+    for (int t = warp; t < nt; t += nw) {
+        const uint64_t *p = a.pt[t / a.nc][t % a.nc];
+        spt[t * kDmTK + lane] = p ? __ldg(p + (size_t)prow * kt.n + k0 + lane) : 0;
+    }
+    __syncthreads();
+    const uint64_t q = kt.q[prime], qi = kt.qinv_neg[prime];
+    const size_t off = (size_t)ry * kt.n + k0 + lane;
+    for (uint32_t b = warp; b < a.B; b += nw) {
+        uint64_t x[NCMAX];
 #pragma unroll
-    for (int c = 0; c < NCMAX; ++c) x[c] = c < a.nc ? a.ct[c][boff] : 0;
+        for (int c = 0; c < NCMAX; ++c) x[c] = c < a.nc ? a.ct[c][(size_t)b * a.is + off] : 0;
+        const uint64_t *w = spt + lane;
+        for (int o = 0; o < a.no; ++o, w += a.nc * kDmTK) {
+            U128 acc{0, 0};  // <= 16 terms < q^2 each: < q 2^64 for q < 2^60; absent terms are 0
 #pragma unroll
-    for (int c = 0; c < NCMAX; ++c) w[c] = (c < a.nc && a.pt[0][c]) ? __ldg(a.pt[0][c] + off) : 0;
-    for (int o = 0; o < a.no; ++o) {
-        uint64_t wn[NCMAX];
-        const bool more = o + 1 < a.no;
-#pragma unroll
-        for (int c = 0; c < NCMAX; ++c) wn[c] = (more && c < a.nc && a.pt[o + 1][c]) ? __ldg(a.pt[o + 1][c] + off) : 0;
-        U128 acc{0, 0};  // <= 16 terms < q*2^60 each: < q*2^64 for q < 2^60; absent terms are 0
-#pragma unroll
-        for (int c = 0; c < NCMAX; ++c) mac128(acc, x[c], w[c]);
-        a.out[o][(size_t)item * a.os + poff] = redc(acc, q, qi);
-#pragma unroll
-        for (int c = 0; c < NCMAX; ++c) w[c] = wn[c];
+            for (int c = 0; c < NCMAX; ++c)
+                if (c < a.nc) mac128(acc, x[c], w[c * kDmTK]);
+            a.out[o][(size_t)b * a.os + off] = redc(acc, q, qi);
+        }
     }
 }
 
@@ -710,6 +719,37 @@ __global__ void k_add_plain(uint64_t *__restrict__ c0, size_t s, const uint64_t 
     c[off] = add_mod(c[off], v, q);
 }
 
+// Double hoisting's P lift: Q rows of out (+)= [P]_{q_i} (.) src, read
+// through sigma_g (NTT-domain gather; g = 1: none); rows = npoly (l+1), row r = poly (l+1) + i.
+__global__ void k_pq_lift(uint64_t *__restrict__ out, size_t os, size_t ops, const uint64_t *__restrict__ src,
+                          size_t ss, size_t sps, const TwPair *__restrict__ pmod, KTables kt, uint32_t l1, uint32_t g,
+                          int accumulate)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t poly = blockIdx.y / l1, i = blockIdx.y % l1;
+    const uint64_t q = kt.q[i];
+    const TwPair m = pmod[i];
+    const uint64_t v = shoup(src[blockIdx.z * ss + poly * sps + (size_t)i * kt.n + galois_perm(k, g, kt.log_n)], m.w,
+                             m.wp, q);
+    uint64_t *o = out + blockIdx.z * os + poly * ops + (size_t)i * kt.n + k;
+    *o = accumulate ? add_mod(*o, v, q) : v;
+}
+
+// PQ giant step's addend: poly 0 of out (+)= sigma_g(poly 0 of src) over Q_l u P, both PQ
+// ciphertexts ([2][l+1] Q rows then [2][K] P rows per item).
+__global__ void k_pq_add_perm(uint64_t *__restrict__ out, const uint64_t *__restrict__ src, size_t is, KTables kt,
+                              uint32_t l1, uint32_t L, uint32_t g)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t r = blockIdx.y;  // 0..l: q_r (Q part, poly 0), l+1..: p_{r-l-1} (P part, poly 0)
+    const size_t off = r < l1 ? (size_t)r * kt.n : (size_t)(2 * l1 + (r - l1)) * kt.n;
+    const uint64_t q = kt.q[r < l1 ? r : L + 1 + (r - l1)];
+    const size_t b = (size_t)blockIdx.z * is;
+    out[b + off + k] = add_mod(out[b + off + k], src[b + off + galois_perm(k, g, kt.log_n)], q);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -777,10 +817,21 @@ void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, 
 
 void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, size_t xs, const uint64_t *y,
                    size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B,
-                   uint32_t gx, uint32_t gy)
+                   uint32_t gx, uint32_t gy, const IPOut *os)
 {
     const auto &plans = c.modup[level];
     IPArgs a{};
+    if (os) {
+        a.oqs = os->qs;
+        a.oqp = os->qp;
+        a.ops = os->ps;
+        a.opp = os->pp;
+    } else {  // compact accQ [B][2][l+1][N], accP [B][2][K][N]
+        a.oqp = (size_t)(level + 1) * c.n;
+        a.oqs = 2 * a.oqp;
+        a.opp = (size_t)c.K * c.n;
+        a.ops = 2 * a.opp;
+    }
     a.dnum = (uint32_t)plans.size();
     a.level = level;
     a.L = c.L;
@@ -825,12 +876,13 @@ static MDArgs md_args(Ctx &c, uint32_t level)
     return a;
 }
 
-void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B)
+void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B, uint32_t npoly)
 {
     MMFHE_REQUIRE(c.K <= 16, MMFHE_E_PARAMS, "K too large");
-    ProfScope ps(c, "moddown_bconv", 16.0 * (c.K + level + 1) * c.n * B, 2.0 * c.K * (level + 1) * c.n * B);
+    ProfScope ps(c, "moddown_bconv", 8.0 * npoly * (c.K + level + 1) * c.n * B,
+                 (double)npoly * c.K * (level + 1) * c.n * B);
     const size_t smem = 8 * ((size_t)c.K * (level + 1) + 2 * (level + 1));
-    const dim3 g((c.n + kBcK * kTB - 1) / (kBcK * kTB), 2 * B);
+    const dim3 g((c.n + kBcK * kTB - 1) / (kBcK * kTB), npoly * B);
     if (c.K <= 1)
         k_moddown_bconv<1><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, md_args(c, level));
     else if (c.K <= 4)
@@ -870,16 +922,20 @@ void launch_pmult_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &pt, const
 
 void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is,
                      const std::vector<std::vector<const uint64_t *>> &pts, const std::vector<uint64_t *> &outs,
-                     size_t os, uint32_t level, uint32_t B)
+                     size_t os, uint32_t level, uint32_t B, uint32_t pk)
 {
     MMFHE_REQUIRE(cts.size() <= (size_t)kDiagMax && outs.size() <= (size_t)kDiagMax && pts.size() == outs.size(),
                   MMFHE_E_LAYOUT, "diag_mac shape");
+    MMFHE_REQUIRE(c.n % kDmTK == 0, MMFHE_E_PARAMS, "N must be a multiple of 32");
     DiagMacArgs a{};
     a.nc = (int)cts.size();
     a.no = (int)outs.size();
     a.is = is;
     a.os = os;
     a.level = level;
+    a.L = c.L;
+    a.pk = pk;
+    a.B = B;
     double terms = 0;
     for (size_t i = 0; i < cts.size(); ++i) a.ct[i] = cts[i];
     for (size_t o = 0; o < outs.size(); ++o) {
@@ -889,16 +945,25 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
             terms += pts[o][i] != nullptr;
         }
     }
-    // algorithmic: babies read once, plaintexts once per batch, outputs written once
-    ProfScope ps(c, "diag_mac", 8.0 * (level + 1) * c.n * (terms + B * 2.0 * (a.nc + a.no)),
-                 2.0 * terms * (level + 1) * c.n * B);
-    const dim3 g(((c.n + kTB - 1) / kTB) * B, 2 * (level + 1));
+    const double rows = level + 1 + pk;
+    // algorithmic: babies read once, plaintexts once per launch, outputs written once
+    ProfScope ps(c, "diag_mac", 8.0 * rows * c.n * (terms + B * 2.0 * (a.nc + a.no)), 2.0 * terms * rows * c.n * B);
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, [] {
+        const int mx = (int)(sizeof(uint64_t) * kDiagMax * kDiagMax * kDmTK);
+        CUDA_CHECK(cudaFuncSetAttribute(k_diag_mac<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        CUDA_CHECK(cudaFuncSetAttribute(k_diag_mac<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        CUDA_CHECK(cudaFuncSetAttribute(k_diag_mac<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    });
+    const size_t smem = sizeof(uint64_t) * (size_t)a.no * a.nc * kDmTK;
+    const int threads = 32 * (int)std::min<uint32_t>(8, std::max<uint32_t>(4, B));
+    const dim3 g(c.n / kDmTK, 2 * (level + 1 + pk));
     if (a.nc <= 4)
-        k_diag_mac<4><<<g, kTB, 0, c.stream>>>(a, c.kt, B);
+        k_diag_mac<4><<<g, threads, smem, c.stream>>>(a, c.kt);
     else if (a.nc <= 8)
-        k_diag_mac<8><<<g, kTB, 0, c.stream>>>(a, c.kt, B);
+        k_diag_mac<8><<<g, threads, smem, c.stream>>>(a, c.kt);
     else
-        k_diag_mac<16><<<g, kTB, 0, c.stream>>>(a, c.kt, B);
+        k_diag_mac<16><<<g, threads, smem, c.stream>>>(a, c.kt);
     LAUNCH_CHECK(c);
 }
 
@@ -964,6 +1029,22 @@ void launch_scatter(Ctx &c, const PtrList &dst, const uint64_t *in, int n, size_
     ProfScope ps(c, "scatter", 16.0 * words * n);
     const size_t threads = (words + 1) / 2;
     k_scatter<<<dim3((unsigned)((threads + kTB - 1) / kTB), n), kTB, 0, c.stream>>>(dst, in, words);
+    LAUNCH_CHECK(c);
+}
+
+void launch_pq_lift(Ctx &c, uint64_t *out, size_t os, size_t ops, const uint64_t *src, size_t ss, size_t sps,
+                    uint32_t level, uint32_t npoly, uint32_t B, uint32_t g, bool accumulate)
+{
+    ProfScope ps(c, "pq_lift", 8.0 * npoly * (level + 1) * c.n * B * (accumulate ? 3.0 : 2.0));
+    k_pq_lift<<<grid3(c.n, npoly * (level + 1), B), kTB, 0, c.stream>>>(
+        out, os, ops, src, ss, sps, (const TwPair *)c.bconv_ptr(c.off_pd_pmod), c.kt, level + 1, g, accumulate ? 1 : 0);
+    LAUNCH_CHECK(c);
+}
+
+void launch_pq_add_perm(Ctx &c, uint64_t *out, const uint64_t *src, size_t is, uint32_t level, uint32_t B, uint32_t g)
+{
+    ProfScope ps(c, "pq_add_perm", 24.0 * (level + 1 + c.K) * c.n * B);
+    k_pq_add_perm<<<grid3(c.n, level + 1 + c.K, B), kTB, 0, c.stream>>>(out, src, is, c.kt, level + 1, c.L, g);
     LAUNCH_CHECK(c);
 }
 

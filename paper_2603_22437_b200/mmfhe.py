@@ -100,6 +100,7 @@ def lib():
             "mmfhe_load_relin_key": [V, V, S, ctypes.c_int],
             "mmfhe_load_galois_key": [V, I32, V, S, ctypes.c_int],
             "mmfhe_load_plain": [V, ctypes.c_char_p, CTP],
+            "mmfhe_load_plain_pq": [V, ctypes.c_char_p, CTP],
             "mmfhe_encode_plain": [V, ctypes.c_char_p, P(ctypes.c_double), S, U32, ctypes.c_double],
             "mmfhe_prepare_chain": [V, ctypes.c_char_p, P(ChainCfg), U32, V, V, V],
             "mmfhe_load_scalars": [V, ctypes.c_char_p, P(ctypes.c_double), S],
@@ -156,7 +157,7 @@ EXPORTED = [
     "mmfhe_hmult_batch", "mmfhe_trace_get", "mmfhe_trace_clear", "mmfhe_trace_enable", "mmfhe_profile_enable",
     "mmfhe_profile_get", "mmfhe_microbench", "mmfhe_graph_enable", "mmfhe_graph_stats", "mmfhe_eval_chain_async",
     "mmfhe_ctx_sync", "mmfhe_params_digest", "mmfhe_serialize_ct", "mmfhe_deserialize_ct", "mmfhe_serialize_key",
-    "mmfhe_load_key_serialized",
+    "mmfhe_load_key_serialized", "mmfhe_load_plain_pq",
 ]
 
 SER_CT, SER_RELIN_KEY, SER_GALOIS_KEY = 0, 1, 2
@@ -255,9 +256,14 @@ class Context:
         self._check(self._lib.mmfhe_load_galois_key(self.h, int(step), addr, _numel(words), dev))
 
     def load_plain(self, name, residues, level, scale):
+        """Import a coefficient-form plaintext; a name ending in ".pq" is over Q_level u P
+        (residues [level+1+K][N], mmfhe_load_plain_pq; stored under that name)."""
         ct = Ct(residues, level, scale, 0, self.log_n, FORM_COEFF, 1)
         s = ct.struct()
-        self._check(self._lib.mmfhe_load_plain(self.h, name.encode(), ctypes.byref(s)))
+        if name.endswith(".pq"):
+            self._check(self._lib.mmfhe_load_plain_pq(self.h, name[:-3].encode(), ctypes.byref(s)))
+        else:
+            self._check(self._lib.mmfhe_load_plain(self.h, name.encode(), ctypes.byref(s)))
 
     def encode_plain(self, name, values, level, scale):
         v = np.ascontiguousarray(values, dtype=np.float64)

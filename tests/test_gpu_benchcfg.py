@@ -7,9 +7,10 @@ variants, on fewer frames than a full session so the oracle finishes.
   (k_lincomb_sym), packed I/Q rotate-and-sum over 4 frames with the hoisted unpack
   (iq_pack = 3, hoist = 1, DESIGN R19) -- 16 of the session's 256 frames.
 * C4 (PS4: N=2^16, 20 Q + 7 P limbs, alpha 7, dnum 3, entry level 19): the gesture
-  chain (K3 hoisted BSGS -> K1 -> K6 -> K2b per frame, frame sum, FC 4096->64->32->8
-  hoisted), both in the paper's one-frame-per-ciphertext layout and SIMD-dense with
-  8 frames per ciphertext (cfg.lanes, DESIGN R20).
+  chain (K3 BSGS -> K1 -> K6 -> K2b per frame, frame sum, FC 4096->64->32->8), in the
+  paper's one-frame-per-ciphertext layout with hoisted BSGS and as the bench times it:
+  SIMD-dense with 8 frames per ciphertext (cfg.lanes, DESIGN R20) and double-hoisted BSGS
+  (cfg.hoist = 2, DESIGN R22).
 * The library's own encoder: against the oracle's encoding,
   |coefficient difference| <= 1 and decode error <= 2^-30, at N = 2^14 and 2^16.
 
@@ -130,11 +131,11 @@ def test_c2_bench_params_residue_parity(m):
 
 # ------------------------------------------------------------------ C4 (bench configs[3])
 
-def _c4_case(lanes, F, seed):
+def _c4_case(lanes, F, seed, hoist=1):
     P = ps4()
     A, R, D = 4, 32, 32
     cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25,
-                      hoist=1, lanes=lanes)
+                      hoist=hoist, lanes=lanes)
     Z, _ = radar.gesture_scene(A, R, D, F, seed=seed, cls=seed % 5)
     Zt = radar.preprocess_gesture(Z)
     keys = orc.keygen(P, seed=seed + 1, rotations=cc.required_rotations("gesture", cfg, P.n))
@@ -149,12 +150,12 @@ def _c4_case(lanes, F, seed):
     return P, cfg, keys, cts, np.sum(feats, axis=0)
 
 
-@pytest.mark.parametrize("lanes,F", [(1, 2), (8, 16)])
-def test_c4_bench_params_residue_parity(m, lanes, F):
-    """PS4 gesture at entry level 19 with hoisted BSGS and the FC head (bench C4), bit-exact:
-    canonical (one frame per ciphertext, 2 frames) and SIMD-dense (8 frames per ciphertext,
-    2 packed ciphertext pairs = 16 frames, the bench's headline packing)."""
-    P, cfg, keys, cts, xp = _c4_case(lanes, F, 6100 + lanes)
+@pytest.mark.parametrize("lanes,F,hoist", [(1, 2, 1), (8, 16, 2)])
+def test_c4_bench_params_residue_parity(m, lanes, F, hoist):
+    """PS4 gesture at entry level 19 with the FC head (bench C4), bit-exact: canonical (one
+    frame per ciphertext, 2 frames, hoisted BSGS) and the bench's headline (8 frames per
+    ciphertext, 2 packed ciphertext pairs = 16 frames, double-hoisted BSGS)."""
+    P, cfg, keys, cts, xp = _c4_case(lanes, F, 6100 + lanes, hoist)
     Ws, bs = radar.fc_weights([4096, 64, 32, 5], seed=6200)
     gain = min(0.8 / max(np.max(np.abs(Ws[0] @ xp)), 1e-30), 2000.0 / np.max(np.abs(Ws[0])))
     Ws[0] = Ws[0] * gain
@@ -164,7 +165,7 @@ def test_c4_bench_params_residue_parity(m, lanes, F):
     logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
     ctx = make_ctx(m, P, keys, book)
     mcfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25,
-                       hoist=1, lanes=lanes)
+                       hoist=hoist, lanes=lanes)
     assert sorted(ctx.required_rotations("gesture", mcfg)) == cc.required_rotations("gesture", cfg, P.n)
     levels = ctx.chain_plan("gesture", mcfg, 19, len(cts))
     assert levels == [logits.level] == [19 - 11]

@@ -281,13 +281,16 @@ def test_gesture_chain_small(m, F, fb, hoist):
     _run(m, P, keys, book, "gesture_frame", cfg, cts[:2], [f0])
 
 
-@pytest.mark.parametrize("lanes,F,fb", [(4, 6, 0), (2, 5, 2), (8, 8, 0)])
-def test_gesture_chain_lanes_small(m, lanes, F, fb):
+@pytest.mark.parametrize("lanes,F,fb,hoist", [(4, 6, 0, 1), (2, 5, 2, 1), (8, 8, 0, 1), (4, 6, 0, 2), (2, 5, 2, 2),
+                                              (1, 3, 2, 2)])
+def test_gesture_chain_lanes_small(m, lanes, F, fb, hoist):
     """SIMD-dense gesture pipeline (DESIGN R20): `lanes` frames interleaved per ciphertext,
-    ceil(F / lanes) ciphertext pairs (the last one partly empty), hoisted BSGS, FC head with
-    the lane sum: residues and trace equal the oracle's; the per-frame chain and K3 alone too."""
+    ceil(F / lanes) ciphertext pairs (the last one partly empty), hoisted (hoist = 1) or
+    double-hoisted (hoist = 2: PQ baby steps, PQ diagonals, PQ giant steps, one ModDown per
+    output) BSGS in K3 and the FC head with the lane sum: residues and trace equal the
+    oracle's; K3 alone too."""
     P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
-    cfg, Zt = _gesture(P, 3221, F=F, frame_batch=fb, hoist=1)
+    cfg, Zt = _gesture(P, 3221, F=F, frame_batch=fb, hoist=hoist)
     cfg.lanes = lanes
     keys = orc.keygen(P, seed=3222, rotations=cc.required_rotations("gesture", cfg, P.n))
     n = cfg.n_slots

@@ -435,3 +435,80 @@ def test_gesture_lanes_decrypt_like_canonical(Pg):
     want = dsp.mlp_forward(xp, Ws, bs)
     assert rel_err(got, want) < 1e-3
     assert int(np.argmax(got)) == int(np.argmax(want))
+
+
+# ------------------------------------------------------------------ double-hoisted BSGS (hoist = 2)
+
+def test_pq_lift_moddown_is_exact_and_rotate_pq_rotates():
+    """Double hoisting's PQ ops (SURVEY §8(c)-5 third op): ModDown(P c) = c exactly (the
+    P rows of a lifted ciphertext are zero, so the base conversion adds nothing), and a PQ
+    giant rotation followed by the final ModDown decrypts to the slot rotation."""
+    P = toy(log_n=10, n_q=4, scale_bits=40, n_p=2, alpha=2)
+    keys = orc.keygen(P, seed=2201, rotations=[5])
+    v = np.random.default_rng(5).uniform(-1, 1, P.n // 2)
+    ct = _enc(P, keys, v, 3, 0)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    lifted = ev.lift_pq(ct)
+    assert len(lifted.c[0]) == 4 + P.K and not lifted.c[0][4:].any()
+    back = ev.moddown_ct(lifted)
+    assert all(np.array_equal(a, b) for a, b in zip(back.c, ct.c))
+    r = ev.moddown_ct(ev.rotate_pq(lifted, 5))
+    assert rel_err(orc.decrypt_vector(P, keys, r), np.roll(v, -5)) < 1e-6
+    # a hoisted baby step left in PQ, brought down, decrypts to the rotation as well
+    hb = ev.moddown_ct(ev.hoisted_step_pq(ct, ev.hoist_modup(ct), 5))
+    assert rel_err(orc.decrypt_vector(P, keys, hb), np.roll(v, -5)) < 1e-6
+
+
+@pytest.mark.parametrize("L", [1, 2])
+def test_double_hoisted_k3_decrypts_to_dft(Pg, L):
+    """K3 with double-hoisted BSGS (cfg.hoist = 2) decrypts to fftshift(fft(hann x)) per
+    block like the single-hoisted circuit; the op counts are the double-hoisted schedule:
+    2 lifts + 2(b-1) PQ baby steps, one PQ giant step per nonzero giant offset and output,
+    one ModDown per output (no HRot with its own ModDown)."""
+    P = Pg
+    cfg, Zt = _gesture_setup(P, F=2)
+    cfg.hoist, cfg.lanes = 2, L
+    n = cfg.n_slots
+    keys = orc.keygen(P, seed=2202, rotations=cc.required_rotations("k3_doppler_dft", cfg, P.n))
+    vs = [radar.pack_doppler(Zt[t]) for t in range(L)]
+    cr = _enc(P, keys, cc.interleave([v.real for v in vs], L, n), P.L, 0)
+    ci = _enc(P, keys, cc.interleave([v.imag for v in vs], L, n), P.L, 1)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    dre, dim = cc.k3_doppler_dft(ev, cc.PlainBook(P), cr, ci, cfg)
+    b, giants = cc.k3_schedule(cfg)
+    ops = [op for op, _, _ in ev.trace]
+    assert ops.count("hrot_hoisted_pq") == 2 * (b - 1) and ops.count("lift_pq") == 2
+    assert ops.count("hrot_pq") == 2 * sum(1 for _, G, _ in giants if G) and ops.count("moddown") == 2
+    assert "hrot" not in ops and "hrot_hoisted" not in ops
+    got_re, got_im = orc.decrypt_vector(P, keys, dre), orc.decrypt_vector(P, keys, dim)
+    for f in range(L):
+        want = dsp.doppler_dft(vs[f], cfg.D)
+        assert rel_err(got_re[f::L], want.real) < 1e-3 and rel_err(got_im[f::L], want.imag) < 1e-3
+
+
+def test_double_hoisted_gesture_pipeline(Pg):
+    """The whole gesture pipeline with double-hoisted K3 and FC (hoist = 2, 2 lanes):
+    features and logits decrypt to the plaintext DSP; argmax agrees; depth unchanged."""
+    P = Pg
+    F, L = 4, 2
+    cfg, Zt = _gesture_setup(P, F=F)
+    cfg.hoist, cfg.lanes = 2, L
+    n = cfg.n_slots
+    keys = orc.keygen(P, seed=2203, rotations=cc.required_rotations("gesture", cfg, P.n))
+    vs = [radar.pack_doppler(Zt[t]) for t in range(F)]
+    re = [_enc(P, keys, cc.interleave([v.real for v in vs[g * L:(g + 1) * L]], L, n), P.L, 2 * g) for g in range(2)]
+    im = [_enc(P, keys, cc.interleave([v.imag for v in vs[g * L:(g + 1) * L]], L, n), P.L, 2 * g + 1)
+          for g in range(2)]
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    feat = cc.gesture_features(ev, book, re, im, cfg)
+    xp = np.sum([dsp.gesture_frame_features(v, cfg.A, cfg.R, cfg.D, cfg.gamma) for v in vs], axis=0)
+    dims = cfg.fc_dims
+    Ws, bs = radar.fc_weights([dims[0], dims[1], dims[2], 5], seed=7)
+    Ws[0] = Ws[0] / max(np.max(np.abs(Ws[0] @ xp)), 1e-30) * 0.8
+    logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
+    assert logits.level == P.L - 11
+    got = orc.decrypt_vector(P, keys, logits)[cc.logit_slots(5, L)]
+    want = dsp.mlp_forward(xp, Ws, bs)
+    assert rel_err(got, want) < 1e-3
+    assert int(np.argmax(got)) == int(np.argmax(want))
