@@ -19,15 +19,15 @@ ap.add_argument("--frames", type=int, default=25)
 ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--lanes", type=int, default=1)
+ap.add_argument("--hoist", type=int, default=1)
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
 P = ps4()
 F = args.frames
 stream = torch.cuda.current_stream(dev)
-cfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25, hoist=1,
-                  lanes=args.lanes) if args.lanes > 1 else \
-    m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25, hoist=1)
+cfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8),
+                  frame_batch=25 if args.lanes == 1 else 0, hoist=args.hoist, lanes=args.lanes)
 ctx = m.Context.from_params(P, device=0, stream=stream.cuda_stream)
 gen = torch.Generator(device=dev)
 gen.manual_seed(77)
