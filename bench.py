@@ -299,7 +299,7 @@ def run_gpu(args, rank, world, device):
     extras = {}
     if not args.no_extras:
         extras = extras_n16(args, m, torch, device)
-        for wl in ("C4_canonical", "C4_l11", "C2", "C1", "C3", "C5v"):
+        for wl in ("C4_canonical", "C4_l11", "C2", "C1", "C3", "C5v", "C5v_t3", "Vpaper"):
             try:
                 extras[wl] = bench_workload(wl, m, torch, device)
             except Exception as e:  # report, do not hide
@@ -360,15 +360,22 @@ def bench_workload(name, m, torch, device, steps=3, warmup=2):
         frames = c["F"]
         info = (f"F=100 frames, entry level {c['level']}, hoisted, "
                 + ("one frame per ciphertext, frame_batch 25" if lanes == 1 else f"{lanes} frames per ciphertext"))
-    else:  # C5v
-        P = ps4()
+    else:  # C5v (PS4), C5v_t3 (PS4, third-order K7), Vpaper (the paper's vital parameters, PSV)
+        from synth.params import psv
+        P = psv() if name == "Vpaper" else ps4()
         F, fs = 200, 20.0
-        cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2,
+        t3 = name == "C5v_t3"
+        cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=3 if t3 else 1, n_slots=P.n // 2,
                           bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
                           frame_batch=40, vp_plus=1, iq_pack=3, hoist=1)
-        plan = [("vitals_v1", 3, 2 * F), ("vitals_v2", 9, 2 * F)]
+        plan = [("vitals_v1", 3, 2 * F), ("vitals_v2", 11 if t3 else 9, 2 * F)]
         taps = [radar.fir_taps(41, b, fs) for b in BANDS]
-        frames, info = F, "F=200 frames, frame_batch 40, VP+ in the cloud"
+        frames = F
+        info = ("R=64, F=200 frames @ 20 Hz (the paper's Children config, P:1116-1117), frame_batch 40, VP+ in the "
+                "cloud, " + ("third-order K7 (depth 11)" if t3 else "first-order K7 (depth 9)")
+                + ("; the paper's vital parameters (PSV: N=2^15, 11 Q limbs, dnum 3) -- paper: 103.32 s per "
+                   "200-frame window end to end, 1.94 frames/s (2.78 counting only the cloud stages K2, K5+K7, "
+                   "DFT+PSD) on an RTX 3090 Ti, P:1325-1333" if name == "Vpaper" else ""))
     ctx = m.Context.from_params(P, device=device.index or 0, stream=stream.cuda_stream)
     basis = list(P.q) + list(P.p)
     key_shape = (P.dnum(), 2, len(basis))

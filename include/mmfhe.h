@@ -204,7 +204,10 @@ mmfhe_status mmfhe_load_scalars(mmfhe_ctx *ctx, const char *name, const double *
  * on their own ("used individually or composed"): "k2_soft_attention" (in: E;
  * out: N, D), "k2_doppler_soft_power" (in: K6 outputs Pm_t; out: f_t), "k4_soft_iq" (in:
  * re_t, im_t per frame; out: I_0..I_{F-1}, Q_0..Q_{F-1}), "k5_fir" (in: x_0..x_{F-1}; out:
- * per band b the filtered sequence with taps "k5.b<b>", band-major), "k6_notch" (in: P_t;
+ * per band b the filtered sequence with taps "k5.b<b>", band-major), "k5_fir_rot" (the
+ * rotation-based FIR of P:205-206: every input one ciphertext holding a sequence in its
+ * slots, zeros beyond; out: per band, per input, the filtered sequence in the same slots;
+ * rotation keys -s and -g'b of the BSGS split of the longest band), "k6_notch" (in: P_t;
  * out: Pm_t), "k7_taylor_phase" (in: I_f,t, Q_f,t per frame; out: dphi_1..dphi_{F-1}),
  * "fc_forward" (in: features; out: logits; = gesture_fc).
  * in[0..n_in): input ciphertexts in the order the chain documents (DESIGN.md

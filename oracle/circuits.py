@@ -56,6 +56,7 @@ class ChainCfg:
     hoist: int = 0              # 1: baby-step rotations of K3 / FC share one ModUp (hoisted HRot)
     vp_plus: int = 0            # vital V2: 1 -> sharpen + weighted frequency average in the cloud
     iq_pack: int = 0            # K4: k >= 1 -> packed rotate-and-sum over 2^k vectors (reading R19)
+    n_taps: tuple = ()          # k5_fir_rot: taps per band (rotation keys for the longest)
     lanes: int = 1              # gesture / K3: frames interleaved per ciphertext (reading R20)
 
 
@@ -624,6 +625,32 @@ def k5_fir(ev, xs, taps):
     return [ev.rescale(x) for x in lin]
 
 
+def fir_rot_schedule(W: int):
+    """BSGS split of the W taps of the rotation-based FIR: k = g' b + s."""
+    b = ceil_sqrt(W)
+    g = -(-W // b)
+    return b, [(gp, [s for s in range(b) if gp * b + s < W]) for gp in range(g)]
+
+
+def k5_fir_rot(ev, x, taps, hoist=1):
+    """K5 "Alternate Implementation": y[n] = sum_k h[k] x[n - k] as weighted
+    accumulation over slot rotations, for a sequence packed in the slots of ONE ciphertext
+    (x[t] in slot t, zeros beyond the sequence, reading #23: the rotations then bring zeros in,
+    i.e. causal with zero initial state).  BSGS over the taps: baby steps Rot(x, -s) (hoisted),
+    per giant g' the scalar combination sum_s h[g'b + s] Rot(x, -s) (exact encoding at q_l,
+    c-5), giant rotation by -g'b, sum, one rescale.  Depth 1."""
+    W = len(taps)
+    b, giants = fir_rot_schedule(W)
+    babies = [x] + [r[0] for r in baby_steps(ev, [x], [-s for s in range(1, min(b, W))], hoist)]
+    inners = [ev.lincomb_scalar([babies[s] for s in ss], [taps[gp * b + s] for s in ss]) for gp, ss in giants]
+    acc = None
+    for (gp, ss), inner in zip(giants, inners):
+        if gp:
+            inner = ev.rotate(inner, -gp * b)
+        acc = inner if acc is None else ev.add(acc, inner)
+    return ev.rescale(acc)
+
+
 def k7_taylor_phase(ev, If, Qf, order):
     """K7: y[t] = Q_f[t] I_f[t-1] - I_f[t] Q_f[t-1]; first order y,
     third order y x^2 - y^3/3 (literal polynomial, reading #2); t = 1..F-1."""
@@ -703,6 +730,10 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
     """Rotation amounts (normalised to [0, N/2)) a chain needs."""
     half = n_ring // 2
     ks = set()
+    if chain == "k5_fir_rot":
+        W = max(cfg.n_taps) if getattr(cfg, "n_taps", None) else 0
+        b, giants = fir_rot_schedule(W) if W else (1, [])
+        ks |= {-s for s in range(1, min(b, W))} | {-gp * b for gp, _ in giants if gp}
     if chain in ("k2_soft_attention", "vitals_v1", "k4_soft_iq", "vitals_v2"):
         ks |= set(rotsum_steps(cfg.R, 1))
     if chain in ("k4_soft_iq", "vitals_v2") and cfg.iq_pack:

@@ -478,6 +478,43 @@ class Runner {
         return ev_rescale(c_, ev_lincomb_mat(c_, x, F, W, -(int)(W - 1), 1, coef));
     }
 
+    // K5 "Alternate Implementation": y = sum_k h[k] Rot(x, -k) for a sequence packed
+    // in the slots of one ciphertext (oracle k5_fir_rot): hoisted baby steps Rot(x, -s), per giant
+    // the exact scalar combination of the babies, giant rotation by -g'b, sum, one rescale
+    DCt k5_fir_rot(const DCt &x, const std::vector<double> &taps)
+    {
+        const uint32_t W = (uint32_t)taps.size(), b = ceil_sqrt(W), g = (W + b - 1) / b, nb = std::min(b, W);
+        std::vector<DCt> babies;
+        babies.push_back(copy_ct(c_, x));
+        std::vector<int32_t> st;
+        for (uint32_t s = 1; s < nb; ++s) st.push_back(-(int32_t)s);
+        if (!st.empty()) {
+            if (cfg_.hoist) {
+                for (auto &r : ev_rotate_hoisted(c_, x, st)) babies.push_back(std::move(r));
+            } else {
+                for (int32_t s : st) babies.push_back(ev_rotate(c_, x, s));
+            }
+        }
+        DCt all = babies.size() == 1 ? std::move(babies[0]) : concat(c_, babies);
+        const uint32_t full = W / b, last = W - full * b;  // giants with b taps, then a partial one
+        std::vector<DCt> inners;
+        if (full) {
+            std::vector<double> coef((size_t)full * nb);
+            for (uint32_t j = 0; j < full; ++j)
+                for (uint32_t s = 0; s < nb; ++s) coef[(size_t)j * nb + s] = taps[j * b + s];
+            DCt r = ev_lincomb_mat(c_, all, full, nb, 0, 0, coef);
+            for (uint32_t j = 0; j < full; ++j) inners.push_back(copy_ct(c_, slice(r, j, 1)));
+        }
+        if (last) {
+            std::vector<double> coef(taps.begin() + full * b, taps.end());
+            inners.push_back(ev_lincomb_mat(c_, all, 1, last, 0, 0, coef));
+        }
+        MMFHE_REQUIRE(inners.size() == g, MMFHE_E_SHAPE, "FIR giant count");
+        DCt acc = std::move(inners[0]);
+        for (uint32_t j = 1; j < g; ++j) acc = ev_addsub(c_, acc, ev_rotate(c_, inners[j], -(int32_t)(j * b)), false);
+        return ev_rescale(c_, acc);
+    }
+
     DCt k7_taylor_phase(const DCt &If, const DCt &Qf)
     {
         const uint32_t F = If.batch;
@@ -641,7 +678,7 @@ uint32_t chain_depth(const std::string &chain, const mmfhe_chain_cfg &cfg)
     if (chain == "k2_soft_attention") return lg + 1;
     if (chain == "k2_doppler_soft_power") return lg + 1;
     if (chain == "k4_soft_iq") return 1 + lp + 1;
-    if (chain == "k5_fir") return 1;
+    if (chain == "k5_fir" || chain == "k5_fir_rot") return 1;
     if (chain == "k6_notch") return 1;
     if (chain == "k7_taylor_phase") return cfg.taylor_order == 3 ? 3 : 1;
     if (chain == "fc_forward") return fc;
@@ -670,6 +707,15 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
         }
         if (cfg.hoist)
             for (uint32_t mm = 1; mm < (1u << cfg.iq_pack); ++mm) add((int64_t)mm * cfg.R);
+    }
+    if (chain == "k5_fir_rot") {
+        uint32_t W = 0;
+        for (uint32_t b = 0; b < cfg.n_bands; ++b) W = std::max(W, cfg.n_taps[b]);
+        if (W) {
+            const uint32_t b = ceil_sqrt(W), g = (W + b - 1) / b;
+            for (uint32_t s = 1; s < std::min(b, W); ++s) add(-(int64_t)s);
+            for (uint32_t j = 1; j < g; ++j) add(-(int64_t)(j * b));
+        }
     }
     const bool frames = chain == "gesture_frame" || chain == "gesture" || chain == "gesture_features";
     const int64_t L = lanes_of(cfg);
@@ -734,7 +780,7 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
             MMFHE_REQUIRE(((size_t)cfg.R << cfg.iq_pack) <= (size_t)(cfg.n_slots ? cfg.n_slots : c.n / 2),
                           MMFHE_E_SHAPE, "iq_pack = k needs 2^k R <= n slots");
         }
-    } else if (chain == "k5_fir") {
+    } else if (chain == "k5_fir" || chain == "k5_fir_rot") {
         MMFHE_REQUIRE(n_in >= 1 && cfg.n_bands >= 1 && cfg.n_bands <= 4, MMFHE_E_SHAPE,
                       "expected a frame sequence and 1..4 FIR bands");
         n_out = n_in * cfg.n_bands;
@@ -833,6 +879,10 @@ std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_c
     } else if (chain == "k5_fir") {
         DCt x = import_batch(c, in, 0, 1, n_in);
         for (uint32_t b = 0; b < cfg.n_bands; ++b) out.push_back(r.k5_fir(x, r.band_taps(b)));
+    } else if (chain == "k5_fir_rot") {
+        // every input is one slot-packed sequence; outputs band-major, sequence by sequence
+        for (uint32_t b = 0; b < cfg.n_bands; ++b)
+            for (size_t s = 0; s < n_in; ++s) out.push_back(r.k5_fir_rot(import_batch(c, in, s, 1, 1), r.band_taps(b)));
     } else if (chain == "k7_taylor_phase") {
         DCt If = import_batch(c, in, 0, 2, n_in / 2);
         DCt Qf = import_batch(c, in, 1, 2, n_in / 2);

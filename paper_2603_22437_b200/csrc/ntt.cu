@@ -696,7 +696,8 @@ void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const C
                                    : 8.0 * rows * c.n *
                                          (1.0 + (epi->add0 ? 0.5 : 0.0) + (epi->add1 ? 0.5 : 0.0) +
                                           (epi->add2 ? 0.5 : 0.0));
-        MMFHE_REQUIRE(!epi || (epi->per >= 1 && rows % (2 * epi->per) == 0), MMFHE_E_LAYOUT, "NTT epilogue rows");
+        MMFHE_REQUIRE(!epi || (epi->per >= 1 && rows % ((epi->npoly ? epi->npoly : 2) * epi->per) == 0),
+                      MMFHE_E_LAYOUT, "NTT epilogue rows");
         ProfScope ps(c, epi ? "ntt_fwd_row_epi" : "ntt_fwd_row", bytes + ebytes, 0.5 * rows * c.n * L2);
         launch_pass<true, false>(c.log_n, d, rows, c.kt, pm, nullptr, nullptr, epi, c.stream);
     }

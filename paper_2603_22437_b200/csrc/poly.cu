@@ -9,6 +9,7 @@
 // 256-byte warp accesses), grid.y over limbs/rows, grid.z over batch items;
 // per-prime constants are warp-uniform loads (L1 broadcast).
 #include <algorithm>
+#include <cstdlib>
 
 #include "modarith.cuh"
 #include "ops.h"
@@ -482,31 +483,35 @@ struct DiagMacArgs {
 };
 
 template <int NCMAX>
-__global__ void __launch_bounds__(256) k_diag_mac(DiagMacArgs a, KTables kt)
+__global__ void __launch_bounds__(128) k_diag_mac(DiagMacArgs a, KTables kt)
 {
     extern __shared__ uint64_t spt[];  // [no][nc][kDmTK]
     const uint32_t L1 = a.level + 1;
-    const uint32_t ry = blockIdx.y;  // row inside an item: [2][L1] Q rows, then [2][pk] P rows
-    uint32_t prow, prime;
-    if (ry < 2 * L1) {
-        prow = ry % L1;
-        prime = prow;
-    } else {
-        const uint32_t kk = (ry - 2 * L1) % a.pk;
-        prow = L1 + kk;
-        prime = a.L + 1 + kk;
-    }
+    const uint32_t pr = blockIdx.y;  // residue row of the basis: q_0..q_l, then p_0..p_{pk-1}
+    const uint32_t prime = pr < L1 ? pr : a.L + 1 + (pr - L1);
     const uint32_t k0 = blockIdx.x * kDmTK;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nt = a.no * a.nc;
-    for (int t = warp; t < nt; t += nw) {
-        const uint64_t *p = a.pt[t / a.nc][t % a.nc];
-        spt[t * kDmTK + lane] = p ? __ldg(p + (size_t)prow * kt.n + k0 + lane) : 0;
+    for (int t0 = warp * 4; t0 < nt; t0 += nw * 4) {  // four 256-byte rows in flight per warp
+        uint64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u;
+            const uint64_t *p = t < nt ? a.pt[t / a.nc][t % a.nc] : nullptr;
+            v[u] = p ? __ldg(p + (size_t)pr * kt.n + k0 + lane) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (t0 + u < nt) spt[(t0 + u) * kDmTK + lane] = v[u];
     }
     __syncthreads();
     const uint64_t q = kt.q[prime], qi = kt.qinv_neg[prime];
-    const size_t off = (size_t)ry * kt.n + k0 + lane;
-    for (uint32_t b = warp; b < a.B; b += nw) {
+    // item rows: Q part [2][L1] then P part [2][pk]; this CTA's two rows (poly 0 / 1)
+    const size_t r0 = pr < L1 ? pr : 2 * L1 + (pr - L1);
+    const size_t pstride = pr < L1 ? L1 : a.pk;
+    for (uint32_t u = warp; u < 2 * a.B; u += nw) {
+        const uint32_t b = u >> 1, poly = u & 1;
+        const size_t off = (r0 + poly * pstride) * kt.n + k0 + lane;
         uint64_t x[NCMAX];
 #pragma unroll
         for (int c = 0; c < NCMAX; ++c) x[c] = c < a.nc ? a.ct[c][(size_t)b * a.is + off] : 0;
@@ -518,6 +523,38 @@ __global__ void __launch_bounds__(256) k_diag_mac(DiagMacArgs a, KTables kt)
                 if (c < a.nc) mac128(acc, x[c], w[c * kDmTK]);
             a.out[o][(size_t)b * a.os + off] = redc(acc, q, qi);
         }
+    }
+}
+
+// The L2-shared variant (round 1's design, without its prefetch registers): grid.x = tile * B
+// + item, so the B CTAs of a tile read its plaintext words from L2; one poly row per CTA.
+template <int NCMAX>
+__global__ void __launch_bounds__(256) k_diag_mac_l2(DiagMacArgs a, KTables kt)
+{
+    const uint32_t item = blockIdx.x % a.B, tile = blockIdx.x / a.B;
+    const uint32_t k = tile * blockDim.x + threadIdx.x;
+    if (k >= kt.n) return;
+    const uint32_t L1 = a.level + 1, ry = blockIdx.y;
+    uint32_t prow, prime;
+    if (ry < 2 * L1) {
+        prow = ry % L1;
+        prime = prow;
+    } else {
+        const uint32_t kk = (ry - 2 * L1) % a.pk;
+        prow = L1 + kk;
+        prime = a.L + 1 + kk;
+    }
+    const size_t off = (size_t)ry * kt.n + k, poff = (size_t)prow * kt.n + k;
+    const uint64_t q = kt.q[prime], qi = kt.qinv_neg[prime];
+    uint64_t x[NCMAX];
+#pragma unroll
+    for (int c = 0; c < NCMAX; ++c) x[c] = c < a.nc ? a.ct[c][(size_t)item * a.is + off] : 0;
+    for (int o = 0; o < a.no; ++o) {
+        U128 acc{0, 0};
+#pragma unroll
+        for (int c = 0; c < NCMAX; ++c)
+            if (c < a.nc && a.pt[o][c]) mac128(acc, x[c], __ldg(a.pt[o][c] + poff));
+        a.out[o][(size_t)item * a.os + off] = redc(acc, q, qi);
     }
 }
 
@@ -948,6 +985,21 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
     const double rows = level + 1 + pk;
     // algorithmic: babies read once, plaintexts once per launch, outputs written once
     ProfScope ps(c, "diag_mac", 8.0 * rows * c.n * (terms + B * 2.0 * (a.nc + a.no)), 2.0 * terms * rows * c.n * B);
+    static const bool l2_variant = [] {
+        const char *e = getenv("MMFHE_DIAG_L2");
+        return e && *e == '1';
+    }();
+    if (l2_variant) {
+        const dim3 g(((c.n + 255) / 256) * B, 2 * (level + 1 + pk));
+        if (a.nc <= 4)
+            k_diag_mac_l2<4><<<g, 256, 0, c.stream>>>(a, c.kt);
+        else if (a.nc <= 8)
+            k_diag_mac_l2<8><<<g, 256, 0, c.stream>>>(a, c.kt);
+        else
+            k_diag_mac_l2<16><<<g, 256, 0, c.stream>>>(a, c.kt);
+        LAUNCH_CHECK(c);
+        return;
+    }
     static std::atomic<uint64_t> attr{0};
     once_per_device(attr, [] {
         const int mx = (int)(sizeof(uint64_t) * kDiagMax * kDiagMax * kDmTK);
@@ -956,14 +1008,13 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
         CUDA_CHECK(cudaFuncSetAttribute(k_diag_mac<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     });
     const size_t smem = sizeof(uint64_t) * (size_t)a.no * a.nc * kDmTK;
-    const int threads = 32 * (int)std::min<uint32_t>(8, std::max<uint32_t>(4, B));
-    const dim3 g(c.n / kDmTK, 2 * (level + 1 + pk));
+    const dim3 g(c.n / kDmTK, level + 1 + pk);
     if (a.nc <= 4)
-        k_diag_mac<4><<<g, threads, smem, c.stream>>>(a, c.kt);
+        k_diag_mac<4><<<g, 128, smem, c.stream>>>(a, c.kt);
     else if (a.nc <= 8)
-        k_diag_mac<8><<<g, threads, smem, c.stream>>>(a, c.kt);
+        k_diag_mac<8><<<g, 128, smem, c.stream>>>(a, c.kt);
     else
-        k_diag_mac<16><<<g, threads, smem, c.stream>>>(a, c.kt);
+        k_diag_mac<16><<<g, 128, smem, c.stream>>>(a, c.kt);
     LAUNCH_CHECK(c);
 }
 

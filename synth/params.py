@@ -134,10 +134,18 @@ def ps4() -> ParamSet:  # C4/C5: N=2^16, Q=(60, 19x50), P=7x60, alpha=7 (dnum 3)
     return make_params(16, 20, 50, 7, 7, name="PS4")
 
 
+def psv() -> ParamSet:
+    """The paper's vital column: N=2^15, 11 Q limbs (60 + 10x40,
+    the 5.5 MB ciphertext of P:1405), dnum 3 (the 22.5 MiB relinearisation key of P:1412:
+    3 digits x 2 x 15 limbs x 2^15 x 8 B): alpha 4, K = 4 special primes of 60 bits;
+    log2 PQ ~ 700 <= 881 (128-bit, ternary, N = 2^15)."""
+    return make_params(15, 11, 40, 4, 4, name="PSV")
+
+
 def toy(log_n: int = 10, n_q: int = 6, scale_bits: int = 40, n_p: int = 2,
         alpha: int = 2) -> ParamSet:
     """Small, insecure sets for fast tests (same prime rule)."""
     return make_params(log_n, n_q, scale_bits, n_p, alpha, name=f"toy{log_n}")
 
 
-PARAM_SETS = {"PS1": ps1, "PS2": ps2, "PS3": ps3, "PS4": ps4}
+PARAM_SETS = {"PS1": ps1, "PS2": ps2, "PS3": ps3, "PS4": ps4, "PSV": psv}

@@ -564,3 +564,29 @@ def test_standalone_k6_k2b_fc_chains(m, lanes):
     feat5 = orc.Ct([c[:6].copy() for c in feat.c], 5, feat.scale, feat.n_slots)
     ctx = _run(m, P, keys, book, "fc_forward", cfg, [feat5], [logits])
     assert ctx.trace() == ev.trace
+
+
+@pytest.mark.parametrize("hoist", [0, 1])
+def test_standalone_k5_fir_rot(m, hoist):
+    """The rotation-based FIR as a chain: two slot-packed sequences, a 41-tap and a
+    5-tap band (BSGS over the taps, exact scalar combinations, hoisted or plain baby steps):
+    residues and trace equal the oracle's k5_fir_rot, outputs band-major."""
+    P = toy(log_n=10, n_q=3, scale_bits=40, n_p=2, alpha=2)
+    rng = np.random.default_rng(74)
+    F = 100
+    taps = [radar.fir_taps(41, (0.8, 2.5), 20.0), radar.fir_taps(5, (0.1, 0.6), 20.0)]
+    cfg = cc.ChainCfg(F=F, n_slots=P.n // 2, n_taps=(41, 5), hoist=hoist)
+    keys = orc.keygen(P, seed=3631, rotations=cc.required_rotations("k5_fir_rot", cfg, P.n))
+    seqs = []
+    for _ in range(2):
+        x = np.zeros(P.n // 2)
+        x[:F] = rng.uniform(-1, 1, F)
+        seqs.append(x)
+    xs = _enc_list(P, keys, seqs, 2, 3632)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    want = [cc.k5_fir_rot(ev, x, h, hoist) for h in taps for x in xs]
+    scalars = {f"k5.b{b}": t for b, t in enumerate(taps)}
+    ctx = _run(m, P, keys, None, "k5_fir_rot", cfg, xs, want, scalars=scalars, bins=([1], [1]), taps=taps)
+    assert ctx.trace() == ev.trace
+    assert sorted(ctx.required_rotations("k5_fir_rot", _mcfg(m, cfg, bins=([1], [1]), taps=taps))) == \
+        cc.required_rotations("k5_fir_rot", cfg, P.n)

@@ -512,3 +512,28 @@ def test_double_hoisted_gesture_pipeline(Pg):
     want = dsp.mlp_forward(xp, Ws, bs)
     assert rel_err(got, want) < 1e-3
     assert int(np.argmax(got)) == int(np.argmax(want))
+
+
+# ------------------------------------------------------------------ K5 by slot rotations
+
+@pytest.mark.parametrize("W", [1, 5, 41])
+def test_k5_fir_rot_decrypts_to_lfilter(W):
+    """The rotation-based FIR on a sequence packed in the slots of one ciphertext
+    decrypts to scipy's causal lfilter (zero initial state) over the sequence; depth 1."""
+    P = toy(log_n=10, n_q=3, scale_bits=40, n_p=2, alpha=2)
+    rng = np.random.default_rng(W)
+    F = 120
+    x = np.zeros(P.n // 2)
+    x[:F] = rng.uniform(-1, 1, F)
+    taps = radar.fir_taps(W, (0.8, 2.5), 20.0) if W > 1 else np.array([0.7])
+    cfg = cc.ChainCfg(n_taps=(W,), n_slots=P.n // 2)
+    keys = orc.keygen(P, seed=2301, rotations=cc.required_rotations("k5_fir_rot", cfg, P.n))
+    ct = _enc(P, keys, x, 2, 0)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    y = cc.k5_fir_rot(ev, ct, taps)
+    assert y.level == 1
+    got = orc.decrypt_vector(P, keys, y)[:F]
+    want = dsp.fir(x[:F], taps)
+    assert rel_err(got, want) < 1e-4
+    b, giants = cc.fir_rot_schedule(W)
+    assert sum(1 for op in ev.trace if op[0] in ("hrot", "hrot_hoisted")) == (min(b, W) - 1) + (len(giants) - 1)

@@ -174,3 +174,17 @@ def test_evk_sizes_match_paper():
     assert size / 2 ** 20 == pytest.approx(22.5)
     # ciphertext 5.5 MiB = 2 x 11 limbs x 2^15 x 8 B
     assert 2 * len(P.q) * P.n * 8 / 2 ** 20 == pytest.approx(5.5)
+
+
+def test_paper_vital_parameter_set_reproduces_published_sizes():
+    """PSV: N=2^15, 11 Q limbs (60 + 10 x 40 bits), dnum 3 with
+    K = alpha = 4 special primes reproduces the paper's 5.5 MB ciphertext and 22.5 MB
+    relinearisation key (Table tab:comm_overhead), within the 128-bit HE-standard bound
+    for N = 2^15 (log2 PQ <= 881)."""
+    from synth.params import psv
+    P = psv()
+    MiB = 2 ** 20
+    assert 2 * len(P.q) * P.n * 8 / MiB == 5.5
+    assert P.dnum() * 2 * (len(P.q) + len(P.p)) * P.n * 8 / MiB == 22.5
+    assert sum(q.bit_length() for q in P.q + P.p) <= 881
+    assert all((q - 1) % (2 * P.n) == 0 for q in P.q + P.p)
