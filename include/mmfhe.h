@@ -323,6 +323,22 @@ mmfhe_status mmfhe_serialize_key(mmfhe_ctx *ctx, int kind, int32_t step, const u
 /* Load a relinearisation or Galois key blob into the ctx's key store. */
 mmfhe_status mmfhe_load_key_serialized(mmfhe_ctx *ctx, const void *buf, size_t len);
 
+/* ---- the trusted client on the GPU ----------
+ * For the sensor side only: these derive the secret key from `seed` on the device and never
+ * hand it out; the cloud-side calls above never take it.  Randomness is the counter-based
+ * SplitMix64 of synth/prng.py (client.cu states the streams), so outputs are bit-identical
+ * to the reference client's.
+ * mmfhe_client_keygen: pk [2][L+1][N] (b = e - a s, a), the relinearisation key (relin != 0,
+ * key for s^2) and one Galois key per steps[i] (key for sigma_g(s), g = 5^(k mod N/2)), each
+ * [dnum_L][2][L+1+K][N], coefficient form, written to host or device buffers (on_device).
+ * mmfhe_client_encrypt: out[i] = (u b + e0 + pt_i, u a + e1) at pt_i's level with u ternary
+ * and e0, e1 CBD(21) from the streams of ciphertext index first_index + i; pts are
+ * coefficient-form plaintexts (n_polys = 1) sharing one level; pk as produced above. */
+mmfhe_status mmfhe_client_keygen(mmfhe_ctx *ctx, uint64_t seed, const int32_t *steps, size_t n_steps, int relin,
+                                 uint64_t *pk, uint64_t *rlk, uint64_t *gk, int on_device);
+mmfhe_status mmfhe_client_encrypt(mmfhe_ctx *ctx, const uint64_t *pk, int pk_on_device, const mmfhe_ct *pts, size_t n,
+                                  uint64_t seed, uint32_t first_index, mmfhe_ct *out);
+
 /* ---- op trace (Theorem P:999-1006: data-oblivious execution) -------------- */
 /* One logical op per line: "<op> <level> <arg>".  mmfhe_trace_clear resets. */
 mmfhe_status mmfhe_trace_get(mmfhe_ctx *ctx, char *buf, size_t cap, size_t *len);

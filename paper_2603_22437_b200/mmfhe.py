@@ -136,6 +136,8 @@ def lib():
             "mmfhe_deserialize_ct": [V, V, S, CTP],
             "mmfhe_serialize_key": [V, ctypes.c_int, I32, V, S, ctypes.c_int, V, S, P(S)],
             "mmfhe_load_key_serialized": [V, V, S],
+            "mmfhe_client_keygen": [V, U64, P(I32), S, ctypes.c_int, V, V, V, ctypes.c_int],
+            "mmfhe_client_encrypt": [V, V, ctypes.c_int, CTP, S, U64, U32, CTP],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -157,7 +159,7 @@ EXPORTED = [
     "mmfhe_hmult_batch", "mmfhe_trace_get", "mmfhe_trace_clear", "mmfhe_trace_enable", "mmfhe_profile_enable",
     "mmfhe_profile_get", "mmfhe_microbench", "mmfhe_graph_enable", "mmfhe_graph_stats", "mmfhe_eval_chain_async",
     "mmfhe_ctx_sync", "mmfhe_params_digest", "mmfhe_serialize_ct", "mmfhe_deserialize_ct", "mmfhe_serialize_key",
-    "mmfhe_load_key_serialized", "mmfhe_load_plain_pq",
+    "mmfhe_load_key_serialized", "mmfhe_load_plain_pq", "mmfhe_client_keygen", "mmfhe_client_encrypt",
 ]
 
 SER_CT, SER_RELIN_KEY, SER_GALOIS_KEY = 0, 1, 2
@@ -478,6 +480,33 @@ class Context:
 
     def load_key_serialized(self, blob: bytes):
         self._check(self._lib.mmfhe_load_key_serialized(self.h, blob, len(blob)))
+
+    # ---- the trusted client on the GPU (include/mmfhe.h: never used by the cloud side)
+    def client_keygen(self, seed, steps=(), relin=True, pk=None, rlk=None, gk=None):
+        """pk [2][L+1][N], rlk and gk[i] [dnum][2][L+1+K][N] into the given buffers (numpy or
+        CUDA tensors, all on one side) or new numpy arrays; returns (pk, rlk, gk)."""
+        L1, K1 = len(self.q), len(self.q) + len(self.p)
+        dn = -(-L1 // self.alpha)
+        if pk is None:
+            pk = np.empty((2, L1, self.n), dtype=np.uint64)
+            rlk = np.empty((dn, 2, K1, self.n), dtype=np.uint64) if relin else None
+            gk = np.empty((len(steps), dn, 2, K1, self.n), dtype=np.uint64) if steps else None
+        st = (ctypes.c_int32 * max(len(steps), 1))(*[int(s) for s in steps])
+        addr, dev = _ptr(pk)
+        r_addr = _ptr(rlk)[0] if rlk is not None else None
+        g_addr = _ptr(gk)[0] if gk is not None else None
+        self._check(self._lib.mmfhe_client_keygen(self.h, int(seed), st, len(steps), 1 if relin else 0, addr,
+                                                  r_addr, g_addr, dev))
+        return pk, rlk, gk
+
+    def client_encrypt(self, pk, pts, seed, first_index, outs):
+        """outs[i] = Enc(pts[i]) with the encryption streams of index first_index + i."""
+        addr, dev = _ptr(pk)
+        ai, ao = CtArray(pts), CtArray(outs)
+        self._check(self._lib.mmfhe_client_encrypt(self.h, addr, dev, ai.arr, len(ai), int(seed), int(first_index),
+                                                   ao.arr))
+        ao.sync_back()
+        return outs
 
     def microbench(self, kind):
         """Whole-GPU ops/s of one register-resident op: 0 CT butterfly, 1 GS butterfly,
