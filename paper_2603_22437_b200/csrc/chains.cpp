@@ -21,6 +21,7 @@
 // the ctx was prepared (mmfhe_prepare_chain), they are computed from the
 // paper's formulas and encoded with the library's encoder on first use.
 #include <cmath>
+#include <cstdlib>
 #include <complex>
 #include <functional>
 
@@ -253,12 +254,17 @@ class Runner {
         };
         // inner sums of every giant step in one pass over the 2b baby steps (fused diagonal
         // MAC: babies read once, each diagonal once per frame batch), then the giant rotations
-        std::vector<const DCt *> cts;
+        std::vector<const DCt *> cts, pr, pi;
         for (uint32_t b = 0; b < s.b; ++b) cts.push_back(&xr[b]);
         for (uint32_t b = 0; b < s.b; ++b) cts.push_back(&xi[b]);
-        std::vector<std::vector<const DPlain *>> rows;
+        for (uint32_t b = 0; b < s.b; ++b) {
+            pr.push_back(&xr[b]);
+            pi.push_back(&xi[b]);
+        }
+        std::vector<std::vector<const DPlain *>> rows, PC, PS, PN;
         for (auto &g : s.giants) {
-            std::vector<const DPlain *> re(2 * s.b, nullptr), im(2 * s.b, nullptr);
+            std::vector<const DPlain *> re(2 * s.b, nullptr), im(2 * s.b, nullptr), gc(s.b, nullptr), gs(s.b, nullptr),
+                gn(s.b, nullptr);
             for (uint32_t b : g.babies) {
                 const int32_t o = g.G + (int32_t)b;
                 const std::string sfx = "." + std::to_string(g.gp) + "." + std::to_string(b);
@@ -269,11 +275,25 @@ class Runner {
                 re[s.b + b] = &pn;
                 im[b] = &ps;
                 im[s.b + b] = &pc;
+                gc[b] = &pc;
+                gs[b] = &ps;
+                gn[b] = &pn;
             }
             rows.push_back(re);
             rows.push_back(im);
+            PC.push_back(gc);
+            PS.push_back(gs);
+            PN.push_back(gn);
         }
-        std::vector<DCt> inner = ev_diag_mac(c_, cts, rows);
+        // Gauss's three-product form (ev_k3_mac: the same residues and trace, 3/4 of the MACs);
+        // MMFHE_K3_GAUSS=0 selects the generic four-product diagonal MAC (A/B runs)
+        static const bool gauss = [] {
+            const char *e = getenv("MMFHE_K3_GAUSS");
+            return !(e && *e == '0');
+        }();
+        std::vector<DCt> inner = gauss && s.b <= (uint32_t)kDiagMax && s.giants.size() <= (size_t)kDiagMax
+                                     ? ev_k3_mac(c_, pr, pi, PC, PS, PN)
+                                     : ev_diag_mac(c_, cts, rows);
         DCt out_re, out_im;
         bool first = true;
         for (size_t gi = 0; gi < s.giants.size(); ++gi) {

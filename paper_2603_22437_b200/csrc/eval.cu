@@ -399,6 +399,55 @@ std::vector<DCt> ev_diag_mac(Ctx &c, const std::vector<const DCt *> &cts,
     return out;
 }
 
+std::vector<DCt> ev_k3_mac(Ctx &c, const std::vector<const DCt *> &xr, const std::vector<const DCt *> &xi,
+                           const std::vector<std::vector<const DPlain *>> &pc,
+                           const std::vector<std::vector<const DPlain *>> &ps,
+                           const std::vector<std::vector<const DPlain *>> &pns)
+{
+    MMFHE_REQUIRE(!xr.empty() && xr.size() == xi.size() && !pc.empty(), MMFHE_E_INVALID_ARG, "empty K3 MAC");
+    const DCt &a0 = *xr[0];
+    std::vector<const uint64_t *> r, i;
+    for (size_t s = 0; s < xr.size(); ++s) {
+        for (const DCt *x : {xr[s], xi[s]})
+            MMFHE_REQUIRE(x->level == a0.level && x->batch == a0.batch && x->npolys == 2 && x->scale == a0.scale &&
+                              x->pk == a0.pk,
+                          MMFHE_E_LAYOUT, "K3 MAC operands must share level, batch, basis and scale");
+        r.push_back(xr[s]->data());
+        i.push_back(xi[s]->data());
+    }
+    std::vector<std::vector<const uint64_t *>> C(pc.size()), S(pc.size()), NS(pc.size());
+    std::vector<DCt> out;
+    std::vector<uint64_t *> re, im;
+    for (size_t g = 0; g < pc.size(); ++g) {
+        double sc = 0;
+        int cnt = 0;
+        for (size_t s = 0; s < xr.size(); ++s) {
+            const DPlain *p = pc[g][s];
+            C[g].push_back(p ? p->buf.get() : nullptr);
+            S[g].push_back(p ? ps[g][s]->buf.get() : nullptr);
+            NS[g].push_back(p ? pns[g][s]->buf.get() : nullptr);
+            if (!p) continue;
+            for (const DPlain *x : {pc[g][s], ps[g][s], pns[g][s]})
+                MMFHE_REQUIRE(x->level == a0.level && x->pk == a0.pk && x->scale == p->scale, MMFHE_E_LAYOUT,
+                              "plaintext level / basis / scale mismatch");
+            const double v = a0.scale * p->scale;
+            MMFHE_REQUIRE(cnt == 0 || v == sc, MMFHE_E_SCALE, "K3 MAC scale mismatch");
+            sc = v;
+            cnt += 2;
+        }
+        MMFHE_REQUIRE(cnt > 0, MMFHE_E_INVALID_ARG, "giant step without terms");
+        for (int part = 0; part < 2; ++part) {
+            rec_n(c, a0.pk ? "pmult_sum_pq" : "pmult_sum", a0.level, a0.batch, std::to_string(cnt));
+            out.push_back(a0.pk ? make_pq(c, a0.level, a0.n_slots, sc, a0.batch)
+                                : make_ct(c, a0.level, 2, a0.n_slots, sc, a0.batch));
+        }
+        re.push_back(out[out.size() - 2].data());
+        im.push_back(out.back().data());
+    }
+    launch_k3_gauss_mac(c, r, i, a0.item_words(), C, S, NS, re, im, out[0].item_words(), a0.level, a0.batch, a0.pk);
+    return out;
+}
+
 uint64_t encode_scalar_mod(double v, uint64_t q_scale, uint64_t m)
 {
     // v = mant * 2^e exactly with mant < 2^53; |x| = mant * q_scale * 2^e rounded

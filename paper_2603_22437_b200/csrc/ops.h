@@ -62,6 +62,14 @@ void launch_pmult_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &pt, const
 void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is,
                      const std::vector<std::vector<const uint64_t *>> &pts, const std::vector<uint64_t *> &outs,
                      size_t os, uint32_t level, uint32_t B, uint32_t pk = 0);
+// K3's inner sums with Gauss's three-product complex multiplication (babies xr[s], xi[s];
+// plaintexts pc / ps / pns [g][s] (nullptr: no term); outputs re[g], im[g]): equal to the
+// four-product sums bit for bit.
+void launch_k3_gauss_mac(Ctx &c, const std::vector<const uint64_t *> &xr, const std::vector<const uint64_t *> &xi,
+                         size_t is, const std::vector<std::vector<const uint64_t *>> &pc,
+                         const std::vector<std::vector<const uint64_t *>> &ps,
+                         const std::vector<std::vector<const uint64_t *>> &pns, const std::vector<uint64_t *> &re,
+                         const std::vector<uint64_t *> &im, size_t os, uint32_t level, uint32_t B, uint32_t pk);
 // Scalar "modular matrix product" over a batch of 2-poly cts (CK10):
 //   out[j] = sum_{w < W} C[j][w] in[lo_j + w],  j < J,  lo_j = lo0 + j*lo_step,
 // C given as (value, Montgomery form) pairs [J][W][l+1]; inputs outside [0, M) contribute nothing.

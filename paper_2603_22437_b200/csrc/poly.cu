@@ -526,8 +526,9 @@ __global__ void __launch_bounds__(128) k_diag_mac(DiagMacArgs a, KTables kt)
     }
 }
 
-// The L2-shared variant (round 1's design, without its prefetch registers): grid.x = tile * B
-// + item, so the B CTAs of a tile read its plaintext words from L2; one poly row per CTA.
+// The L2-shared variant (round 1's design): grid.x = tile * B + item, so the B CTAs of a tile
+// read its plaintext words from L2; one (poly, residue row) per CTA; the next output's
+// plaintext words are prefetched into registers while the current output accumulates.
 template <int NCMAX>
 __global__ void __launch_bounds__(256) k_diag_mac_l2(DiagMacArgs a, KTables kt)
 {
@@ -546,15 +547,95 @@ __global__ void __launch_bounds__(256) k_diag_mac_l2(DiagMacArgs a, KTables kt)
     }
     const size_t off = (size_t)ry * kt.n + k, poff = (size_t)prow * kt.n + k;
     const uint64_t q = kt.q[prime], qi = kt.qinv_neg[prime];
-    uint64_t x[NCMAX];
+    uint64_t x[NCMAX], w[NCMAX];
 #pragma unroll
     for (int c = 0; c < NCMAX; ++c) x[c] = c < a.nc ? a.ct[c][(size_t)item * a.is + off] : 0;
+#pragma unroll
+    for (int c = 0; c < NCMAX; ++c) w[c] = (c < a.nc && a.pt[0][c]) ? __ldg(a.pt[0][c] + poff) : 0;
     for (int o = 0; o < a.no; ++o) {
-        U128 acc{0, 0};
+        uint64_t wn[NCMAX];
+        const bool more = o + 1 < a.no;
 #pragma unroll
         for (int c = 0; c < NCMAX; ++c)
-            if (c < a.nc && a.pt[o][c]) mac128(acc, x[c], __ldg(a.pt[o][c] + poff));
+            wn[c] = (more && c < a.nc && a.pt[o + 1][c]) ? __ldg(a.pt[o + 1][c] + poff) : 0;
+        U128 acc{0, 0};  // <= 16 terms < q^2 each: < q 2^64 for q < 2^60; absent terms are 0
+#pragma unroll
+        for (int c = 0; c < NCMAX; ++c) mac128(acc, x[c], w[c]);
         a.out[o][(size_t)item * a.os + off] = redc(acc, q, qi);
+#pragma unroll
+        for (int c = 0; c < NCMAX; ++c) w[c] = wn[c];
+    }
+}
+
+// K3's inner sums with Gauss's three-product complex multiplication:
+// for giant g and baby s with plaintexts C = pc, S = ps, NS = pns (Eqs. dft_re / dft_im),
+//   re_g = sum_s C xr + NS xi = sum_s C (xr + xi) - (C - NS) xi
+//   im_g = sum_s S xr + C xi  = sum_s C (xr + xi) + (S - C) xr
+// -- exact modular identities of the same encoded residues, so the outputs equal the four-
+// product sums bit for bit with 3/4 of the MACs.  Staged like k_diag_mac: per tile the words
+// C, S - C and C - NS of every (g, s) in shared memory, then the batch items.
+struct K3MacArgs {
+    const uint64_t *xr[kDiagMax], *xi[kDiagMax];
+    const uint64_t *pc[kDiagMax][kDiagMax], *ps[kDiagMax][kDiagMax], *pns[kDiagMax][kDiagMax];  // [g][s]
+    uint64_t *re[kDiagMax], *im[kDiagMax];
+    size_t is, os;
+    int nb, ng;
+    uint32_t level, L, pk, B;
+};
+
+template <int NB>
+__global__ void __launch_bounds__(128) k_k3_gauss_mac(K3MacArgs a, KTables kt)
+{
+    extern __shared__ uint64_t sw[];  // [ng][3][nb][kDmTK]: C, S - C, C - NS (0 for absent)
+    const uint32_t L1 = a.level + 1;
+    const uint32_t pr = blockIdx.y;
+    const uint32_t prime = pr < L1 ? pr : a.L + 1 + (pr - L1);
+    const uint64_t q = kt.q[prime], qi = kt.qinv_neg[prime];
+    const uint32_t k0 = blockIdx.x * kDmTK;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nt = a.ng * a.nb;
+    for (int t = warp; t < nt; t += nw) {
+        const int g = t / a.nb, s = t % a.nb;
+        uint64_t c = 0, d = 0, e = 0;
+        if (a.pc[g][s]) {
+            const size_t o = (size_t)pr * kt.n + k0 + lane;
+            c = __ldg(a.pc[g][s] + o);
+            const uint64_t sv = __ldg(a.ps[g][s] + o), nv = __ldg(a.pns[g][s] + o);
+            d = sub_mod(sv, c, q);
+            e = sub_mod(c, nv, q);
+        }
+        uint64_t *dst = sw + ((size_t)(g * 3) * a.nb + s) * kDmTK + lane;
+        dst[0] = c;
+        dst[(size_t)a.nb * kDmTK] = d;
+        dst[(size_t)2 * a.nb * kDmTK] = e;
+    }
+    __syncthreads();
+    const size_t r0 = pr < L1 ? pr : 2 * L1 + (pr - L1);
+    const size_t pstride = pr < L1 ? L1 : a.pk;
+    for (uint32_t u = warp; u < 2 * a.B; u += nw) {
+        const uint32_t b = u >> 1, poly = u & 1;
+        const size_t off = (r0 + poly * pstride) * kt.n + k0 + lane;
+        uint64_t xr[NB], xi[NB];
+#pragma unroll
+        for (int s = 0; s < NB; ++s) {
+            xr[s] = s < a.nb ? a.xr[s][(size_t)b * a.is + off] : 0;
+            xi[s] = s < a.nb ? a.xi[s][(size_t)b * a.is + off] : 0;
+        }
+        const uint64_t *w = sw + lane;
+        for (int g = 0; g < a.ng; ++g, w += (size_t)3 * a.nb * kDmTK) {
+            U128 k1{0, 0}, k2{0, 0}, k3{0, 0};  // <= 16 terms < q^2 each: < q 2^64 for q < 2^60
+#pragma unroll
+            for (int s = 0; s < NB; ++s) {
+                if (s < a.nb) {
+                    mac128(k1, add_mod(xr[s], xi[s], q), w[s * kDmTK]);
+                    mac128(k2, xr[s], w[(a.nb + s) * kDmTK]);
+                    mac128(k3, xi[s], w[(2 * a.nb + s) * kDmTK]);
+                }
+            }
+            const uint64_t v1 = redc(k1, q, qi), v2 = redc(k2, q, qi), v3 = redc(k3, q, qi);
+            a.re[g][(size_t)b * a.os + off] = sub_mod(v1, v3, q);
+            a.im[g][(size_t)b * a.os + off] = add_mod(v1, v2, q);
+        }
     }
 }
 
@@ -986,8 +1067,8 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
     // algorithmic: babies read once, plaintexts once per launch, outputs written once
     ProfScope ps(c, "diag_mac", 8.0 * rows * c.n * (terms + B * 2.0 * (a.nc + a.no)), 2.0 * terms * rows * c.n * B);
     static const bool l2_variant = [] {
-        const char *e = getenv("MMFHE_DIAG_L2");
-        return e && *e == '1';
+        const char *e = getenv("MMFHE_DIAG_STAGED");
+        return !(e && *e == '1');
     }();
     if (l2_variant) {
         const dim3 g(((c.n + 255) / 256) * B, 2 * (level + 1 + pk));
@@ -1015,6 +1096,56 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
         k_diag_mac<8><<<g, 128, smem, c.stream>>>(a, c.kt);
     else
         k_diag_mac<16><<<g, 128, smem, c.stream>>>(a, c.kt);
+    LAUNCH_CHECK(c);
+}
+
+void launch_k3_gauss_mac(Ctx &c, const std::vector<const uint64_t *> &xr, const std::vector<const uint64_t *> &xi,
+                         size_t is, const std::vector<std::vector<const uint64_t *>> &pc,
+                         const std::vector<std::vector<const uint64_t *>> &ps,
+                         const std::vector<std::vector<const uint64_t *>> &pns, const std::vector<uint64_t *> &re,
+                         const std::vector<uint64_t *> &im, size_t os, uint32_t level, uint32_t B, uint32_t pk)
+{
+    const int nb = (int)xr.size(), ng = (int)re.size();
+    MMFHE_REQUIRE(nb <= kDiagMax && ng <= kDiagMax && xi.size() == xr.size() && im.size() == re.size(),
+                  MMFHE_E_LAYOUT, "K3 MAC shape");
+    K3MacArgs a{};
+    a.nb = nb;
+    a.ng = ng;
+    a.is = is;
+    a.os = os;
+    a.level = level;
+    a.L = c.L;
+    a.pk = pk;
+    a.B = B;
+    double terms = 0;
+    for (int s = 0; s < nb; ++s) {
+        a.xr[s] = xr[s];
+        a.xi[s] = xi[s];
+    }
+    for (int g = 0; g < ng; ++g) {
+        a.re[g] = re[g];
+        a.im[g] = im[g];
+        for (int s = 0; s < nb; ++s) {
+            a.pc[g][s] = pc[g][s];
+            a.ps[g][s] = ps[g][s];
+            a.pns[g][s] = pns[g][s];
+            terms += pc[g][s] != nullptr;
+        }
+    }
+    const double rows = level + 1 + pk;
+    ProfScope ps_(c, "diag_mac", 8.0 * rows * c.n * (3 * terms + B * 2.0 * 2 * (nb + ng)), 2.0 * 3 * terms * rows * c.n * B);
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, [] {
+        const int mx = (int)(sizeof(uint64_t) * 3 * kDiagMax * kDiagMax * kDmTK);
+        CUDA_CHECK(cudaFuncSetAttribute(k_k3_gauss_mac<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        CUDA_CHECK(cudaFuncSetAttribute(k_k3_gauss_mac<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    });
+    const size_t smem = sizeof(uint64_t) * 3 * (size_t)ng * nb * kDmTK;
+    const dim3 g(c.n / kDmTK, level + 1 + pk);
+    if (nb <= 8)
+        k_k3_gauss_mac<8><<<g, 128, smem, c.stream>>>(a, c.kt);
+    else
+        k_k3_gauss_mac<16><<<g, 128, smem, c.stream>>>(a, c.kt);
     LAUNCH_CHECK(c);
 }
 
