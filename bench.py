@@ -59,7 +59,8 @@ def c4_config(lanes=LANES, level=19, F=100):
     P = ps4()
     # frame_batch counts ciphertext pairs: all 13 packed pairs in one batch (lanes 8), or
     # batches of 25 frames in the canonical layout (bounds the hoisted babies' memory)
-    return P, dict(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=FC_DIMS, hoist=1, lanes=lanes, level=level,
+    # hoist = 2: double-hoisted BSGS in K3 and the FC head (DESIGN R22)
+    return P, dict(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=FC_DIMS, hoist=2, lanes=lanes, level=level,
                    frame_batch=0 if lanes > 1 else 25)
 
 
@@ -85,6 +86,9 @@ def c4_bench_config(world, cfg):
             "packing": (f"SIMD-dense: {L} frames interleaved per ciphertext (lanes = {L}, DESIGN R20), "
                         f"{n_pairs(cfg)} ciphertext pairs per session" if L > 1 else
                         "one frame per ciphertext (the paper's layout, P:741)"),
+            "bsgs": ("double-hoisted (hoist = 2, DESIGN R22): PQ baby steps, PQ-encoded diagonals (K3 by Gauss's "
+                     "three-product form), PQ giant steps, one ModDown per output" if cfg["hoist"] == 2 else
+                     "hoisted baby steps (hoist = 1)"),
             "sessions_per_step_per_gpu": 1, "parallelism": f"session-sharded x{world}",
             "l2": f"inputs larger than L2 ({2 * n_pairs(cfg) * 20} MiB of ciphertexts per step, L2 126 MB)",
             "inputs": "coefficient form, device-resident; import NTT and export INTT inside the step"}
@@ -299,6 +303,10 @@ def run_gpu(args, rank, world, device):
     extras = {}
     if not args.no_extras:
         extras = extras_n16(args, m, torch, device)
+        try:
+            extras["client"] = extras_client(m, torch, device)
+        except Exception as e:  # report, do not hide
+            extras["client"] = {"error": f"{type(e).__name__}: {e}"}
         for wl in ("C4_canonical", "C4_l11", "C2", "C1", "C3", "C5v", "C5v_t3", "Vpaper"):
             try:
                 extras[wl] = bench_workload(wl, m, torch, device)
@@ -598,6 +606,40 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
                        f"per step at PS4 (N=2^16), one shared key set; device-resident inputs cycle a pool of {pool} "
                        f"distinct sessions per type; h2d_included uploads every session from pinned host memory "
                        f"inside the timed region (copy-stream waves)")}
+
+
+def extras_client(m, torch, device, batch=64, reps=3):
+    """The trusted client on the GPU (DESIGN R26): mmfhe_client_encrypt of a batch
+    of coefficient-form plaintexts under a GPU-generated public key, at the paper's vital
+    parameters (PSV, level 10) and at PS4 (level 19).  Paper: 33 ms per ciphertext on one
+    Ryzen 9 5950X core."""
+    from synth.params import psv, ps4
+    out = {}
+    for name, P, lvl in (("PSV", psv(), 10), ("PS4", ps4(), 19)):
+        ctx = m.Context.from_params(P, device=device.index or 0, stream=torch.cuda.current_stream(device).cuda_stream)
+        pk = torch.empty((2, P.L + 1, P.n), dtype=torch.int64, device=device)
+        t0 = time.perf_counter()
+        ctx.client_keygen(5, steps=(), relin=False, pk=pk)
+        kg = time.perf_counter() - t0
+        gen = torch.Generator(device=device)
+        gen.manual_seed(6)
+        pts = uniform_dev(torch, gen, (batch, 1, lvl + 1), list(P.q[: lvl + 1]), P.n, device)
+        pa = [m.Ct(pts[i], lvl, float(2 ** P.scale_bits), P.n // 2, P.log_n, m.FORM_COEFF, 1) for i in range(batch)]
+        ob = torch.empty((batch, 2, lvl + 1, P.n), dtype=torch.int64, device=device)
+        oa = [m.Ct(ob[i], lvl, 0.0, 0, P.log_n) for i in range(batch)]
+        ctx.client_encrypt(pk, pa, 7, 0, oa)
+        torch.cuda.synchronize(device)
+        t0 = time.perf_counter()
+        for r in range(reps):
+            ctx.client_encrypt(pk, pa, 7, batch * (r + 1), oa)
+        torch.cuda.synchronize(device)
+        us = (time.perf_counter() - t0) / (reps * batch) * 1e6
+        out[name] = {"encrypt_us_per_ct": us, "cts_per_s": 1e6 / us, "pk_keygen_s": kg,
+                     "config": f"N=2^{P.log_n}, level {lvl}, batch {batch}, device-resident plaintexts and outputs, "
+                               f"host wall clock"}
+        ctx.close()
+    out["paper"] = "33 ms per ciphertext on one CPU core (P:1385-1387)"
+    return out
 
 
 def extras_n16(args, m, torch, device, batch=8, reps=3):
