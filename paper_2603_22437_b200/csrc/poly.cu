@@ -252,18 +252,13 @@ __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uin
     uint64_t *o = isq ? accQ + (size_t)r * kt.n + k : accP + (size_t)(r - a.level - 1) * kt.n + k;
     const size_t ostride = isq ? a.oqs : a.ops;
     const size_t opoly = isq ? a.oqp : a.opp;
-    // software-pipelined over the batch items: item b+1's digit words are loaded while item b
-    // multiplies (the loop is otherwise one exposed load latency per item)
-    uint64_t s[DMAX];
-#pragma unroll
-    for (int j = 0; j < DMAX; ++j)
-        if (j < (int)a.dnum && b0 < b1) s[j] = src[j][(size_t)b0 * sstr[j]];
+    // (a software-pipelined variant loading item b+1's digit words during item b's MACs measured
+    // slower on C4: 72 registers, 3 CTAs/SM, 9.96 -> 10.44 ms/step)
     for (uint32_t b = b0; b < b1; ++b) {
-        uint64_t sn[DMAX];
-        const bool more = b + 1 < b1;
+        uint64_t s[DMAX];
 #pragma unroll
         for (int j = 0; j < DMAX; ++j)
-            if (j < (int)a.dnum && more) sn[j] = src[j][(size_t)(b + 1) * sstr[j]];
+            if (j < (int)a.dnum) s[j] = src[j][(size_t)b * sstr[j]];
         U128 acc0{0, 0}, acc1{0, 0};
 #pragma unroll
         for (int j = 0; j < DMAX; ++j) {
@@ -274,8 +269,6 @@ __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uin
         }
         o[(size_t)b * ostride] = redc(acc0, q, qi);
         o[(size_t)b * ostride + opoly] = redc(acc1, q, qi);
-#pragma unroll
-        for (int j = 0; j < DMAX; ++j) s[j] = sn[j];
     }
 }
 
@@ -621,36 +614,14 @@ __global__ void __launch_bounds__(128) k_k3_gauss_mac(K3MacArgs a, KTables kt)
     __syncthreads();
     const size_t r0 = pr < L1 ? pr : 2 * L1 + (pr - L1);
     const size_t pstride = pr < L1 ? L1 : a.pk;
-    // units (item, poly) over the warps, software-pipelined: the next unit's baby words are
-    // loaded while this unit multiplies (the kernel is otherwise load-latency bound)
-    auto uoff = [&](uint32_t u) {
-        return (size_t)(u >> 1) * a.is + (r0 + (u & 1) * pstride) * kt.n + k0 + lane;
-    };
-    uint64_t nr[NB], ni[NB];
-    if ((uint32_t)warp < 2 * a.B) {
-        const size_t o0 = uoff(warp);
-#pragma unroll
-        for (int s = 0; s < NB; ++s) {
-            nr[s] = s < a.nb ? a.xr[s][o0] : 0;
-            ni[s] = s < a.nb ? a.xi[s][o0] : 0;
-        }
-    }
     for (uint32_t u = warp; u < 2 * a.B; u += nw) {
         const uint32_t b = u >> 1, poly = u & 1;
         const size_t off = (r0 + poly * pstride) * kt.n + k0 + lane;
         uint64_t xr[NB], xi[NB];
 #pragma unroll
         for (int s = 0; s < NB; ++s) {
-            xr[s] = nr[s];
-            xi[s] = ni[s];
-        }
-        if (u + nw < 2 * a.B) {
-            const size_t on = uoff(u + nw);
-#pragma unroll
-            for (int s = 0; s < NB; ++s) {
-                nr[s] = s < a.nb ? a.xr[s][on] : 0;
-                ni[s] = s < a.nb ? a.xi[s][on] : 0;
-            }
+            xr[s] = s < a.nb ? a.xr[s][(size_t)b * a.is + off] : 0;
+            xi[s] = s < a.nb ? a.xi[s][(size_t)b * a.is + off] : 0;
         }
         const uint64_t *w = sw + lane;
         for (int g = 0; g < a.ng; ++g, w += (size_t)3 * a.nb * kDmTK) {
