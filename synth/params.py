@@ -134,6 +134,12 @@ def ps4() -> ParamSet:  # C4/C5: N=2^16, Q=(60, 19x50), P=7x60, alpha=7 (dnum 3)
     return make_params(16, 20, 50, 7, 7, name="PS4")
 
 
+def ps4d2() -> ParamSet:
+    """PS4 with dnum 2 (SURVEY §8(d) lever 3): N=2^16, the same 20 Q limbs, alpha 10 and
+    K = 10 special primes of 60 bits; log2 PQ ~ 1610 <= 1772 (128-bit, N = 2^16)."""
+    return make_params(16, 20, 50, 10, 10, name="PS4d2")
+
+
 def psv() -> ParamSet:
     """The paper's vital column: N=2^15, 11 Q limbs (60 + 10x40,
     the 5.5 MB ciphertext of P:1405), dnum 3 (the 22.5 MiB relinearisation key of P:1412:
@@ -148,4 +154,4 @@ def toy(log_n: int = 10, n_q: int = 6, scale_bits: int = 40, n_p: int = 2,
     return make_params(log_n, n_q, scale_bits, n_p, alpha, name=f"toy{log_n}")
 
 
-PARAM_SETS = {"PS1": ps1, "PS2": ps2, "PS3": ps3, "PS4": ps4, "PSV": psv}
+PARAM_SETS = {"PS1": ps1, "PS2": ps2, "PS3": ps3, "PS4": ps4, "PS4d2": ps4d2, "PSV": psv}

@@ -12,7 +12,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2603_22437_b200 import mmfhe as m  # noqa: E402
 from synth import radar  # noqa: E402
-from synth.params import ps4  # noqa: E402
+from synth.params import PARAM_SETS  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--frames", type=int, default=25)
@@ -20,10 +20,11 @@ ap.add_argument("--steps", type=int, default=1)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--lanes", type=int, default=1)
 ap.add_argument("--hoist", type=int, default=1)
+ap.add_argument("--params", default="PS4")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
-P = ps4()
+P = PARAM_SETS[args.params]()
 F = args.frames
 stream = torch.cuda.current_stream(dev)
 cfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8),
