@@ -294,20 +294,20 @@ class Runner {
         std::vector<DCt> inner = gauss && s.b <= (uint32_t)kDiagMax && s.giants.size() <= (size_t)kDiagMax
                                      ? ev_k3_mac(c_, pr, pi, PC, PS, PN)
                                      : ev_diag_mac(c_, cts, rows);
+        // per giant: rotate + accumulate d_re, then d_im (oracle k3_giant_steps' order); double
+        // hoisting fuses the accumulation into the giant step's inner product
         DCt out_re, out_im;
-        bool first = true;
         for (size_t gi = 0; gi < s.giants.size(); ++gi) {
-            const auto &g = s.giants[gi];
-            const int32_t step = g.G * (int32_t)L();
-            DCt ir = dh() ? ev_rotate_pq(c_, inner[2 * gi], step) : ev_rotate(c_, inner[2 * gi], step);
-            DCt ii = dh() ? ev_rotate_pq(c_, inner[2 * gi + 1], step) : ev_rotate(c_, inner[2 * gi + 1], step);
-            if (first) {
-                out_re = std::move(ir);
-                out_im = std::move(ii);
-                first = false;
+            const int32_t step = s.giants[gi].G * (int32_t)L();
+            if (gi == 0) {
+                out_re = dh() ? ev_rotate_pq(c_, inner[0], step) : ev_rotate(c_, inner[0], step);
+                out_im = dh() ? ev_rotate_pq(c_, inner[1], step) : ev_rotate(c_, inner[1], step);
+            } else if (dh()) {
+                ev_rotate_pq_acc(c_, out_re, inner[2 * gi], step);
+                ev_rotate_pq_acc(c_, out_im, inner[2 * gi + 1], step);
             } else {
-                out_re = ev_addsub(c_, out_re, ir, false);
-                out_im = ev_addsub(c_, out_im, ii, false);
+                out_re = ev_addsub(c_, out_re, ev_rotate(c_, inner[2 * gi], step), false);
+                out_im = ev_addsub(c_, out_im, ev_rotate(c_, inner[2 * gi + 1], step), false);
             }
         }
         if (dh()) {  // one ModDown per output ends the double-hoisted giant sum
@@ -393,20 +393,16 @@ class Runner {
         }
         std::vector<DCt> inners = ev_diag_mac(c_, cts, rows);
         DCt acc;
-        bool first = true;
         for (size_t gi = 0; gi < s.giants.size(); ++gi) {
             const auto &g = s.giants[gi];
+            const int32_t step = g.G * (int32_t)L();
+            if (gi > 0 && dh() && g.G) {  // rotate + accumulate, fused
+                ev_rotate_pq_acc(c_, acc, inners[gi], step);
+                continue;
+            }
             DCt inner = std::move(inners[gi]);
-            if (g.G) {
-                const int32_t step = g.G * (int32_t)L();
-                inner = dh() ? ev_rotate_pq(c_, inner, step) : ev_rotate(c_, inner, step);
-            }
-            if (first) {
-                acc = std::move(inner);
-                first = false;
-            } else {
-                acc = ev_addsub(c_, acc, inner, false);
-            }
+            if (g.G) inner = dh() ? ev_rotate_pq(c_, inner, step) : ev_rotate(c_, inner, step);
+            acc = gi == 0 ? std::move(inner) : ev_addsub(c_, acc, inner, false);
         }
         if (dh()) acc = ev_moddown_ct(c_, acc);
         DCt z = ev_rescale(c_, acc);

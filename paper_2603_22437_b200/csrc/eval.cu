@@ -880,15 +880,41 @@ std::vector<DCt> ev_rotate_hoisted_pq(Ctx &c, const DCt &a, const std::vector<in
         rec_n(c, "hrot_hoisted_pq", l, B, std::to_string(k));
         DCt r = make_pq(c, l, a.n_slots, a.scale, B);
         const IPOut os{r.item_words(), r.poly_words(), r.item_words(), (size_t)c.K * c.n};
+        // (P sigma_g(c0) + IP0, IP1): the P lift of sigma_g(c0) is the inner product's fused
+        // poly-0 addend on the Q rows (none on the P rows: P = 0 mod p_k)
+        IPEpi ep;
+        ep.add = a.data();
+        ep.pmod = (const TwPair *)c.bconv_ptr(c.off_pd_pmod);
+        ep.as = a.item_words();
+        ep.ag = g;
         launch_key_ip(c, r.data(), r.ppoly(0), a.poly(1), a.item_words(), m.y.get(), m.T * c.n, m.off, key.buf.get(),
-                      l, B, g, g, &os);
-        // (P sigma_g(c0) + IP0, IP1): the P lift of sigma_g(c0) into poly 0's Q rows
-        launch_pq_lift(c, r.data(), r.item_words(), r.poly_words(), a.data(), a.item_words(), a.poly_words(), l, 1, B,
-                       g, true);
+                      l, B, g, g, &os, &ep);
         out.push_back(std::move(r));
     }
     return out;
 }
+
+namespace {
+// the PQ giant step into `r` (fresh, or += with accumulate): ModDown(a1), sigma_g, ModUp, key
+// inner product whose fused epilogue adds sigma_g(a0) over Q_l u P (and r's old contents)
+void rotate_pq_into(Ctx &c, const DCt &a, uint32_t g, const DKey &key, DCt &r, bool accumulate)
+{
+    const uint32_t l = a.level, B = a.batch;
+    const size_t lw = (size_t)(l + 1) * c.n;
+    DBuf a1(lw * B, c.stream);
+    moddown(c, a.poly(1), a.item_words(), 0, a.ppoly(1), a.item_words(), l, B, 1, a1.get(), lw, 0);
+    ModUpOut m = ks_modup(c, a1.get(), lw, l, B, g);
+    const IPOut os{r.item_words(), r.poly_words(), r.item_words(), (size_t)c.K * c.n};
+    IPEpi ep;
+    ep.add = a.data();
+    ep.as = a.item_words();
+    ep.apbase = (size_t)2 * (l + 1) * c.n;  // a0's P rows: the PQ item layout's P part, poly 0
+    ep.ag = g;
+    ep.accumulate = accumulate ? 1 : 0;
+    launch_key_ip(c, r.data(), r.ppoly(0), a1.get(), lw, m.y.get(), m.T * c.n, m.off, key.buf.get(), l, B, g, 1, &os,
+                  &ep);
+}
+}  // namespace
 
 DCt ev_rotate_pq(Ctx &c, const DCt &a, int32_t step)
 {
@@ -903,15 +929,26 @@ DCt ev_rotate_pq(Ctx &c, const DCt &a, int32_t step)
     }
     const DKey &key = find_gk(c, k);
     rec_n(c, "hrot_pq", l, B, std::to_string(k));
-    // a1' = ModDown(a1) to Q_l (NTT form), then the rotation's key switch without ModDown
-    const size_t lw = (size_t)(l + 1) * c.n;
-    DBuf a1(lw * B, c.stream);
-    moddown(c, a.poly(1), a.item_words(), 0, a.ppoly(1), a.item_words(), l, B, 1, a1.get(), lw, 0);
-    ModUpOut m = ks_modup(c, a1.get(), lw, l, B, g);
-    const IPOut os{r.item_words(), r.poly_words(), r.item_words(), (size_t)c.K * c.n};
-    launch_key_ip(c, r.data(), r.ppoly(0), a1.get(), lw, m.y.get(), m.T * c.n, m.off, key.buf.get(), l, B, g, 1, &os);
-    launch_pq_add_perm(c, r.data(), a.data(), a.item_words(), l, B, g);
+    rotate_pq_into(c, a, g, key, r, false);
     return r;
+}
+
+void ev_rotate_pq_acc(Ctx &c, DCt &acc, const DCt &a, int32_t step)
+{
+    MMFHE_REQUIRE(a.pk == c.K && acc.pk == c.K && a.npolys == 2 && a.level == acc.level && a.batch == acc.batch,
+                  MMFHE_E_LAYOUT, "PQ rotate-accumulate needs PQ ciphertexts of one shape");
+    MMFHE_REQUIRE(a.scale == acc.scale, MMFHE_E_SCALE, "hadd scale mismatch");
+    int32_t k;
+    const uint32_t g = (uint32_t)galois_element(c, step, &k);
+    if (k == 0) {
+        DCt s = ev_addsub(c, acc, a, false);
+        acc = std::move(s);
+        return;
+    }
+    const DKey &key = find_gk(c, k);
+    rec_n(c, "hrot_pq", a.level, a.batch, std::to_string(k));
+    rec_n(c, "hadd_pq", a.level, a.batch);
+    rotate_pq_into(c, a, g, key, acc, true);
 }
 
 DCt ev_moddown_ct(Ctx &c, const DCt &a)

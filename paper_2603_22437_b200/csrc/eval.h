@@ -73,6 +73,9 @@ DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride);
 DCt ev_lift_pq(Ctx &c, const DCt &a);                                                    // (P c0, P c1)
 std::vector<DCt> ev_rotate_hoisted_pq(Ctx &c, const DCt &a, const std::vector<int32_t> &steps);  // no ModDown
 DCt ev_rotate_pq(Ctx &c, const DCt &a, int32_t step);  // ModDown(a1), sigma_g, key switch kept over Q_l u P
+// acc += ev_rotate_pq(a, step), fused (the inner product accumulates into acc); records
+// "hrot_pq" then "hadd_pq" per item
+void ev_rotate_pq_acc(Ctx &c, DCt &acc, const DCt &a, int32_t step);
 DCt ev_moddown_ct(Ctx &c, const DCt &a);               // both polys back to Q_l
 
 // composites

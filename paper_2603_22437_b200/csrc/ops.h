@@ -34,9 +34,19 @@ void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, 
 struct IPOut {
     size_t qs, qp, ps, pp;
 };
+// ep: fused epilogue (double hoisting): poly 0 += add (item stride as, Q rows at r N, P rows at
+// apbase + k N or none if apbase == ~0), read through sigma_ag, Q-row addends times [P]_{q_r}
+// when pmod is set; with accumulate, both polys += the output's previous contents.
+struct IPEpi {
+    const uint64_t *add = nullptr;
+    const TwPair *pmod = nullptr;
+    size_t as = 0, apbase = ~(size_t)0;
+    uint32_t ag = 1;
+    int accumulate = 0;
+};
 void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, size_t xs, const uint64_t *y,
                    size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B,
-                   uint32_t gx = 1, uint32_t gy = 1, const IPOut *os = nullptr);
+                   uint32_t gx = 1, uint32_t gy = 1, const IPOut *os = nullptr, const IPEpi *ep = nullptr);
 // w [B*npoly][l+1][N] = BConv_{P->Q}(zP [B*npoly][K][N]) (coefficient form).
 void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B, uint32_t npoly = 2);
 // double hoisting: Q rows of out (+)= [P]_{q_i} sigma_g(src) for npoly polys per

@@ -145,7 +145,33 @@ struct IPArgs {
     size_t oqs, oqp, ops, opp;  // output item / poly strides of the Q rows (accQ) and P rows (accP)
     uint32_t dnum, level, L, K, B, per_z;
     uint32_t gx, gy;  // sigma_g applied on the fly to the x / y reads (1 = none)
+    IPEpi ep;         // fused output epilogue (double hoisting): poly-0 addend, accumulation
 };
+
+// The key inner product's output epilogue: poly 0 += the addend (read through sigma_ag; on Q
+// rows optionally times [P]_{q_r}: the P lift of a hoisted baby step; on P rows only when the
+// addend has them), and with accumulate both polys += the previous output contents.
+__device__ __forceinline__ void ip_store(uint64_t *o, size_t opoly, uint64_t v0, uint64_t v1, const IPEpi &e,
+                                         size_t b, uint32_t r, uint32_t level, uint32_t n, uint32_t kadd, uint64_t q,
+                                         const TwPair *pm)
+{
+    if (e.add) {
+        const bool isq = r <= level;
+        if (isq) {
+            uint64_t s = e.add[b * e.as + (size_t)r * n + kadd];
+            if (pm) s = shoup(s, pm->w, pm->wp, q);
+            v0 = add_mod(v0, s, q);
+        } else if (e.apbase != ~(size_t)0) {
+            v0 = add_mod(v0, e.add[b * e.as + e.apbase + (size_t)(r - level - 1) * n + kadd], q);
+        }
+    }
+    if (e.accumulate) {
+        v0 = add_mod(v0, o[0], q);
+        v1 = add_mod(v1, o[opoly], q);
+    }
+    o[0] = v0;
+    o[opoly] = v1;
+}
 
 // Key inner product (see k_key_ip below for the formula).
 // Low-register variant for 5..8 digits: 32-bit in-item source offsets instead of
@@ -159,7 +185,7 @@ struct IPArgs {
 // items per loop iteration (both items' source loads in flight before the MACs) spills
 // 396 B at 3 CTAs/SM (C2 5194 -> 5000 frames/s) and at 2 CTAs/SM (no spills) is 0.6%
 // slower (5165): the kernel already has enough loads in flight at 3 CTAs/SM.
-template <int DMAX>
+template <int DMAX, bool EPI = false>
 __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
                                                 const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
                                                 const uint64_t *__restrict__ key, KTables kt, IPArgs a)
@@ -195,6 +221,8 @@ __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ acc
     uint64_t *o = isq ? accQ + (size_t)r * kt.n + k : accP + (size_t)(r - a.level - 1) * kt.n + k;
     const size_t ostride = isq ? a.oqs : a.ops;
     const size_t opoly = isq ? a.oqp : a.opp;
+    const uint32_t kadd = EPI && a.ep.add ? galois_perm(k, a.ep.ag, kt.log_n) : 0;
+    const TwPair *pmq = (EPI && a.ep.pmod && isq) ? a.ep.pmod + r : nullptr;
     for (uint32_t b = b0; b < b1; ++b) {
         const uint64_t *xb = x + (size_t)b * a.xs, *yb = y + (size_t)b * a.ys;
         uint64_t s[DMAX];
@@ -209,15 +237,20 @@ __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ acc
                 mac128(acc1, s[j], ka[j]);
             }
         }
-        o[(size_t)b * ostride] = redc(acc0, q, qi);
-        o[(size_t)b * ostride + opoly] = redc(acc1, q, qi);
+        if (EPI) {
+            ip_store(o + (size_t)b * ostride, opoly, redc(acc0, q, qi), redc(acc1, q, qi), a.ep, b, r, a.level, kt.n,
+                     kadd, q, pmq);
+        } else {
+            o[(size_t)b * ostride] = redc(acc0, q, qi);
+            o[(size_t)b * ostride + opoly] = redc(acc1, q, qi);
+        }
     }
 }
 
 // For every batch item b: (accQ|accP)_{b,p}[r] = sum_j src_{b,j}[r] (.) evk_j[p][r] with
 // src = x_b[r] for r in I_j, else the ModUp'd row.  The 2*dnum key words of (r, k) are
 // loaded once per thread and reused for its per_z items (grid.z splits the batch).
-template <int DMAX>
+template <int DMAX, bool EPI = false>
 __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
                                                 const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
                                                 const uint64_t *__restrict__ key, KTables kt, IPArgs a)
@@ -252,6 +285,8 @@ __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uin
     uint64_t *o = isq ? accQ + (size_t)r * kt.n + k : accP + (size_t)(r - a.level - 1) * kt.n + k;
     const size_t ostride = isq ? a.oqs : a.ops;
     const size_t opoly = isq ? a.oqp : a.opp;
+    const uint32_t kadd = EPI && a.ep.add ? galois_perm(k, a.ep.ag, kt.log_n) : 0;
+    const TwPair *pmq = (EPI && a.ep.pmod && isq) ? a.ep.pmod + r : nullptr;
     // (a software-pipelined variant loading item b+1's digit words during item b's MACs measured
     // slower on C4: 72 registers, 3 CTAs/SM, 9.96 -> 10.44 ms/step)
     for (uint32_t b = b0; b < b1; ++b) {
@@ -267,8 +302,13 @@ __global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uin
                 mac128(acc1, s[j], ka[j]);
             }
         }
-        o[(size_t)b * ostride] = redc(acc0, q, qi);
-        o[(size_t)b * ostride + opoly] = redc(acc1, q, qi);
+        if (EPI) {
+            ip_store(o + (size_t)b * ostride, opoly, redc(acc0, q, qi), redc(acc1, q, qi), a.ep, b, r, a.level, kt.n,
+                     kadd, q, pmq);
+        } else {
+            o[(size_t)b * ostride] = redc(acc0, q, qi);
+            o[(size_t)b * ostride + opoly] = redc(acc1, q, qi);
+        }
     }
 }
 
@@ -937,10 +977,11 @@ void launch_modup_bconv(Ctx &c, uint64_t *y, size_t ys, const uint64_t *x_coef, 
 
 void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, size_t xs, const uint64_t *y,
                    size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B,
-                   uint32_t gx, uint32_t gy, const IPOut *os)
+                   uint32_t gx, uint32_t gy, const IPOut *os, const IPEpi *ep)
 {
     const auto &plans = c.modup[level];
     IPArgs a{};
+    if (ep) a.ep = *ep;
     if (os) {
         a.oqs = os->qs;
         a.oqp = os->qp;
@@ -975,7 +1016,14 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
     a.per_z = (B + nz - 1) / nz;
     nz = (B + a.per_z - 1) / a.per_z;
     const dim3 g = grid3(c.n, level + 1 + c.K, nz);
-    if (a.dnum <= 4)
+    if (ep) {  // the fused-epilogue instantiations (double hoisting) carry its registers alone
+        if (a.dnum <= 4)
+            k_key_ip<4, true><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
+        else if (a.dnum <= 8)
+            k_key_ip_lr<8, true><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
+        else
+            k_key_ip<16, true><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
+    } else if (a.dnum <= 4)
         k_key_ip<4><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
     else if (a.dnum <= 8)
         k_key_ip_lr<8><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
