@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ acc
 // src = x_b[r] for r in I_j, else the ModUp'd row.  The 2*dnum key words of (r, k) are
 // loaded once per thread and reused for its per_z items (grid.z splits the batch).
 template <int DMAX, bool EPI = false>
-__global__ void __launch_bounds__(kTB) k_key_ip(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
+__global__ void __launch_bounds__(kTB, DMAX <= 4 ? 4 : 1) k_key_ip(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
                                                 const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
                                                 const uint64_t *__restrict__ key, KTables kt, IPArgs a)
 {
