@@ -698,7 +698,12 @@ void ntt_forward(Ctx &c, uint64_t *d, uint32_t rows, const PrimeMap &pm, const C
                                           (epi->add2 ? 0.5 : 0.0));
         MMFHE_REQUIRE(!epi || (epi->per >= 1 && rows % ((epi->npoly ? epi->npoly : 2) * epi->per) == 0),
                       MMFHE_E_LAYOUT, "NTT epilogue rows");
-        ProfScope ps(c, epi ? "ntt_fwd_row_epi" : "ntt_fwd_row", bytes + ebytes, 0.5 * rows * c.n * L2);
+        // ops: the pass's butterflies, plus (epilogue) the final step's Shoup product by P^{-1} or
+        // q_l^{-1} per word -- SURVEY §8(d)'s "2L'N [x P^{-1}]" modmuls -- counted as one
+        // butterfly-equivalent each (the microbenchmark's Shoup modmul and CT butterfly rates
+        // agree within 2%)
+        ProfScope ps(c, epi ? "ntt_fwd_row_epi" : "ntt_fwd_row", bytes + ebytes,
+                     0.5 * rows * c.n * L2 + (epi ? 1.0 * rows * c.n : 0.0));
         launch_pass<true, false>(c.log_n, d, rows, c.kt, pm, nullptr, nullptr, epi, c.stream);
     }
     c.launches += 2;
