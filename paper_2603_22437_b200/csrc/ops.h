@@ -50,12 +50,10 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
 // w [B*npoly][l+1][N] = BConv_{P->Q}(zP [B*npoly][K][N]) (coefficient form).
 void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B, uint32_t npoly = 2);
 // double hoisting: Q rows of out (+)= [P]_{q_i} sigma_g(src) for npoly polys per
-// item (out / src item strides os / ss, poly strides ops / sps); and poly 0 of a PQ ciphertext
-// out (+)= sigma_g(poly 0 of src) over Q_l u P (item stride is, PQ item layout).
+// item (out / src item strides os / ss, poly strides ops / sps): the identity baby step's P lift
+// (the other PQ addends are the key inner product's fused epilogue, IPEpi)
 void launch_pq_lift(Ctx &c, uint64_t *out, size_t os, size_t ops, const uint64_t *src, size_t ss, size_t sps,
                     uint32_t level, uint32_t npoly, uint32_t B, uint32_t g, bool accumulate);
-void launch_pq_add_perm(Ctx &c, uint64_t *out, const uint64_t *src, size_t is, uint32_t level, uint32_t B,
-                        uint32_t g);
 // (ModDown's final step (accQ - w) P^{-1} + addends and the rescale's (a_i - v_i) q_l^{-1}
 // run as the epilogue of the forward NTT's row pass: ntt_forward(..., RowEpi).)
 

@@ -896,20 +896,6 @@ __global__ void k_pq_lift(uint64_t *__restrict__ out, size_t os, size_t ops, con
     *o = accumulate ? add_mod(*o, v, q) : v;
 }
 
-// PQ giant step's addend: poly 0 of out (+)= sigma_g(poly 0 of src) over Q_l u P, both PQ
-// ciphertexts ([2][l+1] Q rows then [2][K] P rows per item).
-__global__ void k_pq_add_perm(uint64_t *__restrict__ out, const uint64_t *__restrict__ src, size_t is, KTables kt,
-                              uint32_t l1, uint32_t L, uint32_t g)
-{
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= kt.n) return;
-    const uint32_t r = blockIdx.y;  // 0..l: q_r (Q part, poly 0), l+1..: p_{r-l-1} (P part, poly 0)
-    const size_t off = r < l1 ? (size_t)r * kt.n : (size_t)(2 * l1 + (r - l1)) * kt.n;
-    const uint64_t q = kt.q[r < l1 ? r : L + 1 + (r - l1)];
-    const size_t b = (size_t)blockIdx.z * is;
-    out[b + off + k] = add_mod(out[b + off + k], src[b + off + galois_perm(k, g, kt.log_n)], q);
-}
-
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -1270,13 +1256,6 @@ void launch_pq_lift(Ctx &c, uint64_t *out, size_t os, size_t ops, const uint64_t
     ProfScope ps(c, "pq_lift", 8.0 * npoly * (level + 1) * c.n * B * (accumulate ? 3.0 : 2.0));
     k_pq_lift<<<grid3(c.n, npoly * (level + 1), B), kTB, 0, c.stream>>>(
         out, os, ops, src, ss, sps, (const TwPair *)c.bconv_ptr(c.off_pd_pmod), c.kt, level + 1, g, accumulate ? 1 : 0);
-    LAUNCH_CHECK(c);
-}
-
-void launch_pq_add_perm(Ctx &c, uint64_t *out, const uint64_t *src, size_t is, uint32_t level, uint32_t B, uint32_t g)
-{
-    ProfScope ps(c, "pq_add_perm", 24.0 * (level + 1 + c.K) * c.n * B);
-    k_pq_add_perm<<<grid3(c.n, level + 1 + c.K, B), kTB, 0, c.stream>>>(out, src, is, c.kt, level + 1, c.L, g);
     LAUNCH_CHECK(c);
 }
 
