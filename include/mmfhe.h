@@ -138,6 +138,7 @@ typedef struct {
                               head, logits sit in slots L*c.  Inputs: ceil(F/L) ciphertext pairs
                               (n_slots = L*n; unused lanes of the last pair zero); frame_batch then
                               counts ciphertext pairs.  L a power of two with L*n <= N/2 (E_SHAPE) */
+    uint32_t fc_baby;      /* FC layers' BSGS baby steps b: min(fc_baby, h) (0: ceil(sqrt(h))) */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */

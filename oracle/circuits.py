@@ -58,6 +58,7 @@ class ChainCfg:
     iq_pack: int = 0            # K4: k >= 1 -> packed rotate-and-sum over 2^k vectors (reading R19)
     n_taps: tuple = ()          # k5_fir_rot: taps per band (rotation keys for the longest)
     lanes: int = 1              # gesture / K3: frames interleaved per ciphertext (reading R20)
+    fc_baby: int = 0            # FC BSGS baby steps (0: ceil(sqrt(h)))
 
 
 def log2_exact(x: int, name: str) -> int:
@@ -495,20 +496,21 @@ def fc_diagonal(W: np.ndarray, n_in: int, i: int) -> np.ndarray:
     return W[j % h, (j + i) % n_in]
 
 
-def fc_schedule(h: int):
-    b = ceil_sqrt(h)
+def fc_schedule(h: int, fc_baby: int = 0):
+    """BSGS split of an FC layer's h diagonals: b = min(fc_baby, h), or ceil(sqrt(h))."""
+    b = min(fc_baby, h) if fc_baby else ceil_sqrt(h)
     g = -(-h // b)
     return b, [(gp, gp * b, [s for s in range(b) if gp * b + s < h]) for gp in range(g)]
 
 
 def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int, square: bool, hoist: int = 0,
-             L: int = 1):
+             L: int = 1, fc_baby: int = 0):
     """One layer of Eq. mlp_forward: z = sum_i diag_i (.) Rot(x, i) by BSGS,
     y = rotsum_{n_in/h}(z, stride h) (h-periodic W x), + b, then (.)^2 unless last.
     L lanes: rotations by L i, lane-interleaved diagonals and bias (reading R20)."""
     h = W.shape[0]
     lvl = x.level
-    b, giants = fc_schedule(h)
+    b, giants = fc_schedule(h, fc_baby)
     pq = hoist == 2  # double-hoisted BSGS (see dh())
     babies = ([ev.lift_pq(x)] if pq else [x]) + [r[0] for r in baby_steps(ev, [x], [s * L for s in range(1, min(b, h))],
                                                                            hoist)]
@@ -556,7 +558,8 @@ def gesture_fc(ev, book, feat, Ws, bs, cfg):
     L = lanes_of(cfg)
     x = ev.rotsum_all([feat], L, 1)[0] if L > 1 else feat
     for layer in range(len(Ws)):
-        x = fc_layer(ev, book, x, Ws[layer], bs[layer], dims[layer], layer + 1, layer < len(Ws) - 1, cfg.hoist, L)
+        x = fc_layer(ev, book, x, Ws[layer], bs[layer], dims[layer], layer + 1, layer < len(Ws) - 1, cfg.hoist, L,
+                     getattr(cfg, "fc_baby", 0))
     return x
 
 
@@ -754,7 +757,7 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
         dims = cfg.fc_dims
         for layer in range(len(dims) - 1):
             h = dims[layer + 1]
-            b, giants = fc_schedule(h)
+            b, giants = fc_schedule(h, getattr(cfg, "fc_baby", 0))
             ks |= {s * L for s in range(1, min(b, h))}
             ks |= {G * L for _, G, _ in giants if G != 0}
             ks |= set(rotsum_steps(dims[layer] // h, h * L))

@@ -103,10 +103,10 @@ Sched k3_schedule(const mmfhe_chain_cfg &cfg)
     return s;
 }
 
-Sched fc_schedule(uint32_t h)
+Sched fc_schedule(uint32_t h, uint32_t fc_baby)
 {
     Sched s;
-    s.b = ceil_sqrt(h);
+    s.b = fc_baby ? std::min(fc_baby, h) : ceil_sqrt(h);
     const uint32_t g = (h + s.b - 1) / s.b;
     for (uint32_t gp = 0; gp < g; ++gp) {
         Sched::G gg{gp, (int32_t)(gp * s.b), {}};
@@ -366,7 +366,7 @@ class Runner {
     {
         const uint32_t n_in = cfg_.fc_dims[layer - 1], h = cfg_.fc_dims[layer];
         const uint32_t lvl = x.level;
-        Sched s = fc_schedule(h);
+        Sched s = fc_schedule(h, cfg_.fc_baby);
         const std::vector<double> *W = nullptr, *bias = nullptr;
         if (c_.fc_w.size() >= layer) {
             W = &c_.fc_w[layer - 1];
@@ -746,7 +746,7 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
         for (uint32_t s : rotsum_steps((uint32_t)L, 1)) add(s);
         for (int layer = 0; layer < 3; ++layer) {
             const uint32_t h = cfg.fc_dims[layer + 1], n_in = cfg.fc_dims[layer];
-            Sched s = fc_schedule(h);
+            Sched s = fc_schedule(h, cfg.fc_baby);
             for (uint32_t b = 1; b < std::min(s.b, h); ++b) add(b * L);
             for (auto &g : s.giants) add(g.G * L);
             for (uint32_t st : rotsum_steps(n_in / h, h * (uint32_t)L)) add(st);

@@ -22,6 +22,7 @@ ap.add_argument("--lanes", type=int, default=1)
 ap.add_argument("--hoist", type=int, default=1)
 ap.add_argument("--params", default="PS4")
 ap.add_argument("--bsgs", type=int, default=0, help="K3 baby steps b (0: ceil(sqrt(2D-1)))")
+ap.add_argument("--fc-baby", type=int, default=0)
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -29,7 +30,8 @@ P = PARAM_SETS[args.params]()
 F = args.frames
 stream = torch.cuda.current_stream(dev)
 cfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8),
-                  frame_batch=25 if args.lanes == 1 else 0, hoist=args.hoist, lanes=args.lanes, bsgs_baby=args.bsgs)
+                  frame_batch=25 if args.lanes == 1 else 0, hoist=args.hoist, lanes=args.lanes, bsgs_baby=args.bsgs,
+                  fc_baby=args.fc_baby)
 ctx = m.Context.from_params(P, device=0, stream=stream.cuda_stream)
 gen = torch.Generator(device=dev)
 gen.manual_seed(77)
