@@ -625,8 +625,11 @@ struct K3MacArgs {
     uint32_t level, L, pk, B;
 };
 
+#ifndef MMFHE_K3_THREADS
+#define MMFHE_K3_THREADS 128
+#endif
 template <int NB>
-__global__ void __launch_bounds__(128) k_k3_gauss_mac(K3MacArgs a, KTables kt)
+__global__ void __launch_bounds__(MMFHE_K3_THREADS) k_k3_gauss_mac(K3MacArgs a, KTables kt)
 {
     extern __shared__ uint64_t sw[];  // [ng][3][nb][kDmTK]: C, S - C, C - NS (0 for absent)
     const uint32_t L1 = a.level + 1;
@@ -1179,9 +1182,9 @@ void launch_k3_gauss_mac(Ctx &c, const std::vector<const uint64_t *> &xr, const 
     const size_t smem = sizeof(uint64_t) * 3 * (size_t)ng * nb * kDmTK;
     const dim3 g(c.n / kDmTK, level + 1 + pk);
     if (nb <= 8)
-        k_k3_gauss_mac<8><<<g, 128, smem, c.stream>>>(a, c.kt);
+        k_k3_gauss_mac<8><<<g, MMFHE_K3_THREADS, smem, c.stream>>>(a, c.kt);
     else
-        k_k3_gauss_mac<16><<<g, 128, smem, c.stream>>>(a, c.kt);
+        k_k3_gauss_mac<16><<<g, MMFHE_K3_THREADS, smem, c.stream>>>(a, c.kt);
     LAUNCH_CHECK(c);
 }
 

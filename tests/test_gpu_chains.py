@@ -590,3 +590,42 @@ def test_standalone_k5_fir_rot(m, hoist):
     assert ctx.trace() == ev.trace
     assert sorted(ctx.required_rotations("k5_fir_rot", _mcfg(m, cfg, bins=([1], [1]), taps=taps))) == \
         cc.required_rotations("k5_fir_rot", cfg, P.n)
+
+
+def test_raw_adc_range_fft_then_vitals_v1(m):
+    """The paper's raw-ADC variant: the encrypted range FFT of
+    raw complex ADC samples by the K3 kernel (block DFT over the M samples of a chirp, Eq.
+    range_fft P:1634-1640, windowed and fftshifted), composed with vitals_v1 on the K3
+    outputs: residues and traces equal the oracle's; the decrypted soft-argmax bin equals
+    the plaintext one computed from numpy's FFT of the same samples."""
+    P = toy(log_n=10, n_q=6, scale_bits=40, n_p=2, alpha=2)
+    M, F = 16, 6
+    x, truth = radar.vital_adc_scene(M, F, 20.0, seed=3701)
+    xt = radar.preprocess_adc(x)
+    cfg3 = cc.ChainCfg(A=1, R=1, D=M, n_slots=M, hoist=1)
+    cfg1 = cc.ChainCfg(R=M, F=F, gamma=2, n_slots=M)
+    rots = sorted(set(cc.required_rotations("k3_doppler_dft", cfg3, P.n)) |
+                  set(cc.required_rotations("vitals_v1", cfg1, P.n)))
+    keys = orc.keygen(P, seed=3702, rotations=rots)
+    cts = []
+    for t in range(F):
+        for part in (xt[t].real, xt[t].imag):
+            cts.append(orc.encrypt_vector(P, keys, part, P.L, seed=3703, index=len(cts)))
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    dre, dim = cc.k3_doppler_dft_frames(ev, book, cts[0::2], cts[1::2], cfg3)
+    ctx = _run(m, P, keys, book, "k3_doppler_dft", cfg3, cts, dre + dim)
+    assert ctx.trace() == ev.trace
+    spec = [c for t in range(F) for c in (dre[t], dim[t])]
+    ev1 = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book1 = cc.PlainBook(P)
+    N, D = cc.vitals_v1(ev1, book1, spec[0::2], spec[1::2], cfg1)
+    ctx1 = _run(m, P, keys, book1, "vitals_v1", cfg1, spec, [N, D])
+    assert ctx1.trace() == ev1.trace
+    X = np.fft.fftshift(np.fft.fft(np.hanning(M) * xt, axis=1), axes=1)
+    got = orc.decrypt_vector(P, keys, dre[0])
+    assert np.max(np.abs(got - X[0].real)) <= 1e-3 * np.max(np.abs(X[0].real))
+    _, _, r_plain = dsp.soft_attention(dsp.energy(X), 2, F)
+    r_enc = orc.decrypt_vector(P, keys, N)[0] / orc.decrypt_vector(P, keys, D)[0]
+    assert round(r_enc) == round(r_plain)
+    assert abs(round(r_plain) - (truth["r_star"] + M // 2) % M) <= 1
