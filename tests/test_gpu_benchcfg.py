@@ -150,7 +150,7 @@ def _c4_case(lanes, F, seed, hoist=1, bsgs=0, fc_baby=0):
     return P, cfg, keys, cts, np.sum(feats, axis=0)
 
 
-@pytest.mark.parametrize("lanes,F,hoist,bsgs,fc_baby", [(1, 2, 1, 0, 0), (8, 16, 2, 16, 0)])
+@pytest.mark.parametrize("lanes,F,hoist,bsgs,fc_baby", [(1, 2, 1, 0, 0), (8, 16, 2, 16, 16)])
 def test_c4_bench_params_residue_parity(m, lanes, F, hoist, bsgs, fc_baby):
     """PS4 gesture at entry level 19 with the FC head (bench C4), bit-exact: canonical (one
     frame per ciphertext, 2 frames, hoisted BSGS) and the bench's headline (8 frames per
