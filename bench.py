@@ -89,8 +89,10 @@ def c4_bench_config(world, cfg):
             "packing": (f"SIMD-dense: {L} frames interleaved per ciphertext (lanes = {L}, DESIGN R20), "
                         f"{n_pairs(cfg)} ciphertext pairs per session" if L > 1 else
                         "one frame per ciphertext (the paper's layout, P:741)"),
-            "bsgs": ("double-hoisted (hoist = 2, DESIGN R22): PQ baby steps, PQ-encoded diagonals (K3 by Gauss's "
-                     "three-product form), PQ giant steps, one ModDown per output" if cfg["hoist"] == 2 else
+            "bsgs": (f"double-hoisted (hoist = 2, DESIGN R22): PQ baby steps, PQ-encoded diagonals (K3 by Gauss's "
+                     f"three-product form), PQ giant steps, one ModDown per output; K3 split "
+                     f"{cfg['bsgs_baby']} x {-(-63 // cfg['bsgs_baby'])}, FC baby steps min({cfg['fc_baby']}, h); "
+                     f"rotate-and-sums with a double-hoisted first level of 8 (R27)" if cfg["hoist"] == 2 else
                      "hoisted baby steps (hoist = 1)"),
             "sessions_per_step_per_gpu": 1, "parallelism": f"session-sharded x{world}",
             "l2": f"inputs larger than L2 ({2 * n_pairs(cfg) * 20} MiB of ciphertexts per step, L2 126 MB)",

@@ -258,6 +258,25 @@ class CircuitEvaluator(orc.Evaluator):
         return acc
 
 
+    def rotsum_dh_all(self, cts, count: int, stride: int, inner: int = 8):
+        """Rotate-and-sum with a double-hoisted first level (reading R27):
+        with a = min(inner, count), t = ModDown(P x + sum_{0<j<a} Rot_PQ(x, j stride)) -- one
+        ModUp of x, a - 1 hoisted rotations left over Q_l u P (hoisted_step_pq), their PQ sum
+        and one ModDown -- then the remaining log2(count / a) rotate-and-add steps with
+        strides a stride 2^i.  The same slot sums as rotsum_all (decryption), other residues.
+        Op-major: the lifts, every rotation (step-major), then the PQ additions."""
+        a = min(inner, count)
+        if a <= 1:
+            return self.rotsum_all(cts, count, stride)
+        ys = [self.hoist_modup(x) for x in cts]
+        acc = [self.lift_pq(x) for x in cts]
+        rots = [[self.hoisted_step_pq(x, y, stride * j) for x, y in zip(cts, ys)] for j in range(1, a)]
+        for r in rots:
+            acc = [self.add_pq(p, q) for p, q in zip(acc, r)]
+        t = [self.moddown_ct(p) for p in acc]
+        return self.rotsum_all(t, count // a, stride * a)
+
+
 # ------------------------------------------------------------------ K1 / K2
 
 def k1_energy(ev: CircuitEvaluator, re_list, im_list) -> orc.Ct:
@@ -450,7 +469,8 @@ def k2_doppler_soft_power(ev, Pm, cfg):
     (stride D; every block then holds sum_{a,r}, reading #8); S^gamma by squarings;
     f = Pm (.) S^gamma (P:906 'feature weighting')."""
     L = lanes_of(cfg)
-    S = ev.rotsum_all(Pm, Pm[0].n_slots // L // cfg.D, cfg.D * L)
+    rs = ev.rotsum_dh_all if dh(cfg) else ev.rotsum_all
+    S = rs(Pm, Pm[0].n_slots // L // cfg.D, cfg.D * L)
     for _ in range(log2_exact(cfg.gamma, "gamma")):
         S = ev.square_rescale_all(S)
     Pd = [ev.drop_to(p, s.level) for p, s in zip(Pm, S)]
@@ -528,7 +548,7 @@ def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int
             inner = ev.rotate_pq(inner, G * L) if pq else ev.rotate(inner, G * L)
         acc = inner if acc is None else (ev.add_pq(acc, inner) if pq else ev.add(acc, inner))
     z = ev.rescale(ev.moddown_ct(acc) if pq else acc)
-    y = ev.rotsum_all([z], n_in // h, h * L)[0]
+    y = (ev.rotsum_dh_all if pq else ev.rotsum_all)([z], n_in // h, h * L)[0]
     bv = lane_vec(np.asarray(bias, dtype=np.float64), L)
     y = ev.add_plain(y, book.vec(f"fc{layer}.bias", bv, y.level, scale=y.scale))
     if square:
@@ -556,7 +576,7 @@ def gesture_fc(ev, book, feat, Ws, bs, cfg):
     dims = cfg.fc_dims
     Ws, bs = pad_fc(Ws, bs, dims)
     L = lanes_of(cfg)
-    x = ev.rotsum_all([feat], L, 1)[0] if L > 1 else feat
+    x = (ev.rotsum_dh_all if dh(cfg) else ev.rotsum_all)([feat], L, 1)[0] if L > 1 else feat
     for layer in range(len(Ws)):
         x = fc_layer(ev, book, x, Ws[layer], bs[layer], dims[layer], layer + 1, layer < len(Ws) - 1, cfg.hoist, L,
                      getattr(cfg, "fc_baby", 0))
@@ -746,19 +766,26 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
         if cfg.hoist:
             ks |= {m * cfg.R for m in range(1, 1 << cfg.iq_pack)}
     L = lanes_of(cfg)
+
+    def rotsum_keys(count, stride):  # + the double-hoisted inner group's strides (R27)
+        out = set(rotsum_steps(count, stride))
+        if dh(cfg):
+            out |= {j * stride for j in range(1, min(8, count))}
+        return out
+
     if chain in ("k3_doppler_dft", "gesture_frame", "gesture"):
         b, giants = k3_schedule(cfg)
         ks |= {s * L for s in range(1, b)}
         ks |= {G * L for _, G, _ in giants if G != 0}
     if chain in ("k2_doppler_soft_power", "gesture_frame", "gesture"):
-        ks |= set(rotsum_steps(cfg.n_slots // cfg.D, cfg.D * L))
+        ks |= rotsum_keys(cfg.n_slots // cfg.D, cfg.D * L)
     if chain in ("gesture_fc", "gesture", "fc_forward"):
-        ks |= set(rotsum_steps(L, 1))
+        ks |= rotsum_keys(L, 1)
         dims = cfg.fc_dims
         for layer in range(len(dims) - 1):
             h = dims[layer + 1]
             b, giants = fc_schedule(h, getattr(cfg, "fc_baby", 0))
             ks |= {s * L for s in range(1, min(b, h))}
             ks |= {G * L for _, G, _ in giants if G != 0}
-            ks |= set(rotsum_steps(dims[layer] // h, h * L))
+            ks |= rotsum_keys(dims[layer] // h, h * L)
     return sorted({k % half for k in ks} - {0})

@@ -169,6 +169,22 @@ class Runner {
 
     uint32_t L() const { return lanes_of(cfg_); }
 
+    // rotate-and-sum; with double hoisting the first min(8, count) terms are one hoisted group
+    // left over Q_l u P, summed there and brought down by one ModDown (oracle rotsum_dh_all,
+    // reading R27), then the remaining rotate-and-add steps
+    DCt rotsum(const DCt &x, uint32_t count, uint32_t stride)
+    {
+        const uint32_t a = std::min<uint32_t>(8, count);
+        if (!dh() || a <= 1) return ev_rotsum(c_, x, count, stride);
+        DCt acc = ev_lift_pq(c_, x);
+        std::vector<int32_t> st;
+        for (uint32_t j = 1; j < a; ++j) st.push_back((int32_t)(stride * j));
+        std::vector<DCt> rots = ev_rotate_hoisted_pq(c_, x, st);
+        for (auto &r : rots) acc = ev_addsub(c_, acc, r, false);
+        DCt t = ev_moddown_ct(c_, acc);
+        return ev_rotsum(c_, t, count / a, stride * a);
+    }
+
     // [x, Rot(x,L), ..., Rot(x,(nb-1)L)] (L = lanes): plain HRots, or (cfg.hoist) hoisted HRots
     // sharing one ModUp
     std::vector<DCt> baby_steps(const DCt &x, uint32_t nb)
@@ -347,7 +363,7 @@ class Runner {
 
     DCt k2_doppler_soft_power(const DCt &Pm)
     {
-        DCt S = ev_rotsum(c_, Pm, Pm.n_slots / L() / cfg_.D, cfg_.D * L());
+        DCt S = rotsum(Pm, Pm.n_slots / L() / cfg_.D, cfg_.D * L());
         for (uint32_t i = 0; i < ilog2(cfg_.gamma); ++i) S = ev_square_rescale(c_, S);
         DCt Pd = ev_drop_to(c_, Pm, S.level);
         return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&Pd, &S}}));
@@ -406,7 +422,7 @@ class Runner {
         }
         if (dh()) acc = ev_moddown_ct(c_, acc);
         DCt z = ev_rescale(c_, acc);
-        DCt y = ev_rotsum(c_, z, n_in / h, h * L());
+        DCt y = rotsum(z, n_in / h, h * L());
         const DPlain &bp = plain("fc" + std::to_string(layer) + ".bias", y.level, y.scale, [&] {
             MMFHE_REQUIRE(bias != nullptr, MMFHE_E_MISSING_PLAIN, "FC bias not prepared");
             return lane_rep(*bias, L());
@@ -421,7 +437,7 @@ class Runner {
     // sum, so frame-sharded partial sums stay exact modular sums
     DCt gesture_fc(const DCt &feat)
     {
-        DCt x = L() > 1 ? fc_layer(ev_rotsum(c_, feat, L(), 1), 1, true) : fc_layer(feat, 1, true);
+        DCt x = L() > 1 ? fc_layer(rotsum(feat, L(), 1), 1, true) : fc_layer(feat, 1, true);
         x = fc_layer(x, 2, true);
         return fc_layer(x, 3, false);
     }
@@ -740,16 +756,21 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
         for (uint32_t b = 1; b < s.b; ++b) add(b * L);
         for (auto &g : s.giants) add(g.G * L);
     }
-    if (frames || chain == "k2_doppler_soft_power")
-        for (uint32_t s : rotsum_steps(cfg.n_slots / cfg.D, cfg.D * (uint32_t)L)) add(s);
+    // a rotate-and-sum's keys; with double hoisting (R27) also j stride, j < min(8, count)
+    auto add_rotsum = [&](uint32_t count, uint32_t stride) {
+        for (uint32_t s : rotsum_steps(count, stride)) add(s);
+        if (cfg.hoist == 2)
+            for (uint32_t j = 1; j < std::min<uint32_t>(8, count); ++j) add((int64_t)j * stride);
+    };
+    if (frames || chain == "k2_doppler_soft_power") add_rotsum(cfg.n_slots / cfg.D, cfg.D * (uint32_t)L);
     if (chain == "gesture_fc" || chain == "gesture" || chain == "fc_forward") {
-        for (uint32_t s : rotsum_steps((uint32_t)L, 1)) add(s);
+        add_rotsum((uint32_t)L, 1);
         for (int layer = 0; layer < 3; ++layer) {
             const uint32_t h = cfg.fc_dims[layer + 1], n_in = cfg.fc_dims[layer];
             Sched s = fc_schedule(h, cfg.fc_baby);
             for (uint32_t b = 1; b < std::min(s.b, h); ++b) add(b * L);
             for (auto &g : s.giants) add(g.G * L);
-            for (uint32_t st : rotsum_steps(n_in / h, h * (uint32_t)L)) add(st);
+            add_rotsum(n_in / h, h * (uint32_t)L);
         }
     }
     return std::vector<int32_t>(ks.begin(), ks.end());

@@ -537,3 +537,24 @@ def test_k5_fir_rot_decrypts_to_lfilter(W):
     assert rel_err(got, want) < 1e-4
     b, giants = cc.fir_rot_schedule(W)
     assert sum(1 for op in ev.trace if op[0] in ("hrot", "hrot_hoisted")) == (min(b, W) - 1) + (len(giants) - 1)
+
+
+@pytest.mark.parametrize("count,inner", [(8, 8), (32, 8), (4, 8), (16, 4)])
+def test_double_hoisted_rotsum_equals_rotsum(count, inner):
+    """Reading R27: the rotate-and-sum with a double-hoisted first level (one ModUp, inner - 1
+    PQ rotations, one ModDown, then the remaining rotate-and-add steps) decrypts to the same
+    slot sums as the sequential one, sum_{m < count} Rot(v, m stride), with fewer key switches."""
+    P = toy(log_n=10, n_q=4, scale_bits=40, n_p=2, alpha=2)
+    stride = 3
+    rots = sorted({(j * stride) % (P.n // 2) for j in range(1, count)})
+    keys = orc.keygen(P, seed=2401, rotations=rots)
+    v = np.random.default_rng(count).uniform(-1, 1, P.n // 2)
+    ct = _enc(P, keys, v, 3, 0)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    got = orc.decrypt_vector(P, keys, ev.rotsum_dh_all([ct], count, stride, inner)[0])
+    want = sum(np.roll(v, -m * stride) for m in range(count))
+    assert rel_err(got, want) < 1e-6
+    a = min(inner, count)
+    ops = [op for op, _, _ in ev.trace]
+    assert ops.count("hrot_hoisted_pq") == a - 1 and ops.count("moddown") == 1
+    assert ops.count("hrot") == int(np.log2(count // a))
