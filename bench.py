@@ -836,9 +836,9 @@ class OracleC4Stages:
             layer = int(s[2])
             L, dims = cc.lanes_of(cfg), cfg.fc_dims
             if layer == 1 and L > 1:
-                x = ev.rotsum_all([x], L, 1)[0]
+                x = (ev.rotsum_dh_all if cc.dh(cfg) else ev.rotsum_all)([x], L, 1)[0]
             y = cc.fc_layer(ev, book, x, self.Ws[layer - 1], self.bs[layer - 1], dims[layer - 1], layer,
-                            layer < 3, cfg.hoist, L)
+                            layer < 3, cfg.hoist, L, cfg.fc_baby)
         dt = time.perf_counter() - t0 - (book.encode_s - e0)
         nxt = self.stages.index(s) + 1
         if nxt < len(self.stages):

@@ -371,6 +371,10 @@ def dh(cfg) -> bool:
 def k3_baby_steps(ev: CircuitEvaluator, v_re, v_im, cfg: ChainCfg):
     """K3 BSGS baby steps: [x, Rot(x, s)] for s < b, for v_re and v_im."""
     L = lanes_of(cfg)
+    n = v_re[0].n_slots // L
+    if n % cfg.D or n < 2 * cfg.D:
+        # the 2D-1 offsets of the block-diagonal matrix alias when a period holds one block
+        raise ValueError("K3 needs the packing period to be a multiple of D and at least 2D")
     b, _ = k3_schedule(cfg)
     if dh(cfg):
         xr = [[ev.lift_pq(x) for x in v_re]] + baby_steps(ev, v_re, [s * L for s in range(1, b)], 2)

@@ -846,6 +846,11 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
         MMFHE_REQUIRE((size_t)lanes_of(cfg) * (cfg.n_slots ? cfg.n_slots : 1) <= c.n / 2, MMFHE_E_SHAPE,
                       "lanes * n_slots must not exceed N/2");
     }
+    const bool k3_chain = chain == "k3_doppler_dft" || chain == "gesture" || chain == "gesture_frame" ||
+                          chain == "gesture_features";
+    if (k3_chain)  // the 2D-1 block-diagonal offsets alias when a period holds a single block
+        MMFHE_REQUIRE(cfg.D >= 1 && cfg.n_slots % cfg.D == 0 && cfg.n_slots >= 2 * cfg.D, MMFHE_E_SHAPE,
+                      "K3 needs n_slots a multiple of D and at least 2D");
     if (chain == "vitals_v1") n_out = 2;
     if (chain == "vitals_v2") {
         n_out = 0;

@@ -602,15 +602,17 @@ def test_raw_adc_range_fft_then_vitals_v1(m):
     M, F = 16, 6
     x, truth = radar.vital_adc_scene(M, F, 20.0, seed=3701)
     xt = radar.preprocess_adc(x)
-    cfg3 = cc.ChainCfg(A=1, R=1, D=M, n_slots=M, hoist=1)
-    cfg1 = cc.ChainCfg(R=M, F=F, gamma=2, n_slots=M)
+    # one chirp of M samples in the first M slots of a period-2M vector (K3's Halevi-Shoup
+    # diagonals over [-(D-1), D-1] need at least two blocks per period); block 1 stays zero
+    cfg3 = cc.ChainCfg(A=1, R=2, D=M, n_slots=2 * M, hoist=1)
+    cfg1 = cc.ChainCfg(R=M, F=F, gamma=2, n_slots=2 * M)
     rots = sorted(set(cc.required_rotations("k3_doppler_dft", cfg3, P.n)) |
                   set(cc.required_rotations("vitals_v1", cfg1, P.n)))
     keys = orc.keygen(P, seed=3702, rotations=rots)
     cts = []
     for t in range(F):
         for part in (xt[t].real, xt[t].imag):
-            cts.append(orc.encrypt_vector(P, keys, part, P.L, seed=3703, index=len(cts)))
+            cts.append(orc.encrypt_vector(P, keys, radar.pack_vital(part, 2 * M), P.L, seed=3703, index=len(cts)))
     ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
     book = cc.PlainBook(P)
     dre, dim = cc.k3_doppler_dft_frames(ev, book, cts[0::2], cts[1::2], cfg3)
@@ -624,7 +626,8 @@ def test_raw_adc_range_fft_then_vitals_v1(m):
     assert ctx1.trace() == ev1.trace
     X = np.fft.fftshift(np.fft.fft(np.hanning(M) * xt, axis=1), axes=1)
     got = orc.decrypt_vector(P, keys, dre[0])
-    assert np.max(np.abs(got - X[0].real)) <= 1e-3 * np.max(np.abs(X[0].real))
+    assert np.max(np.abs(got[:M] - X[0].real)) <= 1e-3 * np.max(np.abs(X[0].real))
+    assert np.max(np.abs(got[M:])) <= 1e-6
     _, _, r_plain = dsp.soft_attention(dsp.energy(X), 2, F)
     r_enc = orc.decrypt_vector(P, keys, N)[0] / orc.decrypt_vector(P, keys, D)[0]
     assert round(r_enc) == round(r_plain)
