@@ -428,8 +428,8 @@ def k3_giant_steps(ev: CircuitEvaluator, inner, cfg: ChainCfg):
     rot, add = (ev.rotate_pq, ev.add_pq) if dh(cfg) else (ev.rotate, ev.add)
     for (gp, G, babies), (pr, pi) in zip(giants, inner):
         ir = [rot(x, G * L) for x in pr]
-        out_re = ir if out_re is None else [add(a, x) for a, x in zip(out_re, ir)]
         ii = [rot(x, G * L) for x in pi]
+        out_re = ir if out_re is None else [add(a, x) for a, x in zip(out_re, ir)]
         out_im = ii if out_im is None else [add(a, x) for a, x in zip(out_im, ii)]
     if dh(cfg):
         out_re = [ev.moddown_ct(x) for x in out_re]

@@ -307,32 +307,35 @@ class Runner {
             const char *e = getenv("MMFHE_K3_GAUSS");
             return !(e && *e == '0');
         }();
-        std::vector<DCt> inner = gauss && s.b <= (uint32_t)kDiagMax && s.giants.size() <= (size_t)kDiagMax
-                                     ? ev_k3_mac(c_, pr, pi, PC, PS, PN)
-                                     : ev_diag_mac(c_, cts, rows);
-        // per giant: rotate + accumulate d_re, then d_im (oracle k3_giant_steps' order); double
-        // hoisting fuses the accumulation into the giant step's inner product
-        DCt out_re, out_im;
-        for (size_t gi = 0; gi < s.giants.size(); ++gi) {
-            const int32_t step = s.giants[gi].G * (int32_t)L();
-            if (gi == 0) {
-                out_re = dh() ? ev_rotate_pq(c_, inner[0], step) : ev_rotate(c_, inner[0], step);
-                out_im = dh() ? ev_rotate_pq(c_, inner[1], step) : ev_rotate(c_, inner[1], step);
-            } else if (dh()) {
-                ev_rotate_pq_acc(c_, out_re, inner[2 * gi], step);
-                ev_rotate_pq_acc(c_, out_im, inner[2 * gi + 1], step);
-            } else {
-                out_re = ev_addsub(c_, out_re, ev_rotate(c_, inner[2 * gi], step), false);
-                out_im = ev_addsub(c_, out_im, ev_rotate(c_, inner[2 * gi + 1], step), false);
+        std::vector<DCt> inner;  // per giant one 2B batch: d_re items, then d_im items
+        if (gauss && s.b <= (uint32_t)kDiagMax && s.giants.size() <= (size_t)kDiagMax) {
+            inner = ev_k3_mac(c_, pr, pi, PC, PS, PN);
+        } else {
+            std::vector<DCt> sep = ev_diag_mac(c_, cts, rows);
+            for (size_t gi = 0; gi < s.giants.size(); ++gi) {
+                std::vector<DCt> two;
+                two.push_back(std::move(sep[2 * gi]));
+                two.push_back(std::move(sep[2 * gi + 1]));
+                inner.push_back(concat(c_, two));
             }
         }
-        if (dh()) {  // one ModDown per output ends the double-hoisted giant sum
-            out_re = ev_moddown_ct(c_, out_re);
-            out_im = ev_moddown_ct(c_, out_im);
+        // per giant: rotate d_re and d_im (one 2B launch set sharing the key), then accumulate
+        // (oracle k3_giant_steps' order); double hoisting fuses the accumulation into the giant
+        // step's inner product
+        DCt out;
+        for (size_t gi = 0; gi < s.giants.size(); ++gi) {
+            const int32_t step = s.giants[gi].G * (int32_t)L();
+            if (gi == 0)
+                out = dh() ? ev_rotate_pq(c_, inner[0], step) : ev_rotate(c_, inner[0], step);
+            else if (dh())
+                ev_rotate_pq_acc(c_, out, inner[gi], step);
+            else
+                out = ev_addsub(c_, out, ev_rotate(c_, inner[gi], step), false);
         }
-        DCt a = ev_rescale(c_, out_re);
-        DCt b = ev_rescale(c_, out_im);
-        return {std::move(a), std::move(b)};
+        if (dh()) out = ev_moddown_ct(c_, out);  // one ModDown per output ends the giant sum
+        DCt r = ev_rescale(c_, out);
+        const uint32_t B = vre.batch;
+        return {copy_ct(c_, slice(r, 0, B)), copy_ct(c_, slice(r, B, B))};
     }
 
     // ---------------------------------------------------------- gesture frame (batched)

@@ -436,13 +436,14 @@ std::vector<DCt> ev_k3_mac(Ctx &c, const std::vector<const DCt *> &xr, const std
             cnt += 2;
         }
         MMFHE_REQUIRE(cnt > 0, MMFHE_E_INVALID_ARG, "giant step without terms");
-        for (int part = 0; part < 2; ++part) {
+        for (int part = 0; part < 2; ++part)
             rec_n(c, a0.pk ? "pmult_sum_pq" : "pmult_sum", a0.level, a0.batch, std::to_string(cnt));
-            out.push_back(a0.pk ? make_pq(c, a0.level, a0.n_slots, sc, a0.batch)
-                                : make_ct(c, a0.level, 2, a0.n_slots, sc, a0.batch));
-        }
-        re.push_back(out[out.size() - 2].data());
-        im.push_back(out.back().data());
+        // one 2B batch per giant: its d_re items, then its d_im items (the giant rotations of
+        // both then run as one launch set sharing the key)
+        out.push_back(a0.pk ? make_pq(c, a0.level, a0.n_slots, sc, 2 * a0.batch)
+                            : make_ct(c, a0.level, 2, a0.n_slots, sc, 2 * a0.batch));
+        re.push_back(out.back().data());
+        im.push_back(out.back().item(a0.batch));
     }
     launch_k3_gauss_mac(c, r, i, a0.item_words(), C, S, NS, re, im, out[0].item_words(), a0.level, a0.batch, a0.pk);
     return out;

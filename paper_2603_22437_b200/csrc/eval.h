@@ -35,9 +35,9 @@ DCt ev_pmult_sum(Ctx &c, const std::vector<std::pair<const DPlain *, const DCt *
 // out[o] = sum_c pts[o][c] (.) cts[c] (pts[o][c] may be null); records one pmult_sum per output.
 std::vector<DCt> ev_diag_mac(Ctx &c, const std::vector<const DCt *> &cts,
                              const std::vector<std::vector<const DPlain *>> &pts);
-// K3's inner sums (re_g = sum_s pc xr_s + pns xi_s, im_g = sum_s ps xr_s + pc xi_s, outputs
-// re_0, im_0, re_1, ...) by Gauss's three-product form: the same residues and trace as
-// ev_diag_mac over the four-product rows, 3/4 of the MACs.
+// K3's inner sums (re_g = sum_s pc xr_s + pns xi_s, im_g = sum_s ps xr_s + pc xi_s) by Gauss's
+// three-product form: the same residues and trace as ev_diag_mac over the four-product rows,
+// 3/4 of the MACs.  Output g is one batch of 2B items: re_g's B items, then im_g's.
 std::vector<DCt> ev_k3_mac(Ctx &c, const std::vector<const DCt *> &xr, const std::vector<const DCt *> &xi,
                            const std::vector<std::vector<const DPlain *>> &pc,
                            const std::vector<std::vector<const DPlain *>> &ps,
