@@ -870,6 +870,40 @@ std::vector<DCt> ev_rotate_hoisted_pq(Ctx &c, const DCt &a, const std::vector<in
     ModUpOut m;
     if (need) m = ks_modup(c, a.poly(1), a.item_words(), l, B);
     std::vector<DCt> out;
+    // the group's nonzero steps in one launch per 16 (y, x and c0 read once), when the batch's
+    // digit tile fits the kernel's shared memory; otherwise one inner product per step
+    const bool grouped = need && c.modup[l].size() <= 4 &&
+                         (size_t)B * (c.modup[l].size() + 1) * 128 * sizeof(uint64_t) <= 200 * 1024;
+    if (grouped) {
+        std::vector<const uint64_t *> keys;
+        std::vector<uint32_t> ginv;
+        std::vector<uint64_t *> outs;
+        auto flush = [&] {
+            if (keys.empty()) return;
+            launch_hoisted_ip_pq(c, a.poly(1), a.item_words(), m.y.get(), m.T * c.n, m.off, a.data(), a.item_words(),
+                                 keys, ginv, outs, out.back().item_words(), l, B);
+            keys.clear();
+            ginv.clear();
+            outs.clear();
+        };
+        for (int32_t s : steps) {
+            int32_t k;
+            const uint64_t g = galois_element(c, s, &k);
+            if (k == 0) {
+                out.push_back(ev_lift_pq(c, a));
+                continue;
+            }
+            rec_n(c, "hrot_hoisted_pq", l, B, std::to_string(k));
+            out.push_back(make_pq(c, l, a.n_slots, a.scale, B));
+            keys.push_back(find_gk(c, k).buf.get());
+            // g is odd; the units mod 2N = 2^(log N + 1) have order N: g^-1 = g^(N-1) mod 2N
+            ginv.push_back((uint32_t)host::pow(g, c.n - 1, 2ull * c.n));
+            outs.push_back(out.back().data());
+            if (keys.size() == (size_t)kDiagMax) flush();
+        }
+        flush();
+        return out;
+    }
     for (int32_t s : steps) {
         int32_t k;
         const uint32_t g = (uint32_t)galois_element(c, s, &k);

@@ -49,6 +49,13 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
                    uint32_t gx = 1, uint32_t gy = 1, const IPOut *os = nullptr, const IPEpi *ep = nullptr);
 // w [B*npoly][l+1][N] = BConv_{P->Q}(zP [B*npoly][K][N]) (coefficient form).
 void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B, uint32_t npoly = 2);
+// A group of hoisted rotations left over Q_l u P in one launch (double hoisting's baby steps):
+// outs[s] (PQ ciphertexts, item stride os) = (P sigma_s(c0) + IP0, IP1) of the digits of x / y
+// through sigma_s, with ginv[s] the inverse Galois element of step s and keys[s] its evk.
+void launch_hoisted_ip_pq(Ctx &c, const uint64_t *x, size_t xs, const uint64_t *y, size_t ys,
+                          const std::vector<size_t> &off, const uint64_t *c0, size_t cs,
+                          const std::vector<const uint64_t *> &keys, const std::vector<uint32_t> &ginv,
+                          const std::vector<uint64_t *> &outs, size_t os, uint32_t level, uint32_t B);
 // double hoisting: Q rows of out (+)= [P]_{q_i} sigma_g(src) for npoly polys per
 // item (out / src item strides os / ss, poly strides ops / sps): the identity baby step's P lift
 // (the other PQ addends are the key inner product's fused epilogue, IPEpi)

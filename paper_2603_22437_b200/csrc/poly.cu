@@ -312,6 +312,87 @@ __global__ void __launch_bounds__(kTB, DMAX <= 4 ? 4 : 1) k_key_ip(uint64_t *__r
     }
 }
 
+// A group of hoisted rotations left over Q_l u P (double hoisting's baby steps, R22/R27) in one
+// launch: for every step s, item b, PQ row r and coefficient j
+//   r_s[j] = sum_d y_d[perm_s(j)] evk_s[d][j] (+ [P]_{q_r} c0[perm_s(j)] on poly 0's Q rows).
+// A thread owns the source index k = perm_s(j) instead: y_d[k] and c0[k] are the same for every
+// step, so the CTA stages its tile of them for all B items in shared memory once, then walks
+// the steps: each step's 2 dnum key words are gathered at j = perm_s^{-1}(k) (an aligned
+// 32-word span maps onto one aligned span: the gathers stay coalesced), reused across the B
+// items, and the results are scattered to j.  y, x and c0 are read from HBM once for the whole
+// group instead of once per step; every key word once per launch.
+constexpr int kHTile = 128;
+struct HoistIPArgs {
+    const uint64_t *key[kDiagMax];
+    uint64_t *out[kDiagMax];      // PQ ciphertexts: [B][2][l+1] Q rows, then [B][2][K] P rows
+    uint32_t ginv[kDiagMax];      // inverse Galois elements (perm_s^{-1})
+    size_t y_off[16];
+    uint32_t lo[16], hi[16];
+    size_t xs, ys, cs, os;        // item strides: x (c1), y (ModUp'd digits), c0, outputs
+    uint32_t dnum, level, L, K, B, nsteps;
+};
+
+template <int DMAX>
+__global__ void __launch_bounds__(kHTile) k_hoisted_ip_pq(const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
+                                                        const uint64_t *__restrict__ c0, const TwPair *__restrict__ pmod,
+                                                        KTables kt, HoistIPArgs a)
+{
+    extern __shared__ uint64_t sh[];  // [B][dnum][kHTile] digit words, then [B][kHTile] c0 (Q rows)
+    const uint32_t r = blockIdx.y;    // PQ row: 0..l = q_r, l+1.. = p_{r-l-1}
+    const uint32_t k0 = blockIdx.x * kHTile, t = threadIdx.x, k = k0 + t;
+    const bool isq = r <= a.level;
+    const uint32_t pr = ext_prime(r, a.level, a.L);
+    const uint64_t q = kt.q[pr], qi = kt.qinv_neg[pr];
+    uint64_t *sy = sh, *sc = sh + (size_t)a.B * a.dnum * kHTile;
+    for (uint32_t b = 0; b < a.B; ++b) {
+        for (uint32_t j = 0; j < a.dnum; ++j) {
+            const uint64_t *src;
+            if (r >= a.lo[j] && r < a.hi[j]) {
+                src = x + (size_t)b * a.xs + (size_t)r * kt.n;
+            } else {
+                const uint32_t row = r < a.lo[j] ? r : r - (a.hi[j] - a.lo[j]);
+                src = y + (size_t)b * a.ys + a.y_off[j] + (size_t)row * kt.n;
+            }
+            sy[((size_t)b * a.dnum + j) * kHTile + t] = src[k];
+        }
+        if (isq) sc[(size_t)b * kHTile + t] = c0[(size_t)b * a.cs + (size_t)r * kt.n + k];
+    }
+    __syncthreads();
+    const size_t key_rows = a.L + 1 + a.K;
+    const TwPair pm = isq ? pmod[r] : TwPair{0, 0};
+    const size_t qrow = isq ? (size_t)r * kt.n : 0;
+    const size_t prow = isq ? 0 : (size_t)(2 * (a.level + 1) + (r - a.level - 1)) * kt.n;
+    const size_t opoly = isq ? (size_t)(a.level + 1) * kt.n : (size_t)a.K * kt.n;
+    for (uint32_t s = 0; s < a.nsteps; ++s) {
+        const uint32_t j = galois_perm(k, a.ginv[s], kt.log_n);
+        uint64_t kb[DMAX], ka[DMAX];
+#pragma unroll
+        for (int d = 0; d < DMAX; ++d) {
+            if (d < (int)a.dnum) {
+                kb[d] = __ldg(a.key[s] + ((size_t)(2 * d) * key_rows + pr) * kt.n + j);
+                ka[d] = __ldg(a.key[s] + ((size_t)(2 * d + 1) * key_rows + pr) * kt.n + j);
+            }
+        }
+        uint64_t *o = a.out[s] + (isq ? qrow : prow) + j;
+        for (uint32_t b = 0; b < a.B; ++b) {
+            U128 acc0{0, 0}, acc1{0, 0};
+            const uint64_t *v = sy + (size_t)b * a.dnum * kHTile + t;
+#pragma unroll
+            for (int d = 0; d < DMAX; ++d) {
+                if (d < (int)a.dnum) {
+                    const uint64_t w = v[d * kHTile];
+                    mac128(acc0, w, kb[d]);
+                    mac128(acc1, w, ka[d]);
+                }
+            }
+            uint64_t v0 = redc(acc0, q, qi);
+            if (isq) v0 = add_mod(v0, shoup(sc[(size_t)b * kHTile + t], pm.w, pm.wp, q), q);
+            o[(size_t)b * a.os] = v0;
+            o[(size_t)b * a.os + opoly] = redc(acc1, q, qi);
+        }
+    }
+}
+
 struct MDArgs {
     const TwPair *phat_inv;  // [K]
     const uint64_t *phat;    // [K][L+1] Montgomery
@@ -1250,6 +1331,52 @@ void launch_scatter(Ctx &c, const PtrList &dst, const uint64_t *in, int n, size_
     ProfScope ps(c, "scatter", 16.0 * words * n);
     const size_t threads = (words + 1) / 2;
     k_scatter<<<dim3((unsigned)((threads + kTB - 1) / kTB), n), kTB, 0, c.stream>>>(dst, in, words);
+    LAUNCH_CHECK(c);
+}
+
+void launch_hoisted_ip_pq(Ctx &c, const uint64_t *x, size_t xs, const uint64_t *y, size_t ys,
+                          const std::vector<size_t> &off, const uint64_t *c0, size_t cs,
+                          const std::vector<const uint64_t *> &keys, const std::vector<uint32_t> &ginv,
+                          const std::vector<uint64_t *> &outs, size_t os, uint32_t level, uint32_t B)
+{
+    const auto &plans = c.modup[level];
+    MMFHE_REQUIRE(keys.size() == outs.size() && keys.size() == ginv.size() && keys.size() <= (size_t)kDiagMax &&
+                      plans.size() <= 4,
+                  MMFHE_E_LAYOUT, "hoisted PQ inner product: <= 16 steps, <= 4 digits");
+    HoistIPArgs a{};
+    a.dnum = (uint32_t)plans.size();
+    a.level = level;
+    a.L = c.L;
+    a.K = c.K;
+    a.B = B;
+    a.xs = xs;
+    a.ys = ys;
+    a.cs = cs;
+    a.os = os;
+    a.nsteps = (uint32_t)keys.size();
+    for (size_t s = 0; s < keys.size(); ++s) {
+        a.key[s] = keys[s];
+        a.out[s] = outs[s];
+        a.ginv[s] = ginv[s];
+    }
+    for (size_t j = 0; j < plans.size(); ++j) {
+        a.y_off[j] = off[j] * c.n;
+        a.lo[j] = plans[j].lo;
+        a.hi[j] = plans[j].hi;
+    }
+    const double rows = level + 1 + c.K, S = (double)keys.size();
+    // algorithmic: digit words and c0 once, every step's key once, every output once
+    ProfScope ps(c, "key_ip", 8.0 * c.n * (rows * B * a.dnum + (level + 1.0) * B + S * rows * 2.0 * a.dnum +
+                                          S * B * 2.0 * rows),
+                 2.0 * a.dnum * rows * c.n * B * S);
+    const size_t smem = sizeof(uint64_t) * (size_t)B * (a.dnum + 1) * kHTile;
+    MMFHE_REQUIRE(smem <= 200 * 1024, MMFHE_E_SHAPE, "hoisted PQ inner product: batch too large for one tile");
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, [] {
+        CUDA_CHECK(cudaFuncSetAttribute(k_hoisted_ip_pq<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    });
+    const dim3 g(c.n / kHTile, level + 1 + c.K);
+    k_hoisted_ip_pq<4><<<g, kHTile, smem, c.stream>>>(x, y, c0, (const TwPair *)c.bconv_ptr(c.off_pd_pmod), c.kt, a);
     LAUNCH_CHECK(c);
 }
 
