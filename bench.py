@@ -931,7 +931,7 @@ def run_reference(args, rank, world):
 
 # ---------------------------------------------------------------- main
 NTT_PREFIX = "ntt_"
-MAC_KERNELS = ("modup_bconv", "moddown_bconv", "key_ip", "diag_mac", "lincomb_mat", "pmult_sum")
+MAC_KERNELS = ("modup_bconv", "moddown_bconv", "key_ip", "key_ip_group", "diag_mac", "lincomb_mat", "pmult_sum")
 
 
 def _fracs(name, ms, by, ops, hbm_peak, int_peaks):

@@ -1366,7 +1366,7 @@ void launch_hoisted_ip_pq(Ctx &c, const uint64_t *x, size_t xs, const uint64_t *
     }
     const double rows = level + 1 + c.K, S = (double)keys.size();
     // algorithmic: digit words and c0 once, every step's key once, every output once
-    ProfScope ps(c, "key_ip", 8.0 * c.n * (rows * B * a.dnum + (level + 1.0) * B + S * rows * 2.0 * a.dnum +
+    ProfScope ps(c, "key_ip_group", 8.0 * c.n * (rows * B * a.dnum + (level + 1.0) * B + S * rows * 2.0 * a.dnum +
                                           S * B * 2.0 * rows),
                  2.0 * a.dnum * rows * c.n * B * S);
     const size_t smem = sizeof(uint64_t) * (size_t)B * (a.dnum + 1) * kHTile;
