@@ -47,6 +47,7 @@ BANDS = ((0.1, 0.6), (0.8, 2.5))  # RR, HR
 LANES = 8                          # frames per ciphertext in the headline (N/2 / 4096 active slots)
 FC_DIMS = (4096, 64, 32, 8)        # 5 logits padded to 8
 FC_BABY = 16                       # FC BSGS baby steps: min(16, h) (measured 78.0 -> 76.7 ms vs ceil(sqrt(h)))
+CPLX = 1                           # complex slots z = v_re + j v_im, one ciphertext per frame group (DESIGN R28)
 
 
 def band_bins(F_phase, fs, band):
@@ -55,7 +56,7 @@ def band_bins(F_phase, fs, band):
     return [int(x) for x in k[(f >= band[0]) & (f <= band[1])]]
 
 
-def c4_config(lanes=LANES, level=19, F=100):
+def c4_config(lanes=LANES, level=19, F=100, cplx=CPLX):
     from synth.params import ps4
     P = ps4()
     # frame_batch counts ciphertext pairs: all 13 packed pairs in one batch (lanes 8), or
@@ -64,17 +65,24 @@ def c4_config(lanes=LANES, level=19, F=100):
     # bsgs_baby = 16: K3's BSGS split 16 x 4 (with double hoisting the baby steps are key inner
     # products only, the giant steps full key switches: fewer giants, measured 89.3 -> 77.5 ms)
     return P, dict(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=FC_DIMS, hoist=2, lanes=lanes, level=level,
-                   frame_batch=0 if lanes > 1 else 25, bsgs_baby=16, fc_baby=FC_BABY)
+                   frame_batch=0 if lanes > 1 else 25, bsgs_baby=16, fc_baby=FC_BABY, cplx=cplx)
 
 
 def gesture_mcfg(m, cfg):
     return m.chain_cfg(A=cfg["A"], R=cfg["R"], D=cfg["D"], F=cfg["F"], gamma=cfg["gamma"], n_slots=cfg["n_slots"],
                        fc_dims=cfg["fc_dims"], frame_batch=cfg["frame_batch"], hoist=cfg["hoist"],
-                       lanes=cfg["lanes"], bsgs_baby=cfg["bsgs_baby"], fc_baby=cfg["fc_baby"])
+                       lanes=cfg["lanes"], bsgs_baby=cfg["bsgs_baby"], fc_baby=cfg["fc_baby"],
+                       cplx=cfg.get("cplx", 0))
 
 
 def n_pairs(cfg):
+    """Frame groups of a session (ceil(F / lanes)): ciphertext pairs, or single complex-slot
+    ciphertexts with cfg cplx (DESIGN R28)."""
     return -(-cfg["F"] // cfg["lanes"])
+
+
+def n_inputs(cfg):
+    return n_pairs(cfg) * (1 if cfg.get("cplx", 0) else 2)
 
 
 def c4_bench_config(world, cfg):
@@ -86,16 +94,21 @@ def c4_bench_config(world, cfg):
             "N": 2 ** 16, "A": cfg["A"], "R": cfg["R"], "D": cfg["D"], "F": cfg["F"],
             "params": f"PS4: 20 Q limbs (60 + 19x50 bits) + 7 P (60 bits), alpha 7, dnum 3, Delta 2^50, "
                       f"entry level {cfg['level']}",
-            "packing": (f"SIMD-dense: {L} frames interleaved per ciphertext (lanes = {L}, DESIGN R20), "
-                        f"{n_pairs(cfg)} ciphertext pairs per session" if L > 1 else
-                        "one frame per ciphertext (the paper's layout, P:741)"),
-            "bsgs": (f"double-hoisted (hoist = 2, DESIGN R22): PQ baby steps, PQ-encoded diagonals (K3 by Gauss's "
-                     f"three-product form), PQ giant steps, one ModDown per output; K3 split "
+            "packing": ((f"SIMD-dense: {L} frames interleaved per ciphertext (lanes = {L}, DESIGN R20), "
+                         if L > 1 else "one frame per ciphertext (the paper's layout, P:741), ")
+                        + (f"complex slots z = v_re + j v_im (DESIGN R28): {n_pairs(cfg)} input ciphertexts per "
+                           f"session, K1 = d Conj(d)" if cfg.get("cplx") else
+                           f"re / im in separate ciphertexts (P:733-739): {n_pairs(cfg)} ciphertext pairs per "
+                           f"session")),
+            "bsgs": (f"double-hoisted (hoist = 2, DESIGN R22): PQ baby steps, PQ-encoded diagonals ("
+                     + ("complex diagonals of W, one product each" if cfg.get("cplx") else
+                        "K3 by Gauss's three-product form")
+                     + f"), PQ giant steps, one ModDown per output; K3 split "
                      f"{cfg['bsgs_baby']} x {-(-63 // cfg['bsgs_baby'])}, FC baby steps min({cfg['fc_baby']}, h); "
                      f"rotate-and-sums with a double-hoisted first level of 8 (R27)" if cfg["hoist"] == 2 else
                      "hoisted baby steps (hoist = 1)"),
             "sessions_per_step_per_gpu": 1, "parallelism": f"session-sharded x{world}",
-            "l2": f"inputs larger than L2 ({2 * n_pairs(cfg) * 20} MiB of ciphertexts per step, L2 126 MB)",
+            "l2": f"inputs larger than L2 ({n_inputs(cfg) * 20} MiB of ciphertexts per step, L2 126 MB)",
             "inputs": "coefficient form, device-resident; import NTT and export INTT inside the step"}
 
 
@@ -197,10 +210,11 @@ def gesture_inputs(m, torch, P, cfg, device, seed, sessions=1):
     gen = torch.Generator(device=device)
     gen.manual_seed(seed)
     lvl, npair = cfg["level"], n_pairs(cfg)
-    data = uniform_dev(torch, gen, (sessions, 2 * npair, 2, lvl + 1), list(P.q[: lvl + 1]), P.n, device)
+    nin = n_inputs(cfg)
+    data = uniform_dev(torch, gen, (sessions, nin, 2, lvl + 1), list(P.q[: lvl + 1]), P.n, device)
     slots = cfg["n_slots"] * cfg["lanes"]
     scale = float(2 ** P.scale_bits)
-    return data, [[m.Ct(data[s, i], lvl, scale, slots, P.log_n) for i in range(2 * npair)] for s in range(sessions)]
+    return data, [[m.Ct(data[s, i], lvl, scale, slots, P.log_n) for i in range(nin)] for s in range(sessions)]
 
 
 def run_gpu(args, rank, world, device):
@@ -210,7 +224,7 @@ def run_gpu(args, rank, world, device):
     dist = world > 1
     if dist:
         import torch.distributed as tdist
-    P, cfg = c4_config(args.lanes)
+    P, cfg = c4_config(args.lanes, cplx=args.cplx)
     torch.cuda.set_device(device)
     ctx, mcfg = make_gesture_ctx(m, torch, P, cfg, device, seed=1004)  # same key set on every rank
     data, sess = gesture_inputs(m, torch, P, cfg, device, seed=2004 + rank)
@@ -312,7 +326,7 @@ def run_gpu(args, rank, world, device):
             extras["client"] = extras_client(m, torch, device)
         except Exception as e:  # report, do not hide
             extras["client"] = {"error": f"{type(e).__name__}: {e}"}
-        for wl in ("C4_canonical", "C4_l11", "C2", "C1", "C3", "C5v", "C5v_t3", "Vpaper"):
+        for wl in ("C4_split", "C4_canonical", "C4_l11", "C2", "C1", "C3", "C5v", "C5v_t3", "Vpaper"):
             try:
                 extras[wl] = bench_workload(wl, m, torch, device)
             except Exception as e:  # report, do not hide
@@ -363,16 +377,17 @@ def bench_workload(name, m, torch, device, steps=3, warmup=2):
         cfg = m.chain_cfg(A=4, R=32, D=32, n_slots=4096, frame_batch=8, hoist=1, lanes=lanes)
         plan = [("k3_doppler_dft", P.L, 2 * 32 // lanes)]
         frames, info = 32, "32 frames (8 ciphertext pairs at 4 frames each), hoisted"
-    elif name in ("C4_canonical", "C4_l11"):
+    elif name in ("C4_canonical", "C4_l11", "C4_split"):
         P = ps4()
         lanes = 1 if name == "C4_canonical" else LANES
-        _, c = c4_config(lanes, 19 if name == "C4_canonical" else 11)
+        _, c = c4_config(lanes, 11 if name == "C4_l11" else 19, cplx=CPLX if name == "C4_l11" else 0)
         cfg = gesture_mcfg(m, c)
-        plan = [("gesture", c["level"], 2 * n_pairs(c))]
+        plan = [("gesture", c["level"], n_inputs(c))]
         fc_w, fc_b = fc_weights_padded()
         frames = c["F"]
-        info = (f"F=100 frames, entry level {c['level']}, hoisted, "
-                + ("one frame per ciphertext, frame_batch 25" if lanes == 1 else f"{lanes} frames per ciphertext"))
+        info = (f"F=100 frames, entry level {c['level']}, double-hoisted, "
+                + ("one frame per ciphertext, frame_batch 25" if lanes == 1 else f"{lanes} frames per ciphertext")
+                + (", complex slots (R28)" if c["cplx"] else ", re / im in separate ciphertexts (P:733-739)"))
     else:  # C5v (PS4), C5v_t3 (PS4, third-order K7), Vpaper (the paper's vital parameters, PSV)
         from synth.params import psv
         P = psv() if name == "Vpaper" else ps4()
@@ -470,6 +485,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
     import torch.distributed as tdist
     distributed = tdist.is_available() and tdist.is_initialized()
     P, gcfg = c4_config(LANES)
+    ipp = 1 if gcfg["cplx"] else 2  # input ciphertexts per frame group
     per_rank = args.c5_per_rank
     Gv = Gg = args.c5_sessions // 2 if args.c5_sessions else per_rank * world
     stream = torch.cuda.current_stream(device)
@@ -506,8 +522,8 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
     npair = n_pairs(gcfg)
     plo, phi = mdist.shard(npair, rank, world)
     gdata, gsess = gesture_inputs(m, torch, P, gcfg, device, seed=9200 + rank, sessions=pool)
-    gpool = [m.CtArray(s[2 * plo:2 * phi]) for s in gsess]
-    lvf = ctx.chain_plan("gesture_features", gm, gcfg["level"], max(2 * (phi - plo), 2))[0]
+    gpool = [m.CtArray(s[ipp * plo:ipp * phi]) for s in gsess]
+    lvf = ctx.chain_plan("gesture_features", gm, gcfg["level"], max(ipp * (phi - plo), ipp))[0]
     lvo = ctx.chain_plan("gesture_fc", gm, lvf, 1)[0]
     feat_bufs = torch.empty((Gg, 2, lvf + 1, P.n), dtype=torch.int64, device=device)
     mine = [s for s in range(Gg) if mdist.owner(s, world) == rank]
@@ -532,7 +548,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
 
     # the features' scale (the reduce needs it before the first gather)
     probe = m.Ct(torch.empty((2, lvf + 1, P.n), dtype=torch.int64, device=device), lvf, 0.0, 0, P.log_n, m.FORM_EVAL)
-    ctx.eval_chain("gesture_features", gm, gpool[0] if phi > plo else gsess[0][:2], [probe])
+    ctx.eval_chain("gesture_features", gm, gpool[0] if phi > plo else gsess[0][:ipp], [probe])
     scale_f = [probe.scale]
 
     def step_dev():
@@ -572,7 +588,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
     hv1a = m.CtArray([m.Ct(hv1[j], 3, scale, vcfg.n_slots, P.log_n) for j in range(2 * Fv)])
     hv2a = m.CtArray([m.Ct(hv2[j], 9, scale, vcfg.n_slots, P.log_n) for j in range(2 * Fv)])
     hga = m.CtArray([m.Ct(hg[j], gcfg["level"], scale, gcfg["n_slots"] * LANES, P.log_n)
-                     for j in range(2 * plo, 2 * phi)]) if phi > plo else None
+                     for j in range(ipp * plo, ipp * phi)]) if phi > plo else None
     h2d = [0]
 
     def sessions_features_async():
@@ -751,15 +767,15 @@ def extras_n16(args, m, torch, device, batch=8, reps=3):
 
 
 # ---------------------------------------------------------------- oracle (CPU) arms
-def oracle_c4_setup(lanes):
+def oracle_c4_setup(lanes, cplx=CPLX):
     """The oracle's view of the headline workload: uniform evaluation keys (the same PRNG
     recipe as the tests' uniform inputs), the FC weights, the chain config."""
     from oracle import circuits as cc
     from synth import prng
-    P, cfg = c4_config(lanes)
+    P, cfg = c4_config(lanes, cplx=cplx)
     ccfg = cc.ChainCfg(A=cfg["A"], R=cfg["R"], D=cfg["D"], F=cfg["F"], gamma=cfg["gamma"], n_slots=cfg["n_slots"],
                        fc_dims=cfg["fc_dims"], frame_batch=cfg["frame_batch"], hoist=cfg["hoist"], lanes=lanes,
-                       bsgs_baby=cfg["bsgs_baby"], fc_baby=cfg["fc_baby"])
+                       bsgs_baby=cfg["bsgs_baby"], fc_baby=cfg["fc_baby"], cplx=cplx)
     basis = list(P.q) + list(P.p)
     seed = 77
 
@@ -773,27 +789,29 @@ def oracle_c4_setup(lanes):
 
     rots = cc.required_rotations("gesture", ccfg, P.n)
     rlk = ukey(prng.SID_UNIFORM)
-    gk = {k: ukey(prng.SID_UNIFORM + 100 * (i + 1)) for i, k in enumerate(rots)}
+    gk = {k: ukey(prng.SID_UNIFORM + 100 * (i + 1)) for i, k in enumerate(rots)}  # (+ the conjugation key)
     Ws, bs = fc_weights_padded()
     return P, cfg, ccfg, rlk, gk, Ws, bs
 
 
 class OracleC4Stages:
     """The headline session as the oracle computes it, cut into its stages so that each
-    timed piece of CPU work is bounded: per ciphertext pair (lanes frames) K3 baby steps,
-    K3 inner sums, K3 giant steps, K1 + K6, K2b + frame sum; per session the lane sum + FC1,
-    FC2, FC3 (oracle/circuits.py functions, as they stand).  Stage s consumes stage s-1's
-    output (stage 0 a fresh uniform-residue pair), so cycling through the stages runs the
-    whole chain; the session time is pairs x (sum of pair stages) + (sum of FC stages).
+    timed piece of CPU work is bounded: per frame group (lanes frames: one complex-slot
+    ciphertext, or a (v_re, v_im) pair in the split layout) K3 baby steps, K3 inner sums, K3
+    giant steps, K1 + K6, K2b + frame sum; per session the lane sum + FC1, FC2, FC3
+    (oracle/circuits.py functions, as they stand).  Stage s consumes stage s-1's output
+    (stage 0 a fresh uniform-residue group), so cycling through the stages runs the whole
+    chain; the session time is groups x (sum of group stages) + (sum of FC stages).
     Public-operand encoding (setup) is excluded from every stage time."""
 
     PAIR = ("k3_babies", "k3_inner_sums", "k3_giants", "k1_k6", "k2b_sum")
     FC = ("fc1", "fc2", "fc3")
 
-    def __init__(self, lanes):
+    def __init__(self, lanes, cplx=CPLX):
         from oracle import circuits as cc
         self.cc = cc
-        self.P, self.cfg, self.ccfg, self.rlk, self.gk, Ws, bs = oracle_c4_setup(lanes)
+        self.cplx = bool(cplx)
+        self.P, self.cfg, self.ccfg, self.rlk, self.gk, Ws, bs = oracle_c4_setup(lanes, cplx)
         self.Ws, self.bs = cc.pad_fc(Ws, bs, self.cfg["fc_dims"])
         self.book = cc.PlainBook(self.P)
         self.stages = self.PAIR + self.FC
@@ -815,7 +833,7 @@ class OracleC4Stages:
                            for t, q in enumerate(P.q[: lvl + 1])]) for p in range(2)]
             return orc.Ct(c, lvl, float(2 ** P.scale_bits), slots)
 
-        return [uct(2 * i)], [uct(2 * i + 1)]
+        return ([uct(2 * i)], None) if self.cplx else ([uct(2 * i)], [uct(2 * i + 1)])
 
     def run_stage(self, s):
         cc, ev = self.cc, self.cc.CircuitEvaluator(self.P, self.rlk, self.gk)
@@ -823,13 +841,13 @@ class OracleC4Stages:
         x = self.cache.get(s) if s != "k3_babies" else self._pair()
         e0, t0 = book.encode_s, time.perf_counter()
         if s == "k3_babies":
-            y = cc.k3_baby_steps(ev, x[0], x[1], cfg)
+            y = cc.k3_babies(ev, x[0], cfg) if self.cplx else cc.k3_baby_steps(ev, x[0], x[1], cfg)
         elif s == "k3_inner_sums":
-            y = cc.k3_inner_sums(ev, book, x[0], x[1], cfg)
+            y = cc.k3_inner_sums_c(ev, book, x, cfg) if self.cplx else cc.k3_inner_sums(ev, book, x[0], x[1], cfg)
         elif s == "k3_giants":
-            y = cc.k3_giant_steps(ev, x, cfg)
+            y = cc.k3_giant_steps_c(ev, x, cfg) if self.cplx else cc.k3_giant_steps(ev, x, cfg)
         elif s == "k1_k6":
-            y = cc.k6_notch(ev, book, cc.k1_power(ev, x[0], x[1]), cfg)
+            y = cc.k6_notch(ev, book, cc.k1_power_c(ev, x) if self.cplx else cc.k1_power(ev, x[0], x[1]), cfg)
         elif s == "k2b_sum":
             y = cc.frame_accumulate(ev, cc.k2_doppler_soft_power(ev, x, cfg))
         else:
@@ -877,12 +895,12 @@ def cpu_model():
     return "unknown"
 
 
-def oracle_c4_baseline(lanes):
+def oracle_c4_baseline(lanes, cplx=CPLX):
     """cpu_baseline: the oracle as it stands on the box's host cores (OpenMP across limbs,
     nproc threads) on a bounded sample of the headline session: ONE ciphertext pair
     (lanes frames) through the per-frame chain plus the FC head once, extrapolated to the
     session: frames/s = F / (pairs * t_pair + t_fc)."""
-    st = OracleC4Stages(lanes)
+    st = OracleC4Stages(lanes, cplx)
     for _ in st.stages:
         st.step()
     total, mean = st.session_seconds()
@@ -890,11 +908,11 @@ def oracle_c4_baseline(lanes):
     t_fc = sum(mean[s] for s in st.FC)
     return {"value": st.cfg["F"] / total, "unit": "frames/s", "cores": omp_threads(), "kind": "oracle",
             "cpu": cpu_model(), "stage_seconds": {k: round(v, 2) for k, v in mean.items()},
-            "sample": (f"C4 headline workload (PS4, N=2^16, entry level 19, {lanes} frames per ciphertext): one "
-                       f"ciphertext pair ({lanes} frames) through the per-frame chain ({t_pair:.1f} s) + the FC head "
-                       f"once ({t_fc:.1f} s), public-operand encoding excluded; extrapolated to the session: "
-                       f"F / ({n_pairs(st.cfg)} pairs x t_pair + t_fc); OpenMP across limbs on "
-                       f"{omp_threads()} threads")}
+            "sample": (f"C4 headline workload (PS4, N=2^16, entry level 19, {lanes} frames per ciphertext"
+                       + (", complex slots" if cplx else "") + f"): one frame group ({lanes} frames) through the "
+                       f"per-frame chain ({t_pair:.1f} s) + the FC head once ({t_fc:.1f} s), public-operand encoding "
+                       f"excluded; extrapolated to the session: F / ({n_pairs(st.cfg)} groups x t_group + t_fc); "
+                       f"OpenMP across limbs on {omp_threads()} threads")}
 
 
 def run_reference(args, rank, world):
@@ -905,7 +923,7 @@ def run_reference(args, rank, world):
     stage times)."""
     if rank != 0:
         return None
-    st = OracleC4Stages(args.lanes)
+    st = OracleC4Stages(args.lanes, args.cplx)
     for _ in range(args.warmup):
         st.step(timed=False)
     t0 = time.perf_counter()
@@ -1028,6 +1046,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["mmfhe", "reference"], default="mmfhe")
     ap.add_argument("--lanes", type=int, default=LANES, help="frames per ciphertext (1 = the paper's layout)")
+    ap.add_argument("--cplx", type=int, default=CPLX, help="1: complex slots (DESIGN R28), 0: re / im ciphertexts")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the multi-GPU C5 exchange workload")
     ap.add_argument("--no-e2e", action="store_true")
@@ -1071,7 +1090,7 @@ def main():
         cfg = r["cfg"]
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            cpu = oracle_c4_baseline(args.lanes)
+            cpu = oracle_c4_baseline(args.lanes, args.cplx)
         rl = roofline(r["prof"], peaks, r["int_peaks"])
         out = {
             "metric": METRIC, "value": r["value"], "unit": "frames/s", "n_gpus": world, "steps": args.steps,

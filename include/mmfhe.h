@@ -139,6 +139,14 @@ typedef struct {
                               (n_slots = L*n; unused lanes of the last pair zero); frame_batch then
                               counts ciphertext pairs.  L a power of two with L*n <= N/2 (E_SHAPE) */
     uint32_t fc_baby;      /* FC layers' BSGS baby steps b: min(fc_baby, h) (0: ceil(sqrt(h))) */
+    uint32_t cplx;         /* gesture / k3_doppler_dft chains: 1 = complex slots (DESIGN R28, SURVEY
+                              §8(f)-3): each input ciphertext carries z = v_re + j v_im (complex slot
+                              values; the paper splits re and im into two ciphertexts), so
+                              inputs are ONE ciphertext per frame (group): ceil(F/L) for chain gesture.
+                              K3 multiplies complex diagonals of W (Eq. dft_kernel) -- one product per
+                              diagonal instead of four -- and outputs d = d_re + j d_im; K1 computes
+                              |d|^2 = d Conj(d) with the conjugation key (MMFHE_STEP_CONJ, listed by
+                              mmfhe_chain_required_rotations).  Same depth; 0 = split re/im layout */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */
@@ -163,6 +171,13 @@ mmfhe_status mmfhe_launch_count(mmfhe_ctx *ctx, uint64_t *count);
  * most cap entries, *n = total count (MMFHE_E_LAYOUT if cap too small). */
 mmfhe_status mmfhe_chain_required_rotations(mmfhe_ctx *ctx, const char *chain, const mmfhe_chain_cfg *cfg,
                                             int32_t *steps, size_t cap, size_t *n);
+
+/* Key id of the complex conjugation automorphism X -> X^(2N-1) (DESIGN R28): pass it as the
+ * step of mmfhe_load_galois_key / mmfhe_client_keygen / mmfhe_serialize_key (and of the
+ * HRot primitive, which then conjugates every slot).  It lies outside every normalised
+ * rotation amount [0, N/2).  Its key is the key for sigma_{2N-1}(s); client keygen draws it
+ * from PRNG key index 1 + N/2 (rotation k uses 1 + k). */
+#define MMFHE_STEP_CONJ ((int32_t)(-2147483647 - 1))
 
 /* Evaluation keys in coefficient form, layout [dnum_L][2][L+1+K][N]
  * (b_j then a_j, limbs q_0..q_L then p_0..p_{K-1}); n_words must equal

@@ -59,6 +59,9 @@ class ChainCfg:
     n_taps: tuple = ()          # k5_fir_rot: taps per band (rotation keys for the longest)
     lanes: int = 1              # gesture / K3: frames interleaved per ciphertext (reading R20)
     fc_baby: int = 0            # FC BSGS baby steps (0: ceil(sqrt(h)))
+    cplx: int = 0               # gesture / K3: 1 -> complex slots, z = v_re + j v_im in ONE ciphertext
+                                # per frame (group); K3 multiplies complex diagonals, K1 is z conj(z)
+                                # (reading R28)
 
 
 def log2_exact(x: int, name: str) -> int:
@@ -95,8 +98,9 @@ def lane_vec(v: np.ndarray, L: int) -> np.ndarray:
 
 
 def interleave(frames, L: int, n: int) -> np.ndarray:
-    """Client packing: up to L frame vectors of length n into one slot vector (unused lanes 0)."""
-    out = np.zeros(n * L)
+    """Client packing: up to L frame vectors of length n into one slot vector (unused lanes 0);
+    complex frames give a complex slot vector (reading R28)."""
+    out = np.zeros(n * L, dtype=np.complex128 if any(np.iscomplexobj(v) for v in frames) else np.float64)
     for f, v in enumerate(frames):
         out[f::L] = v
     return out
@@ -368,20 +372,29 @@ def dh(cfg) -> bool:
     return getattr(cfg, "hoist", 0) == 2
 
 
-def k3_baby_steps(ev: CircuitEvaluator, v_re, v_im, cfg: ChainCfg):
-    """K3 BSGS baby steps (P:164-176): [x, Rot(x, s)] for s < b, for v_re and v_im."""
+def cplx_of(cfg) -> bool:
+    """Complex-slot packing (reading R28): one ciphertext z = v_re + j v_im per frame (group)."""
+    return bool(getattr(cfg, "cplx", 0))
+
+
+def k3_babies(ev: CircuitEvaluator, v, cfg: ChainCfg):
+    """[x, Rot(x, s L)] for s < b and every x of the frame list v (the identity step lifted
+    to Q_l u P under double hoisting)."""
     L = lanes_of(cfg)
-    n = v_re[0].n_slots // L
+    n = v[0].n_slots // L
     if n % cfg.D or n < 2 * cfg.D:
         # the 2D-1 offsets of the block-diagonal matrix alias when a period holds one block
         raise ValueError("K3 needs the packing period to be a multiple of D and at least 2D")
     b, _ = k3_schedule(cfg)
     if dh(cfg):
-        xr = [[ev.lift_pq(x) for x in v_re]] + baby_steps(ev, v_re, [s * L for s in range(1, b)], 2)
-        xi = [[ev.lift_pq(x) for x in v_im]] + baby_steps(ev, v_im, [s * L for s in range(1, b)], 2)
-        return xr, xi
-    xr = [list(v_re)] + baby_steps(ev, v_re, [s * L for s in range(1, b)], cfg.hoist)
-    xi = [list(v_im)] + baby_steps(ev, v_im, [s * L for s in range(1, b)], cfg.hoist)
+        return [[ev.lift_pq(x) for x in v]] + baby_steps(ev, v, [s * L for s in range(1, b)], 2)
+    return [list(v)] + baby_steps(ev, v, [s * L for s in range(1, b)], cfg.hoist)
+
+
+def k3_baby_steps(ev: CircuitEvaluator, v_re, v_im, cfg: ChainCfg):
+    """K3 BSGS baby steps (P:164-176): [x, Rot(x, s)] for s < b, for v_re and v_im."""
+    xr = k3_babies(ev, v_re, cfg)
+    xi = k3_babies(ev, v_im, cfg)
     return xr, xi
 
 
@@ -445,6 +458,47 @@ def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg
     return k3_giant_steps(ev, k3_inner_sums(ev, book, xr, xi, cfg), cfg)
 
 
+def k3_inner_sums_c(ev: CircuitEvaluator, book: PlainBook, xs, cfg: ChainCfg):
+    """Complex slots (reading R28): every giant step's inner sum sum_s W~'_{g',s} Rot(z, s)
+    with the complex diagonals of W~ = I_{AR} (x) W (Eq. dft_kernel; Eq. dft_re's
+    d_re + j d_im = (C~ + j S~)(v_re + j v_im)) pre-rotated by -G -- one product
+    per (giant, baby), the complex multiplication done by the slot-wise plaintext product."""
+    L = lanes_of(cfg)
+    n = xs[0][0].n_slots // L
+    lvl = xs[0][0].level
+    W = dsp.dft_matrix(cfg.D)
+    _, giants = k3_schedule(cfg)
+    nf = len(xs[0])
+    vec = book.vec_pq if dh(cfg) else book.vec
+    psum = ev.pmult_sum_pq if dh(cfg) else ev.pmult_sum
+    inner = []
+    for gp, G, babies in giants:
+        pts = [(vec(f"k3.w.{gp}.{s}", lane_vec(rot(block_diag_diagonal(W, n, G + s), -G), L), lvl), s)
+               for s in babies]
+        inner.append([psum([(pt, xs[s][f]) for pt, s in pts]) for f in range(nf)])
+    return inner
+
+
+def k3_giant_steps_c(ev: CircuitEvaluator, inner, cfg: ChainCfg):
+    """Giant rotations of the complex inner sums, summed, one ModDown (double hoisting) and
+    one rescale after the sum (c-6)."""
+    L = lanes_of(cfg)
+    _, giants = k3_schedule(cfg)
+    out = None
+    rot_, add = (ev.rotate_pq, ev.add_pq) if dh(cfg) else (ev.rotate, ev.add)
+    for (gp, G, babies), pr in zip(giants, inner):
+        r = [rot_(x, G * L) for x in pr]
+        out = r if out is None else [add(a, x) for a, x in zip(out, r)]
+    if dh(cfg):
+        out = [ev.moddown_ct(x) for x in out]
+    return [ev.rescale(x) for x in out]
+
+
+def k3_doppler_dft_frames_c(ev: CircuitEvaluator, book: PlainBook, z, cfg: ChainCfg):
+    """K3 on complex-slot frames (reading R28): d = W~ z by BSGS, d in complex slots."""
+    return k3_giant_steps_c(ev, k3_inner_sums_c(ev, book, k3_babies(ev, z, cfg), cfg), cfg)
+
+
 def k3_doppler_dft(ev, book, v_re, v_im, cfg):
     """K3 on one frame."""
     dre, dim = k3_doppler_dft_frames(ev, book, [v_re], [v_im], cfg)
@@ -456,6 +510,13 @@ def k3_doppler_dft(ev, book, v_re, v_im, cfg):
 def k1_power(ev, d_re, d_im):
     """K1 on the K3 output: P = rescale(relin(tensor(d_re,d_re) + tensor(d_im,d_im)))."""
     return ev.relin_rescale_all([ev.tensor_sum([(a, a), (b, b)]) for a, b in zip(d_re, d_im)])
+
+
+def k1_power_c(ev, d):
+    """K1 on complex-slot K3 outputs (reading R28): P = rescale(relin(tensor(d, Conj(d)))),
+    d conj(d) = d_re^2 + d_im^2 in every slot (Eq. energy's |.|^2)."""
+    cj = [ev.conjugate(x) for x in d]
+    return ev.relin_rescale_all([ev.tensor_sum([(a, b)]) for a, b in zip(d, cj)])
 
 
 def k6_notch(ev, book, P_cts, cfg):
@@ -482,15 +543,21 @@ def k2_doppler_soft_power(ev, Pm, cfg):
 
 
 def gesture_frames(ev, book, v_re, v_im, cfg):
-    """Per frame: K3 -> K1 -> K6 -> K2b -> weighting, on a list of frames."""
-    d_re, d_im = k3_doppler_dft_frames(ev, book, v_re, v_im, cfg)
-    P_cts = k1_power(ev, d_re, d_im)
+    """Per frame: K3 -> K1 -> K6 -> K2b -> weighting, on a list of frames.
+    With complex slots (cfg.cplx) v_re holds the frames' z ciphertexts and v_im is None."""
+    if cplx_of(cfg):
+        if v_im is not None:
+            raise ValueError("complex slots: one ciphertext per frame (v_im must be None)")
+        P_cts = k1_power_c(ev, k3_doppler_dft_frames_c(ev, book, v_re, cfg))
+    else:
+        d_re, d_im = k3_doppler_dft_frames(ev, book, v_re, v_im, cfg)
+        P_cts = k1_power(ev, d_re, d_im)
     Pm = k6_notch(ev, book, P_cts, cfg)
     return k2_doppler_soft_power(ev, Pm, cfg)
 
 
 def gesture_frame(ev, book, v_re, v_im, cfg):
-    return gesture_frames(ev, book, [v_re], [v_im], cfg)[0]
+    return gesture_frames(ev, book, [v_re], None if v_im is None else [v_im], cfg)[0]
 
 
 def frame_accumulate(ev, feats):
@@ -506,7 +573,7 @@ def gesture_features(ev, book, v_re, v_im, cfg):
     batch's features summed, batches then added in order."""
     acc = None
     for s, e in chunks(len(v_re), cfg.frame_batch):
-        part = frame_accumulate(ev, gesture_frames(ev, book, v_re[s:e], v_im[s:e], cfg))
+        part = frame_accumulate(ev, gesture_frames(ev, book, v_re[s:e], None if v_im is None else v_im[s:e], cfg))
         acc = part if acc is None else ev.add(acc, part)
     return acc
 
@@ -754,9 +821,11 @@ def rotsum_steps(count: int, stride: int):
 
 
 def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
-    """Rotation amounts (normalised to [0, N/2)) a chain needs."""
+    """Rotation amounts (normalised to [0, N/2)) a chain needs, plus the
+    conjugation key id orc.CONJ where K1 runs on complex slots (reading R28)."""
     half = n_ring // 2
     ks = set()
+    extra = {orc.CONJ} if cplx_of(cfg) and chain in ("gesture_frame", "gesture", "gesture_features") else set()
     if chain == "k5_fir_rot":
         W = max(cfg.n_taps) if getattr(cfg, "n_taps", None) else 0
         b, giants = fir_rot_schedule(W) if W else (1, [])
@@ -777,11 +846,11 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
             out |= {j * stride for j in range(1, min(8, count))}
         return out
 
-    if chain in ("k3_doppler_dft", "gesture_frame", "gesture"):
+    if chain in ("k3_doppler_dft", "gesture_frame", "gesture", "gesture_features"):
         b, giants = k3_schedule(cfg)
         ks |= {s * L for s in range(1, b)}
         ks |= {G * L for _, G, _ in giants if G != 0}
-    if chain in ("k2_doppler_soft_power", "gesture_frame", "gesture"):
+    if chain in ("k2_doppler_soft_power", "gesture_frame", "gesture", "gesture_features"):
         ks |= rotsum_keys(cfg.n_slots // cfg.D, cfg.D * L)
     if chain in ("gesture_fc", "gesture", "fc_forward"):
         ks |= rotsum_keys(L, 1)
@@ -792,4 +861,4 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
             ks |= {s * L for s in range(1, min(b, h))}
             ks |= {G * L for _, G, _ in giants if G != 0}
             ks |= rotsum_keys(dims[layer] // h, h * L)
-    return sorted({k % half for k in ks} - {0})
+    return sorted(({k % half for k in ks} - {0}) | extra)

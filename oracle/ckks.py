@@ -16,6 +16,9 @@ Paper passages:
 Readings where the paper is silent: canonical embedding
 slot j <-> zeta^(5^j mod 2N); left rotation Rot(v,k)[j] = v[(j+k) mod n];
 Galois element g = 5^(k mod N/2) mod 2N; ternary secret; CBD(21) errors.
+Complex slots (reading R28): the same embedding carries a complex
+vector z (coefficients stay real: m(zeta^-e) = conj m(zeta^e)); the conjugation
+automorphism X -> X^(2N-1) conjugates every slot and has its own key (id CONJ).
 """
 from __future__ import annotations
 
@@ -186,8 +189,10 @@ def embed(m: np.ndarray, n_ring: int) -> np.ndarray:
 
 
 def replicate(v: np.ndarray, n_ring: int) -> np.ndarray:
-    """Sparse packing: period-n vector replicated N/(2n) times."""
-    v = np.asarray(v, dtype=np.float64)
+    """Sparse packing: period-n vector replicated N/(2n) times (real, or
+    complex slot values, reading R28)."""
+    v = np.asarray(v)
+    v = v.astype(np.complex128) if np.iscomplexobj(v) else v.astype(np.float64)
     n = len(v)
     assert (n_ring // 2) % n == 0, "packing period must divide N/2"
     return np.tile(v, (n_ring // 2) // n)
@@ -210,10 +215,13 @@ def encode_pq(P: ParamSet, v, scale: float, level: int) -> np.ndarray:
     return small_to_rns(m.astype(np.int64), list(P.q[: level + 1]) + list(P.p))
 
 
-def decode(P: ParamSet, res: np.ndarray, level: int, scale: float, n_slots: int) -> np.ndarray:
+def decode(P: ParamSet, res: np.ndarray, level: int, scale: float, n_slots: int,
+           complex_out: bool = False) -> np.ndarray:
+    """Slot values of a plaintext (real parts, or complex with complex_out, reading R28)."""
     ints = crt_centered(res, P.q[: level + 1])
     m = np.array([float(x) for x in ints]) / float(scale)
-    return embed(m, P.n)[:n_slots].real
+    z = embed(m, P.n)[:n_slots]
+    return z if complex_out else z.real
 
 
 def encode_scalar(c: float, q_l: int) -> int:
@@ -235,9 +243,29 @@ class Keys:
     gk: dict = field(default_factory=dict)  # k (normalised) -> [dnum][2][L+1+K][N]
 
 
+# Key id of the conjugation automorphism (reading R28): outside every normalised rotation
+# amount [0, N/2); the C ABI uses the same value (MMFHE_STEP_CONJ = INT32_MIN).
+CONJ = -(1 << 31)
+
+
 def galois_element(P: ParamSet, k: int) -> int:
-    """g = 5^(k mod N/2) mod 2N; k is normalised to [0, N/2) first."""
+    """g = 5^(k mod N/2) mod 2N; k is normalised to [0, N/2) first.
+    k = CONJ: g = 2N - 1 = -1 mod 2N, the complex conjugation of every slot (reading R28:
+    zeta^(5^j) -> zeta^(-5^j) = conj zeta^(5^j))."""
+    if k == CONJ:
+        return 2 * P.n - 1
     return pow(5, k % (P.n // 2), 2 * P.n)
+
+
+def key_id(P: ParamSet, k: int) -> int:
+    """Normalised Galois-key id: k mod N/2 for a rotation, CONJ for the conjugation."""
+    return CONJ if k == CONJ else k % (P.n // 2)
+
+
+def key_index(P: ParamSet, kid: int) -> int:
+    """PRNG stream index of a Galois key (make_evk): 1 + k for rotation k in [1, N/2),
+    1 + N/2 for the conjugation (0 is the relinearisation key)."""
+    return 1 + P.n // 2 if kid == CONJ else 1 + kid
 
 
 def _full_basis(P: ParamSet):
@@ -286,9 +314,9 @@ def keygen(P: ParamSet, seed: int, rotations=(), relin: bool = True) -> Keys:
     s_res = small_to_rns(s, basis)
     if relin:
         keys.rlk = make_evk(P, s, poly_mul(basis, s_res, s_res), seed, 0)
-    for k in sorted({r % (P.n // 2) for r in rotations} - {0}):
+    for k in sorted({key_id(P, r) for r in rotations} - {0}):
         g = galois_element(P, k)
-        keys.gk[k] = make_evk(P, s, automorphism(basis, s_res, g), seed, 1 + k)
+        keys.gk[k] = make_evk(P, s, automorphism(basis, s_res, g), seed, key_index(P, k))
     return keys
 
 
@@ -336,8 +364,8 @@ def decrypt(P: ParamSet, keys: Keys, ct: Ct) -> np.ndarray:
     return m
 
 
-def decrypt_vector(P, keys, ct: Ct) -> np.ndarray:
-    return decode(P, decrypt(P, keys, ct), ct.level, ct.scale, ct.n_slots)
+def decrypt_vector(P, keys, ct: Ct, complex_out: bool = False) -> np.ndarray:
+    return decode(P, decrypt(P, keys, ct), ct.level, ct.scale, ct.n_slots, complex_out)
 
 
 # --------------------------------------------------------------------------
@@ -455,12 +483,23 @@ class Evaluator:
         if kn not in self.gk:
             raise KeyError(f"missing Galois key for rotation {kn}")
         self._rec("hrot", a.level, str(kn))
-        g = galois_element(P, kn)
+        return self._automorphism_ks(a, galois_element(P, kn), self.gk[kn])
+
+    def _automorphism_ks(self, a: Ct, g: int, evk: np.ndarray) -> Ct:
         qs = self.qs(a.level)
         c0 = automorphism(qs, a.c[0], g)
         c1 = automorphism(qs, a.c[1], g)
-        d0, d1 = self.keyswitch(c1, a.level, self.gk[kn])
+        d0, d1 = self.keyswitch(c1, a.level, evk)
         return Ct([poly_add(qs, c0, d0), d1], a.level, a.scale, a.n_slots)
+
+    def conjugate(self, a: Ct) -> Ct:
+        """Conj (reading R28): (sigma_g c0 + d0, d1), (d0, d1) = KS(sigma_g c1; gk_CONJ) with
+        g = 2N - 1 -- HRot's algorithm with the conjugation's Galois element; every slot
+        value is conjugated."""
+        if CONJ not in self.gk:
+            raise KeyError("missing conjugation key")
+        self._rec("conj", a.level)
+        return self._automorphism_ks(a, galois_element(self.P, CONJ), self.gk[CONJ])
 
     def rotate_hoisted(self, a: Ct, ks) -> list:
         """Hoisted HRot (a separate op): ModUp(c1) once, then per step

@@ -56,27 +56,39 @@ std::vector<double> hann(uint32_t M)
     return w;
 }
 
+typedef std::complex<double> cd;
+
 // Rot(v, k)[j] = v[(j + k) mod n]
-std::vector<double> rot(const std::vector<double> &v, int64_t k)
+template <typename T>
+std::vector<T> rot(const std::vector<T> &v, int64_t k)
 {
     const int64_t n = (int64_t)v.size();
-    std::vector<double> o(n);
+    std::vector<T> o(n);
     for (int64_t j = 0; j < n; ++j) o[j] = v[(size_t)(((j + k) % n + n) % n)];
     return o;
 }
 
 // Lane-interleaved layout (DESIGN R20): a per-frame public vector with every
 // entry repeated L times (slot L i + f holds entry i for every frame lane f).
-std::vector<double> lane_rep(const std::vector<double> &v, uint32_t L)
+template <typename T>
+std::vector<T> lane_rep(const std::vector<T> &v, uint32_t L)
 {
     if (L <= 1) return v;
-    std::vector<double> o(v.size() * L);
+    std::vector<T> o(v.size() * L);
     for (size_t i = 0; i < v.size(); ++i)
         for (uint32_t f = 0; f < L; ++f) o[i * L + f] = v[i];
     return o;
 }
 
 uint32_t lanes_of(const mmfhe_chain_cfg &cfg) { return cfg.lanes ? cfg.lanes : 1; }
+
+// K3 / gesture chains on complex slots (DESIGN R28): one input ciphertext z = v_re + j v_im per
+// frame (group) instead of the (v_re, v_im) pair
+bool cplx_chain(const std::string &chain, const mmfhe_chain_cfg &cfg)
+{
+    return cfg.cplx && (chain == "k3_doppler_dft" || chain == "gesture" || chain == "gesture_frame" ||
+                        chain == "gesture_features");
+}
 
 struct Sched {
     uint32_t b;
@@ -152,6 +164,17 @@ class Runner {
         if (p) return *p;
         MMFHE_REQUIRE(c_.auto_encode, MMFHE_E_MISSING_PLAIN, "missing plaintext operand " + plain_key(key, level));
         encode_plain(c_, name, values(), level, scale, pq);
+        return *c_.find_plain(key, level);
+    }
+    // a complex-valued public vector (DESIGN R28), encoded by the library's complex encoder
+    const DPlain &plain_c(const std::string &name, uint32_t level, double scale,
+                          const std::function<std::vector<cd>()> &values, bool pq = false)
+    {
+        const std::string key = pq ? name + ".pq" : name;
+        DPlain *p = c_.find_plain(key, level);
+        if (p) return *p;
+        MMFHE_REQUIRE(c_.auto_encode, MMFHE_E_MISSING_PLAIN, "missing plaintext operand " + plain_key(key, level));
+        encode_plain_c(c_, name, values(), level, scale, pq);
         return *c_.find_plain(key, level);
     }
     bool dh() const { return cfg_.hoist == 2; }
@@ -338,10 +361,64 @@ class Runner {
         return {copy_ct(c_, slice(r, 0, B)), copy_ct(c_, slice(r, B, B))};
     }
 
+    // K3 on complex slots (DESIGN R28, oracle k3_doppler_dft_frames_c): d = W~ z with the complex
+    // diagonals of I (x) W pre-rotated by -G; one plaintext product per (giant, baby) -- the
+    // complex multiplication is the slot-wise plaintext product -- then the giant rotations
+    DCt k3_doppler_dft_c(const DCt &z)
+    {
+        const uint32_t n = z.n_slots / L(), D = cfg_.D, lvl = z.level;
+        Sched s = k3_schedule(cfg_);
+        std::vector<DCt> xs = baby_steps(z, s.b);
+        std::vector<double> w = hann(D);
+        auto diag = [&](int32_t o, int32_t G) {
+            std::vector<cd> v(n, cd(0, 0));
+            for (uint32_t j = 0; j < n; ++j) {
+                const uint32_t col = (uint32_t)((((int64_t)j + o) % (int64_t)n + n) % n);
+                if (j / D != col / D) continue;
+                const uint32_t d = j % D, m = col % D;
+                const uint32_t sig = (d + D / 2) % D;
+                const double ang = -2.0 * M_PI * (double)sig * (double)m / (double)D;
+                v[j] = w[m] * std::polar(1.0, ang);
+            }
+            return lane_rep(rot(v, -G), L());
+        };
+        std::vector<const DCt *> cts;
+        for (auto &x : xs) cts.push_back(&x);
+        std::vector<std::vector<const DPlain *>> rows;
+        for (auto &g : s.giants) {
+            std::vector<const DPlain *> row(s.b, nullptr);
+            for (uint32_t b : g.babies) {
+                const std::string name = "k3.w." + std::to_string(g.gp) + "." + std::to_string(b);
+                row[b] = &plain_c(name, lvl, qscale(lvl), [&] { return diag(g.G + (int32_t)b, g.G); }, dh());
+            }
+            rows.push_back(row);
+        }
+        std::vector<DCt> inner = ev_diag_mac(c_, cts, rows);
+        DCt out;
+        for (size_t gi = 0; gi < s.giants.size(); ++gi) {
+            const int32_t step = s.giants[gi].G * (int32_t)L();
+            if (gi == 0)
+                out = dh() ? ev_rotate_pq(c_, inner[0], step) : ev_rotate(c_, inner[0], step);
+            else if (dh())
+                ev_rotate_pq_acc(c_, out, inner[gi], step);
+            else
+                out = ev_addsub(c_, out, ev_rotate(c_, inner[gi], step), false);
+        }
+        if (dh()) out = ev_moddown_ct(c_, out);
+        return ev_rescale(c_, out);
+    }
+
     // ---------------------------------------------------------- gesture frame (batched)
     DCt k1_power(const DCt &dre, const DCt &dim)
     {
         return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&dre, &dre}, {&dim, &dim}}));
+    }
+
+    // K1 on complex K3 outputs (oracle k1_power_c): |d|^2 = d Conj(d)
+    DCt k1_power_c(const DCt &d)
+    {
+        DCt cj = ev_conjugate(c_, d);
+        return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&d, &cj}}));
     }
 
     DCt k6_notch(const DCt &P)
@@ -379,6 +456,8 @@ class Runner {
         DCt Pm = k6_notch(P);
         return k2_doppler_soft_power(Pm);
     }
+
+    DCt gesture_frame_c(const DCt &z) { return k2_doppler_soft_power(k6_notch(k1_power_c(k3_doppler_dft_c(z)))); }
 
     // ---------------------------------------------------------- FC
     DCt fc_layer(const DCt &x, uint32_t layer, bool square)
@@ -656,13 +735,18 @@ class Runner {
     // per frame batch: frame kernels, batch sum; batches added in order
     DCt gesture_features(const mmfhe_ct *in, size_t n_in)
     {
-        const uint32_t F = (uint32_t)(n_in / 2), fb = frame_batch(F);
+        const uint32_t F = (uint32_t)(cfg_.cplx ? n_in : n_in / 2), fb = frame_batch(F);
         DCt acc;
         for (uint32_t t0 = 0; t0 < F; t0 += fb) {
             const uint32_t cnt = std::min(fb, F - t0);
-            DCt vre = import_batch(c_, in, 2 * (size_t)t0, 2, cnt);
-            DCt vim = import_batch(c_, in, 2 * (size_t)t0 + 1, 2, cnt);
-            DCt f = gesture_frame(vre, vim);
+            DCt f;
+            if (cfg_.cplx) {
+                f = gesture_frame_c(import_batch(c_, in, t0, 1, cnt));
+            } else {
+                DCt vre = import_batch(c_, in, 2 * (size_t)t0, 2, cnt);
+                DCt vim = import_batch(c_, in, 2 * (size_t)t0 + 1, 2, cnt);
+                f = gesture_frame(vre, vim);
+            }
             DCt part = ev_batch_sum(c_, f);
             acc = t0 == 0 ? std::move(part) : ev_addsub(c_, acc, part, false);
         }
@@ -693,6 +777,11 @@ void validate_cfg(const std::string &chain, const mmfhe_chain_cfg &cfg)
         MMFHE_REQUIRE(cfg.R >= 1 && pow2_or_zero(cfg.R), MMFHE_E_SHAPE, "iq_pack needs R a power of two");
     MMFHE_REQUIRE(pow2_or_zero(cfg.lanes), MMFHE_E_SHAPE, "lanes must be a power of two");
     MMFHE_REQUIRE(cfg.hoist <= 2, MMFHE_E_INVALID_ARG, "hoist must be 0, 1 or 2");
+    MMFHE_REQUIRE(cfg.cplx <= 1, MMFHE_E_INVALID_ARG, "cplx must be 0 or 1");
+    if (cfg.cplx)
+        MMFHE_REQUIRE(cplx_chain(chain, cfg) || chain == "gesture_fc" || chain == "fc_forward" ||
+                          chain == "k2_doppler_soft_power" || chain == "k6_notch",
+                      MMFHE_E_SHAPE, "complex slots apply to the K3 / gesture chains only");
 }
 
 uint32_t chain_depth(const std::string &chain, const mmfhe_chain_cfg &cfg)
@@ -766,6 +855,7 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
             for (uint32_t j = 1; j < std::min<uint32_t>(8, count); ++j) add((int64_t)j * stride);
     };
     if (frames || chain == "k2_doppler_soft_power") add_rotsum(cfg.n_slots / cfg.D, cfg.D * (uint32_t)L);
+    if (frames && cfg.cplx) ks.insert(MMFHE_STEP_CONJ);  // K1 = d Conj(d) (DESIGN R28)
     if (chain == "gesture_fc" || chain == "gesture" || chain == "fc_forward") {
         add_rotsum((uint32_t)L, 1);
         for (int layer = 0; layer < 3; ++layer) {
@@ -797,8 +887,15 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
         MMFHE_REQUIRE(n_in == 2 * (size_t)cfg.F && cfg.F > 0, MMFHE_E_SHAPE, "expected 2F input ciphertexts");
     } else if (chain == "gesture") {
         const size_t L = lanes_of(cfg);
-        MMFHE_REQUIRE(cfg.F > 0 && n_in == 2 * ((cfg.F + L - 1) / L), MMFHE_E_SHAPE,
-                      "expected 2 ceil(F / lanes) input ciphertexts");
+        if (cfg.cplx)
+            MMFHE_REQUIRE(cfg.F > 0 && n_in == (cfg.F + L - 1) / L, MMFHE_E_SHAPE,
+                          "expected ceil(F / lanes) complex-slot input ciphertexts");
+        else
+            MMFHE_REQUIRE(cfg.F > 0 && n_in == 2 * ((cfg.F + L - 1) / L), MMFHE_E_SHAPE,
+                          "expected 2 ceil(F / lanes) input ciphertexts");
+    } else if (cplx_chain(chain, cfg)) {  // k3_doppler_dft / gesture_frame / gesture_features
+        MMFHE_REQUIRE(n_in >= 1, MMFHE_E_SHAPE, "expected one complex-slot ciphertext z per frame (group)");
+        n_out = chain == "gesture_features" ? 1 : n_in;
     } else if (chain == "k3_doppler_dft" || chain == "gesture_frame" || chain == "gesture_features") {
         MMFHE_REQUIRE(n_in >= 2 && n_in % 2 == 0, MMFHE_E_SHAPE, "expected (v_re, v_im) per frame");
         n_out = chain == "k3_doppler_dft" ? n_in : chain == "gesture_frame" ? n_in / 2 : 1;
@@ -885,6 +982,13 @@ std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_c
         out.push_back(std::move(nd.second));
     } else if (chain == "vitals_v2") {
         out = r.vitals_v2(in, n_in);
+    } else if (cplx_chain(chain, cfg) && (chain == "k3_doppler_dft" || chain == "gesture_frame")) {
+        // complex slots: one z per frame (group); per batch one output batch (d, or the features)
+        const uint32_t F = (uint32_t)n_in, fb = r.frame_batch(F);
+        for (uint32_t t0 = 0; t0 < F; t0 += fb) {
+            DCt z = import_batch(c, in, t0, 1, std::min(fb, F - t0));
+            out.push_back(chain == "k3_doppler_dft" ? r.k3_doppler_dft_c(z) : r.gesture_frame_c(z));
+        }
     } else if (chain == "k3_doppler_dft" || chain == "gesture_frame") {
         // frames in batches of cfg.frame_batch; k3 outputs per batch: its d_re items, then its d_im items
         const uint32_t F = (uint32_t)(n_in / 2), fb = r.frame_batch(F);

@@ -269,7 +269,8 @@ mmfhe_status mmfhe_client_keygen(mmfhe_ctx *ctx, uint64_t seed, const int32_t *s
         const InvSrc src{s.get(), (size_t)R * c.n, c.n, R, g};
         ntt_inverse(c, tmp.get(), R, make_map(fb), &src);
         ntt_forward(c, tmp.get(), R, make_map(fb));
-        make_evk(c, key.get(), s.get(), tmp.get(), seed, 1 + (uint64_t)k);
+        // PRNG key index (oracle ckks.key_index): 1 + k for rotation k, 1 + N/2 for the conjugation
+        make_evk(c, key.get(), s.get(), tmp.get(), seed, k == MMFHE_STEP_CONJ ? 1 + (uint64_t)c.n / 2 : 1 + (uint64_t)k);
         copy_out(c, gk + i * kw, key.get(), kw, on_device);
     }
     CUDA_CHECK(cudaStreamSynchronize(c.stream));

@@ -1,6 +1,6 @@
 // encoder.cpp -- the library's own CKKS encoder (setup-time, host): canonical
 // embedding with slot j <-> zeta^(5^j mod 2N), zeta = e^(i pi / N) (P:397-402,
-// "packs up to N/2 real values"); period-n vectors are replicated to N/2
+// "packs up to N/2 real values"; complex slot values for DESIGN R28); period-n vectors are replicated to N/2
 // slots (sparse packing).  Used by mmfhe_encode_plain and
 // mmfhe_prepare_chain; parity tests import the oracle's encodings instead
 // (floating-point encodings are not bit-reproducible across implementations,
@@ -38,16 +38,18 @@ void fft(std::vector<cd> &a, int sign)
 }
 }  // namespace
 
-std::vector<int64_t> encode_real(const Ctx &c, const std::vector<double> &v, double scale)
+// m with m(zeta^(5^j)) = z_j and m(zeta^(-5^j)) = conj z_j: real coefficients for any complex
+// slot vector (DESIGN R28); a real vector is the special case z = conj z.
+std::vector<int64_t> encode_slots(const Ctx &c, const std::vector<cd> &v, double scale)
 {
     const uint32_t n = c.n, half = n / 2;
     MMFHE_REQUIRE(!v.empty() && half % v.size() == 0, MMFHE_E_LAYOUT, "packing period must divide N/2");
     std::vector<cd> E(n, cd(0, 0));
     uint64_t e = 1;
     for (uint32_t j = 0; j < half; ++j) {
-        const double z = v[j % v.size()];
-        E[(e - 1) / 2] = cd(z, 0);
-        E[(2ull * n - e - 1) / 2] = cd(z, 0);
+        const cd z = v[j % v.size()];
+        E[(e - 1) / 2] = z;
+        E[(2ull * n - e - 1) / 2] = std::conj(z);
         e = e * 5 % (2ull * n);
     }
     fft(E, -1);  // b_i = sum_k E_k e^{-2 pi i ik/N}
@@ -61,11 +63,15 @@ std::vector<int64_t> encode_real(const Ctx &c, const std::vector<double> &v, dou
     return m;
 }
 
-void encode_plain(Ctx &c, const std::string &name, const std::vector<double> &v, uint32_t level, double scale,
-                  bool pq)
+std::vector<int64_t> encode_real(const Ctx &c, const std::vector<double> &v, double scale)
 {
-    MMFHE_REQUIRE(level <= c.L, MMFHE_E_DEPTH, "plaintext level above the chain");
-    std::vector<int64_t> m = encode_real(c, v, scale);
+    return encode_slots(c, std::vector<cd>(v.begin(), v.end()), scale);
+}
+
+namespace {
+void store_encoded(Ctx &c, const std::string &name, const std::vector<int64_t> &m, uint32_t level, double scale,
+                   bool pq)
+{
     std::vector<uint32_t> basis = pq ? c.ext_basis(level) : c.q_basis(level);
     std::vector<uint64_t> res(basis.size() * c.n);
     for (size_t i = 0; i < basis.size(); ++i) {
@@ -77,6 +83,21 @@ void encode_plain(Ctx &c, const std::string &name, const std::vector<double> &v,
     }
     load_plain(c, name, level, scale, res.data(), false, pq);
     CUDA_CHECK(cudaStreamSynchronize(c.stream));
+}
+}  // namespace
+
+void encode_plain(Ctx &c, const std::string &name, const std::vector<double> &v, uint32_t level, double scale,
+                  bool pq)
+{
+    MMFHE_REQUIRE(level <= c.L, MMFHE_E_DEPTH, "plaintext level above the chain");
+    store_encoded(c, name, encode_real(c, v, scale), level, scale, pq);
+}
+
+void encode_plain_c(Ctx &c, const std::string &name, const std::vector<cd> &v, uint32_t level, double scale,
+                    bool pq)
+{
+    MMFHE_REQUIRE(level <= c.L, MMFHE_E_DEPTH, "plaintext level above the chain");
+    store_encoded(c, name, encode_slots(c, v, scale), level, scale, pq);
 }
 
 }  // namespace mmfhe

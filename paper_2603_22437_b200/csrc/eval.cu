@@ -731,6 +731,10 @@ DCt ev_relin(Ctx &c, const DCt &a3)
 
 uint64_t galois_element(const Ctx &c, int32_t step, int32_t *normalised)
 {
+    if (step == MMFHE_STEP_CONJ) {  // complex conjugation of every slot (DESIGN R28)
+        if (normalised) *normalised = MMFHE_STEP_CONJ;
+        return 2ull * c.n - 1;
+    }
     const int64_t half = c.n / 2;
     int64_t k = ((int64_t)step % half + half) % half;
     if (normalised) *normalised = (int32_t)k;
@@ -740,18 +744,16 @@ uint64_t galois_element(const Ctx &c, int32_t step, int32_t *normalised)
 const DKey &find_gk(const Ctx &c, int32_t k)
 {
     auto it = c.gk.find(k);
-    MMFHE_REQUIRE(it != c.gk.end(), MMFHE_E_MISSING_KEY, "missing Galois key for rotation " + std::to_string(k));
+    MMFHE_REQUIRE(it != c.gk.end(), MMFHE_E_MISSING_KEY,
+                  k == MMFHE_STEP_CONJ ? std::string("missing conjugation key")
+                                       : "missing Galois key for rotation " + std::to_string(k));
     return *it->second;
 }
 
-DCt ev_rotate(Ctx &c, const DCt &a, int32_t step)
+namespace {
+// HRot's algorithm for Galois element g (a rotation, or the conjugation)
+DCt automorphism_ks(Ctx &c, const DCt &a, uint64_t g, const DKey &key)
 {
-    MMFHE_REQUIRE(a.npolys == 2, MMFHE_E_LAYOUT, "rotate needs a 2-poly ciphertext");
-    int32_t k;
-    const uint64_t g = galois_element(c, step, &k);
-    if (k == 0) return copy_ct(c, a);
-    const DKey &key = find_gk(c, k);
-    rec_n(c, "hrot", a.level, a.batch, std::to_string(k));
     DCt r = make_ct(c, a.level, 2, a.n_slots, a.scale, a.batch);
     // sigma_g fused: into the INTT's first read (c1), the inner product's reads of the
     // digit-own rows (sigma_g c1) and ModDown's addend (sigma_g c0)
@@ -761,6 +763,24 @@ DCt ev_rotate(Ctx &c, const DCt &a, int32_t step)
                   a.data(), nullptr, a.item_words(), g32, 1, g32);
     return r;
 }
+}  // namespace
+
+DCt ev_rotate(Ctx &c, const DCt &a, int32_t step)
+{
+    MMFHE_REQUIRE(a.npolys == 2, MMFHE_E_LAYOUT, "rotate needs a 2-poly ciphertext");
+    int32_t k;
+    const uint64_t g = galois_element(c, step, &k);
+    if (k == 0) return copy_ct(c, a);
+    const DKey &key = find_gk(c, k);
+    if (k == MMFHE_STEP_CONJ)
+        rec_n(c, "conj", a.level, a.batch);
+    else
+        rec_n(c, "hrot", a.level, a.batch, std::to_string(k));
+    return automorphism_ks(c, a, g, key);
+}
+
+// Conj (DESIGN R28, oracle Evaluator.conjugate): every slot value conjugated
+DCt ev_conjugate(Ctx &c, const DCt &a) { return ev_rotate(c, a, MMFHE_STEP_CONJ); }
 
 DCt ev_rescale(Ctx &c, const DCt &a)
 {

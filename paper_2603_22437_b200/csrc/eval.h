@@ -6,6 +6,7 @@
 // Every op works on a batch of B ciphertexts in one set of launches and records
 // one logical op per item in the ctx trace (item order).
 #pragma once
+#include <complex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -55,7 +56,9 @@ DCt ev_lincomb_mat(Ctx &c, const DCt &in, uint32_t J, uint32_t W, int lo0, int l
 void ev_keyswitch(Ctx &c, const uint64_t *x_ntt, size_t xs, uint32_t level, uint32_t B, const DKey &key,
                   uint64_t *out, size_t os, const uint64_t *add0, const uint64_t *add1, size_t as);
 DCt ev_relin(Ctx &c, const DCt &a3);
-DCt ev_rotate(Ctx &c, const DCt &a, int32_t step);
+DCt ev_rotate(Ctx &c, const DCt &a, int32_t step);  // step MMFHE_STEP_CONJ: records "conj"
+// Conj (DESIGN R28): every slot value conjugated (HRot with g = 2N - 1 and the conjugation key)
+DCt ev_conjugate(Ctx &c, const DCt &a);
 // sum over the m items of each of S sessions (all = [S][m] items) of x (x) x
 DCt ev_square_sum_items(Ctx &c, const DCt &all, uint32_t m, uint32_t S);
 // Hoisted HRot: one ModUp of c1 shared by every step; per step the
@@ -93,6 +96,9 @@ void load_plain(Ctx &c, const std::string &name, uint32_t level, double scale, c
                 bool on_device, bool pq = false);
 // host encoder (canonical embedding), csrc/encoder.cpp
 std::vector<int64_t> encode_real(const Ctx &c, const std::vector<double> &v, double scale);
+// complex slot values (DESIGN R28): the same canonical-embedding encoder, z_j and conj z_j
+void encode_plain_c(Ctx &c, const std::string &name, const std::vector<std::complex<double>> &v, uint32_t level,
+                    double scale, bool pq = false);
 void encode_plain(Ctx &c, const std::string &name, const std::vector<double> &v, uint32_t level, double scale,
                   bool pq = false);
 // exact round-half-away(v * q_scale) reduced mod m

@@ -201,7 +201,7 @@ def test_frame_sharded_exchange_with_ckks_partials_world2():
     procs = [ctx.Process(target=_exchange_worker, args=(r, 2, port, 4401, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=300) for _ in procs]
+    res = [q.get(timeout=900) for _ in procs]
     for p in procs:
         p.join(timeout=60)
     assert sorted(r[1] for r in res) == ["ok", "ok"], res

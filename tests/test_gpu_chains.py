@@ -29,7 +29,7 @@ def _mcfg(m, cfg: cc.ChainCfg, bins=(), taps=()):
                        taylor_order=cfg.taylor_order, n_slots=cfg.n_slots, bsgs_baby=cfg.bsgs_baby,
                        fc_dims=cfg.fc_dims, notch_width=cfg.notch_width, bands_bins=bins,
                        n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch, hoist=cfg.hoist,
-                       vp_plus=cfg.vp_plus, iq_pack=cfg.iq_pack, lanes=cfg.lanes)
+                       vp_plus=cfg.vp_plus, iq_pack=cfg.iq_pack, lanes=cfg.lanes, cplx=cfg.cplx)
 
 
 def _run(m, P, keys, book, chain, cfg, cts, want, scalars=None, bins=(), taps=()):
@@ -314,6 +314,47 @@ def test_gesture_chain_lanes_small(m, lanes, F, fb, hoist):
     book2 = cc.PlainBook(P)
     dre, dim = cc.k3_doppler_dft_frames(ev2, book2, cts[0:2:2], cts[1:2:2], cfg)
     _run(m, P, keys, book2, "k3_doppler_dft", cfg, cts[:2], dre + dim)
+
+
+@pytest.mark.parametrize("lanes,F,fb,hoist", [(1, 2, 0, 0), (1, 3, 2, 1), (2, 5, 2, 2), (4, 6, 0, 2)])
+def test_gesture_chain_complex_small(m, lanes, F, fb, hoist):
+    """Complex-slot gesture pipeline (cfg.cplx, DESIGN R28): one ciphertext z = v_re + j v_im
+    per frame group, K3 with complex diagonals (one plaintext product per diagonal), K1 as
+    d Conj(d) with the conjugation key: residues and trace equal the oracle's for the whole
+    chain, and for K3 and the per-frame chain on their own; the required key set ends with
+    the conjugation key id."""
+    P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
+    cfg, Zt = _gesture(P, 3241, F=F, frame_batch=fb, hoist=hoist)
+    cfg.lanes, cfg.cplx = lanes, 1
+    rots = cc.required_rotations("gesture", cfg, P.n)
+    assert rots[0] == orc.CONJ == m.STEP_CONJ
+    keys = orc.keygen(P, seed=3242, rotations=rots)
+    n = cfg.n_slots
+    vs = [radar.pack_doppler(Zt[t]) for t in range(F)]
+    cts = [orc.encrypt_vector(P, keys, cc.interleave(vs[g * lanes:(g + 1) * lanes], lanes, n), P.L, seed=3243, index=g)
+           for g in range(cc.n_packed(F, lanes))]
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    feat = cc.gesture_features(ev, book, cts, None, cfg)
+    dims = cfg.fc_dims
+    Ws, bs = radar.fc_weights([dims[0], dims[1], dims[2], 5], seed=3244)
+    logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
+    ctx = _run(m, P, keys, book, "gesture", cfg, cts, [logits])
+    assert ctx.trace() == ev.trace
+    assert ("conj", P.L - 1, "") in ev.trace
+    assert sorted(ctx.required_rotations("gesture", _mcfg(m, cfg))) == rots
+    ev2 = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book2 = cc.PlainBook(P)
+    d = cc.k3_doppler_dft_frames_c(ev2, book2, cts[:1], cfg)
+    c2 = _run(m, P, keys, book2, "k3_doppler_dft", cfg, cts[:1], d)
+    assert c2.trace() == ev2.trace
+    ev3 = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book3 = cc.PlainBook(P)
+    f0 = cc.gesture_frame(ev3, book3, cts[0], None, cfg)
+    _run(m, P, keys, book3, "gesture_frame", cfg, cts[:1], [f0])
+    # the split layout's input count is rejected for complex slots, and vice versa
+    with pytest.raises(m.MmfheError):
+        ctx.chain_plan("gesture", _mcfg(m, cfg), P.L, 2 * len(cts))
 
 
 def test_frame_sharded_gesture_exchange(m):

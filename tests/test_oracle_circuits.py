@@ -558,3 +558,71 @@ def test_double_hoisted_rotsum_equals_rotsum(count, inner):
     ops = [op for op, _, _ in ev.trace]
     assert ops.count("hrot_hoisted_pq") == a - 1 and ops.count("moddown") == 1
     assert ops.count("hrot") == int(np.log2(count // a))
+
+
+# ------------------------------------------------------------------ complex slots (reading R28)
+
+@pytest.mark.parametrize("hoist,L", [(1, 1), (2, 2)])
+def test_complex_k3_decrypts_to_dft(Pg, hoist, L):
+    """K3 on complex slots (cfg.cplx): z = v_re + j v_im in one ciphertext, complex diagonals
+    of W~ -- decrypts (complex decode) to fftshift(fft(hann x)) per block and
+    lane, with half the baby steps and giant rotations of the split layout."""
+    P = Pg
+    cfg, Zt = _gesture_setup(P, F=2)
+    cfg.hoist, cfg.lanes, cfg.cplx = hoist, L, 1
+    n = cfg.n_slots
+    keys = orc.keygen(P, seed=2301, rotations=cc.required_rotations("k3_doppler_dft", cfg, P.n))
+    assert orc.CONJ not in keys.gk  # K3 alone needs no conjugation
+    vs = [radar.pack_doppler(Zt[t]) for t in range(L)]
+    cz = _enc(P, keys, cc.interleave(vs, L, n), P.L, 0)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    d = cc.k3_doppler_dft_frames_c(ev, cc.PlainBook(P), [cz], cfg)[0]
+    b, giants = cc.k3_schedule(cfg)
+    ops = [op for op, _, _ in ev.trace]
+    base = "hrot_hoisted_pq" if hoist == 2 else "hrot_hoisted"
+    assert ops.count(base) == b - 1
+    assert ops.count("hrot_pq" if hoist == 2 else "hrot") == sum(1 for _, G, _ in giants if G)
+    assert d.level == P.L - 1
+    got = orc.decrypt_vector(P, keys, d, complex_out=True)
+    for f in range(L):
+        want = dsp.doppler_dft(vs[f], cfg.D)
+        assert rel_err(got[f::L], want) < 1e-3
+
+
+@pytest.mark.parametrize("hoist", [1, 2])
+def test_complex_gesture_pipeline(Pg, hoist):
+    """The gesture pipeline on complex slots (one ciphertext per frame group, 2 lanes): per
+    frame P = |d|^2 by d Conj(d) (one conjugation key switch per ciphertext), features and
+    logits decrypt to the plaintext DSP, argmax agrees, depth unchanged (11)."""
+    P = Pg
+    F, L = 4, 2
+    cfg, Zt = _gesture_setup(P, F=F)
+    cfg.hoist, cfg.lanes, cfg.cplx = hoist, L, 1
+    n = cfg.n_slots
+    rots = cc.required_rotations("gesture", cfg, P.n)
+    assert orc.CONJ in rots and rots[0] == orc.CONJ
+    keys = orc.keygen(P, seed=2302, rotations=rots)
+    vs = [radar.pack_doppler(Zt[t]) for t in range(F)]
+    z = [_enc(P, keys, cc.interleave(vs[g * L:(g + 1) * L], L, n), P.L, g) for g in range(2)]
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    fr = cc.gesture_frames(ev, book, z, None, cfg)
+    assert [op for op, _, _ in ev.trace].count("conj") == 2
+    fp = [dsp.gesture_frame_features(v, cfg.A, cfg.R, cfg.D, cfg.gamma) for v in vs]
+    for g, c in enumerate(fr):
+        dec = orc.decrypt_vector(P, keys, c)
+        for f in range(L):
+            assert np.max(np.abs(dec[f::L] - fp[g * L + f])) <= 1e-3 * np.max(np.abs(fp))
+    feat = cc.frame_accumulate(ev, fr)
+    xp = np.sum(fp, axis=0)
+    dims = cfg.fc_dims
+    Ws, bs = radar.fc_weights([dims[0], dims[1], dims[2], 5], seed=7)
+    Ws[0] = Ws[0] / max(np.max(np.abs(Ws[0] @ xp)), 1e-30) * 0.8
+    logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
+    assert logits.level == P.L - 11
+    got = orc.decrypt_vector(P, keys, logits)[cc.logit_slots(5, L)]
+    want = dsp.mlp_forward(xp, Ws, bs)
+    assert rel_err(got, want) < 1e-3
+    assert int(np.argmax(got)) == int(np.argmax(want))
+    with pytest.raises(ValueError):
+        cc.gesture_frames(ev, book, z, z, cfg)

@@ -188,3 +188,74 @@ def test_paper_vital_parameter_set_reproduces_published_sizes():
     assert P.dnum() * 2 * (len(P.q) + len(P.p)) * P.n * 8 / MiB == 22.5
     assert sum(q.bit_length() for q in P.q + P.p) <= 881
     assert all((q - 1) % (2 * P.n) == 0 for q in P.q + P.p)
+
+
+# ------------------------------------------------------------------ complex slots (reading R28)
+
+def test_complex_embedding_is_evaluation_at_roots():
+    """A complex slot vector z encodes to REAL coefficients m with m(zeta^(5^j)) = z_j (the
+    polynomial evaluated directly at the roots, N = 16), and m(zeta^(-5^j)) = conj z_j."""
+    n = 16
+    rng = np.random.default_rng(3)
+    z = rng.normal(size=n // 2) + 1j * rng.normal(size=n // 2)
+    m = orc.embed_inverse(z, n)
+    assert m.dtype.kind == "f"
+    for j in range(n // 2):
+        e = pow(5, j, 2 * n)
+        assert abs(np.polyval(m[::-1], np.exp(1j * np.pi * e / n)) - z[j]) < 1e-9
+        assert abs(np.polyval(m[::-1], np.exp(-1j * np.pi * e / n)) - np.conj(z[j])) < 1e-9
+
+
+def test_conjugation_automorphism_conjugates_slots():
+    """sigma_{2N-1} (X -> X^-1 = -X^(N-1)) applied to the coefficients written out by hand
+    conjugates every slot (N = 32), and orc.galois_element maps CONJ to 2N - 1."""
+    n = 32
+    P = toy(log_n=5, n_q=2, scale_bits=30, n_p=1, alpha=2)
+    assert orc.galois_element(P, orc.CONJ) == 2 * n - 1
+    rng = np.random.default_rng(4)
+    z = rng.uniform(-1, 1, n // 2) + 1j * rng.uniform(-1, 1, n // 2)
+    m = np.rint(orc.embed_inverse(z, n) * 2 ** 30).astype(np.int64)
+    out = np.zeros(n)
+    out[0] = m[0]
+    out[1:] = -m[1:][::-1]  # X^i -> X^(-i) = -X^(N-i)
+    got = orc.embed(out / 2 ** 30, n)
+    assert np.max(np.abs(got - np.conj(z))) < 1e-6
+
+
+def test_complex_slots_encrypted(P):
+    """Complex slot vectors through the evaluator: encrypt -> decrypt, Conj (the conjugation
+    key switch), rotation, and the slot-wise complex product z w and z conj(z) = |z|^2."""
+    keys = orc.keygen(P, seed=321, rotations=[3, orc.CONJ])
+    assert orc.CONJ in keys.gk and 3 in keys.gk
+    rng = np.random.default_rng(9)
+    h = P.n // 2
+    z = rng.uniform(-1, 1, h) + 1j * rng.uniform(-1, 1, h)
+    w = rng.uniform(-1, 1, h) + 1j * rng.uniform(-1, 1, h)
+    lvl = P.L
+    cz = orc.encrypt_vector(P, keys, z, lvl, seed=5, index=0)
+    cw = orc.encrypt_vector(P, keys, w, lvl, seed=5, index=1)
+    dec = orc.decrypt_vector(P, keys, cz, complex_out=True)
+    assert np.max(np.abs(dec - z)) < 1e-6
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, cz) - z.real)) < 1e-6
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    cj = ev.conjugate(cz)
+    assert ev.trace[-1] == ("conj", lvl, "")
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, cj, complex_out=True) - np.conj(z))) < 1e-6
+    r = ev.rotate(cz, 3)
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, r, complex_out=True) - np.roll(z, -3))) < 1e-6
+    zw = ev.mul_rescale(cz, cw)
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, zw, complex_out=True) - z * w)) < 1e-5
+    p = orc.decrypt_vector(P, keys, ev.mul_rescale(cz, cj), complex_out=True)
+    assert np.max(np.abs(p.real - np.abs(z) ** 2)) < 1e-5 and np.max(np.abs(p.imag)) < 1e-5
+    with pytest.raises(KeyError):
+        orc.Evaluator(P, keys.rlk, {3: keys.gk[3]}).conjugate(cz)
+
+
+def test_real_encoding_unchanged_by_complex_support(P):
+    """A real vector and the same vector as complex with zero imaginary parts encode to the
+    same integers (the real path is the complex path's special case)."""
+    rng = np.random.default_rng(11)
+    v = rng.uniform(-1, 1, 64)
+    a = orc.encode(P, v, 2.0 ** 30, 1)
+    b = orc.encode(P, v.astype(np.complex128), 2.0 ** 30, 1)
+    assert np.array_equal(a, b)

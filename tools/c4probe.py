@@ -23,6 +23,8 @@ ap.add_argument("--hoist", type=int, default=1)
 ap.add_argument("--params", default="PS4")
 ap.add_argument("--bsgs", type=int, default=0, help="K3 baby steps b (0: ceil(sqrt(2D-1)))")
 ap.add_argument("--fc-baby", type=int, default=0)
+ap.add_argument("--cplx", type=int, default=0, help="complex slots (DESIGN R28)")
+ap.add_argument("--split", action="store_true", help="also profile gesture_features and gesture_fc on their own")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
@@ -31,7 +33,7 @@ F = args.frames
 stream = torch.cuda.current_stream(dev)
 cfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8),
                   frame_batch=25 if args.lanes == 1 else 0, hoist=args.hoist, lanes=args.lanes, bsgs_baby=args.bsgs,
-                  fc_baby=args.fc_baby)
+                  fc_baby=args.fc_baby, cplx=args.cplx)
 ctx = m.Context.from_params(P, device=0, stream=stream.cuda_stream)
 gen = torch.Generator(device=dev)
 gen.manual_seed(77)
@@ -44,7 +46,7 @@ Ws, bs = radar.fc_weights([4096, 64, 32, 5], seed=11)
 Ws[-1] = np.vstack([Ws[-1], np.zeros((3, 32))])
 bs[-1] = np.concatenate([bs[-1], np.zeros(3)])
 ctx.prepare_chain("gesture", cfg, 19, fc_w=Ws, fc_b=bs)
-n_in = 2 * -(-F // max(args.lanes, 1))
+n_in = (1 if args.cplx else 2) * -(-F // max(args.lanes, 1))
 data = bench.uniform_dev(torch, gen, (n_in, 2, 20), list(P.q[:20]), P.n, dev)
 ins = m.CtArray([m.Ct(data[i], 19, 2.0 ** P.scale_bits, cfg.n_slots * max(args.lanes, 1), P.log_n)
                   for i in range(n_in)])
@@ -64,3 +66,23 @@ if args.profile:
     print(f"gesture F={F}: kernel sum {tot:.2f} ms ({tot / F:.3f} ms/frame)")
     for k, (c, ms, by, ops) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
         print(f"   {k:16s} {ms:8.2f} ms {ms / tot:6.3f}  {c:5d} launches  {by / (ms * 1e-3) / 1e9:7.1f} GB/s")
+
+if args.profile and args.split:
+    # the per-frame part (K3 -> K1 -> K6 -> K2b, pair sum) and the FC head (lane sum + 3 layers)
+    fo = m.CtArray([m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=dev), lv, 0.0, 0, P.log_n)
+                    for lv in ctx.chain_plan("gesture_features", cfg, 19, n_in)])
+    stages = [("gesture_features", ins, fo)]
+    lf = ctx.chain_plan("gesture_features", cfg, 19, n_in)[0]
+    fc_out = m.CtArray([m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=dev), lv, 0.0, 0, P.log_n)
+                        for lv in ctx.chain_plan("gesture_fc", cfg, lf, 1)])
+    stages.append(("gesture_fc", fo, fc_out))
+    for name, i_, o_ in stages:
+        ctx.eval_chain(name, cfg, i_, o_)
+        torch.cuda.synchronize()
+        ctx.profile()
+        ctx.eval_chain(name, cfg, i_, o_)
+        prof = ctx.profile()
+        tot = sum(v[1] for v in prof.values())
+        print(f"{name}: kernel sum {tot:.2f} ms")
+        for k, (c, ms, by, ops) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+            print(f"   {k:16s} {ms:8.2f} ms {ms / tot:6.3f}  {c:5d} launches  {by / (ms * 1e-3) / 1e9:7.1f} GB/s")
