@@ -199,12 +199,10 @@ class Runner {
     {
         const uint32_t a = std::min<uint32_t>(8, count);
         if (!dh() || a <= 1) return ev_rotsum(c_, x, count, stride);
-        DCt acc = ev_lift_pq(c_, x);
         std::vector<int32_t> st;
         for (uint32_t j = 1; j < a; ++j) st.push_back((int32_t)(stride * j));
-        std::vector<DCt> rots = ev_rotate_hoisted_pq(c_, x, st);
-        for (auto &r : rots) acc = ev_addsub(c_, acc, r, false);
-        DCt t = ev_moddown_ct(c_, acc);
+        // lift + the a-1 PQ steps summed in one pass (k_hoisted_rotsum_pq), one ModDown
+        DCt t = ev_moddown_ct(c_, ev_rotsum_hoisted_pq(c_, x, st));
         return ev_rotsum(c_, t, count / a, stride * a);
     }
 

@@ -863,6 +863,34 @@ DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride)
 // ------------------------------------------------------------------ double hoisting
 // (SURVEY §8(c)-5 "a third op"; oracle Evaluator.lift_pq / hoisted_step_pq / rotate_pq /
 // add_pq / moddown_ct, pmult_sum_pq)
+DCt ev_rotsum_hoisted_pq(Ctx &c, const DCt &a, const std::vector<int32_t> &steps)
+{
+    MMFHE_REQUIRE(a.npolys == 2 && !a.pk, MMFHE_E_LAYOUT, "rotate needs a 2-poly Q ciphertext");
+    const uint32_t l = a.level, B = a.batch;
+    std::vector<const uint64_t *> keys;
+    std::vector<uint32_t> gs;
+    std::vector<int32_t> ks;
+    for (int32_t s : steps) {
+        int32_t k;
+        const uint64_t g = galois_element(c, s, &k);
+        MMFHE_REQUIRE(k != 0 && k != MMFHE_STEP_CONJ, MMFHE_E_INVALID_ARG, "hoisted rotate-and-sum steps are rotations");
+        keys.push_back(find_gk(c, k).buf.get());
+        gs.push_back((uint32_t)g);
+        ks.push_back(k);
+    }
+    MMFHE_REQUIRE(!keys.empty() && keys.size() <= (size_t)kDiagMax && c.modup[l].size() <= 8, MMFHE_E_LAYOUT,
+                  "hoisted rotate-and-sum: 1..16 steps, <= 8 digits");
+    // the oracle's op sequence (rotsum_dh_all): lift, the PQ steps, their PQ additions
+    rec_n(c, "lift_pq", l, B);
+    for (int32_t k : ks) rec_n(c, "hrot_hoisted_pq", l, B, std::to_string(k));
+    for (size_t i = 0; i < ks.size(); ++i) rec_n(c, "hadd_pq", l, B);
+    ModUpOut m = ks_modup(c, a.poly(1), a.item_words(), l, B);
+    DCt r = make_pq(c, l, a.n_slots, a.scale, B);
+    launch_hoisted_rotsum_pq(c, r.data(), r.item_words(), a.poly(1), a.item_words(), m.y.get(), m.T * c.n, m.off,
+                             a.data(), a.item_words(), keys, gs, l, B);
+    return r;
+}
+
 DCt ev_lift_pq(Ctx &c, const DCt &a)
 {
     MMFHE_REQUIRE(a.npolys == 2 && !a.pk, MMFHE_E_LAYOUT, "lift needs a 2-poly Q ciphertext");

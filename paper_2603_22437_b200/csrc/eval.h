@@ -75,6 +75,9 @@ DCt ev_rotsum(Ctx &c, const DCt &a, uint32_t count, uint32_t stride);
 // double-hoisted BSGS (SURVEY §8(c)-5 third op): ciphertexts over Q_l u P (DCt::pk = K)
 DCt ev_lift_pq(Ctx &c, const DCt &a);                                                    // (P c0, P c1)
 std::vector<DCt> ev_rotate_hoisted_pq(Ctx &c, const DCt &a, const std::vector<int32_t> &steps);  // no ModDown
+// lift_pq(a) + sum of ev_rotate_hoisted_pq(a, steps) over Q_l u P in one pass (R27's first level; records
+// the lift, the steps and the PQ additions it replaces)
+DCt ev_rotsum_hoisted_pq(Ctx &c, const DCt &a, const std::vector<int32_t> &steps);
 DCt ev_rotate_pq(Ctx &c, const DCt &a, int32_t step);  // ModDown(a1), sigma_g, key switch kept over Q_l u P
 // acc += ev_rotate_pq(a, step), fused (the inner product accumulates into acc); records
 // "hrot_pq" then "hadd_pq" per item

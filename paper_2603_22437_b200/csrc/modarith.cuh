@@ -75,12 +75,17 @@ __device__ __forceinline__ uint64_t shoup_lazy4(uint64_t a, uint64_t w, uint64_t
     uint64_t Q;
     asm("{\n\t.reg .u32 al, ah, wl, wh, t1, t2;\n\t.reg .u64 s;\n\t"
         "mov.b64 {al, ah}, %1;\n\tmov.b64 {wl, wh}, %2;\n\t"
-        "mul.hi.u32 t1, ah, wl;\n\tmul.hi.u32 t2, al, wh;\n\t"
-        "add.cc.u32 t1, t1, t2;\n\taddc.u32 t2, 0, 0;\n\t"
+        "mul.hi.u32 t1, ah, wl;\n\tmad.hi.cc.u32 t1, al, wh, t1;\n\taddc.u32 t2, 0, 0;\n\t"
         "mov.b64 s, {t1, t2};\n\tmad.wide.u32 %0, ah, wh, s;\n\t}"
         : "=l"(Q)
         : "l"(a), "l"(wp));
-    return a * w - Q * q;
+    // a w - Q q = a w + Q (2^64 - q) mod 2^64: with -q a (hoisted) operand the two low products chain
+    // into one another (IMAD.WIDE accumulate) and no 64-bit negation is issued per butterfly; the asm
+    // keeps the compiler from folding it back into a subtraction
+    const uint64_t nq = 0 - q;
+    uint64_t r;
+    asm("mul.lo.u64 %0, %1, %2;\n\tmad.lo.u64 %0, %3, %4, %0;" : "=&l"(r) : "l"(Q), "l"(nq), "l"(a), "l"(w));
+    return r;
 }
 
 // Montgomery reduction of x = hi*2^64 + lo < q*2^64: returns x*2^-64 mod q in [0, 2q).

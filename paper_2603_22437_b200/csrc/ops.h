@@ -56,6 +56,12 @@ void launch_hoisted_ip_pq(Ctx &c, const uint64_t *x, size_t xs, const uint64_t *
                           const std::vector<size_t> &off, const uint64_t *c0, size_t cs,
                           const std::vector<const uint64_t *> &keys, const std::vector<uint32_t> &ginv,
                           const std::vector<uint64_t *> &outs, size_t os, uint32_t level, uint32_t B);
+// Double hoisting's first rotate-and-sum level in one pass: out (PQ ciphertexts, item stride os) =
+// (P c0, P c1) + sum_s (P sigma_s(c0) + IP_s,0, IP_s,1), g[s] the Galois element of step s.
+void launch_hoisted_rotsum_pq(Ctx &c, uint64_t *out, size_t os, const uint64_t *x, size_t xs, const uint64_t *y,
+                              size_t ys, const std::vector<size_t> &off, const uint64_t *c0, size_t cs,
+                              const std::vector<const uint64_t *> &keys, const std::vector<uint32_t> &g,
+                              uint32_t level, uint32_t B);
 // double hoisting: Q rows of out (+)= [P]_{q_i} sigma_g(src) for npoly polys per
 // item (out / src item strides os / ss, poly strides ops / sps): the identity baby step's P lift
 // (the other PQ addends are the key inner product's fused epilogue, IPEpi)

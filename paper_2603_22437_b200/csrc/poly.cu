@@ -393,6 +393,97 @@ __global__ void __launch_bounds__(kHTile) k_hoisted_ip_pq(const uint64_t *__rest
     }
 }
 
+// Double hoisting's first rotate-and-sum level (R27) in ONE pass: for every item b, PQ row r and
+// coefficient j, the sum of the lift and of every hoisted PQ step s,
+//   acc_0[j] = [P]_r c0[j] + sum_s ( IP_s,0[j] + [P]_r c0[perm_s(j)] ),   acc_1[j] = [P]_r c1[j] + sum_s IP_s,1[j]
+// with IP_s,p[j] = sum_d src_d[perm_s(j)] evk_s[d][p][j] (Q rows: [P]_r terms; P rows: the inner products
+// only) -- the oracle's lift_pq + hoisted_step_pq + add_pq chain (rotsum_dh_all), whose modular sum is exact
+// in any order.  The thread owns the OUTPUT index j and gathers the sources at perm_s(j) (an aligned
+// 32-word span maps onto an aligned span: the gathers stay coalesced, and a row's sources stay L2-resident
+// across its CTAs), so the steps accumulate in registers and only the sum reaches HBM: no per-step PQ
+// outputs and no PQ additions.  Every key word is read once (staged in the thread's own shared-memory
+// column, reused across the batch items).
+constexpr int kRTile = 128;
+struct HoistSumArgs {
+    const uint64_t *key[kDiagMax];
+    uint32_t g[kDiagMax];  // Galois elements of the steps (perm_s)
+    size_t y_off[16];
+    uint32_t lo[16], hi[16];
+    size_t xs, ys, cs, os;  // item strides: x (c1), y (ModUp'd digits), c0, output
+    uint32_t dnum, level, L, K, B, nsteps;
+};
+
+template <int DMAX>
+__global__ void __launch_bounds__(kRTile) k_hoisted_rotsum_pq(uint64_t *__restrict__ out, const uint64_t *__restrict__ x,
+                                                            const uint64_t *__restrict__ y,
+                                                            const uint64_t *__restrict__ c0,
+                                                            const TwPair *__restrict__ pmod, KTables kt,
+                                                            HoistSumArgs a)
+{
+    extern __shared__ uint64_t sk[];  // [nsteps][2 dnum][kRTile] key words (each thread its own column)
+    uint32_t *sj = reinterpret_cast<uint32_t *>(sk + (size_t)a.nsteps * 2 * a.dnum * kRTile);  // [nsteps][kRTile]
+    const uint32_t r = blockIdx.y, t = threadIdx.x, j = blockIdx.x * kRTile + t;
+    const bool isq = r <= a.level;
+    const uint32_t pr = ext_prime(r, a.level, a.L);
+    const uint64_t q = kt.q[pr], qi = kt.qinv_neg[pr];
+    const size_t key_rows = a.L + 1 + a.K;
+    for (uint32_t s = 0; s < a.nsteps; ++s) {
+        for (uint32_t d = 0; d < 2 * a.dnum; ++d)
+            sk[((size_t)s * 2 * a.dnum + d) * kRTile + t] = __ldg(a.key[s] + ((size_t)d * key_rows + pr) * kt.n + j);
+        sj[s * kRTile + t] = galois_perm(j, a.g[s], kt.log_n);
+    }
+    // digit d's source row: x row r (r in I_d) or its ModUp'd row of y
+    const uint64_t *src[DMAX];
+    size_t sst[DMAX];
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) {
+        if (d < (int)a.dnum) {
+            if (r >= a.lo[d] && r < a.hi[d]) {
+                src[d] = x + (size_t)r * kt.n;
+                sst[d] = a.xs;
+            } else {
+                const uint32_t row = r < a.lo[d] ? r : r - (a.hi[d] - a.lo[d]);
+                src[d] = y + a.y_off[d] + (size_t)row * kt.n;
+                sst[d] = a.ys;
+            }
+        }
+    }
+    const TwPair pm = isq ? pmod[r] : TwPair{0, 0};
+    const size_t orow = isq ? (size_t)r * kt.n : (size_t)(2 * (a.level + 1) + (r - a.level - 1)) * kt.n;
+    const size_t opoly = isq ? (size_t)(a.level + 1) * kt.n : (size_t)a.K * kt.n;
+    for (uint32_t b = 0; b < a.B; ++b) {
+        const uint64_t *c0r = c0 + (size_t)b * a.cs + (size_t)r * kt.n;
+        uint64_t acc0 = 0, acc1 = 0;
+        if (isq) {
+            acc0 = shoup(c0r[j], pm.w, pm.wp, q);
+            acc1 = shoup(x[(size_t)b * a.xs + (size_t)r * kt.n + j], pm.w, pm.wp, q);
+        }
+        for (uint32_t s = 0; s < a.nsteps; ++s) {
+            const uint32_t kk = sj[s * kRTile + t];
+            const uint64_t *kw = sk + (size_t)s * 2 * a.dnum * kRTile + t;
+            uint64_t w[DMAX];
+#pragma unroll
+            for (int d = 0; d < DMAX; ++d)
+                if (d < (int)a.dnum) w[d] = src[d][(size_t)b * sst[d] + kk];
+            const uint64_t cw = isq ? c0r[kk] : 0;
+            U128 p0{0, 0}, p1{0, 0};
+#pragma unroll
+            for (int d = 0; d < DMAX; ++d) {
+                if (d < (int)a.dnum) {
+                    mac128(p0, w[d], kw[(2 * d) * kRTile]);
+                    mac128(p1, w[d], kw[(2 * d + 1) * kRTile]);
+                }
+            }
+            acc0 = add_mod(acc0, redc(p0, q, qi), q);
+            acc1 = add_mod(acc1, redc(p1, q, qi), q);
+            if (isq) acc0 = add_mod(acc0, shoup(cw, pm.w, pm.wp, q), q);
+        }
+        uint64_t *o = out + (size_t)b * a.os + orow + j;
+        o[0] = acc0;
+        o[opoly] = acc1;
+    }
+}
+
 struct MDArgs {
     const TwPair *phat_inv;  // [K]
     const uint64_t *phat;    // [K][L+1] Montgomery
@@ -1377,6 +1468,55 @@ void launch_hoisted_ip_pq(Ctx &c, const uint64_t *x, size_t xs, const uint64_t *
     });
     const dim3 g(c.n / kHTile, level + 1 + c.K);
     k_hoisted_ip_pq<4><<<g, kHTile, smem, c.stream>>>(x, y, c0, (const TwPair *)c.bconv_ptr(c.off_pd_pmod), c.kt, a);
+    LAUNCH_CHECK(c);
+}
+
+void launch_hoisted_rotsum_pq(Ctx &c, uint64_t *out, size_t os, const uint64_t *x, size_t xs, const uint64_t *y,
+                              size_t ys, const std::vector<size_t> &off, const uint64_t *c0, size_t cs,
+                              const std::vector<const uint64_t *> &keys, const std::vector<uint32_t> &g,
+                              uint32_t level, uint32_t B)
+{
+    const auto &plans = c.modup[level];
+    MMFHE_REQUIRE(keys.size() == g.size() && !keys.empty() && keys.size() <= (size_t)kDiagMax && plans.size() <= 8,
+                  MMFHE_E_LAYOUT, "hoisted PQ rotate-and-sum: 1..16 steps, <= 8 digits");
+    HoistSumArgs a{};
+    a.dnum = (uint32_t)plans.size();
+    a.level = level;
+    a.L = c.L;
+    a.K = c.K;
+    a.B = B;
+    a.xs = xs;
+    a.ys = ys;
+    a.cs = cs;
+    a.os = os;
+    a.nsteps = (uint32_t)keys.size();
+    for (size_t s = 0; s < keys.size(); ++s) {
+        a.key[s] = keys[s];
+        a.g[s] = g[s];
+    }
+    for (size_t j = 0; j < plans.size(); ++j) {
+        a.y_off[j] = off[j] * c.n;
+        a.lo[j] = plans[j].lo;
+        a.hi[j] = plans[j].hi;
+    }
+    const double rows = level + 1 + c.K, S = (double)keys.size();
+    // algorithmic: digit words, c1 and c0 once (read S times through L2), every step's key once, the sum once
+    ProfScope ps(c, "key_ip_rotsum", 8.0 * c.n * (rows * B * a.dnum + 2.0 * (level + 1.0) * B + S * rows * 2.0 * a.dnum +
+                                            B * 2.0 * rows),
+                 2.0 * a.dnum * rows * c.n * B * S);
+    const size_t smem = sizeof(uint64_t) * a.nsteps * 2 * a.dnum * kRTile + sizeof(uint32_t) * a.nsteps * kRTile;
+    MMFHE_REQUIRE(smem <= 200 * 1024, MMFHE_E_SHAPE, "hoisted PQ rotate-and-sum: too many key words per tile");
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, [] {
+        CUDA_CHECK(cudaFuncSetAttribute(k_hoisted_rotsum_pq<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(k_hoisted_rotsum_pq<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    });
+    const dim3 grid(c.n / kRTile, level + 1 + c.K);
+    const TwPair *pmod = (const TwPair *)c.bconv_ptr(c.off_pd_pmod);
+    if (a.dnum <= 4)
+        k_hoisted_rotsum_pq<4><<<grid, kRTile, smem, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
+    else
+        k_hoisted_rotsum_pq<8><<<grid, kRTile, smem, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
     LAUNCH_CHECK(c);
 }
 
