@@ -291,6 +291,15 @@ mmfhe_status mmfhe_hrot(mmfhe_ctx *ctx, const mmfhe_ct *a, int32_t step, mmfhe_c
  * mmfhe_hrot, decryption is the same rotation).  out[i] receives step i. */
 mmfhe_status mmfhe_hrot_hoisted(mmfhe_ctx *ctx, const mmfhe_ct *a, const int32_t *steps, size_t n_steps,
                                 mmfhe_ct *out);
+/* Double hoisting's baby steps (DESIGN R22, SURVEY §8(c)-5 "a third op"): one ModUp of c1 shared
+ * by n_steps rotations left over Q_level u P without ModDown, out[i] = (P sigma_g(c0) + IP_0,
+ * IP_1) for step i (step 0: the P lift (P c0, P c1)).  Steps are grouped into one inner-product
+ * launch per 16 (k_hoisted_ip_pq: the evaluation keys streamed once -- the path's evk-streaming
+ * key-switch step).  Each out[i].data receives 2 (level+1+K) N words in the library's PQ layout:
+ * poly 0 over q_0..q_level, poly 1 over q_0..q_level, poly 0 over p_0..p_{K-1}, poly 1 over
+ * p_0..p_{K-1}; out[i].form selects coefficient or evaluation form, n_polys is set to 2. */
+mmfhe_status mmfhe_hrot_hoisted_pq(mmfhe_ctx *ctx, const mmfhe_ct *a, const int32_t *steps, size_t n_steps,
+                                   mmfhe_ct *out);
 /* Rescale by q_level, round-half-up. */
 mmfhe_status mmfhe_rescale(mmfhe_ctx *ctx, const mmfhe_ct *a, mmfhe_ct *out);
 /* Hybrid key switching of one polynomial x (n_polys = 1, level l) with the

@@ -563,6 +563,17 @@ mmfhe_status mmfhe_hrot_hoisted(mmfhe_ctx *ctx, const mmfhe_ct *a, const int32_t
     API_END(ctx)
 }
 
+mmfhe_status mmfhe_hrot_hoisted_pq(mmfhe_ctx *ctx, const mmfhe_ct *a, const int32_t *steps, size_t n_steps,
+                                   mmfhe_ct *out)
+{
+    API_BEGIN
+    MMFHE_REQUIRE(a && steps && out && n_steps, MMFHE_E_INVALID_ARG, "null argument");
+    DCt x = input_ct(*ctx, *a);
+    std::vector<DCt> r = ev_rotate_hoisted_pq(*ctx, x, std::vector<int32_t>(steps, steps + n_steps));
+    for (size_t i = 0; i < n_steps; ++i) export_pq(*ctx, r[i], out[i]);
+    API_END(ctx)
+}
+
 mmfhe_status mmfhe_rescale(mmfhe_ctx *ctx, const mmfhe_ct *a, mmfhe_ct *out)
 {
     API_BEGIN

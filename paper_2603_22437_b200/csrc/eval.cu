@@ -177,6 +177,36 @@ void export_ct(Ctx &c, const DCt &in, mmfhe_ct &out)
     }
 }
 
+PrimeMap pq_item_map(const Ctx &c, uint32_t l);
+
+void export_pq(Ctx &c, const DCt &in, mmfhe_ct &out)
+{
+    MMFHE_REQUIRE(out.data != nullptr, MMFHE_E_INVALID_ARG, "null output buffer");
+    MMFHE_REQUIRE(in.batch == 1 && in.pk == c.K && in.npolys == 2, MMFHE_E_LAYOUT, "export one PQ ciphertext");
+    const uint32_t rows = in.rows();
+    const size_t words = in.item_words();
+    out.log_n = c.log_n;
+    out.level = in.level;
+    out.scale = in.scale;
+    out.n_slots = in.n_slots;
+    out.n_polys = 2;
+    const InvSrc src{in.data(), words, c.n, rows, 1};
+    uint64_t *dst = out.data;
+    DBuf tmp;
+    if (!out.on_device) {
+        tmp = DBuf(words, c.stream);
+        dst = tmp.get();
+    }
+    if (out.form == MMFHE_FORM_COEFF)
+        ntt_inverse(c, dst, rows, pq_item_map(c, in.level), &src);
+    else
+        memcpy_d2d(c, dst, in.data(), words);
+    if (!out.on_device) {
+        CUDA_CHECK(cudaMemcpyAsync(out.data, dst, words * 8, cudaMemcpyDeviceToHost, c.stream));
+        CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    }
+}
+
 // Every item of a batch to its own output: one out-of-place INTT of the whole batch into a
 // staging buffer (coefficient-form outputs), then one scatter launch per 64 device outputs
 // or one D2H copy per host output -- instead of two INTT launches per ciphertext.

@@ -25,6 +25,7 @@ DCt copy_ct(Ctx &c, const DCt &a);
 DCt import_ct(Ctx &c, const mmfhe_ct &in, uint32_t npolys);
 DCt import_batch(Ctx &c, const mmfhe_ct *cts, size_t first, size_t step, size_t count);
 void export_ct(Ctx &c, const DCt &in, mmfhe_ct &out);  // in.batch == 1
+void export_pq(Ctx &c, const DCt &in, mmfhe_ct &out);  // a PQ ciphertext (in.batch == 1), library PQ layout
 void export_batch(Ctx &c, const DCt &in, mmfhe_ct *outs);  // outs[0 .. in.batch)
 
 // exact ops (batched)

@@ -124,6 +124,7 @@ def lib():
             "mmfhe_relin": [V, CTP, CTP],
             "mmfhe_hrot": [V, CTP, I32, CTP],
             "mmfhe_hrot_hoisted": [V, CTP, P(I32), S, CTP],
+            "mmfhe_hrot_hoisted_pq": [V, CTP, P(I32), S, CTP],
             "mmfhe_rescale": [V, CTP, CTP],
             "mmfhe_keyswitch": [V, CTP, I32, ctypes.c_int, CTP],
             "mmfhe_mod_switch": [V, CTP, U32, CTP],
@@ -161,7 +162,7 @@ EXPORTED = [
     "mmfhe_chain_required_rotations", "mmfhe_load_relin_key", "mmfhe_load_galois_key", "mmfhe_load_plain",
     "mmfhe_encode_plain", "mmfhe_prepare_chain", "mmfhe_load_scalars", "mmfhe_chain_plan", "mmfhe_eval_chain",
     "mmfhe_sum_partials", "mmfhe_ntt", "mmfhe_intt", "mmfhe_hadd", "mmfhe_hsub", "mmfhe_pmult", "mmfhe_hmult",
-    "mmfhe_relin", "mmfhe_hrot", "mmfhe_hrot_hoisted", "mmfhe_rescale", "mmfhe_keyswitch", "mmfhe_mod_switch", "mmfhe_hrot_batch",
+    "mmfhe_relin", "mmfhe_hrot", "mmfhe_hrot_hoisted", "mmfhe_hrot_hoisted_pq", "mmfhe_rescale", "mmfhe_keyswitch", "mmfhe_mod_switch", "mmfhe_hrot_batch",
     "mmfhe_hmult_batch", "mmfhe_trace_get", "mmfhe_trace_clear", "mmfhe_trace_enable", "mmfhe_profile_enable",
     "mmfhe_profile_get", "mmfhe_microbench", "mmfhe_graph_enable", "mmfhe_graph_stats", "mmfhe_eval_chain_async",
     "mmfhe_ctx_sync", "mmfhe_params_digest", "mmfhe_serialize_ct", "mmfhe_deserialize_ct", "mmfhe_serialize_key",
@@ -385,6 +386,17 @@ class Context:
         st = (ctypes.c_int32 * len(steps))(*[int(s) for s in steps])
         o = (CT * len(outs))(*[c.struct() for c in outs])
         self._check(self._lib.mmfhe_hrot_hoisted(self.h, ctypes.byref(sa), st, len(steps), o))
+        for c, s in zip(outs, o):
+            c.level, c.scale, c.n_slots = s.level, s.scale, s.n_slots
+        return outs
+
+    def hrot_hoisted_pq(self, a, steps, outs):
+        """Double-hoisted baby steps: outs[i] <- PQ ciphertext of step i (data: 2 (level+1+K) N words,
+        Q rows of poly 0 / poly 1, then P rows of poly 0 / poly 1)."""
+        sa = a.struct()
+        st = (ctypes.c_int32 * len(steps))(*[int(s) for s in steps])
+        o = (CT * len(outs))(*[c.struct() for c in outs])
+        self._check(self._lib.mmfhe_hrot_hoisted_pq(self.h, ctypes.byref(sa), st, len(steps), o))
         for c, s in zip(outs, o):
             c.level, c.scale, c.n_slots = s.level, s.scale, s.n_slots
         return outs

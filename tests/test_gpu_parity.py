@@ -127,6 +127,52 @@ def test_hrot_hoisted_parity(m, toy_keys, level):
     assert ctx.trace() == ev.trace
 
 
+def _pq_want(ct):
+    """Oracle PQ ciphertext (coefficient form over q_0..q_l, p_0..p_{K-1} per poly) in the
+    library's PQ layout: Q rows of poly 0 / poly 1, then P rows of poly 0 / poly 1."""
+    l1 = ct.level + 1
+    return np.concatenate([ct.c[0][:l1], ct.c[1][:l1], ct.c[0][l1:], ct.c[1][l1:]])
+
+
+def _pq_out(m, P, level):
+    import torch
+    data = torch.empty((2 * (level + 1 + P.K), P.n), dtype=torch.int64, device="cuda:0")
+    return m.Ct(data, level, 0.0, 0, P.log_n, m.FORM_COEFF, 2)
+
+
+@pytest.mark.parametrize("level", [5, 2])
+def test_hrot_hoisted_pq_parity(m, toy_keys, level):
+    """Double hoisting's baby steps through mmfhe_hrot_hoisted_pq (the PQ lift for step 0):
+    residues equal the oracle's lift_pq / hoisted_step_pq."""
+    P, keys = toy_keys
+    ctx = make_ctx(m, P, keys)
+    a = _rand_ct(P, level, 75 + level)
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    steps = [0, 1, 3, -1, 100]
+    ys = ev.hoist_modup(a)
+    want = [ev.hoisted_step_pq(a, ys, s) for s in steps]
+    outs = [_pq_out(m, P, level) for _ in steps]
+    ctx.hrot_hoisted_pq(ct_in(m, P, a), steps, outs)
+    for o, w in zip(outs, want):
+        assert np.array_equal(residues(o), _pq_want(w))
+
+
+@pytest.mark.parametrize("level", [5, 0])
+def test_conjugation_parity(m, toy_keys, level):
+    """Conj (DESIGN R28) through the HRot primitive with MMFHE_STEP_CONJ: residues and trace
+    equal the oracle's Evaluator.conjugate (key from the oracle keygen's CONJ entry)."""
+    P, _ = toy_keys
+    keys = orc.keygen(P, seed=1777, rotations=[orc.CONJ])
+    ctx = make_ctx(m, P, keys)
+    a = _rand_ct(P, level, 85 + level)
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    want = ev.conjugate(a)
+    out = ct_out(m, P, level)
+    ctx.hrot(ct_in(m, P, a), m.STEP_CONJ, out)
+    assert np.array_equal(residues(out), np.stack(want.c))
+    assert ctx.trace() == ev.trace == [("conj", level, "")]
+
+
 @pytest.mark.parametrize("level", [5, 2])
 def test_hmult_relin_parity(m, toy_keys, level):
     P, keys = toy_keys
@@ -186,7 +232,7 @@ def test_errors(m, toy_keys):
 @pytest.fixture(scope="module")
 def ps4_keys():
     P = ps4()
-    return P, orc.keygen(P, seed=4001, rotations=[1, 2048])
+    return P, orc.keygen(P, seed=4001, rotations=[1, 5, 2048])
 
 
 @pytest.mark.parametrize("step", [1, 2048])
@@ -213,3 +259,19 @@ def test_ps4_hmult_rescale_parity(m, ps4_keys):
     out_r = ct_out(m, P, P.L - 1)
     ctx.rescale(out, out_r)
     assert np.array_equal(residues(out_r), np.stack(want_r.c))
+
+
+def test_ps4_hrot_hoisted_pq_parity(m, ps4_keys):
+    """The bench's evk-streaming step at N = 2^16 (PS4 top level, 3 digits: the grouped inner
+    product k_hoisted_ip_pq): PQ baby steps bit-exact against the oracle."""
+    P, keys = ps4_keys
+    ctx = make_ctx(m, P, keys)
+    a = _rand_ct(P, P.L, 4300)
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    steps = [1, 5, 2048]
+    ys = ev.hoist_modup(a)
+    want = [ev.hoisted_step_pq(a, ys, s) for s in steps]
+    outs = [_pq_out(m, P, P.L) for _ in steps]
+    ctx.hrot_hoisted_pq(ct_in(m, P, a), steps, outs)
+    for o, w in zip(outs, want):
+        assert np.array_equal(residues(o), _pq_want(w))
