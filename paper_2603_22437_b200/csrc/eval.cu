@@ -908,8 +908,8 @@ DCt ev_rotsum_hoisted_pq(Ctx &c, const DCt &a, const std::vector<int32_t> &steps
         gs.push_back((uint32_t)g);
         ks.push_back(k);
     }
-    MMFHE_REQUIRE(!keys.empty() && keys.size() <= (size_t)kDiagMax && c.modup[l].size() <= 8, MMFHE_E_LAYOUT,
-                  "hoisted rotate-and-sum: 1..16 steps, <= 8 digits");
+    MMFHE_REQUIRE(!keys.empty() && keys.size() <= 64 && c.modup[l].size() <= 8, MMFHE_E_LAYOUT,
+                  "hoisted rotate-and-sum: 1..64 steps, <= 8 digits");
     // the oracle's op sequence (rotsum_dh_all): lift, the PQ steps, their PQ additions
     rec_n(c, "lift_pq", l, B);
     for (int32_t k : ks) rec_n(c, "hrot_hoisted_pq", l, B, std::to_string(k));

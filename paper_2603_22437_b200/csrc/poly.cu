@@ -401,12 +401,16 @@ __global__ void __launch_bounds__(kHTile) k_hoisted_ip_pq(const uint64_t *__rest
 // in any order.  The thread owns the OUTPUT index j and gathers the sources at perm_s(j) (an aligned
 // 32-word span maps onto an aligned span: the gathers stay coalesced, and a row's sources stay L2-resident
 // across its CTAs), so the steps accumulate in registers and only the sum reaches HBM: no per-step PQ
-// outputs and no PQ additions.  Every key word is read once (staged in the thread's own shared-memory
-// column, reused across the batch items).
+// outputs and no PQ additions.  Steps outer, items inner: each step's 2 dnum key words are loaded once
+// into registers and reused for the CTA's chunk of up to RB items (grid.z splits larger batches), whose
+// running sums stay in the thread's own shared-memory column (16 KiB-per-item-chunk: no barriers), so the
+// group may have any number of steps and occupancy is not bound by a key tile.
 constexpr int kRTile = 128;
+constexpr int kRItems = 16;  // items per CTA (register accumulators)
+constexpr int kRSteps = 64;  // steps per launch (kernel-parameter arrays)
 struct HoistSumArgs {
-    const uint64_t *key[kDiagMax];
-    uint32_t g[kDiagMax];  // Galois elements of the steps (perm_s)
+    const uint64_t *key[kRSteps];
+    uint32_t g[kRSteps];  // Galois elements (perm_s)
     size_t y_off[16];
     uint32_t lo[16], hi[16];
     size_t xs, ys, cs, os;  // item strides: x (c1), y (ModUp'd digits), c0, output
@@ -420,67 +424,78 @@ __global__ void __launch_bounds__(kRTile) k_hoisted_rotsum_pq(uint64_t *__restri
                                                             const TwPair *__restrict__ pmod, KTables kt,
                                                             HoistSumArgs a)
 {
-    extern __shared__ uint64_t sk[];  // [nsteps][2 dnum][kRTile] key words (each thread its own column)
-    uint32_t *sj = reinterpret_cast<uint32_t *>(sk + (size_t)a.nsteps * 2 * a.dnum * kRTile);  // [nsteps][kRTile]
+    __shared__ uint64_t sacc[kRItems][2][kRTile];  // this thread's column: the chunk's running sums
     const uint32_t r = blockIdx.y, t = threadIdx.x, j = blockIdx.x * kRTile + t;
+    const uint32_t b0 = blockIdx.z * kRItems, nb = min((uint32_t)kRItems, a.B - b0);
     const bool isq = r <= a.level;
     const uint32_t pr = ext_prime(r, a.level, a.L);
     const uint64_t q = kt.q[pr], qi = kt.qinv_neg[pr];
     const size_t key_rows = a.L + 1 + a.K;
-    for (uint32_t s = 0; s < a.nsteps; ++s) {
-        for (uint32_t d = 0; d < 2 * a.dnum; ++d)
-            sk[((size_t)s * 2 * a.dnum + d) * kRTile + t] = __ldg(a.key[s] + ((size_t)d * key_rows + pr) * kt.n + j);
-        sj[s * kRTile + t] = galois_perm(j, a.g[s], kt.log_n);
-    }
-    // digit d's source row: x row r (r in I_d) or its ModUp'd row of y
+    // digit d's source row: x row r (r in I_d) or its ModUp'd row of y (item b0 onwards)
     const uint64_t *src[DMAX];
     size_t sst[DMAX];
 #pragma unroll
     for (int d = 0; d < DMAX; ++d) {
         if (d < (int)a.dnum) {
             if (r >= a.lo[d] && r < a.hi[d]) {
-                src[d] = x + (size_t)r * kt.n;
+                src[d] = x + (size_t)b0 * a.xs + (size_t)r * kt.n;
                 sst[d] = a.xs;
             } else {
                 const uint32_t row = r < a.lo[d] ? r : r - (a.hi[d] - a.lo[d]);
-                src[d] = y + a.y_off[d] + (size_t)row * kt.n;
+                src[d] = y + (size_t)b0 * a.ys + a.y_off[d] + (size_t)row * kt.n;
                 sst[d] = a.ys;
             }
         }
     }
+    const uint64_t *c0r = c0 + (size_t)b0 * a.cs + (size_t)r * kt.n;
     const TwPair pm = isq ? pmod[r] : TwPair{0, 0};
-    const size_t orow = isq ? (size_t)r * kt.n : (size_t)(2 * (a.level + 1) + (r - a.level - 1)) * kt.n;
-    const size_t opoly = isq ? (size_t)(a.level + 1) * kt.n : (size_t)a.K * kt.n;
-    for (uint32_t b = 0; b < a.B; ++b) {
-        const uint64_t *c0r = c0 + (size_t)b * a.cs + (size_t)r * kt.n;
-        uint64_t acc0 = 0, acc1 = 0;
+    for (uint32_t b = 0; b < nb; ++b) {
+        uint64_t v0 = 0, v1 = 0;
         if (isq) {
-            acc0 = shoup(c0r[j], pm.w, pm.wp, q);
-            acc1 = shoup(x[(size_t)b * a.xs + (size_t)r * kt.n + j], pm.w, pm.wp, q);
+            v0 = shoup(c0r[(size_t)b * a.cs + j], pm.w, pm.wp, q);
+            v1 = shoup(x[(size_t)(b0 + b) * a.xs + (size_t)r * kt.n + j], pm.w, pm.wp, q);
         }
-        for (uint32_t s = 0; s < a.nsteps; ++s) {
-            const uint32_t kk = sj[s * kRTile + t];
-            const uint64_t *kw = sk + (size_t)s * 2 * a.dnum * kRTile + t;
+        sacc[b][0][t] = v0;
+        sacc[b][1][t] = v1;
+    }
+    for (uint32_t s = 0; s < a.nsteps; ++s) {
+        const uint64_t *ks = a.key[s] + (size_t)pr * kt.n + j;
+        uint64_t kb[DMAX], ka[DMAX];
+#pragma unroll
+        for (int d = 0; d < DMAX; ++d) {
+            if (d < (int)a.dnum) {
+                kb[d] = __ldg(ks + (size_t)(2 * d) * key_rows * kt.n);
+                ka[d] = __ldg(ks + (size_t)(2 * d + 1) * key_rows * kt.n);
+            }
+        }
+        const uint32_t kk = galois_perm(j, a.g[s], kt.log_n);
+#pragma unroll 2
+        for (uint32_t b = 0; b < nb; ++b) {
             uint64_t w[DMAX];
 #pragma unroll
             for (int d = 0; d < DMAX; ++d)
                 if (d < (int)a.dnum) w[d] = src[d][(size_t)b * sst[d] + kk];
-            const uint64_t cw = isq ? c0r[kk] : 0;
+            const uint64_t cw = isq ? c0r[(size_t)b * a.cs + kk] : 0;
             U128 p0{0, 0}, p1{0, 0};
 #pragma unroll
             for (int d = 0; d < DMAX; ++d) {
                 if (d < (int)a.dnum) {
-                    mac128(p0, w[d], kw[(2 * d) * kRTile]);
-                    mac128(p1, w[d], kw[(2 * d + 1) * kRTile]);
+                    mac128(p0, w[d], kb[d]);
+                    mac128(p1, w[d], ka[d]);
                 }
             }
-            acc0 = add_mod(acc0, redc(p0, q, qi), q);
-            acc1 = add_mod(acc1, redc(p1, q, qi), q);
-            if (isq) acc0 = add_mod(acc0, shoup(cw, pm.w, pm.wp, q), q);
+            uint64_t v0 = add_mod(sacc[b][0][t], redc(p0, q, qi), q);
+            if (isq) v0 = add_mod(v0, shoup(cw, pm.w, pm.wp, q), q);
+            sacc[b][0][t] = v0;
+            sacc[b][1][t] = add_mod(sacc[b][1][t], redc(p1, q, qi), q);
         }
-        uint64_t *o = out + (size_t)b * a.os + orow + j;
-        o[0] = acc0;
-        o[opoly] = acc1;
+    }
+    const size_t orow = isq ? (size_t)r * kt.n : (size_t)(2 * (a.level + 1) + (r - a.level - 1)) * kt.n;
+    const size_t opoly = isq ? (size_t)(a.level + 1) * kt.n : (size_t)a.K * kt.n;
+    for (uint32_t b = 0; b < nb; ++b) {
+        uint64_t *o = out + (size_t)(b0 + b) * a.os + orow + j;
+        o[0] = sacc[b][0][t];
+        o[opoly] = sacc[b][1][t];
     }
 }
 
@@ -1477,8 +1492,8 @@ void launch_hoisted_rotsum_pq(Ctx &c, uint64_t *out, size_t os, const uint64_t *
                               uint32_t level, uint32_t B)
 {
     const auto &plans = c.modup[level];
-    MMFHE_REQUIRE(keys.size() == g.size() && !keys.empty() && keys.size() <= (size_t)kDiagMax && plans.size() <= 8,
-                  MMFHE_E_LAYOUT, "hoisted PQ rotate-and-sum: 1..16 steps, <= 8 digits");
+    MMFHE_REQUIRE(keys.size() == g.size() && !keys.empty() && keys.size() <= (size_t)kRSteps && plans.size() <= 8,
+                  MMFHE_E_LAYOUT, "hoisted PQ rotate-and-sum: 1..64 steps, <= 8 digits");
     HoistSumArgs a{};
     a.dnum = (uint32_t)plans.size();
     a.level = level;
@@ -1490,33 +1505,26 @@ void launch_hoisted_rotsum_pq(Ctx &c, uint64_t *out, size_t os, const uint64_t *
     a.cs = cs;
     a.os = os;
     a.nsteps = (uint32_t)keys.size();
-    for (size_t s = 0; s < keys.size(); ++s) {
-        a.key[s] = keys[s];
-        a.g[s] = g[s];
-    }
     for (size_t j = 0; j < plans.size(); ++j) {
         a.y_off[j] = off[j] * c.n;
         a.lo[j] = plans[j].lo;
         a.hi[j] = plans[j].hi;
+    }
+    for (size_t s = 0; s < keys.size(); ++s) {
+        a.key[s] = keys[s];
+        a.g[s] = g[s];
     }
     const double rows = level + 1 + c.K, S = (double)keys.size();
     // algorithmic: digit words, c1 and c0 once (read S times through L2), every step's key once, the sum once
     ProfScope ps(c, "key_ip_rotsum", 8.0 * c.n * (rows * B * a.dnum + 2.0 * (level + 1.0) * B + S * rows * 2.0 * a.dnum +
                                             B * 2.0 * rows),
                  2.0 * a.dnum * rows * c.n * B * S);
-    const size_t smem = sizeof(uint64_t) * a.nsteps * 2 * a.dnum * kRTile + sizeof(uint32_t) * a.nsteps * kRTile;
-    MMFHE_REQUIRE(smem <= 200 * 1024, MMFHE_E_SHAPE, "hoisted PQ rotate-and-sum: too many key words per tile");
-    static std::atomic<uint64_t> attr{0};
-    once_per_device(attr, [] {
-        CUDA_CHECK(cudaFuncSetAttribute(k_hoisted_rotsum_pq<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        CUDA_CHECK(cudaFuncSetAttribute(k_hoisted_rotsum_pq<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    });
-    const dim3 grid(c.n / kRTile, level + 1 + c.K);
+    const dim3 grid(c.n / kRTile, level + 1 + c.K, (B + kRItems - 1) / kRItems);
     const TwPair *pmod = (const TwPair *)c.bconv_ptr(c.off_pd_pmod);
     if (a.dnum <= 4)
-        k_hoisted_rotsum_pq<4><<<grid, kRTile, smem, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
+        k_hoisted_rotsum_pq<4><<<grid, kRTile, 0, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
     else
-        k_hoisted_rotsum_pq<8><<<grid, kRTile, smem, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
+        k_hoisted_rotsum_pq<8><<<grid, kRTile, 0, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
     LAUNCH_CHECK(c);
 }
 

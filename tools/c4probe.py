@@ -24,6 +24,8 @@ ap.add_argument("--params", default="PS4")
 ap.add_argument("--bsgs", type=int, default=0, help="K3 baby steps b (0: ceil(sqrt(2D-1)))")
 ap.add_argument("--fc-baby", type=int, default=0)
 ap.add_argument("--cplx", type=int, default=0, help="complex slots (DESIGN R28)")
+ap.add_argument("--chains", default="", help="comma-separated extra chains to profile on the session's inputs "
+                                             "(k3_doppler_dft, gesture_frame)")
 ap.add_argument("--split", action="store_true", help="also profile gesture_features and gesture_fc on their own")
 args = ap.parse_args()
 
@@ -86,3 +88,17 @@ if args.profile and args.split:
         print(f"{name}: kernel sum {tot:.2f} ms")
         for k, (c, ms, by, ops) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
             print(f"   {k:16s} {ms:8.2f} ms {ms / tot:6.3f}  {c:5d} launches  {by / (ms * 1e-3) / 1e9:7.1f} GB/s")
+
+for name in [c for c in args.chains.split(",") if c]:
+    lv = ctx.chain_plan(name, cfg, 19, n_in)
+    o_ = m.CtArray([m.Ct(torch.empty((2, l + 1, P.n), dtype=torch.int64, device=dev), l, 0.0, 0, P.log_n) for l in lv])
+    ctx.eval_chain(name, cfg, ins, o_)
+    torch.cuda.synchronize()
+    ctx.profile_enable(True)
+    ctx.profile()
+    ctx.eval_chain(name, cfg, ins, o_)
+    prof = ctx.profile()
+    tot = sum(v[1] for v in prof.values())
+    print(f"{name}: kernel sum {tot:.2f} ms")
+    for k, (c, ms, by, ops) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        print(f"   {k:16s} {ms:8.2f} ms {ms / tot:6.3f}  {c:5d} launches  {by / (ms * 1e-3) / 1e9:7.1f} GB/s")
