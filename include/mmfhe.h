@@ -147,6 +147,10 @@ typedef struct {
                               diagonal instead of four -- and outputs d = d_re + j d_im; K1 computes
                               |d|^2 = d Conj(d) with the conjugation key (MMFHE_STEP_CONJ, listed by
                               mmfhe_chain_required_rotations).  Same depth; 0 = split re/im layout */
+    uint32_t bsgs_aligned; /* K3 BSGS: 1 = giant offsets at multiples of b (G = b k, k = floor(-(D-1)/b) ..
+                              floor((D-1)/b)), so the giant G = 0 needs no rotation (DESIGN R29; one giant
+                              key switch fewer per input); 0 = the SURVEY §8(c)-7 split o = -(D-1) + g'b + s.
+                              Different rotation keys and residues, same decryption */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */

@@ -59,6 +59,7 @@ class ChainCfg:
     n_taps: tuple = ()          # k5_fir_rot: taps per band (rotation keys for the longest)
     lanes: int = 1              # gesture / K3: frames interleaved per ciphertext (reading R20)
     fc_baby: int = 0            # FC BSGS baby steps (0: ceil(sqrt(h)))
+    bsgs_aligned: int = 0       # K3: 1 -> giant offsets at multiples of b, one giant step the identity (R29)
     cplx: int = 0               # gesture / K3: 1 -> complex slots, z = v_re + j v_im in ONE ciphertext
                                 # per frame (group); K3 multiplies complex diagonals, K1 is z conj(z)
                                 # (reading R28)
@@ -338,18 +339,30 @@ def block_diag_diagonal(M: np.ndarray, n: int, o: int) -> np.ndarray:
 
 
 def k3_schedule(cfg: ChainCfg):
-    """BSGS split over the offsets o in [-(D-1), D-1]: o = o_min + g'b + s."""
+    """BSGS split over the offsets o in [-(D-1), D-1]: o = o_min + g'b + s, or with
+    cfg.bsgs_aligned (reading R29) o = G + s with giant offsets G = b k, k = floor(-(D-1)/b) ..
+    floor((D-1)/b): the giant G = 0 needs no rotation (one giant key switch fewer per input)."""
     D = cfg.D
     d = 2 * D - 1
     b = cfg.bsgs_baby or ceil_sqrt(d)
+    giants = []
+    if getattr(cfg, "bsgs_aligned", 0):
+        for gp, k in enumerate(range(-((D - 1 + b - 1) // b), (D - 1) // b + 1)):
+            G = b * k
+            giants.append((gp, G, [s for s in range(b) if -(D - 1) <= G + s <= D - 1]))
+        return b, giants
     g = -(-d // b)
     o_min = -(D - 1)
-    giants = []
     for gp in range(g):
         G = o_min + gp * b
         babies = [s for s in range(b) if G + s <= D - 1]
         giants.append((gp, G, babies))
     return b, giants
+
+
+def k3_prefix(cfg) -> str:
+    """Plaintext-name prefix of K3's diagonals (the aligned schedule's differ, R29)."""
+    return "k3a" if getattr(cfg, "bsgs_aligned", 0) else "k3"
 
 
 def baby_steps(ev, cts, steps, hoist):
@@ -422,9 +435,9 @@ def k3_inner_sums(ev: CircuitEvaluator, book: PlainBook, xr, xi, cfg: ChainCfg):
             dc = lane_vec(rot(block_diag_diagonal(C, n, o), -G), L)
             ds = lane_vec(rot(block_diag_diagonal(S, n, o), -G), L)
             vec = book.vec_pq if dh(cfg) else book.vec
-            pc = vec(f"k3.c.{gp}.{s}", dc, lvl)
-            ps = vec(f"k3.s.{gp}.{s}", ds, lvl)
-            pns = vec(f"k3.ns.{gp}.{s}", -ds, lvl)
+            pc = vec(f"{k3_prefix(cfg)}.c.{gp}.{s}", dc, lvl)
+            ps = vec(f"{k3_prefix(cfg)}.s.{gp}.{s}", ds, lvl)
+            pns = vec(f"{k3_prefix(cfg)}.ns.{gp}.{s}", -ds, lvl)
             t_re += [(pc, s, "r"), (pns, s, "i")]
             t_im += [(ps, s, "r"), (pc, s, "i")]
         psum = ev.pmult_sum_pq if dh(cfg) else ev.pmult_sum
@@ -473,7 +486,7 @@ def k3_inner_sums_c(ev: CircuitEvaluator, book: PlainBook, xs, cfg: ChainCfg):
     psum = ev.pmult_sum_pq if dh(cfg) else ev.pmult_sum
     inner = []
     for gp, G, babies in giants:
-        pts = [(vec(f"k3.w.{gp}.{s}", lane_vec(rot(block_diag_diagonal(W, n, G + s), -G), L), lvl), s)
+        pts = [(vec(f"{k3_prefix(cfg)}.w.{gp}.{s}", lane_vec(rot(block_diag_diagonal(W, n, G + s), -G), L), lvl), s)
                for s in babies]
         inner.append([psum([(pt, xs[s][f]) for pt, s in pts]) for f in range(nf)])
     return inner

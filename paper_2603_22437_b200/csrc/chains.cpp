@@ -105,6 +105,18 @@ Sched k3_schedule(const mmfhe_chain_cfg &cfg)
     const int32_t D = (int32_t)cfg.D, d = 2 * D - 1, o_min = -(D - 1);
     Sched s;
     s.b = cfg.bsgs_baby ? cfg.bsgs_baby : ceil_sqrt((uint32_t)d);
+    const int32_t b = (int32_t)s.b;
+    if (cfg.bsgs_aligned) {
+        // DESIGN R29: giants G = b k, k = floor(-(D-1)/b) .. floor((D-1)/b); G = 0 needs no rotation
+        uint32_t gp = 0;
+        for (int32_t k = -((D - 1 + b - 1) / b); k <= (D - 1) / b; ++k, ++gp) {
+            Sched::G gg{gp, b * k, {}};
+            for (int32_t bs = 0; bs < b; ++bs)
+                if (gg.G + bs >= -(D - 1) && gg.G + bs <= D - 1) gg.babies.push_back((uint32_t)bs);
+            s.giants.push_back(gg);
+        }
+        return s;
+    }
     const uint32_t g = ((uint32_t)d + s.b - 1) / s.b;
     for (uint32_t gp = 0; gp < g; ++gp) {
         Sched::G gg{gp, o_min + (int32_t)(gp * s.b), {}};
@@ -114,6 +126,9 @@ Sched k3_schedule(const mmfhe_chain_cfg &cfg)
     }
     return s;
 }
+
+// plaintext-name prefix of K3's diagonals (the aligned schedule's differ, R29)
+std::string k3_prefix(const mmfhe_chain_cfg &cfg) { return cfg.bsgs_aligned ? "k3a" : "k3"; }
 
 Sched fc_schedule(uint32_t h, uint32_t fc_baby)
 {
@@ -305,9 +320,10 @@ class Runner {
             for (uint32_t b : g.babies) {
                 const int32_t o = g.G + (int32_t)b;
                 const std::string sfx = "." + std::to_string(g.gp) + "." + std::to_string(b);
-                const DPlain &pc = plain("k3.c" + sfx, lvl, qscale(lvl), [&] { return diag(false, o, g.G, false); }, dh());
-                const DPlain &ps = plain("k3.s" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, false); }, dh());
-                const DPlain &pn = plain("k3.ns" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, true); }, dh());
+                const std::string k3p = k3_prefix(cfg_);
+                const DPlain &pc = plain(k3p + ".c" + sfx, lvl, qscale(lvl), [&] { return diag(false, o, g.G, false); }, dh());
+                const DPlain &ps = plain(k3p + ".s" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, false); }, dh());
+                const DPlain &pn = plain(k3p + ".ns" + sfx, lvl, qscale(lvl), [&] { return diag(true, o, g.G, true); }, dh());
                 re[b] = &pc;
                 re[s.b + b] = &pn;
                 im[b] = &ps;
@@ -386,7 +402,7 @@ class Runner {
         for (auto &g : s.giants) {
             std::vector<const DPlain *> row(s.b, nullptr);
             for (uint32_t b : g.babies) {
-                const std::string name = "k3.w." + std::to_string(g.gp) + "." + std::to_string(b);
+                const std::string name = k3_prefix(cfg_) + ".w." + std::to_string(g.gp) + "." + std::to_string(b);
                 row[b] = &plain_c(name, lvl, qscale(lvl), [&] { return diag(g.G + (int32_t)b, g.G); }, dh());
             }
             rows.push_back(row);
@@ -776,6 +792,7 @@ void validate_cfg(const std::string &chain, const mmfhe_chain_cfg &cfg)
     MMFHE_REQUIRE(pow2_or_zero(cfg.lanes), MMFHE_E_SHAPE, "lanes must be a power of two");
     MMFHE_REQUIRE(cfg.hoist <= 2, MMFHE_E_INVALID_ARG, "hoist must be 0, 1 or 2");
     MMFHE_REQUIRE(cfg.cplx <= 1, MMFHE_E_INVALID_ARG, "cplx must be 0 or 1");
+    MMFHE_REQUIRE(cfg.bsgs_aligned <= 1, MMFHE_E_INVALID_ARG, "bsgs_aligned must be 0 or 1");
     if (cfg.cplx)
         MMFHE_REQUIRE(cplx_chain(chain, cfg) || chain == "gesture_fc" || chain == "fc_forward" ||
                           chain == "k2_doppler_soft_power" || chain == "k6_notch",

@@ -36,12 +36,14 @@ def test_dft_matrix_is_shifted_windowed_fft():
     assert np.allclose(W @ x, want, atol=1e-12)
 
 
-@pytest.mark.parametrize("D,b", [(8, 0), (32, 0), (32, 4), (16, 5)])
-def test_k3_bsgs_schedule_on_plain_slots(D, b):
+@pytest.mark.parametrize("D,b,aligned", [(8, 0, 0), (32, 0, 0), (32, 4, 0), (16, 5, 0), (8, 0, 1), (32, 0, 1),
+                                         (32, 16, 1), (16, 5, 1), (32, 7, 1)])
+def test_k3_bsgs_schedule_on_plain_slots(D, b, aligned):
     """The BSGS schedule (pre-rotated diagonals, babies, giants) reproduces the
-    block-diagonal matvec exactly on plaintext slot vectors."""
+    block-diagonal matvec exactly on plaintext slot vectors -- the SURVEY §8(c)-7 split and
+    the aligned one (R29: giants at multiples of b, one of them the identity)."""
     n = 4 * D
-    cfg = cc.ChainCfg(D=D, bsgs_baby=b)
+    cfg = cc.ChainCfg(D=D, bsgs_baby=b, bsgs_aligned=aligned)
     rng = np.random.default_rng(D + b)
     M = rng.normal(size=(D, D))
     x = rng.normal(size=n)
@@ -58,7 +60,12 @@ def test_k3_bsgs_schedule_on_plain_slots(D, b):
     # 2D-1 nonzero diagonals; ~2 sqrt(d) rotations per input
     assert sum(len(ss) for _, _, ss in giants) == 2 * D - 1
     if D == 32 and b == 0:
-        assert n_rot == 15  # 7 baby + 8 giant; x2 inputs -> 30 HRots per frame
+        # 7 baby + 8 giant; x2 inputs -> 30 HRots per frame (aligned: 7 + 7, the giant G = 0 is free)
+        assert n_rot == (14 if aligned else 15)
+    if aligned:
+        assert [G for _, G, _ in giants].count(0) == 1 and all(G % bb == 0 for _, G, _ in giants)
+    if D == 32 and b == 16:
+        assert n_rot == 15 + 3  # the headline's K3 split: 15 baby steps, 3 giant rotations
 
 
 @pytest.mark.parametrize("h,n_in", [(8, 64), (16, 64), (5, 40)])
@@ -562,14 +569,14 @@ def test_double_hoisted_rotsum_equals_rotsum(count, inner):
 
 # ------------------------------------------------------------------ complex slots (reading R28)
 
-@pytest.mark.parametrize("hoist,L", [(1, 1), (2, 2)])
-def test_complex_k3_decrypts_to_dft(Pg, hoist, L):
+@pytest.mark.parametrize("hoist,L,aligned", [(1, 1, 0), (2, 2, 0), (2, 2, 1)])
+def test_complex_k3_decrypts_to_dft(Pg, hoist, L, aligned):
     """K3 on complex slots (cfg.cplx): z = v_re + j v_im in one ciphertext, complex diagonals
     of W~ -- decrypts (complex decode) to fftshift(fft(hann x)) per block and
     lane, with half the baby steps and giant rotations of the split layout."""
     P = Pg
     cfg, Zt = _gesture_setup(P, F=2)
-    cfg.hoist, cfg.lanes, cfg.cplx = hoist, L, 1
+    cfg.hoist, cfg.lanes, cfg.cplx, cfg.bsgs_aligned = hoist, L, 1, aligned
     n = cfg.n_slots
     keys = orc.keygen(P, seed=2301, rotations=cc.required_rotations("k3_doppler_dft", cfg, P.n))
     assert orc.CONJ not in keys.gk  # K3 alone needs no conjugation
