@@ -1292,10 +1292,14 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
     const double rows = level + 1 + pk;
     // algorithmic: babies read once, plaintexts once per launch, outputs written once
     ProfScope ps(c, "diag_mac", 8.0 * rows * c.n * (terms + B * 2.0 * (a.nc + a.no)), 2.0 * terms * rows * c.n * B);
-    static const bool l2_variant = [] {
+    // plaintext-stationary staging (k_diag_mac) once a batch amortises the tile's plaintext words
+    // (C4 complex K3, B = 13: 4.98 -> 4.15 ms, profiles/r02/c4prof_staged_r02ag.log); the L2-shared
+    // variant for small batches (FC, B = 1).  MMFHE_DIAG_STAGED=1 / 0 forces one (A/B runs).
+    static const int forced = [] {
         const char *e = getenv("MMFHE_DIAG_STAGED");
-        return !(e && *e == '1');
+        return e ? (*e == '1' ? 1 : 0) : -1;
     }();
+    const bool l2_variant = forced >= 0 ? forced == 0 : B < 4;
     if (l2_variant) {
         const dim3 g(((c.n + 255) / 256) * B, 2 * (level + 1 + pk));
         if (a.nc <= 4)

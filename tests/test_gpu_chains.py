@@ -318,7 +318,8 @@ def test_gesture_chain_lanes_small(m, lanes, F, fb, hoist):
 
 
 @pytest.mark.parametrize("lanes,F,fb,hoist,aligned", [(1, 2, 0, 0, 0), (1, 3, 2, 1, 0), (2, 5, 2, 2, 0), (4, 6, 0, 2, 0),
-                                                      (1, 2, 0, 0, 1), (2, 5, 2, 2, 1), (4, 6, 0, 2, 1)])
+                                                      (1, 2, 0, 0, 1), (2, 5, 2, 2, 1), (4, 6, 0, 2, 1),
+                                                      (1, 6, 0, 2, 1)])
 def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     """Complex-slot gesture pipeline (cfg.cplx, DESIGN R28): one ciphertext z = v_re + j v_im
     per frame group, K3 with complex diagonals (one plaintext product per diagonal), K1 as
