@@ -151,6 +151,10 @@ typedef struct {
                               floor((D-1)/b)), so the giant G = 0 needs no rotation (DESIGN R29; one giant
                               key switch fewer per input); 0 = the SURVEY §8(c)-7 split o = -(D-1) + g'b + s.
                               Different rotation keys and residues, same decryption */
+    uint32_t rotsum_inner; /* hoist = 2: size a of every rotate-and-sum's double-hoisted first level (DESIGN
+                              R27): one ModUp, a - 1 PQ steps summed in one pass, one ModDown, then log2(count/a)
+                              rotate-and-add steps; a power of two <= 64 (0 = 8).  Its Galois keys j*stride,
+                              j < a, are listed by mmfhe_chain_required_rotations; same decryption */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */

@@ -60,6 +60,7 @@ class ChainCfg:
     lanes: int = 1              # gesture / K3: frames interleaved per ciphertext (reading R20)
     fc_baby: int = 0            # FC BSGS baby steps (0: ceil(sqrt(h)))
     bsgs_aligned: int = 0       # K3: 1 -> giant offsets at multiples of b, one giant step the identity (R29)
+    rotsum_inner: int = 0       # double hoisting: size of the rotate-and-sum's hoisted first level (R27; 0 -> 8)
     cplx: int = 0               # gesture / K3: 1 -> complex slots, z = v_re + j v_im in ONE ciphertext
                                 # per frame (group); K3 multiplies complex diagonals, K1 is z conj(z)
                                 # (reading R28)
@@ -377,6 +378,14 @@ def baby_steps(ev, cts, steps, hoist):
     return [[ev.hoisted_step(x, y, s) for x, y in zip(cts, ys)] for s in steps]
 
 
+def rotsum_inner(cfg) -> int:
+    """Size a of the double-hoisted first rotate-and-sum level (R27): cfg.rotsum_inner, a power of
+    two (0 -> 8)."""
+    a = int(getattr(cfg, "rotsum_inner", 0) or 8)
+    log2_exact(a, "rotsum_inner")
+    return a
+
+
 def dh(cfg) -> bool:
     """Double-hoisted BSGS (cfg.hoist = 2): baby steps stay over
     Q_l u P (no ModDown), the inner sums multiply PQ-encoded diagonals, every giant step
@@ -547,8 +556,8 @@ def k2_doppler_soft_power(ev, Pm, cfg):
     (stride D; every block then holds sum_{a,r}, reading #8); S^gamma by squarings;
     f = Pm (.) S^gamma (P:906 'feature weighting')."""
     L = lanes_of(cfg)
-    rs = ev.rotsum_dh_all if dh(cfg) else ev.rotsum_all
-    S = rs(Pm, Pm[0].n_slots // L // cfg.D, cfg.D * L)
+    count, stride = Pm[0].n_slots // L // cfg.D, cfg.D * L
+    S = ev.rotsum_dh_all(Pm, count, stride, rotsum_inner(cfg)) if dh(cfg) else ev.rotsum_all(Pm, count, stride)
     for _ in range(log2_exact(cfg.gamma, "gamma")):
         S = ev.square_rescale_all(S)
     Pd = [ev.drop_to(p, s.level) for p, s in zip(Pm, S)]
@@ -608,7 +617,7 @@ def fc_schedule(h: int, fc_baby: int = 0):
 
 
 def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int, square: bool, hoist: int = 0,
-             L: int = 1, fc_baby: int = 0):
+             L: int = 1, fc_baby: int = 0, rs_inner: int = 8):
     """One layer of Eq. mlp_forward: z = sum_i diag_i (.) Rot(x, i) by BSGS,
     y = rotsum_{n_in/h}(z, stride h) (h-periodic W x), + b, then (.)^2 unless last.
     L lanes: rotations by L i, lane-interleaved diagonals and bias (reading R20)."""
@@ -632,7 +641,7 @@ def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int
             inner = ev.rotate_pq(inner, G * L) if pq else ev.rotate(inner, G * L)
         acc = inner if acc is None else (ev.add_pq(acc, inner) if pq else ev.add(acc, inner))
     z = ev.rescale(ev.moddown_ct(acc) if pq else acc)
-    y = (ev.rotsum_dh_all if pq else ev.rotsum_all)([z], n_in // h, h * L)[0]
+    y = (ev.rotsum_dh_all([z], n_in // h, h * L, rs_inner) if pq else ev.rotsum_all([z], n_in // h, h * L))[0]
     bv = lane_vec(np.asarray(bias, dtype=np.float64), L)
     y = ev.add_plain(y, book.vec(f"fc{layer}.bias", bv, y.level, scale=y.scale))
     if square:
@@ -660,10 +669,14 @@ def gesture_fc(ev, book, feat, Ws, bs, cfg):
     dims = cfg.fc_dims
     Ws, bs = pad_fc(Ws, bs, dims)
     L = lanes_of(cfg)
-    x = (ev.rotsum_dh_all if dh(cfg) else ev.rotsum_all)([feat], L, 1)[0] if L > 1 else feat
+    inner = rotsum_inner(cfg)
+    if L > 1:
+        x = (ev.rotsum_dh_all([feat], L, 1, inner) if dh(cfg) else ev.rotsum_all([feat], L, 1))[0]
+    else:
+        x = feat
     for layer in range(len(Ws)):
         x = fc_layer(ev, book, x, Ws[layer], bs[layer], dims[layer], layer + 1, layer < len(Ws) - 1, cfg.hoist, L,
-                     getattr(cfg, "fc_baby", 0))
+                     getattr(cfg, "fc_baby", 0), inner)
     return x
 
 
@@ -856,7 +869,7 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
     def rotsum_keys(count, stride):  # + the double-hoisted inner group's strides (R27)
         out = set(rotsum_steps(count, stride))
         if dh(cfg):
-            out |= {j * stride for j in range(1, min(8, count))}
+            out |= {j * stride for j in range(1, min(rotsum_inner(cfg), count))}
         return out
 
     if chain in ("k3_doppler_dft", "gesture_frame", "gesture", "gesture_features"):

@@ -127,6 +127,9 @@ Sched k3_schedule(const mmfhe_chain_cfg &cfg)
     return s;
 }
 
+// size of the double-hoisted first rotate-and-sum level (R27): cfg.rotsum_inner, a power of two (0 -> 8)
+uint32_t rotsum_inner(const mmfhe_chain_cfg &cfg) { return cfg.rotsum_inner ? cfg.rotsum_inner : 8; }
+
 // plaintext-name prefix of K3's diagonals (the aligned schedule's differ, R29)
 std::string k3_prefix(const mmfhe_chain_cfg &cfg) { return cfg.bsgs_aligned ? "k3a" : "k3"; }
 
@@ -212,7 +215,7 @@ class Runner {
     // reading R27), then the remaining rotate-and-add steps
     DCt rotsum(const DCt &x, uint32_t count, uint32_t stride)
     {
-        const uint32_t a = std::min<uint32_t>(8, count);
+        const uint32_t a = std::min<uint32_t>(rotsum_inner(cfg_), count);
         if (!dh() || a <= 1) return ev_rotsum(c_, x, count, stride);
         std::vector<int32_t> st;
         for (uint32_t j = 1; j < a; ++j) st.push_back((int32_t)(stride * j));
@@ -793,6 +796,8 @@ void validate_cfg(const std::string &chain, const mmfhe_chain_cfg &cfg)
     MMFHE_REQUIRE(cfg.hoist <= 2, MMFHE_E_INVALID_ARG, "hoist must be 0, 1 or 2");
     MMFHE_REQUIRE(cfg.cplx <= 1, MMFHE_E_INVALID_ARG, "cplx must be 0 or 1");
     MMFHE_REQUIRE(cfg.bsgs_aligned <= 1, MMFHE_E_INVALID_ARG, "bsgs_aligned must be 0 or 1");
+    MMFHE_REQUIRE(pow2_or_zero(cfg.rotsum_inner) && cfg.rotsum_inner <= 64, MMFHE_E_INVALID_ARG,
+                  "rotsum_inner must be a power of two <= 64");
     if (cfg.cplx)
         MMFHE_REQUIRE(cplx_chain(chain, cfg) || chain == "gesture_fc" || chain == "fc_forward" ||
                           chain == "k2_doppler_soft_power" || chain == "k6_notch",
@@ -867,7 +872,7 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
     auto add_rotsum = [&](uint32_t count, uint32_t stride) {
         for (uint32_t s : rotsum_steps(count, stride)) add(s);
         if (cfg.hoist == 2)
-            for (uint32_t j = 1; j < std::min<uint32_t>(8, count); ++j) add((int64_t)j * stride);
+            for (uint32_t j = 1; j < std::min<uint32_t>(rotsum_inner(cfg), count); ++j) add((int64_t)j * stride);
     };
     if (frames || chain == "k2_doppler_soft_power") add_rotsum(cfg.n_slots / cfg.D, cfg.D * (uint32_t)L);
     if (frames && cfg.cplx) ks.insert(MMFHE_STEP_CONJ);  // K1 = d Conj(d) (DESIGN R28)

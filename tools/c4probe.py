@@ -25,6 +25,7 @@ ap.add_argument("--bsgs", type=int, default=0, help="K3 baby steps b (0: ceil(sq
 ap.add_argument("--fc-baby", type=int, default=0)
 ap.add_argument("--cplx", type=int, default=0, help="complex slots (DESIGN R28)")
 ap.add_argument("--aligned", type=int, default=0, help="K3 giants at multiples of b (DESIGN R29)")
+ap.add_argument("--inner", type=int, default=0, help="double-hoisted rotate-and-sum first level (R27; 0 = 8)")
 ap.add_argument("--chains", default="", help="comma-separated extra chains to profile on the session's inputs "
                                              "(k3_doppler_dft, gesture_frame)")
 ap.add_argument("--split", action="store_true", help="also profile gesture_features and gesture_fc on their own")
@@ -36,7 +37,8 @@ F = args.frames
 stream = torch.cuda.current_stream(dev)
 cfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8),
                   frame_batch=25 if args.lanes == 1 else 0, hoist=args.hoist, lanes=args.lanes, bsgs_baby=args.bsgs,
-                  fc_baby=args.fc_baby, cplx=args.cplx, bsgs_aligned=args.aligned)
+                  fc_baby=args.fc_baby, cplx=args.cplx, bsgs_aligned=args.aligned,
+                  rotsum_inner=args.inner)
 ctx = m.Context.from_params(P, device=0, stream=stream.cuda_stream)
 gen = torch.Generator(device=dev)
 gen.manual_seed(77)
