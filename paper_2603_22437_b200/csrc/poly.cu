@@ -84,7 +84,10 @@ __device__ __forceinline__ uint32_t ext_prime(uint32_t r, uint32_t level, uint32
 // small modular matrix product (n_tgt x alpha per coefficient) and MAC-bound at PS3/PS4:
 // the digit's constants are staged in shared memory once per CTA (broadcast reads) and
 // each thread converts kBcK coefficients, so every constant feeds kBcK MAC chains.
-constexpr int kBcK = 2;
+#ifndef MMFHE_BCK
+#define MMFHE_BCK 2
+#endif
+constexpr int kBcK = MMFHE_BCK;
 
 template <int AMAX>
 __global__ void __launch_bounds__(kTB) k_modup(uint64_t *__restrict__ y_base, const uint64_t *__restrict__ x_base,
