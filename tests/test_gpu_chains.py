@@ -360,6 +360,12 @@ def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     # the split layout's input count is rejected for complex slots, and vice versa
     with pytest.raises(m.MmfheError):
         ctx.chain_plan("gesture", _mcfg(m, cfg), P.L, 2 * len(cts))
+    # without the conjugation key the chain stops with E_MISSING_KEY naming that key
+    nokey = orc.Keys(keys.s, keys.pk, keys.rlk, {k: v for k, v in keys.gk.items() if k != orc.CONJ})
+    ctx3 = make_ctx(m, P, nokey, book)
+    with pytest.raises(m.MmfheError) as e:
+        ctx3.eval_chain("gesture", _mcfg(m, cfg), [ct_in(m, P, c) for c in cts], [ct_out(m, P, logits.level)])
+    assert e.value.name == "E_MISSING_KEY" and "conjugation" in str(e.value)
 
 
 def test_frame_sharded_gesture_exchange(m):
@@ -503,6 +509,25 @@ def test_chain_shape_and_depth_errors(m):
     rots = ctx.required_rotations("vitals_v2", c3)
     assert all((8 << j) in rots and (P.n // 2 - (8 << j)) in rots for j in range(3))
     assert rots == cc.required_rotations("vitals_v2", cc.ChainCfg(R=8, F=8, n_slots=P.n // 2, iq_pack=3), P.n)
+    # round-2 cfg fields (R27-R29): invalid values and chains they do not apply to are rejected
+    g = dict(A=2, R=4, D=8, F=2, gamma=4, n_slots=64, fc_dims=(64, 16, 8, 8), hoist=2)
+    ctx12 = make_ctx(m, toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2))
+    for bad, name in ((dict(cplx=2), "E_INVALID_ARG"), (dict(bsgs_aligned=2), "E_INVALID_ARG"),
+                      (dict(rotsum_inner=3), "E_INVALID_ARG"), (dict(rotsum_inner=128), "E_INVALID_ARG")):
+        with pytest.raises(m.MmfheError) as e:
+            ctx12.chain_plan("gesture", m.chain_cfg(**g, **bad), 11, 4)
+        assert e.value.name == name, bad
+    with pytest.raises(m.MmfheError) as e:
+        ctx8.chain_plan("vitals_v1", m.chain_cfg(R=8, F=3, gamma=2, n_slots=P.n // 2, cplx=1), 3, 6)
+    assert e.value.name == "E_SHAPE"
+    # complex slots: one input per frame group, and the conjugation key is required
+    cc_ = m.chain_cfg(**g, cplx=1)
+    assert len(ctx12.chain_plan("gesture", cc_, 11, 2)) == 1
+    with pytest.raises(m.MmfheError) as e:
+        ctx12.chain_plan("gesture", cc_, 11, 4)
+    assert e.value.name == "E_SHAPE"
+    assert ctx12.required_rotations("gesture", cc_)[0] == m.STEP_CONJ
+    assert m.STEP_CONJ not in ctx12.required_rotations("gesture", m.chain_cfg(**g))
 
 
 # ------------------------------------------------------------------ the kernels on their own

@@ -633,3 +633,20 @@ def test_complex_gesture_pipeline(Pg, hoist):
     assert int(np.argmax(got)) == int(np.argmax(want))
     with pytest.raises(ValueError):
         cc.gesture_frames(ev, book, z, z, cfg)
+
+
+def test_round2_cfg_fields_validated():
+    """rotsum_inner must be a power of two (R27); the aligned K3 schedule (R29) and complex slots
+    (R28) change the key set as stated: the conjugation key only with complex slots, and aligned
+    giants drop the G = 0 rotation key."""
+    with pytest.raises(ValueError):
+        cc.rotsum_inner(cc.ChainCfg(rotsum_inner=3))
+    assert cc.rotsum_inner(cc.ChainCfg()) == 8 and cc.rotsum_inner(cc.ChainCfg(rotsum_inner=16)) == 16
+    n_ring = 1 << 16
+    base = dict(A=4, R=32, D=32, n_slots=4096, gamma=4, fc_dims=(4096, 64, 32, 8), bsgs_baby=16, hoist=2, lanes=8)
+    k_plain = cc.required_rotations("gesture", cc.ChainCfg(**base), n_ring)
+    k_cplx = cc.required_rotations("gesture", cc.ChainCfg(**base, cplx=1), n_ring)
+    assert orc.CONJ not in k_plain and k_cplx == [orc.CONJ] + k_plain
+    k3a = cc.required_rotations("k3_doppler_dft", cc.ChainCfg(**base, bsgs_aligned=1), n_ring)
+    assert k3a == sorted({(s * 8) % (n_ring // 2) for s in range(1, 16)} |
+                         {(G * 8) % (n_ring // 2) for G in (-32, -16, 16)})
