@@ -969,7 +969,7 @@ def run_reference(args, rank, world):
     total, mean = st.session_seconds()
     v = st.cfg["F"] / total
     sample = (f"step i = stage i mod 8 of the C4 session ({', '.join(st.stages)}), each fed by the previous stage; "
-              f"session = {n_pairs(st.cfg)} pairs x pair stages + FC stages = {total:.1f} s; mean stage seconds "
+              f"session = {n_pairs(st.cfg)} frame groups x group stages + FC stages = {total:.1f} s; mean stage seconds "
               + ", ".join(f"{k} {v_:.1f}" for k, v_ in mean.items())
               + f"; OpenMP across limbs on {omp_threads()} threads ({cpu_model()}); public-operand encoding excluded")
     return {"metric": METRIC, "value": v, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
