@@ -49,7 +49,8 @@ FC_DIMS = (4096, 64, 32, 8)        # 5 logits padded to 8
 FC_BABY = 16                       # FC BSGS baby steps: min(16, h) (measured 78.0 -> 76.7 ms vs ceil(sqrt(h)))
 CPLX = 1                           # complex slots z = v_re + j v_im, one ciphertext per frame group (DESIGN R28)
 ALIGNED = 1                        # K3 giants at multiples of b: the giant G = 0 needs no rotation (DESIGN R29)
-ROTSUM_INNER = 16                  # double-hoisted first rotate-and-sum level (R27): 16 measured 46.7 vs 47.3 ms (8)
+ROTSUM_INNER = 16                  # double-hoisted rotate-and-sum levels of 16 (R27)
+ROTSUM_HOIST_ALL = 1               # every level hoisted (R30): C4 46.7 -> 43.6 ms (profiles/r02/c4prof_*_r02ao.log)
 
 
 def band_bins(F_phase, fs, band):
@@ -68,7 +69,7 @@ def c4_config(lanes=LANES, level=19, F=100, cplx=CPLX):
     # products only, the giant steps full key switches: fewer giants, measured 89.3 -> 77.5 ms)
     return P, dict(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=FC_DIMS, hoist=2, lanes=lanes, level=level,
                    frame_batch=0 if lanes > 1 else 25, bsgs_baby=16, fc_baby=FC_BABY, cplx=cplx, bsgs_aligned=ALIGNED,
-                   rotsum_inner=ROTSUM_INNER)
+                   rotsum_inner=ROTSUM_INNER, rotsum_hoist_all=ROTSUM_HOIST_ALL)
 
 
 def gesture_mcfg(m, cfg):
@@ -76,7 +77,7 @@ def gesture_mcfg(m, cfg):
                        fc_dims=cfg["fc_dims"], frame_batch=cfg["frame_batch"], hoist=cfg["hoist"],
                        lanes=cfg["lanes"], bsgs_baby=cfg["bsgs_baby"], fc_baby=cfg["fc_baby"],
                        cplx=cfg.get("cplx", 0), bsgs_aligned=cfg.get("bsgs_aligned", 0),
-                       rotsum_inner=cfg.get("rotsum_inner", 0))
+                       rotsum_inner=cfg.get("rotsum_inner", 0), rotsum_hoist_all=cfg.get("rotsum_hoist_all", 0))
 
 
 def n_pairs(cfg):
@@ -111,8 +112,9 @@ def c4_bench_config(world, cfg):
                      f"{cfg['bsgs_baby']} x {-(-63 // cfg['bsgs_baby'])}"
                      + (" with giants at multiples of b (R29: the giant G = 0 is not rotated)"
                         if cfg.get("bsgs_aligned") else "") + f", FC baby steps min({cfg['fc_baby']}, h); "
-                     f"rotate-and-sums with a double-hoisted first level of {cfg.get('rotsum_inner') or 8} (R27, one "
-                     f"pass)" if cfg["hoist"] == 2 else
+                     f"rotate-and-sums with double-hoisted levels of {cfg.get('rotsum_inner') or 8} (R27, one pass per "
+                     f"level" + (", every level hoisted, R30)" if cfg.get("rotsum_hoist_all") else ")")
+                     if cfg["hoist"] == 2 else
                      "hoisted baby steps (hoist = 1)"),
             "sessions_per_step_per_gpu": 1, "parallelism": f"session-sharded x{world}",
             "l2": f"inputs larger than L2 ({n_inputs(cfg) * 20} MiB of ciphertexts per step, L2 126 MB)",
@@ -810,7 +812,8 @@ def oracle_c4_setup(lanes, cplx=CPLX):
     ccfg = cc.ChainCfg(A=cfg["A"], R=cfg["R"], D=cfg["D"], F=cfg["F"], gamma=cfg["gamma"], n_slots=cfg["n_slots"],
                        fc_dims=cfg["fc_dims"], frame_batch=cfg["frame_batch"], hoist=cfg["hoist"], lanes=lanes,
                        bsgs_baby=cfg["bsgs_baby"], fc_baby=cfg["fc_baby"], cplx=cplx,
-                       bsgs_aligned=cfg["bsgs_aligned"], rotsum_inner=cfg["rotsum_inner"])
+                       bsgs_aligned=cfg["bsgs_aligned"], rotsum_inner=cfg["rotsum_inner"],
+                       rotsum_hoist_all=cfg["rotsum_hoist_all"])
     basis = list(P.q) + list(P.p)
     seed = 77
 

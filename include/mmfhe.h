@@ -155,6 +155,10 @@ typedef struct {
                               R27): one ModUp, a - 1 PQ steps summed in one pass, one ModDown, then log2(count/a)
                               rotate-and-add steps; a power of two <= 64 (0 = 8).  Its Galois keys j*stride,
                               j < a, are listed by mmfhe_chain_required_rotations; same decryption */
+    uint32_t rotsum_hoist_all; /* hoist = 2: 1 = EVERY level of a rotate-and-sum double-hoisted (DESIGN R30):
+                              levels of min(rotsum_inner, what is left) terms, each one ModUp + one-pass PQ
+                              steps + one ModDown, no plain rotate-and-add key switches; 0 = R27 (first
+                              level hoisted, then rotate-and-adds).  Same decryption */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */

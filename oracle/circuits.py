@@ -61,6 +61,7 @@ class ChainCfg:
     fc_baby: int = 0            # FC BSGS baby steps (0: ceil(sqrt(h)))
     bsgs_aligned: int = 0       # K3: 1 -> giant offsets at multiples of b, one giant step the identity (R29)
     rotsum_inner: int = 0       # double hoisting: size of the rotate-and-sum's hoisted first level (R27; 0 -> 8)
+    rotsum_hoist_all: int = 0   # double hoisting: 1 -> every rotate-and-sum level hoisted (groups of rotsum_inner, R30)
     cplx: int = 0               # gesture / K3: 1 -> complex slots, z = v_re + j v_im in ONE ciphertext
                                 # per frame (group); K3 multiplies complex diagonals, K1 is z conj(z)
                                 # (reading R28)
@@ -264,7 +265,7 @@ class CircuitEvaluator(orc.Evaluator):
         return acc
 
 
-    def rotsum_dh_all(self, cts, count: int, stride: int, inner: int = 8):
+    def rotsum_dh_all(self, cts, count: int, stride: int, inner: int = 8, all_levels: bool = False):
         """Rotate-and-sum with a double-hoisted first level (reading R27):
         with a = min(inner, count), t = ModDown(P x + sum_{0<j<a} Rot_PQ(x, j stride)) -- one
         ModUp of x, a - 1 hoisted rotations left over Q_l u P (hoisted_step_pq), their PQ sum
@@ -280,6 +281,9 @@ class CircuitEvaluator(orc.Evaluator):
         for r in rots:
             acc = [self.add_pq(p, q) for p, q in zip(acc, r)]
         t = [self.moddown_ct(p) for p in acc]
+        if all_levels and count // a > 1:
+            # reading R30: the remaining sum is again a double-hoisted level (groups of `inner`)
+            return self.rotsum_dh_all(t, count // a, stride * a, inner, True)
         return self.rotsum_all(t, count // a, stride * a)
 
 
@@ -384,6 +388,26 @@ def rotsum_inner(cfg) -> int:
     a = int(getattr(cfg, "rotsum_inner", 0) or 8)
     log2_exact(a, "rotsum_inner")
     return a
+
+
+def rotsum_dh(ev, cts, count: int, stride: int, cfg, inner: int | None = None):
+    """The rotate-and-sum of the double-hoisted circuits: rotsum_dh_all with the chain's level size
+    (R27) and, with cfg.rotsum_hoist_all, every level hoisted (R30)."""
+    return ev.rotsum_dh_all(cts, count, stride, rotsum_inner(cfg) if inner is None else inner,
+                            bool(getattr(cfg, "rotsum_hoist_all", 0)))
+
+
+def rotsum_levels(count: int, inner: int, all_levels: bool):
+    """Group sizes of the double-hoisted levels of a rotate-and-sum over `count` terms (R27 / R30);
+    the plain rotate-and-add steps that follow the hoisted levels are log2 of what is left."""
+    out, c = [], count
+    while c > 1:
+        a = min(inner, c)
+        out.append(a)
+        c //= a
+        if not all_levels:
+            break
+    return out
 
 
 def dh(cfg) -> bool:
@@ -557,7 +581,7 @@ def k2_doppler_soft_power(ev, Pm, cfg):
     f = Pm (.) S^gamma (P:906 'feature weighting')."""
     L = lanes_of(cfg)
     count, stride = Pm[0].n_slots // L // cfg.D, cfg.D * L
-    S = ev.rotsum_dh_all(Pm, count, stride, rotsum_inner(cfg)) if dh(cfg) else ev.rotsum_all(Pm, count, stride)
+    S = rotsum_dh(ev, Pm, count, stride, cfg) if dh(cfg) else ev.rotsum_all(Pm, count, stride)
     for _ in range(log2_exact(cfg.gamma, "gamma")):
         S = ev.square_rescale_all(S)
     Pd = [ev.drop_to(p, s.level) for p, s in zip(Pm, S)]
@@ -617,7 +641,7 @@ def fc_schedule(h: int, fc_baby: int = 0):
 
 
 def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int, square: bool, hoist: int = 0,
-             L: int = 1, fc_baby: int = 0, rs_inner: int = 8):
+             L: int = 1, fc_baby: int = 0, rs_inner: int = 8, rs_all: bool = False):
     """One layer of Eq. mlp_forward: z = sum_i diag_i (.) Rot(x, i) by BSGS,
     y = rotsum_{n_in/h}(z, stride h) (h-periodic W x), + b, then (.)^2 unless last.
     L lanes: rotations by L i, lane-interleaved diagonals and bias (reading R20)."""
@@ -641,7 +665,7 @@ def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int
             inner = ev.rotate_pq(inner, G * L) if pq else ev.rotate(inner, G * L)
         acc = inner if acc is None else (ev.add_pq(acc, inner) if pq else ev.add(acc, inner))
     z = ev.rescale(ev.moddown_ct(acc) if pq else acc)
-    y = (ev.rotsum_dh_all([z], n_in // h, h * L, rs_inner) if pq else ev.rotsum_all([z], n_in // h, h * L))[0]
+    y = (ev.rotsum_dh_all([z], n_in // h, h * L, rs_inner, rs_all) if pq else ev.rotsum_all([z], n_in // h, h * L))[0]
     bv = lane_vec(np.asarray(bias, dtype=np.float64), L)
     y = ev.add_plain(y, book.vec(f"fc{layer}.bias", bv, y.level, scale=y.scale))
     if square:
@@ -671,12 +695,12 @@ def gesture_fc(ev, book, feat, Ws, bs, cfg):
     L = lanes_of(cfg)
     inner = rotsum_inner(cfg)
     if L > 1:
-        x = (ev.rotsum_dh_all([feat], L, 1, inner) if dh(cfg) else ev.rotsum_all([feat], L, 1))[0]
+        x = (rotsum_dh(ev, [feat], L, 1, cfg) if dh(cfg) else ev.rotsum_all([feat], L, 1))[0]
     else:
         x = feat
     for layer in range(len(Ws)):
         x = fc_layer(ev, book, x, Ws[layer], bs[layer], dims[layer], layer + 1, layer < len(Ws) - 1, cfg.hoist, L,
-                     getattr(cfg, "fc_baby", 0), inner)
+                     getattr(cfg, "fc_baby", 0), inner, bool(getattr(cfg, "rotsum_hoist_all", 0)))
     return x
 
 
@@ -866,10 +890,15 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
             ks |= {m * cfg.R for m in range(1, 1 << cfg.iq_pack)}
     L = lanes_of(cfg)
 
-    def rotsum_keys(count, stride):  # + the double-hoisted inner group's strides (R27)
-        out = set(rotsum_steps(count, stride))
-        if dh(cfg):
-            out |= {j * stride for j in range(1, min(rotsum_inner(cfg), count))}
+    def rotsum_keys(count, stride):  # + the double-hoisted levels' strides (R27 / R30)
+        if not dh(cfg):
+            return set(rotsum_steps(count, stride))
+        out, st, c = set(), stride, count
+        for a in rotsum_levels(count, rotsum_inner(cfg), bool(getattr(cfg, "rotsum_hoist_all", 0))):
+            out |= {j * st for j in range(1, a)}
+            st *= a
+            c //= a
+        return out | set(rotsum_steps(c, st))
         return out
 
     if chain in ("k3_doppler_dft", "gesture_frame", "gesture", "gesture_features"):

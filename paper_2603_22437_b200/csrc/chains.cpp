@@ -221,6 +221,8 @@ class Runner {
         for (uint32_t j = 1; j < a; ++j) st.push_back((int32_t)(stride * j));
         // lift + the a-1 PQ steps summed in one pass (k_hoisted_rotsum_pq), one ModDown
         DCt t = ev_moddown_ct(c_, ev_rotsum_hoisted_pq(c_, x, st));
+        // R30: every level hoisted (oracle rotsum_dh_all(..., all_levels)); else rotate-and-adds
+        if (cfg_.rotsum_hoist_all && count / a > 1) return rotsum(t, count / a, stride * a);
         return ev_rotsum(c_, t, count / a, stride * a);
     }
 
@@ -798,6 +800,7 @@ void validate_cfg(const std::string &chain, const mmfhe_chain_cfg &cfg)
     MMFHE_REQUIRE(cfg.bsgs_aligned <= 1, MMFHE_E_INVALID_ARG, "bsgs_aligned must be 0 or 1");
     MMFHE_REQUIRE(pow2_or_zero(cfg.rotsum_inner) && cfg.rotsum_inner <= 64, MMFHE_E_INVALID_ARG,
                   "rotsum_inner must be a power of two <= 64");
+    MMFHE_REQUIRE(cfg.rotsum_hoist_all <= 1, MMFHE_E_INVALID_ARG, "rotsum_hoist_all must be 0 or 1");
     if (cfg.cplx)
         MMFHE_REQUIRE(cplx_chain(chain, cfg) || chain == "gesture_fc" || chain == "fc_forward" ||
                           chain == "k2_doppler_soft_power" || chain == "k6_notch",
@@ -870,9 +873,16 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
     }
     // a rotate-and-sum's keys; with double hoisting (R27) also j stride, j < min(8, count)
     auto add_rotsum = [&](uint32_t count, uint32_t stride) {
+        if (cfg.hoist == 2) {  // the double-hoisted levels (R27 / R30), then plain rotate-and-add steps
+            do {
+                const uint32_t a = std::min<uint32_t>(rotsum_inner(cfg), count);
+                if (a <= 1) break;
+                for (uint32_t j = 1; j < a; ++j) add((int64_t)j * stride);
+                count /= a;
+                stride *= a;
+            } while (cfg.rotsum_hoist_all && count > 1);
+        }
         for (uint32_t s : rotsum_steps(count, stride)) add(s);
-        if (cfg.hoist == 2)
-            for (uint32_t j = 1; j < std::min<uint32_t>(rotsum_inner(cfg), count); ++j) add((int64_t)j * stride);
     };
     if (frames || chain == "k2_doppler_soft_power") add_rotsum(cfg.n_slots / cfg.D, cfg.D * (uint32_t)L);
     if (frames && cfg.cplx) ks.insert(MMFHE_STEP_CONJ);  // K1 = d Conj(d) (DESIGN R28)

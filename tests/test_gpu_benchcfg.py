@@ -132,11 +132,12 @@ def test_c2_bench_params_residue_parity(m):
 # ------------------------------------------------------------------ C4 (bench configs[3])
 
 def _c4_case(lanes, F, seed, hoist=1, bsgs=0, fc_baby=0, cplx=0, aligned=0, inner=0):
+    """inner: the rotate-and-sum level size (R27); inner > 0 with cplx also hoists every level (R30)."""
     P = ps4()
     A, R, D = 4, 32, 32
     cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25,
                       hoist=hoist, lanes=lanes, bsgs_baby=bsgs, fc_baby=fc_baby, cplx=cplx, bsgs_aligned=aligned,
-                      rotsum_inner=inner)
+                      rotsum_inner=inner, rotsum_hoist_all=int(inner > 0 and cplx > 0))
     Z, _ = radar.gesture_scene(A, R, D, F, seed=seed, cls=seed % 5)
     Zt = radar.preprocess_gesture(Z)
     keys = orc.keygen(P, seed=seed + 1, rotations=cc.required_rotations("gesture", cfg, P.n))
@@ -156,12 +157,15 @@ def _c4_case(lanes, F, seed, hoist=1, bsgs=0, fc_baby=0, cplx=0, aligned=0, inne
 
 
 @pytest.mark.parametrize("lanes,F,hoist,bsgs,fc_baby,cplx,aligned,inner", [
-    (1, 2, 1, 0, 0, 0, 0, 0), (8, 16, 2, 16, 16, 0, 0, 0), (8, 16, 2, 16, 16, 1, 1, 16)])
+    (1, 2, 1, 0, 0, 0, 0, 0), (8, 16, 2, 16, 16, 0, 0, 0), (8, 16, 2, 16, 16, 1, 1, 16),
+    (8, 32, 2, 16, 16, 1, 1, 16)])
 def test_c4_bench_params_residue_parity(m, lanes, F, hoist, bsgs, fc_baby, cplx, aligned, inner):
     """PS4 gesture at entry level 19 with the FC head (bench C4), bit-exact: canonical (one
     frame per ciphertext, 2 frames, hoisted BSGS), the split-layout variant (8 frames per
     ciphertext, 2 packed ciphertext pairs = 16 frames, double-hoisted BSGS with K3 split 16 x 4)
-    and the bench's headline: the same on complex slots (2 ciphertexts, DESIGN R28)."""
+    and the bench's headline: the same on complex slots (2 ciphertexts, DESIGN R28) with aligned giants
+    (R29) and rotate-and-sum levels of 16 (R27) -- and with 4 ciphertexts (32 frames), the batch from
+    which K3's inner sums take the plaintext-stationary staged kernel (k_diag_mac<16> over Q_l u P)."""
     P, cfg, keys, cts, xp = _c4_case(lanes, F, 6100 + lanes + 7 * cplx, hoist, bsgs, fc_baby, cplx, aligned, inner)
     Ws, bs = radar.fc_weights([4096, 64, 32, 5], seed=6200)
     gain = min(0.8 / max(np.max(np.abs(Ws[0] @ xp)), 1e-30), 2000.0 / np.max(np.abs(Ws[0])))
@@ -174,7 +178,7 @@ def test_c4_bench_params_residue_parity(m, lanes, F, hoist, bsgs, fc_baby, cplx,
     ctx = make_ctx(m, P, keys, book)
     mcfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25,
                        hoist=hoist, lanes=lanes, bsgs_baby=bsgs, fc_baby=fc_baby, cplx=cplx, bsgs_aligned=aligned,
-                      rotsum_inner=inner)
+                      rotsum_inner=inner, rotsum_hoist_all=int(inner > 0 and cplx > 0))
     assert sorted(ctx.required_rotations("gesture", mcfg)) == cc.required_rotations("gesture", cfg, P.n)
     levels = ctx.chain_plan("gesture", mcfg, 19, len(cts))
     assert levels == [logits.level] == [19 - 11]

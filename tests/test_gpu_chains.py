@@ -30,7 +30,8 @@ def _mcfg(m, cfg: cc.ChainCfg, bins=(), taps=()):
                        fc_dims=cfg.fc_dims, notch_width=cfg.notch_width, bands_bins=bins,
                        n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch, hoist=cfg.hoist,
                        vp_plus=cfg.vp_plus, iq_pack=cfg.iq_pack, lanes=cfg.lanes, cplx=cfg.cplx,
-                       bsgs_aligned=cfg.bsgs_aligned, rotsum_inner=cfg.rotsum_inner)
+                       bsgs_aligned=cfg.bsgs_aligned, rotsum_inner=cfg.rotsum_inner,
+                       rotsum_hoist_all=cfg.rotsum_hoist_all)
 
 
 def _run(m, P, keys, book, chain, cfg, cts, want, scalars=None, bins=(), taps=()):
@@ -319,7 +320,8 @@ def test_gesture_chain_lanes_small(m, lanes, F, fb, hoist):
 
 @pytest.mark.parametrize("lanes,F,fb,hoist,aligned", [(1, 2, 0, 0, 0), (1, 3, 2, 1, 0), (2, 5, 2, 2, 0), (4, 6, 0, 2, 0),
                                                       (1, 2, 0, 0, 1), (2, 5, 2, 2, 1), (4, 6, 0, 2, 1),
-                                                      (1, 6, 0, 2, 1), (4, 6, 0, 2, 2), (2, 5, 2, 2, 3)])
+                                                      (1, 6, 0, 2, 1), (4, 6, 0, 2, 2), (2, 5, 2, 2, 3),
+                                                      (4, 6, 0, 2, 4), (1, 3, 0, 2, 5)])
 def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     """Complex-slot gesture pipeline (cfg.cplx, DESIGN R28): one ciphertext z = v_re + j v_im
     per frame group, K3 with complex diagonals (one plaintext product per diagonal), K1 as
@@ -328,9 +330,11 @@ def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     the conjugation key id."""
     P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
     cfg, Zt = _gesture(P, 3241, F=F, frame_batch=fb, hoist=hoist)
-    # aligned 2 / 3: the aligned schedule with a double-hoisted rotate-and-sum level of 16 / 4 (R27)
+    # aligned 2 / 3: the aligned schedule with a double-hoisted rotate-and-sum level of 16 / 4 (R27);
+    # 4 / 5: every level hoisted in groups of 2 / 4 (R30)
     cfg.lanes, cfg.cplx, cfg.bsgs_aligned = lanes, 1, min(aligned, 1)
-    cfg.rotsum_inner = {2: 16, 3: 4}.get(aligned, 0)
+    cfg.rotsum_inner = {2: 16, 3: 4, 4: 2, 5: 4}.get(aligned, 0)
+    cfg.rotsum_hoist_all = int(aligned >= 4)
     rots = cc.required_rotations("gesture", cfg, P.n)
     assert rots[0] == orc.CONJ == m.STEP_CONJ
     keys = orc.keygen(P, seed=3242, rotations=rots)

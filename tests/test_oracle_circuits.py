@@ -567,6 +567,35 @@ def test_double_hoisted_rotsum_equals_rotsum(count, inner):
     assert ops.count("hrot") == int(np.log2(count // a))
 
 
+@pytest.mark.parametrize("count,inner", [(32, 4), (16, 2), (8, 8), (64, 4)])
+def test_all_levels_hoisted_rotsum_equals_rotsum(count, inner):
+    """Reading R30: every level of the rotate-and-sum double-hoisted (groups of `inner`, the last
+    one what is left) decrypts to the same slot sums; no plain HRot remains, one ModDown per level."""
+    P = toy(log_n=10, n_q=4, scale_bits=40, n_p=2, alpha=2)
+    stride = 3
+    levels = cc.rotsum_levels(count, inner, True)
+    assert int(np.prod(levels)) == count
+    rots = sorted({(j * stride) % (P.n // 2) for j in range(1, count)})
+    keys = orc.keygen(P, seed=2402, rotations=rots)
+    v = np.random.default_rng(count + 7).uniform(-1, 1, P.n // 2)
+    ct = _enc(P, keys, v, 3, 0)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    got = orc.decrypt_vector(P, keys, ev.rotsum_dh_all([ct], count, stride, inner, True)[0])
+    want = sum(np.roll(v, -m * stride) for m in range(count))
+    assert rel_err(got, want) < 1e-6
+    ops = [op for op, _, _ in ev.trace]
+    assert ops.count("hrot") == 0 and ops.count("moddown") == len(levels)
+    assert ops.count("hrot_hoisted_pq") == sum(a - 1 for a in levels)
+    # the key set of a chain using it (K2b: count = n / D terms at stride D): exactly the levels' strides
+    cfg = cc.ChainCfg(D=stride, n_slots=stride * count, hoist=2, rotsum_inner=inner, rotsum_hoist_all=1)
+    st, want_keys = stride, set()
+    for a in levels:
+        want_keys |= {j * st for j in range(1, a)}
+        st *= a
+    assert cc.required_rotations("k2_doppler_soft_power", cfg, P.n) == sorted(k % (P.n // 2) for k in want_keys)
+    assert cc.rotsum_levels(count, inner, False) == [min(inner, count)]
+
+
 # ------------------------------------------------------------------ complex slots (reading R28)
 
 @pytest.mark.parametrize("hoist,L,aligned", [(1, 1, 0), (2, 2, 0), (2, 2, 1)])
