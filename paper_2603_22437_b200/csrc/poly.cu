@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kHTile) k_hoisted_ip_pq(const uint64_t *__rest
 // running sums stay in the thread's own shared-memory column (16 KiB-per-item-chunk: no barriers), so the
 // group may have any number of steps and occupancy is not bound by a key tile.
 constexpr int kRTile = 128;
-constexpr int kRItems = 16;  // items per CTA (register accumulators)
+constexpr int kRItems = 16;  // items per CTA (running sums in shared memory)
 constexpr int kRSteps = 64;  // steps per launch (kernel-parameter arrays)
 struct HoistSumArgs {
     const uint64_t *key[kRSteps];
@@ -420,8 +420,11 @@ struct HoistSumArgs {
     uint32_t dnum, level, L, K, B, nsteps;
 };
 
+#ifndef MMFHE_RS_MINB
+#define MMFHE_RS_MINB 4  // measured: 4 (123 regs) 4.18 ms, 1 (128 regs) 5.98, 5 (96) 4.69, 6 (80) 5.34 (C4 K2b + FC)
+#endif
 template <int DMAX>
-__global__ void __launch_bounds__(kRTile) k_hoisted_rotsum_pq(uint64_t *__restrict__ out, const uint64_t *__restrict__ x,
+__global__ void __launch_bounds__(kRTile, MMFHE_RS_MINB) k_hoisted_rotsum_pq(uint64_t *__restrict__ out, const uint64_t *__restrict__ x,
                                                             const uint64_t *__restrict__ y,
                                                             const uint64_t *__restrict__ c0,
                                                             const TwPair *__restrict__ pmod, KTables kt,
@@ -461,34 +464,55 @@ __global__ void __launch_bounds__(kRTile) k_hoisted_rotsum_pq(uint64_t *__restri
         sacc[b][0][t] = v0;
         sacc[b][1][t] = v1;
     }
-    for (uint32_t s = 0; s < a.nsteps; ++s) {
-        const uint64_t *ks = a.key[s] + (size_t)pr * kt.n + j;
-        uint64_t kb[DMAX], ka[DMAX];
+    // steps in chunks of kRChunk: the chunk's key words and source indices in registers, then per item
+    // the chunk's products summed in 128 bits (<= 16 terms < q^2 each: < q 2^64 for q < 2^60) and its c0 words summed before ONE Shoup product by [P]_r (P times a sum
+    // = the sum of the P multiples): one Montgomery reduction per poly per chunk instead of per step
+#ifndef MMFHE_RS_TERMS
+#define MMFHE_RS_TERMS 16
+#endif
+    static_assert(MMFHE_RS_TERMS <= 16, "128-bit accumulation bound: <= 16 products < q^2, q < 2^60");
+    constexpr int kRChunk = MMFHE_RS_TERMS / DMAX > 0 ? MMFHE_RS_TERMS / DMAX : 1;  // steps per 128-bit sum
+    for (uint32_t s0 = 0; s0 < a.nsteps; s0 += kRChunk) {
+        const uint32_t ns = min((uint32_t)kRChunk, a.nsteps - s0);
+        uint64_t kb[kRChunk][DMAX], ka[kRChunk][DMAX];
+        uint32_t kk[kRChunk];
 #pragma unroll
-        for (int d = 0; d < DMAX; ++d) {
-            if (d < (int)a.dnum) {
-                kb[d] = __ldg(ks + (size_t)(2 * d) * key_rows * kt.n);
-                ka[d] = __ldg(ks + (size_t)(2 * d + 1) * key_rows * kt.n);
+        for (int u = 0; u < kRChunk; ++u) {
+            kk[u] = 0;
+            if (u < (int)ns) {
+                const uint64_t *ks = a.key[s0 + u] + (size_t)pr * kt.n + j;
+#pragma unroll
+                for (int d = 0; d < DMAX; ++d) {
+                    if (d < (int)a.dnum) {
+                        kb[u][d] = __ldg(ks + (size_t)(2 * d) * key_rows * kt.n);
+                        ka[u][d] = __ldg(ks + (size_t)(2 * d + 1) * key_rows * kt.n);
+                    }
+                }
+                kk[u] = galois_perm(j, a.g[s0 + u], kt.log_n);
             }
         }
-        const uint32_t kk = galois_perm(j, a.g[s], kt.log_n);
-#pragma unroll 2
         for (uint32_t b = 0; b < nb; ++b) {
-            uint64_t w[DMAX];
-#pragma unroll
-            for (int d = 0; d < DMAX; ++d)
-                if (d < (int)a.dnum) w[d] = src[d][(size_t)b * sst[d] + kk];
-            const uint64_t cw = isq ? c0r[(size_t)b * a.cs + kk] : 0;
             U128 p0{0, 0}, p1{0, 0};
+            uint64_t csum = 0;  // < kRChunk q
 #pragma unroll
-            for (int d = 0; d < DMAX; ++d) {
-                if (d < (int)a.dnum) {
-                    mac128(p0, w[d], kb[d]);
-                    mac128(p1, w[d], ka[d]);
+            for (int u = 0; u < kRChunk; ++u) {
+                if (u < (int)ns) {
+                    uint64_t w[DMAX];
+#pragma unroll
+                    for (int d = 0; d < DMAX; ++d)
+                        if (d < (int)a.dnum) w[d] = src[d][(size_t)b * sst[d] + kk[u]];
+                    if (isq) csum += c0r[(size_t)b * a.cs + kk[u]];
+#pragma unroll
+                    for (int d = 0; d < DMAX; ++d) {
+                        if (d < (int)a.dnum) {
+                            mac128(p0, w[d], kb[u][d]);
+                            mac128(p1, w[d], ka[u][d]);
+                        }
+                    }
                 }
             }
             uint64_t v0 = add_mod(sacc[b][0][t], redc(p0, q, qi), q);
-            if (isq) v0 = add_mod(v0, shoup(cw, pm.w, pm.wp, q), q);
+            if (isq) v0 = add_mod(v0, shoup(csum, pm.w, pm.wp, q), q);
             sacc[b][0][t] = v0;
             sacc[b][1][t] = add_mod(sacc[b][1][t], redc(p1, q, qi), q);
         }
