@@ -51,6 +51,7 @@ CPLX = 1                           # complex slots z = v_re + j v_im, one cipher
 ALIGNED = 1                        # K3 giants at multiples of b: the giant G = 0 needs no rotation (DESIGN R29)
 ROTSUM_INNER = 16                  # double-hoisted rotate-and-sum levels of 16 (R27)
 ROTSUM_HOIST_ALL = 1               # every level hoisted (R30): C4 46.7 -> 43.6 ms (profiles/r02/c4prof_*_r02ao.log)
+KS_MERGE = 1                       # relin / ModDown + rescale as one division by P q_l (R31): 42.5 -> 40.6 ms
 
 
 def band_bins(F_phase, fs, band):
@@ -69,7 +70,7 @@ def c4_config(lanes=LANES, level=19, F=100, cplx=CPLX):
     # products only, the giant steps full key switches: fewer giants, measured 89.3 -> 77.5 ms)
     return P, dict(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=FC_DIMS, hoist=2, lanes=lanes, level=level,
                    frame_batch=0 if lanes > 1 else 25, bsgs_baby=16, fc_baby=FC_BABY, cplx=cplx, bsgs_aligned=ALIGNED,
-                   rotsum_inner=ROTSUM_INNER, rotsum_hoist_all=ROTSUM_HOIST_ALL)
+                   rotsum_inner=ROTSUM_INNER, rotsum_hoist_all=ROTSUM_HOIST_ALL, ks_merge=KS_MERGE)
 
 
 def gesture_mcfg(m, cfg):
@@ -77,7 +78,8 @@ def gesture_mcfg(m, cfg):
                        fc_dims=cfg["fc_dims"], frame_batch=cfg["frame_batch"], hoist=cfg["hoist"],
                        lanes=cfg["lanes"], bsgs_baby=cfg["bsgs_baby"], fc_baby=cfg["fc_baby"],
                        cplx=cfg.get("cplx", 0), bsgs_aligned=cfg.get("bsgs_aligned", 0),
-                       rotsum_inner=cfg.get("rotsum_inner", 0), rotsum_hoist_all=cfg.get("rotsum_hoist_all", 0))
+                       rotsum_inner=cfg.get("rotsum_inner", 0), rotsum_hoist_all=cfg.get("rotsum_hoist_all", 0),
+                       ks_merge=cfg.get("ks_merge", 0))
 
 
 def n_pairs(cfg):
@@ -114,6 +116,8 @@ def c4_bench_config(world, cfg):
                         if cfg.get("bsgs_aligned") else "") + f", FC baby steps min({cfg['fc_baby']}, h); "
                      f"rotate-and-sums with double-hoisted levels of {cfg.get('rotsum_inner') or 8} (R27, one pass per "
                      f"level" + (", every level hoisted, R30)" if cfg.get("rotsum_hoist_all") else ")")
+                     + ("; relinearisation / ModDown + rescale as one division by P q_l (R31)" if cfg.get("ks_merge")
+                        else "")
                      if cfg["hoist"] == 2 else
                      "hoisted baby steps (hoist = 1)"),
             "sessions_per_step_per_gpu": 1, "parallelism": f"session-sharded x{world}",
@@ -813,7 +817,7 @@ def oracle_c4_setup(lanes, cplx=CPLX):
                        fc_dims=cfg["fc_dims"], frame_batch=cfg["frame_batch"], hoist=cfg["hoist"], lanes=lanes,
                        bsgs_baby=cfg["bsgs_baby"], fc_baby=cfg["fc_baby"], cplx=cplx,
                        bsgs_aligned=cfg["bsgs_aligned"], rotsum_inner=cfg["rotsum_inner"],
-                       rotsum_hoist_all=cfg["rotsum_hoist_all"])
+                       rotsum_hoist_all=cfg["rotsum_hoist_all"], ks_merge=cfg["ks_merge"])
     basis = list(P.q) + list(P.p)
     seed = 77
 

@@ -62,6 +62,8 @@ class ChainCfg:
     bsgs_aligned: int = 0       # K3: 1 -> giant offsets at multiples of b, one giant step the identity (R29)
     rotsum_inner: int = 0       # double hoisting: size of the rotate-and-sum's hoisted first level (R27; 0 -> 8)
     rotsum_hoist_all: int = 0   # double hoisting: 1 -> every rotate-and-sum level hoisted (groups of rotsum_inner, R30)
+    ks_merge: int = 0           # gesture / K3 / FC: 1 -> every ModDown or relinearisation followed by a rescale is
+                                # ONE division by P q_l (R31)
     cplx: int = 0               # gesture / K3: 1 -> complex slots, z = v_re + j v_im in ONE ciphertext
                                 # per frame (group); K3 multiplies complex diagonals, K1 is z conj(z)
                                 # (reading R28)
@@ -163,7 +165,11 @@ class PlainBook:
 # ------------------------------------------------------------------ evaluator ext
 
 class CircuitEvaluator(orc.Evaluator):
-    """Logical ops used by the circuits, each recorded once in the trace."""
+    """Logical ops used by the circuits, each recorded once in the trace.  merge_rescale (set by the
+    gesture / K3 / FC entry points from cfg.ks_merge, reading R31): relinearisation + rescale and
+    ModDown + rescale run as one division by P q_l."""
+
+    merge_rescale = False
 
     def tensor_sum(self, pairs) -> orc.Ct:
         """sum_i tensor(a_i, b_i) -- the lazy-relinearisation input (c-6)."""
@@ -247,7 +253,13 @@ class CircuitEvaluator(orc.Evaluator):
 
     # ---- op-major helpers over frame lists
     def relin_rescale_all(self, cts):
+        if self.merge_rescale:
+            return [self.relin_rescale_merged(x) for x in cts]
         return [self.rescale(x) for x in [self.relin(x) for x in cts]]
+
+    def down_rescale(self, x):
+        """A PQ ciphertext's ModDown followed by the rescale (one division with merge_rescale, R31)."""
+        return self.moddown_rescale_ct(x) if self.merge_rescale else self.rescale(self.moddown_ct(x))
 
     def square_rescale_all(self, cts):
         return self.relin_rescale_all([self.tensor_sum([(x, x)]) for x in cts])
@@ -410,6 +422,12 @@ def rotsum_levels(count: int, inner: int, all_levels: bool):
     return out
 
 
+def set_merge(ev, cfg):
+    """Reading R31 for the gesture / K3 / FC chains: the evaluator merges every relinearisation or
+    ModDown that a rescale follows into one division by P q_l (cfg.ks_merge)."""
+    ev.merge_rescale = bool(getattr(cfg, "ks_merge", 0))
+
+
 def dh(cfg) -> bool:
     """Double-hoisted BSGS (cfg.hoist = 2): baby steps stay over
     Q_l u P (no ModDown), the inner sums multiply PQ-encoded diagonals, every giant step
@@ -490,6 +508,8 @@ def k3_giant_steps(ev: CircuitEvaluator, inner, cfg: ChainCfg):
         ii = [rot(x, G * L) for x in pi]
         out_re = ir if out_re is None else [add(a, x) for a, x in zip(out_re, ir)]
         out_im = ii if out_im is None else [add(a, x) for a, x in zip(out_im, ii)]
+    if dh(cfg) and ev.merge_rescale:
+        return [ev.down_rescale(x) for x in out_re], [ev.down_rescale(x) for x in out_im]
     if dh(cfg):
         out_re = [ev.moddown_ct(x) for x in out_re]
         out_im = [ev.moddown_ct(x) for x in out_im]
@@ -500,6 +520,7 @@ def k3_doppler_dft_frames(ev: CircuitEvaluator, book: PlainBook, v_re, v_im, cfg
     """K3 (Eqs. dft_re/dft_im P:805-815) on a list of frames: d_re = C~ v_re - S~ v_im,
     d_im = S~ v_re + C~ v_im via BSGS with pre-rotated diagonals: baby steps, all giant
     steps' inner sums, then the giant rotations; one rescale after the giant sum (c-6)."""
+    set_merge(ev, cfg)
     xr, xi = k3_baby_steps(ev, v_re, v_im, cfg)
     return k3_giant_steps(ev, k3_inner_sums(ev, book, xr, xi, cfg), cfg)
 
@@ -535,6 +556,8 @@ def k3_giant_steps_c(ev: CircuitEvaluator, inner, cfg: ChainCfg):
     for (gp, G, babies), pr in zip(giants, inner):
         r = [rot_(x, G * L) for x in pr]
         out = r if out is None else [add(a, x) for a, x in zip(out, r)]
+    if dh(cfg) and ev.merge_rescale:
+        return [ev.down_rescale(x) for x in out]
     if dh(cfg):
         out = [ev.moddown_ct(x) for x in out]
     return [ev.rescale(x) for x in out]
@@ -542,6 +565,7 @@ def k3_giant_steps_c(ev: CircuitEvaluator, inner, cfg: ChainCfg):
 
 def k3_doppler_dft_frames_c(ev: CircuitEvaluator, book: PlainBook, z, cfg: ChainCfg):
     """K3 on complex-slot frames (reading R28): d = W~ z by BSGS, d in complex slots."""
+    set_merge(ev, cfg)
     return k3_giant_steps_c(ev, k3_inner_sums_c(ev, book, k3_babies(ev, z, cfg), cfg), cfg)
 
 
@@ -591,6 +615,7 @@ def k2_doppler_soft_power(ev, Pm, cfg):
 def gesture_frames(ev, book, v_re, v_im, cfg):
     """Per frame: K3 -> K1 -> K6 -> K2b -> weighting, on a list of frames.
     With complex slots (cfg.cplx) v_re holds the frames' z ciphertexts and v_im is None."""
+    set_merge(ev, cfg)
     if cplx_of(cfg):
         if v_im is not None:
             raise ValueError("complex slots: one ciphertext per frame (v_im must be None)")
@@ -664,7 +689,7 @@ def fc_layer(ev, book, x, W: np.ndarray, bias: np.ndarray, n_in: int, layer: int
         if G:
             inner = ev.rotate_pq(inner, G * L) if pq else ev.rotate(inner, G * L)
         acc = inner if acc is None else (ev.add_pq(acc, inner) if pq else ev.add(acc, inner))
-    z = ev.rescale(ev.moddown_ct(acc) if pq else acc)
+    z = ev.down_rescale(acc) if pq else ev.rescale(acc)
     y = (ev.rotsum_dh_all([z], n_in // h, h * L, rs_inner, rs_all) if pq else ev.rotsum_all([z], n_in // h, h * L))[0]
     bv = lane_vec(np.asarray(bias, dtype=np.float64), L)
     y = ev.add_plain(y, book.vec(f"fc{layer}.bias", bv, y.level, scale=y.scale))
@@ -693,6 +718,7 @@ def gesture_fc(ev, book, feat, Ws, bs, cfg):
     dims = cfg.fc_dims
     Ws, bs = pad_fc(Ws, bs, dims)
     L = lanes_of(cfg)
+    set_merge(ev, cfg)
     inner = rotsum_inner(cfg)
     if L > 1:
         x = (rotsum_dh(ev, [feat], L, 1, cfg) if dh(cfg) else ev.rotsum_all([feat], L, 1))[0]

@@ -73,6 +73,8 @@ def lib():
         _lib.or_modup.restype = None
         _lib.or_moddown.argtypes = [u32, u32, u64p, u32, u64p, u64p, u64p]
         _lib.or_moddown.restype = None
+        _lib.or_moddown_rescale.argtypes = [u32, u32, u64p, u32, u64p, u64p, u64p]
+        _lib.or_moddown_rescale.restype = None
         _lib.or_keyswitch.argtypes = [u32, u32, u32, u64p, u32, u64p, u32, u64p, u64p, u64p, u64p]
     return _lib
 
@@ -645,6 +647,53 @@ class Evaluator:
         self._rec("hadd_pq", a.level)
         basis = self.pq_basis(a.level)
         return Ct([poly_add(basis, x, y) for x, y in zip(a.c, b.c)], a.level, a.scale, a.n_slots)
+
+    def moddown_rescale_poly(self, x: np.ndarray, level: int) -> np.ndarray:
+        """ModDown and rescale as one division by P q_level (reading R31) of one polynomial over
+        Q_l u P: BConv of its p_0..p_{K-1}, q_l residues to q_0..q_{l-1}, out = (x - w) (P q_l)^{-1}."""
+        P = self.P
+        out = np.empty((level, P.n), dtype=np.uint64)
+        lib().or_moddown_rescale(P.n, level, _arr(P.q), P.K, _arr(P.p), _arr(x), out)
+        return out
+
+    def moddown_rescale_ct(self, a: Ct) -> Ct:
+        """A PQ ciphertext brought down to Q_{l-1} in one division (ModDown, then rescale, merged:
+        reading R31); scale / q_l."""
+        if a.level == 0:
+            raise DepthError("depth exhausted")
+        self._rec("moddown_rescale", a.level)
+        return Ct([self.moddown_rescale_poly(x, a.level) for x in a.c], a.level - 1, a.scale / self.P.q[a.level],
+                  a.n_slots)
+
+    def relin_rescale_merged(self, a: Ct) -> Ct:
+        """Relinearisation and rescale with one division (reading R31): the inner product of
+        ModUp(c2) with rlk left over Q_l u P, plus the P lift (P c0, P c1), then ModDown and rescale
+        as one division by P q_l."""
+        if len(a.c) != 3:
+            raise ValueError("relin needs a 3-poly ciphertext")
+        if self.rlk is None:
+            raise KeyError("missing relinearisation key")
+        if a.level == 0:
+            raise DepthError("depth exhausted")
+        self._rec("relin_rescale", a.level)
+        P = self.P
+        l = a.level
+        basis = self.pq_basis(l)
+        nkey = P.L + 1 + P.K
+        acc0 = np.zeros((l + 1 + P.K, P.n), dtype=np.uint64)
+        acc1 = np.zeros_like(acc0)
+        for j in range(-(-(l + 1) // P.alpha)):
+            y = np.empty((l + 1 + P.K, P.n), dtype=np.uint64)
+            lib().or_modup(P.n, l, _arr(P.q), P.K, _arr(P.p), P.alpha, j, _arr(a.c[2]), y)
+            kb = np.concatenate([self.rlk[j, 0, : l + 1], self.rlk[j, 0, P.L + 1: nkey]])
+            ka = np.concatenate([self.rlk[j, 1, : l + 1], self.rlk[j, 1, P.L + 1: nkey]])
+            acc0 = poly_add(basis, acc0, poly_mul(basis, y, kb))
+            acc1 = poly_add(basis, acc1, poly_mul(basis, y, ka))
+        pm = self._p_mod(basis)
+        acc0[: l + 1] = poly_add(basis[: l + 1], acc0[: l + 1], poly_scalar(basis[: l + 1], a.c[0], pm[: l + 1]))
+        acc1[: l + 1] = poly_add(basis[: l + 1], acc1[: l + 1], poly_scalar(basis[: l + 1], a.c[1], pm[: l + 1]))
+        return Ct([self.moddown_rescale_poly(acc0, l), self.moddown_rescale_poly(acc1, l)], l - 1,
+                  a.scale / P.q[l], a.n_slots)
 
     def moddown_ct(self, a: Ct) -> Ct:
         """Both polynomials of a PQ ciphertext back to Q_l (divides out P)."""

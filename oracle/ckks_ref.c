@@ -296,6 +296,37 @@ void or_moddown(uint32_t n, uint32_t l, const uint64_t *qs, uint32_t k_p, const 
     free(w);
 }
 
+/* ModDown and rescale as ONE division (reading R31): c over q_0..q_l, p_0..p_{K-1} (coefficient form,
+ * layout [l+1+K][N]: q rows then p rows) -> out over q_0..q_{l-1}:
+ *   w = BConv_{p_0..p_{K-1}, q_l -> q_i}(c)  (fast base conversion, the sources' residues),
+ *   out_i = (c_i - w_i) (P q_l)^{-1} mod q_i,  i < l.
+ * (ModDown's formula with the special modulus P q_l: q_l is converted like a special prime.) */
+void or_moddown_rescale(uint32_t n, uint32_t l, const uint64_t *qs, uint32_t k_p, const uint64_t *ps,
+                        const uint64_t *c, uint64_t *out)
+{
+    uint32_t ns = k_p + 1;
+    uint64_t *src = (uint64_t *)malloc(sizeof(uint64_t) * ns);
+    uint64_t *x = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)ns * n);
+    uint64_t *w = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(l ? l : 1) * n);
+    for (uint32_t k = 0; k < k_p; ++k) src[k] = ps[k];
+    src[k_p] = qs[l];
+    memcpy(x, c + (size_t)(l + 1) * n, sizeof(uint64_t) * (size_t)k_p * n);
+    memcpy(x + (size_t)k_p * n, c + (size_t)l * n, sizeof(uint64_t) * n);
+    bconv(n, src, ns, x, qs, l, w);
+#pragma omp parallel for
+    for (uint32_t i = 0; i < l; ++i) {
+        uint64_t qi = qs[i];
+        uint64_t m_inv = invmod(mulmod(prod_mod(ps, k_p, qi), qs[l] % qi, qi), qi);
+        for (uint32_t k = 0; k < n; ++k) {
+            size_t idx = (size_t)i * n + k;
+            out[idx] = mulmod(submod(c[idx], w[idx], qi), m_inv, qi);
+        }
+    }
+    free(src);
+    free(x);
+    free(w);
+}
+
 /* Hybrid key switching of x (coefficient form, level l) with the key
  *   evk[j] = (b_j, a_j),  j < dnum_L,  each over q_0..q_L, p_0..p_{K-1}
  * (layout [dnum_L][2][L+1+K][N]).  At level l the limbs q_{l+1..L} of the key

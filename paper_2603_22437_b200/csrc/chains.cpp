@@ -196,6 +196,14 @@ class Runner {
         return *c_.find_plain(key, level);
     }
     bool dh() const { return cfg_.hoist == 2; }
+
+    // DESIGN R31 (cfg.ks_merge, gesture / K3 / FC chains): relinearisation + rescale and a PQ ciphertext's
+    // ModDown + rescale as ONE division by P q_l (oracle CircuitEvaluator.merge_rescale)
+    DCt relin_rescale(const DCt &t3) { return cfg_.ks_merge ? ev_relin_rescale_merged(c_, t3) : ev_relin_rescale(c_, t3); }
+    DCt down_rescale(const DCt &x)
+    {
+        return cfg_.ks_merge ? ev_moddown_rescale_ct(c_, x) : ev_rescale(c_, ev_moddown_ct(c_, x));
+    }
     double qscale(uint32_t level) const { return (double)c_.primes[level]; }
 
     const std::vector<double> &scalars(const std::string &name, const std::function<std::vector<double>()> &fn)
@@ -374,8 +382,8 @@ class Runner {
             else
                 out = ev_addsub(c_, out, ev_rotate(c_, inner[gi], step), false);
         }
-        if (dh()) out = ev_moddown_ct(c_, out);  // one ModDown per output ends the giant sum
-        DCt r = ev_rescale(c_, out);
+        // one ModDown per output ends the giant sum (with the rescale as one division under R31)
+        DCt r = dh() ? down_rescale(out) : ev_rescale(c_, out);
         const uint32_t B = vre.batch;
         return {copy_ct(c_, slice(r, 0, B)), copy_ct(c_, slice(r, B, B))};
     }
@@ -423,21 +431,20 @@ class Runner {
             else
                 out = ev_addsub(c_, out, ev_rotate(c_, inner[gi], step), false);
         }
-        if (dh()) out = ev_moddown_ct(c_, out);
-        return ev_rescale(c_, out);
+        return dh() ? down_rescale(out) : ev_rescale(c_, out);
     }
 
     // ---------------------------------------------------------- gesture frame (batched)
     DCt k1_power(const DCt &dre, const DCt &dim)
     {
-        return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&dre, &dre}, {&dim, &dim}}));
+        return relin_rescale(ev_tensor_sum(c_, {{&dre, &dre}, {&dim, &dim}}));
     }
 
     // K1 on complex K3 outputs (oracle k1_power_c): |d|^2 = d Conj(d)
     DCt k1_power_c(const DCt &d)
     {
         DCt cj = ev_conjugate(c_, d);
-        return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&d, &cj}}));
+        return relin_rescale(ev_tensor_sum(c_, {{&d, &cj}}));
     }
 
     DCt k6_notch(const DCt &P)
@@ -463,9 +470,9 @@ class Runner {
     DCt k2_doppler_soft_power(const DCt &Pm)
     {
         DCt S = rotsum(Pm, Pm.n_slots / L() / cfg_.D, cfg_.D * L());
-        for (uint32_t i = 0; i < ilog2(cfg_.gamma); ++i) S = ev_square_rescale(c_, S);
+        for (uint32_t i = 0; i < ilog2(cfg_.gamma); ++i) S = relin_rescale(ev_tensor_sum(c_, {{&S, &S}}));
         DCt Pd = ev_drop_to(c_, Pm, S.level);
-        return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&Pd, &S}}));
+        return relin_rescale(ev_tensor_sum(c_, {{&Pd, &S}}));
     }
 
     DCt gesture_frame(const DCt &vre, const DCt &vim)
@@ -521,15 +528,14 @@ class Runner {
             if (g.G) inner = dh() ? ev_rotate_pq(c_, inner, step) : ev_rotate(c_, inner, step);
             acc = gi == 0 ? std::move(inner) : ev_addsub(c_, acc, inner, false);
         }
-        if (dh()) acc = ev_moddown_ct(c_, acc);
-        DCt z = ev_rescale(c_, acc);
+        DCt z = dh() ? down_rescale(acc) : ev_rescale(c_, acc);
         DCt y = rotsum(z, n_in / h, h * L());
         const DPlain &bp = plain("fc" + std::to_string(layer) + ".bias", y.level, y.scale, [&] {
             MMFHE_REQUIRE(bias != nullptr, MMFHE_E_MISSING_PLAIN, "FC bias not prepared");
             return lane_rep(*bias, L());
         });
         y = ev_add_plain(c_, y, bp);
-        if (square) y = ev_square_rescale(c_, y);
+        if (square) y = relin_rescale(ev_tensor_sum(c_, {{&y, &y}}));
         return y;
     }
 
@@ -801,6 +807,11 @@ void validate_cfg(const std::string &chain, const mmfhe_chain_cfg &cfg)
     MMFHE_REQUIRE(pow2_or_zero(cfg.rotsum_inner) && cfg.rotsum_inner <= 64, MMFHE_E_INVALID_ARG,
                   "rotsum_inner must be a power of two <= 64");
     MMFHE_REQUIRE(cfg.rotsum_hoist_all <= 1, MMFHE_E_INVALID_ARG, "rotsum_hoist_all must be 0 or 1");
+    MMFHE_REQUIRE(cfg.ks_merge <= 1, MMFHE_E_INVALID_ARG, "ks_merge must be 0 or 1");
+    if (cfg.ks_merge)
+        MMFHE_REQUIRE(chain == "gesture" || chain == "gesture_frame" || chain == "gesture_features" ||
+                          chain == "gesture_fc" || chain == "fc_forward" || chain == "k3_doppler_dft",
+                      MMFHE_E_SHAPE, "ks_merge applies to the gesture / K3 / FC chains only");
     if (cfg.cplx)
         MMFHE_REQUIRE(cplx_chain(chain, cfg) || chain == "gesture_fc" || chain == "fc_forward" ||
                           chain == "k2_doppler_soft_power" || chain == "k6_notch",

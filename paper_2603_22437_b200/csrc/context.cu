@@ -353,6 +353,39 @@ void Ctx::build_tables()
             pinv[i] = {v, host::shoup(v, qi)};
             pmod[i] = {P, host::shoup(P, qi)};
         }
+        // R31: ModDown and rescale as one division by M = P q_l (row l = the level being left)
+        std::vector<TwPair> mhinv((size_t)(L + 1) * (K + 1), TwPair{0, 0}), mminv((size_t)(L + 1) * (L + 1), TwPair{0, 0});
+        std::vector<uint64_t> mhat((size_t)(L + 1) * (K + 1) * (L + 1), 0);
+        for (uint32_t l = 1; l <= L; ++l) {
+            std::vector<uint64_t> src;
+            for (uint32_t k = 0; k < K; ++k) src.push_back(primes[L + 1 + k]);
+            src.push_back(primes[l]);
+            for (uint32_t bi = 0; bi <= K; ++bi) {
+                const uint64_t b = src[bi];
+                uint64_t prod = 1;  // (M / b) mod b
+                for (uint32_t m = 0; m <= K; ++m)
+                    if (m != bi) prod = host::mul(prod, src[m] % b, b);
+                const uint64_t v = host::inv(prod, b);
+                mhinv[(size_t)l * (K + 1) + bi] = {v, host::shoup(v, b)};
+                for (uint32_t i = 0; i < l; ++i) {
+                    const uint64_t qi = primes[i];
+                    uint64_t pr = 1;
+                    for (uint32_t m = 0; m <= K; ++m)
+                        if (m != bi) pr = host::mul(pr, src[m] % qi, qi);
+                    mhat[((size_t)l * (K + 1) + bi) * (L + 1) + i] = host::to_mont(pr, qi);
+                }
+            }
+            for (uint32_t i = 0; i < l; ++i) {
+                const uint64_t qi = primes[i];
+                uint64_t M = primes[l] % qi;
+                for (uint32_t m = 0; m < K; ++m) M = host::mul(M, primes[L + 1 + m] % qi, qi);
+                const uint64_t v = host::inv(M, qi);
+                mminv[(size_t)l * (L + 1) + i] = {v, host::shoup(v, qi)};
+            }
+        }
+        off_mr_hinv = blob.push(mhinv);
+        off_mr_hat = blob.push(mhat);
+        off_mr_minv = blob.push(mminv);
         off_pd_hat_inv = blob.push(phinv);
         off_pd_hat = blob.push(phat);
         off_pd_pinv = blob.push(pinv);

@@ -137,6 +137,10 @@ class Ctx {
     size_t off_pd_hat = 0;       // uint64[K][L+1]       [Phat_k]_{q_i} * 2^64 mod q_i
     size_t off_pd_pinv = 0;      // TwPair[L+1]          [P^{-1}]_{q_i}
     size_t off_pd_pmod = 0;      // TwPair[L+1]          [P]_{q_i} (double hoisting's P lift)
+    size_t off_mr_hinv = 0;      // TwPair[L+1][K+1]     R31 (ModDown + rescale, M = P q_l, row l): [(M/b)^{-1}]_b,
+                                 //                      b = p_0..p_{K-1}, q_l
+    size_t off_mr_hat = 0;       // uint64[L+1][K+1][L+1] [M/b]_{q_i} * 2^64 mod q_i
+    size_t off_mr_minv = 0;      // TwPair[L+1][L+1]     [M^{-1}]_{q_i}
     size_t off_rs = 0;           // TwPair[L+1][L+1]     [q_l^{-1}]_{q_i} (row l)
     size_t off_rs_h = 0;         // uint64[L+1][L+1]     floor(q_l/2) mod q_i (row l)
     size_t off_recip = 0;        // uint64[np]           floor(2^64 / prime)

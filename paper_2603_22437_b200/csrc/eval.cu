@@ -1074,6 +1074,74 @@ DCt ev_moddown_ct(Ctx &c, const DCt &a)
     return r;
 }
 
+// ------------------------------------------------------------------ merged ModDown + rescale (R31)
+// (oracle Evaluator.moddown_rescale_ct / relin_rescale_merged, ckks_ref.c or_moddown_rescale)
+namespace {
+// out (level l-1) = (a - BConv_{P u q_l -> Q_{l-1}}(a)) (P q_l)^{-1} for both polys of every item of the PQ
+// batch a: INTT of its P rows and of its q_l rows, one conversion from K + 1 sources, then the forward
+// NTT of the l converted rows whose row-pass epilogue writes (a_i - v_i) M^{-1}
+void moddown_rescale_into(Ctx &c, const DCt &a, DCt &r)
+{
+    const uint32_t l = a.level, B = a.batch;
+    const size_t N = c.n;
+    std::vector<uint32_t> pm;
+    for (uint32_t k = 0; k < c.K; ++k) pm.push_back(c.L + 1 + k);
+    DBuf zP((size_t)B * 2 * c.K * N, c.stream), zq((size_t)B * 2 * N, c.stream);
+    const InvSrc ps{a.ppoly(0), a.item_words(), N, 2 * c.K, 1};
+    ntt_inverse(c, zP.get(), B * 2 * c.K, make_map(pm), &ps);
+    const InvSrc qsrc{a.data() + (size_t)l * N, a.item_words(), a.poly_words(), 2, 1};
+    ntt_inverse(c, zq.get(), B * 2, make_map({l}), &qsrc);
+    DBuf w((size_t)B * 2 * l * N, c.stream);
+    launch_moddown_bconv(c, w.get(), zP.get(), l, B, 2, zq.get());
+    RowEpi ep{};
+    ep.out = r.data();
+    ep.X = a.data();
+    ep.mul = (const TwPair *)c.bconv_ptr(c.off_mr_minv) + (size_t)l * (c.L + 1);
+    ep.os = r.item_words();
+    ep.ops = r.poly_words();
+    ep.xs = a.item_words();
+    ep.xps = a.poly_words();
+    ep.per = l;
+    ep.g0 = 1;
+    ep.npoly = 2;
+    ntt_forward(c, w.get(), B * 2 * l, qmap(c, l - 1), nullptr, &ep);
+}
+}  // namespace
+
+DCt ev_moddown_rescale_ct(Ctx &c, const DCt &a)
+{
+    MMFHE_REQUIRE(a.pk == c.K && a.npolys == 2, MMFHE_E_LAYOUT, "ModDown needs a PQ ciphertext");
+    MMFHE_REQUIRE(a.level >= 1, MMFHE_E_DEPTH, "depth exhausted");
+    rec_n(c, "moddown_rescale", a.level, a.batch);
+    DCt r = make_ct(c, a.level - 1, 2, a.n_slots, a.scale / (double)c.primes[a.level], a.batch);
+    moddown_rescale_into(c, a, r);
+    return r;
+}
+
+DCt ev_relin_rescale_merged(Ctx &c, const DCt &a3)
+{
+    MMFHE_REQUIRE(a3.npolys == 3, MMFHE_E_LAYOUT, "relin needs a 3-poly ciphertext");
+    MMFHE_REQUIRE(c.rlk != nullptr, MMFHE_E_MISSING_KEY, "missing relinearisation key");
+    MMFHE_REQUIRE(a3.level >= 1, MMFHE_E_DEPTH, "depth exhausted");
+    const uint32_t l = a3.level, B = a3.batch;
+    rec_n(c, "relin_rescale", l, B);
+    // the inner product of ModUp(c2) with rlk left over Q_l u P, its Q rows plus the P lift of
+    // (c0, c1) (the key inner product's fused epilogue), then one division by P q_l
+    ModUpOut m = ks_modup(c, a3.poly(2), a3.item_words(), l, B);
+    DCt acc = make_pq(c, l, a3.n_slots, a3.scale, B);
+    const IPOut os{acc.item_words(), acc.poly_words(), acc.item_words(), (size_t)c.K * c.n};
+    IPEpi ep;
+    ep.add = a3.data();
+    ep.add1 = a3.poly(1);
+    ep.pmod = (const TwPair *)c.bconv_ptr(c.off_pd_pmod);
+    ep.as = a3.item_words();
+    launch_key_ip(c, acc.data(), acc.ppoly(0), a3.poly(2), a3.item_words(), m.y.get(), m.T * c.n, m.off,
+                  c.rlk->buf.get(), l, B, 1, 1, &os, &ep);
+    DCt r = make_ct(c, l - 1, 2, a3.n_slots, a3.scale / (double)c.primes[l], B);
+    moddown_rescale_into(c, acc, r);
+    return r;
+}
+
 // ------------------------------------------------------------------ stores
 void load_key(Ctx &c, DKey &k, const uint64_t *words, size_t n_words, bool on_device)
 {

@@ -87,6 +87,10 @@ DCt ev_moddown_ct(Ctx &c, const DCt &a);               // both polys back to Q_l
 
 // composites
 inline DCt ev_relin_rescale(Ctx &c, const DCt &a3) { return ev_rescale(c, ev_relin(c, a3)); }
+// DESIGN R31: relinearisation + rescale, and a PQ ciphertext's ModDown + rescale, as ONE division by
+// P q_l (records "relin_rescale" / "moddown_rescale")
+DCt ev_relin_rescale_merged(Ctx &c, const DCt &a3);
+DCt ev_moddown_rescale_ct(Ctx &c, const DCt &a);
 inline DCt ev_square_rescale(Ctx &c, const DCt &a) { return ev_relin_rescale(c, ev_tensor_sum(c, {{&a, &a}})); }
 
 uint64_t galois_element(const Ctx &c, int32_t step, int32_t *normalised);

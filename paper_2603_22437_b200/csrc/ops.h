@@ -39,6 +39,7 @@ struct IPOut {
 // when pmod is set; with accumulate, both polys += the output's previous contents.
 struct IPEpi {
     const uint64_t *add = nullptr;
+    const uint64_t *add1 = nullptr;  // poly-1 addend on the Q rows, times [P]_{q_r} (R31's relinearisation lift)
     const TwPair *pmod = nullptr;
     size_t as = 0, apbase = ~(size_t)0;
     uint32_t ag = 1;
@@ -47,8 +48,10 @@ struct IPEpi {
 void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt, size_t xs, const uint64_t *y,
                    size_t ys, const std::vector<size_t> &off, const uint64_t *key, uint32_t level, uint32_t B,
                    uint32_t gx = 1, uint32_t gy = 1, const IPOut *os = nullptr, const IPEpi *ep = nullptr);
-// w [B*npoly][l+1][N] = BConv_{P->Q}(zP [B*npoly][K][N]) (coefficient form).
-void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B, uint32_t npoly = 2);
+// w [B*npoly][l+1][N] = BConv_{P->Q}(zP [B*npoly][K][N]) (coefficient form); with zq ([B*npoly][N], the
+// q_l rows) the merged ModDown + rescale's conversion (R31): w [B*npoly][l][N] = BConv_{P u q_l -> Q_{l-1}}.
+void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B, uint32_t npoly = 2,
+                          const uint64_t *zq = nullptr);
 // A group of hoisted rotations left over Q_l u P in one launch (double hoisting's baby steps):
 // outs[s] (PQ ciphertexts, item stride os) = (P sigma_s(c0) + IP0, IP1) of the digits of x / y
 // through sigma_s, with ginv[s] the inverse Galois element of step s and keys[s] its evk.

@@ -168,6 +168,11 @@ __device__ __forceinline__ void ip_store(uint64_t *o, size_t opoly, uint64_t v0,
             v0 = add_mod(v0, e.add[b * e.as + e.apbase + (size_t)(r - level - 1) * n + kadd], q);
         }
     }
+    if (e.add1 && r <= level) {  // poly 1's P lift (R31): Q rows only (P = 0 mod p_k)
+        uint64_t s = e.add1[b * e.as + (size_t)r * n + kadd];
+        if (pm) s = shoup(s, pm->w, pm->wp, q);
+        v1 = add_mod(v1, s, q);
+    }
     if (e.accumulate) {
         v0 = add_mod(v0, o[0], q);
         v1 = add_mod(v1, o[opoly], q);
@@ -224,7 +229,7 @@ __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ acc
     uint64_t *o = isq ? accQ + (size_t)r * kt.n + k : accP + (size_t)(r - a.level - 1) * kt.n + k;
     const size_t ostride = isq ? a.oqs : a.ops;
     const size_t opoly = isq ? a.oqp : a.opp;
-    const uint32_t kadd = EPI && a.ep.add ? galois_perm(k, a.ep.ag, kt.log_n) : 0;
+    const uint32_t kadd = EPI && (a.ep.add || a.ep.add1) ? galois_perm(k, a.ep.ag, kt.log_n) : 0;
     const TwPair *pmq = (EPI && a.ep.pmod && isq) ? a.ep.pmod + r : nullptr;
     for (uint32_t b = b0; b < b1; ++b) {
         const uint64_t *xb = x + (size_t)b * a.xs, *yb = y + (size_t)b * a.ys;
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(kTB, DMAX <= 4 ? 4 : 1) k_key_ip(uint64_t *__r
     uint64_t *o = isq ? accQ + (size_t)r * kt.n + k : accP + (size_t)(r - a.level - 1) * kt.n + k;
     const size_t ostride = isq ? a.oqs : a.ops;
     const size_t opoly = isq ? a.oqp : a.opp;
-    const uint32_t kadd = EPI && a.ep.add ? galois_perm(k, a.ep.ag, kt.log_n) : 0;
+    const uint32_t kadd = EPI && (a.ep.add || a.ep.add1) ? galois_perm(k, a.ep.ag, kt.log_n) : 0;
     const TwPair *pmq = (EPI && a.ep.pmod && isq) ? a.ep.pmod + r : nullptr;
     // (a software-pipelined variant loading item b+1's digit words during item b's MACs measured
     // slower on C4: 72 registers, 3 CTAs/SM, 9.96 -> 10.44 ms/step)
@@ -527,9 +532,10 @@ __global__ void __launch_bounds__(kRTile, MMFHE_RS_MINB) k_hoisted_rotsum_pq(uin
 }
 
 struct MDArgs {
-    const TwPair *phat_inv;  // [K]
-    const uint64_t *phat;    // [K][L+1] Montgomery
+    const TwPair *phat_inv;  // [ns] [(S/s_k)^{-1}]_{s_k} of the sources
+    const uint64_t *phat;    // [ns][L+1] [S/s_k]_{q_i} Montgomery
     const TwPair *pinv;      // [L+1]
+    const uint64_t *zq;      // R31: the q_level rows [B*npoly][N] as an extra source (S = P q_l), or null
     uint32_t level, L, K;
 };
 
@@ -539,10 +545,13 @@ template <int KMAX>
 __global__ void __launch_bounds__(kTB) k_moddown_bconv(uint64_t *__restrict__ w, const uint64_t *__restrict__ zP,
                                                        KTables kt, MDArgs a)
 {
-    extern __shared__ uint64_t sh[];  // phat [K][level+1], then q_i and -q_i^{-1}
-    const uint32_t L1 = a.level + 1;
-    uint64_t *s_hat = sh, *s_q = sh + a.K * L1, *s_qi = s_q + L1;
-    for (uint32_t t = threadIdx.x; t < a.K * L1; t += blockDim.x)
+    extern __shared__ uint64_t sh[];  // phat [ns][targets], then q_i and -q_i^{-1}
+    // sources: p_0..p_{K-1} (zP), plus q_level (zq) for the merged ModDown + rescale (R31), whose
+    // targets are q_0..q_{level-1}
+    const uint32_t ns = a.K + (a.zq ? 1u : 0u);
+    const uint32_t L1 = a.zq ? a.level : a.level + 1;
+    uint64_t *s_hat = sh, *s_q = sh + ns * L1, *s_qi = s_q + L1;
+    for (uint32_t t = threadIdx.x; t < ns * L1; t += blockDim.x)
         s_hat[t] = a.phat[(size_t)(t / L1) * (a.L + 1) + t % L1];
     for (uint32_t i = threadIdx.x; i < L1; i += blockDim.x) {
         s_q[i] = kt.q[i];
@@ -554,14 +563,16 @@ __global__ void __launch_bounds__(kTB) k_moddown_bconv(uint64_t *__restrict__ w,
     uint64_t v[kBcK][KMAX];
 #pragma unroll
     for (int kk = 0; kk < KMAX; ++kk) {
-        if (kk < (int)a.K) {
-            const uint32_t pi = a.L + 1 + kk;
+        if (kk < (int)ns) {
+            const bool pk = kk < (int)a.K;
+            const uint32_t pi = pk ? a.L + 1 + kk : a.level;
             const TwPair h = a.phat_inv[kk];
             const uint64_t qp = kt.q[pi];
+            const uint64_t *row = pk ? zP + ((size_t)ip * a.K + kk) * kt.n : a.zq + (size_t)ip * kt.n;
 #pragma unroll
             for (int c = 0; c < kBcK; ++c) {
                 const uint32_t k = k0 + c * kTB;
-                v[c][kk] = k < kt.n ? shoup(zP[((size_t)ip * a.K + kk) * kt.n + k], h.w, h.wp, qp) : 0;
+                v[c][kk] = k < kt.n ? shoup(row[k], h.w, h.wp, qp) : 0;
             }
         }
     }
@@ -571,7 +582,7 @@ __global__ void __launch_bounds__(kTB) k_moddown_bconv(uint64_t *__restrict__ w,
         for (int c = 0; c < kBcK; ++c) acc[c] = U128{0, 0};
 #pragma unroll
         for (int kk = 0; kk < KMAX; ++kk)
-            if (kk < (int)a.K) {
+            if (kk < (int)ns) {
                 const uint64_t hc = s_hat[kk * L1 + i];
 #pragma unroll
                 for (int c = 0; c < kBcK; ++c) mac128(acc[c], v[c][kk], hc);
@@ -1235,33 +1246,42 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
     LAUNCH_CHECK(c);
 }
 
-static MDArgs md_args(Ctx &c, uint32_t level)
+static MDArgs md_args(Ctx &c, uint32_t level, const uint64_t *zq)
 {
     MDArgs a;
-    a.phat_inv = (const TwPair *)c.bconv_ptr(c.off_pd_hat_inv);
-    a.phat = (const uint64_t *)c.bconv_ptr(c.off_pd_hat);
+    if (zq) {  // R31: sources p_0..p_{K-1}, q_level; modulus M = P q_level
+        a.phat_inv = (const TwPair *)c.bconv_ptr(c.off_mr_hinv) + (size_t)level * (c.K + 1);
+        a.phat = (const uint64_t *)c.bconv_ptr(c.off_mr_hat) + (size_t)level * (c.K + 1) * (c.L + 1);
+    } else {
+        a.phat_inv = (const TwPair *)c.bconv_ptr(c.off_pd_hat_inv);
+        a.phat = (const uint64_t *)c.bconv_ptr(c.off_pd_hat);
+    }
     a.pinv = (const TwPair *)c.bconv_ptr(c.off_pd_pinv);
+    a.zq = zq;
     a.level = level;
     a.L = c.L;
     a.K = c.K;
     return a;
 }
 
-void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B, uint32_t npoly)
+void launch_moddown_bconv(Ctx &c, uint64_t *w, const uint64_t *zP, uint32_t level, uint32_t B, uint32_t npoly,
+                          const uint64_t *zq)
 {
-    MMFHE_REQUIRE(c.K <= 16, MMFHE_E_PARAMS, "K too large");
-    ProfScope ps(c, "moddown_bconv", 8.0 * npoly * (c.K + level + 1) * c.n * B,
-                 (double)npoly * c.K * (level + 1) * c.n * B);
-    const size_t smem = 8 * ((size_t)c.K * (level + 1) + 2 * (level + 1));
+    const uint32_t ns = c.K + (zq ? 1 : 0), nt = zq ? level : level + 1;
+    MMFHE_REQUIRE(ns <= 16, MMFHE_E_PARAMS, "K too large");
+    MMFHE_REQUIRE(!zq || level >= 1, MMFHE_E_DEPTH, "merged ModDown + rescale needs level >= 1");
+    ProfScope ps(c, "moddown_bconv", 8.0 * npoly * (ns + nt) * c.n * B, (double)npoly * ns * nt * c.n * B);
+    const size_t smem = 8 * ((size_t)ns * nt + 2 * nt);
     const dim3 g((c.n + kBcK * kTB - 1) / (kBcK * kTB), npoly * B);
-    if (c.K <= 1)
-        k_moddown_bconv<1><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, md_args(c, level));
-    else if (c.K <= 4)
-        k_moddown_bconv<4><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, md_args(c, level));
-    else if (c.K <= 8)
-        k_moddown_bconv<8><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, md_args(c, level));
+    const MDArgs a = md_args(c, level, zq);
+    if (ns <= 1)
+        k_moddown_bconv<1><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, a);
+    else if (ns <= 4)
+        k_moddown_bconv<4><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, a);
+    else if (ns <= 8)
+        k_moddown_bconv<8><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, a);
     else
-        k_moddown_bconv<16><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, md_args(c, level));
+        k_moddown_bconv<16><<<g, kTB, smem, c.stream>>>(w, zP, c.kt, a);
     LAUNCH_CHECK(c);
 }
 

@@ -31,7 +31,7 @@ def _mcfg(m, cfg: cc.ChainCfg, bins=(), taps=()):
                        n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch, hoist=cfg.hoist,
                        vp_plus=cfg.vp_plus, iq_pack=cfg.iq_pack, lanes=cfg.lanes, cplx=cfg.cplx,
                        bsgs_aligned=cfg.bsgs_aligned, rotsum_inner=cfg.rotsum_inner,
-                       rotsum_hoist_all=cfg.rotsum_hoist_all)
+                       rotsum_hoist_all=cfg.rotsum_hoist_all, ks_merge=cfg.ks_merge)
 
 
 def _run(m, P, keys, book, chain, cfg, cts, want, scalars=None, bins=(), taps=()):
@@ -283,9 +283,9 @@ def test_gesture_chain_small(m, F, fb, hoist):
     _run(m, P, keys, book, "gesture_frame", cfg, cts[:2], [f0])
 
 
-@pytest.mark.parametrize("lanes,F,fb,hoist", [(4, 6, 0, 1), (2, 5, 2, 1), (8, 8, 0, 1), (4, 6, 0, 2), (2, 5, 2, 2),
-                                              (1, 3, 2, 2)])
-def test_gesture_chain_lanes_small(m, lanes, F, fb, hoist):
+@pytest.mark.parametrize("lanes,F,fb,hoist,merge", [(4, 6, 0, 1, 0), (2, 5, 2, 1, 0), (8, 8, 0, 1, 0), (4, 6, 0, 2, 0),
+                                                    (2, 5, 2, 2, 0), (1, 3, 2, 2, 0), (2, 5, 2, 2, 1), (1, 3, 2, 2, 1)])
+def test_gesture_chain_lanes_small(m, lanes, F, fb, hoist, merge):
     """SIMD-dense gesture pipeline (DESIGN R20): `lanes` frames interleaved per ciphertext,
     ceil(F / lanes) ciphertext pairs (the last one partly empty), hoisted (hoist = 1) or
     double-hoisted (hoist = 2: PQ baby steps, PQ diagonals, PQ giant steps, one ModDown per
@@ -293,7 +293,7 @@ def test_gesture_chain_lanes_small(m, lanes, F, fb, hoist):
     oracle's; K3 alone too."""
     P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
     cfg, Zt = _gesture(P, 3221, F=F, frame_batch=fb, hoist=hoist)
-    cfg.lanes = lanes
+    cfg.lanes, cfg.ks_merge = lanes, merge  # merge: relin / ModDown + rescale as one division (R31)
     keys = orc.keygen(P, seed=3222, rotations=cc.required_rotations("gesture", cfg, P.n))
     n = cfg.n_slots
     cts = []
@@ -321,7 +321,8 @@ def test_gesture_chain_lanes_small(m, lanes, F, fb, hoist):
 @pytest.mark.parametrize("lanes,F,fb,hoist,aligned", [(1, 2, 0, 0, 0), (1, 3, 2, 1, 0), (2, 5, 2, 2, 0), (4, 6, 0, 2, 0),
                                                       (1, 2, 0, 0, 1), (2, 5, 2, 2, 1), (4, 6, 0, 2, 1),
                                                       (1, 6, 0, 2, 1), (4, 6, 0, 2, 2), (2, 5, 2, 2, 3),
-                                                      (4, 6, 0, 2, 4), (1, 3, 0, 2, 5)])
+                                                      (4, 6, 0, 2, 4), (1, 3, 0, 2, 5), (4, 6, 0, 2, 6),
+                                                      (1, 6, 0, 2, 6)])
 def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     """Complex-slot gesture pipeline (cfg.cplx, DESIGN R28): one ciphertext z = v_re + j v_im
     per frame group, K3 with complex diagonals (one plaintext product per diagonal), K1 as
@@ -335,6 +336,9 @@ def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     cfg.lanes, cfg.cplx, cfg.bsgs_aligned = lanes, 1, min(aligned, 1)
     cfg.rotsum_inner = {2: 16, 3: 4, 4: 2, 5: 4}.get(aligned, 0)
     cfg.rotsum_hoist_all = int(aligned >= 4)
+    cfg.ks_merge = int(aligned >= 6)  # 6: + relin / ModDown + rescale as one division (R31)
+    if aligned == 6:
+        cfg.rotsum_inner = 2
     rots = cc.required_rotations("gesture", cfg, P.n)
     assert rots[0] == orc.CONJ == m.STEP_CONJ
     keys = orc.keygen(P, seed=3242, rotations=rots)

@@ -625,15 +625,15 @@ def test_complex_k3_decrypts_to_dft(Pg, hoist, L, aligned):
         assert rel_err(got[f::L], want) < 1e-3
 
 
-@pytest.mark.parametrize("hoist", [1, 2])
-def test_complex_gesture_pipeline(Pg, hoist):
+@pytest.mark.parametrize("hoist,merge", [(1, 0), (2, 0), (2, 1)])
+def test_complex_gesture_pipeline(Pg, hoist, merge):
     """The gesture pipeline on complex slots (one ciphertext per frame group, 2 lanes): per
     frame P = |d|^2 by d Conj(d) (one conjugation key switch per ciphertext), features and
     logits decrypt to the plaintext DSP, argmax agrees, depth unchanged (11)."""
     P = Pg
     F, L = 4, 2
     cfg, Zt = _gesture_setup(P, F=F)
-    cfg.hoist, cfg.lanes, cfg.cplx = hoist, L, 1
+    cfg.hoist, cfg.lanes, cfg.cplx, cfg.ks_merge = hoist, L, 1, merge
     n = cfg.n_slots
     rots = cc.required_rotations("gesture", cfg, P.n)
     assert orc.CONJ in rots and rots[0] == orc.CONJ
@@ -644,6 +644,9 @@ def test_complex_gesture_pipeline(Pg, hoist):
     book = cc.PlainBook(P)
     fr = cc.gesture_frames(ev, book, z, None, cfg)
     assert [op for op, _, _ in ev.trace].count("conj") == 2
+    # R31: every relinearisation / ModDown that a rescale follows is one division
+    ops = [op for op, _, _ in ev.trace]
+    assert (ops.count("relin_rescale") > 0) == bool(merge) and (ops.count("relin") == 0) == bool(merge)
     fp = [dsp.gesture_frame_features(v, cfg.A, cfg.R, cfg.D, cfg.gamma) for v in vs]
     for g, c in enumerate(fr):
         dec = orc.decrypt_vector(P, keys, c)

@@ -259,3 +259,31 @@ def test_real_encoding_unchanged_by_complex_support(P):
     a = orc.encode(P, v, 2.0 ** 30, 1)
     b = orc.encode(P, v.astype(np.complex128), 2.0 ** 30, 1)
     assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ merged ModDown + rescale (reading R31)
+
+def test_relin_rescale_merged_and_moddown_rescale(P, keys):
+    """Reading R31: relinearisation + rescale as one division by P q_l decrypts to the product like
+    mul_rescale (scale, level, values), and the PQ lift brought down by the merged division equals
+    the rescaled ciphertext's message; the trace records the merged ops."""
+    rng = np.random.default_rng(21)
+    h = P.n // 2
+    a = rng.uniform(-1, 1, h)
+    b = rng.uniform(-1, 1, h)
+    lvl = P.L
+    ca = orc.encrypt_vector(P, keys, a, lvl, seed=7, index=0)
+    cb = orc.encrypt_vector(P, keys, b, lvl, seed=7, index=1)
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    t = ev.tensor(ca, cb)
+    m = ev.relin_rescale_merged(t)
+    r = ev.mul_rescale(ca, cb)
+    assert m.level == r.level == lvl - 1 and m.scale == r.scale
+    assert ev.trace[1] == ("relin_rescale", lvl, "")
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, m) - a * b)) < 1e-5
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, m) - orc.decrypt_vector(P, keys, r))) < 1e-6
+    rl = ev.relin(t)  # scale Delta^2: the PQ lift of it divided by P q_l is the rescaled product
+    d = ev.moddown_rescale_ct(ev.lift_pq(rl))
+    assert d.level == lvl - 1 and d.scale == rl.scale / P.q[lvl]
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, d) - a * b)) < 1e-5
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, d) - orc.decrypt_vector(P, keys, ev.rescale(rl)))) < 1e-6

@@ -181,6 +181,31 @@ def test_moddown_is_division_by_p_within_k():
         assert abs(rr * P - cc) <= (len(ps) + 1) * P
 
 
+def test_moddown_rescale_is_division_by_p_ql_within_k1():
+    # Reading R31: the merged ModDown + rescale is (c' - BConv_{P u q_l}(c')) / (P q_l); with the
+    # big-integer CRT value C of c' over Q_l u P and R of the result over Q_{l-1}:
+    # R = (C - [C]_{P q_l} - u P q_l) / (P q_l) for a fast-BConv error u in [0, K + 1), i.e.
+    # |R - C / (P q_l)| <= K + 1 -- checked against the big-integer division, not the RNS formula.
+    n = 16
+    qs, ps = _small_chain(n, 4)
+    rng = random.Random(6)
+    basis = qs + ps
+    P = ps[0] * ps[1]
+    for l in (3, 2, 1):
+        qb = qs[: l + 1] + ps
+        c = _rand_res(rng, qb, n)
+        out = np.empty((l, n), dtype=np.uint64)
+        orc.lib().or_moddown_rescale(n, l, orc._arr(qs), len(ps), orc._arr(ps), orc._arr(c), out)
+        C, QP = big.crt([c[t] for t in range(len(qb))], qb)
+        R, Q = big.crt([out[t] for t in range(l)], qs[:l])
+        M = P * qs[l]
+        for k in range(n):
+            cc = big.centered(C[k], QP)
+            rr = big.centered(R[k], Q)
+            assert abs(rr * M - cc) <= (len(ps) + 2) * M
+    del basis
+
+
 def test_keyswitch_correctness_bound():
     # Dec_s(KS(x; s')) - x*s' is small, with keys made at the
     # top level and used at lower levels with truncated digits.
