@@ -52,6 +52,7 @@ ALIGNED = 1                        # K3 giants at multiples of b: the giant G = 
 ROTSUM_INNER = 16                  # double-hoisted rotate-and-sum levels of 16 (R27)
 ROTSUM_HOIST_ALL = 1               # every level hoisted (R30): C4 46.7 -> 43.6 ms (profiles/r02/c4prof_*_r02ao.log)
 KS_MERGE = 1                       # relin / ModDown + rescale as one division by P q_l (R31): 42.5 -> 40.6 ms
+K1_CONJ_FUSE = 1                   # K1 as one conjugate-product key switch (R32): 40.4 -> 39.7 ms
 
 
 def band_bins(F_phase, fs, band):
@@ -70,7 +71,8 @@ def c4_config(lanes=LANES, level=19, F=100, cplx=CPLX):
     # products only, the giant steps full key switches: fewer giants, measured 89.3 -> 77.5 ms)
     return P, dict(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=FC_DIMS, hoist=2, lanes=lanes, level=level,
                    frame_batch=0 if lanes > 1 else 25, bsgs_baby=16, fc_baby=FC_BABY, cplx=cplx, bsgs_aligned=ALIGNED,
-                   rotsum_inner=ROTSUM_INNER, rotsum_hoist_all=ROTSUM_HOIST_ALL, ks_merge=KS_MERGE)
+                   rotsum_inner=ROTSUM_INNER, rotsum_hoist_all=ROTSUM_HOIST_ALL, ks_merge=KS_MERGE,
+                   k1_conj_fuse=K1_CONJ_FUSE if cplx else 0)
 
 
 def gesture_mcfg(m, cfg):
@@ -79,7 +81,7 @@ def gesture_mcfg(m, cfg):
                        lanes=cfg["lanes"], bsgs_baby=cfg["bsgs_baby"], fc_baby=cfg["fc_baby"],
                        cplx=cfg.get("cplx", 0), bsgs_aligned=cfg.get("bsgs_aligned", 0),
                        rotsum_inner=cfg.get("rotsum_inner", 0), rotsum_hoist_all=cfg.get("rotsum_hoist_all", 0),
-                       ks_merge=cfg.get("ks_merge", 0))
+                       ks_merge=cfg.get("ks_merge", 0), k1_conj_fuse=cfg.get("k1_conj_fuse", 0))
 
 
 def n_pairs(cfg):
@@ -104,7 +106,8 @@ def c4_bench_config(world, cfg):
             "packing": ((f"SIMD-dense: {L} frames interleaved per ciphertext (lanes = {L}, DESIGN R20), "
                          if L > 1 else "one frame per ciphertext (the paper's layout, P:741), ")
                         + (f"complex slots z = v_re + j v_im (DESIGN R28): {n_pairs(cfg)} input ciphertexts per "
-                           f"session, K1 = d Conj(d)" if cfg.get("cplx") else
+                           f"session, K1 = d Conj(d)" + (" as one conjugate-product key switch (R32)"
+                                                         if cfg.get("k1_conj_fuse") else "") if cfg.get("cplx") else
                            f"re / im in separate ciphertexts (P:733-739): {n_pairs(cfg)} ciphertext pairs per "
                            f"session")),
             "bsgs": (f"double-hoisted (hoist = 2, DESIGN R22): PQ baby steps, PQ-encoded diagonals ("
@@ -817,7 +820,8 @@ def oracle_c4_setup(lanes, cplx=CPLX):
                        fc_dims=cfg["fc_dims"], frame_batch=cfg["frame_batch"], hoist=cfg["hoist"], lanes=lanes,
                        bsgs_baby=cfg["bsgs_baby"], fc_baby=cfg["fc_baby"], cplx=cplx,
                        bsgs_aligned=cfg["bsgs_aligned"], rotsum_inner=cfg["rotsum_inner"],
-                       rotsum_hoist_all=cfg["rotsum_hoist_all"], ks_merge=cfg["ks_merge"])
+                       rotsum_hoist_all=cfg["rotsum_hoist_all"], ks_merge=cfg["ks_merge"],
+                       k1_conj_fuse=cfg["k1_conj_fuse"])
     basis = list(P.q) + list(P.p)
     seed = 77
 

@@ -163,6 +163,11 @@ typedef struct {
                               rescale follows runs as ONE division by P q_l (DESIGN R31: fast base conversion
                               from p_0..p_{K-1}, q_l, one forward NTT of the q_0..q_{l-1} rows fewer); records
                               "relin_rescale" / "moddown_rescale".  Other residues, same decryption */
+    uint32_t k1_conj_fuse; /* cplx = 1 with ks_merge = 1: K1's d Conj(d) as ONE key switch (DESIGN R32): the inner
+                              products of ModUp(d0 sigma(d1)) with the conjugation key and of ModUp(d1 sigma(d1))
+                              with the conjugate-product key (MMFHE_STEP_CONJ_PROD, listed by
+                              mmfhe_chain_required_rotations) share one division by P q_l; records
+                              "conj_mul_relin_rescale".  Same decryption */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */
@@ -194,6 +199,10 @@ mmfhe_status mmfhe_chain_required_rotations(mmfhe_ctx *ctx, const char *chain, c
  * rotation amount [0, N/2).  Its key is the key for sigma_{2N-1}(s); client keygen draws it
  * from PRNG key index 1 + N/2 (rotation k uses 1 + k). */
 #define MMFHE_STEP_CONJ ((int32_t)(-2147483647 - 1))
+/* Key id of the conjugate-product key (DESIGN R32): the key switching s * sigma_{2N-1}(s) to s, with
+ * which K1's d * Conj(d) is relinearised in one step (cfg.k1_conj_fuse); client keygen draws it from
+ * PRNG key index 2 + N/2.  Not a Galois key: the HRot primitive rejects it. */
+#define MMFHE_STEP_CONJ_PROD ((int32_t)(-2147483647))
 
 /* Evaluation keys in coefficient form, layout [dnum_L][2][L+1+K][N]
  * (b_j then a_j, limbs q_0..q_L then p_0..p_{K-1}); n_words must equal

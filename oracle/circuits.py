@@ -64,6 +64,8 @@ class ChainCfg:
     rotsum_hoist_all: int = 0   # double hoisting: 1 -> every rotate-and-sum level hoisted (groups of rotsum_inner, R30)
     ks_merge: int = 0           # gesture / K3 / FC: 1 -> every ModDown or relinearisation followed by a rescale is
                                 # ONE division by P q_l (R31)
+    k1_conj_fuse: int = 0       # complex slots + ks_merge: 1 -> K1's d Conj(d) as one conjugate-product key switch
+                                # (R32; needs the CONJ_PROD key)
     cplx: int = 0               # gesture / K3: 1 -> complex slots, z = v_re + j v_im in ONE ciphertext
                                 # per frame (group); K3 multiplies complex diagonals, K1 is z conj(z)
                                 # (reading R28)
@@ -422,6 +424,15 @@ def rotsum_levels(count: int, inner: int, all_levels: bool):
     return out
 
 
+def k1_fused(cfg) -> bool:
+    """Reading R32: K1's d Conj(d) as one conjugate-product key switch (complex slots with ks_merge)."""
+    if not getattr(cfg, "k1_conj_fuse", 0):
+        return False
+    if not (cplx_of(cfg) and getattr(cfg, "ks_merge", 0)):
+        raise ValueError("k1_conj_fuse needs complex slots (cplx) and ks_merge")
+    return True
+
+
 def set_merge(ev, cfg):
     """Reading R31 for the gesture / K3 / FC chains: the evaluator merges every relinearisation or
     ModDown that a rescale follows into one division by P q_l (cfg.ks_merge)."""
@@ -582,9 +593,12 @@ def k1_power(ev, d_re, d_im):
     return ev.relin_rescale_all([ev.tensor_sum([(a, a), (b, b)]) for a, b in zip(d_re, d_im)])
 
 
-def k1_power_c(ev, d):
+def k1_power_c(ev, d, fuse=False):
     """K1 on complex-slot K3 outputs (reading R28): P = rescale(relin(tensor(d, Conj(d)))),
-    d conj(d) = d_re^2 + d_im^2 in every slot (Eq. energy's |.|^2)."""
+    d conj(d) = d_re^2 + d_im^2 in every slot (Eq. energy's |.|^2); with fuse (R32) the
+    conjugation and the relinearisation share one division (Evaluator.conj_mul_relin_rescale)."""
+    if fuse:
+        return [ev.conj_mul_relin_rescale(x) for x in d]
     cj = [ev.conjugate(x) for x in d]
     return ev.relin_rescale_all([ev.tensor_sum([(a, b)]) for a, b in zip(d, cj)])
 
@@ -619,7 +633,7 @@ def gesture_frames(ev, book, v_re, v_im, cfg):
     if cplx_of(cfg):
         if v_im is not None:
             raise ValueError("complex slots: one ciphertext per frame (v_im must be None)")
-        P_cts = k1_power_c(ev, k3_doppler_dft_frames_c(ev, book, v_re, cfg))
+        P_cts = k1_power_c(ev, k3_doppler_dft_frames_c(ev, book, v_re, cfg), k1_fused(cfg))
     else:
         d_re, d_im = k3_doppler_dft_frames(ev, book, v_re, v_im, cfg)
         P_cts = k1_power(ev, d_re, d_im)
@@ -902,6 +916,8 @@ def required_rotations(chain: str, cfg: ChainCfg, n_ring: int):
     half = n_ring // 2
     ks = set()
     extra = {orc.CONJ} if cplx_of(cfg) and chain in ("gesture_frame", "gesture", "gesture_features") else set()
+    if extra and getattr(cfg, "k1_conj_fuse", 0):
+        extra.add(orc.CONJ_PROD)
     if chain == "k5_fir_rot":
         W = max(cfg.n_taps) if getattr(cfg, "n_taps", None) else 0
         b, giants = fir_rot_schedule(W) if W else (1, [])

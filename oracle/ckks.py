@@ -248,6 +248,9 @@ class Keys:
 # Key id of the conjugation automorphism (reading R28): outside every normalised rotation
 # amount [0, N/2); the C ABI uses the same value (MMFHE_STEP_CONJ = INT32_MIN).
 CONJ = -(1 << 31)
+# Key id of the conjugate-product key (reading R32): the key switching s * sigma_{2N-1}(s) to s, which
+# relinearises a product d * sigma_{2N-1}(d) directly (C ABI: MMFHE_STEP_CONJ_PROD = INT32_MIN + 1).
+CONJ_PROD = CONJ + 1
 
 
 def galois_element(P: ParamSet, k: int) -> int:
@@ -260,14 +263,19 @@ def galois_element(P: ParamSet, k: int) -> int:
 
 
 def key_id(P: ParamSet, k: int) -> int:
-    """Normalised Galois-key id: k mod N/2 for a rotation, CONJ for the conjugation."""
-    return CONJ if k == CONJ else k % (P.n // 2)
+    """Normalised Galois-key id: k mod N/2 for a rotation, CONJ / CONJ_PROD for the conjugation and
+    the conjugate-product key."""
+    return k if k in (CONJ, CONJ_PROD) else k % (P.n // 2)
 
 
 def key_index(P: ParamSet, kid: int) -> int:
-    """PRNG stream index of a Galois key (make_evk): 1 + k for rotation k in [1, N/2),
-    1 + N/2 for the conjugation (0 is the relinearisation key)."""
-    return 1 + P.n // 2 if kid == CONJ else 1 + kid
+    """PRNG stream index of a key (make_evk): 1 + k for rotation k in [1, N/2), 1 + N/2 for the
+    conjugation, 2 + N/2 for the conjugate-product key (0 is the relinearisation key)."""
+    if kid == CONJ:
+        return 1 + P.n // 2
+    if kid == CONJ_PROD:
+        return 2 + P.n // 2
+    return 1 + kid
 
 
 def _full_basis(P: ParamSet):
@@ -317,6 +325,10 @@ def keygen(P: ParamSet, seed: int, rotations=(), relin: bool = True) -> Keys:
     if relin:
         keys.rlk = make_evk(P, s, poly_mul(basis, s_res, s_res), seed, 0)
     for k in sorted({key_id(P, r) for r in rotations} - {0}):
+        if k == CONJ_PROD:  # s * sigma_{2N-1}(s) (reading R32)
+            sp = poly_mul(basis, s_res, automorphism(basis, s_res, 2 * P.n - 1))
+            keys.gk[k] = make_evk(P, s, sp, seed, key_index(P, k))
+            continue
         g = galois_element(P, k)
         keys.gk[k] = make_evk(P, s, automorphism(basis, s_res, g), seed, key_index(P, k))
     return keys
@@ -694,6 +706,54 @@ class Evaluator:
         acc1[: l + 1] = poly_add(basis[: l + 1], acc1[: l + 1], poly_scalar(basis[: l + 1], a.c[1], pm[: l + 1]))
         return Ct([self.moddown_rescale_poly(acc0, l), self.moddown_rescale_poly(acc1, l)], l - 1,
                   a.scale / P.q[l], a.n_slots)
+
+    def _ip_pq(self, x: np.ndarray, level: int, evk: np.ndarray):
+        """The key inner product of ModUp(x) with evk left over Q_l u P (no ModDown)."""
+        P = self.P
+        basis = self.pq_basis(level)
+        nkey = P.L + 1 + P.K
+        acc0 = np.zeros((level + 1 + P.K, P.n), dtype=np.uint64)
+        acc1 = np.zeros_like(acc0)
+        for j in range(-(-(level + 1) // P.alpha)):
+            y = np.empty((level + 1 + P.K, P.n), dtype=np.uint64)
+            lib().or_modup(P.n, level, _arr(P.q), P.K, _arr(P.p), P.alpha, j, _arr(x), y)
+            kb = np.concatenate([evk[j, 0, : level + 1], evk[j, 0, P.L + 1: nkey]])
+            ka = np.concatenate([evk[j, 1, : level + 1], evk[j, 1, P.L + 1: nkey]])
+            acc0 = poly_add(basis, acc0, poly_mul(basis, y, kb))
+            acc1 = poly_add(basis, acc1, poly_mul(basis, y, ka))
+        return acc0, acc1
+
+    def conj_mul_relin_rescale(self, a: Ct) -> Ct:
+        """d * Conj(d), relinearised and rescaled with ONE division by P q_l (reading R32): with
+        sigma = sigma_{2N-1}, the product (a0 + a1 s)(sigma a0 + sigma a1 sigma s) has the terms
+        t0 = a0 sigma(a0), t1 = a1 sigma(a0) (times s), t2 = a0 sigma(a1) (times sigma s) and
+        t3 = a1 sigma(a1) (times s sigma s); the inner products of ModUp(t2) with the conjugation key
+        and of ModUp(t3) with the conjugate-product key are summed over Q_l u P with the P lift of
+        (t0, t1), then divided by P q_l (or_moddown_rescale).  Slots: |d|^2; scale s_d^2 / q_l."""
+        if len(a.c) != 2:
+            raise ValueError("needs a 2-poly ciphertext")
+        for k in (CONJ, CONJ_PROD):
+            if k not in self.gk:
+                raise KeyError("missing conjugation key" if k == CONJ else "missing conjugate-product key")
+        if a.level == 0:
+            raise DepthError("depth exhausted")
+        self._rec("conj_mul_relin_rescale", a.level)
+        P = self.P
+        l = a.level
+        qs = self.qs(l)
+        g = 2 * P.n - 1
+        s0, s1 = automorphism(qs, a.c[0], g), automorphism(qs, a.c[1], g)
+        t0, t1 = poly_mul(qs, a.c[0], s0), poly_mul(qs, a.c[1], s0)
+        t2, t3 = poly_mul(qs, a.c[0], s1), poly_mul(qs, a.c[1], s1)
+        u0, u1 = self._ip_pq(t2, l, self.gk[CONJ])
+        v0, v1 = self._ip_pq(t3, l, self.gk[CONJ_PROD])
+        basis = self.pq_basis(l)
+        acc0, acc1 = poly_add(basis, u0, v0), poly_add(basis, u1, v1)
+        pm = self._p_mod(basis)
+        acc0[: l + 1] = poly_add(qs, acc0[: l + 1], poly_scalar(qs, t0, pm[: l + 1]))
+        acc1[: l + 1] = poly_add(qs, acc1[: l + 1], poly_scalar(qs, t1, pm[: l + 1]))
+        return Ct([self.moddown_rescale_poly(acc0, l), self.moddown_rescale_poly(acc1, l)], l - 1,
+                  a.scale * a.scale / P.q[l], a.n_slots)
 
     def moddown_ct(self, a: Ct) -> Ct:
         """Both polynomials of a PQ ciphertext back to Q_l (divides out P)."""

@@ -440,9 +440,11 @@ class Runner {
         return relin_rescale(ev_tensor_sum(c_, {{&dre, &dre}, {&dim, &dim}}));
     }
 
-    // K1 on complex K3 outputs (oracle k1_power_c): |d|^2 = d Conj(d)
+    // K1 on complex K3 outputs (oracle k1_power_c): |d|^2 = d Conj(d); with k1_conj_fuse (R32) one
+    // conjugate-product key switch sharing a single division by P q_l
     DCt k1_power_c(const DCt &d)
     {
+        if (cfg_.k1_conj_fuse) return ev_conj_mul_relin_rescale(c_, d);
         DCt cj = ev_conjugate(c_, d);
         return relin_rescale(ev_tensor_sum(c_, {{&d, &cj}}));
     }
@@ -808,6 +810,9 @@ void validate_cfg(const std::string &chain, const mmfhe_chain_cfg &cfg)
                   "rotsum_inner must be a power of two <= 64");
     MMFHE_REQUIRE(cfg.rotsum_hoist_all <= 1, MMFHE_E_INVALID_ARG, "rotsum_hoist_all must be 0 or 1");
     MMFHE_REQUIRE(cfg.ks_merge <= 1, MMFHE_E_INVALID_ARG, "ks_merge must be 0 or 1");
+    MMFHE_REQUIRE(cfg.k1_conj_fuse <= 1, MMFHE_E_INVALID_ARG, "k1_conj_fuse must be 0 or 1");
+    MMFHE_REQUIRE(!cfg.k1_conj_fuse || (cfg.cplx && cfg.ks_merge), MMFHE_E_INVALID_ARG,
+                  "k1_conj_fuse needs cplx and ks_merge");
     if (cfg.ks_merge)
         MMFHE_REQUIRE(chain == "gesture" || chain == "gesture_frame" || chain == "gesture_features" ||
                           chain == "gesture_fc" || chain == "fc_forward" || chain == "k3_doppler_dft",
@@ -897,6 +902,7 @@ std::vector<int32_t> chain_rotations(const Ctx &c, const std::string &chain, con
     };
     if (frames || chain == "k2_doppler_soft_power") add_rotsum(cfg.n_slots / cfg.D, cfg.D * (uint32_t)L);
     if (frames && cfg.cplx) ks.insert(MMFHE_STEP_CONJ);  // K1 = d Conj(d) (DESIGN R28)
+    if (frames && cfg.cplx && cfg.k1_conj_fuse) ks.insert(MMFHE_STEP_CONJ_PROD);  // R32
     if (chain == "gesture_fc" || chain == "gesture" || chain == "fc_forward") {
         add_rotsum((uint32_t)L, 1);
         for (int layer = 0; layer < 3; ++layer) {

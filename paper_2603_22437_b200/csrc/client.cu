@@ -264,6 +264,17 @@ mmfhe_status mmfhe_client_keygen(mmfhe_ctx *ctx, uint64_t seed, const int32_t *s
         int32_t k;
         const uint32_t g = (uint32_t)galois_element(c, steps[i], &k);
         MMFHE_REQUIRE(k != 0, MMFHE_E_INVALID_ARG, "Galois key for the identity rotation");
+        if (k == MMFHE_STEP_CONJ_PROD) {  // s * sigma_{2N-1}(s) (DESIGN R32), PRNG key index 2 + N/2
+            DBuf tmp((size_t)R * c.n, c.stream);
+            const InvSrc src{s.get(), (size_t)R * c.n, c.n, R, (uint32_t)(2 * c.n - 1)};
+            ntt_inverse(c, tmp.get(), R, make_map(fb), &src);
+            ntt_forward(c, tmp.get(), R, make_map(fb));
+            DBuf sp2((size_t)R * c.n, c.stream);
+            mulmod(c, sp2.get(), 0, s.get(), 0, tmp.get(), 0, nullptr, 0, fb, 1, false);
+            make_evk(c, key.get(), s.get(), sp2.get(), seed, 2 + (uint64_t)c.n / 2);
+            copy_out(c, gk + i * kw, key.get(), kw, on_device);
+            continue;
+        }
         // sigma_g(s) in the NTT domain: the permutation of the inverse NTT's read (InvSrc) and back
         DBuf tmp((size_t)R * c.n, c.stream);
         const InvSrc src{s.get(), (size_t)R * c.n, c.n, R, g};

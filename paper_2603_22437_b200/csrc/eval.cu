@@ -765,6 +765,10 @@ uint64_t galois_element(const Ctx &c, int32_t step, int32_t *normalised)
         if (normalised) *normalised = MMFHE_STEP_CONJ;
         return 2ull * c.n - 1;
     }
+    if (step == MMFHE_STEP_CONJ_PROD) {  // the conjugate-product key (R32): an id, no Galois element
+        if (normalised) *normalised = MMFHE_STEP_CONJ_PROD;
+        return 0;
+    }
     const int64_t half = c.n / 2;
     int64_t k = ((int64_t)step % half + half) % half;
     if (normalised) *normalised = (int32_t)k;
@@ -775,8 +779,9 @@ const DKey &find_gk(const Ctx &c, int32_t k)
 {
     auto it = c.gk.find(k);
     MMFHE_REQUIRE(it != c.gk.end(), MMFHE_E_MISSING_KEY,
-                  k == MMFHE_STEP_CONJ ? std::string("missing conjugation key")
-                                       : "missing Galois key for rotation " + std::to_string(k));
+                  k == MMFHE_STEP_CONJ        ? std::string("missing conjugation key")
+                  : k == MMFHE_STEP_CONJ_PROD ? std::string("missing conjugate-product key")
+                                              : "missing Galois key for rotation " + std::to_string(k));
     return *it->second;
 }
 
@@ -798,6 +803,7 @@ DCt automorphism_ks(Ctx &c, const DCt &a, uint64_t g, const DKey &key)
 DCt ev_rotate(Ctx &c, const DCt &a, int32_t step)
 {
     MMFHE_REQUIRE(a.npolys == 2, MMFHE_E_LAYOUT, "rotate needs a 2-poly ciphertext");
+    MMFHE_REQUIRE(step != MMFHE_STEP_CONJ_PROD, MMFHE_E_INVALID_ARG, "the conjugate-product key is not a rotation");
     int32_t k;
     const uint64_t g = galois_element(c, step, &k);
     if (k == 0) return copy_ct(c, a);
@@ -1107,6 +1113,38 @@ void moddown_rescale_into(Ctx &c, const DCt &a, DCt &r)
     ntt_forward(c, w.get(), B * 2 * l, qmap(c, l - 1), nullptr, &ep);
 }
 }  // namespace
+
+DCt ev_conj_mul_relin_rescale(Ctx &c, const DCt &d)
+{
+    MMFHE_REQUIRE(d.npolys == 2 && !d.pk, MMFHE_E_LAYOUT, "needs a 2-poly Q ciphertext");
+    MMFHE_REQUIRE(d.level >= 1, MMFHE_E_DEPTH, "depth exhausted");
+    const DKey &kc = find_gk(c, MMFHE_STEP_CONJ), &kp = find_gk(c, MMFHE_STEP_CONJ_PROD);
+    const uint32_t l = d.level, B = d.batch;
+    rec_n(c, "conj_mul_relin_rescale", l, B);
+    // t0 = d0 s(d0), t1 = d1 s(d0) as a 2-poly batch; t2 = d0 s(d1) for every item, then t3 = d1 s(d1)
+    // for every item, as one 2B batch of single polynomials (s = sigma_{2N-1}, a gather in the NTT domain)
+    DCt t01 = make_ct(c, l, 2, d.n_slots, d.scale * d.scale, B);
+    DCt t23 = make_ct(c, l, 1, d.n_slots, d.scale * d.scale, 2 * B);
+    launch_conj_tensor(c, t01.data(), t01.item_words(), t23.data(), t23.item(B), t23.item_words(), d.data(),
+                       d.item_words(), l, B, (uint32_t)(2 * c.n - 1));
+    ModUpOut m = ks_modup(c, t23.data(), t23.item_words(), l, 2 * B);
+    DCt acc = make_pq(c, l, d.n_slots, d.scale * d.scale, B);
+    const IPOut os{acc.item_words(), acc.poly_words(), acc.item_words(), (size_t)c.K * c.n};
+    IPEpi ep;  // first inner product: + the P lift of (t0, t1)
+    ep.add = t01.data();
+    ep.add1 = t01.poly(1);
+    ep.pmod = (const TwPair *)c.bconv_ptr(c.off_pd_pmod);
+    ep.as = t01.item_words();
+    launch_key_ip(c, acc.data(), acc.ppoly(0), t23.data(), t23.item_words(), m.y.get(), m.T * c.n, m.off,
+                  kc.buf.get(), l, B, 1, 1, &os, &ep);
+    IPEpi ea;  // second: accumulated
+    ea.accumulate = 1;
+    launch_key_ip(c, acc.data(), acc.ppoly(0), t23.item(B), t23.item_words(), m.y.get() + (size_t)B * m.T * c.n,
+                  m.T * c.n, m.off, kp.buf.get(), l, B, 1, 1, &os, &ea);
+    DCt r = make_ct(c, l - 1, 2, d.n_slots, d.scale * d.scale / (double)c.primes[l], B);
+    moddown_rescale_into(c, acc, r);
+    return r;
+}
 
 DCt ev_moddown_rescale_ct(Ctx &c, const DCt &a)
 {

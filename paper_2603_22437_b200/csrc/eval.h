@@ -91,6 +91,9 @@ inline DCt ev_relin_rescale(Ctx &c, const DCt &a3) { return ev_rescale(c, ev_rel
 // P q_l (records "relin_rescale" / "moddown_rescale")
 DCt ev_relin_rescale_merged(Ctx &c, const DCt &a3);
 DCt ev_moddown_rescale_ct(Ctx &c, const DCt &a);
+// DESIGN R32: d * Conj(d) relinearised with the conjugation and conjugate-product keys and rescaled by
+// one division by P q_l (records "conj_mul_relin_rescale")
+DCt ev_conj_mul_relin_rescale(Ctx &c, const DCt &d);
 inline DCt ev_square_rescale(Ctx &c, const DCt &a) { return ev_relin_rescale(c, ev_tensor_sum(c, {{&a, &a}})); }
 
 uint64_t galois_element(const Ctx &c, int32_t step, int32_t *normalised);

@@ -65,6 +65,10 @@ void launch_hoisted_rotsum_pq(Ctx &c, uint64_t *out, size_t os, const uint64_t *
                               size_t ys, const std::vector<size_t> &off, const uint64_t *c0, size_t cs,
                               const std::vector<const uint64_t *> &keys, const std::vector<uint32_t> &g,
                               uint32_t level, uint32_t B);
+// DESIGN R32: t01 (2-poly batch, item stride t01s) = (d0 s(d0), d1 s(d0)); t2 / t3 (single polys, item
+// stride t23s) = d0 s(d1) / d1 s(d1); s = sigma_g, a gather in the NTT domain
+void launch_conj_tensor(Ctx &c, uint64_t *t01, size_t t01s, uint64_t *t2, uint64_t *t3, size_t t23s,
+                        const uint64_t *d, size_t ds, uint32_t level, uint32_t B, uint32_t g);
 // double hoisting: Q rows of out (+)= [P]_{q_i} sigma_g(src) for npoly polys per
 // item (out / src item strides os / ss, poly strides ops / sps): the identity baby step's P lift
 // (the other PQ addends are the key inner product's fused epilogue, IPEpi)

@@ -646,6 +646,30 @@ __global__ void __launch_bounds__(kTB) k_tensor1(uint64_t *__restrict__ out_base
 
 // ------------------------------------------------------------------ fused sums
 // d0 = sum a0 b0, d1 = sum a0 b1 + a1 b0, d2 = sum a1 b1 over n pairs; grid.z = item.
+// DESIGN R32: the terms of d (x) s(d), s = sigma_g a permutation of the NTT domain (g = 2N - 1: the
+// conjugation): t0 = d0 s(d0), t1 = d1 s(d0) into the 2-poly batch t01, t2 = d0 s(d1) into t2 and
+// t3 = d1 s(d1) into t3 (single polys); grid (n / kTB, level + 1, B)
+__global__ void __launch_bounds__(kTB) k_conj_tensor(uint64_t *__restrict__ t01, size_t t01s, uint64_t *__restrict__ t2,
+                                                     uint64_t *__restrict__ t3, size_t t23s,
+                                                     const uint64_t *__restrict__ d, size_t ds, KTables kt,
+                                                     uint32_t level, uint32_t g)
+{
+    const uint32_t r = blockIdx.y, b = blockIdx.z;
+    const uint32_t j = blockIdx.x * kTB + threadIdx.x;
+    if (j >= kt.n) return;
+    const uint64_t q = kt.q[r], qi = kt.qinv_neg[r], r2 = kt.r2[r];
+    const size_t ps = (size_t)(level + 1) * kt.n;
+    const uint64_t *d0 = d + (size_t)b * ds + (size_t)r * kt.n, *d1 = d0 + ps;
+    const uint32_t pj = galois_perm(j, g, kt.log_n);
+    const uint64_t x0 = mont_mul(d0[j], r2, q, qi), x1 = mont_mul(d1[j], r2, q, qi);
+    const uint64_t s0 = d0[pj], s1 = d1[pj];
+    const size_t o = (size_t)r * kt.n + j;
+    t01[(size_t)b * t01s + o] = redc(mul128(x0, s0), q, qi);
+    t01[(size_t)b * t01s + ps + o] = redc(mul128(x1, s0), q, qi);
+    t2[(size_t)b * t23s + o] = redc(mul128(x0, s1), q, qi);
+    t3[(size_t)b * t23s + o] = redc(mul128(x1, s1), q, qi);
+}
+
 __global__ void __launch_bounds__(kTB) k_tensor_sum(uint64_t *__restrict__ out_base, size_t os, PtrList A, PtrList B,
                                                     size_t is, int n, KTables kt, uint32_t level, int accumulate)
 {
@@ -1576,6 +1600,14 @@ void launch_hoisted_rotsum_pq(Ctx &c, uint64_t *out, size_t os, const uint64_t *
         k_hoisted_rotsum_pq<4><<<grid, kRTile, 0, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
     else
         k_hoisted_rotsum_pq<8><<<grid, kRTile, 0, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
+    LAUNCH_CHECK(c);
+}
+
+void launch_conj_tensor(Ctx &c, uint64_t *t01, size_t t01s, uint64_t *t2, uint64_t *t3, size_t t23s,
+                        const uint64_t *d, size_t ds, uint32_t level, uint32_t B, uint32_t g)
+{
+    ProfScope ps(c, "tensor_sum", 8.0 * (level + 1) * c.n * B * (2.0 + 4.0), 4.0 * (level + 1) * c.n * B);
+    k_conj_tensor<<<grid3(c.n, level + 1, B), kTB, 0, c.stream>>>(t01, t01s, t2, t3, t23s, d, ds, c.kt, level, g);
     LAUNCH_CHECK(c);
 }
 

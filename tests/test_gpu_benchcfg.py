@@ -139,7 +139,7 @@ def _c4_case(lanes, F, seed, hoist=1, bsgs=0, fc_baby=0, cplx=0, aligned=0, inne
     cfg = cc.ChainCfg(A=A, R=R, D=D, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25,
                       hoist=hoist, lanes=lanes, bsgs_baby=bsgs, fc_baby=fc_baby, cplx=cplx, bsgs_aligned=aligned,
                       rotsum_inner=inner, rotsum_hoist_all=int(inner > 0 and cplx > 0),
-                      ks_merge=int(inner > 0 and cplx > 0))
+                      ks_merge=int(inner > 0 and cplx > 0), k1_conj_fuse=int(inner > 0 and cplx > 0))
     Z, _ = radar.gesture_scene(A, R, D, F, seed=seed, cls=seed % 5)
     Zt = radar.preprocess_gesture(Z)
     keys = orc.keygen(P, seed=seed + 1, rotations=cc.required_rotations("gesture", cfg, P.n))
@@ -181,7 +181,7 @@ def test_c4_bench_params_residue_parity(m, lanes, F, hoist, bsgs, fc_baby, cplx,
     mcfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64, 32, 8), frame_batch=25,
                        hoist=hoist, lanes=lanes, bsgs_baby=bsgs, fc_baby=fc_baby, cplx=cplx, bsgs_aligned=aligned,
                       rotsum_inner=inner, rotsum_hoist_all=int(inner > 0 and cplx > 0),
-                      ks_merge=int(inner > 0 and cplx > 0))
+                      ks_merge=int(inner > 0 and cplx > 0), k1_conj_fuse=int(inner > 0 and cplx > 0))
     assert sorted(ctx.required_rotations("gesture", mcfg)) == cc.required_rotations("gesture", cfg, P.n)
     levels = ctx.chain_plan("gesture", mcfg, 19, len(cts))
     assert levels == [logits.level] == [19 - 11]

@@ -31,7 +31,8 @@ def _mcfg(m, cfg: cc.ChainCfg, bins=(), taps=()):
                        n_taps=[len(t) for t in taps], fs=cfg.fs, frame_batch=cfg.frame_batch, hoist=cfg.hoist,
                        vp_plus=cfg.vp_plus, iq_pack=cfg.iq_pack, lanes=cfg.lanes, cplx=cfg.cplx,
                        bsgs_aligned=cfg.bsgs_aligned, rotsum_inner=cfg.rotsum_inner,
-                       rotsum_hoist_all=cfg.rotsum_hoist_all, ks_merge=cfg.ks_merge)
+                       rotsum_hoist_all=cfg.rotsum_hoist_all, ks_merge=cfg.ks_merge,
+                       k1_conj_fuse=cfg.k1_conj_fuse)
 
 
 def _run(m, P, keys, book, chain, cfg, cts, want, scalars=None, bins=(), taps=()):
@@ -322,7 +323,7 @@ def test_gesture_chain_lanes_small(m, lanes, F, fb, hoist, merge):
                                                       (1, 2, 0, 0, 1), (2, 5, 2, 2, 1), (4, 6, 0, 2, 1),
                                                       (1, 6, 0, 2, 1), (4, 6, 0, 2, 2), (2, 5, 2, 2, 3),
                                                       (4, 6, 0, 2, 4), (1, 3, 0, 2, 5), (4, 6, 0, 2, 6),
-                                                      (1, 6, 0, 2, 6)])
+                                                      (1, 6, 0, 2, 6), (4, 6, 0, 2, 7), (1, 3, 0, 2, 7)])
 def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     """Complex-slot gesture pipeline (cfg.cplx, DESIGN R28): one ciphertext z = v_re + j v_im
     per frame group, K3 with complex diagonals (one plaintext product per diagonal), K1 as
@@ -337,10 +338,12 @@ def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     cfg.rotsum_inner = {2: 16, 3: 4, 4: 2, 5: 4}.get(aligned, 0)
     cfg.rotsum_hoist_all = int(aligned >= 4)
     cfg.ks_merge = int(aligned >= 6)  # 6: + relin / ModDown + rescale as one division (R31)
+    cfg.k1_conj_fuse = int(aligned >= 7)  # 7: + K1 as one conjugate-product key switch (R32)
     if aligned == 6:
         cfg.rotsum_inner = 2
     rots = cc.required_rotations("gesture", cfg, P.n)
     assert rots[0] == orc.CONJ == m.STEP_CONJ
+    assert (orc.CONJ_PROD in rots) == bool(cfg.k1_conj_fuse) and orc.CONJ_PROD == m.STEP_CONJ_PROD
     keys = orc.keygen(P, seed=3242, rotations=rots)
     n = cfg.n_slots
     vs = [radar.pack_doppler(Zt[t]) for t in range(F)]
@@ -354,7 +357,7 @@ def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     logits = cc.gesture_fc(ev, book, feat, Ws, bs, cfg)
     ctx = _run(m, P, keys, book, "gesture", cfg, cts, [logits])
     assert ctx.trace() == ev.trace
-    assert ("conj", P.L - 1, "") in ev.trace
+    assert (("conj_mul_relin_rescale" if cfg.k1_conj_fuse else "conj"), P.L - 1, "") in ev.trace
     assert sorted(ctx.required_rotations("gesture", _mcfg(m, cfg))) == rots
     ev2 = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
     book2 = cc.PlainBook(P)

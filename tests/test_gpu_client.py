@@ -22,14 +22,15 @@ def m(cuda_ctx_ok):
 @pytest.mark.parametrize("alpha,n_p", [(2, 2), (1, 1)])
 def test_client_keygen_matches_oracle(m, alpha, n_p):
     P = toy(log_n=10, n_q=5, scale_bits=40, n_p=n_p, alpha=alpha)
-    steps = [1, 3, P.n // 2 - 5]
+    # rotations, the conjugation (R28) and the conjugate-product key (R32)
+    steps = [1, 3, P.n // 2 - 5, orc.CONJ, orc.CONJ_PROD]
     keys = orc.keygen(P, seed=8201, rotations=steps)
     ctx = m.Context.from_params(P)
     pk, rlk, gk = ctx.client_keygen(8201, steps)
     assert np.array_equal(pk, np.stack(keys.pk))
     assert np.array_equal(rlk, keys.rlk)
     for i, k in enumerate(steps):
-        assert np.array_equal(gk[i], keys.gk[k % (P.n // 2)]), k
+        assert np.array_equal(gk[i], keys.gk[orc.key_id(P, k)]), k
 
 
 def test_client_encrypt_matches_oracle_and_decrypts(m):

@@ -625,7 +625,7 @@ def test_complex_k3_decrypts_to_dft(Pg, hoist, L, aligned):
         assert rel_err(got[f::L], want) < 1e-3
 
 
-@pytest.mark.parametrize("hoist,merge", [(1, 0), (2, 0), (2, 1)])
+@pytest.mark.parametrize("hoist,merge", [(1, 0), (2, 0), (2, 1), (2, 2)])
 def test_complex_gesture_pipeline(Pg, hoist, merge):
     """The gesture pipeline on complex slots (one ciphertext per frame group, 2 lanes): per
     frame P = |d|^2 by d Conj(d) (one conjugation key switch per ciphertext), features and
@@ -633,9 +633,11 @@ def test_complex_gesture_pipeline(Pg, hoist, merge):
     P = Pg
     F, L = 4, 2
     cfg, Zt = _gesture_setup(P, F=F)
-    cfg.hoist, cfg.lanes, cfg.cplx, cfg.ks_merge = hoist, L, 1, merge
+    cfg.hoist, cfg.lanes, cfg.cplx, cfg.ks_merge = hoist, L, 1, min(merge, 1)
+    cfg.k1_conj_fuse = int(merge == 2)  # merge 2: + K1 as one conjugate-product key switch (R32)
     n = cfg.n_slots
     rots = cc.required_rotations("gesture", cfg, P.n)
+    assert (orc.CONJ_PROD in rots) == (merge == 2)
     assert orc.CONJ in rots and rots[0] == orc.CONJ
     keys = orc.keygen(P, seed=2302, rotations=rots)
     vs = [radar.pack_doppler(Zt[t]) for t in range(F)]
@@ -643,7 +645,8 @@ def test_complex_gesture_pipeline(Pg, hoist, merge):
     ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
     book = cc.PlainBook(P)
     fr = cc.gesture_frames(ev, book, z, None, cfg)
-    assert [op for op, _, _ in ev.trace].count("conj") == 2
+    assert [op for op, _, _ in ev.trace].count("conj") == (0 if merge == 2 else 2)
+    assert [op for op, _, _ in ev.trace].count("conj_mul_relin_rescale") == (2 if merge == 2 else 0)
     # R31: every relinearisation / ModDown that a rescale follows is one division
     ops = [op for op, _, _ in ev.trace]
     assert (ops.count("relin_rescale") > 0) == bool(merge) and (ops.count("relin") == 0) == bool(merge)

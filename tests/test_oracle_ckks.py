@@ -287,3 +287,26 @@ def test_relin_rescale_merged_and_moddown_rescale(P, keys):
     assert d.level == lvl - 1 and d.scale == rl.scale / P.q[lvl]
     assert np.max(np.abs(orc.decrypt_vector(P, keys, d) - a * b)) < 1e-5
     assert np.max(np.abs(orc.decrypt_vector(P, keys, d) - orc.decrypt_vector(P, keys, ev.rescale(rl)))) < 1e-6
+
+
+def test_conj_mul_relin_rescale(P):
+    """Reading R32: d Conj(d) with the conjugation and conjugate-product keys and one division by
+    P q_l decrypts to |d|^2 (complex slots), equals the two-key-switch path to the noise level, and
+    the key set / trace are as stated."""
+    keys = orc.keygen(P, seed=654, rotations=[orc.CONJ, orc.CONJ_PROD])
+    assert orc.CONJ in keys.gk and orc.CONJ_PROD in keys.gk
+    rng = np.random.default_rng(31)
+    h = P.n // 2
+    z = rng.uniform(-1, 1, h) + 1j * rng.uniform(-1, 1, h)
+    lvl = P.L
+    cz = orc.encrypt_vector(P, keys, z, lvl, seed=9, index=0)
+    ev = orc.Evaluator(P, keys.rlk, keys.gk)
+    f = ev.conj_mul_relin_rescale(cz)
+    assert ev.trace == [("conj_mul_relin_rescale", lvl, "")]
+    assert f.level == lvl - 1 and f.scale == cz.scale * cz.scale / P.q[lvl]
+    got = orc.decrypt_vector(P, keys, f, complex_out=True)
+    assert np.max(np.abs(got.real - np.abs(z) ** 2)) < 1e-5 and np.max(np.abs(got.imag)) < 1e-5
+    two = ev.relin_rescale_merged(ev.tensor(cz, ev.conjugate(cz)))
+    assert np.max(np.abs(orc.decrypt_vector(P, keys, two) - got.real)) < 1e-5
+    with pytest.raises(KeyError):
+        orc.Evaluator(P, keys.rlk, {orc.CONJ: keys.gk[orc.CONJ]}).conj_mul_relin_rescale(cz)

@@ -28,6 +28,7 @@ ap.add_argument("--aligned", type=int, default=0, help="K3 giants at multiples o
 ap.add_argument("--inner", type=int, default=0, help="double-hoisted rotate-and-sum first level (R27; 0 = 8)")
 ap.add_argument("--hoist-all", type=int, default=0, help="every rotate-and-sum level hoisted (R30)")
 ap.add_argument("--merge", type=int, default=0, help="relin / ModDown + rescale as one division (R31)")
+ap.add_argument("--fuse", type=int, default=0, help="K1 as one conjugate-product key switch (R32)")
 ap.add_argument("--chains", default="", help="comma-separated extra chains to profile on the session's inputs "
                                              "(k3_doppler_dft, gesture_frame)")
 ap.add_argument("--split", action="store_true", help="also profile gesture_features and gesture_fc on their own")
@@ -41,7 +42,7 @@ cfg = m.chain_cfg(A=4, R=32, D=32, F=F, gamma=4, n_slots=4096, fc_dims=(4096, 64
                   frame_batch=25 if args.lanes == 1 else 0, hoist=args.hoist, lanes=args.lanes, bsgs_baby=args.bsgs,
                   fc_baby=args.fc_baby, cplx=args.cplx, bsgs_aligned=args.aligned,
                   rotsum_inner=args.inner, rotsum_hoist_all=args.hoist_all,
-                  ks_merge=args.merge)
+                  ks_merge=args.merge, k1_conj_fuse=args.fuse)
 ctx = m.Context.from_params(P, device=0, stream=stream.cuda_stream)
 gen = torch.Generator(device=dev)
 gen.manual_seed(77)
