@@ -1081,7 +1081,7 @@ DCt ev_moddown_ct(Ctx &c, const DCt &a)
 }
 
 // ------------------------------------------------------------------ merged ModDown + rescale (R31)
-// (oracle Evaluator.moddown_rescale_ct / relin_rescale_merged, ckks_ref.c or_moddown_rescale)
+// (the same ops as the oracle's Evaluator.moddown_rescale_ct / relin_rescale_merged)
 namespace {
 // out (level l-1) = (a - BConv_{P u q_l -> Q_{l-1}}(a)) (P q_l)^{-1} for both polys of every item of the PQ
 // batch a: INTT of its P rows and of its q_l rows, one conversion from K + 1 sources, then the forward
