@@ -342,7 +342,7 @@ def run_gpu(args, rank, world, device):
             extras["client"] = extras_client(m, torch, device)
         except Exception as e:  # report, do not hide
             extras["client"] = {"error": f"{type(e).__name__}: {e}"}
-        for wl in ("C4_split", "C4_canonical", "C4_l11", "C2", "C1", "C3", "C5v", "C5v_t3", "Vpaper"):
+        for wl in ("C4_split", "C4_canonical", "C4_l11", "C2", "C2_packed", "C1", "C3", "C5v", "C5v_t3", "Vpaper"):
             try:
                 extras[wl] = bench_workload(wl, m, torch, device)
             except Exception as e:  # report, do not hide
@@ -378,15 +378,19 @@ def bench_workload(name, m, torch, device, steps=3, warmup=2):
         cfg = m.chain_cfg(R=64, F=32, n_slots=P.n // 2)
         plan = [("k1_energy", 1, 2 * 32 * 256)]
         frames, info = 32 * 256, "256 sessions x F=32"
-    elif name == "C2":
+    elif name in ("C2", "C2_packed"):
         P = ps2()
         F, fs = 256, 20.0
-        cfg = m.chain_cfg(R=128, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2,
+        packed = name == "C2_packed"  # 8 sessions per ciphertext in blocks of R 2^iq_pack = 1024 slots (R33)
+        cfg = m.chain_cfg(R=128, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=(128 << 3) if packed else P.n // 2,
                           bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
                           iq_pack=3, hoist=1)
         plan = [("vitals_v1", 3, 2 * F), ("vitals_v2", 7, 2 * F)]
         taps = [radar.fir_taps(41, b, fs) for b in BANDS]
-        frames, info = F, "R=128, F=256 frames, iq_pack 3 + hoisted unpack, V2 through |X|^2"
+        spc = (P.n // 2) // (128 << 3) if packed else 1
+        frames = F * spc
+        info = ("R=128, F=256 frames, iq_pack 3 + hoisted unpack, V2 through |X|^2"
+                + (f", {spc} sessions packed per ciphertext (DESIGN R33)" if packed else ""))
     elif name == "C3":
         P = ps3()
         lanes = 4
@@ -470,12 +474,16 @@ def bench_workload(name, m, torch, device, steps=3, warmup=2):
     return res
 
 
+VITAL_PERIOD = 64 << 3  # R 2^iq_pack: the slot block of one packed vital session (DESIGN R33)
+
+
 def c5_vital_cfg(m):
     """C5's vital session (the paper's config): R=64, F=200 @ 20 Hz at PS4,
-    vitals_v1 (entry 3) + vitals_v2 first order with VP+ in the cloud (entry 9, depth 9)."""
+    vitals_v1 (entry 3) + vitals_v2 first order with VP+ in the cloud (entry 9, depth 9); sessions
+    packed (N/2) / (R 2^iq_pack) = 64 per ciphertext (cfg.n_slots = the block, DESIGN R33)."""
     F, fs = 200, 20.0
     from synth import radar
-    cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=1 << 15,
+    cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=VITAL_PERIOD,
                       bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
                       frame_batch=40, vp_plus=1, iq_pack=3, hoist=1)
     return cfg, F, [radar.fir_taps(41, b, fs) for b in BANDS]
@@ -534,6 +542,8 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
              m.CtArray([m.Ct(torch.empty((2, lv + 1, P.n), dtype=torch.int64, device=device), lv, 0.0, 0, P.log_n)
                         for lv in lv2]))
     my_vital = list(range(*mdist.shard(Gv, rank, world)))
+    sp = (P.n // 2) // VITAL_PERIOD  # vital sessions per ciphertext (R33)
+    n_vgroups = -(-len(my_vital) // sp)
     # gesture pool: this rank's pair shard of a session
     npair = n_pairs(gcfg)
     plo, phi = mdist.shard(npair, rank, world)
@@ -568,7 +578,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
     scale_f = [probe.scale]
 
     def step_dev():
-        for i, s in enumerate(my_vital):
+        for i in range(n_vgroups):  # one packed group of up to sp sessions per chain call
             _, _, a1, a2 = vpool[i % pool]
             ctx.eval_chain("vitals_v1", vcfg, a1, vouts[0])
             ctx.eval_chain("vitals_v2", vcfg, a2, vouts[1])
@@ -613,7 +623,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
             ctx.eval_chain_async("gesture_features", gm, hga, m.CtArray([o]))
 
     def step_h2d():
-        for s in my_vital:
+        for _ in range(n_vgroups):
             ctx.eval_chain_async("vitals_v1", vcfg, hv1a, vouts[0])
             ctx.eval_chain_async("vitals_v2", vcfg, hv2a, vouts[1])
         if hga is not None:
@@ -624,7 +634,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
             total = mdist.reduce_partials(ctx, m, gathered, s, lvf, scale_f[0], gcfg["n_slots"] * LANES, P.log_n,
                                           buf=sum_bufs[s])
             ctx.eval_chain("gesture_fc", gm, [total], [fc_outs[s]])
-        h2d[0] = len(my_vital) * (hv1.numel() + hv2.numel()) * 8 + (Gg * hg[2 * plo:2 * phi].numel() * 8)
+        h2d[0] = n_vgroups * (hv1.numel() + hv2.numel()) * 8 + (Gg * hg[ipp * plo:ipp * phi].numel() * 8)
 
     _, ms_h2d = timed(step_h2d)
     ctx.close()
@@ -637,8 +647,12 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
                              "h2d_bytes_per_step_rank0": h2d[0], "clock": "host wall, max over ranks"},
             "sessions_per_step": {"vital": Gv, "gesture": Gg}, "n_gpus": world,
             "allgather_bytes_per_rank_per_step": xbytes[0], "device_pool_sessions_per_type": pool,
-            "config": (f"{Gv} vital sessions (R=64, F=200 @ 20 Hz, V1 + full-depth V2 with VP+, session-sharded) + "
-                       f"{Gg} gesture sessions (C4, 8 frames per ciphertext, {npair} pairs frame-sharded over the "
+            "vital_sessions_per_ciphertext": sp,
+            "config": (f"{Gv} vital sessions (R=64, F=200 @ 20 Hz, V1 + full-depth V2 with VP+, session-sharded, "
+                       f"packed {sp} per ciphertext in slot blocks of R 2^iq_pack = {VITAL_PERIOD} (DESIGN R33): "
+                       f"{n_vgroups} packed groups on rank 0) + "
+                       f"{Gg} gesture sessions (C4 headline config, 8 frames per ciphertext, {npair} frame groups "
+                       f"frame-sharded over the "
                        f"ranks, NCCL all-gather of partial feature ciphertexts, library mod-q sum + FC on the owner) "
                        f"per step at PS4 (N=2^16), one shared key set; device-resident inputs cycle a pool of {pool} "
                        f"distinct sessions per type; h2d_included uploads every session from pinned host memory "

@@ -493,6 +493,54 @@ def test_vitals_v2_vp_plus(m, taps, iq_pack, hoist):
     assert ctx.trace() == ev.trace
 
 
+@pytest.mark.parametrize("iq_pack,hoist", [(0, 0), (3, 1)])
+def test_vital_sessions_packed(m, iq_pack, hoist):
+    """Vital sessions packed per ciphertext (DESIGN R33): S = N / (2 R 2^iq_pack) sessions in the slot
+    blocks of every input ciphertext, cfg.n_slots = R 2^iq_pack; V1 and the full-depth V2 (VP+):
+    residues and op traces equal the oracle's (whose per-session decryption is pinned against each
+    session's DSP in test_oracle_circuits.py::test_vital_sessions_packed_per_ciphertext)."""
+    P = toy(log_n=10, n_q=10, scale_bits=50, n_p=2, alpha=2)
+    R, F = 8, 12
+    n = R << iq_pack
+    S = (P.n // 2) // n
+    cfg = cc.ChainCfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=n, fs=2.0, bands=((0.1, 0.6), (0.7, 1.0)),
+                      frame_batch=4, vp_plus=1, iq_pack=iq_pack, hoist=hoist)
+    scenes = [radar.preprocess_vital(radar.vital_scene(R, F, cfg.fs, seed=3600 + s)[0]) for s in range(S)]
+    rots = sorted(set(cc.required_rotations("vitals_v1", cfg, P.n)) | set(cc.required_rotations("vitals_v2", cfg, P.n)))
+    keys = orc.keygen(P, seed=3601, rotations=rots)
+
+    def cts(lvl):
+        out = []
+        for t in range(F):
+            for part in ("real", "imag"):
+                v = np.concatenate([radar.pack_vital(getattr(scenes[s][t], part), n) for s in range(S)])
+                sc = float(2 ** P.scale_bits)
+                out.append(orc.encrypt(P, keys, orc.encode(P, v, sc, lvl), lvl, sc, n, seed=3602, index=len(out)))
+        return out
+
+    c1 = cts(3)
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    book = cc.PlainBook(P)
+    Nc, Dc = cc.vitals_v1(ev, book, c1[0::2], c1[1::2], cfg)
+    ctx = _run(m, P, keys, book, "vitals_v1", cfg, c1, [Nc, Dc])
+    assert ctx.trace() == ev.trace
+    c2 = cts(9)
+    taps = [np.array([0.2, 0.3, 0.3, 0.2]), np.array([0.25, -0.5, 0.25])]
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    out = cc.vitals_v2(ev, c2[0::2], c2[1::2], taps, cfg)
+    scalars = {f"k5.b{b}": t for b, t in enumerate(taps)}
+    bins = []
+    for b in range(2):
+        ks = dsp.band_bins(F - 1, cfg.fs, cfg.bands[b])
+        bins.append([int(k) for k in ks])
+        for k in ks:
+            c, s_ = dsp.narrowband_dft_coefs(F - 1, int(k))
+            scalars[f"vp.c.{b}.{int(k)}"] = c
+            scalars[f"vp.s.{b}.{int(k)}"] = s_
+    ctx = _run(m, P, keys, None, "vitals_v2", cfg, c2, out[0] + out[1], scalars=scalars, bins=bins, taps=taps)
+    assert ctx.trace() == ev.trace
+
+
 def test_chain_shape_and_depth_errors(m):
     P = toy(log_n=10, n_q=4, scale_bits=40, n_p=2, alpha=2)
     ctx = make_ctx(m, P)

@@ -685,3 +685,56 @@ def test_round2_cfg_fields_validated():
     k3a = cc.required_rotations("k3_doppler_dft", cc.ChainCfg(**base, bsgs_aligned=1), n_ring)
     assert k3a == sorted({(s * 8) % (n_ring // 2) for s in range(1, 16)} |
                          {(G * 8) % (n_ring // 2) for G in (-32, -16, 16)})
+
+
+# ------------------------------------------------------------------ vital sessions packed per ciphertext (R33)
+
+def _decode_all(P, keys, ct):
+    return orc.decode(P, orc.decrypt(P, keys, ct), ct.level, ct.scale, P.n // 2)
+
+
+@pytest.mark.parametrize("iq_pack", [0, 3])
+def test_vital_sessions_packed_per_ciphertext(iq_pack):
+    """Reading R33 (SURVEY §8(f)-3 "several sessions per ciphertext"): with the packing period
+    n = R 2^iq_pack (cfg.n_slots), S = N / (2n) vital sessions share every ciphertext, session s in
+    slots [s n, s n + R) (zeros up to the next block, reading #23).  Every vital op is slot-wise or
+    rotates by less than n within the block it reads, and the public vectors are period-n, so V1 and
+    V2 give each session's outputs in slot s n: checked against each session's plaintext DSP."""
+    P = toy(log_n=10, n_q=8, scale_bits=40, n_p=2, alpha=2)
+    R, F = 8, 16
+    n = R << iq_pack
+    S = (P.n // 2) // n
+    cfg = cc.ChainCfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=n, fs=2.0,
+                      bands=((0.1, 0.6), (0.7, 1.0)), iq_pack=iq_pack, frame_batch=F)
+    scenes = [radar.preprocess_vital(radar.vital_scene(R, F, cfg.fs, seed=1100 + s)[0]) for s in range(S)]
+    rots = sorted(set(cc.required_rotations("vitals_v1", cfg, P.n)) | set(cc.required_rotations("vitals_v2", cfg, P.n)))
+    keys = orc.keygen(P, seed=2100, rotations=rots)
+
+    def enc(t, part, lvl, idx):
+        v = np.concatenate([radar.pack_vital(getattr(scenes[s][t], part), n) for s in range(S)])
+        return orc.encrypt(P, keys, orc.encode(P, v, float(2 ** P.scale_bits), lvl), lvl, float(2 ** P.scale_bits),
+                           n, seed=31, index=idx)
+
+    # V1 at level 3
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    re = [enc(t, "real", 3, 2 * t) for t in range(F)]
+    im = [enc(t, "imag", 3, 2 * t + 1) for t in range(F)]
+    Nc, Dc = cc.vitals_v1(ev, cc.PlainBook(P), re, im, cfg)
+    Nd, Dd = _decode_all(P, keys, Nc), _decode_all(P, keys, Dc)
+    for s in range(S):
+        Np, Dp, _ = dsp.soft_attention(dsp.energy(scenes[s]), cfg.gamma, F)
+        assert abs(Nd[s * n] - Np) <= 1e-3 * abs(Np) and abs(Dd[s * n] - Dp) <= 1e-3 * abs(Dp), s
+    # V2 at level 7
+    ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+    re = [enc(t, "real", 7, 2 * t) for t in range(F)]
+    im = [enc(t, "imag", 7, 2 * t + 1) for t in range(F)]
+    taps = [np.array([0.2, 0.3, 0.3, 0.2]), np.array([0.25, -0.5, 0.25])]
+    out = cc.vitals_v2(ev, re, im, taps, cfg)
+    for s in range(S):
+        I = np.array([dsp.soft_iq(scenes[s][t], cfg.p_phi)[0] for t in range(F)])
+        Q = np.array([dsp.soft_iq(scenes[s][t], cfg.p_phi)[1] for t in range(F)])
+        for bi, h in enumerate(taps):
+            y = dsp.taylor_phase(dsp.fir(I, h), dsp.fir(Q, h), cfg.taylor_order)
+            want = dsp.narrowband_power(y, dsp.band_bins(len(y), cfg.fs, cfg.bands[bi]))
+            got = np.array([_decode_all(P, keys, c)[s * n] for c in out[bi]])
+            assert rel_err(got, want) < 1e-3, (s, bi)
