@@ -1111,7 +1111,8 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the multi-GPU C5 exchange workload")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--c5-per-rank", type=int, default=8, help="C5: vital and gesture sessions per rank (weak scaling)")
+    ap.add_argument("--c5-per-rank", type=int, default=64,
+                    help="C5: vital and gesture sessions per rank (weak scaling; 64 fills one packed vital group, R33)")
     ap.add_argument("--c5-sessions", type=int, default=0,
                     help="C5: total sessions per step (half vital, half gesture; 1024 = SURVEY's full C5)")
     ap.add_argument("--c5-pool", type=int, default=2, help="C5: distinct device-resident sessions per type")

@@ -146,7 +146,9 @@ void eval_chain_impl(Ctx &c, const char *chain, const mmfhe_chain_cfg &cfg, cons
                      mmfhe_ct *out, size_t n)
 {
     if (c.graphs_on && !c.trace_on && !c.prof_on && all_device(in, n_in) && all_device(out, n)) {
-        if (c.graphs.size() >= 64) c.drop_graphs();
+        // (one graph per distinct chain + buffer-address set: C5 keeps 2 per gesture session + its vital
+        // groups, 1024 sessions included; a full cache is dropped and re-filled)
+        if (c.graphs.size() >= 1100) c.drop_graphs();
         Ctx::ChainGraph &g = c.graphs[chain_key(c, chain, cfg, in, n_in, out, n)];
         if (!g.exec && g.seen >= 1) capture_chain(c, g, chain, cfg, in, n_in, out, n);
         if (g.exec) {
