@@ -363,22 +363,41 @@ __global__ void __launch_bounds__(kHTile) k_hoisted_ip_pq(const uint64_t *__rest
             }
             sy[((size_t)b * a.dnum + j) * kHTile + t] = src[k];
         }
-        if (isq) sc[(size_t)b * kHTile + t] = c0[(size_t)b * a.cs + (size_t)r * kt.n + k];
+        // [P]_r c0[k]: the same P lift for every step (the steps differ only in where it lands)
+        if (isq)
+            sc[(size_t)b * kHTile + t] = shoup(c0[(size_t)b * a.cs + (size_t)r * kt.n + k], pmod[r].w, pmod[r].wp, q);
     }
     __syncthreads();
     const size_t key_rows = a.L + 1 + a.K;
-    const TwPair pm = isq ? pmod[r] : TwPair{0, 0};
     const size_t qrow = isq ? (size_t)r * kt.n : 0;
     const size_t prow = isq ? 0 : (size_t)(2 * (a.level + 1) + (r - a.level - 1)) * kt.n;
     const size_t opoly = isq ? (size_t)(a.level + 1) * kt.n : (size_t)a.K * kt.n;
+    // the next step's key words are loaded while this step's items are computed
+    uint64_t nkb[DMAX], nka[DMAX];
+    uint32_t nj = galois_perm(k, a.ginv[0], kt.log_n);
+#pragma unroll
+    for (int d = 0; d < DMAX; ++d) {
+        if (d < (int)a.dnum) {
+            nkb[d] = __ldg(a.key[0] + ((size_t)(2 * d) * key_rows + pr) * kt.n + nj);
+            nka[d] = __ldg(a.key[0] + ((size_t)(2 * d + 1) * key_rows + pr) * kt.n + nj);
+        }
+    }
     for (uint32_t s = 0; s < a.nsteps; ++s) {
-        const uint32_t j = galois_perm(k, a.ginv[s], kt.log_n);
+        const uint32_t j = nj;
         uint64_t kb[DMAX], ka[DMAX];
 #pragma unroll
         for (int d = 0; d < DMAX; ++d) {
-            if (d < (int)a.dnum) {
-                kb[d] = __ldg(a.key[s] + ((size_t)(2 * d) * key_rows + pr) * kt.n + j);
-                ka[d] = __ldg(a.key[s] + ((size_t)(2 * d + 1) * key_rows + pr) * kt.n + j);
+            kb[d] = nkb[d];
+            ka[d] = nka[d];
+        }
+        if (s + 1 < a.nsteps) {
+            nj = galois_perm(k, a.ginv[s + 1], kt.log_n);
+#pragma unroll
+            for (int d = 0; d < DMAX; ++d) {
+                if (d < (int)a.dnum) {
+                    nkb[d] = __ldg(a.key[s + 1] + ((size_t)(2 * d) * key_rows + pr) * kt.n + nj);
+                    nka[d] = __ldg(a.key[s + 1] + ((size_t)(2 * d + 1) * key_rows + pr) * kt.n + nj);
+                }
             }
         }
         uint64_t *o = a.out[s] + (isq ? qrow : prow) + j;
@@ -394,7 +413,7 @@ __global__ void __launch_bounds__(kHTile) k_hoisted_ip_pq(const uint64_t *__rest
                 }
             }
             uint64_t v0 = redc(acc0, q, qi);
-            if (isq) v0 = add_mod(v0, shoup(sc[(size_t)b * kHTile + t], pm.w, pm.wp, q), q);
+            if (isq) v0 = add_mod(v0, sc[(size_t)b * kHTile + t], q);
             o[(size_t)b * a.os] = v0;
             o[(size_t)b * a.os + opoly] = redc(acc1, q, qi);
         }
