@@ -898,6 +898,7 @@ class OracleC4Stages:
     def run_stage(self, s):
         cc, ev = self.cc, self.cc.CircuitEvaluator(self.P, self.rlk, self.gk)
         cfg, book = self.ccfg, self.book
+        cc.set_merge(ev, cfg)  # the headline's merged divisions (R31)
         x = self.cache.get(s) if s != "k3_babies" else self._pair()
         e0, t0 = book.encode_s, time.perf_counter()
         if s == "k3_babies":
@@ -907,16 +908,17 @@ class OracleC4Stages:
         elif s == "k3_giants":
             y = cc.k3_giant_steps_c(ev, x, cfg) if self.cplx else cc.k3_giant_steps(ev, x, cfg)
         elif s == "k1_k6":
-            y = cc.k6_notch(ev, book, cc.k1_power_c(ev, x) if self.cplx else cc.k1_power(ev, x[0], x[1]), cfg)
+            y = cc.k6_notch(ev, book, cc.k1_power_c(ev, x, cc.k1_fused(cfg)) if self.cplx else cc.k1_power(ev, x[0], x[1]),
+                            cfg)
         elif s == "k2b_sum":
             y = cc.frame_accumulate(ev, cc.k2_doppler_soft_power(ev, x, cfg))
         else:
             layer = int(s[2])
             L, dims = cc.lanes_of(cfg), cfg.fc_dims
-            if layer == 1 and L > 1:
-                x = (ev.rotsum_dh_all if cc.dh(cfg) else ev.rotsum_all)([x], L, 1)[0]
+            if layer == 1 and L > 1:  # the lane sum (oracle gesture_fc's first step)
+                x = (cc.rotsum_dh(ev, [x], L, 1, cfg) if cc.dh(cfg) else ev.rotsum_all([x], L, 1))[0]
             y = cc.fc_layer(ev, book, x, self.Ws[layer - 1], self.bs[layer - 1], dims[layer - 1], layer,
-                            layer < 3, cfg.hoist, L, cfg.fc_baby)
+                            layer < 3, cfg.hoist, L, cfg.fc_baby, cc.rotsum_inner(cfg), bool(cfg.rotsum_hoist_all))
         dt = time.perf_counter() - t0 - (book.encode_s - e0)
         nxt = self.stages.index(s) + 1
         if nxt < len(self.stages):
