@@ -390,8 +390,8 @@ std::vector<DCt> ev_diag_mac(Ctx &c, const std::vector<const DCt *> &cts,
                           x->pk == a0.pk,
                       MMFHE_E_LAYOUT, "diag MAC operands must share level, batch, basis and scale");
     std::vector<DCt> out;
-    const bool fused = cts.size() <= (size_t)kDiagMax && pts.size() <= (size_t)kDiagMax;
-    MMFHE_REQUIRE(fused || !a0.pk, MMFHE_E_LAYOUT, "PQ diagonal MAC: at most 16 baby steps and outputs");
+    const bool fused = cts.size() <= (size_t)kDiagIn && pts.size() <= (size_t)kDiagMax;
+    MMFHE_REQUIRE(fused || !a0.pk, MMFHE_E_LAYOUT, "PQ diagonal MAC: at most 32 baby steps and 16 outputs");
     std::vector<const uint64_t *> ctp;
     for (auto *x : cts) ctp.push_back(x->data());
     std::vector<std::vector<const uint64_t *>> ptp;

@@ -11,6 +11,7 @@ namespace mmfhe {
 
 constexpr int kMaxTerms = 64;  // operands per fused-sum launch (chunked above)
 constexpr int kDiagMax = 16;   // baby steps / outputs of one fused BSGS diagonal MAC
+constexpr int kDiagIn = 32;    // baby steps of the plaintext-stationary (staged) diagonal MAC
 
 struct PtrList {
     const uint64_t *p[kMaxTerms];
@@ -85,7 +86,7 @@ void launch_tensor_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &a, const
 void launch_pmult_sum(Ctx &c, uint64_t *out, size_t os, const PtrList &pt, const PtrList &ct, size_t is, int n,
                       uint32_t level, bool accumulate, uint32_t B);
 // Fused BSGS inner sums (CK9): out_o (+0) = sum_c pts[o][c] (.) cts[c] for a batch of B
-// (cts item stride is, outs item stride os); pts[o][c] may be null; <= kDiagMax each.
+// (cts item stride is, outs item stride os); pts[o][c] may be null; <= kDiagIn inputs, <= kDiagMax outputs.
 // pk = K: the operands are PQ ciphertexts / plaintexts (rows over Q_l u P, double hoisting).
 void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is,
                      const std::vector<std::vector<const uint64_t *>> &pts, const std::vector<uint64_t *> &outs,

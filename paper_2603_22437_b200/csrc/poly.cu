@@ -784,8 +784,8 @@ __global__ void __launch_bounds__(kTB) k_pmult_sum(uint64_t *__restrict__ out_ba
 // operands (double hoisting: pk = K extra limbs) map to the special primes.
 constexpr int kDmTK = 32;
 struct DiagMacArgs {
-    const uint64_t *ct[kDiagMax];
-    const uint64_t *pt[kDiagMax][kDiagMax];
+    const uint64_t *ct[kDiagIn];
+    const uint64_t *pt[kDiagMax][kDiagIn];
     uint64_t *out[kDiagMax];
     size_t is, os;
     int nc, no;
@@ -827,11 +827,20 @@ __global__ void __launch_bounds__(128) k_diag_mac(DiagMacArgs a, KTables kt)
         for (int c = 0; c < NCMAX; ++c) x[c] = c < a.nc ? a.ct[c][(size_t)b * a.is + off] : 0;
         const uint64_t *w = spt + lane;
         for (int o = 0; o < a.no; ++o, w += a.nc * kDmTK) {
-            U128 acc{0, 0};  // <= 16 terms < q^2 each: < q 2^64 for q < 2^60; absent terms are 0
+            // <= 16 terms < q^2 each per 128-bit sum (< q 2^64 for q < 2^60); absent terms are 0; a
+            // 32-wide instantiation reduces its first 16 terms before the next 16
+            U128 acc{0, 0};
+            uint64_t part = 0;
 #pragma unroll
-            for (int c = 0; c < NCMAX; ++c)
+            for (int c = 0; c < NCMAX; ++c) {
+                if (c == 16) {
+                    part = redc(acc, q, qi);
+                    acc = U128{0, 0};
+                }
                 if (c < a.nc) mac128(acc, x[c], w[c * kDmTK]);
-            a.out[o][(size_t)b * a.os + off] = redc(acc, q, qi);
+            }
+            const uint64_t v = redc(acc, q, qi);
+            a.out[o][(size_t)b * a.os + off] = NCMAX > 16 ? add_mod(v, part, q) : v;
         }
     }
 }
@@ -1358,7 +1367,7 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
                      const std::vector<std::vector<const uint64_t *>> &pts, const std::vector<uint64_t *> &outs,
                      size_t os, uint32_t level, uint32_t B, uint32_t pk)
 {
-    MMFHE_REQUIRE(cts.size() <= (size_t)kDiagMax && outs.size() <= (size_t)kDiagMax && pts.size() == outs.size(),
+    MMFHE_REQUIRE(cts.size() <= (size_t)kDiagIn && outs.size() <= (size_t)kDiagMax && pts.size() == outs.size(),
                   MMFHE_E_LAYOUT, "diag_mac shape");
     MMFHE_REQUIRE(c.n % kDmTK == 0, MMFHE_E_PARAMS, "N must be a multiple of 32");
     DiagMacArgs a{};
@@ -1389,7 +1398,8 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
         const char *e = getenv("MMFHE_DIAG_STAGED");
         return e ? (*e == '1' ? 1 : 0) : -1;
     }();
-    const bool l2_variant = forced >= 0 ? forced == 0 : B < 4;
+    // more than 16 baby steps: the staged kernel only (its 32-wide instantiation)
+    const bool l2_variant = a.nc <= kDiagMax && (forced >= 0 ? forced == 0 : B < 4);
     if (l2_variant) {
         const dim3 g(((c.n + 255) / 256) * B, 2 * (level + 1 + pk));
         if (a.nc <= 4)
@@ -1403,10 +1413,11 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
     }
     static std::atomic<uint64_t> attr{0};
     once_per_device(attr, [] {
-        const int mx = (int)(sizeof(uint64_t) * kDiagMax * kDiagMax * kDmTK);
+        const int mx = (int)(sizeof(uint64_t) * kDiagMax * kDiagIn * kDmTK);
         CUDA_CHECK(cudaFuncSetAttribute(k_diag_mac<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         CUDA_CHECK(cudaFuncSetAttribute(k_diag_mac<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         CUDA_CHECK(cudaFuncSetAttribute(k_diag_mac<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        CUDA_CHECK(cudaFuncSetAttribute(k_diag_mac<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     });
     const size_t smem = sizeof(uint64_t) * (size_t)a.no * a.nc * kDmTK;
     const dim3 g(c.n / kDmTK, level + 1 + pk);
@@ -1414,8 +1425,10 @@ void launch_diag_mac(Ctx &c, const std::vector<const uint64_t *> &cts, size_t is
         k_diag_mac<4><<<g, 128, smem, c.stream>>>(a, c.kt);
     else if (a.nc <= 8)
         k_diag_mac<8><<<g, 128, smem, c.stream>>>(a, c.kt);
-    else
+    else if (a.nc <= 16)
         k_diag_mac<16><<<g, 128, smem, c.stream>>>(a, c.kt);
+    else
+        k_diag_mac<32><<<g, 128, smem, c.stream>>>(a, c.kt);
     LAUNCH_CHECK(c);
 }
 

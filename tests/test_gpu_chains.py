@@ -323,7 +323,8 @@ def test_gesture_chain_lanes_small(m, lanes, F, fb, hoist, merge):
                                                       (1, 2, 0, 0, 1), (2, 5, 2, 2, 1), (4, 6, 0, 2, 1),
                                                       (1, 6, 0, 2, 1), (4, 6, 0, 2, 2), (2, 5, 2, 2, 3),
                                                       (4, 6, 0, 2, 4), (1, 3, 0, 2, 5), (4, 6, 0, 2, 6),
-                                                      (1, 6, 0, 2, 6), (4, 6, 0, 2, 7), (1, 3, 0, 2, 7)])
+                                                      (1, 6, 0, 2, 6), (4, 6, 0, 2, 7), (1, 3, 0, 2, 7),
+                                                      (1, 3, 0, 2, 8)])
 def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     """Complex-slot gesture pipeline (cfg.cplx, DESIGN R28): one ciphertext z = v_re + j v_im
     per frame group, K3 with complex diagonals (one plaintext product per diagonal), K1 as
@@ -339,6 +340,8 @@ def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     cfg.rotsum_hoist_all = int(aligned >= 4)
     cfg.ks_merge = int(aligned >= 6)  # 6: + relin / ModDown + rescale as one division (R31)
     cfg.k1_conj_fuse = int(aligned >= 7)  # 7: + K1 as one conjugate-product key switch (R32)
+    if aligned == 8:  # 8: 20 baby steps (> 16): the 32-wide staged diagonal MAC with its split sum
+        cfg.bsgs_baby = 20
     if aligned == 6:
         cfg.rotsum_inner = 2
     rots = cc.required_rotations("gesture", cfg, P.n)
