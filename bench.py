@@ -52,6 +52,7 @@ ALIGNED = 1                        # K3 giants at multiples of b: the giant G = 
 ROTSUM_INNER = 16                  # double-hoisted rotate-and-sum levels of 16 (R27)
 ROTSUM_HOIST_ALL = 1               # every level hoisted (R30): C4 46.7 -> 43.6 ms (profiles/r02/c4prof_*_r02ao.log)
 KS_MERGE = 1                       # relin / ModDown + rescale as one division by P q_l (R31): 42.5 -> 40.6 ms
+                                   # (C4); also the vital extras and C5's vital sessions
 K1_CONJ_FUSE = 1                   # K1 as one conjugate-product key switch (R32): 40.4 -> 39.7 ms
 
 
@@ -384,7 +385,7 @@ def bench_workload(name, m, torch, device, steps=3, warmup=2):
         packed = name == "C2_packed"  # 8 sessions per ciphertext in blocks of R 2^iq_pack = 1024 slots (R33)
         cfg = m.chain_cfg(R=128, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=(128 << 3) if packed else P.n // 2,
                           bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
-                          iq_pack=3, hoist=1)
+                          iq_pack=3, hoist=1, ks_merge=KS_MERGE)
         plan = [("vitals_v1", 3, 2 * F), ("vitals_v2", 7, 2 * F)]
         taps = [radar.fir_taps(41, b, fs) for b in BANDS]
         spc = (P.n // 2) // (128 << 3) if packed else 1
@@ -415,7 +416,7 @@ def bench_workload(name, m, torch, device, steps=3, warmup=2):
         t3 = name == "C5v_t3"
         cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=3 if t3 else 1, n_slots=P.n // 2,
                           bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
-                          frame_batch=40, vp_plus=1, iq_pack=3, hoist=1)
+                          frame_batch=40, vp_plus=1, iq_pack=3, hoist=1, ks_merge=KS_MERGE)
         plan = [("vitals_v1", 3, 2 * F), ("vitals_v2", 11 if t3 else 9, 2 * F)]
         taps = [radar.fir_taps(41, b, fs) for b in BANDS]
         frames = F
@@ -485,7 +486,7 @@ def c5_vital_cfg(m):
     from synth import radar
     cfg = m.chain_cfg(R=64, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=VITAL_PERIOD,
                       bands_bins=[band_bins(F - 1, fs, b) for b in BANDS], n_taps=[41, 41], fs=fs,
-                      frame_batch=40, vp_plus=1, iq_pack=3, hoist=1)
+                      frame_batch=40, vp_plus=1, iq_pack=3, hoist=1, ks_merge=KS_MERGE)
     return cfg, F, [radar.fir_taps(41, b, fs) for b in BANDS]
 
 

@@ -159,7 +159,7 @@ typedef struct {
                               levels of min(rotsum_inner, what is left) terms, each one ModUp + one-pass PQ
                               steps + one ModDown, no plain rotate-and-add key switches; 0 = R27 (first
                               level hoisted, then rotate-and-adds).  Same decryption */
-    uint32_t ks_merge;     /* gesture / K3 / FC chains: 1 = every relinearisation or double-hoisted ModDown that a
+    uint32_t ks_merge;     /* gesture / K3 / FC / vital V1, V2 chains: 1 = every relinearisation or double-hoisted ModDown that a
                               rescale follows runs as ONE division by P q_l (DESIGN R31: fast base conversion
                               from p_0..p_{K-1}, q_l, one forward NTT of the q_0..q_{l-1} rows fewer); records
                               "relin_rescale" / "moddown_rescale".  Other residues, same decryption */

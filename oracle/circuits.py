@@ -62,8 +62,8 @@ class ChainCfg:
     bsgs_aligned: int = 0       # K3: 1 -> giant offsets at multiples of b, one giant step the identity (R29)
     rotsum_inner: int = 0       # double hoisting: size of the rotate-and-sum's hoisted first level (R27; 0 -> 8)
     rotsum_hoist_all: int = 0   # double hoisting: 1 -> every rotate-and-sum level hoisted (groups of rotsum_inner, R30)
-    ks_merge: int = 0           # gesture / K3 / FC: 1 -> every ModDown or relinearisation followed by a rescale is
-                                # ONE division by P q_l (R31)
+    ks_merge: int = 0           # gesture / K3 / FC / vital V1, V2: 1 -> every ModDown or relinearisation followed
+                                # by a rescale is ONE division by P q_l (R31)
     k1_conj_fuse: int = 0       # complex slots + ks_merge: 1 -> K1's d Conj(d) as one conjugate-product key switch
                                 # (R32; needs the CONJ_PROD key)
     cplx: int = 0               # gesture / K3: 1 -> complex slots, z = v_re + j v_im in ONE ciphertext
@@ -341,6 +341,7 @@ def k2_soft_attention(ev: CircuitEvaluator, book: PlainBook, E: orc.Ct, cfg: Cha
 
 def vitals_v1(ev, book, re_list, im_list, cfg):
     """Chain V1 = K1 -> K2; the client decrypts N and D, r_hat = N/D."""
+    set_merge(ev, cfg)
     return k2_soft_attention(ev, book, k1_energy(ev, re_list, im_list), cfg)
 
 
@@ -434,7 +435,7 @@ def k1_fused(cfg) -> bool:
 
 
 def set_merge(ev, cfg):
-    """Reading R31 for the gesture / K3 / FC chains: the evaluator merges every relinearisation or
+    """Reading R31 for the gesture / K3 / FC and vital (V1 / V2) chains: the evaluator merges every relinearisation or
     ModDown that a rescale follows into one division by P q_l (cfg.ks_merge)."""
     ev.merge_rescale = bool(getattr(cfg, "ks_merge", 0))
 
@@ -882,6 +883,7 @@ def vitals_v2(ev, re_list, im_list, taps_by_band, cfg):
     """Chain V2: K4 -> K5 -> K7 -> narrowband DFT -> |X|^2 per band (P:901-902);
     returns {band index: [P_k ciphertexts]} (sharpen/average on the client, reading #4),
     or with cfg.vp_plus {band index: [N_f, D_f]} (VP+ in the cloud, the full-depth chain)."""
+    set_merge(ev, cfg)
     I, Q = [], []
     for s, e in chunks(len(re_list), cfg.frame_batch):
         Ib, Qb = k4_soft_iq(ev, re_list[s:e], im_list[s:e], cfg)

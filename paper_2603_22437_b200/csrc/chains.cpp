@@ -271,14 +271,14 @@ class Runner {
         }
         std::vector<std::pair<const DCt *, const DCt *>> pairs;
         for (auto &v : views) pairs.push_back({&v, &v});
-        return ev_relin_rescale(c_, ev_tensor_sum(c_, pairs));
+        return relin_rescale(ev_tensor_sum(c_, pairs));
     }
 
     // K1 for S sessions at once: re[t], im[t] are batches over the sessions
     std::pair<DCt, DCt> k2_soft_attention(const DCt &E)
     {
         DCt w = copy_ct(c_, E);
-        for (uint32_t i = 0; i < ilog2(cfg_.gamma); ++i) w = ev_square_rescale(c_, w);
+        for (uint32_t i = 0; i < ilog2(cfg_.gamma); ++i) w = relin_rescale(ev_tensor_sum(c_, {{&w, &w}}));
         const uint32_t n = E.n_slots, R = cfg_.R;
         const double FFR = (double)cfg_.F * cfg_.F * R;
         const DPlain &ramp = plain("k2.ramp", w.level, qscale(w.level), [&] {
@@ -554,12 +554,12 @@ class Runner {
     // ---------------------------------------------------------- vital V2 (batched over frames)
     std::pair<DCt, DCt> k4_soft_iq(const DCt &re, const DCt &im)
     {
-        DCt p = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&re, &re}, {&im, &im}}));
-        for (uint32_t i = 0; i < ilog2(cfg_.p_phi); ++i) p = ev_square_rescale(c_, p);
+        DCt p = relin_rescale(ev_tensor_sum(c_, {{&re, &re}, {&im, &im}}));
+        for (uint32_t i = 0; i < ilog2(cfg_.p_phi); ++i) p = relin_rescale(ev_tensor_sum(c_, {{&p, &p}}));
         DCt red = ev_drop_to(c_, re, p.level);
-        DCt i_ = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&p, &red}}));
+        DCt i_ = relin_rescale(ev_tensor_sum(c_, {{&p, &red}}));
         DCt imd = ev_drop_to(c_, im, p.level);
-        DCt q_ = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&p, &imd}}));
+        DCt q_ = relin_rescale(ev_tensor_sum(c_, {{&p, &imd}}));
         if (cfg_.iq_pack) {
             // reading R19: pack i, q (and 2^(k-1) frames) into the slot blocks of one
             // ciphertext, one rotate-and-sum, unpack (see oracle k4_packed_rotsum)
@@ -663,16 +663,16 @@ class Runner {
         DCt Q1 = slice(Qf, 1, F - 1), Q0 = slice(Qf, 0, F - 1);
         DCt ty = ev_tensor_sum(c_, {{&Q1, &I0}});
         DCt ty2 = ev_tensor_sum(c_, {{&I1, &Q0}});
-        DCt y = ev_relin_rescale(c_, ev_addsub(c_, ty, ty2, true));
+        DCt y = relin_rescale(ev_addsub(c_, ty, ty2, true));
         if (cfg_.taylor_order == 1) return y;
-        DCt x = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&I1, &I0}, {&Q1, &Q0}}));
-        DCt x2 = ev_square_rescale(c_, x);
-        DCt y2 = ev_square_rescale(c_, y);
+        DCt x = relin_rescale(ev_tensor_sum(c_, {{&I1, &I0}, {&Q1, &Q0}}));
+        DCt x2 = relin_rescale(ev_tensor_sum(c_, {{&x, &x}}));
+        DCt y2 = relin_rescale(ev_tensor_sum(c_, {{&y, &y}}));
         std::vector<double> third(y.batch, -1.0 / 3.0);
         DCt yt = ev_rescale(c_, ev_lincomb_mat(c_, y, y.batch, 1, 0, 1, third));
         DCt yd = ev_drop_to(c_, y, x2.level);
-        DCt yx2 = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&yd, &x2}}));
-        DCt y3 = ev_relin_rescale(c_, ev_tensor_sum(c_, {{&y2, &yt}}));
+        DCt yx2 = relin_rescale(ev_tensor_sum(c_, {{&yd, &x2}}));
+        DCt y3 = relin_rescale(ev_tensor_sum(c_, {{&y2, &yt}}));
         return ev_addsub(c_, yx2, y3, false);
     }
 
@@ -701,7 +701,7 @@ class Runner {
         }
         DCt X = ev_rescale(c_, ev_lincomb_mat(c_, ys, 2 * K, Fp, 0, 0, coef));
         DCt Xr = slice(X, 0, K), Xi = slice(X, K, K);
-        return ev_relin_rescale(c_, ev_tensor_sum(c_, {{&Xr, &Xr}, {&Xi, &Xi}}));
+        return relin_rescale(ev_tensor_sum(c_, {{&Xr, &Xr}, {&Xi, &Xi}}));
     }
 
     // VP+ (SURVEY §8(c)-7): sharpen S_k = P_k^2, then N_f = sum_k f_k S_k and
@@ -709,7 +709,7 @@ class Runner {
     DCt vp_weighted_average(const DCt &Pk, uint32_t band, uint32_t Fp)
     {
         const uint32_t K = Pk.batch;
-        DCt S = ev_square_rescale(c_, Pk);
+        DCt S = relin_rescale(ev_tensor_sum(c_, {{&Pk, &Pk}}));
         std::vector<double> coef((size_t)2 * K);
         for (uint32_t bi = 0; bi < K; ++bi) {
             coef[bi] = (double)cfg_.bins[band][bi] * cfg_.fs / (double)Fp;
@@ -815,8 +815,9 @@ void validate_cfg(const std::string &chain, const mmfhe_chain_cfg &cfg)
                   "k1_conj_fuse needs cplx and ks_merge");
     if (cfg.ks_merge)
         MMFHE_REQUIRE(chain == "gesture" || chain == "gesture_frame" || chain == "gesture_features" ||
-                          chain == "gesture_fc" || chain == "fc_forward" || chain == "k3_doppler_dft",
-                      MMFHE_E_SHAPE, "ks_merge applies to the gesture / K3 / FC chains only");
+                          chain == "gesture_fc" || chain == "fc_forward" || chain == "k3_doppler_dft" ||
+                          chain == "vitals_v1" || chain == "vitals_v2",
+                      MMFHE_E_SHAPE, "ks_merge applies to the gesture / K3 / FC / vital V1, V2 chains only");
     if (cfg.cplx)
         MMFHE_REQUIRE(cplx_chain(chain, cfg) || chain == "gesture_fc" || chain == "fc_forward" ||
                           chain == "k2_doppler_soft_power" || chain == "k6_notch",

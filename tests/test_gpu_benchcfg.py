@@ -84,7 +84,7 @@ def test_c2_bench_params_residue_parity(m):
     # the bench's chain config; bins chosen inside the 16-frame DFT grid (k fs / (F-1))
     bands_for_bins = ((1.0, 1.4), (2.0, 4.0))
     cfg = cc.ChainCfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=P.n // 2, fs=fs, bands=bands_for_bins,
-                      iq_pack=3, hoist=1)
+                      iq_pack=3, hoist=1, ks_merge=1)
     rots = sorted(set(cc.required_rotations("vitals_v1", cfg, P.n)) | set(cc.required_rotations("vitals_v2", cfg, P.n)))
     keys = orc.keygen(P, seed=6001, rotations=rots)
     z, _ = radar.vital_scene(R, F, fs, seed=6002)
@@ -115,7 +115,7 @@ def test_c2_bench_params_residue_parity(m):
             scalars[f"vp.s.{b}.{k}"] = s
     ctx = make_ctx(m, P, keys, book, scalars)
     mcfg = m.chain_cfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=cfg.n_slots, bands_bins=bins,
-                       n_taps=[41, 41], fs=fs, iq_pack=3, hoist=1)
+                       n_taps=[41, 41], fs=fs, iq_pack=3, hoist=1, ks_merge=1)
     for chain, ins, want, ev in (("vitals_v1", v1, want1, ev1), ("vitals_v2", v2, want2, ev2)):
         ctx.trace_clear()
         levels = ctx.chain_plan(chain, mcfg, ins[0].level, len(ins))

@@ -496,8 +496,8 @@ def test_vitals_v2_vp_plus(m, taps, iq_pack, hoist):
     assert ctx.trace() == ev.trace
 
 
-@pytest.mark.parametrize("iq_pack,hoist", [(0, 0), (3, 1)])
-def test_vital_sessions_packed(m, iq_pack, hoist):
+@pytest.mark.parametrize("iq_pack,hoist,merge", [(0, 0, 0), (3, 1, 0), (3, 1, 1)])
+def test_vital_sessions_packed(m, iq_pack, hoist, merge):
     """Vital sessions packed per ciphertext (DESIGN R33): S = N / (2 R 2^iq_pack) sessions in the slot
     blocks of every input ciphertext, cfg.n_slots = R 2^iq_pack; V1 and the full-depth V2 (VP+):
     residues and op traces equal the oracle's (whose per-session decryption is pinned against each
@@ -507,7 +507,7 @@ def test_vital_sessions_packed(m, iq_pack, hoist):
     n = R << iq_pack
     S = (P.n // 2) // n
     cfg = cc.ChainCfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=n, fs=2.0, bands=((0.1, 0.6), (0.7, 1.0)),
-                      frame_batch=4, vp_plus=1, iq_pack=iq_pack, hoist=hoist)
+                      frame_batch=4, vp_plus=1, iq_pack=iq_pack, hoist=hoist, ks_merge=merge)
     scenes = [radar.preprocess_vital(radar.vital_scene(R, F, cfg.fs, seed=3600 + s)[0]) for s in range(S)]
     rots = sorted(set(cc.required_rotations("vitals_v1", cfg, P.n)) | set(cc.required_rotations("vitals_v2", cfg, P.n)))
     keys = orc.keygen(P, seed=3601, rotations=rots)

@@ -693,8 +693,8 @@ def _decode_all(P, keys, ct):
     return orc.decode(P, orc.decrypt(P, keys, ct), ct.level, ct.scale, P.n // 2)
 
 
-@pytest.mark.parametrize("iq_pack", [0, 3])
-def test_vital_sessions_packed_per_ciphertext(iq_pack):
+@pytest.mark.parametrize("iq_pack,merge", [(0, 0), (3, 0), (3, 1)])
+def test_vital_sessions_packed_per_ciphertext(iq_pack, merge):
     """Reading R33 (SURVEY §8(f)-3 "several sessions per ciphertext"): with the packing period
     n = R 2^iq_pack (cfg.n_slots), S = N / (2n) vital sessions share every ciphertext, session s in
     slots [s n, s n + R) (zeros up to the next block, reading #23).  Every vital op is slot-wise or
@@ -705,7 +705,7 @@ def test_vital_sessions_packed_per_ciphertext(iq_pack):
     n = R << iq_pack
     S = (P.n // 2) // n
     cfg = cc.ChainCfg(R=R, F=F, gamma=2, p_phi=2, taylor_order=1, n_slots=n, fs=2.0,
-                      bands=((0.1, 0.6), (0.7, 1.0)), iq_pack=iq_pack, frame_batch=F)
+                      bands=((0.1, 0.6), (0.7, 1.0)), iq_pack=iq_pack, frame_batch=F, ks_merge=merge)
     scenes = [radar.preprocess_vital(radar.vital_scene(R, F, cfg.fs, seed=1100 + s)[0]) for s in range(S)]
     rots = sorted(set(cc.required_rotations("vitals_v1", cfg, P.n)) | set(cc.required_rotations("vitals_v2", cfg, P.n)))
     keys = orc.keygen(P, seed=2100, rotations=rots)
@@ -720,6 +720,7 @@ def test_vital_sessions_packed_per_ciphertext(iq_pack):
     re = [enc(t, "real", 3, 2 * t) for t in range(F)]
     im = [enc(t, "imag", 3, 2 * t + 1) for t in range(F)]
     Nc, Dc = cc.vitals_v1(ev, cc.PlainBook(P), re, im, cfg)
+    assert ("relin_rescale" in [op for op, _, _ in ev.trace]) == bool(merge)  # R31 on the vital chains
     Nd, Dd = _decode_all(P, keys, Nc), _decode_all(P, keys, Dc)
     for s in range(S):
         Np, Dp, _ = dsp.soft_attention(dsp.energy(scenes[s]), cfg.gamma, F)
