@@ -559,6 +559,15 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
                        m.FORM_EVAL) for s in mine}
     ctx.trace_enable(False)
     xbytes = [0]
+    fcb = max(1, args.c5_fc_batch)
+
+    def fc_heads(gathered):
+        # the owner's sessions: library mod-q sum of every rank's partial, then the FC head of
+        # up to fcb sessions per call as one batch (gesture_fc over several sessions)
+        totals = [mdist.reduce_partials(ctx, m, gathered, s, lvf, scale_f[0], gcfg["n_slots"] * LANES, P.log_n,
+                                        buf=sum_bufs[s]) for s in mine]
+        for c0 in range(0, len(mine), fcb):
+            ctx.eval_chain("gesture_fc", gm, totals[c0:c0 + fcb], [fc_outs[s] for s in mine[c0:c0 + fcb]])
 
     def gesture_phase(frames_of):
         if phi > plo:
@@ -568,10 +577,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
             feat_bufs.zero_()
         gathered = mdist.allgather_partials(feat_bufs)
         xbytes[0] = feat_bufs.numel() * 8
-        for s in mine:
-            total = mdist.reduce_partials(ctx, m, gathered, s, lvf, scale_f[0], gcfg["n_slots"] * LANES, P.log_n,
-                                          buf=sum_bufs[s])
-            ctx.eval_chain("gesture_fc", gm, [total], [fc_outs[s]])
+        fc_heads(gathered)
 
     # the features' scale (the reduce needs it before the first gather)
     probe = m.Ct(torch.empty((2, lvf + 1, P.n), dtype=torch.int64, device=device), lvf, 0.0, 0, P.log_n, m.FORM_EVAL)
@@ -631,10 +637,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
             sessions_features_async()
         ctx.sync()
         gathered = mdist.allgather_partials(feat_bufs)
-        for s in mine:
-            total = mdist.reduce_partials(ctx, m, gathered, s, lvf, scale_f[0], gcfg["n_slots"] * LANES, P.log_n,
-                                          buf=sum_bufs[s])
-            ctx.eval_chain("gesture_fc", gm, [total], [fc_outs[s]])
+        fc_heads(gathered)
         h2d[0] = n_vgroups * (hv1.numel() + hv2.numel()) * 8 + (Gg * hg[ipp * plo:ipp * phi].numel() * 8)
 
     _, ms_h2d = timed(step_h2d)
@@ -654,7 +657,8 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
                        f"{n_vgroups} packed groups on rank 0) + "
                        f"{Gg} gesture sessions (C4 headline config, 8 frames per ciphertext, {npair} frame groups "
                        f"frame-sharded over the "
-                       f"ranks, NCCL all-gather of partial feature ciphertexts, library mod-q sum + FC on the owner) "
+                       f"ranks, NCCL all-gather of partial feature ciphertexts, library mod-q sum + FC on the owner, "
+                       f"{fcb} sessions per FC-head batch) "
                        f"per step at PS4 (N=2^16), one shared key set; device-resident inputs cycle a pool of {pool} "
                        f"distinct sessions per type; h2d_included uploads every session from pinned host memory "
                        f"inside the timed region (copy-stream waves)")}
@@ -1119,6 +1123,8 @@ def main():
     ap.add_argument("--c5-sessions", type=int, default=0,
                     help="C5: total sessions per step (half vital, half gesture; 1024 = SURVEY's full C5)")
     ap.add_argument("--c5-pool", type=int, default=2, help="C5: distinct device-resident sessions per type")
+    ap.add_argument("--c5-fc-batch", type=int, default=16,
+                    help="C5: gesture sessions per FC-head call (the sessions' heads run as one batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-out", default="")
     args = ap.parse_args()

@@ -256,7 +256,9 @@ mmfhe_status mmfhe_load_scalars(mmfhe_ctx *ctx, const char *name, const double *
  * Outputs: k1_energy one E per session; vitals_v1 (N, D); vitals_v2 the P_k of every
  * band's bins in band order, or with cfg.vp_plus (N_f, D_f) per band; k3_doppler_dft
  * per frame batch its d_re items then its d_im items; gesture_frame one f per frame;
- * gesture / gesture_fc the logits.  Every output is valid in slot 0 (or the documented
+ * gesture the logits; gesture_fc / fc_forward take one feature ciphertext per session and
+ * run the head once over all of them as one batch (every op one launch over the sessions),
+ * one logits ciphertext per session in input order.  Every output is valid in slot 0 (or the documented
  * slots); other slots may hold partial sums.
  * out: caller buffers; mmfhe_chain_plan tells their count and levels.  Outputs leave
  * through one batched INTT (coefficient form) per output batch.

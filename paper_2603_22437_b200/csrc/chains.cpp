@@ -948,7 +948,9 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
         MMFHE_REQUIRE(n_in >= 2 && n_in % 2 == 0, MMFHE_E_SHAPE, "expected (v_re, v_im) per frame");
         n_out = chain == "k3_doppler_dft" ? n_in : chain == "gesture_frame" ? n_in / 2 : 1;
     } else if (chain == "gesture_fc" || chain == "fc_forward") {
-        MMFHE_REQUIRE(n_in == 1, MMFHE_E_SHAPE, "expected one feature ciphertext");
+        // one feature ciphertext per session, the sessions as one batch (one launch per op)
+        MMFHE_REQUIRE(n_in >= 1, MMFHE_E_SHAPE, "expected one feature ciphertext per session");
+        n_out = n_in;
     } else if (chain == "k2_soft_attention") {
         MMFHE_REQUIRE(n_in == 1 && cfg.F > 0, MMFHE_E_SHAPE, "expected one energy ciphertext E (and cfg.F)");
         n_out = 2;
@@ -1052,16 +1054,15 @@ std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_c
                 out.push_back(r.gesture_frame(vre, vim));
             }
         }
-    } else if (chain == "gesture_fc") {
-        DCt x = import_batch(c, in, 0, 1, 1);
+    } else if (chain == "gesture_fc" || chain == "fc_forward") {
+        // sessions batched: every op of the head runs once over all sessions' features (the same
+        // plaintext diagonals and keys for every item), item s = session s's logits
+        DCt x = import_batch(c, in, 0, 1, n_in);
         out.push_back(r.gesture_fc(x));
     } else if (chain == "gesture") {
         out.push_back(r.gesture(in, n_in));
     } else if (chain == "gesture_features") {
         out.push_back(r.gesture_features(in, n_in));
-    } else if (chain == "fc_forward") {
-        DCt x = import_batch(c, in, 0, 1, 1);
-        out.push_back(r.gesture_fc(x));
     } else if (chain == "k2_soft_attention") {
         auto nd = r.k2_soft_attention(import_batch(c, in, 0, 1, 1));
         out.push_back(std::move(nd.first));

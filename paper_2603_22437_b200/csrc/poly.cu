@@ -296,7 +296,9 @@ __global__ void __launch_bounds__(kTB, DMAX <= 4 ? 4 : 1) k_key_ip(uint64_t *__r
     const uint32_t kadd = EPI && (a.ep.add || a.ep.add1) ? galois_perm(k, a.ep.ag, kt.log_n) : 0;
     const TwPair *pmq = (EPI && a.ep.pmod && isq) ? a.ep.pmod + r : nullptr;
     // (a software-pipelined variant loading item b+1's digit words during item b's MACs measured
-    // slower on C4: 72 registers, 3 CTAs/SM, 9.96 -> 10.44 ms/step)
+    // slower on C4: 72 registers, 3 CTAs/SM, 9.96 -> 10.44 ms/step; so did two items per
+    // iteration with both items' loads issued first (32-bit offsets, 62 / 80 registers): C4
+    // key_ip 2.86 -> 3.17 ms, 3.46 with the epilogue instantiation at 4 CTAs/SM, r02bo)
     for (uint32_t b = b0; b < b1; ++b) {
         uint64_t s[DMAX];
 #pragma unroll

@@ -699,6 +699,28 @@ def test_standalone_k6_k2b_fc_chains(m, lanes):
     assert ctx.trace() == ev.trace
 
 
+@pytest.mark.parametrize("lanes,mode", [(1, 0), (4, 0), (4, 1)])
+def test_fc_forward_sessions_batched(m, lanes, mode):
+    """gesture_fc / fc_forward over several sessions' features in one call (the sessions as one
+    batch, every op one launch): output s equals the oracle's gesture_fc of session s alone,
+    residue for residue.  mode 1 is the bench's head configuration (double-hoisted BSGS, every
+    rotate-and-sum level hoisted in groups of 4, merged divisions, R27 / R30 / R31)."""
+    P = toy(log_n=10, n_q=8, scale_bits=40, n_p=2, alpha=2)
+    n = 64
+    cfg = cc.ChainCfg(A=2, R=4, D=8, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8), hoist=1 + mode, lanes=lanes)
+    if mode:
+        cfg.rotsum_inner, cfg.rotsum_hoist_all, cfg.ks_merge = 4, 1, 1
+    keys = orc.keygen(P, seed=3625, rotations=cc.required_rotations("fc_forward", cfg, P.n))
+    rng = np.random.default_rng(75)
+    vals = [cc.interleave([rng.uniform(0, 1, n) for _ in range(lanes)], lanes, n) for _ in range(3)]
+    feats = [orc.Ct([c[:6].copy() for c in f.c], 5, f.scale, f.n_slots) for f in _enc_list(P, keys, vals, 7, 3626)]
+    Ws, bs = radar.fc_weights([n, 16, 8, 5], seed=3627)
+    book = cc.PlainBook(P)
+    want = [cc.gesture_fc(cc.CircuitEvaluator(P, keys.rlk, keys.gk), book, f, Ws, bs, cfg) for f in feats]
+    _run(m, P, keys, book, "fc_forward", cfg, feats, want)
+    _run(m, P, keys, book, "gesture_fc", cfg, feats[:2], want[:2])
+
+
 @pytest.mark.parametrize("hoist", [0, 1])
 def test_standalone_k5_fir_rot(m, hoist):
     """The rotation-based FIR as a chain: two slot-packed sequences, a 41-tap and a
