@@ -954,18 +954,25 @@ std::vector<DCt> ev_rotate_hoisted_pq(Ctx &c, const DCt &a, const std::vector<in
     ModUpOut m;
     if (need) m = ks_modup(c, a.poly(1), a.item_words(), l, B);
     std::vector<DCt> out;
-    // the group's nonzero steps in one launch per 16 (y, x and c0 read once), when the batch's
-    // digit tile fits the kernel's shared memory; otherwise one inner product per step
-    const bool grouped = need && c.modup[l].size() <= 4 &&
-                         (size_t)B * (c.modup[l].size() + 1) * 128 * sizeof(uint64_t) <= 200 * 1024;
+    // the group's nonzero steps in one launch per 16 (y, x and c0 read once); the kernel stages
+    // the digit tile of every batch item in shared memory, so batches above kHoistChunk items run
+    // as chunks of at most kHoistChunk (>= 3 CTAs/SM; each chunk re-reads the keys); with more
+    // than 4 digits one inner product per step
+    constexpr uint32_t kHoistChunk = 16;
+    const bool grouped = need && c.modup[l].size() <= 4;
     if (grouped) {
         std::vector<const uint64_t *> keys;
         std::vector<uint32_t> ginv;
         std::vector<uint64_t *> outs;
         auto flush = [&] {
             if (keys.empty()) return;
-            launch_hoisted_ip_pq(c, a.poly(1), a.item_words(), m.y.get(), m.T * c.n, m.off, a.data(), a.item_words(),
-                                 keys, ginv, outs, out.back().item_words(), l, B);
+            const size_t ow = out.back().item_words(), aw = a.item_words(), yw = m.T * c.n;
+            for (uint32_t b0 = 0; b0 < B; b0 += kHoistChunk) {
+                std::vector<uint64_t *> o(outs);
+                for (auto &p : o) p += b0 * ow;
+                launch_hoisted_ip_pq(c, a.poly(1) + b0 * aw, aw, m.y.get() + b0 * yw, yw, m.off, a.data() + b0 * aw,
+                                     aw, keys, ginv, o, ow, l, std::min(kHoistChunk, B - b0));
+            }
             keys.clear();
             ginv.clear();
             outs.clear();

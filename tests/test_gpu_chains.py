@@ -699,12 +699,13 @@ def test_standalone_k6_k2b_fc_chains(m, lanes):
     assert ctx.trace() == ev.trace
 
 
-@pytest.mark.parametrize("lanes,mode", [(1, 0), (4, 0), (4, 1)])
-def test_fc_forward_sessions_batched(m, lanes, mode):
+@pytest.mark.parametrize("lanes,mode,S", [(1, 0, 3), (4, 0, 3), (4, 1, 3), (1, 1, 18)])
+def test_fc_forward_sessions_batched(m, lanes, mode, S):
     """gesture_fc / fc_forward over several sessions' features in one call (the sessions as one
     batch, every op one launch): output s equals the oracle's gesture_fc of session s alone,
     residue for residue.  mode 1 is the bench's head configuration (double-hoisted BSGS, every
-    rotate-and-sum level hoisted in groups of 4, merged divisions, R27 / R30 / R31)."""
+    rotate-and-sum level hoisted in groups of 4, merged divisions, R27 / R30 / R31); S = 18
+    runs the grouped hoisted inner product in batch chunks of 16 + 2."""
     P = toy(log_n=10, n_q=8, scale_bits=40, n_p=2, alpha=2)
     n = 64
     cfg = cc.ChainCfg(A=2, R=4, D=8, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8), hoist=1 + mode, lanes=lanes)
@@ -712,7 +713,7 @@ def test_fc_forward_sessions_batched(m, lanes, mode):
         cfg.rotsum_inner, cfg.rotsum_hoist_all, cfg.ks_merge = 4, 1, 1
     keys = orc.keygen(P, seed=3625, rotations=cc.required_rotations("fc_forward", cfg, P.n))
     rng = np.random.default_rng(75)
-    vals = [cc.interleave([rng.uniform(0, 1, n) for _ in range(lanes)], lanes, n) for _ in range(3)]
+    vals = [cc.interleave([rng.uniform(0, 1, n) for _ in range(lanes)], lanes, n) for _ in range(S)]
     feats = [orc.Ct([c[:6].copy() for c in f.c], 5, f.scale, f.n_slots) for f in _enc_list(P, keys, vals, 7, 3626)]
     Ws, bs = radar.fc_weights([n, 16, 8, 5], seed=3627)
     book = cc.PlainBook(P)

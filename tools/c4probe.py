@@ -31,6 +31,8 @@ ap.add_argument("--merge", type=int, default=0, help="relin / ModDown + rescale 
 ap.add_argument("--fuse", type=int, default=0, help="K1 as one conjugate-product key switch (R32)")
 ap.add_argument("--chains", default="", help="comma-separated extra chains to profile on the session's inputs "
                                              "(k3_doppler_dft, gesture_frame)")
+ap.add_argument("--fc-sessions", default="", help="comma-separated session counts: profile gesture_fc over "
+                "that many sessions' features as one batch")
 ap.add_argument("--split", action="store_true", help="also profile gesture_features and gesture_fc on their own")
 args = ap.parse_args()
 
@@ -107,5 +109,24 @@ for name in [c for c in args.chains.split(",") if c]:
     prof = ctx.profile()
     tot = sum(v[1] for v in prof.values())
     print(f"{name}: kernel sum {tot:.2f} ms")
+    for k, (c, ms, by, ops) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+        print(f"   {k:16s} {ms:8.2f} ms {ms / tot:6.3f}  {c:5d} launches  {by / (ms * 1e-3) / 1e9:7.1f} GB/s")
+
+for S in [int(x) for x in args.fc_sessions.split(",") if x]:
+    # the FC head over S sessions' features as one batch (chain gesture_fc with S inputs)
+    lf = ctx.chain_plan("gesture_features", cfg, 19, n_in)[0]
+    fo = m.Ct(torch.empty((2, lf + 1, P.n), dtype=torch.int64, device=dev), lf, 0.0, 0, P.log_n)
+    ctx.eval_chain("gesture_features", cfg, ins, m.CtArray([fo]))
+    fi = m.CtArray([fo] * S)
+    lo = ctx.chain_plan("gesture_fc", cfg, lf, S)
+    o_ = m.CtArray([m.Ct(torch.empty((2, l + 1, P.n), dtype=torch.int64, device=dev), l, 0.0, 0, P.log_n) for l in lo])
+    ctx.eval_chain("gesture_fc", cfg, fi, o_)
+    torch.cuda.synchronize()
+    ctx.profile_enable(True)
+    ctx.profile()
+    ctx.eval_chain("gesture_fc", cfg, fi, o_)
+    prof = ctx.profile()
+    tot = sum(v[1] for v in prof.values())
+    print(f"gesture_fc x {S} sessions: kernel sum {tot:.2f} ms ({tot / S:.3f} ms/session)")
     for k, (c, ms, by, ops) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
         print(f"   {k:16s} {ms:8.2f} ms {ms / tot:6.3f}  {c:5d} launches  {by / (ms * 1e-3) / 1e9:7.1f} GB/s")
