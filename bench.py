@@ -560,6 +560,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
     ctx.trace_enable(False)
     xbytes = [0]
     fcb = max(1, args.c5_fc_batch)
+    ffb = max(1, args.c5_feat_batch)
 
     def fc_heads(gathered):
         # the owner's sessions: library mod-q sum of every rank's partial, then the FC head of
@@ -572,7 +573,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
     def gesture_phase(frames_of):
         if phi > plo:
             mdist.sessions_features(ctx, m, gm, [frames_of(s) for s in range(Gg)], gcfg["level"], scale,
-                                    gcfg["n_slots"] * LANES, P.log_n, device, bufs=feat_bufs)
+                                    gcfg["n_slots"] * LANES, P.log_n, device, bufs=feat_bufs, per_call=ffb)
         else:  # more ranks than pairs: this rank contributes zero partials
             feat_bufs.zero_()
         gathered = mdist.allgather_partials(feat_bufs)
@@ -624,10 +625,20 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
                      for j in range(ipp * plo, ipp * phi)]) if phi > plo else None
     h2d = [0]
 
+    # ffb sessions per call: their uplinks (the same pinned session, re-uploaded per session) as one batch
+    gmb = type(gm).from_buffer_copy(gm)
+    gmb.sessions = ffb
+    hgab = m.CtArray(list(hga.cts) * ffb) if hga is not None and ffb > 1 else hga
+
     def sessions_features_async():
-        for s in range(Gg):
-            o = m.Ct(feat_bufs[s], lvf, 0.0, 0, P.log_n, m.FORM_EVAL)
-            ctx.eval_chain_async("gesture_features", gm, hga, m.CtArray([o]))
+        for s0 in range(0, Gg, ffb):
+            k = min(ffb, Gg - s0)
+            os_ = m.CtArray([m.Ct(feat_bufs[s], lvf, 0.0, 0, P.log_n, m.FORM_EVAL) for s in range(s0, s0 + k)])
+            if k == ffb and ffb > 1:
+                ctx.eval_chain_async("gesture_features", gmb, hgab, os_)
+            else:
+                for o in os_.cts:
+                    ctx.eval_chain_async("gesture_features", gm, hga, m.CtArray([o]))
 
     def step_h2d():
         for _ in range(n_vgroups):
@@ -658,7 +669,7 @@ def bench_c5(args, m, torch, device, rank, world, steps=2, warmup=2):
                        f"{Gg} gesture sessions (C4 headline config, 8 frames per ciphertext, {npair} frame groups "
                        f"frame-sharded over the "
                        f"ranks, NCCL all-gather of partial feature ciphertexts, library mod-q sum + FC on the owner, "
-                       f"{fcb} sessions per FC-head batch) "
+                       f"{ffb} sessions per gesture_features batch, {fcb} per FC-head batch) "
                        f"per step at PS4 (N=2^16), one shared key set; device-resident inputs cycle a pool of {pool} "
                        f"distinct sessions per type; h2d_included uploads every session from pinned host memory "
                        f"inside the timed region (copy-stream waves)")}
@@ -1123,6 +1134,8 @@ def main():
     ap.add_argument("--c5-sessions", type=int, default=0,
                     help="C5: total sessions per step (half vital, half gesture; 1024 = SURVEY's full C5)")
     ap.add_argument("--c5-pool", type=int, default=2, help="C5: distinct device-resident sessions per type")
+    ap.add_argument("--c5-feat-batch", type=int, default=4,
+                    help="C5: gesture sessions per gesture_features call (one batch through the per-frame chain)")
     ap.add_argument("--c5-fc-batch", type=int, default=16,
                     help="C5: gesture sessions per FC-head call (the sessions' heads run as one batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

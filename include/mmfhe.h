@@ -168,6 +168,11 @@ typedef struct {
                               with the conjugate-product key (MMFHE_STEP_CONJ_PROD, listed by
                               mmfhe_chain_required_rotations) share one division by P q_l; records
                               "conj_mul_relin_rescale".  Same decryption */
+    uint32_t sessions;     /* gesture_features only: 0 / 1 = one session; S >= 2 = the inputs are S equal
+                              contiguous runs (one per session, each the chain's usual input list), run
+                              as ONE batch through the per-frame chain, one feature ciphertext per
+                              session out (each the modular sum of its own frames: the residues of S
+                              separate calls).  Needs frame_batch 0 (or >= the groups of all sessions) */
 } mmfhe_chain_cfg;
 
 /* ---- context ------------------------------------------------------------ */

@@ -780,6 +780,21 @@ class Runner {
         return acc;
     }
 
+    // S sessions' inputs (S equal contiguous runs) as ONE batch through the per-frame chain, then
+    // each session's frames summed on their own: item s = session s's features (cfg.sessions)
+    DCt gesture_features_sessions(const mmfhe_ct *in, size_t n_in, uint32_t S)
+    {
+        DCt f;
+        if (cfg_.cplx) {
+            f = gesture_frame_c(import_batch(c_, in, 0, 1, n_in));
+        } else {
+            DCt vre = import_batch(c_, in, 0, 2, n_in / 2);
+            DCt vim = import_batch(c_, in, 1, 2, n_in / 2);
+            f = gesture_frame(vre, vim);
+        }
+        return ev_batch_sum_runs(c_, f, S);
+    }
+
     DCt gesture(const mmfhe_ct *in, size_t n_in) { return gesture_fc(gesture_features(in, n_in)); }
 
   private:
@@ -818,6 +833,8 @@ void validate_cfg(const std::string &chain, const mmfhe_chain_cfg &cfg)
                           chain == "gesture_fc" || chain == "fc_forward" || chain == "k3_doppler_dft" ||
                           chain == "vitals_v1" || chain == "vitals_v2",
                       MMFHE_E_SHAPE, "ks_merge applies to the gesture / K3 / FC / vital V1, V2 chains only");
+    if (cfg.sessions > 1)
+        MMFHE_REQUIRE(chain == "gesture_features", MMFHE_E_SHAPE, "sessions > 1 applies to gesture_features only");
     if (cfg.cplx)
         MMFHE_REQUIRE(cplx_chain(chain, cfg) || chain == "gesture_fc" || chain == "fc_forward" ||
                           chain == "k2_doppler_soft_power" || chain == "k6_notch",
@@ -947,6 +964,14 @@ std::vector<uint32_t> chain_plan(const Ctx &c, const std::string &chain, const m
     } else if (chain == "k3_doppler_dft" || chain == "gesture_frame" || chain == "gesture_features") {
         MMFHE_REQUIRE(n_in >= 2 && n_in % 2 == 0, MMFHE_E_SHAPE, "expected (v_re, v_im) per frame");
         n_out = chain == "k3_doppler_dft" ? n_in : chain == "gesture_frame" ? n_in / 2 : 1;
+    }
+    if (chain == "gesture_features" && cfg.sessions > 1) {
+        const size_t per = cfg.cplx ? 1 : 2, groups = n_in / per;
+        MMFHE_REQUIRE(groups % cfg.sessions == 0, MMFHE_E_SHAPE,
+                      "sessions > 1: the inputs must split into equal runs, one per session");
+        MMFHE_REQUIRE(cfg.frame_batch == 0 || cfg.frame_batch >= groups, MMFHE_E_SHAPE,
+                      "sessions > 1 runs every session's frames as one batch (frame_batch 0)");
+        n_out = cfg.sessions;
     } else if (chain == "gesture_fc" || chain == "fc_forward") {
         // one feature ciphertext per session, the sessions as one batch (one launch per op)
         MMFHE_REQUIRE(n_in >= 1, MMFHE_E_SHAPE, "expected one feature ciphertext per session");
@@ -1062,7 +1087,8 @@ std::vector<DCt> run_chain(Ctx &c, const std::string &chain, const mmfhe_chain_c
     } else if (chain == "gesture") {
         out.push_back(r.gesture(in, n_in));
     } else if (chain == "gesture_features") {
-        out.push_back(r.gesture_features(in, n_in));
+        out.push_back(cfg.sessions > 1 ? r.gesture_features_sessions(in, n_in, cfg.sessions)
+                                       : r.gesture_features(in, n_in));
     } else if (chain == "k2_soft_attention") {
         auto nd = r.k2_soft_attention(import_batch(c, in, 0, 1, 1));
         out.push_back(std::move(nd.first));

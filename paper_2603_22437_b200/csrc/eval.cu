@@ -302,6 +302,18 @@ DCt ev_batch_sum(Ctx &c, const DCt &a)
     return r;
 }
 
+DCt ev_batch_sum_runs(Ctx &c, const DCt &a, uint32_t S)
+{
+    MMFHE_REQUIRE(S >= 1 && a.batch % S == 0, MMFHE_E_SHAPE, "batch does not split into equal runs");
+    const uint32_t g = a.batch / S;
+    for (uint32_t s = 0; s < S; ++s) rec_n(c, "hadd", a.level, g - 1);
+    DCt r = make_ct(c, a.level, a.npolys, a.n_slots, a.scale, S);
+    for (uint32_t s = 0; s < S; ++s)
+        launch_batch_sum(c, r.data() + (size_t)s * r.item_words(), a.data() + (size_t)s * g * a.item_words(), g,
+                         a.npolys, a.level);
+    return r;
+}
+
 DCt ev_drop_to(Ctx &c, const DCt &a, uint32_t level)
 {
     MMFHE_REQUIRE(level <= a.level, MMFHE_E_DEPTH, "cannot raise a level");

@@ -46,6 +46,8 @@ std::vector<DCt> ev_k3_mac(Ctx &c, const std::vector<const DCt *> &xr, const std
                            const std::vector<std::vector<const DPlain *>> &pns);
 // sum of all items of a batch (frame accumulation, depth 0)
 DCt ev_batch_sum(Ctx &c, const DCt &a);
+// S equal contiguous runs of a's items, each summed: item s of the result = sum of run s
+DCt ev_batch_sum_runs(Ctx &c, const DCt &a, uint32_t S);
 DCt ev_sum(Ctx &c, const std::vector<const DCt *> &cts);
 DCt ev_add_plain(Ctx &c, const DCt &a, const DPlain &pt);
 // Scalar linear maps over a batch (CK10): out[j] = sum_{w<W} coef[j][w] in[lo0 + j*lo_step + w]

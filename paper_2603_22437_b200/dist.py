@@ -47,21 +47,36 @@ def allgather_partials(local, group=None):
     return out.view((world, k) + tuple(local.shape[1:]))
 
 
-def sessions_features(ctx, m, cfg, frames_by_session, level, scale, n_slots, log_n, device, bufs=None):
+def sessions_features(ctx, m, cfg, frames_by_session, level, scale, n_slots, log_n, device, bufs=None,
+                      per_call=1):
     """Partial features of this rank's frame shard for every session: one ciphertext per
     session, stacked [S, 2, level_out+1, N] (device, int64 view of the residues).  `bufs`:
     optional persistent [S, 2, level_out+1, N] output tensor (stable buffer addresses let the
-    library replay its captured chain graphs from call to call)."""
+    library replay its captured chain graphs from call to call).  per_call > 1: that many
+    sessions' shards per gesture_features call as one batch (cfg.sessions; every session holds
+    the same number of frame groups)."""
     import torch
 
     outs = []
-    for s, ins in enumerate(frames_by_session):
-        lv = ctx.chain_plan("gesture_features", cfg, level, len(ins))[0]
-        data = bufs[s] if bufs is not None else torch.empty((2, lv + 1, 1 << log_n), dtype=torch.int64,
-                                                            device=device)
-        o = m.Ct(data, lv, 0.0, 0, log_n, m.FORM_EVAL)
-        ctx.eval_chain("gesture_features", cfg, ins, [o])
-        outs.append(o)
+    S = len(frames_by_session)
+    for s0 in range(0, S, max(1, per_call)):
+        chunk = frames_by_session[s0:s0 + max(1, per_call)]
+        k = len(chunk)
+        ccfg = cfg
+        if k > 1:
+            ccfg = type(cfg).from_buffer_copy(cfg)
+            ccfg.sessions = k
+            ins = m.CtArray([c for a in chunk for c in (a.cts if isinstance(a, m.CtArray) else a)])
+        else:
+            ins = chunk[0]
+        lvs = ctx.chain_plan("gesture_features", ccfg, level, len(ins))
+        os_ = []
+        for i, lv in enumerate(lvs):
+            data = bufs[s0 + i] if bufs is not None else torch.empty((2, lv + 1, 1 << log_n), dtype=torch.int64,
+                                                                     device=device)
+            os_.append(m.Ct(data, lv, 0.0, 0, log_n, m.FORM_EVAL))
+        ctx.eval_chain("gesture_features", ccfg, ins, os_)
+        outs += os_
     stacked = bufs if bufs is not None else torch.stack([o.data for o in outs])
     return stacked, outs[0].level, outs[0].scale
 

@@ -54,7 +54,7 @@ class ChainCfg(ctypes.Structure):
                 ("iq_pack", ctypes.c_uint32), ("lanes", ctypes.c_uint32), ("fc_baby", ctypes.c_uint32),
                 ("cplx", ctypes.c_uint32), ("bsgs_aligned", ctypes.c_uint32), ("rotsum_inner", ctypes.c_uint32),
                 ("rotsum_hoist_all", ctypes.c_uint32), ("ks_merge", ctypes.c_uint32),
-                ("k1_conj_fuse", ctypes.c_uint32)]
+                ("k1_conj_fuse", ctypes.c_uint32), ("sessions", ctypes.c_uint32)]
 
 # Key id of the conjugation automorphism (include/mmfhe.h MMFHE_STEP_CONJ, DESIGN R28)
 STEP_CONJ = -(1 << 31)
@@ -64,7 +64,7 @@ STEP_CONJ_PROD = STEP_CONJ + 1  # the conjugate-product key (MMFHE_STEP_CONJ_PRO
 def chain_cfg(R=0, D=0, A=0, F=0, gamma=1, p_phi=1, taylor_order=1, n_slots=0, bsgs_baby=0,
               fc_dims=(0, 0, 0, 0), notch_width=1, bands_bins=(), n_taps=(), fs=0.0, frame_batch=0,
               hoist=0, vp_plus=0, iq_pack=0, lanes=1, fc_baby=0, cplx=0, bsgs_aligned=0,
-              rotsum_inner=0, rotsum_hoist_all=0, ks_merge=0, k1_conj_fuse=0) -> ChainCfg:
+              rotsum_inner=0, rotsum_hoist_all=0, ks_merge=0, k1_conj_fuse=0, sessions=0) -> ChainCfg:
     c = ChainCfg()
     c.R, c.D, c.A, c.F = R, D, A, F
     c.gamma, c.p_phi, c.taylor_order, c.n_slots, c.bsgs_baby = gamma, p_phi, taylor_order, n_slots, bsgs_baby
@@ -90,6 +90,7 @@ def chain_cfg(R=0, D=0, A=0, F=0, gamma=1, p_phi=1, taylor_order=1, n_slots=0, b
     c.rotsum_hoist_all = int(rotsum_hoist_all)
     c.ks_merge = int(ks_merge)
     c.k1_conj_fuse = int(k1_conj_fuse)
+    c.sessions = int(sessions)
     return c
 
 

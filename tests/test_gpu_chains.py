@@ -382,6 +382,56 @@ def test_gesture_chain_complex_small(m, lanes, F, fb, hoist, aligned):
     assert e.value.name == "E_MISSING_KEY" and "conjugation" in str(e.value)
 
 
+@pytest.mark.parametrize("cplx", [0, 1])
+def test_gesture_features_sessions_batched(m, cplx):
+    """gesture_features over S = 3 sessions in one call (cfg.sessions): every session's frame
+    groups run as one batch through the per-frame chain and each session's frames are summed on
+    their own; output s equals the oracle's gesture_features of session s alone, residue for
+    residue (split re / im layout, and complex slots with the headline's R27-R32 options)."""
+    P = toy(log_n=10, n_q=12, scale_bits=40, n_p=2, alpha=2)
+    S, F, lanes = 3, 4, 2
+    cfg, _ = _gesture(P, 3251, F=F, hoist=2)
+    cfg.lanes, cfg.cplx = lanes, cplx
+    if cplx:
+        cfg.bsgs_aligned, cfg.rotsum_inner, cfg.rotsum_hoist_all, cfg.ks_merge, cfg.k1_conj_fuse = 1, 4, 1, 1, 1
+    keys = orc.keygen(P, seed=3252, rotations=cc.required_rotations("gesture_features", cfg, P.n))
+    n = cfg.n_slots
+    book = cc.PlainBook(P)
+    ins, want = [], []
+    for s in range(S):
+        _, Zt = _gesture(P, 3260 + s, F=F)
+        vs = [radar.pack_doppler(Zt[t]) for t in range(F)]
+        groups = [vs[g * lanes:(g + 1) * lanes] for g in range(cc.n_packed(F, lanes))]
+        ev = cc.CircuitEvaluator(P, keys.rlk, keys.gk)
+        if cplx:
+            cts = [orc.encrypt_vector(P, keys, cc.interleave(grp, lanes, n), P.L, seed=3270 + s, index=g)
+                   for g, grp in enumerate(groups)]
+            want.append(cc.gesture_features(ev, book, cts, None, cfg))
+        else:
+            cts = []
+            for grp in groups:
+                for part in ("real", "imag"):
+                    cts.append(orc.encrypt_vector(P, keys, cc.interleave([getattr(v, part) for v in grp], lanes, n),
+                                                  P.L, seed=3270 + s, index=len(cts)))
+            want.append(cc.gesture_features(ev, book, cts[0::2], cts[1::2], cfg))
+        ins += cts
+    ctx = make_ctx(m, P, keys, book)
+    mcfg = _mcfg(m, cfg)
+    mcfg.sessions = S
+    levels = ctx.chain_plan("gesture_features", mcfg, P.L, len(ins))
+    assert levels == [w.level for w in want]
+    outs = [ct_out(m, P, lv) for lv in levels]
+    assert ctx.eval_chain("gesture_features", mcfg, [ct_in(m, P, c) for c in ins], outs) == S
+    for o, w in zip(outs, want):
+        assert np.array_equal(residues(o), np.stack(w.c)), "residues differ from the oracle"
+        assert o.scale == w.scale and o.level == w.level
+    # the inputs must split into equal runs, and only gesture_features takes sessions
+    with pytest.raises(m.MmfheError):
+        ctx.chain_plan("gesture_features", mcfg, P.L, len(ins) - (1 if cplx else 2))
+    with pytest.raises(m.MmfheError):
+        ctx.chain_plan("gesture", mcfg, P.L, len(ins))
+
+
 def test_frame_sharded_gesture_exchange(m):
     """frames of one session split over 'ranks' (here 3 shards on one GPU),
     per-shard gesture_features, library sum of the partials, FC head -- equals the
