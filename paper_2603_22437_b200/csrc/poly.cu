@@ -19,6 +19,10 @@ namespace mmfhe {
 namespace {
 
 constexpr int kTB = 256;
+// DMAX = 3 instantiations of the digit-templated kernels for dnum = 3 (PS3 / PS4 / PSV)
+#ifndef MMFHE_D3
+#define MMFHE_D3 1
+#endif
 
 __device__ __forceinline__ uint32_t bitrev(uint32_t x, uint32_t log_n) { return __brev(x) >> (32 - log_n); }
 
@@ -1284,7 +1288,12 @@ void launch_key_ip(Ctx &c, uint64_t *accQ, uint64_t *accP, const uint64_t *x_ntt
     a.per_z = (B + nz - 1) / nz;
     nz = (B + a.per_z - 1) / a.per_z;
     const dim3 g = grid3(c.n, level + 1 + c.K, nz);
-    if (ep) {  // the fused-epilogue instantiations (double hoisting) carry its registers alone
+    if (MMFHE_D3 && a.dnum == 3) {  // PS3 / PS4 / PSV: exact digit count
+        if (ep)
+            k_key_ip<3, true><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
+        else
+            k_key_ip<3><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
+    } else if (ep) {  // the fused-epilogue instantiations (double hoisting) carry its registers alone
         if (a.dnum <= 4)
             k_key_ip<4, true><<<g, kTB, 0, c.stream>>>(accQ, accP, x_ntt, y, key, c.kt, a);
         else if (a.dnum <= 8)
@@ -1589,9 +1598,13 @@ void launch_hoisted_ip_pq(Ctx &c, const uint64_t *x, size_t xs, const uint64_t *
     static std::atomic<uint64_t> attr{0};
     once_per_device(attr, [] {
         CUDA_CHECK(cudaFuncSetAttribute(k_hoisted_ip_pq<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_CHECK(cudaFuncSetAttribute(k_hoisted_ip_pq<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     });
     const dim3 g(c.n / kHTile, level + 1 + c.K);
-    k_hoisted_ip_pq<4><<<g, kHTile, smem, c.stream>>>(x, y, c0, (const TwPair *)c.bconv_ptr(c.off_pd_pmod), c.kt, a);
+    if (MMFHE_D3 && a.dnum == 3)
+        k_hoisted_ip_pq<3><<<g, kHTile, smem, c.stream>>>(x, y, c0, (const TwPair *)c.bconv_ptr(c.off_pd_pmod), c.kt, a);
+    else
+        k_hoisted_ip_pq<4><<<g, kHTile, smem, c.stream>>>(x, y, c0, (const TwPair *)c.bconv_ptr(c.off_pd_pmod), c.kt, a);
     LAUNCH_CHECK(c);
 }
 
@@ -1630,7 +1643,9 @@ void launch_hoisted_rotsum_pq(Ctx &c, uint64_t *out, size_t os, const uint64_t *
                  2.0 * a.dnum * rows * c.n * B * S);
     const dim3 grid(c.n / kRTile, level + 1 + c.K, (B + kRItems - 1) / kRItems);
     const TwPair *pmod = (const TwPair *)c.bconv_ptr(c.off_pd_pmod);
-    if (a.dnum <= 4)
+    if (MMFHE_D3 && a.dnum == 3)  // PS3 / PS4 / PSV: exact digit count, 5 steps per 128-bit sum
+        k_hoisted_rotsum_pq<3><<<grid, kRTile, 0, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
+    else if (a.dnum <= 4)
         k_hoisted_rotsum_pq<4><<<grid, kRTile, 0, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
     else
         k_hoisted_rotsum_pq<8><<<grid, kRTile, 0, c.stream>>>(out, x, y, c0, pmod, c.kt, a);
