@@ -453,8 +453,10 @@ struct HoistSumArgs {
 #ifndef MMFHE_RS_MINB
 #define MMFHE_RS_MINB 4  // measured: 4 (123 regs) 4.18 ms, 1 (128 regs) 5.98, 5 (96) 4.69, 6 (80) 5.34 (C4 K2b + FC)
 #endif
+// dnum = 3 (DMAX = 3): 5 CTAs/SM with 4 steps per 128-bit sum (96 registers, no spills): C4's
+// rotate-and-sums 3.97 -> 3.85 ms against 4 CTAs/SM with 5 steps (r02bx; 6 CTAs/SM with 3 steps 3.91)
 template <int DMAX>
-__global__ void __launch_bounds__(kRTile, MMFHE_RS_MINB) k_hoisted_rotsum_pq(uint64_t *__restrict__ out, const uint64_t *__restrict__ x,
+__global__ void __launch_bounds__(kRTile, DMAX == 3 ? 5 : MMFHE_RS_MINB) k_hoisted_rotsum_pq(uint64_t *__restrict__ out, const uint64_t *__restrict__ x,
                                                             const uint64_t *__restrict__ y,
                                                             const uint64_t *__restrict__ c0,
                                                             const TwPair *__restrict__ pmod, KTables kt,
@@ -501,7 +503,8 @@ __global__ void __launch_bounds__(kRTile, MMFHE_RS_MINB) k_hoisted_rotsum_pq(uin
 #define MMFHE_RS_TERMS 16
 #endif
     static_assert(MMFHE_RS_TERMS <= 16, "128-bit accumulation bound: <= 16 products < q^2, q < 2^60");
-    constexpr int kRChunk = MMFHE_RS_TERMS / DMAX > 0 ? MMFHE_RS_TERMS / DMAX : 1;  // steps per 128-bit sum
+    constexpr int kRTerms = DMAX == 3 ? 12 : MMFHE_RS_TERMS;
+    constexpr int kRChunk = kRTerms / DMAX > 0 ? kRTerms / DMAX : 1;  // steps per 128-bit sum
     for (uint32_t s0 = 0; s0 < a.nsteps; s0 += kRChunk) {
         const uint32_t ns = min((uint32_t)kRChunk, a.nsteps - s0);
         uint64_t kb[kRChunk][DMAX], ka[kRChunk][DMAX];
