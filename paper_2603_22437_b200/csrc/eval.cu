@@ -966,11 +966,16 @@ std::vector<DCt> ev_rotate_hoisted_pq(Ctx &c, const DCt &a, const std::vector<in
     ModUpOut m;
     if (need) m = ks_modup(c, a.poly(1), a.item_words(), l, B);
     std::vector<DCt> out;
-    // the group's nonzero steps in one launch per 16 (y, x and c0 read once); the kernel stages
-    // the digit tile of every batch item in shared memory, so batches above kHoistChunk items run
-    // as chunks of at most kHoistChunk (>= 3 CTAs/SM; each chunk re-reads the keys); with more
-    // than 4 digits one inner product per step
-    constexpr uint32_t kHoistChunk = 16;
+    // the group's nonzero steps in one launch per 16 (y, x and c0 read once); the kernel keeps
+    // every batch item's digit and c0 words of its coefficient in shared memory, so its occupancy
+    // falls with the batch: batches run as balanced chunks of at most kHoistChunk items (each
+    // chunk re-reads the keys).  Measured at C4 (B = 13, r02bz): one launch 3.58 ms, 7 + 6 3.33,
+    // 5 + 5 + 3 3.46.  With more than 4 digits one inner product per step
+#ifndef MMFHE_HOIST_CHUNK
+#define MMFHE_HOIST_CHUNK 8
+#endif
+    const uint32_t n_chunks = (B + MMFHE_HOIST_CHUNK - 1) / MMFHE_HOIST_CHUNK;
+    const uint32_t kHoistChunk = (B + n_chunks - 1) / n_chunks;
     const bool grouped = need && c.modup[l].size() <= 4;
     if (grouped) {
         std::vector<const uint64_t *> keys;

@@ -755,7 +755,7 @@ def test_fc_forward_sessions_batched(m, lanes, mode, S):
     batch, every op one launch): output s equals the oracle's gesture_fc of session s alone,
     residue for residue.  mode 1 is the bench's head configuration (double-hoisted BSGS, every
     rotate-and-sum level hoisted in groups of 4, merged divisions, R27 / R30 / R31); S = 18
-    runs the grouped hoisted inner product in batch chunks of 16 + 2."""
+    runs the grouped hoisted inner product in balanced batch chunks (6 + 6 + 6)."""
     P = toy(log_n=10, n_q=8, scale_bits=40, n_p=2, alpha=2)
     n = 64
     cfg = cc.ChainCfg(A=2, R=4, D=8, gamma=4, n_slots=n, fc_dims=(n, 16, 8, 8), hoist=1 + mode, lanes=lanes)
