@@ -262,8 +262,13 @@ __global__ void __launch_bounds__(kTB, 3) k_key_ip_lr(uint64_t *__restrict__ acc
 // For every batch item b: (accQ|accP)_{b,p}[r] = sum_j src_{b,j}[r] (.) evk_j[p][r] with
 // src = x_b[r] for r in I_j, else the ModUp'd row.  The 2*dnum key words of (r, k) are
 // loaded once per thread and reused for its per_z items (grid.z splits the batch).
+// dnum = 3: 5 CTAs/SM (48 registers, 8-28 B of spills outside the item loop): C4 key_ip
+// 2.78 -> 2.55 ms against 4 CTAs/SM (62 registers; ncu long_scoreboard 0.76), r02cc
+#ifndef MMFHE_KIP3_MINB
+#define MMFHE_KIP3_MINB 5
+#endif
 template <int DMAX, bool EPI = false>
-__global__ void __launch_bounds__(kTB, DMAX <= 4 ? 4 : 1) k_key_ip(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
+__global__ void __launch_bounds__(kTB, DMAX == 3 ? MMFHE_KIP3_MINB : DMAX <= 4 ? 4 : 1) k_key_ip(uint64_t *__restrict__ accQ, uint64_t *__restrict__ accP,
                                                 const uint64_t *__restrict__ x, const uint64_t *__restrict__ y,
                                                 const uint64_t *__restrict__ key, KTables kt, IPArgs a)
 {
